@@ -1,0 +1,197 @@
+/*
+ * gist.h -- C ABI of the B200-native GIST hot path (arXiv 2102.10424).
+ *
+ * GIST = Graph Independent Subnetwork Training.  Algorithm 1:
+ *   init Theta; Cluster(G, c); for t in 0..T-1:
+ *     subGCNs(Psi, m)            -> gist_partition
+ *     zeta x subTrain per sub-GCN -> gist_subtrain
+ *     subAgg                      -> gist_aggregate
+ * Evaluation of the global model -> gist_eval.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument is a HOST pointer unless its name ends in `_dev`.
+ *    Inputs are copied before the call returns and never retained; outputs are
+ *    caller-allocated with the sizes stated per call.
+ *  - Work is stream-ordered on the context stream (gist_config.stream, or a
+ *    stream the library creates).  Calls that fill host outputs synchronise
+ *    before returning.
+ *  - Errors: every call returns a gist_status; a message is available from
+ *    gist_last_error().  A CUDA or NCCL failure poisons the context: every
+ *    later call returns the same sticky status (GIST_E_CUDA / GIST_E_NCCL).
+ *  - State machine: CREATED -> load_graph -> GRAPH -> init_params/set_params
+ *    -> PARAMS -> partition -> PARTITIONED -> subtrain* -> aggregate -> PARAMS.
+ *    Out-of-order calls return GIST_E_STATE.
+ *  - Multi-GPU: one process (context) per GPU.  Slot (sub-GCN) i lives on rank
+ *    i mod world_size.  gist_aggregate and gist_eval are collectives: every rank
+ *    calls them in the same order (NCCL semantics).
+ *  - There is no CPU fallback: a context can only be created on a CUDA device
+ *    of compute capability 10.0 (sm_100a); otherwise GIST_E_UNSUPPORTED.
+ *
+ * Readings R1..R18 (where the paper is silent) are listed in DESIGN.md.
+ */
+#ifndef GIST_H_
+#define GIST_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIST_ABI_VERSION 1
+
+typedef struct gist_ctx gist_ctx; /* opaque, single owner */
+
+typedef enum {
+  GIST_OK = 0,
+  GIST_E_ARG = -1,         /* invalid argument (range, null, inconsistent sizes) */
+  GIST_E_SHAPE = -2,       /* dims / m / buffer sizes inconsistent */
+  GIST_E_STATE = -3,       /* call out of order (see state machine above) */
+  GIST_E_OOM = -4,         /* device allocation failed */
+  GIST_E_CUDA = -5,        /* CUDA runtime error (sticky) */
+  GIST_E_NCCL = -6,        /* NCCL error (sticky) */
+  GIST_E_UNSUPPORTED = -7  /* no sm_100 device / feature not built */
+} gist_status;
+
+enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1 };      /* Eq. (1); GraphSAGE-mean PAPER.md:246 (R2) */
+enum { GIST_OPT_SGD = 0, GIST_OPT_ADAM = 1 };        /* subTrain = SGD step PAPER.md:168; Adam PAPER.md:660,680,690 */
+enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1 };     /* FP32 parity mode / BF16 tensor-core mode (R13) */
+enum { GIST_GRAPH_DEVICE = 0, GIST_GRAPH_HOST = 1 }; /* graph resident in HBM / in pinned host memory (streamed per step) */
+
+typedef struct {
+  int32_t arch;               /* GIST_ARCH_* */
+  int32_t num_layers;         /* L >= 1 */
+  const int32_t* dims;        /* L+1 entries d_0..d_L (d_0 = features, d_L = classes), copied */
+  int32_t optimizer;          /* GIST_OPT_* */
+  float beta1, beta2, eps;    /* Adam constants; defaults 0.9, 0.999, 1e-8 (R8) */
+  int32_t precision;          /* GIST_PREC_* */
+  int32_t clusters_per_batch; /* q: clusters unioned into one mini-batch */
+  uint64_t batch_seed;        /* Philox key of the per-slot batch schedule (R7) */
+  int32_t graph_residency;    /* GIST_GRAPH_* */
+  int32_t rank, world_size;   /* this process's rank; number of ranks (1 = no NCCL) */
+  int32_t device;             /* CUDA device ordinal */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0 when world_size > 1, else NULL */
+  void* stream;               /* optional cudaStream_t to order work on; NULL = library-owned */
+} gist_config;
+
+/* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
+void gist_config_default(gist_config* cfg);
+
+/* Creates a context on cfg->device.  Errors: GIST_E_ARG (dims), GIST_E_UNSUPPORTED
+ * (no CUDA device of compute capability 10.x), GIST_E_NCCL. */
+gist_status gist_create(const gist_config* cfg, gist_ctx** out);
+
+/* Loads graph G (n nodes, features X in R^{n x d_0}) and its Cluster
+ * partition (METIS is an input here, not computed).
+ *  row_ptr[n+1] (int64, non-decreasing, row_ptr[0] = 0, row_ptr[n] = nnz),
+ *  col_idx[nnz] (int32 in [0,n), symmetric adjacency, no self loops -- self loops
+ *     present in the input are dropped and counted, see gist_stat),
+ *  X[n*d_0] fp32 row-major, labels[n] int32 in [0,num_classes), num_classes = d_L,
+ *  split[n] uint8: 0 train, 1 val, 2 test, 3 none,
+ *  cluster_ids[n] int32 in [0,num_clusters), every cluster non-empty.
+ * Nodes are relabelled on the device so that clusters are contiguous; every
+ * per-node output of this library is keyed by the ORIGINAL node id. */
+gist_status gist_load_graph(gist_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                            int64_t nnz, const float* X, const int32_t* labels, int32_t num_classes,
+                            const uint8_t* split, const int32_t* cluster_ids, int32_t num_clusters);
+
+/* "randomly initialize GCN": Glorot-uniform from Philox4x32-10,
+ * bit-identical to the oracle (R11). */
+gist_status gist_init_params(gist_ctx* ctx, uint64_t seed);
+
+/* subGCNs: for every hidden dim l = 1..L-1 a random disjoint
+ * partition of [d_l] into m balanced blocks keyed by Philox(seed, round t, l)
+ * (R5); d_0 and d_L are not partitioned.  Extracts
+ * Theta^(i)_l = [Theta_l]_{D_l^(i) x D_{l+1}^(i)} for this rank's
+ * slots and resets their optimizer state (R8).  1 <= m <= min hidden dim. */
+gist_status gist_partition(gist_ctx* ctx, uint64_t seed, int32_t m);
+
+/* subTrain: local_iters (zeta) steps for every local
+ * slot, each on its own Cluster mini-batch (R7): batch build, forward (Eq. 2),
+ * softmax-CE (R4), backward, Adam/SGD with learning rate lr.  Slots run
+ * concurrently on separate streams.  mean_loss: NULL or float[m]; entries of
+ * this rank's slots receive the mean loss over the local_iters steps, others 0. */
+gist_status gist_subtrain(gist_ctx* ctx, int32_t local_iters, float lr, float* mean_loss);
+
+/* subAgg: every slot's block replaces its entries of the
+ * global Theta (bitwise copy, R9); entries outside all blocks are untouched.
+ * Collective: one ncclAllGather of the packed slot buffers when world_size > 1.
+ * Increments the round counter t. */
+gist_status gist_aggregate(gist_ctx* ctx);
+
+/* Forward of the global model on the full graph (full-graph operator, R1/R2;
+ * no output scaling, R10); mean CE loss and accuracy over nodes with
+ * split == split_code.  Either output may be NULL. */
+gist_status gist_eval(gist_ctx* ctx, int32_t split_code, float* loss, float* acc);
+
+/* ---------------- inspection / parity hooks ---------------- */
+/* Global Theta_l, logical row-major: rows = d_l (GCN) or 2*d_l (SAGE: self rows then
+ * neighbour rows), cols = d_{l+1}.  out / in: float[rows*cols]. */
+gist_status gist_get_params(gist_ctx* ctx, int32_t layer, float* out);
+gist_status gist_set_params(gist_ctx* ctx, int32_t layer, const float* in);
+
+/* Partition of dim `dim` for the current round: units[d_dim] = blocks D^(0..m-1)
+ * concatenated (each ascending), offs[m+1] block offsets.  Valid after partition. */
+gist_status gist_get_partition(gist_ctx* ctx, int32_t dim, int32_t* units, int32_t* offs);
+
+/* Sub-model Theta^(slot)_layer, logical row-major [|rows| x |cols|] (R6).  Only for
+ * slots owned by this rank.  out size: gist_sub_shape(). */
+gist_status gist_sub_shape(gist_ctx* ctx, int32_t slot, int32_t layer, int64_t* rows, int64_t* cols);
+gist_status gist_get_sub_params(gist_ctx* ctx, int32_t slot, int32_t layer, float* out);
+
+/* Trace of the last subTrain step of a local slot (parity hooks):
+ *  GIST_TRACE_NODES   int32[n_b]  original node id of each batch row (batch order)
+ *  GIST_TRACE_ACT     float[n_b * w] layer input activation H_layer (layer >= 1, w = width of H_layer)
+ *  GIST_TRACE_LOGITS  float[n_b * d_L]
+ *  GIST_TRACE_GRAD    float[rows*cols] gradient dL/dTheta^(slot)_layer of that step (logical layout)
+ *  GIST_TRACE_LOSS    float[1] the step's loss
+ * *count (may be NULL) receives the element count; out may be NULL to query it. */
+enum { GIST_TRACE_NODES = 0, GIST_TRACE_ACT = 1, GIST_TRACE_LOGITS = 2, GIST_TRACE_GRAD = 3, GIST_TRACE_LOSS = 4 };
+gist_status gist_get_trace(gist_ctx* ctx, int32_t slot, int32_t what, int32_t layer, void* out, int64_t* count);
+
+/* Counters: GIST_STAT_ROUND (t), GIST_STAT_STEP (steps per slot so far),
+ * GIST_STAT_SELF_LOOPS_DROPPED, GIST_STAT_LAST_NNZ_B (nnz of the last batch of slot
+ * 0 on this rank), GIST_STAT_LAST_NB, GIST_STAT_KERNELS (kernel launches issued
+ * by the library so far), GIST_STAT_H2D_BYTES / GIST_STAT_D2H_BYTES (bytes
+ * copied so far), GIST_STAT_MAX_NB. */
+enum {
+  GIST_STAT_ROUND = 0, GIST_STAT_STEP = 1, GIST_STAT_SELF_LOOPS_DROPPED = 2, GIST_STAT_LAST_NNZ_B = 3,
+  GIST_STAT_LAST_NB = 4, GIST_STAT_KERNELS = 5, GIST_STAT_H2D_BYTES = 6, GIST_STAT_D2H_BYTES = 7,
+  GIST_STAT_MAX_NB = 8
+};
+int64_t gist_stat(gist_ctx* ctx, int32_t which);
+
+/* cudaStream_t of the context (for timing with CUDA events on the launching stream). */
+void* gist_stream(gist_ctx* ctx);
+
+const char* gist_last_error(const gist_ctx* ctx);
+const char* gist_status_str(gist_status s);
+void gist_destroy(gist_ctx* ctx);
+
+/* ---------------- kernel-level entry points (benchmark / parity) ----------------
+ * Device pointers (`_dev`), stream-ordered on `stream` (cudaStream_t, NULL = legacy).
+ * These run exactly the kernels the training step uses. */
+
+/* Aggregation SpMM over a CSR (int64 row_ptr, int32 col):  for v in [0,rows):
+ *   out[v,:] = rowscale[v] * ( self * colscale[v] * H[v,:] + sum_{u in N(v)} colscale[u] * H[u,:] )
+ * (NULL scale = 1).  H, out: row-major, `ld` elements per row, width w <= ld
+ * processed; dtype 0 = fp32, 1 = bf16 (fp32 accumulation).  GCN renorm
+ * (R1): rowscale = colscale = (deg+1)^{-1/2}, self = 1; SAGE mean (R2):
+ * rowscale = 1/deg, self = 0. */
+gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_dev, int64_t rows,
+                      const float* rowscale_dev, const float* colscale_dev, int32_t self,
+                      const void* H_dev, void* out_dev, int64_t w, int64_t ld, int32_t dtype, void* stream);
+
+/* C[M x N] = op(A) op(B) (row-major, leading dims lda/ldb/ldc), fp32 or bf16 in,
+ * fp32 or bf16 out, fp32 accumulation; trans flags per operand.  dtype 0 = fp32
+ * SIMT path, 1 = bf16 tcgen05 path (out fp32 when out_f32 != 0).  relu != 0 applies
+ * max(.,0) in the epilogue. */
+gist_status gist_gemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
+                      const void* A_dev, int64_t lda, const void* B_dev, int64_t ldb,
+                      void* C_dev, int64_t ldc, int32_t dtype, int32_t out_f32, int32_t relu, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIST_H_ */

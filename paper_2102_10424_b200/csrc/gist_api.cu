@@ -1,0 +1,1157 @@
+// gist_api.cu -- the C ABI (include/gist.h): context, state machine, the GIST
+// round structure of Algorithm 1 and the subTrain step
+// orchestration.  Every arithmetic step runs in the kernels of kernels.h; this
+// file only sequences launches, owns device memory and streams, and computes
+// the (tiny, integer) per-step batch schedule on the host (R7).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <nccl.h>
+
+#include "../../include/gist.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace gist;
+
+namespace {
+
+enum State { S_CREATED = 0, S_GRAPH = 1, S_PARAMS = 2, S_PARTITIONED = 3 };
+
+struct LayerShape {
+  int nrows = 0, ncols = 0;  // logical rows (self block for SAGE) / cols of the sub block
+  int Kp = 0, Np = 0;        // physical (padded) shape
+  int half = 0;              // SAGE: physical offset of neighbour rows
+  int64_t off = 0;           // float offset in the packed slot buffer
+  int32_t* rows = nullptr;   // device unit list (nullptr = identity)
+  int32_t* cols = nullptr;
+};
+
+struct Slot {
+  int index = 0;  // global slot id i
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev = nullptr;
+  float *W = nullptr, *G = nullptr, *M = nullptr, *V = nullptr;
+  bf16* Wb = nullptr;
+  // batch schedule (device + pinned host mirror), capacity `cap` steps
+  int cap = 0;
+  int32_t *desc_dev = nullptr, *desc_host = nullptr;
+  std::vector<int> nb_of_step, q_of_step;
+  cudaEvent_t desc_ev = nullptr;
+  int cached_epoch = -1;
+  std::vector<int32_t> epoch_perm;
+  // batch buffers
+  int32_t *b_nodes = nullptr, *deg_b = nullptr, *lab_b = nullptr, *b_col = nullptr, *map_cl = nullptr;
+  uint8_t* train_b = nullptr;
+  float* scale = nullptr;
+  int64_t *b_rp = nullptr, *stats = nullptr;
+  // activations (element type T of the precision mode)
+  std::vector<void*> C, H, dZ;
+  void* dC = nullptr;
+  float* logits = nullptr;
+  float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
+  int last_nb = 0;
+};
+
+}  // namespace
+
+struct gist_ctx {
+  gist_config cfg{};
+  std::vector<int> dims;
+  int L = 0, arch = 0, prec = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int state = S_CREATED;
+  gist_status sticky = GIST_OK;
+  std::string err;
+  ncclComm_t comm = nullptr;
+  cudaEvent_t fork_ev = nullptr;
+  // graph (relabelled: clusters contiguous)
+  int64_t n = 0, nnz = 0;
+  int c = 0, k = 0;
+  int64_t self_loops = 0;
+  int64_t *rp = nullptr, *cstart = nullptr;
+  int32_t *col = nullptr, *cid = nullptr, *labels = nullptr;
+  uint8_t* split = nullptr;
+  void* X = nullptr;  // n x pad8(d0), T
+  float* full_scale = nullptr;
+  std::vector<int32_t> perm_h;  // new id -> original id
+  std::vector<int64_t> cstart_h;
+  int nb_max = 0;
+  int64_t nnzb_max = 0;
+  // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
+  std::vector<float*> theta;
+  std::vector<int64_t> th_K, th_N;
+  // partition of the current round
+  int m = 0;
+  std::vector<int32_t*> units;                 // per dim (hidden dims only)
+  std::vector<std::vector<int32_t>> offs;      // per dim, m+1
+  std::vector<std::vector<LayerShape>> shapes;  // [slot][layer] for all m slots
+  int64_t S_max = 0;                           // floats per packed slot buffer
+  int slots_per_rank = 0;
+  std::vector<Slot> slots;                     // local slots
+  float* Wall = nullptr;                       // slots_per_rank * S_max (local slot weights, contiguous)
+  float* Wrecv = nullptr;                      // world * slots_per_rank * S_max (world > 1)
+  int alloc_m = 0;
+  void* sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  uint64_t *keys_a = nullptr, *keys_b = nullptr;
+  int32_t *idx_a = nullptr, *idx_b = nullptr, *blk = nullptr, *offs_dev = nullptr;
+  int64_t round = 0, step = 0, adam_t = 0;
+  int64_t nk = 0, h2d = 0, d2h = 0;
+  std::vector<void*> allocs;
+};
+
+// ============================================================== helpers ====
+namespace {
+
+gist_status fail(gist_ctx* c, gist_status s, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (s == GIST_E_CUDA || s == GIST_E_NCCL) c->sticky = s;
+  }
+  return s;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? GIST_E_OOM : GIST_E_CUDA,           \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+#define NK(x)                                                                              \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess) return fail(c, GIST_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#define TRY(x)                        \
+  do {                                \
+    gist_status s_ = (x);             \
+    if (s_ != GIST_OK) return s_;     \
+  } while (0)
+#define PRE(c)                                                        \
+  do {                                                                \
+    if (!(c)) return GIST_E_ARG;                                      \
+    if ((c)->sticky != GIST_OK) return (c)->sticky;                   \
+    cudaSetDevice((c)->cfg.device);                                   \
+  } while (0)
+// launch bookkeeping: every kernel launch of the library goes through LK
+#define LK(expr)  \
+  do {            \
+    expr;         \
+    ++c->nk;      \
+  } while (0)
+
+gist_status dalloc(gist_ctx* c, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, GIST_E_OOM, "cudaMalloc(" + std::to_string(bytes) + " bytes) failed: " + cudaGetErrorString(e));
+  }
+  c->allocs.push_back(*p);
+  return GIST_OK;
+}
+template <typename P>
+gist_status dalloc_t(gist_ctx* c, P** p, size_t count) {
+  return dalloc(c, reinterpret_cast<void**>(p), count * sizeof(P));
+}
+void dfree(gist_ctx* c, void* p) {
+  if (!p) return;
+  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
+  if (it != c->allocs.end()) c->allocs.erase(it);
+  cudaFree(p);
+}
+
+gist_status check_launch(gist_ctx* c, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, GIST_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return GIST_OK;
+}
+
+size_t esize(const gist_ctx* c) { return c->prec == GIST_PREC_BF16 ? 2 : 4; }
+
+int hidden_block_max(const gist_ctx* c, int l, int m) {
+  return (c->dims[l] + m - 1) / m;  // ceil: the largest balanced block (R5)
+}
+
+// logical shape of the sub-weight of slot i, layer l (R6)
+void sub_logical(const gist_ctx* c, int i, int l, int* nrows, int* ncols) {
+  auto bsize = [&](int dim) {
+    if (dim == 0 || dim == c->L) return c->dims[dim];
+    return c->offs[dim][i + 1] - c->offs[dim][i];
+  };
+  *nrows = bsize(l);
+  *ncols = bsize(l + 1);
+}
+
+// Host side of R7: cluster permutation of slot i in epoch e; batch p = perm[pq : (p+1)q)
+void epoch_perm(const gist_ctx* c, int slot, int64_t e, std::vector<int32_t>& out) {
+  std::vector<std::pair<uint64_t, int32_t>> kv(c->c);
+  for (int j = 0; j < c->c; ++j)
+    kv[j] = {philox_key64((uint32_t)j, (uint32_t)e, (uint32_t)slot, PURPOSE_BATCH, c->cfg.batch_seed), j};
+  std::sort(kv.begin(), kv.end());
+  out.resize(c->c);
+  for (int j = 0; j < c->c; ++j) out[j] = kv[j].second;
+}
+
+}  // namespace
+
+// ============================================================ lifecycle ====
+extern "C" void gist_config_default(gist_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->arch = GIST_ARCH_GCN;
+  cfg->optimizer = GIST_OPT_ADAM;
+  cfg->beta1 = 0.9f;
+  cfg->beta2 = 0.999f;
+  cfg->eps = 1e-8f;
+  cfg->precision = GIST_PREC_FP32;
+  cfg->clusters_per_batch = 1;
+  cfg->world_size = 1;
+}
+
+extern "C" const char* gist_status_str(gist_status s) {
+  switch (s) {
+    case GIST_OK: return "GIST_OK";
+    case GIST_E_ARG: return "GIST_E_ARG";
+    case GIST_E_SHAPE: return "GIST_E_SHAPE";
+    case GIST_E_STATE: return "GIST_E_STATE";
+    case GIST_E_OOM: return "GIST_E_OOM";
+    case GIST_E_CUDA: return "GIST_E_CUDA";
+    case GIST_E_NCCL: return "GIST_E_NCCL";
+    case GIST_E_UNSUPPORTED: return "GIST_E_UNSUPPORTED";
+  }
+  return "GIST_E_?";
+}
+
+extern "C" const char* gist_last_error(const gist_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
+  if (!cfg || !out || !cfg->dims || cfg->num_layers < 1) return GIST_E_ARG;
+  *out = nullptr;
+  if (cfg->arch != GIST_ARCH_GCN && cfg->arch != GIST_ARCH_SAGE) return GIST_E_ARG;
+  if (cfg->optimizer != GIST_OPT_SGD && cfg->optimizer != GIST_OPT_ADAM) return GIST_E_ARG;
+  if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
+  if (cfg->clusters_per_batch < 1 || cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    return GIST_E_ARG;
+  for (int l = 0; l <= cfg->num_layers; ++l)
+    if (cfg->dims[l] < 1) return GIST_E_SHAPE;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
+    cudaGetLastError();
+    return GIST_E_UNSUPPORTED;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return GIST_E_UNSUPPORTED;
+  gist_ctx* c = new gist_ctx();
+  c->cfg = *cfg;
+  c->dims.assign(cfg->dims, cfg->dims + cfg->num_layers + 1);
+  c->cfg.dims = c->dims.data();
+  c->L = cfg->num_layers;
+  c->arch = cfg->arch;
+  c->prec = cfg->precision;
+  cudaSetDevice(cfg->device);
+  if (cfg->stream) {
+    c->stream = (cudaStream_t)cfg->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return GIST_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return GIST_E_CUDA;
+  }
+  if (cfg->graph_residency != GIST_GRAPH_DEVICE) {
+    delete c;
+    return GIST_E_UNSUPPORTED;
+  }
+  if (cfg->world_size > 1) {
+    if (!cfg->nccl_unique_id) {
+      delete c;
+      return GIST_E_ARG;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&c->comm, cfg->world_size, id, cfg->rank) != ncclSuccess) {
+      delete c;
+      return GIST_E_NCCL;
+    }
+  }
+  *out = c;
+  return GIST_OK;
+}
+
+static void free_slots(gist_ctx* c) {
+  for (auto& s : c->slots) {
+    if (s.st) cudaStreamDestroy(s.st);
+    if (s.ev) cudaEventDestroy(s.ev);
+    if (s.desc_ev) cudaEventDestroy(s.desc_ev);
+    if (s.desc_host) cudaFreeHost(s.desc_host);
+  }
+  c->slots.clear();
+}
+
+extern "C" void gist_destroy(gist_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  free_slots(c);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+extern "C" void* gist_stream(gist_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+extern "C" int64_t gist_stat(gist_ctx* c, int32_t which) {
+  if (!c) return -1;
+  switch (which) {
+    case GIST_STAT_ROUND: return c->round;
+    case GIST_STAT_STEP: return c->step;
+    case GIST_STAT_SELF_LOOPS_DROPPED: return c->self_loops;
+    case GIST_STAT_LAST_NNZ_B: {
+      if (c->slots.empty()) return 0;
+      int64_t st[2] = {0, 0};
+      cudaMemcpy(st, c->slots[0].stats, sizeof(st), cudaMemcpyDeviceToHost);
+      return st[0];
+    }
+    case GIST_STAT_LAST_NB: return c->slots.empty() ? 0 : c->slots[0].last_nb;
+    case GIST_STAT_KERNELS: return c->nk;
+    case GIST_STAT_H2D_BYTES: return c->h2d;
+    case GIST_STAT_D2H_BYTES: return c->d2h;
+    case GIST_STAT_MAX_NB: return c->nb_max;
+  }
+  return -1;
+}
+
+// ============================================================ load graph ===
+extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                       int64_t nnz, const float* X, const int32_t* labels, int32_t num_classes,
+                                       const uint8_t* split, const int32_t* cluster_ids, int32_t num_clusters) {
+  PRE(c);
+  if (c->state != S_CREATED) return fail(c, GIST_E_STATE, "load_graph: graph already loaded");
+  if (n < 1 || n > INT32_MAX - 1 || !row_ptr || (!col_idx && nnz > 0) || !X || !labels || !split || !cluster_ids)
+    return fail(c, GIST_E_ARG, "load_graph: null pointer or bad n");
+  if (num_classes != c->dims[c->L]) return fail(c, GIST_E_SHAPE, "load_graph: num_classes != d_L");
+  if (num_clusters < 1 || num_clusters > n) return fail(c, GIST_E_ARG, "load_graph: bad num_clusters");
+  if (c->cfg.clusters_per_batch > num_clusters) return fail(c, GIST_E_ARG, "load_graph: q > num_clusters");
+  if (row_ptr[0] != 0 || row_ptr[n] != nnz) return fail(c, GIST_E_ARG, "load_graph: row_ptr[0]/row_ptr[n] mismatch");
+  int64_t self = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    if (row_ptr[v + 1] < row_ptr[v]) return fail(c, GIST_E_ARG, "load_graph: row_ptr decreasing");
+    for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+      const int32_t u = col_idx[e];
+      if (u < 0 || u >= n) return fail(c, GIST_E_ARG, "load_graph: col_idx out of range");
+      self += (u == v);
+    }
+    if (labels[v] < 0 || labels[v] >= num_classes) return fail(c, GIST_E_ARG, "load_graph: label out of range");
+    if (split[v] > 3) return fail(c, GIST_E_ARG, "load_graph: split code > 3");
+    if (cluster_ids[v] < 0 || cluster_ids[v] >= num_clusters)
+      return fail(c, GIST_E_ARG, "load_graph: cluster id out of range");
+  }
+  c->n = n;
+  c->c = num_clusters;
+  c->k = num_classes;
+  c->self_loops = self;
+  c->nnz = nnz - self;
+  // counting sort by cluster (stable in original id): new id -> original id
+  std::vector<int64_t> csize(num_clusters, 0);
+  for (int64_t v = 0; v < n; ++v) csize[cluster_ids[v]]++;
+  c->cstart_h.assign(num_clusters + 1, 0);
+  for (int j = 0; j < num_clusters; ++j) {
+    if (csize[j] == 0) return fail(c, GIST_E_ARG, "load_graph: empty cluster " + std::to_string(j));
+    c->cstart_h[j + 1] = c->cstart_h[j] + csize[j];
+  }
+  c->perm_h.assign(n, 0);
+  std::vector<int32_t> inv(n), cid_new(n), lab_new(n);
+  std::vector<uint8_t> split_new(n);
+  {
+    std::vector<int64_t> pos(c->cstart_h.begin(), c->cstart_h.end() - 1);
+    for (int64_t v = 0; v < n; ++v) {
+      const int64_t g = pos[cluster_ids[v]]++;
+      c->perm_h[g] = (int32_t)v;
+      inv[v] = (int32_t)g;
+    }
+  }
+  for (int64_t g = 0; g < n; ++g) {
+    const int32_t v = c->perm_h[g];
+    cid_new[g] = cluster_ids[v];
+    lab_new[g] = labels[v];
+    split_new[g] = split[v];
+  }
+  // largest possible batch (sum of the q largest clusters) and its nnz bound (sum of q largest volumes)
+  {
+    std::vector<int64_t> sz(csize), vol(num_clusters, 0);
+    for (int64_t v = 0; v < n; ++v) vol[cluster_ids[v]] += row_ptr[v + 1] - row_ptr[v];
+    std::sort(sz.rbegin(), sz.rend());
+    std::sort(vol.rbegin(), vol.rend());
+    int64_t a = 0, b = 0;
+    for (int j = 0; j < c->cfg.clusters_per_batch; ++j) a += sz[j], b += vol[j];
+    c->nb_max = (int)a;
+    c->nnzb_max = b;
+  }
+  cudaStream_t s = c->stream;
+  // device copies of the original CSR, then relabel on the device
+  int64_t *rp_o = nullptr;
+  int32_t *col_o = nullptr, *perm_d = nullptr, *inv_d = nullptr;
+  int64_t* deg_new = nullptr;
+  TRY(dalloc_t(c, &rp_o, n + 1));
+  TRY(dalloc_t(c, &col_o, std::max<int64_t>(nnz, 1)));
+  TRY(dalloc_t(c, &perm_d, n));
+  TRY(dalloc_t(c, &inv_d, n));
+  TRY(dalloc_t(c, &deg_new, n + 1));
+  TRY(dalloc_t(c, &c->rp, n + 1));
+  TRY(dalloc_t(c, &c->col, std::max<int64_t>(c->nnz, 1)));
+  CK(cudaMemcpyAsync(rp_o, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (nnz > 0) CK(cudaMemcpyAsync(col_o, col_idx, nnz * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(perm_d, c->perm_h.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(inv_d, inv.data(), n * 4, cudaMemcpyHostToDevice, s));
+  c->h2d += (n + 1) * 8 + nnz * 4 + n * 8;
+  LK(relabel_count(rp_o, col_o, perm_d, n, deg_new, s));
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, deg_new, c->rp, n + 1, s);
+    void* tmp = nullptr;
+    TRY(dalloc(c, &tmp, tb));
+    CK(cudaMemsetAsync(deg_new + n, 0, 8, s));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, deg_new, c->rp, n + 1, s);
+    ++c->nk;
+    CK(cudaStreamSynchronize(s));
+    dfree(c, tmp);
+  }
+  LK(relabel_fill(rp_o, col_o, perm_d, inv_d, c->rp, n, c->col, s));
+  // features: X_new[g] = X[perm[g]], padded to pad8(d0), in the mode's element type
+  const int d0 = c->dims[0];
+  const int64_t ldx = pad8(d0);
+  float* x_o = nullptr;
+  TRY(dalloc_t(c, &x_o, (size_t)n * d0));
+  CK(cudaMemcpyAsync(x_o, X, (size_t)n * d0 * 4, cudaMemcpyHostToDevice, s));
+  c->h2d += (int64_t)n * d0 * 4;
+  TRY(dalloc(c, &c->X, (size_t)n * ldx * esize(c)));
+  if (c->prec == GIST_PREC_BF16)
+    LK(gather_rows_f32<bf16>(x_o, d0, perm_d, n, d0, (bf16*)c->X, ldx, s));
+  else
+    LK(gather_rows_f32<float>(x_o, d0, perm_d, n, d0, (float*)c->X, ldx, s));
+  TRY(dalloc_t(c, &c->cid, n));
+  TRY(dalloc_t(c, &c->labels, n));
+  TRY(dalloc_t(c, &c->split, n));
+  TRY(dalloc_t(c, &c->cstart, num_clusters + 1));
+  TRY(dalloc_t(c, &c->full_scale, n));
+  CK(cudaMemcpyAsync(c->cid, cid_new.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->labels, lab_new.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->split, split_new.data(), n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->cstart, c->cstart_h.data(), (num_clusters + 1) * 8, cudaMemcpyHostToDevice, s));
+  c->h2d += n * 9 + (num_clusters + 1) * 8;
+  LK(full_graph_scales(c->rp, n, c->arch, c->full_scale, s));
+  CK(cudaStreamSynchronize(s));
+  TRY(check_launch(c, "load_graph"));
+  dfree(c, rp_o);
+  dfree(c, col_o);
+  dfree(c, perm_d);
+  dfree(c, inv_d);
+  dfree(c, deg_new);
+  dfree(c, x_o);
+  // global parameter storage (physical layout)
+  c->theta.assign(c->L, nullptr);
+  c->th_K.assign(c->L, 0);
+  c->th_N.assign(c->L, 0);
+  for (int l = 0; l < c->L; ++l) {
+    c->th_K[l] = c->arch == GIST_ARCH_SAGE ? 2 * pad8(c->dims[l]) : pad8(c->dims[l]);
+    c->th_N[l] = pad8(c->dims[l + 1]);
+    TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
+    CK(cudaMemsetAsync(c->theta[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, s));
+  }
+  c->state = S_GRAPH;
+  return GIST_OK;
+}
+
+// ============================================================= params =====
+extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
+  PRE(c);
+  if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "init_params: bad state");
+  for (int l = 0; l < c->L; ++l) {
+    const int rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[l] : c->dims[l];
+    const int cols = c->dims[l + 1];
+    const float sc = std::sqrt(6.0f / (float)(rows + cols));  // fp32, correctly rounded (R11)
+    LK(glorot_init(c->theta[l], rows, cols, c->arch == GIST_ARCH_SAGE, c->dims[l], (int)pad8(c->dims[l]),
+                   c->th_N[l], (uint32_t)l, seed, sc, c->stream));
+  }
+  TRY(check_launch(c, "init_params"));
+  c->state = S_PARAMS;
+  return GIST_OK;
+}
+
+static int64_t logical_to_phys_row(const gist_ctx* c, int l, int64_t r) {
+  if (c->arch == GIST_ARCH_SAGE && r >= c->dims[l]) return pad8(c->dims[l]) + (r - c->dims[l]);
+  return r;
+}
+
+extern "C" gist_status gist_get_params(gist_ctx* c, int32_t layer, float* out) {
+  PRE(c);
+  if (c->state == S_CREATED) return fail(c, GIST_E_STATE, "get_params: no graph");
+  if (layer < 0 || layer >= c->L || !out) return GIST_E_ARG;
+  const int64_t K = c->th_K[layer], N = c->th_N[layer];
+  std::vector<float> buf(K * N);
+  CK(cudaMemcpyAsync(buf.data(), c->theta[layer], K * N * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const int64_t rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[layer] : c->dims[layer];
+  const int64_t cols = c->dims[layer + 1];
+  for (int64_t r = 0; r < rows; ++r)
+    std::memcpy(out + r * cols, buf.data() + logical_to_phys_row(c, layer, r) * N, cols * 4);
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* in) {
+  PRE(c);
+  if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "set_params: bad state");
+  if (layer < 0 || layer >= c->L || !in) return GIST_E_ARG;
+  const int64_t K = c->th_K[layer], N = c->th_N[layer];
+  std::vector<float> buf(K * N, 0.f);
+  const int64_t rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[layer] : c->dims[layer];
+  const int64_t cols = c->dims[layer + 1];
+  for (int64_t r = 0; r < rows; ++r)
+    std::memcpy(buf.data() + logical_to_phys_row(c, layer, r) * N, in + r * cols, cols * 4);
+  CK(cudaMemcpyAsync(c->theta[layer], buf.data(), K * N * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->h2d += K * N * 4;
+  bool all = true;  // params become valid once every layer was set or init_params ran
+  c->state = S_PARAMS;
+  (void)all;
+  return GIST_OK;
+}
+
+// ============================================================ partition ===
+static gist_status alloc_slots(gist_ctx* c, int m) {
+  free_slots(c);
+  const int W = c->cfg.world_size, r = c->cfg.rank;
+  c->slots_per_rank = (m + W - 1) / W;
+  // largest packed slot (every hidden block at ceil(d/m))
+  int64_t smax = 0;
+  std::vector<int> maxK(c->L), maxN(c->L);
+  for (int l = 0; l < c->L; ++l) {
+    const int nr = (l == 0) ? c->dims[0] : hidden_block_max(c, l, m);
+    const int nc = (l + 1 == c->L) ? c->dims[c->L] : hidden_block_max(c, l + 1, m);
+    maxK[l] = (int)(c->arch == GIST_ARCH_SAGE ? 2 * pad8(nr) : pad8(nr));
+    maxN[l] = (int)pad8(nc);
+    smax += (int64_t)maxK[l] * maxN[l];
+  }
+  c->S_max = smax;
+  TRY(dalloc_t(c, &c->Wall, (size_t)c->slots_per_rank * smax));
+  if (W > 1) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * c->slots_per_rank * smax));
+  const int nbm = std::max(c->nb_max, 1);
+  const size_t E = esize(c);
+  int maxKall = 0;
+  for (int l = 0; l < c->L; ++l) maxKall = std::max(maxKall, maxK[l]);
+  for (int i = r, j = 0; i < m; i += W, ++j) {
+    c->slots.emplace_back();
+    Slot& s = c->slots.back();
+    s.index = i;
+    CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.desc_ev, cudaEventDisableTiming));
+    s.W = c->Wall + (size_t)j * smax;
+    TRY(dalloc_t(c, &s.G, smax));
+    if (c->cfg.optimizer == GIST_OPT_ADAM) {
+      TRY(dalloc_t(c, &s.M, smax));
+      TRY(dalloc_t(c, &s.V, smax));
+    }
+    if (c->prec == GIST_PREC_BF16) TRY(dalloc_t(c, &s.Wb, smax));
+    TRY(dalloc_t(c, &s.b_nodes, nbm));
+    TRY(dalloc_t(c, &s.deg_b, nbm));
+    TRY(dalloc_t(c, &s.lab_b, nbm));
+    TRY(dalloc_t(c, &s.train_b, nbm));
+    TRY(dalloc_t(c, &s.scale, nbm));
+    TRY(dalloc_t(c, &s.b_rp, nbm + 1));
+    TRY(dalloc_t(c, &s.stats, 2));
+    TRY(dalloc_t(c, &s.b_col, std::max<int64_t>(c->nnzb_max, 1)));
+    TRY(dalloc_t(c, &s.map_cl, c->c));
+    CK(cudaMemsetAsync(s.map_cl, 0xff, (size_t)c->c * 4, c->stream));  // -1
+    s.C.assign(c->L, nullptr);
+    s.H.assign(c->L, nullptr);
+    s.dZ.assign(c->L, nullptr);
+    for (int l = 0; l < c->L; ++l) {
+      TRY(dalloc(c, &s.C[l], (size_t)nbm * maxK[l] * E));
+      if (c->arch == GIST_ARCH_GCN && l > 0) TRY(dalloc(c, &s.H[l], (size_t)nbm * maxK[l] * E));
+      TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
+    }
+    TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
+    TRY(dalloc_t(c, &s.logits, (size_t)nbm * maxN[c->L - 1]));
+    TRY(dalloc_t(c, &s.row_loss, nbm));
+    TRY(dalloc_t(c, &s.step_loss, 1));
+    TRY(dalloc_t(c, &s.loss_acc, 1));
+  }
+  c->alloc_m = m;
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
+  PRE(c);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "partition: needs params and no open round");
+  if (m < 1) return fail(c, GIST_E_ARG, "partition: m < 1");
+  for (int l = 1; l < c->L; ++l)
+    if (m > c->dims[l]) return fail(c, GIST_E_ARG, "partition: m exceeds hidden dim " + std::to_string(l));
+  cudaStream_t s = c->stream;
+  if (m != c->alloc_m) TRY(alloc_slots(c, m));
+  c->m = m;
+  // subGCNs keys / sort / blocks for every hidden dim (R5)
+  int dmax = 0;
+  for (int l = 1; l < c->L; ++l) dmax = std::max(dmax, c->dims[l]);
+  if (c->units.empty()) {
+    c->units.assign(c->L + 1, nullptr);
+    for (int l = 1; l < c->L; ++l) TRY(dalloc_t(c, &c->units[l], c->dims[l]));
+    if (dmax > 0) {
+      TRY(dalloc_t(c, &c->keys_a, dmax));
+      TRY(dalloc_t(c, &c->keys_b, dmax));
+      TRY(dalloc_t(c, &c->idx_a, dmax));
+      TRY(dalloc_t(c, &c->idx_b, dmax));
+      TRY(dalloc_t(c, &c->blk, dmax));
+      c->sort_tmp_bytes = partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, dmax, nullptr, 0, s);
+      TRY(dalloc(c, &c->sort_tmp, c->sort_tmp_bytes));
+    }
+  }
+  if (c->offs_dev) dfree(c, c->offs_dev);
+  TRY(dalloc_t(c, &c->offs_dev, (size_t)(m + 1) * (c->L + 1)));
+  c->offs.assign(c->L + 1, std::vector<int32_t>());
+  std::vector<int32_t> offs_all((size_t)(m + 1) * (c->L + 1), 0);
+  for (int l = 0; l <= c->L; ++l) {
+    const int d = c->dims[l];
+    std::vector<int32_t>& o = c->offs[l];
+    o.assign(m + 1, 0);
+    if (l == 0 || l == c->L) {
+      for (int i = 0; i <= m; ++i) o[i] = 0;  // unused: identity
+      continue;
+    }
+    const int base = d / m, extra = d % m;
+    for (int i = 0; i < m; ++i) o[i + 1] = o[i] + base + (i < extra ? 1 : 0);
+    std::copy(o.begin(), o.end(), offs_all.begin() + (size_t)l * (m + 1));
+  }
+  CK(cudaMemcpyAsync(c->offs_dev, offs_all.data(), offs_all.size() * 4, cudaMemcpyHostToDevice, s));
+  for (int l = 1; l < c->L; ++l) {
+    const int d = c->dims[l];
+    LK(partition_keys(d, (uint32_t)c->round, (uint32_t)l, seed, c->keys_a, c->idx_a, s));
+    partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, d, c->sort_tmp, c->sort_tmp_bytes, s);
+    ++c->nk;
+    LK(partition_assign(c->idx_b, d, m, c->blk, s));
+    LK(partition_compact(c->blk, d, m, c->offs_dev + (size_t)l * (m + 1), c->units[l], s));
+  }
+  // shapes of every slot (all ranks know the full partition)
+  c->shapes.assign(m, std::vector<LayerShape>(c->L));
+  for (int i = 0; i < m; ++i) {
+    int64_t off = 0;
+    for (int l = 0; l < c->L; ++l) {
+      LayerShape& sh = c->shapes[i][l];
+      sub_logical(c, i, l, &sh.nrows, &sh.ncols);
+      sh.half = (int)pad8(sh.nrows);
+      sh.Kp = (int)(c->arch == GIST_ARCH_SAGE ? 2 * pad8(sh.nrows) : pad8(sh.nrows));
+      sh.Np = (int)pad8(sh.ncols);
+      sh.off = off;
+      off += (int64_t)sh.Kp * sh.Np;
+      sh.rows = (l == 0) ? nullptr : c->units[l] + c->offs[l][i];
+      sh.cols = (l + 1 == c->L) ? nullptr : c->units[l + 1] + c->offs[l + 1][i];
+    }
+  }
+  // extract Theta^(i) for local slots (R6), reset optimizer state (R8)
+  for (Slot& sl : c->slots) {
+    const auto& shp = c->shapes[sl.index];
+    int64_t tot = 0;
+    for (int l = 0; l < c->L; ++l) {
+      const LayerShape& sh = shp[l];
+      LayerMap mp;
+      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
+      mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
+      mp.ldg = c->th_N[l];
+      LK(extract_sub(c->theta[l], mp, sl.W + sh.off, s));
+      tot = sh.off + (int64_t)sh.Kp * sh.Np;
+    }
+    if (sl.M) {
+      CK(cudaMemsetAsync(sl.M, 0, (size_t)c->S_max * 4, s));
+      CK(cudaMemsetAsync(sl.V, 0, (size_t)c->S_max * 4, s));
+    }
+    if (sl.Wb) LK(f32_to_bf16(sl.W, sl.Wb, tot, s));
+  }
+  TRY(check_launch(c, "partition"));
+  c->adam_t = 0;
+  c->state = S_PARTITIONED;
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_get_partition(gist_ctx* c, int32_t dim, int32_t* units, int32_t* offs) {
+  PRE(c);
+  if (c->m == 0 || c->offs.empty()) return fail(c, GIST_E_STATE, "get_partition: no partition yet");
+  if (dim < 0 || dim > c->L || !units || !offs) return GIST_E_ARG;
+  const int d = c->dims[dim];
+  if (dim == 0 || dim == c->L) {
+    for (int r = 0; r < d; ++r) units[r] = r;
+    for (int i = 0; i <= c->m; ++i) offs[i] = 0;
+    offs[c->m] = d;
+    return GIST_OK;
+  }
+  CK(cudaMemcpyAsync(units, c->units[dim], (size_t)d * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  std::copy(c->offs[dim].begin(), c->offs[dim].end(), offs);
+  return GIST_OK;
+}
+
+// ============================================================== step ======
+static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
+                            cudaStream_t s) {
+  if (c->prec == GIST_PREC_FP32) {
+    LK(gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s));
+    return GIST_OK;
+  }
+  if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s))
+    return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
+  ++c->nk;
+  return GIST_OK;
+}
+
+template <typename T>
+static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
+  cudaStream_t s = sl.st;
+  const int q = c->cfg.clusters_per_batch;
+  const int nb = sl.nb_of_step[z];
+  const int qq = sl.q_of_step[z];  // clusters in this batch (< q only for an epoch's last batch)
+  const int32_t* d = sl.desc_dev + (size_t)z * (2 * q + 2);
+  const int32_t* bcl = d;
+  const int32_t* loff = d + q;
+  const bool sage = c->arch == GIST_ARCH_SAGE;
+  const auto& shp = c->shapes[sl.index];
+  const int L = c->L;
+  sl.last_nb = nb;
+  // ---- a1: Cluster mini-batch build
+  LK(batch_nodes(bcl, loff, qq, c->cstart, sl.map_cl, sl.b_nodes, nb, s));
+  LK(batch_count(c->rp, c->col, c->cid, sl.map_cl, sl.b_nodes, nb, c->arch, c->labels, c->split, sl.deg_b, sl.scale,
+                 sl.lab_b, sl.train_b, s));
+  LK(batch_scan(sl.deg_b, sl.train_b, nb, sl.b_rp, sl.stats, s));
+  LK(batch_fill(c->rp, c->col, c->cid, sl.map_cl, c->cstart, sl.b_nodes, nb, sl.b_rp, sl.b_col, s));
+  LK(batch_reset(bcl, qq, sl.map_cl, s));
+  const T* Wop = c->prec == GIST_PREC_BF16 ? (const T*)sl.Wb : (const T*)sl.W;
+  // ---- a2/a3: forward
+  for (int l = 0; l < L; ++l) {
+    const LayerShape& sh = shp[l];
+    T* C = (T*)sl.C[l];
+    SpmmArgs<T> a;
+    a.row_ptr = sl.b_rp; a.col = sl.b_col; a.rows = nb;
+    if (sage) {
+      a.rowscale = sl.scale;              // N = D^-1 A (R2)
+      a.out = C + sh.half; a.ldo = sh.Kp;  // right half: N H
+      a.w = sh.half;
+      if (l == 0) {
+        a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]);
+        a.self_out = C; a.ld_self = sh.Kp;  // left half: H (gathered X rows)
+      } else {
+        a.H = C; a.ldh = sh.Kp;              // left half written by the previous GEMM epilogue
+      }
+    } else {
+      a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;  // D~^-1/2 (A+I) D~^-1/2 (R1)
+      a.out = C; a.ldo = sh.Kp; a.w = sh.Kp;
+      if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
+      else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
+    }
+    LK(spmm<T>(a, s));
+    const T* Wl = Wop + sh.off;
+    if (l + 1 < L) {
+      const LayerShape& nx = shp[l + 1];
+      T* out = sage ? (T*)sl.C[l + 1] : (T*)sl.H[l + 1];
+      TRY(gemm_any(c, false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, nx.Kp, false, true, s));
+    } else {
+      TRY(gemm_any(c, false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false, s));
+    }
+  }
+  // ---- a4: softmax cross-entropy
+  const LayerShape& last = shp[L - 1];
+  LK(softmax_ce<T>(sl.logits, last.Np, nb, c->k, sl.lab_b, sl.train_b, sl.stats, (T*)sl.dZ[L - 1], sl.row_loss, s));
+  LK(reduce_loss(sl.row_loss, nb, sl.stats, sl.step_loss, sl.loss_acc, s));
+  // ---- a5/a6: backward
+  for (int l = L - 1; l >= 0; --l) {
+    const LayerShape& sh = shp[l];
+    const T* Wl = Wop + sh.off;
+    // dW_l = C_l^T dZ_l  (fp32 into the packed gradient buffer)
+    TRY(gemm_any(c, true, false, sh.Kp, sh.Np, nb, sl.C[l], sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
+                 s));
+    if (l == 0) break;
+    // dC_l = dZ_l W_l^T
+    TRY(gemm_any(c, false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false, s));
+    SpmmArgs<T> a;
+    a.row_ptr = sl.b_rp; a.col = sl.b_col; a.rows = nb;
+    a.out = (T*)sl.dZ[l - 1]; a.ldo = shp[l - 1].Np;
+    if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
+      a.colscale = sl.scale; a.H = (const T*)sl.dC + sh.half; a.ldh = sh.Kp;
+      a.add = (const T*)sl.dC; a.ld_add = sh.Kp;
+      a.mask = (const T*)sl.C[l]; a.ld_mask = sh.Kp;
+      a.w = sh.half;
+    } else {     // dZ_{l-1} = (A_hat^T dC) * 1[H_l > 0]
+      a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;
+      a.H = (const T*)sl.dC; a.ldh = sh.Kp;
+      a.mask = (const T*)sl.H[l]; a.ld_mask = sh.Kp;
+      a.w = sh.Kp;
+    }
+    LK(spmm<T>(a, s));
+  }
+  // ---- a7: optimizer
+  int64_t tot = last.off + (int64_t)last.Kp * last.Np;
+  bf16* Wb = c->prec == GIST_PREC_BF16 ? sl.Wb : nullptr;
+  if (c->cfg.optimizer == GIST_OPT_ADAM) {
+    const double t = (double)(c->adam_t + 1);
+    const float bc1 = (float)(1.0 - std::pow((double)c->cfg.beta1, t));
+    const float bc2 = (float)(1.0 - std::pow((double)c->cfg.beta2, t));
+    LK(adam_step(sl.W, sl.G, sl.M, sl.V, tot, lr, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, bc1, std::sqrt(bc2), Wb, s));
+  } else {
+    LK(sgd_step(sl.W, sl.G, tot, lr, Wb, s));
+  }
+  return GIST_OK;
+}
+
+// host side of R7 for a whole subtrain call: cluster lists, local offsets, n_b per step
+static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
+  const int q = c->cfg.clusters_per_batch;
+  const int per = 2 * q + 2;
+  if (iters > sl.cap) {
+    if (sl.desc_host) {
+      CK(cudaEventSynchronize(sl.desc_ev));
+      cudaFreeHost(sl.desc_host);
+      dfree(c, sl.desc_dev);
+    }
+    sl.cap = std::max(iters, 16);
+    CK(cudaMallocHost(&sl.desc_host, (size_t)sl.cap * per * 4));
+    TRY(dalloc_t(c, &sl.desc_dev, (size_t)sl.cap * per));
+  } else {
+    CK(cudaEventSynchronize(sl.desc_ev));  // previous upload finished reading the pinned buffer
+  }
+  sl.nb_of_step.assign(iters, 0);
+  sl.q_of_step.assign(iters, 0);
+  const int64_t B = (c->c + q - 1) / q;
+  for (int z = 0; z < iters; ++z) {
+    const int64_t st = c->step + z;
+    const int64_t e = st / B, p = st % B;
+    if (sl.cached_epoch != e) {
+      epoch_perm(c, sl.index, e, sl.epoch_perm);
+      sl.cached_epoch = (int)e;
+    }
+    int32_t* d = sl.desc_host + (size_t)z * per;
+    const int64_t lo = p * q, hi = std::min<int64_t>((p + 1) * q, c->c);
+    const int qq = (int)(hi - lo);
+    int32_t off = 0;
+    for (int k = 0; k < q; ++k) {
+      if (k < qq) {
+        const int32_t cl = sl.epoch_perm[lo + k];
+        d[k] = cl;
+        d[q + k] = off;
+        off += (int32_t)(c->cstart_h[cl + 1] - c->cstart_h[cl]);
+      } else {  // last batch of an epoch may hold fewer clusters: empty ranges
+        d[k] = d[qq - 1];
+        d[q + k] = off;
+      }
+    }
+    d[2 * q] = off;
+    d[2 * q + 1] = qq;
+    sl.nb_of_step[z] = off;
+    sl.q_of_step[z] = qq;
+  }
+  CK(cudaMemcpyAsync(sl.desc_dev, sl.desc_host, (size_t)iters * per * 4, cudaMemcpyHostToDevice, sl.st));
+  CK(cudaEventRecord(sl.desc_ev, sl.st));
+  c->h2d += (int64_t)iters * per * 4;
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr, float* mean_loss) {
+  PRE(c);
+  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "subtrain: call partition first");
+  if (local_iters < 0) return fail(c, GIST_E_ARG, "subtrain: local_iters < 0");
+  if (c->prec == GIST_PREC_BF16 && !gemm_bf16(false, false, 0, 0, 0, nullptr, 0, nullptr, 0, nullptr, 0, false, false,
+                                              c->stream))
+    return fail(c, GIST_E_UNSUPPORTED, "bf16 mode needs the tcgen05 GEMM");
+  CK(cudaEventRecord(c->fork_ev, c->stream));
+  for (Slot& sl : c->slots) {
+    CK(cudaStreamWaitEvent(sl.st, c->fork_ev, 0));
+    TRY(schedule(c, sl, local_iters));
+    CK(cudaMemsetAsync(sl.loss_acc, 0, 4, sl.st));
+  }
+  for (int z = 0; z < local_iters; ++z) {
+    for (Slot& sl : c->slots) {
+      if (c->prec == GIST_PREC_BF16) TRY(run_step<bf16>(c, sl, z, lr));
+      else TRY(run_step<float>(c, sl, z, lr));
+    }
+    ++c->adam_t;
+  }
+  for (Slot& sl : c->slots) {
+    CK(cudaEventRecord(sl.ev, sl.st));
+    CK(cudaStreamWaitEvent(c->stream, sl.ev, 0));
+  }
+  c->step += local_iters;
+  TRY(check_launch(c, "subtrain"));
+  if (mean_loss) {
+    std::fill(mean_loss, mean_loss + c->m, 0.f);
+    for (Slot& sl : c->slots) {
+      float v = 0.f;
+      CK(cudaMemcpyAsync(&v, sl.loss_acc, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      mean_loss[sl.index] = local_iters > 0 ? v / (float)local_iters : 0.f;
+      c->d2h += 4;
+    }
+  }
+  return GIST_OK;
+}
+
+// ============================================================ aggregate ===
+extern "C" gist_status gist_aggregate(gist_ctx* c) {
+  PRE(c);
+  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "aggregate: no open round");
+  cudaStream_t s = c->stream;
+  const int W = c->cfg.world_size;
+  const float* src = c->Wall;
+  if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
+    NK(ncclAllGather(c->Wall, c->Wrecv, (size_t)c->slots_per_rank * c->S_max, ncclFloat, c->comm, s));
+    src = c->Wrecv;
+  }
+  for (int i = 0; i < c->m; ++i) {
+    const int rank = i % W, j = i / W;
+    const float* w = src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
+    if (W == 1) w = c->Wall + (size_t)j * c->S_max;
+    for (int l = 0; l < c->L; ++l) {
+      const LayerShape& sh = c->shapes[i][l];
+      LayerMap mp;
+      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
+      mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
+      mp.ldg = c->th_N[l];
+      LK(scatter_sub(c->theta[l], mp, w + sh.off, s));
+    }
+  }
+  TRY(check_launch(c, "aggregate"));
+  c->round += 1;
+  c->state = S_PARAMS;
+  return GIST_OK;
+}
+
+// ================================================================ eval ====
+template <typename T>
+static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->n;
+  const bool sage = c->arch == GIST_ARCH_SAGE;
+  int64_t maxK = 0;
+  for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
+  void *bufA = nullptr, *bufB = nullptr, *wtmp = nullptr;
+  float* logits = nullptr;
+  double* out3 = nullptr;
+  TRY(dalloc(c, &bufA, (size_t)n * maxK * sizeof(T)));
+  TRY(dalloc(c, &bufB, (size_t)n * maxK * sizeof(T)));
+  TRY(dalloc_t(c, &logits, (size_t)n * c->th_N[c->L - 1]));
+  TRY(dalloc_t(c, &out3, 3));
+  T* Cb = (T*)bufA;
+  T* Hn = (T*)bufB;
+  for (int l = 0; l < c->L; ++l) {
+    const int64_t K = c->th_K[l], N = c->th_N[l];
+    const int64_t half = pad8(c->dims[l]);
+    SpmmArgs<T> a;
+    a.row_ptr = c->rp; a.col = c->col; a.rows = n; a.rowscale = c->full_scale;
+    const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
+    if (sage) {
+      if (l == 0) { a.self_out = Cb; a.ld_self = K; }
+      a.H = l == 0 ? Hin : Cb; a.ldh = l == 0 ? half : K;
+      a.out = Cb + half; a.ldo = K; a.w = half;
+    } else {
+      a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
+    }
+    LK(spmm<T>(a, s));
+    const void* Wl = c->theta[l];
+    if (sizeof(T) == 2) {
+      if (wtmp) dfree(c, wtmp);
+      TRY(dalloc(c, &wtmp, (size_t)K * N * 2));
+      LK(f32_to_bf16(c->theta[l], (bf16*)wtmp, K * N, s));
+      Wl = wtmp;
+    }
+    if (l + 1 < c->L) {
+      // next layer input: SAGE writes the left half of the next concat buffer (swap buffers)
+      // GCN: H_{l+1} -> Hn; SAGE: H_{l+1} -> left half of Hn, which becomes the next concat buffer
+      TRY(gemm_any(c, false, false, n, N, K, Cb, K, Wl, N, Hn, c->th_K[l + 1], false, true, s));
+      if (sage) std::swap(Cb, Hn);  // Hn (now holding H_{l+1} as left half) becomes the concat buffer
+    } else {
+      TRY(gemm_any(c, false, false, n, N, K, Cb, K, Wl, N, logits, N, true, false, s));
+    }
+  }
+  LK(eval_rows(logits, c->th_N[c->L - 1], n, c->k, c->labels, c->split, code, out3, s));
+  double h[3];
+  CK(cudaMemcpyAsync(h, out3, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  TRY(check_launch(c, "eval"));
+  if (loss) *loss = h[2] > 0 ? (float)(h[0] / h[2]) : 0.f;
+  if (acc) *acc = h[2] > 0 ? (float)(h[1] / h[2]) : 0.f;
+  dfree(c, bufA);
+  dfree(c, bufB);
+  dfree(c, logits);
+  dfree(c, out3);
+  if (wtmp) dfree(c, wtmp);
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_eval(gist_ctx* c, int32_t split_code, float* loss, float* acc) {
+  PRE(c);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval: needs params and no open round");
+  if (split_code < 0 || split_code > 3) return GIST_E_ARG;
+  if (c->prec == GIST_PREC_BF16) return eval_t<bf16>(c, split_code, loss, acc);
+  return eval_t<float>(c, split_code, loss, acc);
+}
+
+// ====================================================== inspection hooks ===
+extern "C" gist_status gist_sub_shape(gist_ctx* c, int32_t slot, int32_t layer, int64_t* rows, int64_t* cols) {
+  PRE(c);
+  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "sub_shape: no open round");
+  if (slot < 0 || slot >= c->m || layer < 0 || layer >= c->L) return GIST_E_ARG;
+  const LayerShape& sh = c->shapes[slot][layer];
+  if (rows) *rows = c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows;
+  if (cols) *cols = sh.ncols;
+  return GIST_OK;
+}
+
+static Slot* local_slot(gist_ctx* c, int slot) {
+  for (Slot& s : c->slots)
+    if (s.index == slot) return &s;
+  return nullptr;
+}
+
+// physical packed block -> logical row-major
+static void phys_to_logical(const gist_ctx* c, const LayerShape& sh, const std::vector<float>& buf, float* out) {
+  const int rows = c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows;
+  for (int r = 0; r < rows; ++r) {
+    const int p = (c->arch == GIST_ARCH_SAGE && r >= sh.nrows) ? sh.half + (r - sh.nrows) : r;
+    std::memcpy(out + (size_t)r * sh.ncols, buf.data() + (size_t)p * sh.Np, (size_t)sh.ncols * 4);
+  }
+}
+
+extern "C" gist_status gist_get_sub_params(gist_ctx* c, int32_t slot, int32_t layer, float* out) {
+  PRE(c);
+  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "get_sub_params: no open round");
+  if (layer < 0 || layer >= c->L || !out) return GIST_E_ARG;
+  Slot* sl = local_slot(c, slot);
+  if (!sl) return fail(c, GIST_E_ARG, "get_sub_params: slot not on this rank");
+  const LayerShape& sh = c->shapes[slot][layer];
+  std::vector<float> buf((size_t)sh.Kp * sh.Np);
+  CK(cudaStreamSynchronize(sl->st));
+  CK(cudaMemcpy(buf.data(), sl->W + sh.off, buf.size() * 4, cudaMemcpyDeviceToHost));
+  phys_to_logical(c, sh, buf, out);
+  return GIST_OK;
+}
+
+template <typename T>
+static void copy_rows_out(const void* dev, int nb, int64_t ld, int w, float* out) {
+  std::vector<T> buf((size_t)nb * ld);
+  cudaMemcpy(buf.data(), dev, buf.size() * sizeof(T), cudaMemcpyDeviceToHost);
+  for (int v = 0; v < nb; ++v)
+    for (int j = 0; j < w; ++j) {
+      if constexpr (sizeof(T) == 4) out[(size_t)v * w + j] = (float)buf[(size_t)v * ld + j];
+      else out[(size_t)v * w + j] = __bfloat162float(buf[(size_t)v * ld + j]);
+    }
+}
+
+extern "C" gist_status gist_get_trace(gist_ctx* c, int32_t slot, int32_t what, int32_t layer, void* out,
+                                      int64_t* count) {
+  PRE(c);
+  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "get_trace: no open round");
+  Slot* sl = local_slot(c, slot);
+  if (!sl) return fail(c, GIST_E_ARG, "get_trace: slot not on this rank");
+  CK(cudaStreamSynchronize(sl->st));
+  const int nb = sl->last_nb;
+  const auto& shp = c->shapes[slot];
+  int64_t cnt = 0;
+  switch (what) {
+    case GIST_TRACE_NODES: {
+      cnt = nb;
+      if (out) {
+        std::vector<int32_t> b(nb);
+        CK(cudaMemcpy(b.data(), sl->b_nodes, (size_t)nb * 4, cudaMemcpyDeviceToHost));
+        for (int v = 0; v < nb; ++v) ((int32_t*)out)[v] = c->perm_h[b[v]];
+      }
+      break;
+    }
+    case GIST_TRACE_ACT: {
+      if (layer < 1 || layer >= c->L) return GIST_E_ARG;
+      const LayerShape& sh = shp[layer];
+      cnt = (int64_t)nb * sh.nrows;
+      if (out) {
+        const void* src = c->arch == GIST_ARCH_SAGE ? sl->C[layer] : sl->H[layer];
+        if (c->prec == GIST_PREC_BF16) copy_rows_out<bf16>(src, nb, sh.Kp, sh.nrows, (float*)out);
+        else copy_rows_out<float>(src, nb, sh.Kp, sh.nrows, (float*)out);
+      }
+      break;
+    }
+    case GIST_TRACE_LOGITS: {
+      const LayerShape& sh = shp[c->L - 1];
+      cnt = (int64_t)nb * c->k;
+      if (out) copy_rows_out<float>(sl->logits, nb, sh.Np, c->k, (float*)out);
+      break;
+    }
+    case GIST_TRACE_GRAD: {
+      if (layer < 0 || layer >= c->L) return GIST_E_ARG;
+      const LayerShape& sh = shp[layer];
+      cnt = (int64_t)(c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows) * sh.ncols;
+      if (out) {
+        std::vector<float> buf((size_t)sh.Kp * sh.Np);
+        CK(cudaMemcpy(buf.data(), sl->G + sh.off, buf.size() * 4, cudaMemcpyDeviceToHost));
+        phys_to_logical(c, sh, buf, (float*)out);
+      }
+      break;
+    }
+    case GIST_TRACE_LOSS: {
+      cnt = 1;
+      if (out) CK(cudaMemcpy(out, sl->step_loss, 4, cudaMemcpyDeviceToHost));
+      break;
+    }
+    default:
+      return GIST_E_ARG;
+  }
+  if (count) *count = cnt;
+  return GIST_OK;
+}
+
+// ===================================================== kernel entry points =
+extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_dev, int64_t rows,
+                                 const float* rowscale_dev, const float* colscale_dev, int32_t self, const void* H_dev,
+                                 void* out_dev, int64_t w, int64_t ld, int32_t dtype, void* stream) {
+  if (!row_ptr_dev || !H_dev || !out_dev || w < 0 || ld < w || (ld % 8) != 0) return GIST_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 0) {
+    SpmmArgs<float> a;
+    a.row_ptr = row_ptr_dev; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
+    a.self = self; a.H = (const float*)H_dev; a.ldh = ld; a.out = (float*)out_dev; a.ldo = ld; a.w = pad8(w);
+    spmm<float>(a, s);
+  } else if (dtype == 1) {
+    SpmmArgs<bf16> a;
+    a.row_ptr = row_ptr_dev; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
+    a.self = self; a.H = (const bf16*)H_dev; a.ldh = ld; a.out = (bf16*)out_dev; a.ldo = ld; a.w = pad8(w);
+    spmm<bf16>(a, s);
+  } else {
+    return GIST_E_ARG;
+  }
+  return cudaGetLastError() == cudaSuccess ? GIST_OK : GIST_E_CUDA;
+}
+
+extern "C" gist_status gist_gemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, const void* A_dev,
+                                 int64_t lda, const void* B_dev, int64_t ldb, void* C_dev, int64_t ldc, int32_t dtype,
+                                 int32_t out_f32, int32_t relu, void* stream) {
+  if (!A_dev || !B_dev || !C_dev || M < 0 || N < 0 || K < 0) return GIST_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == 0) {
+    gemm_f32(transA, transB, M, N, K, (const float*)A_dev, lda, (const float*)B_dev, ldb, (float*)C_dev, ldc, relu, s);
+  } else if (dtype == 1) {
+    if (!gemm_bf16(transA, transB, M, N, K, (const bf16*)A_dev, lda, (const bf16*)B_dev, ldb, C_dev, ldc, out_f32,
+                   relu, s))
+      return GIST_E_UNSUPPORTED;
+  } else {
+    return GIST_E_ARG;
+  }
+  return cudaGetLastError() == cudaSuccess ? GIST_OK : GIST_E_CUDA;
+}
