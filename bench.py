@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""GIST hot-path benchmark (BASELINE.json metric: sub-GCN epoch time & train steps/s,
+Reddit-shape GraphSAGE; workload = configs[2] = C3 by default).
+
+A bench "step" is one GIST round of Algorithm 1, i.e. one pass
+of every SURVEY 8(a) row: subGCNs (partition + extract), zeta subTrain steps of
+every sub-GCN (batch build, SpMM, GEMMs, CE, backward, Adam), subAgg.
+`value` = sub-GCN train steps per second of the whole job (all ranks), device-timed
+with CUDA events on the library stream, inputs resident in HBM, L2 flushed
+between timed rounds.  `e2e` = the same metric through the public API from host
+buffers: gist_load_graph of the host graph + the rounds + per-round loss readback.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--precision fp32|bf16]
+  python bench.py --impl reference ...   # the FP64 oracle on host cores (rank 0 only)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from synth.planted import GRAPHS, MODELS, generate  # noqa: E402
+
+METRIC = "sub-GCN train steps/s (box-level), Reddit-shape GraphSAGE"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained"),
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                s, mx = float(r[1]), float(r[2])
+            except (ValueError, IndexError):
+                continue
+            smax = mx
+            sm.append(s)
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * (smax or 1)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------- oracle
+def oracle_steps_per_s(spec, g, seconds: float, max_steps: int, min_steps: int = 2, seed: int = 0):
+    """Times the FP64 oracle (as it stands) on a bounded sample of the workload:
+    consecutive subTrain steps of the sub-GCNs (batch build + fwd/bwd + Adam)."""
+    from oracle import gist_oracle as O
+    o = O.OracleGIST(arch=spec.arch, dims=list(spec.dims), optimizer="adam", clusters_per_batch=spec.q, batch_seed=1)
+    o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
+                 g["cluster_ids"], g["num_clusters"])
+    rng = np.random.default_rng(seed)   # timing only: random weights instead of the (slow) Philox init
+    th = []
+    for l in range(len(spec.dims) - 1):
+        rows = spec.dims[l] * (2 if spec.arch == "sage" else 1)
+        th.append(rng.uniform(-0.05, 0.05, size=(rows, spec.dims[l + 1])))
+    o.set_params(th)
+    o.partition(seed=1, m=spec.m)
+    t0 = time.perf_counter()
+    n = 0
+    while n < max_steps and (n < min_steps or time.perf_counter() - t0 < seconds):
+        o.train_step(n % spec.m, n // spec.m, 0.01)
+        n += 1
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return n / dt, n, dt, cores
+
+
+def run_reference(args, spec, rank, world):
+    if rank != 0:
+        return 0
+    g = generate(GRAPHS[spec.graph], seed=args.seed)
+    # warm-up W steps, then K timed steps; each step = one oracle subTrain step (bounded sample)
+    oracle_steps_per_s(spec, g, seconds=0.0, max_steps=args.warmup, min_steps=args.warmup)
+    v, n, dt, cores = oracle_steps_per_s(spec, g, seconds=0.0, max_steps=args.steps, min_steps=args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(n, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": spec.name, "m": spec.m, "q": spec.q, "dims": list(spec.dims), "arch": spec.arch},
+        "cpu_baseline": {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{n} consecutive sub-GCN subTrain steps of {spec.name} (FP64 numpy/scipy)"},
+        "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GIST
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gist", choices=["gist", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(MODELS))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--zeta", type=int, default=0, help="local iterations per round (0 = paper's zeta, capped)")
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--profile-stride", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    spec = MODELS[args.config]
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, spec, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2102_10424_b200 import gist as G
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    zeta = args.zeta or min(spec.zeta, 100)
+    t_gen = time.perf_counter()
+    g = generate(GRAPHS[spec.graph], seed=args.seed, device=f"cuda:{local}")
+    t_gen = time.perf_counter() - t_gen
+    uid = None
+    if world > 1:
+        obj = [G.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+
+    def make():
+        return G.Gist(spec.arch, spec.dims, optimizer="adam", precision=args.precision, clusters_per_batch=spec.q,
+                      batch_seed=1, rank=rank, world_size=world, device=local, nccl_unique_id=uid)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ------------------------------------------------ device-resident timing (value)
+    gx = make()
+    gx.load_graph(g)
+    gx.init_params(args.seed)
+    stream = torch.cuda.ExternalStream(gx.stream())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+
+    def one_round(t, want_loss=False):
+        gx.partition(seed=1000 + t, m=spec.m)
+        loss = gx.subtrain(zeta, args.lr, want_loss=want_loss)
+        gx.aggregate()
+        return loss
+
+    for t in range(args.warmup):
+        one_round(t)
+    torch.cuda.synchronize()
+    k0 = gx.stat(G.STAT_KERNELS)
+    gx.profile(args.profile_stride)
+    times = []
+    with ClockSampler(local) as clk:
+        for t in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one_round(args.warmup + t)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            times.append(e0.elapsed_time(e1))
+    launches = gx.stat(G.STAT_KERNELS) - k0
+    prof = gx.profile_get()
+    gx.profile(0)
+    nb_last = gx.stat(G.STAT_LAST_NB)
+    nnzb_last = gx.stat(G.STAT_LAST_NNZ_B)
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    steps_total = args.steps * zeta * spec.m          # sub-GCN steps of all ranks
+    value = steps_total / (total_ms / 1e3)
+    B = -(-g["num_clusters"] // spec.q)
+    gx.close()
+    del gx
+
+    # ------------------------------------------------ end-to-end through the public API (e2e)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    ge = make()
+    ge.load_graph(g)                                   # host arrays -> device (timed)
+    ge.init_params(args.seed)
+    for t in range(args.steps):
+        ge.partition(seed=1000 + t, m=spec.m)
+        ge.subtrain(zeta, args.lr, want_loss=True)     # per-round loss read back to host
+        ge.aggregate()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = ge.stat(G.STAT_H2D_BYTES)
+    d2h = ge.stat(G.STAT_D2H_BYTES)
+    ge.close()
+
+    # ------------------------------------------------ roofline of the dominant kernel class
+    pk = peaks()
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    pd = prof[dom]
+    avg_ms = pd["ms"] / max(pd["launches"], 1)
+    work_per = pd["work"] / max(pd["launches"], 1)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.precision}:{dom}")
+    if dom == "gemm":
+        if args.precision == "bf16":
+            roof = {"bound": "tensor", "peak": pk["bf16_sustained"] or pk["bf16"], "unit": "TFLOP/s",
+                    "peak_src": f"{pk['src']} bf16 sustained"}
+        else:
+            # FP32 SIMT: 148 SMs x 128 FP32 lanes x 2 flop x max SM clock
+            roof = {"bound": "alu", "peak": 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12, "unit": "TFLOP/s",
+                    "peak_src": "derived: 148 SM x 128 FFMA lanes x 2 x sm_max_mhz"}
+        achieved = work_per / (avg_ms / 1e3) / 1e12
+    else:
+        roof = {"bound": "hbm", "peak": pk["hbm_gbs"], "unit": "GB/s", "peak_src": f"{pk['src']} hbm copy"}
+        achieved = work_per / (avg_ms / 1e3) / 1e9
+    roof.update({"kernel": dom, "achieved": achieved, "frac": achieved / roof["peak"], "traffic": traffic,
+                 "avg_launch_ms": avg_ms, "work_per_launch": work_per,
+                 "share_of_profiled_ms": pd["ms"] / max(sum(v["ms"] for v in prof.values()), 1e-9)})
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16", "data": "synthetic",
+        "config": {"workload": spec.name, "graph": f"{spec.graph}-shaped planted-cluster synthetic "
+                   f"(n={g['n']}, nnz={int(g['row_ptr'][-1])})", "arch": spec.arch, "dims": list(spec.dims),
+                   "m": spec.m, "q": spec.q, "zeta": zeta, "step": "one GIST round (partition + zeta subTrain "
+                   "steps of all m sub-GCNs + aggregate)", "parallelism": f"gist-m{spec.m}-over-{world}gpu",
+                   "precision": args.precision, "l2": "256 MiB buffer written between timed rounds",
+                   "epoch_s": spec.m * B / value, "batches_per_epoch": B, "last_n_b": nb_last,
+                   "last_nnz_b": nnzb_last, "gen_s": t_gen, "profile_stride": args.profile_stride},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "kernel_profile": {k: {"ms": v["ms"], "launches": v["launches"]} for k, v in prof.items()},
+        "e2e": {"value": steps_total / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d / args.steps,
+                "d2h_bytes_per_step": d2h / args.steps,
+                "includes": "gist_load_graph from host arrays + init + K rounds with per-round loss readback"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, dt, cores = oracle_steps_per_s(spec, g, seconds=args.cpu_seconds, max_steps=64)
+        line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                                "sample": f"{n} consecutive sub-GCN subTrain steps of {spec.name} "
+                                          f"(FP64 numpy/scipy, {dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

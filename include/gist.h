@@ -78,6 +78,10 @@ typedef struct {
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
 void gist_config_default(gist_config* cfg);
 
+/* Writes a fresh 128-byte ncclUniqueId into out128 (rank 0 calls it and broadcasts the
+ * bytes, e.g. over torch.distributed; every rank passes them as cfg->nccl_unique_id). */
+gist_status gist_nccl_unique_id(void* out128);
+
 /* Creates a context on cfg->device.  Errors: GIST_E_ARG (dims), GIST_E_UNSUPPORTED
  * (no CUDA device of compute capability 10.x), GIST_E_NCCL. */
 gist_status gist_create(const gist_config* cfg, gist_ctx** out);
@@ -161,6 +165,20 @@ enum {
   GIST_STAT_MAX_NB = 8
 };
 int64_t gist_stat(gist_ctx* ctx, int32_t which);
+
+/* Live per-kernel-class timing (roofline reporting).  stride > 0: every launch of
+ * every stride-th subTrain step (and every partition / aggregate launch) is
+ * bracketed by CUDA events on the stream it is launched on; stride = 0 turns it
+ * off.  Calling gist_profile resets the counters.  gist_profile_get synchronises
+ * and returns, for one class: total event-timed milliseconds, launches, and the
+ * algorithmic work of those launches (FLOPs for GEMM = 2 M N K; compulsory
+ * bytes for the others: every operand read once, every output written once). */
+enum {
+  GIST_PROF_BATCH = 0, GIST_PROF_SPMM = 1, GIST_PROF_GEMM = 2, GIST_PROF_LOSS = 3, GIST_PROF_OPTIM = 4,
+  GIST_PROF_PARTITION = 5, GIST_PROF_AGGREGATE = 6, GIST_PROF_N = 7
+};
+gist_status gist_profile(gist_ctx* ctx, int32_t stride);
+gist_status gist_profile_get(gist_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* work);
 
 /* cudaStream_t of the context (for timing with CUDA events on the launching stream). */
 void* gist_stream(gist_ctx* ctx);

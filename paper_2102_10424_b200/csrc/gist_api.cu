@@ -42,6 +42,7 @@ struct Slot {
   int cap = 0;
   int32_t *desc_dev = nullptr, *desc_host = nullptr;
   std::vector<int> nb_of_step, q_of_step;
+  std::vector<int64_t> vol_of_step;
   cudaEvent_t desc_ev = nullptr;
   int cached_epoch = -1;
   std::vector<int32_t> epoch_perm;
@@ -81,7 +82,7 @@ struct gist_ctx {
   void* X = nullptr;  // n x pad8(d0), T
   float* full_scale = nullptr;
   std::vector<int32_t> perm_h;  // new id -> original id
-  std::vector<int64_t> cstart_h;
+  std::vector<int64_t> cstart_h, cvol_h;  // cluster offsets (new ids) / cluster volumes (sum of degrees)
   int nb_max = 0;
   int64_t nnzb_max = 0;
   // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
@@ -105,6 +106,21 @@ struct gist_ctx {
   int64_t round = 0, step = 0, adam_t = 0;
   int64_t nk = 0, h2d = 0, d2h = 0;
   std::vector<void*> allocs;
+  // live profiling (gist_profile): event pairs around launches of sampled steps
+  struct ProfRec {
+    int cls;
+    double work, per_nnz;
+    int nnz_slot;  // index into nnz_pin (-1: none)
+    cudaEvent_t a, b;
+  };
+  int prof_stride = 0;
+  bool prof_now = false;
+  std::vector<ProfRec> prof_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t* nnz_pin = nullptr;
+  int nnz_pin_cap = 0, nnz_pin_used = 0;
+  double prof_ms[GIST_PROF_N] = {0}, prof_work[GIST_PROF_N] = {0};
+  int64_t prof_n[GIST_PROF_N] = {0};
 };
 
 // ============================================================== helpers ====
@@ -141,7 +157,15 @@ gist_status fail(gist_ctx* c, gist_status s, const std::string& msg) {
     if ((c)->sticky != GIST_OK) return (c)->sticky;                   \
     cudaSetDevice((c)->cfg.device);                                   \
   } while (0)
-// launch bookkeeping: every kernel launch of the library goes through LK
+// profiled launch: PL(class, algorithmic work, stream, launch-expression)
+#define PL(cls, work, st, expr)                     \
+  do {                                              \
+    int id_ = prof_begin(c, (st), (cls), (work));   \
+    expr;                                           \
+    prof_end(c, (st), id_);                         \
+    ++c->nk;                                        \
+  } while (0)
+// launch bookkeeping: every kernel launch of the library goes through LK or PL
 #define LK(expr)  \
   do {            \
     expr;         \
@@ -177,6 +201,46 @@ gist_status check_launch(gist_ctx* c, const char* where) {
 }
 
 size_t esize(const gist_ctx* c) { return c->prec == GIST_PREC_BF16 ? 2 : 4; }
+
+cudaEvent_t pool_event(gist_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+// opens a profiled launch on stream s (only while c->prof_now)
+int prof_begin(gist_ctx* c, cudaStream_t s, int cls, double work, double per_nnz = 0.0, int nnz_slot = -1) {
+  if (!c->prof_now) return -1;
+  gist_ctx::ProfRec r{cls, work, per_nnz, nnz_slot, pool_event(c), pool_event(c)};
+  cudaEventRecord(r.a, s);
+  c->prof_pending.push_back(r);
+  return (int)c->prof_pending.size() - 1;
+}
+void prof_end(gist_ctx* c, cudaStream_t s, int id) {
+  if (id >= 0) cudaEventRecord(c->prof_pending[id].b, s);
+}
+// synchronises and folds pending records into the per-class totals
+void prof_flush(gist_ctx* c) {
+  if (c->prof_pending.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& r : c->prof_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    double w = r.work;
+    if (r.nnz_slot >= 0) w += r.per_nnz * (double)c->nnz_pin[r.nnz_slot];
+    c->prof_ms[r.cls] += ms;
+    c->prof_work[r.cls] += w;
+    c->prof_n[r.cls] += 1;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->prof_pending.clear();
+  c->nnz_pin_used = 0;
+}
 
 int hidden_block_max(const gist_ctx* c, int l, int m) {
   return (c->dims[l] + m - 1) / m;  // ceil: the largest balanced block (R5)
@@ -232,6 +296,14 @@ extern "C" const char* gist_status_str(gist_status s) {
 }
 
 extern "C" const char* gist_last_error(const gist_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" gist_status gist_nccl_unique_id(void* out128) {
+  if (!out128) return GIST_E_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return GIST_E_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return GIST_OK;
+}
 
 extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (!cfg || !out || !cfg->dims || cfg->num_layers < 1) return GIST_E_ARG;
@@ -309,6 +381,9 @@ extern "C" void gist_destroy(gist_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  for (auto& r : c->prof_pending) c->ev_pool.push_back(r.a), c->ev_pool.push_back(r.b);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->nnz_pin) cudaFreeHost(c->nnz_pin);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -395,6 +470,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   {
     std::vector<int64_t> sz(csize), vol(num_clusters, 0);
     for (int64_t v = 0; v < n; ++v) vol[cluster_ids[v]] += row_ptr[v + 1] - row_ptr[v];
+    c->cvol_h = vol;
     std::sort(sz.rbegin(), sz.rend());
     std::sort(vol.rbegin(), vol.rend());
     int64_t a = 0, b = 0;
@@ -604,6 +680,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
     if (m > c->dims[l]) return fail(c, GIST_E_ARG, "partition: m exceeds hidden dim " + std::to_string(l));
   cudaStream_t s = c->stream;
   if (m != c->alloc_m) TRY(alloc_slots(c, m));
+  c->prof_now = c->prof_stride > 0;
   c->m = m;
   // subGCNs keys / sort / blocks for every hidden dim (R5)
   int dmax = 0;
@@ -640,11 +717,12 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
   CK(cudaMemcpyAsync(c->offs_dev, offs_all.data(), offs_all.size() * 4, cudaMemcpyHostToDevice, s));
   for (int l = 1; l < c->L; ++l) {
     const int d = c->dims[l];
-    LK(partition_keys(d, (uint32_t)c->round, (uint32_t)l, seed, c->keys_a, c->idx_a, s));
-    partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, d, c->sort_tmp, c->sort_tmp_bytes, s);
-    ++c->nk;
-    LK(partition_assign(c->idx_b, d, m, c->blk, s));
-    LK(partition_compact(c->blk, d, m, c->offs_dev + (size_t)l * (m + 1), c->units[l], s));
+    PL(GIST_PROF_PARTITION, d * 12.0, s, partition_keys(d, (uint32_t)c->round, (uint32_t)l, seed, c->keys_a, c->idx_a, s));
+    PL(GIST_PROF_PARTITION, d * 24.0, s,
+       partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, d, c->sort_tmp, c->sort_tmp_bytes, s));
+    PL(GIST_PROF_PARTITION, d * 8.0, s, partition_assign(c->idx_b, d, m, c->blk, s));
+    PL(GIST_PROF_PARTITION, d * 4.0 * (m + 1), s,
+       partition_compact(c->blk, d, m, c->offs_dev + (size_t)l * (m + 1), c->units[l], s));
   }
   // shapes of every slot (all ranks know the full partition)
   c->shapes.assign(m, std::vector<LayerShape>(c->L));
@@ -672,7 +750,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
       mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
       mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
       mp.ldg = c->th_N[l];
-      LK(extract_sub(c->theta[l], mp, sl.W + sh.off, s));
+      PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta[l], mp, sl.W + sh.off, s));
       tot = sh.off + (int64_t)sh.Kp * sh.Np;
     }
     if (sl.M) {
@@ -681,6 +759,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
     }
     if (sl.Wb) LK(f32_to_bf16(sl.W, sl.Wb, tot, s));
   }
+  c->prof_now = false;
   TRY(check_launch(c, "partition"));
   c->adam_t = 0;
   c->state = S_PARTITIONED;
@@ -708,14 +787,29 @@ extern "C" gist_status gist_get_partition(gist_ctx* c, int32_t dim, int32_t* uni
 static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                             const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
                             cudaStream_t s) {
+  const int id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * (double)M * (double)N * (double)K);
   if (c->prec == GIST_PREC_FP32) {
-    LK(gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s));
-    return GIST_OK;
-  }
-  if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s))
+    gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s);
+  } else if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s)) {
     return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
+  }
+  prof_end(c, s, id);
   ++c->nk;
   return GIST_OK;
+}
+
+// compulsory bytes of one SpMM launch excluding the nnz-proportional part
+template <typename T>
+static double spmm_bytes(const SpmmArgs<T>& a) {
+  const double rw = (double)a.rows * (double)a.w * sizeof(T);
+  double b = (double)(a.rows + 1) * 8 + rw /*H*/ + rw /*out*/;
+  if (a.add) b += rw;
+  if (a.mask) b += rw;
+  if (a.self_out) b += rw;
+  if (a.rowscale) b += a.rows * 4.0;
+  if (a.colscale) b += a.rows * 4.0;
+  if (a.h_index) b += a.rows * 4.0;
+  return b;
 }
 
 template <typename T>
@@ -731,13 +825,31 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
   const auto& shp = c->shapes[sl.index];
   const int L = c->L;
   sl.last_nb = nb;
-  // ---- a1: Cluster mini-batch build
-  LK(batch_nodes(bcl, loff, qq, c->cstart, sl.map_cl, sl.b_nodes, nb, s));
-  LK(batch_count(c->rp, c->col, c->cid, sl.map_cl, sl.b_nodes, nb, c->arch, c->labels, c->split, sl.deg_b, sl.scale,
-                 sl.lab_b, sl.train_b, s));
-  LK(batch_scan(sl.deg_b, sl.train_b, nb, sl.b_rp, sl.stats, s));
-  LK(batch_fill(c->rp, c->col, c->cid, sl.map_cl, c->cstart, sl.b_nodes, nb, sl.b_rp, sl.b_col, s));
-  LK(batch_reset(bcl, qq, sl.map_cl, s));
+  c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
+  int nnz_slot = -1;
+  if (c->prof_now && c->nnz_pin_used < c->nnz_pin_cap) nnz_slot = c->nnz_pin_used++;
+  // ---- a1: Cluster mini-batch build (5 launches, one profiled record)
+  {
+    const double vol = (double)sl.vol_of_step[z];
+    int id = -1;
+    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, 2.0 * vol * 8.0 + nb * 40.0, 4.0, nnz_slot);
+    batch_nodes(bcl, loff, qq, c->cstart, sl.map_cl, sl.b_nodes, nb, s);
+    batch_count(c->rp, c->col, c->cid, sl.map_cl, sl.b_nodes, nb, c->arch, c->labels, c->split, sl.deg_b, sl.scale,
+                sl.lab_b, sl.train_b, s);
+    batch_scan(sl.deg_b, sl.train_b, nb, sl.b_rp, sl.stats, s);
+    batch_fill(c->rp, c->col, c->cid, sl.map_cl, c->cstart, sl.b_nodes, nb, sl.b_rp, sl.b_col, s);
+    batch_reset(bcl, qq, sl.map_cl, s);
+    prof_end(c, s, id);
+    c->nk += 5;
+    if (nnz_slot >= 0) CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, sl.stats, 8, cudaMemcpyDeviceToHost, s));
+  }
+  auto spmm_prof = [&](const SpmmArgs<T>& a) {
+    int id = -1;
+    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, spmm_bytes(a), 4.0, nnz_slot);
+    spmm<T>(a, s);
+    prof_end(c, s, id);
+    ++c->nk;
+  };
   const T* Wop = c->prec == GIST_PREC_BF16 ? (const T*)sl.Wb : (const T*)sl.W;
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
@@ -761,7 +873,7 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
       if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
       else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
     }
-    LK(spmm<T>(a, s));
+    spmm_prof(a);
     const T* Wl = Wop + sh.off;
     if (l + 1 < L) {
       const LayerShape& nx = shp[l + 1];
@@ -773,8 +885,14 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
   }
   // ---- a4: softmax cross-entropy
   const LayerShape& last = shp[L - 1];
-  LK(softmax_ce<T>(sl.logits, last.Np, nb, c->k, sl.lab_b, sl.train_b, sl.stats, (T*)sl.dZ[L - 1], sl.row_loss, s));
-  LK(reduce_loss(sl.row_loss, nb, sl.stats, sl.step_loss, sl.loss_acc, s));
+  {
+    const double bytes = (double)nb * last.Np * (4.0 + sizeof(T)) + nb * 9.0 + nb * 4.0;
+    int id = prof_begin(c, s, GIST_PROF_LOSS, bytes);
+    softmax_ce<T>(sl.logits, last.Np, nb, c->k, sl.lab_b, sl.train_b, sl.stats, (T*)sl.dZ[L - 1], sl.row_loss, s);
+    reduce_loss(sl.row_loss, nb, sl.stats, sl.step_loss, sl.loss_acc, s);
+    prof_end(c, s, id);
+    c->nk += 2;
+  }
   // ---- a5/a6: backward
   for (int l = L - 1; l >= 0; --l) {
     const LayerShape& sh = shp[l];
@@ -799,7 +917,7 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
       a.mask = (const T*)sl.H[l]; a.ld_mask = sh.Kp;
       a.w = sh.Kp;
     }
-    LK(spmm<T>(a, s));
+    spmm_prof(a);
   }
   // ---- a7: optimizer
   int64_t tot = last.off + (int64_t)last.Kp * last.Np;
@@ -808,10 +926,12 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
     const double t = (double)(c->adam_t + 1);
     const float bc1 = (float)(1.0 - std::pow((double)c->cfg.beta1, t));
     const float bc2 = (float)(1.0 - std::pow((double)c->cfg.beta2, t));
-    LK(adam_step(sl.W, sl.G, sl.M, sl.V, tot, lr, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, bc1, std::sqrt(bc2), Wb, s));
+    PL(GIST_PROF_OPTIM, (double)tot * (28.0 + (Wb ? 2.0 : 0.0)), s,
+       adam_step(sl.W, sl.G, sl.M, sl.V, tot, lr, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, bc1, std::sqrt(bc2), Wb, s));
   } else {
-    LK(sgd_step(sl.W, sl.G, tot, lr, Wb, s));
+    PL(GIST_PROF_OPTIM, (double)tot * (12.0 + (Wb ? 2.0 : 0.0)), s, sgd_step(sl.W, sl.G, tot, lr, Wb, s));
   }
+  c->prof_now = false;
   return GIST_OK;
 }
 
@@ -833,6 +953,7 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
   }
   sl.nb_of_step.assign(iters, 0);
   sl.q_of_step.assign(iters, 0);
+  sl.vol_of_step.assign(iters, 0);
   const int64_t B = (c->c + q - 1) / q;
   for (int z = 0; z < iters; ++z) {
     const int64_t st = c->step + z;
@@ -851,6 +972,7 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
         d[k] = cl;
         d[q + k] = off;
         off += (int32_t)(c->cstart_h[cl + 1] - c->cstart_h[cl]);
+        sl.vol_of_step[z] += c->cvol_h[cl];
       } else {  // last batch of an epoch may hold fewer clusters: empty ranges
         d[k] = d[qq - 1];
         d[q + k] = off;
@@ -893,6 +1015,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
   }
   c->step += local_iters;
   TRY(check_launch(c, "subtrain"));
+  if (c->prof_stride > 0) prof_flush(c);
   if (mean_loss) {
     std::fill(mean_loss, mean_loss + c->m, 0.f);
     for (Slot& sl : c->slots) {
@@ -913,8 +1036,11 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   cudaStream_t s = c->stream;
   const int W = c->cfg.world_size;
   const float* src = c->Wall;
+  c->prof_now = c->prof_stride > 0;
   if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
+    const int id = prof_begin(c, s, GIST_PROF_AGGREGATE, (double)W * c->slots_per_rank * c->S_max * 4.0);
     NK(ncclAllGather(c->Wall, c->Wrecv, (size_t)c->slots_per_rank * c->S_max, ncclFloat, c->comm, s));
+    prof_end(c, s, id);
     src = c->Wrecv;
   }
   for (int i = 0; i < c->m; ++i) {
@@ -927,9 +1053,10 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
       mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
       mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
       mp.ldg = c->th_N[l];
-      LK(scatter_sub(c->theta[l], mp, w + sh.off, s));
+      PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 12.0, s, scatter_sub(c->theta[l], mp, w + sh.off, s));
     }
   }
+  c->prof_now = false;
   TRY(check_launch(c, "aggregate"));
   c->round += 1;
   c->state = S_PARAMS;
@@ -1114,6 +1241,30 @@ extern "C" gist_status gist_get_trace(gist_ctx* c, int32_t slot, int32_t what, i
       return GIST_E_ARG;
   }
   if (count) *count = cnt;
+  return GIST_OK;
+}
+
+// ============================================================ profiling ===
+extern "C" gist_status gist_profile(gist_ctx* c, int32_t stride) {
+  PRE(c);
+  if (stride < 0) return GIST_E_ARG;
+  prof_flush(c);
+  c->prof_stride = stride;
+  for (int k = 0; k < GIST_PROF_N; ++k) c->prof_ms[k] = c->prof_work[k] = 0.0, c->prof_n[k] = 0;
+  if (stride > 0 && !c->nnz_pin) {
+    c->nnz_pin_cap = 1 << 16;
+    CK(cudaMallocHost(&c->nnz_pin, (size_t)c->nnz_pin_cap * 8));
+  }
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_profile_get(gist_ctx* c, int32_t cls, double* ms, int64_t* launches, double* work) {
+  PRE(c);
+  if (cls < 0 || cls >= GIST_PROF_N) return GIST_E_ARG;
+  prof_flush(c);
+  if (ms) *ms = c->prof_ms[cls];
+  if (launches) *launches = c->prof_n[cls];
+  if (work) *work = c->prof_work[cls];
   return GIST_OK;
 }
 

@@ -27,7 +27,9 @@ EXPORTS = [
     "gist_subtrain", "gist_aggregate", "gist_eval", "gist_get_params", "gist_set_params",
     "gist_get_partition", "gist_sub_shape", "gist_get_sub_params", "gist_get_trace", "gist_stat",
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
+    "gist_profile", "gist_profile_get", "gist_nccl_unique_id",
 ]
+PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate"]
 
 
 class GistConfig(C.Structure):
@@ -75,6 +77,9 @@ def lib() -> C.CDLL:
         "gist_destroy": (None, [vp]),
         "gist_spmm": (i32, [vp, vp, i64, vp, vp, i32, vp, vp, i64, i64, i32, vp]),
         "gist_gemm": (i32, [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, vp]),
+        "gist_profile": (i32, [vp, i32]),
+        "gist_nccl_unique_id": (i32, [vp]),
+        "gist_profile_get": (i32, [vp, i32, P(C.c_double), P(i64), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -218,6 +223,25 @@ class Gist:
 
     def stream(self) -> int:
         return lib().gist_stream(self.h)
+
+    def profile(self, stride: int):
+        self._check(lib().gist_profile(self.h, stride))
+
+    def profile_get(self) -> dict:
+        out = {}
+        for k, name in enumerate(PROF_CLASSES):
+            ms, n, w = C.c_double(), C.c_int64(), C.c_double()
+            self._check(lib().gist_profile_get(self.h, k, C.byref(ms), C.byref(n), C.byref(w)))
+            out[name] = {"ms": ms.value, "launches": n.value, "work": w.value}
+        return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().gist_nccl_unique_id(buf)
+    if st != 0:
+        raise GistError(f"gist_nccl_unique_id: {lib().gist_status_str(st).decode()}")
+    return buf.raw
 
 
 def spmm(row_ptr_dev: int, col_dev: int, rows: int, rowscale_dev: int | None, colscale_dev: int | None,
