@@ -1,0 +1,96 @@
+"""BF16 tensor-core mode (tcgen05 GEMMs, bf16 activations, fp32 accumulation/master
+weights/optimizer).  Gates (north_star): relative error <= 2e-2 against the FP64
+oracle; loss curve within 1% of the oracle's over 10 rounds.  The GEMM kernel itself
+is checked against an FP64 product of the same bf16-rounded operands (only fp32
+accumulation-order error remains)."""
+import numpy as np
+import pytest
+
+from synth.planted import generate, tiny_spec, GRAPHS
+from tests.gpu_helpers import align, make_pair, rel_err
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 2e-2
+
+
+def bf16_round(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (517, 131, 263), (3106, 512, 1216), (300, 48, 1024),
+                                   (1216, 512, 3106), (3106, 4096, 1024), (70, 8, 40)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+@pytest.mark.parametrize("out_f32,relu", [(True, False), (False, True)])
+def test_tc_gemm_layouts(M, N, K, ta, tb, out_f32, relu):
+    import torch
+    from paper_2102_10424_b200 import gist
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    pad = lambda x: (x + 7) // 8 * 8
+    a_shape = (K, pad(M)) if ta else (M, pad(K))
+    b_shape = (N, pad(K)) if tb else (K, pad(N))
+    a = bf16_round(rng.standard_normal(a_shape))
+    b = bf16_round(rng.standard_normal(b_shape))
+    dev = torch.device("cuda")
+    ad = torch.from_numpy(a).to(dev).to(torch.bfloat16)
+    bd = torch.from_numpy(b).to(dev).to(torch.bfloat16)
+    ldc = pad(N)
+    c = torch.zeros((M, ldc), dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+    gist.gemm(bool(ta), bool(tb), M, N, K, ad.data_ptr(), a_shape[1], bd.data_ptr(), b_shape[1],
+              c.data_ptr(), ldc, 1, out_f32=out_f32, relu=relu)
+    torch.cuda.synchronize()
+    A = (a[:, :M].T if ta else a[:, :K]).astype(np.float64)
+    B = (b[:, :K].T if tb else b[:, :N]).astype(np.float64)
+    ref = A @ B
+    if relu:
+        ref = np.maximum(ref, 0)
+    got = c.float().cpu().numpy()[:, :N]
+    tol = 1e-5 if out_f32 else 8e-3          # bf16 output rounding: 2^-8 relative
+    assert rel_err(got, ref) <= tol, rel_err(got, ref)
+    assert np.all(c.float().cpu().numpy()[:, N:] == 0)   # never writes past N
+
+
+CASES = [
+    ("gcn-ragged", dict(n=700, nnz=6000, d0=37, classes=5, clusters=14), "gcn", (37, 45, 29, 5), 3),
+    ("sage-ragged", dict(n=650, nnz=5000, d0=23, classes=7, clusters=13), "sage", (23, 40, 33, 7), 4),
+    ("sage-wide", dict(n=900, nnz=20000, d0=130, classes=11, clusters=9), "sage", (130, 300, 11), 2),
+]
+
+
+@pytest.mark.parametrize("name,kw,arch,dims,q", CASES)
+def test_bf16_one_step(name, kw, arch, dims, q):
+    g = generate(tiny_spec(**kw), seed=0)
+    gpu, ora = make_pair(g, arch, dims, optimizer="adam", q=q, precision="bf16")
+    gpu.partition(seed=99, m=2)
+    ora.partition(seed=99, m=2)
+    gpu.subtrain(1, lr=0.01)
+    for i in range(2):
+        ora.train_step(i, 0, 0.01)
+        tr = ora.last_trace[i]
+        nodes = gpu.trace(i, 0)
+        p = align(nodes, tr["nodes"])
+        nb = len(nodes)
+        assert rel_err(gpu.trace(i, 2).reshape(nb, -1), tr["tape"]["logits"][p]) <= BF16_TOL
+        for l in range(1, len(dims) - 1):
+            assert rel_err(gpu.trace(i, 1, l).reshape(nb, -1), tr["tape"]["H"][l][p]) <= BF16_TOL
+        for l in range(len(dims) - 1):
+            assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= BF16_TOL, l
+
+
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 0.5), ("adam", 0.01)])
+def test_bf16_loss_curve_C1_10_rounds(optimizer, lr):
+    """north_star: BF16 mode loss curve within 1% after 10 rounds (C1 = Cora-shaped, m=2,
+    10 local iterations).  Metric: max_t |l_gpu(t) - l_oracle(t)| / max_t l_oracle(t)."""
+    g = generate(GRAPHS["cora"], seed=0)
+    gpu, ora = make_pair(g, "gcn", (1433, 256, 7), optimizer=optimizer, q=1, precision="bf16")
+    lg, lo = [], []
+    for t in range(10):
+        gpu.partition(seed=11, m=2)
+        ora.partition(seed=11, m=2)
+        lg.append(float(np.mean(gpu.subtrain(10, lr=lr))))
+        lo.append(float(np.mean(ora.subtrain(10, lr=lr))))
+        gpu.aggregate()
+        ora.aggregate()
+    err = max(abs(a - b) for a, b in zip(lg, lo)) / max(lo)
+    print(f"bf16 C1 {optimizer} loss curve gpu={lg} oracle={lo} err={err:.3e}")
+    assert err <= 1e-2, (err, lg, lo)
