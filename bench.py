@@ -159,7 +159,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gist", choices=["gist", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(MODELS))
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--zeta", type=int, default=0, help="local iterations per round (0 = paper's zeta, capped)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--seed", type=int, default=0)
@@ -179,7 +179,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    zeta = args.zeta or min(spec.zeta, 100)
+    zeta = args.zeta or spec.zeta
     t_gen = time.perf_counter()
     g = generate(GRAPHS[spec.graph], seed=args.seed, device=f"cuda:{local}")
     t_gen = time.perf_counter() - t_gen

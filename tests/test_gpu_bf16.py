@@ -77,7 +77,7 @@ def test_bf16_one_step(name, kw, arch, dims, q):
             assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= BF16_TOL, l
 
 
-@pytest.mark.parametrize("optimizer,lr", [("sgd", 0.5), ("adam", 0.01)])
+@pytest.mark.parametrize("optimizer,lr", [("sgd", 0.1), ("adam", 0.001)])  # well-conditioned trajectories
 def test_bf16_loss_curve_C1_10_rounds(optimizer, lr):
     """north_star: BF16 mode loss curve within 1% after 10 rounds (C1 = Cora-shaped, m=2,
     10 local iterations).  Metric: max_t |l_gpu(t) - l_oracle(t)| / max_t l_oracle(t)."""
