@@ -47,10 +47,12 @@ struct Slot {
   int cached_epoch = -1;
   std::vector<int32_t> epoch_perm;
   // batch buffers
-  int32_t *b_nodes = nullptr, *deg_b = nullptr, *lab_b = nullptr, *b_col = nullptr, *map_cl = nullptr;
+  int32_t *b_nodes = nullptr, *lab_b = nullptr, *b_col = nullptr;
+  uint64_t* map64 = nullptr;  // cluster -> (step tag, local-id delta)
+  uint32_t tag = 0;
   uint8_t* train_b = nullptr;
   float* scale = nullptr;
-  int64_t *b_rp = nullptr, *stats = nullptr;
+  int64_t *b_beg = nullptr, *b_end = nullptr, *stats = nullptr;
   // activations (element type T of the precision mode)
   std::vector<void*> C, H, dZ;
   void* dC = nullptr;
@@ -645,15 +647,15 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     }
     if (c->prec == GIST_PREC_BF16) TRY(dalloc_t(c, &s.Wb, smax));
     TRY(dalloc_t(c, &s.b_nodes, nbm));
-    TRY(dalloc_t(c, &s.deg_b, nbm));
     TRY(dalloc_t(c, &s.lab_b, nbm));
     TRY(dalloc_t(c, &s.train_b, nbm));
     TRY(dalloc_t(c, &s.scale, nbm));
-    TRY(dalloc_t(c, &s.b_rp, nbm + 1));
+    TRY(dalloc_t(c, &s.b_beg, nbm));
+    TRY(dalloc_t(c, &s.b_end, nbm));
     TRY(dalloc_t(c, &s.stats, 2));
     TRY(dalloc_t(c, &s.b_col, std::max<int64_t>(c->nnzb_max, 1)));
-    TRY(dalloc_t(c, &s.map_cl, c->c));
-    CK(cudaMemsetAsync(s.map_cl, 0xff, (size_t)c->c * 4, c->stream));  // -1
+    TRY(dalloc_t(c, &s.map64, c->c));
+    CK(cudaMemsetAsync(s.map64, 0, (size_t)c->c * 8, c->stream));  // tag 0 = never in a batch
     s.C.assign(c->L, nullptr);
     s.H.assign(c->L, nullptr);
     s.dZ.assign(c->L, nullptr);
@@ -800,7 +802,7 @@ static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N,
 
 // compulsory bytes of one SpMM launch excluding the nnz-proportional part
 template <typename T>
-static double spmm_bytes(const SpmmArgs<T>& a) {
+static double spmm_bytes(const SpmmArgs<T, T>& a) {
   const double rw = (double)a.rows * (double)a.w * sizeof(T);
   double b = (double)(a.rows + 1) * 8 + rw /*H*/ + rw /*out*/;
   if (a.add) b += rw;
@@ -818,9 +820,11 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
   const int q = c->cfg.clusters_per_batch;
   const int nb = sl.nb_of_step[z];
   const int qq = sl.q_of_step[z];  // clusters in this batch (< q only for an epoch's last batch)
-  const int32_t* d = sl.desc_dev + (size_t)z * (2 * q + 2);
+  const int32_t* d = sl.desc_dev + (size_t)z * (3 * q + 3);
   const int32_t* bcl = d;
   const int32_t* loff = d + q;
+  const int32_t* voff = d + 2 * q + 1;
+  const uint32_t tag = ++sl.tag;
   const bool sage = c->arch == GIST_ARCH_SAGE;
   const auto& shp = c->shapes[sl.index];
   const int L = c->L;
@@ -828,25 +832,22 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
   c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
   int nnz_slot = -1;
   if (c->prof_now && c->nnz_pin_used < c->nnz_pin_cap) nnz_slot = c->nnz_pin_used++;
-  // ---- a1: Cluster mini-batch build (5 launches, one profiled record)
+  // ---- a1: Cluster mini-batch build (2 launches, one profiled record)
   {
     const double vol = (double)sl.vol_of_step[z];
     int id = -1;
-    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, 2.0 * vol * 8.0 + nb * 40.0, 4.0, nnz_slot);
-    batch_nodes(bcl, loff, qq, c->cstart, sl.map_cl, sl.b_nodes, nb, s);
-    batch_count(c->rp, c->col, c->cid, sl.map_cl, sl.b_nodes, nb, c->arch, c->labels, c->split, sl.deg_b, sl.scale,
-                sl.lab_b, sl.train_b, s);
-    batch_scan(sl.deg_b, sl.train_b, nb, sl.b_rp, sl.stats, s);
-    batch_fill(c->rp, c->col, c->cid, sl.map_cl, c->cstart, sl.b_nodes, nb, sl.b_rp, sl.b_col, s);
-    batch_reset(bcl, qq, sl.map_cl, s);
+    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + nb * 45.0, 4.0, nnz_slot);
+    batch_setup(bcl, loff, voff, qq, c->cstart, c->rp, tag, sl.map64, sl.b_nodes, sl.b_beg, nb, sl.stats, s);
+    batch_build(c->rp, c->col, c->cid, sl.map64, tag, sl.b_nodes, sl.b_beg, nb, c->arch, c->labels, c->split,
+                sl.b_end, sl.b_col, sl.scale, sl.lab_b, sl.train_b, sl.stats, s);
     prof_end(c, s, id);
-    c->nk += 5;
+    c->nk += 2;
     if (nnz_slot >= 0) CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, sl.stats, 8, cudaMemcpyDeviceToHost, s));
   }
-  auto spmm_prof = [&](const SpmmArgs<T>& a) {
+  auto spmm_prof = [&](const SpmmArgs<T, T>& a) {
     int id = -1;
     if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, spmm_bytes(a), 4.0, nnz_slot);
-    spmm<T>(a, s);
+    spmm<T, T>(a, s);
     prof_end(c, s, id);
     ++c->nk;
   };
@@ -855,8 +856,8 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
   for (int l = 0; l < L; ++l) {
     const LayerShape& sh = shp[l];
     T* C = (T*)sl.C[l];
-    SpmmArgs<T> a;
-    a.row_ptr = sl.b_rp; a.col = sl.b_col; a.rows = nb;
+    SpmmArgs<T, T> a;
+    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
     if (sage) {
       a.rowscale = sl.scale;              // N = D^-1 A (R2)
       a.out = C + sh.half; a.ldo = sh.Kp;  // right half: N H
@@ -903,8 +904,8 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
     if (l == 0) break;
     // dC_l = dZ_l W_l^T
     TRY(gemm_any(c, false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false, s));
-    SpmmArgs<T> a;
-    a.row_ptr = sl.b_rp; a.col = sl.b_col; a.rows = nb;
+    SpmmArgs<T, T> a;
+    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
     a.out = (T*)sl.dZ[l - 1]; a.ldo = shp[l - 1].Np;
     if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
       a.colscale = sl.scale; a.H = (const T*)sl.dC + sh.half; a.ldh = sh.Kp;
@@ -938,7 +939,7 @@ static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
 // host side of R7 for a whole subtrain call: cluster lists, local offsets, n_b per step
 static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
   const int q = c->cfg.clusters_per_batch;
-  const int per = 2 * q + 2;
+  const int per = 3 * q + 3;
   if (iters > sl.cap) {
     if (sl.desc_host) {
       CK(cudaEventSynchronize(sl.desc_ev));
@@ -966,20 +967,26 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
     const int64_t lo = p * q, hi = std::min<int64_t>((p + 1) * q, c->c);
     const int qq = (int)(hi - lo);
     int32_t off = 0;
+    int64_t voff = 0;
+    int32_t* dv = d + 2 * q + 1;
     for (int k = 0; k < q; ++k) {
       if (k < qq) {
         const int32_t cl = sl.epoch_perm[lo + k];
         d[k] = cl;
         d[q + k] = off;
+        dv[k] = (int32_t)voff;
         off += (int32_t)(c->cstart_h[cl + 1] - c->cstart_h[cl]);
-        sl.vol_of_step[z] += c->cvol_h[cl];
+        voff += c->cvol_h[cl];
       } else {  // last batch of an epoch may hold fewer clusters: empty ranges
         d[k] = d[qq - 1];
         d[q + k] = off;
+        dv[k] = (int32_t)voff;
       }
     }
     d[2 * q] = off;
-    d[2 * q + 1] = qq;
+    dv[q] = (int32_t)voff;
+    d[3 * q + 2] = qq;
+    sl.vol_of_step[z] = voff;
     sl.nb_of_step[z] = off;
     sl.q_of_step[z] = qq;
   }
@@ -1083,8 +1090,8 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
   for (int l = 0; l < c->L; ++l) {
     const int64_t K = c->th_K[l], N = c->th_N[l];
     const int64_t half = pad8(c->dims[l]);
-    SpmmArgs<T> a;
-    a.row_ptr = c->rp; a.col = c->col; a.rows = n; a.rowscale = c->full_scale;
+    SpmmArgs<T, T> a;
+    a.row_beg = c->rp; a.row_end = c->rp + 1; a.col = c->col; a.rows = n; a.rowscale = c->full_scale;
     const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
     if (sage) {
       if (l == 0) { a.self_out = Cb; a.ld_self = K; }
@@ -1093,7 +1100,7 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
     } else {
       a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
     }
-    LK(spmm<T>(a, s));
+    LK((spmm<T, T>(a, s)));
     const void* Wl = c->theta[l];
     if (sizeof(T) == 2) {
       if (wtmp) dfree(c, wtmp);
@@ -1275,15 +1282,15 @@ extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_
   if (!row_ptr_dev || !H_dev || !out_dev || w < 0 || ld < w || (ld % 8) != 0) return GIST_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == 0) {
-    SpmmArgs<float> a;
-    a.row_ptr = row_ptr_dev; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
+    SpmmArgs<float, float> a;
+    a.row_beg = row_ptr_dev; a.row_end = row_ptr_dev + 1; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
     a.self = self; a.H = (const float*)H_dev; a.ldh = ld; a.out = (float*)out_dev; a.ldo = ld; a.w = pad8(w);
-    spmm<float>(a, s);
+    spmm<float, float>(a, s);
   } else if (dtype == 1) {
-    SpmmArgs<bf16> a;
-    a.row_ptr = row_ptr_dev; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
+    SpmmArgs<bf16, bf16> a;
+    a.row_beg = row_ptr_dev; a.row_end = row_ptr_dev + 1; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
     a.self = self; a.H = (const bf16*)H_dev; a.ldh = ld; a.out = (bf16*)out_dev; a.ldo = ld; a.w = pad8(w);
-    spmm<bf16>(a, s);
+    spmm<bf16, bf16>(a, s);
   } else {
     return GIST_E_ARG;
   }

@@ -3,10 +3,12 @@
 //
 // On load, nodes are relabelled so that every cluster is a contiguous id range
 // (new id = position in the cluster-sorted order).  A mini-batch is then the
-// union of q clusters = q id ranges; batch row v maps to new id b_nodes[v] and
-// a neighbour u is inside the batch iff map_cl[cid[u]] >= 0, with local id
-// map_cl[cid[u]] + (u - cstart[cid[u]]).  No n-sized scratch map has to be
-// cleared per step: only the q entries of map_cl are set and reset.
+// union of q clusters = q id ranges; batch row v maps to new id b_nodes[v], and a
+// neighbour u is inside the batch iff map64[cid[u]] carries this step's tag, with
+// local id u + delta(cid[u]).  Nothing is cleared between steps (the tag changes).
+// The batch adjacency is written into per-row segments b_col[b_beg[v], b_end[v])
+// sized by the global degree (segment starts are known before the pass), so the
+// build is a single pass with no scan.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -95,127 +97,101 @@ void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cud
 }
 
 // ------------------------------------------------------------ batch build --
-__global__ void k_batch_nodes(const int32_t* __restrict__ bcl, const int32_t* __restrict__ loff, int q,
-                              const int64_t* __restrict__ cstart, int32_t* __restrict__ map_cl,
-                              int32_t* __restrict__ b_nodes, int nb) {
+__global__ void k_batch_setup(const int32_t* __restrict__ bcl, const int32_t* __restrict__ loff,
+                              const int32_t* __restrict__ voff, int q, const int64_t* __restrict__ cstart,
+                              const int64_t* __restrict__ rp, uint32_t tag, uint64_t* __restrict__ map64,
+                              int32_t* __restrict__ b_nodes, int64_t* __restrict__ b_beg, int nb,
+                              int64_t* __restrict__ stats) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < q) map_cl[bcl[v]] = loff[v];
+  if (v < q) {
+    const int32_t c = bcl[v];
+    map64[c] = ((uint64_t)tag << 32) | (uint32_t)(loff[v] - (int32_t)cstart[c]);
+  }
+  if (v == 0) stats[0] = stats[1] = 0;
   if (v >= nb) return;
   int lo = 0, hi = q - 1;  // largest k with loff[k] <= v
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (loff[mid] <= v) lo = mid; else hi = mid - 1;
   }
-  b_nodes[v] = (int32_t)(cstart[bcl[lo]] + (v - loff[lo]));
+  const int32_t c = bcl[lo];
+  const int64_t g = cstart[c] + (v - loff[lo]);
+  b_nodes[v] = (int32_t)g;
+  b_beg[v] = voff[lo] + (rp[g] - rp[cstart[c]]);  // row v's segment inside the batch's adjacency space
 }
-void batch_nodes(const int32_t* bcl, const int32_t* loff, int q, const int64_t* cstart, int32_t* map_cl,
-                 int32_t* b_nodes, int nb, cudaStream_t s) {
+void batch_setup(const int32_t* bcl, const int32_t* loff, const int32_t* voff, int q, const int64_t* cstart,
+                 const int64_t* rp, uint32_t tag, uint64_t* map64, int32_t* b_nodes, int64_t* b_beg, int nb,
+                 int64_t* stats, cudaStream_t s) {
   const int n = nb > q ? nb : q;
-  k_batch_nodes<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(bcl, loff, q, cstart, map_cl, b_nodes, nb);
+  k_batch_setup<<<(unsigned)cdiv(n > 0 ? n : 1, 256), 256, 0, s>>>(bcl, loff, voff, q, cstart, rp, tag, map64,
+                                                                    b_nodes, b_beg, nb, stats);
 }
 
-__global__ void k_batch_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                              const int32_t* __restrict__ cid, const int32_t* __restrict__ map_cl,
-                              const int32_t* __restrict__ b_nodes, int nb, int arch,
-                              const int32_t* __restrict__ labels, const uint8_t* __restrict__ split,
-                              int32_t* __restrict__ deg_b, float* __restrict__ scale, int32_t* __restrict__ lab_b,
-                              uint8_t* __restrict__ train_b) {
-  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (v >= nb) return;
-  const int64_t g = b_nodes[v];
-  int cnt = 0;
-  for (int64_t e = rp[g] + lane; e < rp[g + 1]; e += 32) cnt += map_cl[cid[col[e]]] >= 0;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) {
-    deg_b[v] = cnt;
-    const float d = (float)cnt;
-    scale[v] = arch == 0 ? 1.0f / sqrtf(d + 1.0f) : (cnt > 0 ? 1.0f / d : 0.f);
-    lab_b[v] = labels[g];
-    train_b[v] = split[g] == 0;
-  }
-}
-void batch_count(const int64_t* rp, const int32_t* col, const int32_t* cid, const int32_t* map_cl,
-                 const int32_t* b_nodes, int nb, int arch, const int32_t* labels, const uint8_t* split,
-                 int32_t* deg_b, float* scale, int32_t* lab_b, uint8_t* train_b, cudaStream_t s) {
-  if (nb <= 0) return;
-  k_batch_count<<<(unsigned)cdiv(nb, 8), 256, 0, s>>>(rp, col, cid, map_cl, b_nodes, nb, arch, labels, split, deg_b,
-                                                       scale, lab_b, train_b);
-}
-
-// single-CTA deterministic scan of the batch degrees + count of train rows
-__global__ void __launch_bounds__(1024) k_batch_scan(const int32_t* __restrict__ deg_b,
-                                                     const uint8_t* __restrict__ train_b, int nb,
-                                                     int64_t* __restrict__ b_rp, int64_t* __restrict__ stats) {
-  using Scan = cub::BlockScan<int64_t, 1024>;
-  using Red = cub::BlockReduce<int64_t, 1024>;
-  __shared__ typename Scan::TempStorage ts;
-  __shared__ typename Red::TempStorage tr;
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  int64_t ntrain = 0;
-  for (int base = 0; base < nb; base += 1024) {
-    const int v = base + threadIdx.x;
-    const int64_t d = v < nb ? deg_b[v] : 0;
-    if (v < nb) ntrain += train_b[v];
-    int64_t excl, tot;
-    Scan(ts).ExclusiveSum(d, excl, tot);
-    if (v < nb) b_rp[v] = carry + excl;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  const int64_t nt = Red(tr).Sum(ntrain);
-  if (threadIdx.x == 0) {
-    b_rp[nb] = carry;
-    stats[0] = carry;
-    stats[1] = nt;
-  }
-}
-void batch_scan(const int32_t* deg_b, const uint8_t* train_b, int nb, int64_t* b_rp, int64_t* stats,
-                cudaStream_t s) {
-  k_batch_scan<<<1, 1024, 0, s>>>(deg_b, train_b, nb, b_rp, stats);
-}
-
-__global__ void k_batch_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ cid, const int32_t* __restrict__ map_cl,
-                             const int64_t* __restrict__ cstart, const int32_t* __restrict__ b_nodes, int nb,
-                             const int64_t* __restrict__ b_rp, int32_t* __restrict__ b_col) {
-  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (v >= nb) return;
-  const int64_t g = b_nodes[v];
-  int64_t out = b_rp[v];
-  const int64_t end = rp[g + 1];
-  for (int64_t base = rp[g]; base < end; base += 32) {
-    const int64_t e = base + lane;
-    int32_t loc = -1;
-    if (e < end) {
-      const int32_t u = col[e];
-      const int32_t c = cid[u];
-      const int32_t lo = map_cl[c];
-      if (lo >= 0) loc = lo + (int32_t)(u - cstart[c]);
+// One warp per batch row: walk the row's global adjacency 64 entries per iteration
+// (two independent load chains col -> cid -> map64 in flight), keep the in-batch
+// neighbours (ballot compaction, original order), and write the row's normalisation
+// scale, label and train flag.  Counters are warp -> block reduced, one integer atomic
+// per block (integer addition: deterministic).
+__global__ void __launch_bounds__(256) k_batch_build(
+    const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const int32_t* __restrict__ cid,
+    const uint64_t* __restrict__ map64, uint32_t tag, const int32_t* __restrict__ b_nodes,
+    const int64_t* __restrict__ b_beg, int nb, int arch, const int32_t* __restrict__ labels,
+    const uint8_t* __restrict__ split, int64_t* __restrict__ b_end, int32_t* __restrict__ b_col,
+    float* __restrict__ scale, int32_t* __restrict__ lab_b, uint8_t* __restrict__ train_b,
+    int64_t* __restrict__ stats) {
+  __shared__ int s_cnt[8], s_tr[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int v = blockIdx.x * 8 + w;
+  int cnt = 0, tr = 0;
+  if (v < nb) {
+    const int64_t g = b_nodes[v];
+    const int64_t end = rp[g + 1];
+    const int64_t out0 = b_beg[v];
+    int64_t out = out0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = rp[g]; base < end; base += 64) {
+      const int64_t e0 = base + lane, e1 = base + 32 + lane;
+      const int32_t u0 = e0 < end ? col[e0] : -1;
+      const int32_t u1 = e1 < end ? col[e1] : -1;
+      const int32_t c0 = u0 >= 0 ? cid[u0] : 0;
+      const int32_t c1 = u1 >= 0 ? cid[u1] : 0;
+      const uint64_t m0 = u0 >= 0 ? map64[c0] : 0ull;
+      const uint64_t m1 = u1 >= 0 ? map64[c1] : 0ull;
+      const bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
+      const bool in1 = u1 >= 0 && (uint32_t)(m1 >> 32) == tag;
+      const unsigned b0 = __ballot_sync(0xffffffffu, in0);
+      const unsigned b1 = __ballot_sync(0xffffffffu, in1);
+      if (in0) b_col[out + __popc(b0 & lt)] = u0 + (int32_t)(uint32_t)m0;
+      out += __popc(b0);
+      if (in1) b_col[out + __popc(b1 & lt)] = u1 + (int32_t)(uint32_t)m1;
+      out += __popc(b1);
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, loc >= 0);
-    if (loc >= 0) b_col[out + __popc(bal & ((1u << lane) - 1))] = loc;
-    out += __popc(bal);
+    cnt = (int)(out - out0);
+    if (lane == 0) {
+      b_end[v] = out;
+      const float d = (float)cnt;
+      scale[v] = arch == 0 ? 1.0f / sqrtf(d + 1.0f) : (cnt > 0 ? 1.0f / d : 0.f);
+      lab_b[v] = labels[g];
+      tr = split[g] == 0;
+      train_b[v] = (uint8_t)tr;
+    }
+  }
+  if (lane == 0) { s_cnt[w] = cnt; s_tr[w] = tr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long a = 0, b = 0;
+    for (int k = 0; k < 8; ++k) a += s_cnt[k], b += s_tr[k];
+    if (a) atomicAdd((unsigned long long*)&stats[0], (unsigned long long)a);
+    if (b) atomicAdd((unsigned long long*)&stats[1], (unsigned long long)b);
   }
 }
-void batch_fill(const int64_t* rp, const int32_t* col, const int32_t* cid, const int32_t* map_cl,
-                const int64_t* cstart, const int32_t* b_nodes, int nb, const int64_t* b_rp, int32_t* b_col,
-                cudaStream_t s) {
+void batch_build(const int64_t* rp, const int32_t* col, const int32_t* cid, const uint64_t* map64, uint32_t tag,
+                 const int32_t* b_nodes, const int64_t* b_beg, int nb, int arch, const int32_t* labels,
+                 const uint8_t* split, int64_t* b_end, int32_t* b_col, float* scale, int32_t* lab_b,
+                 uint8_t* train_b, int64_t* stats, cudaStream_t s) {
   if (nb <= 0) return;
-  k_batch_fill<<<(unsigned)cdiv(nb, 8), 256, 0, s>>>(rp, col, cid, map_cl, cstart, b_nodes, nb, b_rp, b_col);
-}
-
-__global__ void k_batch_reset(const int32_t* __restrict__ bcl, int q, int32_t* __restrict__ map_cl) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < q) map_cl[bcl[k]] = -1;
-}
-void batch_reset(const int32_t* bcl, int q, int32_t* map_cl, cudaStream_t s) {
-  k_batch_reset<<<(unsigned)cdiv(q, 256), 256, 0, s>>>(bcl, q, map_cl);
+  k_batch_build<<<(unsigned)cdiv(nb, 8), 256, 0, s>>>(rp, col, cid, map64, tag, b_nodes, b_beg, nb, arch, labels,
+                                                       split, b_end, b_col, scale, lab_b, train_b, stats);
 }
 
 }  // namespace gist

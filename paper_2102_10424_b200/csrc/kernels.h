@@ -15,28 +15,30 @@ using bf16 = __nv_bfloat16;
 // where h(u) = h_index ? h_index[u] : u.  Optionally copies H[h(v)] to self_out[v]
 // (GraphSAGE concat [H || N H], R2).  Widths are padded to multiples of 8.
 // --------------------------------------------------------------------------
-template <typename T>
+template <typename TI, typename TO = TI>
 struct SpmmArgs {
-  const int64_t* row_ptr = nullptr;
+  const int64_t* row_beg = nullptr;  // row v's neighbours are col[row_beg[v] .. row_end[v])
+  const int64_t* row_end = nullptr;  // (plain CSR: row_end = row_ptr + 1)
   const int32_t* col = nullptr;
   int64_t rows = 0;
   const float* rowscale = nullptr;
   const float* colscale = nullptr;
   int self = 0;
+  int relu = 0;
   const int32_t* h_index = nullptr;
-  const T* H = nullptr;
+  const TI* H = nullptr;
   int64_t ldh = 0;
-  const T* add = nullptr;
+  const TI* add = nullptr;
   int64_t ld_add = 0;
-  const T* mask = nullptr;
+  const TI* mask = nullptr;
   int64_t ld_mask = 0;
-  T* out = nullptr;
+  TO* out = nullptr;
   int64_t ldo = 0;
-  T* self_out = nullptr;
+  TI* self_out = nullptr;
   int64_t ld_self = 0;
   int64_t w = 0;  // padded width processed (multiple of 8)
 };
-template <typename T> void spmm(const SpmmArgs<T>& a, cudaStream_t s);
+template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
 
 // --------------------------------------------------------------------------
 // Dense contractions.  C[M x N] = op(A)[M x K] op(B)[K x N].
@@ -62,18 +64,19 @@ void gather_rows_f32(const float* src, int64_t ld_src, const int32_t* idx, int64
                      int64_t ld_dst, cudaStream_t s);
 void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cudaStream_t s);
 
-void batch_nodes(const int32_t* bcl, const int32_t* loff, int q, const int64_t* cstart, int32_t* map_cl,
-                 int32_t* b_nodes, int nb, cudaStream_t s);
-void batch_count(const int64_t* rp, const int32_t* col, const int32_t* cid, const int32_t* map_cl,
-                 const int32_t* b_nodes, int nb, int arch, const int32_t* labels, const uint8_t* split,
-                 int32_t* deg_b, float* scale, int32_t* lab_b, uint8_t* train_b, cudaStream_t s);
-// b_rp[nb+1] exclusive scan of deg_b; stats[0] = nnz_b, stats[1] = number of train rows
-void batch_scan(const int32_t* deg_b, const uint8_t* train_b, int nb, int64_t* b_rp, int64_t* stats,
-                cudaStream_t s);
-void batch_fill(const int64_t* rp, const int32_t* col, const int32_t* cid, const int32_t* map_cl,
-                const int64_t* cstart, const int32_t* b_nodes, int nb, const int64_t* b_rp, int32_t* b_col,
-                cudaStream_t s);
-void batch_reset(const int32_t* bcl, int q, int32_t* map_cl, cudaStream_t s);
+// Per-step descriptor (host-built, R7): bcl[q] cluster ids, loff[q+1] local row offsets,
+// voff[q+1] offsets of each cluster's adjacency segment inside b_col.
+// map64[c] = (tag << 32) | (uint32)(loff_k - cstart[c]) for the batch's clusters: a
+// neighbour u is inside the batch iff (map64[cid[u]] >> 32) == tag (no reset needed).
+void batch_setup(const int32_t* bcl, const int32_t* loff, const int32_t* voff, int q, const int64_t* cstart,
+                 const int64_t* rp, uint32_t tag, uint64_t* map64, int32_t* b_nodes, int64_t* b_beg, int nb,
+                 int64_t* stats, cudaStream_t s);
+// one pass: in-batch neighbours of row v -> b_col[b_beg[v] .. b_end[v]) (local ids), scale,
+// labels, train flags; stats[0] += nnz_b, stats[1] += train rows (integer atomics: deterministic)
+void batch_build(const int64_t* rp, const int32_t* col, const int32_t* cid, const uint64_t* map64, uint32_t tag,
+                 const int32_t* b_nodes, const int64_t* b_beg, int nb, int arch, const int32_t* labels,
+                 const uint8_t* split, int64_t* b_end, int32_t* b_col, float* scale, int32_t* lab_b,
+                 uint8_t* train_b, int64_t* stats, cudaStream_t s);
 
 // --------------------------------------------------------------------------
 // Loss (R4), optimizers (R8), reductions.

@@ -1,112 +1,196 @@
 // spmm.cu -- aggregation SpMM of Eq. (1)/(2).
 //
-// One warp owns one output row and one 512-byte column chunk (32 lanes x 16 B).
-// Neighbour indices of the row are loaded 32 at a time with one coalesced load,
-// broadcast by shuffle, and each neighbour row chunk is gathered with 16-byte
-// vector loads (4 fp32 / 8 bf16 per lane), accumulated in fp32 registers in a
-// fixed order (deterministic, no atomics).  The normalisation of A_bar is never
-// materialised: row/column scale vectors (deg+1)^{-1/2} (GCN renorm, R1) or
-// 1/deg (GraphSAGE mean, R2) are applied on the fly; the backward SpMM reuses
-// the same CSR with the scales swapped (N^T = A diag(1/deg)).
+// A group of LPR lanes (32, 16, 8 or 4) owns one output row; each lane owns J
+// 16-byte vectors of the row, so a group covers LPR*J*16 bytes of the row in
+// registers and walks the row's neighbour list once.  Neighbour indices are loaded
+// LPR at a time (one coalesced load) and turned into 32-bit vector offsets
+// (row * ldh/V) before a single shuffle broadcast per neighbour; UNROLL neighbour
+// rows are gathered per iteration into raw uint4 registers (UNROLL*J 16-byte loads
+// in flight per lane) and unpacked with shifts (bf16 -> fp32 is a 16-bit shift).
+// Accumulation is fp32 in a fixed order: deterministic, no atomics.
+// The normalisation of A_bar is never materialised: row/column scale vectors
+// (deg+1)^{-1/2} (GCN renorm, R1) or 1/deg (GraphSAGE mean, R2) are applied on the
+// fly; the backward SpMM reuses the same CSR with swapped scales (SURVEY a6:
+// N^T = A diag(1/deg)).  Rows wider than LPR*J*V elements are split into column
+// chunks handled by separate groups.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace gist {
 
-template <typename T, int UNROLL>
-__global__ void __launch_bounds__(256) k_spmm(const SpmmArgs<T> a, int nchunks) {
-  constexpr int V = Elem<T>::kVec;
-  constexpr int CW = 32 * V;
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t v = wid / nchunks;
-  const int chunk = (int)(wid - v * nchunks);
-  if (v >= a.rows) return;
-  const int64_t c0 = (int64_t)chunk * CW + lane * V;
-  const bool active = c0 < a.w;
+namespace {
 
-  float acc[V];
+// 16 bytes -> V fp32 values
+__device__ __forceinline__ void unpack(const uint4& x, float* v, float) {
+  v[0] = __uint_as_float(x.x); v[1] = __uint_as_float(x.y); v[2] = __uint_as_float(x.z); v[3] = __uint_as_float(x.w);
+}
+__device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-  for (int i = 0; i < V; ++i) acc[i] = 0.f;
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
 
-  const int64_t hv = a.h_index ? (int64_t)a.h_index[v] : v;
-  if (a.self && active) {
-    float t[V];
-    ld16(a.H + hv * a.ldh + c0, t);
+template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE>
+__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2 ? 3 : 2)) k_spmm(const SpmmArgs<TI, TO> a, int nchunks) {
+  constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
+  constexpr int GPW = 32 / LPR;      // groups per warp
+  using Off = typename std::conditional<WIDE, int64_t, uint32_t>::type;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % LPR;         // lane inside the group
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane - gl));
+  const int64_t gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LPR;
+  const int64_t v = gid / nchunks;
+  const int chunk = (int)(gid - v * nchunks);
+  if (v >= a.rows) return;           // whole group exits together
+  const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
+  const Off ldv = (Off)(a.ldh / V);  // row stride in 16-byte vectors
+  const int64_t wv = a.w / V;        // width in vectors
+  const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
+
+  float acc[J][V];
+#pragma unroll
+  for (int j = 0; j < J; ++j)
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+  bool act[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) act[j] = vbase + j * LPR < wv;
+
+  const Off hv = (Off)(a.h_index ? (int64_t)a.h_index[v] : v) * ldv;
+  if (a.self || a.self_out) {
     const float s = a.colscale ? a.colscale[v] : 1.f;
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = s * t[i];
-  }
-  if (a.self_out && active) {
-    float t[V];
-    ld16(a.H + hv * a.ldh + c0, t);
-    st16(a.self_out + v * a.ld_self + c0, t);
+    for (int j = 0; j < J; ++j) {
+      if (!act[j]) continue;
+      const uint4 x = H4[hv + vbase + j * LPR];
+      if (a.self_out) *reinterpret_cast<uint4*>(a.self_out + v * a.ld_self + (int64_t)(vbase + j * LPR) * V) = x;
+      if (a.self) {
+        float t[V];
+        unpack(x, t, TI());
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[j][i] = s * t[i];
+      }
+    }
   }
 
-  const int64_t beg = a.row_ptr[v], end = a.row_ptr[v + 1];
-  for (int64_t base = beg; base < end; base += 32) {
-    const int n = (end - base) < 32 ? (int)(end - base) : 32;
-    int32_t u = lane < n ? a.col[base + lane] : 0;
-    float su = (a.colscale && lane < n) ? a.colscale[u] : 1.f;
-    int64_t hu = a.h_index ? (int64_t)(lane < n ? a.h_index[u] : 0) : (int64_t)u;
-    int j = 0;
-    for (; j + UNROLL <= n; j += UNROLL) {
-      float t[UNROLL][V];
+  const int64_t beg = a.row_beg[v], end = a.row_end[v];
+  for (int64_t base = beg; base < end; base += LPR) {
+    const int n = (end - base) < LPR ? (int)(end - base) : LPR;
+    Off ou = 0;
+    float su = 1.f;
+    if (gl < n) {
+      const int32_t u = a.col[base + gl];
+      if (CSCALE) su = a.colscale[u];
+      ou = (Off)(a.h_index ? (int64_t)a.h_index[u] : (int64_t)u) * ldv + vbase;
+    }
+    int jj = 0;
+    for (; jj + UNROLL <= n; jj += UNROLL) {
+      uint4 x[UNROLL][J];
       float s[UNROLL];
 #pragma unroll
       for (int q = 0; q < UNROLL; ++q) {
-        const int64_t r = __shfl_sync(0xffffffffu, hu, j + q);
-        s[q] = __shfl_sync(0xffffffffu, su, j + q);
-        if (active) ld16(a.H + r * a.ldh + c0, t[q]);
-      }
-      if (active) {
+        const Off r = __shfl_sync(gmask, ou, jj + q, LPR);
+        s[q] = CSCALE ? __shfl_sync(gmask, su, jj + q, LPR) : 1.f;
 #pragma unroll
-        for (int q = 0; q < UNROLL; ++q)
-#pragma unroll
-          for (int i = 0; i < V; ++i) acc[i] = fmaf(s[q], t[q][i], acc[i]);
+        for (int j = 0; j < J; ++j)
+          if (act[j]) x[q][j] = __ldg(H4 + r + j * LPR);
       }
+#pragma unroll
+      for (int q = 0; q < UNROLL; ++q)
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          if (act[j]) {
+            float t[V];
+            unpack(x[q][j], t, TI());
+#pragma unroll
+            for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s[q], t[i], acc[j][i]) : acc[j][i] + t[i];
+          }
     }
-    for (; j < n; ++j) {
-      const int64_t r = __shfl_sync(0xffffffffu, hu, j);
-      const float s = __shfl_sync(0xffffffffu, su, j);
-      if (active) {
-        float t[V];
-        ld16(a.H + r * a.ldh + c0, t);
+    for (; jj < n; ++jj) {
+      const Off r = __shfl_sync(gmask, ou, jj, LPR);
+      const float s = CSCALE ? __shfl_sync(gmask, su, jj, LPR) : 1.f;
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[i] = fmaf(s, t[i], acc[i]);
-      }
+      for (int j = 0; j < J; ++j)
+        if (act[j]) {
+          float t[V];
+          unpack(__ldg(H4 + r + j * LPR), t, TI());
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s, t[i], acc[j][i]) : acc[j][i] + t[i];
+        }
     }
   }
-  if (!active) return;
   const float rs = a.rowscale ? a.rowscale[v] : 1.f;
 #pragma unroll
-  for (int i = 0; i < V; ++i) acc[i] *= rs;
-  if (a.add) {
-    float t[V];
-    ld16(a.add + v * a.ld_add + c0, t);
+  for (int j = 0; j < J; ++j) {
+    if (!act[j]) continue;
+    const int64_t c = (int64_t)(vbase + j * LPR) * V;
+    float o[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] += t[i];
-  }
-  if (a.mask) {
-    float t[V];
-    ld16(a.mask + v * a.ld_mask + c0, t);
+    for (int i = 0; i < V; ++i) o[i] = acc[j][i] * rs;
+    if (a.add) {
+      float t[V];
+      unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] = t[i] > 0.f ? acc[i] : 0.f;  // ReLU'(0) = 0 (R3)
+      for (int i = 0; i < V; ++i) o[i] += t[i];
+    }
+    if (a.mask) {
+      float t[V];
+      unpack(*reinterpret_cast<const uint4*>(a.mask + v * a.ld_mask + c), t, TI());
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = t[i] > 0.f ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
+    }
+    if (a.relu) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = fmaxf(o[i], 0.f);
+    }
+    if constexpr (sizeof(TO) == sizeof(TI)) {
+      st16(a.out + v * a.ldo + c, o);
+    } else {
+      constexpr int VO = Elem<TO>::kVec;
+#pragma unroll
+      for (int p = 0; p < V / VO; ++p) st16(a.out + v * a.ldo + c + p * VO, o + p * VO);
+    }
   }
-  st16(a.out + v * a.ldo + c0, acc);
 }
 
-template <typename T>
-void spmm(const SpmmArgs<T>& a, cudaStream_t s) {
-  if (a.rows <= 0 || a.w <= 0) return;
-  constexpr int CW = 32 * Elem<T>::kVec;
+template <typename TI, typename TO, int LPR, int J>
+void launch(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
+  constexpr int CW = LPR * J * Elem<TI>::kVec;
   const int nchunks = (int)cdiv(a.w, CW);
-  const int64_t warps = a.rows * nchunks;
-  const int64_t blocks = cdiv(warps, 8);
-  k_spmm<T, 4><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
+  const int64_t groups = a.rows * nchunks;
+  const int64_t blocks = cdiv(groups, 8 * (32 / LPR));
+  constexpr int UNROLL = J <= 2 ? 4 : 2;
+  // 32-bit vector offsets whenever the gathered operand spans < 2^31 vectors
+  const int64_t nsrc = a.h_index ? INT32_MAX : a.rows;  // indirect rows (global X) may be anywhere
+  const bool wide = (a.h_index != nullptr) ? true : (nsrc * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31));
+  const bool cs = a.colscale != nullptr;
+  if (!wide && cs) k_spmm<TI, TO, LPR, J, UNROLL, true, false><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
+  else if (!wide) k_spmm<TI, TO, LPR, J, UNROLL, false, false><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
+  else if (cs) k_spmm<TI, TO, LPR, J, UNROLL, true, true><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
+  else k_spmm<TI, TO, LPR, J, UNROLL, false, true><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
 }
 
-template void spmm<float>(const SpmmArgs<float>&, cudaStream_t);
-template void spmm<bf16>(const SpmmArgs<bf16>&, cudaStream_t);
+}  // namespace
+
+template <typename TI, typename TO>
+void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
+  if (a.rows <= 0 || a.w <= 0) return;
+  constexpr int V = Elem<TI>::kVec;
+  const int64_t vecs = cdiv(a.w, V);  // 16-byte vectors per row
+  if (vecs <= 4) launch<TI, TO, 4, 1>(a, s);
+  else if (vecs <= 8) launch<TI, TO, 8, 1>(a, s);
+  else if (vecs <= 16) launch<TI, TO, 16, 1>(a, s);
+  else if (vecs <= 32) launch<TI, TO, 32, 1>(a, s);
+  else if (vecs <= 64) launch<TI, TO, 32, 2>(a, s);
+  else if (vecs <= 96) launch<TI, TO, 32, 3>(a, s);
+  else launch<TI, TO, 32, 4>(a, s);  // wider rows: column chunks of 128 vectors
+}
+
+template void spmm<float, float>(const SpmmArgs<float, float>&, cudaStream_t);
+template void spmm<bf16, bf16>(const SpmmArgs<bf16, bf16>&, cudaStream_t);
+template void spmm<bf16, float>(const SpmmArgs<bf16, float>&, cudaStream_t);
 
 }  // namespace gist
