@@ -101,11 +101,17 @@ struct Cfg {
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU>
-__global__ void __launch_bounds__(128, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M, int N, int K,
-              void* __restrict__ Cout, int64_t ldc) {
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU, bool MASK>
+__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ GemmGroupTC G) {
   using CF = Cfg<BN>;
+  const GemmSlotTC& S = G.s[blockIdx.z];  // one sub-GCN slot per grid layer
+  const int M = S.M, N = S.N, K = S.K;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M || n0 >= N) return;         // slots may be smaller than the grid (uniform exit)
+  const CUtensorMap* mapA = &S.ma;
+  const CUtensorMap* mapB = &S.mb;
+  void* Cout = S.C;
+  const int64_t ldc = S.ldc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE_BYTES);
@@ -114,7 +120,6 @@ __global__ void __launch_bounds__(128, 1)
   uint32_t* tmem_slot = (uint32_t*)(accf + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
@@ -124,8 +129,8 @@ __global__ void __launch_bounds__(128, 1)
     }
     mbar_init(accf, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(&mapA);
-    prefetch_map(&mapB);
+    prefetch_map(mapA);
+    prefetch_map(mapB);
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -148,16 +153,16 @@ __global__ void __launch_bounds__(128, 1)
       mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
       const int k0 = kb * BK;
       if (!A_MN) {
-        tma_load_2d(sa, &mapA, &full[s], k0, m0);
+        tma_load_2d(sa, mapA, &full[s], k0, m0);
       } else {
 #pragma unroll
-        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &mapA, &full[s], m0 + 64 * j, k0);
+        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, mapA, &full[s], m0 + 64 * j, k0);
       }
       if (!B_MN) {
-        tma_load_2d(sb, &mapB, &full[s], k0, n0);
+        tma_load_2d(sb, mapB, &full[s], k0, n0);
       } else {
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &mapB, &full[s], n0 + 64 * j, k0);
+        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, mapB, &full[s], n0 + 64 * j, k0);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -198,6 +203,11 @@ __global__ void __launch_bounds__(128, 1)
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
       }
       const int col = n0 + c;
+      if (MASK) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
+        const bf16* mp = (const bf16*)S.mask + (int64_t)row * S.ldm + col;
+        for (int i = 0; i < 16; ++i)
+          if (col + i < N && !(__bfloat162float(mp[i]) > 0.f)) v[i] = 0.f;
+      }
       if (OUT_F32) {
         float* dst = (float*)Cout + (int64_t)row * ldc + col;
         if (col + 16 <= N && (((uintptr_t)dst & 15) == 0)) {
@@ -257,57 +267,94 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU>
-void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N, int64_t K, void* C, int64_t ldc,
-               cudaStream_t s) {
-  auto kern = k_gemm_tc<BN, A_MN, B_MN, OUT_F32, RELU>;
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU, bool MASK>
+void launch_tc(const GemmPlanTC& P, cudaStream_t s) {
+  auto kern = k_gemm_tc<BN, A_MN, B_MN, OUT_F32, RELU, MASK>;
   static bool attr = false;  // per instantiation
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
     attr = true;
   }
-  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM));
-  kern<<<grid, 128, Cfg<BN>::SMEM, s>>>(ma, mb, (int)M, (int)N, (int)K, C, ldc);
+  dim3 grid((unsigned)cdiv(P.maxN, BN), (unsigned)cdiv(P.maxM, BM), (unsigned)P.G.n);
+  kern<<<grid, 128, Cfg<BN>::SMEM, s>>>(P.G);
 }
 
 template <int BN, bool A_MN, bool B_MN>
-void dispatch_epi(bool out_f32, bool relu, const CUtensorMap& ma, const CUtensorMap& mb, int64_t M, int64_t N,
-                  int64_t K, void* C, int64_t ldc, cudaStream_t s) {
-  if (out_f32) {
-    if (relu) launch_tc<BN, A_MN, B_MN, true, true>(ma, mb, M, N, K, C, ldc, s);
-    else launch_tc<BN, A_MN, B_MN, true, false>(ma, mb, M, N, K, C, ldc, s);
-  } else {
-    if (relu) launch_tc<BN, A_MN, B_MN, false, true>(ma, mb, M, N, K, C, ldc, s);
-    else launch_tc<BN, A_MN, B_MN, false, false>(ma, mb, M, N, K, C, ldc, s);
+void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
+  const int e = (P.out_f32 ? 4 : 0) | (P.relu ? 2 : 0) | (P.mask ? 1 : 0);
+  switch (e) {
+    case 0: launch_tc<BN, A_MN, B_MN, false, false, false>(P, s); break;
+    case 1: launch_tc<BN, A_MN, B_MN, false, false, true>(P, s); break;
+    case 2: launch_tc<BN, A_MN, B_MN, false, true, false>(P, s); break;
+    case 3: launch_tc<BN, A_MN, B_MN, false, true, true>(P, s); break;
+    case 4: launch_tc<BN, A_MN, B_MN, true, false, false>(P, s); break;
+    case 5: launch_tc<BN, A_MN, B_MN, true, false, true>(P, s); break;
+    case 6: launch_tc<BN, A_MN, B_MN, true, true, false>(P, s); break;
+    default: launch_tc<BN, A_MN, B_MN, true, true, true>(P, s); break;
   }
 }
 
+template <int BNV>
+void dispatch_layout(const GemmPlanTC& P, cudaStream_t s) {
+  if (!P.a_mn && P.b_mn) dispatch_epi<BNV, false, true>(P, s);
+  else if (!P.a_mn && !P.b_mn) dispatch_epi<BNV, false, false>(P, s);
+  else if (P.a_mn && P.b_mn) dispatch_epi<BNV, true, true>(P, s);
+  else dispatch_epi<BNV, true, false>(P, s);
+}
+
 }  // namespace
+
+bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
+  if (!get_encode() || n < 1 || n > kMaxGroup) return false;
+  const GemmOp& o0 = ops[0];
+  P->a_mn = o0.transA;     // A stored K x M
+  P->b_mn = !o0.transB;    // B stored K x N
+  P->out_f32 = o0.out_f32;
+  P->relu = o0.relu;
+  P->mask = o0.mask != nullptr;
+  P->maxM = P->maxN = 0;
+  int64_t maxN = 0;
+  for (int i = 0; i < n; ++i) maxN = ops[i].N > maxN ? ops[i].N : maxN;
+  P->bn = maxN > 128 ? 256 : 128;
+  P->G.n = n;
+  for (int i = 0; i < n; ++i) {
+    const GemmOp& o = ops[i];
+    if (o.transA != o0.transA || o.transB != o0.transB || o.out_f32 != o0.out_f32 || o.relu != o0.relu ||
+        (o.mask != nullptr) != P->mask)
+      return false;
+    if (o.K <= 0 || ((uintptr_t)o.A & 15) || ((uintptr_t)o.B & 15) || (o.lda % 8) || (o.ldb % 8)) return false;
+    GemmSlotTC& S = P->G.s[i];
+    bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, 64, 64) : make_map(&S.ma, o.A, o.K, o.M, o.lda, 64, BM);
+    ok = ok && (P->b_mn ? make_map(&S.mb, o.B, o.N, o.K, o.ldb, 64, 64)
+                        : make_map(&S.mb, o.B, o.K, o.N, o.ldb, 64, P->bn));
+    if (!ok) return false;
+    S.C = o.C;
+    S.ldc = o.ldc;
+    S.mask = o.mask;
+    S.ldm = o.ldm;
+    S.M = (int)o.M;
+    S.N = (int)o.N;
+    S.K = (int)o.K;
+    P->maxM = o.M > P->maxM ? o.M : P->maxM;
+    P->maxN = o.N > P->maxN ? o.N : P->maxN;
+  }
+  return true;
+}
+
+void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
+  if (P.G.n <= 0 || P.maxM <= 0 || P.maxN <= 0) return;
+  if (P.bn == 256) dispatch_layout<256>(P, s);
+  else dispatch_layout<128>(P, s);
+}
 
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda, const bf16* B,
                int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s) {
   if (!get_encode()) return false;
   if (M == 0 || N == 0) return true;  // nothing to do (also the availability probe)
-  if (K <= 0) return false;
-  // TMA: 16-byte aligned base and row strides
-  if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || (lda % 8) || (ldb % 8)) return false;
-  const int BN = N > 128 ? 256 : 128;
-  CUtensorMap ma, mb;
-  const bool a_mn = transA;    // A stored K x M
-  const bool b_mn = !transB;   // B stored K x N
-  bool ok = a_mn ? make_map(&ma, A, M, K, lda, 64, 64) : make_map(&ma, A, K, M, lda, 64, BM);
-  ok = ok && (b_mn ? make_map(&mb, B, N, K, ldb, 64, 64) : make_map(&mb, B, K, N, ldb, 64, BN));
-  if (!ok) return false;
-#define GIST_TC_DISPATCH(BNV)                                                                   \
-  do {                                                                                          \
-    if (!a_mn && b_mn) dispatch_epi<BNV, false, true>(out_f32, relu, ma, mb, M, N, K, C, ldc, s); \
-    else if (!a_mn && !b_mn) dispatch_epi<BNV, false, false>(out_f32, relu, ma, mb, M, N, K, C, ldc, s); \
-    else if (a_mn && b_mn) dispatch_epi<BNV, true, true>(out_f32, relu, ma, mb, M, N, K, C, ldc, s); \
-    else dispatch_epi<BNV, true, false>(out_f32, relu, ma, mb, M, N, K, C, ldc, s);             \
-  } while (0)
-  if (BN == 256) GIST_TC_DISPATCH(256);
-  else GIST_TC_DISPATCH(128);
-#undef GIST_TC_DISPATCH
+  GemmOp o{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, out_f32, relu, nullptr, 0};
+  GemmPlanTC P;
+  if (!gemm_bf16_prepare(&o, 1, &P)) return false;
+  gemm_bf16_launch(P, s);
   return true;
 }
 

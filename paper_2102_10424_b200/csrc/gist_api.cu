@@ -34,8 +34,7 @@ struct LayerShape {
 
 struct Slot {
   int index = 0;  // global slot id i
-  cudaStream_t st = nullptr;
-  cudaEvent_t ev = nullptr;
+  // views into the rank's contiguous [slots_per_rank x S_max] buffers (Wall / Gall / Mall / Vall / Wball)
   float *W = nullptr, *G = nullptr, *M = nullptr, *V = nullptr;
   bf16* Wb = nullptr;
   // batch schedule (device + pinned host mirror), capacity `cap` steps
@@ -43,13 +42,11 @@ struct Slot {
   int32_t *desc_dev = nullptr, *desc_host = nullptr;
   std::vector<int> nb_of_step, q_of_step;
   std::vector<int64_t> vol_of_step;
-  cudaEvent_t desc_ev = nullptr;
   int cached_epoch = -1;
   std::vector<int32_t> epoch_perm;
-  // batch buffers
+  // batch buffers (nb_max rows)
   int32_t *b_nodes = nullptr, *lab_b = nullptr, *b_col = nullptr;
   uint64_t* map64 = nullptr;  // cluster -> (step tag, local-id delta)
-  uint32_t tag = 0;
   uint8_t* train_b = nullptr;
   float* scale = nullptr;
   int64_t *b_beg = nullptr, *b_end = nullptr, *stats = nullptr;
@@ -59,6 +56,23 @@ struct Slot {
   float* logits = nullptr;
   float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
   int last_nb = 0;
+};
+
+// Launch plan of one subTrain step for a group of <= kMaxGroup local slots run in lockstep:
+// argument blocks of every grouped launch, built once per partition (TMA descriptors encoded once).
+template <typename T>
+struct StepPlan {
+  struct Group {
+    int first = 0, count = 0;
+    BatchGroup batch;
+    std::vector<SpmmGroup<T, T>> fwd_spmm, bwd_spmm;  // per layer (bwd index l produces dZ_{l-1})
+    std::vector<GemmPlanTC> fwd_tc, dw_tc, dx_tc;     // BF16 mode
+    std::vector<SgemmGroup> fwd_f, dw_f, dx_f;        // FP32 mode
+    std::vector<double> fwd_fl, dw_fl, dx_fl;         // algorithmic FLOPs (profiling)
+    std::vector<double> fwd_by, bwd_by;               // SpMM compulsory bytes excl. nnz part (profiling)
+    CeGroup<T> ce;
+  };
+  std::vector<Group> groups;
 };
 
 }  // namespace
@@ -99,6 +113,14 @@ struct gist_ctx {
   int slots_per_rank = 0;
   std::vector<Slot> slots;                     // local slots
   float* Wall = nullptr;                       // slots_per_rank * S_max (local slot weights, contiguous)
+  float *Gall = nullptr, *Mall = nullptr, *Vall = nullptr;  // same packing: gradients, Adam moments
+  bf16* Wball = nullptr;                       // bf16 shadow of Wall (BF16 mode)
+  int nb_max_rows = 0;                         // static row count of every batch launch
+  StepState* dstate = nullptr;                 // device step state (z, t, lr)
+  StepState* hstate = nullptr;                 // pinned host staging for it
+  cudaEvent_t hstate_ev = nullptr;
+  StepPlan<float> plan_f;
+  StepPlan<bf16> plan_b;
   float* Wrecv = nullptr;                      // world * slots_per_rank * S_max (world > 1)
   int alloc_m = 0;
   void* sort_tmp = nullptr;
@@ -366,12 +388,8 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
 }
 
 static void free_slots(gist_ctx* c) {
-  for (auto& s : c->slots) {
-    if (s.st) cudaStreamDestroy(s.st);
-    if (s.ev) cudaEventDestroy(s.ev);
-    if (s.desc_ev) cudaEventDestroy(s.desc_ev);
+  for (auto& s : c->slots)
     if (s.desc_host) cudaFreeHost(s.desc_host);
-  }
   c->slots.clear();
 }
 
@@ -386,6 +404,8 @@ extern "C" void gist_destroy(gist_ctx* c) {
   for (auto& r : c->prof_pending) c->ev_pool.push_back(r.a), c->ev_pool.push_back(r.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->nnz_pin) cudaFreeHost(c->nnz_pin);
+  if (c->hstate) cudaFreeHost(c->hstate);
+  if (c->hstate_ev) cudaEventDestroy(c->hstate_ev);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -613,6 +633,10 @@ extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* 
 // ============================================================ partition ===
 static gist_status alloc_slots(gist_ctx* c, int m) {
   free_slots(c);
+  for (void* p : {(void*)c->Wall, (void*)c->Gall, (void*)c->Mall, (void*)c->Vall, (void*)c->Wball, (void*)c->Wrecv})
+    dfree(c, p);
+  c->Wall = c->Gall = c->Mall = c->Vall = c->Wrecv = nullptr;
+  c->Wball = nullptr;
   const int W = c->cfg.world_size, r = c->cfg.rank;
   c->slots_per_rank = (m + W - 1) / W;
   // largest packed slot (every hidden block at ceil(d/m))
@@ -626,9 +650,27 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     smax += (int64_t)maxK[l] * maxN[l];
   }
   c->S_max = smax;
-  TRY(dalloc_t(c, &c->Wall, (size_t)c->slots_per_rank * smax));
-  if (W > 1) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * c->slots_per_rank * smax));
+  const size_t tot = (size_t)c->slots_per_rank * smax;
+  TRY(dalloc_t(c, &c->Wall, tot));
+  TRY(dalloc_t(c, &c->Gall, tot));
+  CK(cudaMemsetAsync(c->Wall, 0, tot * 4, c->stream));
+  CK(cudaMemsetAsync(c->Gall, 0, tot * 4, c->stream));
+  if (c->cfg.optimizer == GIST_OPT_ADAM) {
+    TRY(dalloc_t(c, &c->Mall, tot));
+    TRY(dalloc_t(c, &c->Vall, tot));
+  }
+  if (c->prec == GIST_PREC_BF16) {
+    TRY(dalloc_t(c, &c->Wball, tot));
+    CK(cudaMemsetAsync(c->Wball, 0, tot * 2, c->stream));
+  }
+  if (W > 1) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
+  if (!c->dstate) {
+    TRY(dalloc_t(c, &c->dstate, 1));
+    CK(cudaMallocHost(&c->hstate, sizeof(StepState)));
+    CK(cudaEventCreateWithFlags(&c->hstate_ev, cudaEventDisableTiming));
+  }
   const int nbm = std::max(c->nb_max, 1);
+  c->nb_max_rows = nbm;
   const size_t E = esize(c);
   int maxKall = 0;
   for (int l = 0; l < c->L; ++l) maxKall = std::max(maxKall, maxK[l]);
@@ -636,16 +678,10 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     c->slots.emplace_back();
     Slot& s = c->slots.back();
     s.index = i;
-    CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&s.desc_ev, cudaEventDisableTiming));
     s.W = c->Wall + (size_t)j * smax;
-    TRY(dalloc_t(c, &s.G, smax));
-    if (c->cfg.optimizer == GIST_OPT_ADAM) {
-      TRY(dalloc_t(c, &s.M, smax));
-      TRY(dalloc_t(c, &s.V, smax));
-    }
-    if (c->prec == GIST_PREC_BF16) TRY(dalloc_t(c, &s.Wb, smax));
+    s.G = c->Gall + (size_t)j * smax;
+    if (c->Mall) s.M = c->Mall + (size_t)j * smax, s.V = c->Vall + (size_t)j * smax;
+    if (c->Wball) s.Wb = c->Wball + (size_t)j * smax;
     TRY(dalloc_t(c, &s.b_nodes, nbm));
     TRY(dalloc_t(c, &s.lab_b, nbm));
     TRY(dalloc_t(c, &s.train_b, nbm));
@@ -659,18 +695,165 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     s.C.assign(c->L, nullptr);
     s.H.assign(c->L, nullptr);
     s.dZ.assign(c->L, nullptr);
-    for (int l = 0; l < c->L; ++l) {
+    for (int l = 0; l < c->L; ++l) {  // zero-initialised: padding columns must read as 0
       TRY(dalloc(c, &s.C[l], (size_t)nbm * maxK[l] * E));
-      if (c->arch == GIST_ARCH_GCN && l > 0) TRY(dalloc(c, &s.H[l], (size_t)nbm * maxK[l] * E));
+      CK(cudaMemsetAsync(s.C[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
+      if (c->arch == GIST_ARCH_GCN && l > 0) {
+        TRY(dalloc(c, &s.H[l], (size_t)nbm * maxK[l] * E));
+        CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
+      }
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
+      CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
     }
     TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
+    CK(cudaMemsetAsync(s.dC, 0, (size_t)nbm * maxKall * E, c->stream));
     TRY(dalloc_t(c, &s.logits, (size_t)nbm * maxN[c->L - 1]));
+    CK(cudaMemsetAsync(s.logits, 0, (size_t)nbm * maxN[c->L - 1] * 4, c->stream));
     TRY(dalloc_t(c, &s.row_loss, nbm));
     TRY(dalloc_t(c, &s.step_loss, 1));
     TRY(dalloc_t(c, &s.loss_acc, 1));
   }
   c->alloc_m = m;
+  return GIST_OK;
+}
+
+// compulsory bytes of one SpMM launch excluding the nnz-proportional part
+template <typename T>
+static double spmm_bytes(const SpmmArgs<T, T>& a) {
+  const double rw = (double)a.rows * (double)a.w * sizeof(T);
+  double b = (double)a.rows * 16 + rw /*H*/ + rw /*out*/;
+  if (a.add) b += rw;
+  if (a.mask) b += rw;
+  if (a.self_out) b += rw;
+  if (a.rowscale) b += a.rows * 4.0;
+  if (a.colscale) b += a.rows * 4.0;
+  if (a.h_index) b += a.rows * 4.0;
+  return b;
+}
+
+// Builds the launch plan of one subTrain step (every grouped launch's argument block).
+template <typename T>
+static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
+  P.groups.clear();
+  const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
+  const bool sage = c->arch == GIST_ARCH_SAGE;
+  const bool tc = c->prec == GIST_PREC_BF16;
+  for (int g0 = 0; g0 < (int)c->slots.size(); g0 += kMaxGroup) {
+    typename StepPlan<T>::Group g;
+    g.first = g0;
+    g.count = std::min<int>(kMaxGroup, (int)c->slots.size() - g0);
+    g.batch.n = g.count;
+    g.batch.q = q;
+    g.batch.nb_max = nb;
+    g.batch.st = c->dstate;
+    g.fwd_spmm.assign(L, SpmmGroup<T, T>());
+    g.bwd_spmm.assign(L, SpmmGroup<T, T>());
+    g.fwd_tc.assign(L, GemmPlanTC());
+    g.dw_tc.assign(L, GemmPlanTC());
+    g.dx_tc.assign(L, GemmPlanTC());
+    g.fwd_f.assign(L, SgemmGroup());
+    g.dw_f.assign(L, SgemmGroup());
+    g.dx_f.assign(L, SgemmGroup());
+    g.fwd_fl.assign(L, 0.0);
+    g.dw_fl.assign(L, 0.0);
+    g.dx_fl.assign(L, 0.0);
+    g.fwd_by.assign(L, 0.0);
+    g.bwd_by.assign(L, 0.0);
+    g.ce.n = g.count;
+    g.ce.rows = nb;
+    g.ce.k = c->k;
+    g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
+    for (int l = 0; l < L; ++l) {
+      std::vector<GemmOp> fw, dw, dx;
+      for (int j = 0; j < g.count; ++j) {
+        Slot& sl = c->slots[g0 + j];
+        const auto& shp = c->shapes[sl.index];
+        const LayerShape& sh = shp[l];
+        if (l == 0) {
+          BatchSlot& b = g.batch.s[j];
+          b.desc = sl.desc_dev; b.map64 = sl.map64; b.b_nodes = sl.b_nodes; b.b_beg = sl.b_beg; b.b_end = sl.b_end;
+          b.b_col = sl.b_col; b.scale = sl.scale; b.lab_b = sl.lab_b; b.train_b = sl.train_b; b.stats = sl.stats;
+          CeSlot<T>& e = g.ce.s[j];
+          e.logits = sl.logits; e.dlog = (T*)sl.dZ[L - 1]; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
+          e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
+        }
+        T* C = (T*)sl.C[l];
+        // forward aggregation (a2)
+        SpmmArgs<T, T>& a = g.fwd_spmm[l].a[j];
+        a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
+        if (sage) {
+          a.rowscale = sl.scale;               // N = D^-1 A (R2)
+          a.out = C + sh.half; a.ldo = sh.Kp;   // right half: N H
+          a.w = sh.half;
+          if (l == 0) {
+            a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]);
+            a.self_out = C; a.ld_self = sh.Kp;  // left half: gathered X rows
+          } else {
+            a.H = C; a.ldh = sh.Kp;             // left half written by the previous GEMM epilogue
+          }
+        } else {
+          a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;  // D~^-1/2 (A+I) D~^-1/2 (R1)
+          a.out = C; a.ldo = sh.Kp; a.w = sh.Kp;
+          if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
+          else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
+        }
+        g.fwd_by[l] += spmm_bytes(a);
+        // forward contraction (a3)
+        const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
+        if (l + 1 < L) {
+          void* out = sage ? sl.C[l + 1] : sl.H[l + 1];
+          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, shp[l + 1].Kp, false, true,
+                              nullptr, 0});
+        } else {
+          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false,
+                              nullptr, 0});
+        }
+        g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
+        // backward: dW_l = C_l^T dZ_l (fp32 into the packed gradient buffer)
+        dw.push_back(GemmOp{true, false, sh.Kp, sh.Np, nb, C, sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
+                            nullptr, 0});
+        g.dw_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
+        if (l > 0) {
+          // dC_l = dZ_l W_l^T
+          dx.push_back(GemmOp{false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false,
+                              nullptr, 0});
+          g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
+          SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
+          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
+          b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
+          if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
+            b.colscale = sl.scale; b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
+            b.add = (const T*)sl.dC; b.ld_add = sh.Kp;
+            b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
+            b.w = sh.half;
+          } else {     // dZ_{l-1} = (A_hat^T dC) * 1[H_l > 0]
+            b.rowscale = sl.scale; b.colscale = sl.scale; b.self = 1;
+            b.H = (const T*)sl.dC; b.ldh = sh.Kp;
+            b.mask = (const T*)sl.H[l]; b.ld_mask = sh.Kp;
+            b.w = sh.Kp;
+          }
+          g.bwd_by[l] += spmm_bytes(b);
+        }
+      }
+      g.fwd_spmm[l].n = g.count;
+      g.bwd_spmm[l].n = l > 0 ? g.count : 0;
+      if (tc) {
+        if (!gemm_bf16_prepare(fw.data(), g.count, &g.fwd_tc[l]) ||
+            !gemm_bf16_prepare(dw.data(), g.count, &g.dw_tc[l]) ||
+            (l > 0 && !gemm_bf16_prepare(dx.data(), g.count, &g.dx_tc[l])))
+          return fail(c, GIST_E_UNSUPPORTED, "tcgen05 GEMM plan failed (alignment / driver entry point)");
+      } else {
+        for (int j = 0; j < g.count; ++j) {
+          g.fwd_f[l].op[j] = fw[j];
+          g.dw_f[l].op[j] = dw[j];
+          if (l > 0) g.dx_f[l].op[j] = dx[j];
+        }
+        g.fwd_f[l].n = g.dw_f[l].n = g.count;
+        g.dx_f[l].n = l > 0 ? g.count : 0;
+      }
+    }
+    P.groups.push_back(g);
+  }
   return GIST_OK;
 }
 
@@ -745,7 +928,6 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
   // extract Theta^(i) for local slots (R6), reset optimizer state (R8)
   for (Slot& sl : c->slots) {
     const auto& shp = c->shapes[sl.index];
-    int64_t tot = 0;
     for (int l = 0; l < c->L; ++l) {
       const LayerShape& sh = shp[l];
       LayerMap mp;
@@ -753,14 +935,16 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
       mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
       mp.ldg = c->th_N[l];
       PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta[l], mp, sl.W + sh.off, s));
-      tot = sh.off + (int64_t)sh.Kp * sh.Np;
     }
-    if (sl.M) {
-      CK(cudaMemsetAsync(sl.M, 0, (size_t)c->S_max * 4, s));
-      CK(cudaMemsetAsync(sl.V, 0, (size_t)c->S_max * 4, s));
-    }
-    if (sl.Wb) LK(f32_to_bf16(sl.W, sl.Wb, tot, s));
   }
+  const int64_t tot_local = (int64_t)c->slots.size() * c->S_max;
+  if (c->Mall && tot_local > 0) {
+    CK(cudaMemsetAsync(c->Mall, 0, (size_t)tot_local * 4, s));
+    CK(cudaMemsetAsync(c->Vall, 0, (size_t)tot_local * 4, s));
+  }
+  if (c->Wball && tot_local > 0) LK(f32_to_bf16(c->Wall, c->Wball, tot_local, s));
+  if (c->prec == GIST_PREC_BF16) TRY(build_plan<bf16>(c, c->plan_b));
+  else TRY(build_plan<float>(c, c->plan_f));
   c->prof_now = false;
   TRY(check_launch(c, "partition"));
   c->adam_t = 0;
@@ -786,171 +970,98 @@ extern "C" gist_status gist_get_partition(gist_ctx* c, int32_t dim, int32_t* uni
 }
 
 // ============================================================== step ======
-static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
-                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
-                            cudaStream_t s) {
-  const int id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * (double)M * (double)N * (double)K);
-  if (c->prec == GIST_PREC_FP32) {
-    gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s);
-  } else if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s)) {
-    return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
-  }
+template <typename T>
+static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp, double flops, cudaStream_t s) {
+  const int id = prof_begin(c, s, GIST_PROF_GEMM, flops);
+  if (c->prec == GIST_PREC_BF16) gemm_bf16_launch(tcp, s);
+  else gemm_f32_group(fp, s);
   prof_end(c, s, id);
   ++c->nk;
-  return GIST_OK;
 }
 
-// compulsory bytes of one SpMM launch excluding the nnz-proportional part
+// One subTrain step of every slot of group g, in lockstep: every
+// kernel below is one launch over all slots of the group.
 template <typename T>
-static double spmm_bytes(const SpmmArgs<T, T>& a) {
-  const double rw = (double)a.rows * (double)a.w * sizeof(T);
-  double b = (double)(a.rows + 1) * 8 + rw /*H*/ + rw /*out*/;
-  if (a.add) b += rw;
-  if (a.mask) b += rw;
-  if (a.self_out) b += rw;
-  if (a.rowscale) b += a.rows * 4.0;
-  if (a.colscale) b += a.rows * 4.0;
-  if (a.h_index) b += a.rows * 4.0;
-  return b;
-}
-
-template <typename T>
-static gist_status run_step(gist_ctx* c, Slot& sl, int z, float lr) {
-  cudaStream_t s = sl.st;
-  const int q = c->cfg.clusters_per_batch;
-  const int nb = sl.nb_of_step[z];
-  const int qq = sl.q_of_step[z];  // clusters in this batch (< q only for an epoch's last batch)
-  const int32_t* d = sl.desc_dev + (size_t)z * (3 * q + 3);
-  const int32_t* bcl = d;
-  const int32_t* loff = d + q;
-  const int32_t* voff = d + 2 * q + 1;
-  const uint32_t tag = ++sl.tag;
-  const bool sage = c->arch == GIST_ARCH_SAGE;
-  const auto& shp = c->shapes[sl.index];
+static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z) {
+  cudaStream_t s = c->stream;
   const int L = c->L;
-  sl.last_nb = nb;
-  c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
+  for (int j = 0; j < g.count; ++j) c->slots[g.first + j].last_nb = c->slots[g.first + j].nb_of_step[z];
   int nnz_slot = -1;
   if (c->prof_now && c->nnz_pin_used < c->nnz_pin_cap) nnz_slot = c->nnz_pin_used++;
-  // ---- a1: Cluster mini-batch build (2 launches, one profiled record)
+  // ---- a1: Cluster mini-batch build
   {
-    const double vol = (double)sl.vol_of_step[z];
+    double vol = 0.0;
+    for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
     int id = -1;
-    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + nb * 45.0, 4.0, nnz_slot);
-    batch_setup(bcl, loff, voff, qq, c->cstart, c->rp, tag, sl.map64, sl.b_nodes, sl.b_beg, nb, sl.stats, s);
-    batch_build(c->rp, c->col, c->cid, sl.map64, tag, sl.b_nodes, sl.b_beg, nb, c->arch, c->labels, c->split,
-                sl.b_end, sl.b_col, sl.scale, sl.lab_b, sl.train_b, sl.stats, s);
+    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + g.count * c->nb_max_rows * 45.0, 4.0, nnz_slot);
+    batch_setup(g.batch, c->cstart, c->rp, s);
+    batch_build(g.batch, c->rp, c->col, c->cid, c->arch, c->labels, c->split, s);
     prof_end(c, s, id);
     c->nk += 2;
-    if (nnz_slot >= 0) CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, sl.stats, 8, cudaMemcpyDeviceToHost, s));
+    if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
+      CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
   }
-  auto spmm_prof = [&](const SpmmArgs<T, T>& a) {
+  const double per_nnz = 4.0 * g.count;
+  auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
     int id = -1;
-    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, spmm_bytes(a), 4.0, nnz_slot);
-    spmm<T, T>(a, s);
+    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, bytes, per_nnz, nnz_slot);
+    spmm_group<T, T>(G, s);
     prof_end(c, s, id);
     ++c->nk;
   };
-  const T* Wop = c->prec == GIST_PREC_BF16 ? (const T*)sl.Wb : (const T*)sl.W;
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
-    const LayerShape& sh = shp[l];
-    T* C = (T*)sl.C[l];
-    SpmmArgs<T, T> a;
-    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-    if (sage) {
-      a.rowscale = sl.scale;              // N = D^-1 A (R2)
-      a.out = C + sh.half; a.ldo = sh.Kp;  // right half: N H
-      a.w = sh.half;
-      if (l == 0) {
-        a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]);
-        a.self_out = C; a.ld_self = sh.Kp;  // left half: H (gathered X rows)
-      } else {
-        a.H = C; a.ldh = sh.Kp;              // left half written by the previous GEMM epilogue
-      }
-    } else {
-      a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;  // D~^-1/2 (A+I) D~^-1/2 (R1)
-      a.out = C; a.ldo = sh.Kp; a.w = sh.Kp;
-      if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
-      else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
-    }
-    spmm_prof(a);
-    const T* Wl = Wop + sh.off;
-    if (l + 1 < L) {
-      const LayerShape& nx = shp[l + 1];
-      T* out = sage ? (T*)sl.C[l + 1] : (T*)sl.H[l + 1];
-      TRY(gemm_any(c, false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, nx.Kp, false, true, s));
-    } else {
-      TRY(gemm_any(c, false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false, s));
-    }
+    spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
+    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
   }
   // ---- a4: softmax cross-entropy
-  const LayerShape& last = shp[L - 1];
   {
-    const double bytes = (double)nb * last.Np * (4.0 + sizeof(T)) + nb * 9.0 + nb * 4.0;
-    int id = prof_begin(c, s, GIST_PROF_LOSS, bytes);
-    softmax_ce<T>(sl.logits, last.Np, nb, c->k, sl.lab_b, sl.train_b, sl.stats, (T*)sl.dZ[L - 1], sl.row_loss, s);
-    reduce_loss(sl.row_loss, nb, sl.stats, sl.step_loss, sl.loss_acc, s);
+    const double bytes = (double)g.count * c->nb_max_rows * (g.ce.ld * (4.0 + sizeof(T)) + 17.0);
+    const int id = prof_begin(c, s, GIST_PROF_LOSS, bytes);
+    softmax_ce<T>(g.ce, s);
+    reduce_loss<T>(g.ce, s);
     prof_end(c, s, id);
     c->nk += 2;
   }
   // ---- a5/a6: backward
   for (int l = L - 1; l >= 0; --l) {
-    const LayerShape& sh = shp[l];
-    const T* Wl = Wop + sh.off;
-    // dW_l = C_l^T dZ_l  (fp32 into the packed gradient buffer)
-    TRY(gemm_any(c, true, false, sh.Kp, sh.Np, nb, sl.C[l], sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
-                 s));
+    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
     if (l == 0) break;
-    // dC_l = dZ_l W_l^T
-    TRY(gemm_any(c, false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false, s));
-    SpmmArgs<T, T> a;
-    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-    a.out = (T*)sl.dZ[l - 1]; a.ldo = shp[l - 1].Np;
-    if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
-      a.colscale = sl.scale; a.H = (const T*)sl.dC + sh.half; a.ldh = sh.Kp;
-      a.add = (const T*)sl.dC; a.ld_add = sh.Kp;
-      a.mask = (const T*)sl.C[l]; a.ld_mask = sh.Kp;
-      a.w = sh.half;
-    } else {     // dZ_{l-1} = (A_hat^T dC) * 1[H_l > 0]
-      a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;
-      a.H = (const T*)sl.dC; a.ldh = sh.Kp;
-      a.mask = (const T*)sl.H[l]; a.ld_mask = sh.Kp;
-      a.w = sh.Kp;
-    }
-    spmm_prof(a);
+    launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
+    spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
   }
-  // ---- a7: optimizer
-  int64_t tot = last.off + (int64_t)last.Kp * last.Np;
-  bf16* Wb = c->prec == GIST_PREC_BF16 ? sl.Wb : nullptr;
-  if (c->cfg.optimizer == GIST_OPT_ADAM) {
-    const double t = (double)(c->adam_t + 1);
-    const float bc1 = (float)(1.0 - std::pow((double)c->cfg.beta1, t));
-    const float bc2 = (float)(1.0 - std::pow((double)c->cfg.beta2, t));
-    PL(GIST_PROF_OPTIM, (double)tot * (28.0 + (Wb ? 2.0 : 0.0)), s,
-       adam_step(sl.W, sl.G, sl.M, sl.V, tot, lr, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, bc1, std::sqrt(bc2), Wb, s));
-  } else {
-    PL(GIST_PROF_OPTIM, (double)tot * (12.0 + (Wb ? 2.0 : 0.0)), s, sgd_step(sl.W, sl.G, tot, lr, Wb, s));
-  }
-  c->prof_now = false;
   return GIST_OK;
 }
 
-// host side of R7 for a whole subtrain call: cluster lists, local offsets, n_b per step
-static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
+// a7 over every local slot at once (the packed buffers are contiguous), then advance the step state
+static gist_status run_optimizer(gist_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t n = (int64_t)c->slots.size() * c->S_max;
+  if (c->cfg.optimizer == GIST_OPT_ADAM)
+    PL(GIST_PROF_OPTIM, (double)n * (28.0 + (c->Wball ? 2.0 : 0.0)), s,
+       adam_step(c->Wall, c->Gall, c->Mall, c->Vall, n, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate, c->Wball,
+                 s));
+  else
+    PL(GIST_PROF_OPTIM, (double)n * (12.0 + (c->Wball ? 2.0 : 0.0)), s,
+       sgd_step(c->Wall, c->Gall, n, c->dstate, c->Wball, s));
+  LK(step_advance(c->dstate, s));
+  return GIST_OK;
+}
+
+// host side of R7 for a whole subtrain call: cluster lists, offsets, n_b, tags per step
+static gist_status schedule(gist_ctx* c, Slot& sl, int iters, bool* grew) {
   const int q = c->cfg.clusters_per_batch;
-  const int per = 3 * q + 3;
-  if (iters > sl.cap) {
+  const int per = 3 * q + 4;
+  if (iters > sl.cap || !sl.desc_dev) {
+    *grew = true;
+    CK(cudaStreamSynchronize(c->stream));  // previous uploads / readers of the old buffers are done
     if (sl.desc_host) {
-      CK(cudaEventSynchronize(sl.desc_ev));
       cudaFreeHost(sl.desc_host);
       dfree(c, sl.desc_dev);
     }
-    sl.cap = std::max(iters, 16);
+    sl.cap = std::max(iters, 64);
     CK(cudaMallocHost(&sl.desc_host, (size_t)sl.cap * per * 4));
     TRY(dalloc_t(c, &sl.desc_dev, (size_t)sl.cap * per));
-  } else {
-    CK(cudaEventSynchronize(sl.desc_ev));  // previous upload finished reading the pinned buffer
   }
   sl.nb_of_step.assign(iters, 0);
   sl.q_of_step.assign(iters, 0);
@@ -977,7 +1088,7 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
         dv[k] = (int32_t)voff;
         off += (int32_t)(c->cstart_h[cl + 1] - c->cstart_h[cl]);
         voff += c->cvol_h[cl];
-      } else {  // last batch of an epoch may hold fewer clusters: empty ranges
+      } else {  // last batch of an epoch may hold fewer clusters
         d[k] = d[qq - 1];
         d[q + k] = off;
         dv[k] = (int32_t)voff;
@@ -986,13 +1097,11 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters) {
     d[2 * q] = off;
     dv[q] = (int32_t)voff;
     d[3 * q + 2] = qq;
-    sl.vol_of_step[z] = voff;
+    d[3 * q + 3] = (int32_t)(uint32_t)(c->step + z + 1);  // unique tag per step (0 = never)
     sl.nb_of_step[z] = off;
     sl.q_of_step[z] = qq;
+    sl.vol_of_step[z] = voff;
   }
-  CK(cudaMemcpyAsync(sl.desc_dev, sl.desc_host, (size_t)iters * per * 4, cudaMemcpyHostToDevice, sl.st));
-  CK(cudaEventRecord(sl.desc_ev, sl.st));
-  c->h2d += (int64_t)iters * per * 4;
   return GIST_OK;
 }
 
@@ -1000,35 +1109,45 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
   PRE(c);
   if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "subtrain: call partition first");
   if (local_iters < 0) return fail(c, GIST_E_ARG, "subtrain: local_iters < 0");
-  if (c->prec == GIST_PREC_BF16 && !gemm_bf16(false, false, 0, 0, 0, nullptr, 0, nullptr, 0, nullptr, 0, false, false,
-                                              c->stream))
-    return fail(c, GIST_E_UNSUPPORTED, "bf16 mode needs the tcgen05 GEMM");
-  CK(cudaEventRecord(c->fork_ev, c->stream));
-  for (Slot& sl : c->slots) {
-    CK(cudaStreamWaitEvent(sl.st, c->fork_ev, 0));
-    TRY(schedule(c, sl, local_iters));
-    CK(cudaMemsetAsync(sl.loss_acc, 0, 4, sl.st));
+  cudaStream_t s = c->stream;
+  // host schedule for every local slot; the previous call's uploads must have left the pinned buffers
+  CK(cudaEventSynchronize(c->hstate_ev));
+  const int per = 3 * c->cfg.clusters_per_batch + 4;
+  bool grew = false;
+  for (Slot& sl : c->slots) TRY(schedule(c, sl, local_iters, &grew));
+  if (grew) {  // descriptor buffers moved: the step plan holds their addresses
+    if (c->prec == GIST_PREC_BF16) TRY(build_plan<bf16>(c, c->plan_b));
+    else TRY(build_plan<float>(c, c->plan_f));
   }
+  for (Slot& sl : c->slots) {
+    if (local_iters > 0)
+      CK(cudaMemcpyAsync(sl.desc_dev, sl.desc_host, (size_t)local_iters * per * 4, cudaMemcpyHostToDevice, s));
+    c->h2d += (int64_t)local_iters * per * 4;
+    CK(cudaMemsetAsync(sl.loss_acc, 0, 4, s));
+  }
+  *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0.f};
+  CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->hstate_ev, s));
   for (int z = 0; z < local_iters; ++z) {
-    for (Slot& sl : c->slots) {
-      if (c->prec == GIST_PREC_BF16) TRY(run_step<bf16>(c, sl, z, lr));
-      else TRY(run_step<float>(c, sl, z, lr));
+    c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
+    if (c->prec == GIST_PREC_BF16) {
+      for (auto& g : c->plan_b.groups) TRY(run_group_step<bf16>(c, g, z));
+    } else {
+      for (auto& g : c->plan_f.groups) TRY(run_group_step<float>(c, g, z));
     }
-    ++c->adam_t;
+    TRY(run_optimizer(c));
+    c->prof_now = false;
   }
-  for (Slot& sl : c->slots) {
-    CK(cudaEventRecord(sl.ev, sl.st));
-    CK(cudaStreamWaitEvent(c->stream, sl.ev, 0));
-  }
+  c->adam_t += local_iters;
   c->step += local_iters;
   TRY(check_launch(c, "subtrain"));
   if (c->prof_stride > 0) prof_flush(c);
   if (mean_loss) {
     std::fill(mean_loss, mean_loss + c->m, 0.f);
+    CK(cudaStreamSynchronize(s));
     for (Slot& sl : c->slots) {
       float v = 0.f;
-      CK(cudaMemcpyAsync(&v, sl.loss_acc, 4, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
+      CK(cudaMemcpy(&v, sl.loss_acc, 4, cudaMemcpyDeviceToHost));
       mean_loss[sl.index] = local_iters > 0 ? v / (float)local_iters : 0.f;
       c->d2h += 4;
     }
@@ -1067,6 +1186,19 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   TRY(check_launch(c, "aggregate"));
   c->round += 1;
   c->state = S_PARAMS;
+  return GIST_OK;
+}
+
+// single GEMM (eval path): FP32 SIMT or BF16 tcgen05
+static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
+                            cudaStream_t s) {
+  if (c->prec == GIST_PREC_FP32) {
+    gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s);
+  } else if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s)) {
+    return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
+  }
+  ++c->nk;
   return GIST_OK;
 }
 
@@ -1174,7 +1306,7 @@ extern "C" gist_status gist_get_sub_params(gist_ctx* c, int32_t slot, int32_t la
   if (!sl) return fail(c, GIST_E_ARG, "get_sub_params: slot not on this rank");
   const LayerShape& sh = c->shapes[slot][layer];
   std::vector<float> buf((size_t)sh.Kp * sh.Np);
-  CK(cudaStreamSynchronize(sl->st));
+  CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(buf.data(), sl->W + sh.off, buf.size() * 4, cudaMemcpyDeviceToHost));
   phys_to_logical(c, sh, buf, out);
   return GIST_OK;
@@ -1197,7 +1329,7 @@ extern "C" gist_status gist_get_trace(gist_ctx* c, int32_t slot, int32_t what, i
   if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "get_trace: no open round");
   Slot* sl = local_slot(c, slot);
   if (!sl) return fail(c, GIST_E_ARG, "get_trace: slot not on this rank");
-  CK(cudaStreamSynchronize(sl->st));
+  CK(cudaStreamSynchronize(c->stream));
   const int nb = sl->last_nb;
   const auto& shp = c->shapes[slot];
   int64_t cnt = 0;

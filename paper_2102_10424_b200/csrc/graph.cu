@@ -97,56 +97,68 @@ void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cud
 }
 
 // ------------------------------------------------------------ batch build --
-__global__ void k_batch_setup(const int32_t* __restrict__ bcl, const int32_t* __restrict__ loff,
-                              const int32_t* __restrict__ voff, int q, const int64_t* __restrict__ cstart,
-                              const int64_t* __restrict__ rp, uint32_t tag, uint64_t* __restrict__ map64,
-                              int32_t* __restrict__ b_nodes, int64_t* __restrict__ b_beg, int nb,
-                              int64_t* __restrict__ stats) {
+// grid (cdiv(nb_max, 256), slots)
+__global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_t* __restrict__ cstart,
+                              const int64_t* __restrict__ rp) {
+  const BatchSlot& S = G.s[blockIdx.y];
+  const int q = G.q;
+  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+  const int32_t* bcl = d;
+  const int32_t* loff = d + q;
+  const int32_t* voff = d + 2 * q + 1;
+  const int qq = d[3 * q + 2];
+  const uint32_t tag = (uint32_t)d[3 * q + 3];
+  const int nb = loff[q];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v < q) {
+  if (v < qq) {
     const int32_t c = bcl[v];
-    map64[c] = ((uint64_t)tag << 32) | (uint32_t)(loff[v] - (int32_t)cstart[c]);
+    S.map64[c] = ((uint64_t)tag << 32) | (uint32_t)(loff[v] - (int32_t)cstart[c]);
   }
-  if (v == 0) stats[0] = stats[1] = 0;
-  if (v >= nb) return;
-  int lo = 0, hi = q - 1;  // largest k with loff[k] <= v
+  if (v == 0) S.stats[0] = S.stats[1] = 0;
+  if (v >= G.nb_max) return;
+  if (v >= nb) {  // inert dummy row
+    S.b_nodes[v] = 0;
+    S.b_beg[v] = 0;
+    return;
+  }
+  int lo = 0, hi = qq - 1;  // largest k with loff[k] <= v
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (loff[mid] <= v) lo = mid; else hi = mid - 1;
   }
   const int32_t c = bcl[lo];
   const int64_t g = cstart[c] + (v - loff[lo]);
-  b_nodes[v] = (int32_t)g;
-  b_beg[v] = voff[lo] + (rp[g] - rp[cstart[c]]);  // row v's segment inside the batch's adjacency space
+  S.b_nodes[v] = (int32_t)g;
+  S.b_beg[v] = voff[lo] + (rp[g] - rp[cstart[c]]);  // row v's segment inside the batch's adjacency space
 }
-void batch_setup(const int32_t* bcl, const int32_t* loff, const int32_t* voff, int q, const int64_t* cstart,
-                 const int64_t* rp, uint32_t tag, uint64_t* map64, int32_t* b_nodes, int64_t* b_beg, int nb,
-                 int64_t* stats, cudaStream_t s) {
-  const int n = nb > q ? nb : q;
-  k_batch_setup<<<(unsigned)cdiv(n > 0 ? n : 1, 256), 256, 0, s>>>(bcl, loff, voff, q, cstart, rp, tag, map64,
-                                                                    b_nodes, b_beg, nb, stats);
+void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s) {
+  const int n = G.nb_max > G.q ? G.nb_max : G.q;
+  k_batch_setup<<<dim3((unsigned)cdiv(n > 0 ? n : 1, 256), (unsigned)G.n), 256, 0, s>>>(G, cstart, rp);
 }
 
 // One warp per batch row: walk the row's global adjacency 64 entries per iteration
 // (two independent load chains col -> cid -> map64 in flight), keep the in-batch
 // neighbours (ballot compaction, original order), and write the row's normalisation
 // scale, label and train flag.  Counters are warp -> block reduced, one integer atomic
-// per block (integer addition: deterministic).
-__global__ void __launch_bounds__(256) k_batch_build(
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const int32_t* __restrict__ cid,
-    const uint64_t* __restrict__ map64, uint32_t tag, const int32_t* __restrict__ b_nodes,
-    const int64_t* __restrict__ b_beg, int nb, int arch, const int32_t* __restrict__ labels,
-    const uint8_t* __restrict__ split, int64_t* __restrict__ b_end, int32_t* __restrict__ b_col,
-    float* __restrict__ scale, int32_t* __restrict__ lab_b, uint8_t* __restrict__ train_b,
-    int64_t* __restrict__ stats) {
+// per block (integer addition: deterministic).  grid (cdiv(nb_max, 8), slots).
+__global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ BatchGroup G,
+                                                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                     const int32_t* __restrict__ cid, int arch,
+                                                     const int32_t* __restrict__ labels,
+                                                     const uint8_t* __restrict__ split) {
+  const BatchSlot& S = G.s[blockIdx.y];
+  const int q = G.q;
+  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+  const int nb = d[2 * q];
+  const uint32_t tag = (uint32_t)d[3 * q + 3];
   __shared__ int s_cnt[8], s_tr[8];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x * 8 + w;
   int cnt = 0, tr = 0;
   if (v < nb) {
-    const int64_t g = b_nodes[v];
+    const int64_t g = S.b_nodes[v];
     const int64_t end = rp[g + 1];
-    const int64_t out0 = b_beg[v];
+    const int64_t out0 = S.b_beg[v];
     int64_t out = out0;
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t base = rp[g]; base < end; base += 64) {
@@ -155,43 +167,46 @@ __global__ void __launch_bounds__(256) k_batch_build(
       const int32_t u1 = e1 < end ? col[e1] : -1;
       const int32_t c0 = u0 >= 0 ? cid[u0] : 0;
       const int32_t c1 = u1 >= 0 ? cid[u1] : 0;
-      const uint64_t m0 = u0 >= 0 ? map64[c0] : 0ull;
-      const uint64_t m1 = u1 >= 0 ? map64[c1] : 0ull;
+      const uint64_t m0 = u0 >= 0 ? S.map64[c0] : 0ull;
+      const uint64_t m1 = u1 >= 0 ? S.map64[c1] : 0ull;
       const bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
       const bool in1 = u1 >= 0 && (uint32_t)(m1 >> 32) == tag;
       const unsigned b0 = __ballot_sync(0xffffffffu, in0);
       const unsigned b1 = __ballot_sync(0xffffffffu, in1);
-      if (in0) b_col[out + __popc(b0 & lt)] = u0 + (int32_t)(uint32_t)m0;
+      if (in0) S.b_col[out + __popc(b0 & lt)] = u0 + (int32_t)(uint32_t)m0;
       out += __popc(b0);
-      if (in1) b_col[out + __popc(b1 & lt)] = u1 + (int32_t)(uint32_t)m1;
+      if (in1) S.b_col[out + __popc(b1 & lt)] = u1 + (int32_t)(uint32_t)m1;
       out += __popc(b1);
     }
     cnt = (int)(out - out0);
     if (lane == 0) {
-      b_end[v] = out;
-      const float d = (float)cnt;
-      scale[v] = arch == 0 ? 1.0f / sqrtf(d + 1.0f) : (cnt > 0 ? 1.0f / d : 0.f);
-      lab_b[v] = labels[g];
+      S.b_end[v] = out;
+      const float dg = (float)cnt;
+      S.scale[v] = arch == 0 ? 1.0f / sqrtf(dg + 1.0f) : (cnt > 0 ? 1.0f / dg : 0.f);
+      S.lab_b[v] = labels[g];
       tr = split[g] == 0;
-      train_b[v] = (uint8_t)tr;
+      S.train_b[v] = (uint8_t)tr;
     }
+  } else if (v < G.nb_max && lane == 0) {  // inert dummy row
+    S.b_end[v] = 0;
+    S.scale[v] = 0.f;
+    S.lab_b[v] = 0;
+    S.train_b[v] = 0;
   }
   if (lane == 0) { s_cnt[w] = cnt; s_tr[w] = tr; }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long a = 0, b = 0;
     for (int k = 0; k < 8; ++k) a += s_cnt[k], b += s_tr[k];
-    if (a) atomicAdd((unsigned long long*)&stats[0], (unsigned long long)a);
-    if (b) atomicAdd((unsigned long long*)&stats[1], (unsigned long long)b);
+    if (a) atomicAdd((unsigned long long*)&S.stats[0], (unsigned long long)a);
+    if (b) atomicAdd((unsigned long long*)&S.stats[1], (unsigned long long)b);
   }
 }
-void batch_build(const int64_t* rp, const int32_t* col, const int32_t* cid, const uint64_t* map64, uint32_t tag,
-                 const int32_t* b_nodes, const int64_t* b_beg, int nb, int arch, const int32_t* labels,
-                 const uint8_t* split, int64_t* b_end, int32_t* b_col, float* scale, int32_t* lab_b,
-                 uint8_t* train_b, int64_t* stats, cudaStream_t s) {
-  if (nb <= 0) return;
-  k_batch_build<<<(unsigned)cdiv(nb, 8), 256, 0, s>>>(rp, col, cid, map64, tag, b_nodes, b_beg, nb, arch, labels,
-                                                       split, b_end, b_col, scale, lab_b, train_b, stats);
+void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
+                 const int32_t* labels, const uint8_t* split, cudaStream_t s) {
+  if (G.nb_max <= 0) return;
+  k_batch_build<<<dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s>>>(G, rp, col, cid, arch, labels,
+                                                                                  split);
 }
 
 }  // namespace gist

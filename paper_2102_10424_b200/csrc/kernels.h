@@ -40,6 +40,15 @@ struct SpmmArgs {
 };
 template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
 
+// Grouped launch: the same SpMM for up to kMaxGroup sub-GCN slots in one grid (grid.y = slot).
+constexpr int kMaxGroup = 8;
+template <typename TI, typename TO = TI>
+struct SpmmGroup {
+  SpmmArgs<TI, TO> a[kMaxGroup];
+  int n = 0;
+};
+template <typename TI, typename TO> void spmm_group(const SpmmGroup<TI, TO>& G, cudaStream_t s);
+
 // --------------------------------------------------------------------------
 // Dense contractions.  C[M x N] = op(A)[M x K] op(B)[K x N].
 //   transA: A stored K x M (lda >= M); else M x K.  transB: B stored N x K; else K x N.
@@ -47,6 +56,50 @@ template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStr
 // --------------------------------------------------------------------------
 void gemm_f32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, bool relu, cudaStream_t s);
+// One operand set of a (grouped) GEMM.  mask (optional, same dtype as the operands):
+// out = acc * 1[mask[row, col] > 0] (the ReLU mask of the layer below).
+struct GemmOp {
+  bool transA, transB;
+  int64_t M, N, K;
+  const void* A;
+  int64_t lda;
+  const void* B;
+  int64_t ldb;
+  void* C;
+  int64_t ldc;
+  bool out_f32, relu;
+  const void* mask;
+  int64_t ldm;
+};
+}  // namespace gist
+#include <cuda.h>
+namespace gist {
+struct alignas(64) GemmSlotTC {
+  CUtensorMap ma, mb;  // TMA descriptors (128 B each)
+  void* C;
+  const void* mask;
+  int64_t ldc, ldm;
+  int M, N, K, pad_;
+};
+struct GemmGroupTC {
+  GemmSlotTC s[kMaxGroup];
+  int n = 0;
+};
+// Host-side plan of one grouped tcgen05 GEMM (tensor maps encoded once, launched many times).
+struct GemmPlanTC {
+  GemmGroupTC G;
+  bool a_mn = false, b_mn = false, out_f32 = false, relu = false, mask = false;
+  int bn = 128;
+  int64_t maxM = 0, maxN = 0;
+};
+bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* plan);
+void gemm_bf16_launch(const GemmPlanTC& plan, cudaStream_t s);
+// FP32 SIMT grouped GEMM (grid.z = slot)
+struct SgemmGroup {
+  GemmOp op[kMaxGroup];
+  int n = 0;
+};
+void gemm_f32_group(const SgemmGroup& g, cudaStream_t s);
 // returns false if the shape/alignment is not supported by the tensor-core path
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda,
                const bf16* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s);
@@ -64,32 +117,70 @@ void gather_rows_f32(const float* src, int64_t ld_src, const int32_t* idx, int64
                      int64_t ld_dst, cudaStream_t s);
 void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cudaStream_t s);
 
-// Per-step descriptor (host-built, R7): bcl[q] cluster ids, loff[q+1] local row offsets,
-// voff[q+1] offsets of each cluster's adjacency segment inside b_col.
-// map64[c] = (tag << 32) | (uint32)(loff_k - cstart[c]) for the batch's clusters: a
-// neighbour u is inside the batch iff (map64[cid[u]] >> 32) == tag (no reset needed).
-void batch_setup(const int32_t* bcl, const int32_t* loff, const int32_t* voff, int q, const int64_t* cstart,
-                 const int64_t* rp, uint32_t tag, uint64_t* map64, int32_t* b_nodes, int64_t* b_beg, int nb,
-                 int64_t* stats, cudaStream_t s);
-// one pass: in-batch neighbours of row v -> b_col[b_beg[v] .. b_end[v]) (local ids), scale,
-// labels, train flags; stats[0] += nnz_b, stats[1] += train rows (integer atomics: deterministic)
-void batch_build(const int64_t* rp, const int32_t* col, const int32_t* cid, const uint64_t* map64, uint32_t tag,
-                 const int32_t* b_nodes, const int64_t* b_beg, int nb, int arch, const int32_t* labels,
-                 const uint8_t* split, int64_t* b_end, int32_t* b_col, float* scale, int32_t* lab_b,
-                 uint8_t* train_b, int64_t* stats, cudaStream_t s);
+// Device-resident step state: the kernels of one subTrain step read everything that
+// changes from step to step from here, so a step is a fixed launch sequence (CUDA-graph
+// capturable).  z = index of the current step in this call's descriptor array,
+// t = optimizer steps taken since the last partition, lr = learning rate of the call.
+struct StepState {
+  int32_t z, t;
+  float lr, pad_;
+};
+// Per-step batch descriptor (host-built, R7), 3q+4 int32:
+//   [bcl(q) | loff(q+1) | voff(q+1) | qq | tag]
+// bcl = cluster ids, loff = local row offsets (loff[qq..q] = n_b), voff = offsets of each
+// cluster's adjacency segment inside b_col, qq = clusters in this batch, tag = unique
+// per slot and step.  map64[c] = (tag << 32) | (uint32)(loff_k - cstart[c]) for the batch's
+// clusters: neighbour u is in the batch iff (map64[cid[u]] >> 32) == tag (nothing to reset).
+// Rows [n_b, nb_max) are inert dummy rows (no neighbours, scale 0, not train), so every
+// launch uses the static row count nb_max.
+struct BatchSlot {
+  const int32_t* desc;
+  uint64_t* map64;
+  int32_t* b_nodes;
+  int64_t *b_beg, *b_end;
+  int32_t* b_col;
+  float* scale;
+  int32_t* lab_b;
+  uint8_t* train_b;
+  int64_t* stats;  // [0] nnz_b, [1] train rows
+};
+struct BatchGroup {
+  BatchSlot s[kMaxGroup];
+  int n = 0, q = 0, nb_max = 0;
+  const StepState* st = nullptr;
+};
+void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s);
+void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
+                 const int32_t* labels, const uint8_t* split, cudaStream_t s);
 
 // --------------------------------------------------------------------------
 // Loss (R4), optimizers (R8), reductions.
 // --------------------------------------------------------------------------
 template <typename T>
-void softmax_ce(const float* logits, int64_t ld, int nb, int k, const int32_t* lab, const uint8_t* train,
-                const int64_t* stats, T* dlog, float* row_loss, cudaStream_t s);
-// step_loss[0] = sum(row_loss)/n_train (0 if none); loss_acc[0] += step_loss[0]
-void reduce_loss(const float* row_loss, int nb, const int64_t* stats, float* step_loss, float* loss_acc,
-                 cudaStream_t s);
-void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float lr, float b1, float b2, float eps,
-               float bc1, float bc2_sqrt, bf16* Wb, cudaStream_t s);
-void sgd_step(float* W, const float* G, int64_t n, float lr, bf16* Wb, cudaStream_t s);
+struct CeSlot {
+  const float* logits;
+  T* dlog;
+  float* row_loss;
+  const int32_t* lab;
+  const uint8_t* train;
+  const int64_t* stats;
+  float *step_loss, *loss_acc;
+};
+template <typename T>
+struct CeGroup {
+  CeSlot<T> s[kMaxGroup];
+  int n = 0, rows = 0, k = 0;
+  int64_t ld = 0;
+};
+// per slot: dlogits = (softmax - onehot)/n_train on train rows (else 0), row losses
+template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);
+// per slot: step_loss = sum(row_loss)/n_train (0 if none); loss_acc += step_loss
+template <typename T> void reduce_loss(const CeGroup<T>& G, cudaStream_t s);
+// Adam (R8) over n packed parameters; bias corrections from st->t (device), lr from st->lr
+void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
+               const StepState* st, bf16* Wb, cudaStream_t s);
+void sgd_step(float* W, const float* G, int64_t n, const StepState* st, bf16* Wb, cudaStream_t s);
+void step_advance(StepState* st, cudaStream_t s);
 void f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
 
 // --------------------------------------------------------------------------

@@ -12,14 +12,19 @@ namespace gist {
 namespace {
 constexpr int BM = 128, BN = 128, BK = 8, PAD = 4;
 
-template <bool TA, bool TB, bool RELU>
-__global__ void __launch_bounds__(256) k_sgemm(int M, int N, int K, const float* __restrict__ A, int64_t lda,
-                                               const float* __restrict__ B, int64_t ldb, float* __restrict__ C,
-                                               int64_t ldc) {
+template <bool TA, bool TB, bool RELU, bool MASK>
+__global__ void __launch_bounds__(256) k_sgemm(const __grid_constant__ SgemmGroup G) {
+  const GemmOp& op = G.op[blockIdx.z];  // one sub-GCN slot per grid layer
+  const int M = (int)op.M, N = (int)op.N, K = (int)op.K;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M || n0 >= N) return;
+  const float* __restrict__ A = (const float*)op.A;
+  const float* __restrict__ B = (const float*)op.B;
+  float* __restrict__ C = (float*)op.C;
+  const int64_t lda = op.lda, ldb = op.ldb, ldc = op.ldc;
   __shared__ __align__(16) float As[2][BK][BM + PAD];
   __shared__ __align__(16) float Bs[2][BK][BN + PAD];
   const int t = threadIdx.x;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int ty = t >> 4, tx = t & 15;
 
   // per-thread load coordinates
@@ -85,29 +90,43 @@ __global__ void __launch_bounds__(256) k_sgemm(int M, int N, int K, const float*
       if (n >= N) continue;
       float v = acc[i][j];
       if (RELU) v = fmaxf(v, 0.f);
+      if (MASK && !(((const float*)op.mask)[(int64_t)m * op.ldm + n] > 0.f)) v = 0.f;  // ReLU'(0) = 0 (R3)
       C[(int64_t)m * ldc + n] = v;
     }
   }
 }
 
 template <bool TA, bool TB>
-void launch(bool relu, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B, int64_t ldb,
-            float* C, int64_t ldc, cudaStream_t s) {
-  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM));
-  if (relu)
-    k_sgemm<TA, TB, true><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc);
-  else
-    k_sgemm<TA, TB, false><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, C, ldc);
+void launch(const SgemmGroup& g, int64_t maxM, int64_t maxN, cudaStream_t s) {
+  dim3 grid((unsigned)cdiv(maxN, BN), (unsigned)cdiv(maxM, BM), (unsigned)g.n);
+  const bool relu = g.op[0].relu, mask = g.op[0].mask != nullptr;
+  if (relu && mask) k_sgemm<TA, TB, true, true><<<grid, 256, 0, s>>>(g);
+  else if (relu) k_sgemm<TA, TB, true, false><<<grid, 256, 0, s>>>(g);
+  else if (mask) k_sgemm<TA, TB, false, true><<<grid, 256, 0, s>>>(g);
+  else k_sgemm<TA, TB, false, false><<<grid, 256, 0, s>>>(g);
 }
 }  // namespace
 
+void gemm_f32_group(const SgemmGroup& g, cudaStream_t s) {
+  int64_t maxM = 0, maxN = 0;
+  for (int i = 0; i < g.n; ++i) {
+    maxM = g.op[i].M > maxM ? g.op[i].M : maxM;
+    maxN = g.op[i].N > maxN ? g.op[i].N : maxN;
+  }
+  if (g.n <= 0 || maxM <= 0 || maxN <= 0) return;
+  const bool ta = g.op[0].transA, tb = g.op[0].transB;
+  if (!ta && !tb) launch<false, false>(g, maxM, maxN, s);
+  else if (!ta && tb) launch<false, true>(g, maxM, maxN, s);
+  else if (ta && !tb) launch<true, false>(g, maxM, maxN, s);
+  else launch<true, true>(g, maxM, maxN, s);
+}
+
 void gemm_f32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, bool relu, cudaStream_t s) {
-  if (M <= 0 || N <= 0) return;
-  if (!transA && !transB) launch<false, false>(relu, M, N, K, A, lda, B, ldb, C, ldc, s);
-  else if (!transA && transB) launch<false, true>(relu, M, N, K, A, lda, B, ldb, C, ldc, s);
-  else if (transA && !transB) launch<true, false>(relu, M, N, K, A, lda, B, ldb, C, ldc, s);
-  else launch<true, true>(relu, M, N, K, A, lda, B, ldb, C, ldc, s);
+  SgemmGroup g;
+  g.op[0] = GemmOp{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, true, relu, nullptr, 0};
+  g.n = 1;
+  gemm_f32_group(g, s);
 }
 
 }  // namespace gist

@@ -34,7 +34,9 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
 }
 
 template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE>
-__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2 ? 3 : 2)) k_spmm(const SpmmArgs<TI, TO> a, int nchunks) {
+__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2 ? 3 : 2))
+    k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
+  const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
   constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
   constexpr int GPW = 32 / LPR;      // groups per warp
   using Off = typename std::conditional<WIDE, int64_t, uint32_t>::type;
@@ -84,7 +86,8 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
     if (gl < n) {
       const int32_t u = a.col[base + gl];
       if (CSCALE) su = a.colscale[u];
-      ou = (Off)(a.h_index ? (int64_t)a.h_index[u] : (int64_t)u) * ldv + vbase;
+      // row offset only: each receiving lane adds its own column after the broadcast
+      ou = (Off)(a.h_index ? (int64_t)a.h_index[u] : (int64_t)u) * ldv;
     }
     int jj = 0;
     for (; jj + UNROLL <= n; jj += UNROLL) {
@@ -96,7 +99,7 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
         s[q] = CSCALE ? __shfl_sync(gmask, su, jj + q, LPR) : 1.f;
 #pragma unroll
         for (int j = 0; j < J; ++j)
-          if (act[j]) x[q][j] = __ldg(H4 + r + j * LPR);
+          if (act[j]) x[q][j] = __ldg(H4 + r + vbase + j * LPR);
       }
 #pragma unroll
       for (int q = 0; q < UNROLL; ++q)
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
       for (int j = 0; j < J; ++j)
         if (act[j]) {
           float t[V];
-          unpack(__ldg(H4 + r + j * LPR), t, TI());
+          unpack(__ldg(H4 + r + vbase + j * LPR), t, TI());
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s, t[i], acc[j][i]) : acc[j][i] + t[i];
         }
@@ -157,40 +160,58 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
 }
 
 template <typename TI, typename TO, int LPR, int J>
-void launch(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
+void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s) {
   constexpr int CW = LPR * J * Elem<TI>::kVec;
-  const int nchunks = (int)cdiv(a.w, CW);
-  const int64_t groups = a.rows * nchunks;
-  const int64_t blocks = cdiv(groups, 8 * (32 / LPR));
+  const int nchunks = (int)cdiv(w, CW);
+  const int64_t groups = rows * nchunks;
+  const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
   constexpr int UNROLL = J <= 2 ? 4 : 2;
-  // 32-bit vector offsets whenever the gathered operand spans < 2^31 vectors
-  const int64_t nsrc = a.h_index ? INT32_MAX : a.rows;  // indirect rows (global X) may be anywhere
-  const bool wide = (a.h_index != nullptr) ? true : (nsrc * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31));
-  const bool cs = a.colscale != nullptr;
-  if (!wide && cs) k_spmm<TI, TO, LPR, J, UNROLL, true, false><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
-  else if (!wide) k_spmm<TI, TO, LPR, J, UNROLL, false, false><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
-  else if (cs) k_spmm<TI, TO, LPR, J, UNROLL, true, true><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
-  else k_spmm<TI, TO, LPR, J, UNROLL, false, true><<<(unsigned)blocks, 256, 0, s>>>(a, nchunks);
+  // 32-bit vector offsets whenever every gathered operand spans < 2^31 vectors
+  bool wide = false, cs = G.a[0].colscale != nullptr;
+  for (int i = 0; i < G.n; ++i) {
+    const SpmmArgs<TI, TO>& a = G.a[i];
+    wide |= a.h_index != nullptr || a.rows * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
+  }
+  if (!wide && cs) k_spmm<TI, TO, LPR, J, UNROLL, true, false><<<grid, 256, 0, s>>>(G, nchunks);
+  else if (!wide) k_spmm<TI, TO, LPR, J, UNROLL, false, false><<<grid, 256, 0, s>>>(G, nchunks);
+  else if (cs) k_spmm<TI, TO, LPR, J, UNROLL, true, true><<<grid, 256, 0, s>>>(G, nchunks);
+  else k_spmm<TI, TO, LPR, J, UNROLL, false, true><<<grid, 256, 0, s>>>(G, nchunks);
 }
 
 }  // namespace
 
 template <typename TI, typename TO>
-void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
-  if (a.rows <= 0 || a.w <= 0) return;
+void spmm_group(const SpmmGroup<TI, TO>& G, cudaStream_t s) {
+  int64_t rows = 0, w = 0;
+  for (int i = 0; i < G.n; ++i) {
+    rows = G.a[i].rows > rows ? G.a[i].rows : rows;
+    w = G.a[i].w > w ? G.a[i].w : w;
+  }
+  if (G.n <= 0 || rows <= 0 || w <= 0) return;
   constexpr int V = Elem<TI>::kVec;
-  const int64_t vecs = cdiv(a.w, V);  // 16-byte vectors per row
-  if (vecs <= 4) launch<TI, TO, 4, 1>(a, s);
-  else if (vecs <= 8) launch<TI, TO, 8, 1>(a, s);
-  else if (vecs <= 16) launch<TI, TO, 16, 1>(a, s);
-  else if (vecs <= 32) launch<TI, TO, 32, 1>(a, s);
-  else if (vecs <= 64) launch<TI, TO, 32, 2>(a, s);
-  else if (vecs <= 96) launch<TI, TO, 32, 3>(a, s);
-  else launch<TI, TO, 32, 4>(a, s);  // wider rows: column chunks of 128 vectors
+  const int64_t vecs = cdiv(w, V);  // 16-byte vectors per row (widest slot)
+  if (vecs <= 4) launch<TI, TO, 4, 1>(G, rows, w, s);
+  else if (vecs <= 8) launch<TI, TO, 8, 1>(G, rows, w, s);
+  else if (vecs <= 16) launch<TI, TO, 16, 1>(G, rows, w, s);
+  else if (vecs <= 32) launch<TI, TO, 32, 1>(G, rows, w, s);
+  else if (vecs <= 64) launch<TI, TO, 32, 2>(G, rows, w, s);
+  else if (vecs <= 96) launch<TI, TO, 32, 3>(G, rows, w, s);
+  else launch<TI, TO, 32, 4>(G, rows, w, s);  // wider rows: column chunks of 128 vectors
+}
+
+template <typename TI, typename TO>
+void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
+  SpmmGroup<TI, TO> G;
+  G.a[0] = a;
+  G.n = 1;
+  spmm_group(G, s);
 }
 
 template void spmm<float, float>(const SpmmArgs<float, float>&, cudaStream_t);
 template void spmm<bf16, bf16>(const SpmmArgs<bf16, bf16>&, cudaStream_t);
 template void spmm<bf16, float>(const SpmmArgs<bf16, float>&, cudaStream_t);
+template void spmm_group<float, float>(const SpmmGroup<float, float>&, cudaStream_t);
+template void spmm_group<bf16, bf16>(const SpmmGroup<bf16, bf16>&, cudaStream_t);
+template void spmm_group<bf16, float>(const SpmmGroup<bf16, float>&, cudaStream_t);
 
 }  // namespace gist

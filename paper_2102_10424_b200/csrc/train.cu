@@ -7,19 +7,20 @@
 
 namespace gist {
 
-// One warp per batch row.  loss_v = logsumexp(z_v) - z_v[y_v] on train rows;
-// dlogits_v = (softmax(z_v) - onehot(y_v)) / n_train on train rows, else 0;
+// One warp per batch row (grid.y = slot).  loss_v = logsumexp(z_v) - z_v[y_v] on train
+// rows; dlogits_v = (softmax(z_v) - onehot(y_v)) / n_train on train rows, else 0;
 // padding columns [k, ld) are written as 0.
 template <typename T>
-__global__ void k_softmax_ce(const float* __restrict__ logits, int64_t ld, int nb, int k,
-                             const int32_t* __restrict__ lab, const uint8_t* __restrict__ train,
-                             const int64_t* __restrict__ stats, T* __restrict__ dlog, float* __restrict__ row_loss) {
+__global__ void k_softmax_ce(const __grid_constant__ CeGroup<T> G) {
+  const CeSlot<T>& S = G.s[blockIdx.y];
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (v >= nb) return;
-  const float* z = logits + (int64_t)v * ld;
-  const int64_t nt = stats[1];
-  const bool tr = train[v] && nt > 0;
+  if (v >= G.rows) return;
+  const int64_t ld = G.ld;
+  const int k = G.k;
+  const float* z = S.logits + (int64_t)v * ld;
+  const int64_t nt = S.stats[1];
+  const bool tr = S.train[v] && nt > 0;
   float mx = -INFINITY;
   for (int c = lane; c < k; c += 32) mx = fmaxf(mx, z[c]);
 #pragma unroll
@@ -29,54 +30,63 @@ __global__ void k_softmax_ce(const float* __restrict__ logits, int64_t ld, int n
 #pragma unroll
   for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
   const float lse = mx + logf(se);
-  const int y = lab[v];
+  const int y = S.lab[v];
   const float inv = tr ? 1.0f / (float)nt : 0.f;
   for (int c = lane; c < ld; c += 32) {
     float g = 0.f;
     if (tr && c < k) g = (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) * inv;
-    dlog[(int64_t)v * ld + c] = Elem<T>::from_f(g);
+    S.dlog[(int64_t)v * ld + c] = Elem<T>::from_f(g);
   }
-  if (lane == 0) row_loss[v] = tr ? lse - z[y] : 0.f;
+  if (lane == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
 }
 
 template <typename T>
-void softmax_ce(const float* logits, int64_t ld, int nb, int k, const int32_t* lab, const uint8_t* train,
-                const int64_t* stats, T* dlog, float* row_loss, cudaStream_t s) {
-  if (nb <= 0) return;
-  k_softmax_ce<T><<<(unsigned)cdiv(nb, 8), 256, 0, s>>>(logits, ld, nb, k, lab, train, stats, dlog, row_loss);
+void softmax_ce(const CeGroup<T>& G, cudaStream_t s) {
+  if (G.rows <= 0 || G.n <= 0) return;
+  k_softmax_ce<T><<<dim3((unsigned)cdiv(G.rows, 8), (unsigned)G.n), 256, 0, s>>>(G);
 }
-template void softmax_ce<float>(const float*, int64_t, int, int, const int32_t*, const uint8_t*, const int64_t*,
-                                float*, float*, cudaStream_t);
-template void softmax_ce<bf16>(const float*, int64_t, int, int, const int32_t*, const uint8_t*, const int64_t*,
-                               bf16*, float*, cudaStream_t);
+template void softmax_ce<float>(const CeGroup<float>&, cudaStream_t);
+template void softmax_ce<bf16>(const CeGroup<bf16>&, cudaStream_t);
 
-__global__ void __launch_bounds__(1024) k_reduce_loss(const float* __restrict__ row_loss, int nb,
-                                                      const int64_t* __restrict__ stats, float* __restrict__ step_loss,
-                                                      float* __restrict__ loss_acc) {
+// one CTA per slot, fixed-order tree: deterministic
+template <typename T>
+__global__ void __launch_bounds__(1024) k_reduce_loss(const __grid_constant__ CeGroup<T> G) {
+  const CeSlot<T>& S = G.s[blockIdx.x];
   using Red = cub::BlockReduce<float, 1024>;
   __shared__ typename Red::TempStorage tr;
   float acc = 0.f;
-  for (int v = threadIdx.x; v < nb; v += 1024) acc += row_loss[v];
+  for (int v = threadIdx.x; v < G.rows; v += 1024) acc += S.row_loss[v];
   const float tot = Red(tr).Sum(acc);
   if (threadIdx.x == 0) {
-    const int64_t nt = stats[1];
+    const int64_t nt = S.stats[1];
     const float l = nt > 0 ? tot / (float)nt : 0.f;
-    step_loss[0] = l;
-    loss_acc[0] += l;
+    S.step_loss[0] = l;
+    S.loss_acc[0] += l;
   }
 }
-void reduce_loss(const float* row_loss, int nb, const int64_t* stats, float* step_loss, float* loss_acc,
-                 cudaStream_t s) {
-  k_reduce_loss<<<1, 1024, 0, s>>>(row_loss, nb, stats, step_loss, loss_acc);
+template <typename T>
+void reduce_loss(const CeGroup<T>& G, cudaStream_t s) {
+  if (G.n <= 0) return;
+  k_reduce_loss<T><<<(unsigned)G.n, 1024, 0, s>>>(G);
 }
+template void reduce_loss<float>(const CeGroup<float>&, cudaStream_t);
+template void reduce_loss<bf16>(const CeGroup<bf16>&, cudaStream_t);
 
 // Adam, PyTorch form (R8): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
-// w -= (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps).  Optionally refreshes the bf16 shadow.
+// w -= (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps), bc_i = 1 - b_i^t, t from the device
+// step state (so the launch is identical every step).  Optionally refreshes the bf16 shadow.
 __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float* __restrict__ M,
-                       float* __restrict__ V, int64_t n, float lr, float b1, float b2, float eps, float bc1,
-                       float bc2_sqrt, bf16* __restrict__ Wb) {
+                       float* __restrict__ V, int64_t n, float b1, float b2, float eps,
+                       const StepState* __restrict__ st, bf16* __restrict__ Wb) {
+  __shared__ float s_step, s_bc2;
+  if (threadIdx.x == 0) {
+    const double t = (double)(st->t + 1);
+    s_step = st->lr / (float)(1.0 - pow((double)b1, t));
+    s_bc2 = sqrtf((float)(1.0 - pow((double)b2, t)));
+  }
+  __syncthreads();
+  const float step = s_step, bc2_sqrt = s_bc2;
   const int64_t n4 = n >> 2;
-  const float step = lr / bc1;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 w = reinterpret_cast<float4*>(W)[i];
     const float4 g = reinterpret_cast<const float4*>(G)[i];
@@ -99,25 +109,33 @@ __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float
     }
   }
 }
-void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float lr, float b1, float b2, float eps,
-               float bc1, float bc2_sqrt, bf16* Wb, cudaStream_t s) {
+void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
+               const StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n >> 2, 256) < 148 * 8 ? cdiv(n >> 2, 256) : 148 * 8;
-  k_adam<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(W, G, M, V, n, lr, b1, b2, eps, bc1, bc2_sqrt, Wb);
+  k_adam<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(W, G, M, V, n, b1, b2, eps, st, Wb);
 }
 
-__global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, float lr, bf16* __restrict__ Wb) {
+__global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, const StepState* st,
+                      bf16* __restrict__ Wb) {
+  const float lr = st->lr;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float w = W[i] - lr * G[i];
     W[i] = w;
     if (Wb) Wb[i] = __float2bfloat16_rn(w);
   }
 }
-void sgd_step(float* W, const float* G, int64_t n, float lr, bf16* Wb, cudaStream_t s) {
+void sgd_step(float* W, const float* G, int64_t n, const StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
-  k_sgd<<<(unsigned)blocks, 256, 0, s>>>(W, G, n, lr, Wb);
+  k_sgd<<<(unsigned)blocks, 256, 0, s>>>(W, G, n, st, Wb);
 }
+
+__global__ void k_step_advance(StepState* st) {
+  st->z += 1;
+  st->t += 1;
+}
+void step_advance(StepState* st, cudaStream_t s) { k_step_advance<<<1, 1, 0, s>>>(st); }
 
 __global__ void k_f32_to_bf16(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
