@@ -4,6 +4,7 @@
 // file only sequences launches, owns device memory and streams, and computes
 // the (tiny, integer) per-step batch schedule on the host (R7).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -99,7 +100,7 @@ struct gist_ctx {
   float* full_scale = nullptr;
   std::vector<int32_t> perm_h;  // new id -> original id
   std::vector<int64_t> cstart_h, cvol_h;  // cluster offsets (new ids) / cluster volumes (sum of degrees)
-  int nb_max = 0;
+  int nb_max = 0, max_csize = 0;
   int64_t nnzb_max = 0;
   // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
   std::vector<float*> theta;
@@ -499,6 +500,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
     for (int j = 0; j < c->cfg.clusters_per_batch; ++j) a += sz[j], b += vol[j];
     c->nb_max = (int)a;
     c->nnzb_max = b;
+    c->max_csize = (int)sz[0];
   }
   cudaStream_t s = c->stream;
   // device copies of the original CSR, then relabel on the device
@@ -738,6 +740,10 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
   const bool sage = c->arch == GIST_ARCH_SAGE;
   const bool tc = c->prec == GIST_PREC_BF16;
+  // GIST_SPMM_SLAB=1 enables the cluster-slab SpMM (measured slower than the L2 row gather
+  // on Reddit-shape batches: issue-bound, profiles/r01*_ncu_spmm_ct.txt); default off
+  const char* slab_env = std::getenv("GIST_SPMM_SLAB");
+  const int slab_max = (slab_env && slab_env[0] == '1') ? c->max_csize : 0;
   for (int g0 = 0; g0 < (int)c->slots.size(); g0 += kMaxGroup) {
     typename StepPlan<T>::Group g;
     g.first = g0;
@@ -781,6 +787,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         // forward aggregation (a2)
         SpmmArgs<T, T>& a = g.fwd_spmm[l].a[j];
         a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
+        a.desc = sl.desc_dev; a.st = c->dstate; a.q = q; a.max_cluster = slab_max;  // cluster slabs
         if (sage) {
           a.rowscale = sl.scale;               // N = D^-1 A (R2)
           a.out = C + sh.half; a.ldo = sh.Kp;   // right half: N H
@@ -820,6 +827,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
           SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
           b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
+          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q; b.max_cluster = slab_max;
           b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
           if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
             b.colscale = sl.scale; b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;

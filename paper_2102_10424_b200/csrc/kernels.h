@@ -15,6 +15,7 @@ using bf16 = __nv_bfloat16;
 // where h(u) = h_index ? h_index[u] : u.  Optionally copies H[h(v)] to self_out[v]
 // (GraphSAGE concat [H || N H], R2).  Widths are padded to multiples of 8.
 // --------------------------------------------------------------------------
+struct StepState;
 template <typename TI, typename TO = TI>
 struct SpmmArgs {
   const int64_t* row_beg = nullptr;  // row v's neighbours are col[row_beg[v] .. row_end[v])
@@ -37,6 +38,14 @@ struct SpmmArgs {
   TI* self_out = nullptr;
   int64_t ld_self = 0;
   int64_t w = 0;  // padded width processed (multiple of 8)
+  // Cluster-slab staging (batch SpMMs only): rows of each batch cluster are a contiguous
+  // local-id range loff[k]..loff[k+1] (from the step descriptor).  When set, one CTA stages
+  // cluster k's rows of H (a column tile) in shared memory and serves intra-cluster
+  // neighbours from it.  max_cluster = largest cluster (rows), bounds the slab.
+  const int32_t* desc = nullptr;
+  const StepState* st = nullptr;
+  int q = 0;
+  int max_cluster = 0;
 };
 template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
 
