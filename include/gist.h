@@ -180,6 +180,14 @@ enum {
 gist_status gist_profile(gist_ctx* ctx, int32_t stride);
 gist_status gist_profile_get(gist_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* work);
 
+/* Sharding layout of the sub-GCN slots (host-only, no device needed; §6 of DESIGN.md):
+ * slot i lives on rank gist_slot_owner(i, W) = i mod W as that rank's local slot i / W;
+ * every rank contributes gist_slots_per_rank(m, W) = ceil(m / W) equal-size packed slot
+ * buffers to the subAgg all-gather, so the gathered buffer of rank r, local slot j is
+ * global slot r + W * j (ignored when >= m). */
+int32_t gist_slot_owner(int32_t slot, int32_t world_size);
+int32_t gist_slots_per_rank(int32_t m, int32_t world_size);
+
 /* cudaStream_t of the context (for timing with CUDA events on the launching stream). */
 void* gist_stream(gist_ctx* ctx);
 

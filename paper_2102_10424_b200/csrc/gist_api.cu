@@ -322,6 +322,13 @@ extern "C" const char* gist_status_str(gist_status s) {
 
 extern "C" const char* gist_last_error(const gist_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+extern "C" int32_t gist_slot_owner(int32_t slot, int32_t world_size) {
+  return world_size > 0 && slot >= 0 ? slot % world_size : -1;
+}
+extern "C" int32_t gist_slots_per_rank(int32_t m, int32_t world_size) {
+  return world_size > 0 && m > 0 ? (m + world_size - 1) / world_size : 0;
+}
+
 extern "C" gist_status gist_nccl_unique_id(void* out128) {
   if (!out128) return GIST_E_ARG;
   ncclUniqueId id;
@@ -640,7 +647,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
   c->Wall = c->Gall = c->Mall = c->Vall = c->Wrecv = nullptr;
   c->Wball = nullptr;
   const int W = c->cfg.world_size, r = c->cfg.rank;
-  c->slots_per_rank = (m + W - 1) / W;
+  c->slots_per_rank = gist_slots_per_rank(m, W);
   // largest packed slot (every hidden block at ceil(d/m))
   int64_t smax = 0;
   std::vector<int> maxK(c->L), maxN(c->L);
@@ -1178,7 +1185,7 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
     src = c->Wrecv;
   }
   for (int i = 0; i < c->m; ++i) {
-    const int rank = i % W, j = i / W;
+    const int rank = gist_slot_owner(i, W), j = i / W;
     const float* w = src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
     if (W == 1) w = c->Wall + (size_t)j * c->S_max;
     for (int l = 0; l < c->L; ++l) {

@@ -27,7 +27,7 @@ EXPORTS = [
     "gist_subtrain", "gist_aggregate", "gist_eval", "gist_get_params", "gist_set_params",
     "gist_get_partition", "gist_sub_shape", "gist_get_sub_params", "gist_get_trace", "gist_stat",
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
-    "gist_profile", "gist_profile_get", "gist_nccl_unique_id",
+    "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
 ]
 PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate"]
 
@@ -79,6 +79,8 @@ def lib() -> C.CDLL:
         "gist_gemm": (i32, [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, vp]),
         "gist_profile": (i32, [vp, i32]),
         "gist_nccl_unique_id": (i32, [vp]),
+        "gist_slot_owner": (i32, [i32, i32]),
+        "gist_slots_per_rank": (i32, [i32, i32]),
         "gist_profile_get": (i32, [vp, i32, P(C.c_double), P(i64), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
@@ -234,6 +236,19 @@ class Gist:
             self._check(lib().gist_profile_get(self.h, k, C.byref(ms), C.byref(n), C.byref(w)))
             out[name] = {"ms": ms.value, "launches": n.value, "work": w.value}
         return out
+
+
+def slot_owner(slot: int, world: int) -> int:
+    """Rank owning sub-GCN slot `slot` (host-only, from the library)."""
+    return int(lib().gist_slot_owner(slot, world))
+
+
+def slots_per_rank(m: int, world: int) -> int:
+    return int(lib().gist_slots_per_rank(m, world))
+
+
+def local_slots(m: int, world: int, rank: int) -> list:
+    return [i for i in range(m) if slot_owner(i, world) == rank]
 
 
 def nccl_unique_id() -> bytes:

@@ -1,0 +1,136 @@
+"""Multi-process (world_size 2, gloo, CPU) coverage of the N>1 subAgg protocol
+(PAPER.md:140, 169, 185-190):
+  * slot i lives on rank gist_slot_owner(i, W) (the library's own layout functions);
+  * every rank derives the same partition from the counter-based PRNG (no exchange);
+  * one all-gather of equal-size packed slot buffers per round, then every rank writes
+    all m blocks into its replica.
+The sub-GCN arithmetic runs in the FP64 oracle here (the test engine); the transport is
+torch.distributed gloo.  Property: the global Theta after every round is bit-identical to
+the single-process run and across ranks (world-size invariance)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import gist_oracle as O
+from synth.planted import generate, tiny_spec
+
+DIMS = (12, 20, 15, 4)
+M, ROUNDS, ZETA = 3, 2, 3
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def make():
+    g = generate(tiny_spec(n=240, nnz=1500, d0=12, classes=4, clusters=8), seed=3)
+    o = O.OracleGIST(arch="sage", dims=list(DIMS), optimizer="adam", clusters_per_batch=2, batch_seed=9)
+    o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
+                 g["cluster_ids"], g["num_clusters"])
+    o.init_params(5)
+    return o
+
+
+def pack(subs, slots, spr, smax):
+    buf = np.zeros(spr * smax)
+    for j, i in enumerate(slots):
+        flat = np.concatenate([w.ravel() for w in subs[i]])
+        buf[j * smax: j * smax + len(flat)] = flat
+    return buf
+
+
+def unpack(flat, shapes):
+    out, off = [], 0
+    for s in shapes:
+        n = s[0] * s[1]
+        out.append(flat[off: off + n].reshape(s))
+        off += n
+    return out
+
+
+def sharded_run(rank, world):
+    from paper_2102_10424_b200 import gist
+    o = make()
+    spr = gist.slots_per_rank(M, world)
+    mine = gist.local_slots(M, world, rank)
+    history = []
+    for t in range(ROUNDS):
+        o.partition(seed=77, m=M)                     # identical on every rank (Philox, no exchange)
+        shapes = [[w.shape for w in o.sub[i]] for i in range(M)]
+        smax = max(sum(a * b for a, b in s) for s in shapes)
+        for i in mine:                                # subTrain only the local slots
+            for z in range(ZETA):
+                o.train_step(i, o.step + z, 0.01)
+        o.step += ZETA
+        send = torch.from_numpy(pack(o.sub, mine, spr, smax))
+        recv = [torch.zeros_like(send) for _ in range(world)]
+        dist.all_gather(recv, send)                   # the one exchange of the round
+        for r in range(world):
+            for j in range(spr):
+                i = r + world * j
+                if i >= M:
+                    continue
+                assert gist.slot_owner(i, world) == r
+                o.sub[i] = unpack(recv[r].numpy()[j * smax:(j + 1) * smax], shapes[i])
+        o.aggregate()
+        history.append([w.copy() for w in o.theta])
+    return history
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hist = sharded_run(rank, world)
+        q.put((rank, [[w.tobytes() for w in th] for th in hist]))
+    finally:
+        dist.destroy_process_group()
+
+
+def reference():
+    o = make()
+    hist = []
+    for t in range(ROUNDS):
+        o.partition(seed=77, m=M)
+        o.subtrain(ZETA, 0.01)
+        o.aggregate()
+        hist.append([w.copy() for w in o.theta])
+    return hist
+
+
+def test_layout_functions():
+    from paper_2102_10424_b200 import gist
+    for m in (1, 2, 3, 8, 13):
+        for W in (1, 2, 4, 8):
+            owners = [gist.slot_owner(i, W) for i in range(m)]
+            assert owners == [i % W for i in range(m)]
+            assert gist.slots_per_rank(m, W) == -(-m // W)
+            assert sorted(sum((gist.local_slots(m, W, r) for r in range(W)), [])) == list(range(m))
+
+
+@pytest.mark.timeout(300)
+def test_world2_gloo_bit_identical_to_world1():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = reference()
+    for t in range(ROUNDS):
+        for l in range(len(DIMS) - 1):
+            want = ref[t][l].tobytes()
+            assert res[0][t][l] == want and res[1][t][l] == want, (t, l)
