@@ -232,6 +232,8 @@ def main():
     prof = gx.profile_get()
     gx.profile(0)
     nb_last = gx.stat(G.STAT_LAST_NB)
+    block_agg = gx.stat(G.STAT_BLOCK_AGG)
+    block_density = gx.stat(G.STAT_BLOCK_DENSITY_PPM) / 1e6
     nnzb_last = gx.stat(G.STAT_LAST_NNZ_B)
     total_ms = float(sum(times))
     if world > 1:
@@ -275,7 +277,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{args.precision}:{dom}")
-    if dom == "gemm":
+    if dom in ("gemm", "agg_tc"):
         if args.precision == "bf16":
             roof = {"bound": "tensor", "peak": pk["bf16_sustained"] or pk["bf16"], "unit": "TFLOP/s",
                     "peak_src": f"{pk['src']} bf16 sustained"}
@@ -301,7 +303,8 @@ def main():
                    "steps of all m sub-GCNs + aggregate)", "parallelism": f"gist-m{spec.m}-over-{world}gpu",
                    "precision": args.precision, "l2": "256 MiB buffer written between timed rounds",
                    "epoch_s": spec.m * B / value, "batches_per_epoch": B, "last_n_b": nb_last,
-                   "last_nnz_b": nnzb_last, "gen_s": t_gen, "profile_stride": args.profile_stride},
+                   "last_nnz_b": nnzb_last, "gen_s": t_gen, "profile_stride": args.profile_stride,
+                   "block_agg": bool(block_agg), "block_density": block_density},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "roofline": roof,

@@ -162,7 +162,8 @@ gist_status gist_get_trace(gist_ctx* ctx, int32_t slot, int32_t what, int32_t la
 enum {
   GIST_STAT_ROUND = 0, GIST_STAT_STEP = 1, GIST_STAT_SELF_LOOPS_DROPPED = 2, GIST_STAT_LAST_NNZ_B = 3,
   GIST_STAT_LAST_NB = 4, GIST_STAT_KERNELS = 5, GIST_STAT_H2D_BYTES = 6, GIST_STAT_D2H_BYTES = 7,
-  GIST_STAT_MAX_NB = 8
+  GIST_STAT_MAX_NB = 8, GIST_STAT_BLOCK_AGG = 9 /* 1 if block-diagonal tensor-core aggregation is on */,
+  GIST_STAT_BLOCK_DENSITY_PPM = 10 /* intra-cluster block density x 1e6 */
 };
 int64_t gist_stat(gist_ctx* ctx, int32_t which);
 
@@ -175,7 +176,9 @@ int64_t gist_stat(gist_ctx* ctx, int32_t which);
  * bytes for the others: every operand read once, every output written once). */
 enum {
   GIST_PROF_BATCH = 0, GIST_PROF_SPMM = 1, GIST_PROF_GEMM = 2, GIST_PROF_LOSS = 3, GIST_PROF_OPTIM = 4,
-  GIST_PROF_PARTITION = 5, GIST_PROF_AGGREGATE = 6, GIST_PROF_N = 7
+  GIST_PROF_PARTITION = 5, GIST_PROF_AGGREGATE = 6,
+  GIST_PROF_AGG_TC = 7, /* block-diagonal (intra-cluster) aggregation on tensor cores; work = FLOPs */
+  GIST_PROF_N = 8
 };
 gist_status gist_profile(gist_ctx* ctx, int32_t stride);
 gist_status gist_profile_get(gist_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* work);

@@ -91,9 +91,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+template <int BN, int ST = (BN == 256 ? 4 : 6)>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = ST;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -101,24 +101,34 @@ struct Cfg {
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU, bool MASK>
-__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ GemmGroupTC G) {
-  using CF = Cfg<BN>;
-  const GemmSlotTC& S = G.s[blockIdx.z];  // one sub-GCN slot per grid layer
-  const int M = S.M, N = S.N, K = S.K;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= M || n0 >= N) return;         // slots may be smaller than the grid (uniform exit)
-  const CUtensorMap* mapA = &S.ma;
-  const CUtensorMap* mapB = &S.mb;
-  void* Cout = S.C;
-  const int64_t ldc = S.ldc;
+// Epilogue options (runtime, warp-uniform): ReLU, ReLU-mask of the layer below, a per-row
+// scale on columns >= rs_from, an added bf16 matrix.
+struct Epi {
+  void* C;
+  int64_t ldc;
+  int relu;
+  const bf16* mask;
+  int64_t ldm;
+  const float* rscale;
+  int rs_from;
+  const bf16* add;
+  int64_t ldadd;
+};
+
+// Shared mainloop + epilogue of both kernels.  The tile's A rows / B columns start at
+// (a_row, b_col); K runs over [0, K) with the B operand's K coordinate offset by b_k0.
+// Output rows out_row0 + r for r < rows_valid, columns n0 + c for c < N - n0.
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
+__device__ __forceinline__ void gemm_tile(const CUtensorMap* mapA, const CUtensorMap* mapB, int a_row, int b_col,
+                                          int b_k0, int K, int out_row0, int rows_valid, int n0, int N,
+                                          const Epi& E) {
+  using CF = Cfg<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE_BYTES);
   uint64_t* empty = full + CF::STAGES;
   uint64_t* accf = empty + CF::STAGES;
   uint32_t* tmem_slot = (uint32_t*)(accf + 1);
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (K + BK - 1) / BK;
 
@@ -153,16 +163,16 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
       mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
       const int k0 = kb * BK;
       if (!A_MN) {
-        tma_load_2d(sa, mapA, &full[s], k0, m0);
+        tma_load_2d(sa, mapA, &full[s], k0, a_row);
       } else {
 #pragma unroll
-        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, mapA, &full[s], m0 + 64 * j, k0);
+        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, mapA, &full[s], a_row + 64 * j, k0);
       }
       if (!B_MN) {
-        tma_load_2d(sb, mapB, &full[s], k0, n0);
+        tma_load_2d(sb, mapB, &full[s], b_k0 + k0, b_col);
       } else {
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, mapB, &full[s], n0 + 64 * j, k0);
+        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, mapB, &full[s], b_col + 64 * j, b_k0 + k0);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -191,38 +201,65 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
   // ------------------------------------------------------------ epilogue (all 4 warps)
   mbar_wait(accf, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + warp * 32 + lane;
+  const int r = warp * 32 + lane;
+  const int64_t row = (int64_t)out_row0 + r;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
   for (int c = 0; c < BN; c += 16) {
     float v[16];
     tmem_ld16(trow + c, v);
-    if (row < M && n0 + c < N) {
-      if (RELU) {
+    const int col = n0 + c;
+    if (r < rows_valid && col < N) {
+      if (E.rscale) {  // per-row scale of the columns >= rs_from
+        const float sc = E.rscale[row];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (col + i >= E.rs_from) v[i] *= sc;
+      }
+      const bool full16 = col + 16 <= N;
+      if (E.add) {
+        const bf16* ap = E.add + row * E.ldadd + col;
+        if (full16 && ((((uintptr_t)ap) & 15) == 0)) {
+          float t[16];
+          ld16(ap, t);
+          ld16(ap + 8, t + 8);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += t[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < N) v[i] += __bfloat162float(ap[i]);
+        }
+      }
+      if (E.relu) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
       }
-      const int col = n0 + c;
-      if (MASK) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
-        const bf16* mp = (const bf16*)S.mask + (int64_t)row * S.ldm + col;
+      if (E.mask) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
+        const bf16* mp = E.mask + row * E.ldm + col;
+#pragma unroll
         for (int i = 0; i < 16; ++i)
           if (col + i < N && !(__bfloat162float(mp[i]) > 0.f)) v[i] = 0.f;
       }
       if (OUT_F32) {
-        float* dst = (float*)Cout + (int64_t)row * ldc + col;
-        if (col + 16 <= N && (((uintptr_t)dst & 15) == 0)) {
+        float* dst = (float*)E.C + row * E.ldc + col;
+        if (full16 && (((uintptr_t)dst & 15) == 0)) {
 #pragma unroll
           for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         } else {
-          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = v[i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < N) dst[i] = v[i];
         }
       } else {
-        bf16* dst = (bf16*)Cout + (int64_t)row * ldc + col;
-        if (col + 16 <= N && (((uintptr_t)dst & 15) == 0)) {
+        bf16* dst = (bf16*)E.C + row * E.ldc + col;
+        if (full16 && (((uintptr_t)dst & 15) == 0)) {
           st16(dst, v);
           st16(dst + 8, v + 8);
         } else {
-          for (int i = 0; i < 16 && col + i < N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
         }
       }
     }
@@ -233,6 +270,39 @@ __global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ Gemm
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
   }
+}
+
+// Plain grouped GEMM: grid (N tiles, M tiles, slots).
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
+__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ GemmGroupTC G) {
+  const GemmSlotTC& S = G.s[blockIdx.z];
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= S.M || n0 >= S.N) return;  // slots may be smaller than the grid (uniform exit)
+  const Epi E{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0};
+  gemm_tile<BN, ST, A_MN, B_MN, OUT_F32>(&S.ma, &S.mb, m0, n0, 0, S.K, m0, S.M - m0, n0, S.N, E);
+}
+
+// Block-diagonal aggregation (SAGE, Cluster batches): for batch cluster k of slot z,
+//   out[loff_k + r, :] = epi( sum_j A_c[r, j] * H[h0 + j, :] ),  r < |cluster|,
+// A_c = the cluster's binary intra-cluster adjacency block (bf16, BS x BS, precomputed at
+// load), h0 = loff_k (batch-local rows) or cstart[c] (global feature rows, layer 0).
+// grid (N tiles, q * M tiles per block, slots); cluster ids / offsets from the step state.
+template <int BN, int ST>
+__global__ void __launch_bounds__(128, 1) k_gemm_bd(const __grid_constant__ BdGroup G) {
+  const BdSlot& S = G.s[blockIdx.z];
+  const int q = G.q;
+  const int mt_per = (G.bs + BM - 1) / BM;
+  const int k = blockIdx.y / mt_per, mt = blockIdx.y % mt_per;
+  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+  if (k >= d[3 * q + 2]) return;
+  const int c = d[k], r0 = d[q + k], size = d[q + k + 1] - r0;
+  if (mt * BM >= size) return;
+  const int n0 = blockIdx.x * BN;
+  if (n0 >= S.N) return;
+  const int h0 = S.global_rows ? (int)G.cstart[c] : r0;
+  const Epi E{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd};
+  gemm_tile<BN, ST, false, true, false>(&G.ma, &S.mb, c * G.bs + mt * BM, n0, h0, G.bs, r0 + mt * BM, size - mt * BM, n0,
+                                    S.N, E);
 }
 
 // ------------------------------------------------------------------ host side
@@ -267,31 +337,25 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool OUT_F32, bool RELU, bool MASK>
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
 void launch_tc(const GemmPlanTC& P, cudaStream_t s) {
-  auto kern = k_gemm_tc<BN, A_MN, B_MN, OUT_F32, RELU, MASK>;
+  auto kern = k_gemm_tc<BN, ST, A_MN, B_MN, OUT_F32>;
   static bool attr = false;  // per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, ST>::SMEM);
     attr = true;
   }
   dim3 grid((unsigned)cdiv(P.maxN, BN), (unsigned)cdiv(P.maxM, BM), (unsigned)P.G.n);
-  kern<<<grid, 128, Cfg<BN>::SMEM, s>>>(P.G);
+  kern<<<grid, 128, Cfg<BN, ST>::SMEM, s>>>(P.G);
 }
 
+// Stage count: big single GEMMs keep the deep ring (1 CTA/SM); grouped step GEMMs use a
+// 3-stage ring at BN=128 (2 CTAs/SM, so one CTA's epilogue overlaps another's mainloop).
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
-  const int e = (P.out_f32 ? 4 : 0) | (P.relu ? 2 : 0) | (P.mask ? 1 : 0);
-  switch (e) {
-    case 0: launch_tc<BN, A_MN, B_MN, false, false, false>(P, s); break;
-    case 1: launch_tc<BN, A_MN, B_MN, false, false, true>(P, s); break;
-    case 2: launch_tc<BN, A_MN, B_MN, false, true, false>(P, s); break;
-    case 3: launch_tc<BN, A_MN, B_MN, false, true, true>(P, s); break;
-    case 4: launch_tc<BN, A_MN, B_MN, true, false, false>(P, s); break;
-    case 5: launch_tc<BN, A_MN, B_MN, true, false, true>(P, s); break;
-    case 6: launch_tc<BN, A_MN, B_MN, true, true, false>(P, s); break;
-    default: launch_tc<BN, A_MN, B_MN, true, true, true>(P, s); break;
-  }
+  constexpr int ST = BN == 256 ? 4 : 3;
+  if (P.out_f32) launch_tc<BN, ST, A_MN, B_MN, true>(P, s);
+  else launch_tc<BN, ST, A_MN, B_MN, false>(P, s);
 }
 
 template <int BNV>
@@ -300,6 +364,20 @@ void dispatch_layout(const GemmPlanTC& P, cudaStream_t s) {
   else if (!P.a_mn && !P.b_mn) dispatch_epi<BNV, false, false>(P, s);
   else if (P.a_mn && P.b_mn) dispatch_epi<BNV, true, true>(P, s);
   else dispatch_epi<BNV, true, false>(P, s);
+}
+
+template <int BN>
+void launch_bd(const BdPlan& P, cudaStream_t s) {
+  constexpr int ST = 2;  // K = cluster block size (<= 256): a short ring, 2+ CTAs per SM
+  auto kern = k_gemm_bd<BN, ST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, ST>::SMEM);
+    attr = true;
+  }
+  const int mt_per = (P.G.bs + BM - 1) / BM;
+  dim3 grid((unsigned)cdiv(P.maxN, BN), (unsigned)(P.G.q * mt_per), (unsigned)P.G.n);
+  kern<<<grid, 128, Cfg<BN, ST>::SMEM, s>>>(P.G);
 }
 
 }  // namespace
@@ -313,15 +391,17 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
   P->relu = o0.relu;
   P->mask = o0.mask != nullptr;
   P->maxM = P->maxN = 0;
-  int64_t maxN = 0;
-  for (int i = 0; i < n; ++i) maxN = ops[i].N > maxN ? ops[i].N : maxN;
-  P->bn = maxN > 128 ? 256 : 128;
+  int64_t maxN = 0, maxM = 0;
+  for (int i = 0; i < n; ++i) {
+    maxN = ops[i].N > maxN ? ops[i].N : maxN;
+    maxM = ops[i].M > maxM ? ops[i].M : maxM;
+  }
+  // wide tiles only when one GEMM alone has enough tiles to fill the GPU
+  P->bn = (maxN > 128 && n == 1 && cdiv(maxM, BM) * cdiv(maxN, 256) >= 148) ? 256 : 128;
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
     const GemmOp& o = ops[i];
-    if (o.transA != o0.transA || o.transB != o0.transB || o.out_f32 != o0.out_f32 || o.relu != o0.relu ||
-        (o.mask != nullptr) != P->mask)
-      return false;
+    if (o.transA != o0.transA || o.transB != o0.transB || o.out_f32 != o0.out_f32) return false;
     if (o.K <= 0 || ((uintptr_t)o.A & 15) || ((uintptr_t)o.B & 15) || (o.lda % 8) || (o.ldb % 8)) return false;
     GemmSlotTC& S = P->G.s[i];
     bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, 64, 64) : make_map(&S.ma, o.A, o.K, o.M, o.lda, 64, BM);
@@ -332,6 +412,9 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.ldc = o.ldc;
     S.mask = o.mask;
     S.ldm = o.ldm;
+    S.relu = o.relu ? 1 : 0;
+    S.rscale = o.rscale;
+    S.rs_from = o.rs_from;
     S.M = (int)o.M;
     S.N = (int)o.N;
     S.K = (int)o.K;
@@ -347,11 +430,47 @@ void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
   else dispatch_layout<128>(P, s);
 }
 
+bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q,
+                     const int64_t* cstart, const StepState* st, BdPlan* P) {
+  if (!get_encode() || n < 1 || n > kMaxGroup || (bs % 8)) return false;
+  if (!make_map(&P->G.ma, blocks, bs, (int64_t)num_clusters * bs, bs, 64, BM)) return false;
+  P->G.n = n;
+  P->G.q = q;
+  P->G.bs = bs;
+  P->G.st = st;
+  P->G.cstart = cstart;
+  P->maxN = 0;
+  for (int i = 0; i < n; ++i) {
+    const BdOp& o = ops[i];
+    BdSlot& S = P->G.s[i];
+    if (((uintptr_t)o.H & 15) || (o.ldh % 8)) return false;
+    // H stored [rows x N] (N contiguous): MN-major B operand, K = rows
+    if (!make_map(&S.mb, o.H, o.N, o.h_rows, o.ldh, 64, 64)) return false;
+    S.C = o.C;
+    S.ldc = o.ldc;
+    S.add = o.add;
+    S.ldadd = o.ldadd;
+    S.rscale = o.rscale;
+    S.desc = o.desc;
+    S.global_rows = o.global_rows;
+    S.N = (int)o.N;
+    P->maxN = o.N > P->maxN ? o.N : P->maxN;
+  }
+  P->bn = 128;
+  return true;
+}
+
+void gemm_bd_launch(const BdPlan& P, cudaStream_t s) {
+  if (P.G.n <= 0 || P.maxN <= 0) return;
+  if (P.bn == 256) launch_bd<256>(P, s);
+  else launch_bd<128>(P, s);
+}
+
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda, const bf16* B,
                int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s) {
   if (!get_encode()) return false;
   if (M == 0 || N == 0) return true;  // nothing to do (also the availability probe)
-  GemmOp o{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, out_f32, relu, nullptr, 0};
+  GemmOp o{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, out_f32, relu, nullptr, 0, nullptr, 0};
   GemmPlanTC P;
   if (!gemm_bf16_prepare(&o, 1, &P)) return false;
   gemm_bf16_launch(P, s);

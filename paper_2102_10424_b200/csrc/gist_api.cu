@@ -71,6 +71,8 @@ struct StepPlan {
     std::vector<SgemmGroup> fwd_f, dw_f, dx_f;        // FP32 mode
     std::vector<double> fwd_fl, dw_fl, dx_fl;         // algorithmic FLOPs (profiling)
     std::vector<double> fwd_by, bwd_by;               // SpMM compulsory bytes excl. nnz part (profiling)
+    std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
+    std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
     CeGroup<T> ce;
   };
   std::vector<Group> groups;
@@ -102,6 +104,11 @@ struct gist_ctx {
   std::vector<int64_t> cstart_h, cvol_h;  // cluster offsets (new ids) / cluster volumes (sum of degrees)
   int nb_max = 0, max_csize = 0;
   int64_t nnzb_max = 0;
+  // block-diagonal tensor-core aggregation (SAGE, BF16): binary intra-cluster blocks
+  bf16* blocks = nullptr;
+  int bs = 0;
+  bool bd = false;
+  double block_density = 0.0;
   // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
   std::vector<float*> theta;
   std::vector<int64_t> th_K, th_N;
@@ -437,6 +444,8 @@ extern "C" int64_t gist_stat(gist_ctx* c, int32_t which) {
     case GIST_STAT_H2D_BYTES: return c->h2d;
     case GIST_STAT_D2H_BYTES: return c->d2h;
     case GIST_STAT_MAX_NB: return c->nb_max;
+    case GIST_STAT_BLOCK_AGG: return c->bd ? 1 : 0;
+    case GIST_STAT_BLOCK_DENSITY_PPM: return (int64_t)(c->block_density * 1e6);
   }
   return -1;
 }
@@ -453,13 +462,16 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   if (num_clusters < 1 || num_clusters > n) return fail(c, GIST_E_ARG, "load_graph: bad num_clusters");
   if (c->cfg.clusters_per_batch > num_clusters) return fail(c, GIST_E_ARG, "load_graph: q > num_clusters");
   if (row_ptr[0] != 0 || row_ptr[n] != nnz) return fail(c, GIST_E_ARG, "load_graph: row_ptr[0]/row_ptr[n] mismatch");
-  int64_t self = 0;
+  int64_t self = 0, intra = 0;
   for (int64_t v = 0; v < n; ++v) {
     if (row_ptr[v + 1] < row_ptr[v]) return fail(c, GIST_E_ARG, "load_graph: row_ptr decreasing");
+    if (cluster_ids[v] < 0 || cluster_ids[v] >= num_clusters)
+      return fail(c, GIST_E_ARG, "load_graph: cluster id out of range");
     for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
       const int32_t u = col_idx[e];
       if (u < 0 || u >= n) return fail(c, GIST_E_ARG, "load_graph: col_idx out of range");
       self += (u == v);
+      if (u != v && cluster_ids[u] == cluster_ids[v]) ++intra;
     }
     if (labels[v] < 0 || labels[v] >= num_classes) return fail(c, GIST_E_ARG, "load_graph: label out of range");
     if (split[v] > 3) return fail(c, GIST_E_ARG, "load_graph: split code > 3");
@@ -508,6 +520,9 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
     c->nb_max = (int)a;
     c->nnzb_max = b;
     c->max_csize = (int)sz[0];
+    double sq = 0.0;
+    for (int j = 0; j < num_clusters; ++j) sq += (double)csize[j] * (double)csize[j];
+    c->block_density = sq > 0 ? (double)intra / sq : 0.0;
   }
   cudaStream_t s = c->stream;
   // device copies of the original CSR, then relabel on the device
@@ -562,6 +577,24 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   CK(cudaMemcpyAsync(c->cstart, c->cstart_h.data(), (num_clusters + 1) * 8, cudaMemcpyHostToDevice, s));
   c->h2d += n * 9 + (num_clusters + 1) * 8;
   LK(full_graph_scales(c->rp, n, c->arch, c->full_scale, s));
+  // Block-diagonal tensor-core aggregation: GraphSAGE in BF16 mode when the
+  // clusters are small (<= 256 rows) and their intra-cluster blocks dense enough (>= 5%).
+  // GIST_BD=0/1 overrides the choice.
+  {
+    const char* env = std::getenv("GIST_BD");
+    const int bs = (int)pad8(c->max_csize);
+    const double bytes = (double)num_clusters * bs * bs * 2.0;
+    bool want = c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->max_csize <= 256 &&
+                c->block_density >= 0.05 && bytes <= 8e9;
+    if (env) want = env[0] == '1' && c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->max_csize <= 256;
+    if (want) {
+      c->bs = bs;
+      TRY(dalloc_t(c, &c->blocks, (size_t)num_clusters * bs * bs));
+      CK(cudaMemsetAsync(c->blocks, 0, (size_t)num_clusters * bs * bs * 2, s));
+      LK(cluster_blocks(c->rp, c->col, c->cid, c->cstart, n, bs, c->blocks, s));
+      c->bd = true;
+    }
+  }
   CK(cudaStreamSynchronize(s));
   TRY(check_launch(c, "load_graph"));
   dfree(c, rp_o);
@@ -772,12 +805,17 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.dx_fl.assign(L, 0.0);
     g.fwd_by.assign(L, 0.0);
     g.bwd_by.assign(L, 0.0);
+    g.fwd_bd.assign(L, BdPlan());
+    g.bwd_bd.assign(L, BdPlan());
+    g.bd_fl.assign(L, 0.0);
+    const bool bd = c->bd && tc && sage;
     g.ce.n = g.count;
     g.ce.rows = nb;
     g.ce.k = c->k;
     g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
     for (int l = 0; l < L; ++l) {
       std::vector<GemmOp> fw, dw, dx;
+      std::vector<BdOp> bfw, bbw;
       for (int j = 0; j < g.count; ++j) {
         Slot& sl = c->slots[g0 + j];
         const auto& shp = c->shapes[sl.index];
@@ -811,32 +849,49 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
           else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
         }
+        if (bd) {  // intra-cluster part on tensor cores, then the sparse kernel adds the rest in place
+          bfw.push_back(BdOp{l == 0 ? (const bf16*)c->X : (const bf16*)C, l == 0 ? pad8(c->dims[0]) : sh.Kp,
+                             l == 0 ? c->n : (int64_t)nb, sh.half, (void*)(C + sh.half), sh.Kp, nullptr, 0,
+                             sl.scale, sl.desc_dev, l == 0 ? 1 : 0});
+          a.add = C + sh.half; a.ld_add = sh.Kp;
+          a.few_nnz = 1;
+          g.bd_fl[l] += 2.0 * q * c->bs * c->bs * sh.half;
+        }
         g.fwd_by[l] += spmm_bytes(a);
         // forward contraction (a3)
         const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
         if (l + 1 < L) {
           void* out = sage ? sl.C[l + 1] : sl.H[l + 1];
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, shp[l + 1].Kp, false, true,
-                              nullptr, 0});
+                              nullptr, 0, nullptr, 0});
         } else {
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false,
-                              nullptr, 0});
+                              nullptr, 0, nullptr, 0});
         }
         g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
         // backward: dW_l = C_l^T dZ_l (fp32 into the packed gradient buffer)
         dw.push_back(GemmOp{true, false, sh.Kp, sh.Np, nb, C, sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
-                            nullptr, 0});
+                            nullptr, 0, nullptr, 0});
         g.dw_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
         if (l > 0) {
           // dC_l = dZ_l W_l^T
+          // (bd: the epilogue pre-scales the neighbour half by 1/deg of the row: N^T = A diag(1/deg))
           dx.push_back(GemmOp{false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false,
-                              nullptr, 0});
+                              nullptr, 0, bd ? sl.scale : nullptr, sh.half});
           g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
           SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
           b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
           b.desc = sl.desc_dev; b.st = c->dstate; b.q = q; b.max_cluster = slab_max;
           b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
-          if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
+          if (sage && bd) {  // dZ_{l-1} = (dC_self + A_blocks dC'_neigh + A_inter dC'_neigh) * 1[H_l > 0]
+            bbw.push_back(BdOp{(const bf16*)sl.dC + sh.half, sh.Kp, (int64_t)nb, sh.half, sl.dZ[l - 1],
+                               shp[l - 1].Np, (const bf16*)sl.dC, sh.Kp, nullptr, sl.desc_dev, 0});
+            b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
+            b.add = (const T*)sl.dZ[l - 1]; b.ld_add = shp[l - 1].Np;
+            b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
+            b.w = sh.half;
+            b.few_nnz = 1;
+          } else if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
             b.colscale = sl.scale; b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
             b.add = (const T*)sl.dC; b.ld_add = sh.Kp;
             b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
@@ -852,6 +907,12 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
       }
       g.fwd_spmm[l].n = g.count;
       g.bwd_spmm[l].n = l > 0 ? g.count : 0;
+      if (bd) {
+        if (!gemm_bd_prepare(c->blocks, c->c, c->bs, bfw.data(), g.count, q, c->cstart, c->dstate, &g.fwd_bd[l]) ||
+            (l > 0 && !gemm_bd_prepare(c->blocks, c->c, c->bs, bbw.data(), g.count, q, c->cstart, c->dstate,
+                                       &g.bwd_bd[l])))
+          return fail(c, GIST_E_UNSUPPORTED, "block-diagonal aggregation plan failed");
+      }
       if (tc) {
         if (!gemm_bf16_prepare(fw.data(), g.count, &g.fwd_tc[l]) ||
             !gemm_bf16_prepare(dw.data(), g.count, &g.dw_tc[l]) ||
@@ -1010,7 +1071,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     int id = -1;
     if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + g.count * c->nb_max_rows * 45.0, 4.0, nnz_slot);
     batch_setup(g.batch, c->cstart, c->rp, s);
-    batch_build(g.batch, c->rp, c->col, c->cid, c->arch, c->labels, c->split, s);
+    batch_build(g.batch, c->rp, c->col, c->cid, c->arch, c->labels, c->split,
+                c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, s);
     prof_end(c, s, id);
     c->nk += 2;
     if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
@@ -1024,8 +1086,16 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     prof_end(c, s, id);
     ++c->nk;
   };
+  auto bd_l = [&](const BdPlan& P, double flops) {
+    const int id = prof_begin(c, s, GIST_PROF_AGG_TC, flops);
+    gemm_bd_launch(P, s);
+    prof_end(c, s, id);
+    ++c->nk;
+  };
+  const bool bd = c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE;
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
+    if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
     spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
     launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
   }
@@ -1043,6 +1113,7 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
     if (l == 0) break;
     launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
+    if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
     spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
   }
   return GIST_OK;

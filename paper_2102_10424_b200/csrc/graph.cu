@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
                                                      const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                      const int32_t* __restrict__ cid, int arch,
                                                      const int32_t* __restrict__ labels,
-                                                     const uint8_t* __restrict__ split) {
+                                                     const uint8_t* __restrict__ split, int skip_intra) {
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
   const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
     const int64_t end = rp[g + 1];
     const int64_t out0 = S.b_beg[v];
     int64_t out = out0;
+    int intra = 0;  // in-batch intra-cluster neighbours (skip_intra: counted, not stored)
+    const int32_t cg = skip_intra ? cid[g] : -1;
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t base = rp[g]; base < end; base += 64) {
       const int64_t e0 = base + lane, e1 = base + 32 + lane;
@@ -169,8 +171,14 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
       const int32_t c1 = u1 >= 0 ? cid[u1] : 0;
       const uint64_t m0 = u0 >= 0 ? S.map64[c0] : 0ull;
       const uint64_t m1 = u1 >= 0 ? S.map64[c1] : 0ull;
-      const bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
-      const bool in1 = u1 >= 0 && (uint32_t)(m1 >> 32) == tag;
+      bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
+      bool in1 = u1 >= 0 && (uint32_t)(m1 >> 32) == tag;
+      if (skip_intra) {
+        const bool i0 = in0 && c0 == cg, i1 = in1 && c1 == cg;
+        intra += __popc(__ballot_sync(0xffffffffu, i0)) + __popc(__ballot_sync(0xffffffffu, i1));
+        in0 &= !i0;
+        in1 &= !i1;
+      }
       const unsigned b0 = __ballot_sync(0xffffffffu, in0);
       const unsigned b1 = __ballot_sync(0xffffffffu, in1);
       if (in0) S.b_col[out + __popc(b0 & lt)] = u0 + (int32_t)(uint32_t)m0;
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
       if (in1) S.b_col[out + __popc(b1 & lt)] = u1 + (int32_t)(uint32_t)m1;
       out += __popc(b1);
     }
-    cnt = (int)(out - out0);
+    cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
     if (lane == 0) {
       S.b_end[v] = out;
       const float dg = (float)cnt;
@@ -203,10 +211,31 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
   }
 }
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
-                 const int32_t* labels, const uint8_t* split, cudaStream_t s) {
+                 const int32_t* labels, const uint8_t* split, int skip_intra, cudaStream_t s) {
   if (G.nb_max <= 0) return;
   k_batch_build<<<dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s>>>(G, rp, col, cid, arch, labels,
-                                                                                  split);
+                                                                                  split, skip_intra);
+}
+
+// one warp per node g: its intra-cluster neighbours -> 1 in its cluster's block row
+__global__ void k_cluster_blocks(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const int32_t* __restrict__ cid, const int64_t* __restrict__ cstart, int64_t n,
+                                 int bs, bf16* __restrict__ blocks) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= n) return;
+  const int32_t c = cid[g];
+  const int64_t c0 = cstart[c];
+  bf16* row = blocks + ((int64_t)c * bs + (g - c0)) * bs;
+  for (int64_t e = rp[g] + lane; e < rp[g + 1]; e += 32) {
+    const int32_t u = col[e];
+    if (cid[u] == c) row[u - c0] = __float2bfloat16_rn(1.0f);
+  }
+}
+void cluster_blocks(const int64_t* rp, const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t n,
+                    int bs, bf16* blocks, cudaStream_t s) {
+  if (n <= 0) return;
+  k_cluster_blocks<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(rp, col, cid, cstart, n, bs, blocks);
 }
 
 }  // namespace gist

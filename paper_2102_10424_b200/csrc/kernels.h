@@ -46,6 +46,7 @@ struct SpmmArgs {
   const StepState* st = nullptr;
   int q = 0;
   int max_cluster = 0;
+  int few_nnz = 0;  // hint: rows have few neighbours (inter-cluster pass): favour occupancy
 };
 template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
 
@@ -79,6 +80,8 @@ struct GemmOp {
   bool out_f32, relu;
   const void* mask;
   int64_t ldm;
+  const float* rscale;  // optional per-row scale of the output columns >= rs_from (BF16 path)
+  int rs_from;
 };
 }  // namespace gist
 #include <cuda.h>
@@ -87,8 +90,9 @@ struct alignas(64) GemmSlotTC {
   CUtensorMap ma, mb;  // TMA descriptors (128 B each)
   void* C;
   const void* mask;
+  const float* rscale;
   int64_t ldc, ldm;
-  int M, N, K, pad_;
+  int M, N, K, relu, rs_from;
 };
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGroup];
@@ -103,6 +107,47 @@ struct GemmPlanTC {
 };
 bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* plan);
 void gemm_bf16_launch(const GemmPlanTC& plan, cudaStream_t s);
+
+// Block-diagonal cluster aggregation on tcgen05 (SAGE, Cluster mini-batches):
+//   out[loff_k + r] = rscale[row] * sum_j A_c[r, j] * H[h0 + j]  (+ add[row]),  r < |cluster k|
+// with A_c the binary intra-cluster adjacency block of cluster c = bcl[k] (BS x BS bf16,
+// precomputed once per graph), h0 = loff_k or cstart[c] (global_rows).  Cluster ids and
+// offsets come from the device step descriptor, so the launch is step-invariant.
+struct BdOp {
+  const bf16* H;
+  int64_t ldh, h_rows, N;
+  void* C;  // bf16 output
+  int64_t ldc;
+  const bf16* add;
+  int64_t ldadd;
+  const float* rscale;
+  const int32_t* desc;
+  int global_rows;
+};
+struct alignas(64) BdSlot {
+  CUtensorMap mb;
+  void* C;
+  const bf16* add;
+  const float* rscale;
+  const int32_t* desc;
+  int64_t ldc, ldadd;
+  int N, global_rows;
+};
+struct BdGroup {
+  CUtensorMap ma;  // all cluster blocks [num_clusters * BS, BS]
+  BdSlot s[kMaxGroup];
+  int n = 0, q = 0, bs = 0;
+  const StepState* st = nullptr;
+  const int64_t* cstart = nullptr;
+};
+struct BdPlan {
+  BdGroup G;
+  int bn = 128;
+  int64_t maxN = 0;
+};
+bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q,
+                     const int64_t* cstart, const StepState* st, BdPlan* plan);
+void gemm_bd_launch(const BdPlan& plan, cudaStream_t s);
 // FP32 SIMT grouped GEMM (grid.z = slot)
 struct SgemmGroup {
   GemmOp op[kMaxGroup];
@@ -159,8 +204,14 @@ struct BatchGroup {
   const StepState* st = nullptr;
 };
 void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s);
+// skip_intra: intra-cluster edges only count towards the degree (they are aggregated by the
+// block-diagonal tensor-core path); the batch CSR then holds the inter-cluster edges only.
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
-                 const int32_t* labels, const uint8_t* split, cudaStream_t s);
+                 const int32_t* labels, const uint8_t* split, int skip_intra, cudaStream_t s);
+// Binary intra-cluster adjacency blocks: blocks[c][i][j] = 1 iff (cstart[c]+i, cstart[c]+j) is an
+// edge (relabelled ids), bf16 [num_clusters x bs x bs], zeroed by the caller.
+void cluster_blocks(const int64_t* rp, const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t n,
+                    int bs, bf16* blocks, cudaStream_t s);
 
 // --------------------------------------------------------------------------
 // Loss (R4), optimizers (R8), reductions.

@@ -124,7 +124,7 @@ void gemm_f32_group(const SgemmGroup& g, cudaStream_t s) {
 void gemm_f32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
               const float* B, int64_t ldb, float* C, int64_t ldc, bool relu, cudaStream_t s) {
   SgemmGroup g;
-  g.op[0] = GemmOp{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, true, relu, nullptr, 0};
+  g.op[0] = GemmOp{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, true, relu, nullptr, 0, nullptr, 0};
   g.n = 1;
   gemm_f32_group(g, s);
 }

@@ -34,7 +34,7 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
 }
 
 template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE>
-__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2 ? 3 : 2))
+__global__ void __launch_bounds__(256, ((J == 1 && sizeof(TI) == 2) || UNROLL == 1) ? 4 : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
   const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
   constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
   const int64_t v = gid / nchunks;
   const int chunk = (int)(gid - v * nchunks);
   if (v >= a.rows) return;           // whole group exits together
+  // inert dummy rows of a batch launch (v >= n_b): exact zeros, never a stale `add`
+  const bool dummy = a.desc && v >= a.desc[(size_t)a.st->z * (3 * a.q + 4) + 2 * a.q];
   const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
   const Off ldv = (Off)(a.ldh / V);  // row stride in 16-byte vectors
   const int64_t wv = a.w / V;        // width in vectors
@@ -133,6 +135,10 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
     float o[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) o[i] = acc[j][i] * rs;
+    if (dummy) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = 0.f;
+    } else {
     if (a.add) {
       float t[V];
       unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
@@ -148,6 +154,7 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4 : (J <= 2
     if (a.relu) {
 #pragma unroll
       for (int i = 0; i < V; ++i) o[i] = fmaxf(o[i], 0.f);
+    }
     }
     if constexpr (sizeof(TO) == sizeof(TI)) {
       st16(a.out + v * a.ldo + c, o);
@@ -340,6 +347,17 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   const int nchunks = (int)cdiv(w, CW);
   const int64_t groups = rows * nchunks;
   const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
+  if (G.a[0].few_nnz && J <= 2) {  // few neighbours per row: occupancy over in-flight loads
+    const bool wide = G.a[0].h_index != nullptr;
+    if (G.a[0].colscale) {
+      if (wide) k_spmm<TI, TO, LPR, J, 1, true, true><<<grid, 256, 0, s>>>(G, nchunks);
+      else k_spmm<TI, TO, LPR, J, 1, true, false><<<grid, 256, 0, s>>>(G, nchunks);
+    } else {
+      if (wide) k_spmm<TI, TO, LPR, J, 1, false, true><<<grid, 256, 0, s>>>(G, nchunks);
+      else k_spmm<TI, TO, LPR, J, 1, false, false><<<grid, 256, 0, s>>>(G, nchunks);
+    }
+    return;
+  }
   constexpr int UNROLL = J <= 2 ? 4 : 2;
   // 32-bit vector offsets whenever every gathered operand spans < 2^31 vectors
   bool wide = false, cs = G.a[0].colscale != nullptr;

@@ -19,7 +19,7 @@ GIST_PREC_FP32, GIST_PREC_BF16 = 0, 1
 GIST_GRAPH_DEVICE, GIST_GRAPH_HOST = 0, 1
 TRACE_NODES, TRACE_ACT, TRACE_LOGITS, TRACE_GRAD, TRACE_LOSS = range(5)
 (STAT_ROUND, STAT_STEP, STAT_SELF_LOOPS_DROPPED, STAT_LAST_NNZ_B, STAT_LAST_NB, STAT_KERNELS,
- STAT_H2D_BYTES, STAT_D2H_BYTES, STAT_MAX_NB) = range(9)
+ STAT_H2D_BYTES, STAT_D2H_BYTES, STAT_MAX_NB, STAT_BLOCK_AGG, STAT_BLOCK_DENSITY_PPM) = range(11)
 
 # every symbol include/gist.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -29,7 +29,7 @@ EXPORTS = [
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
     "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
 ]
-PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate"]
+PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc"]
 
 
 class GistConfig(C.Structure):

@@ -94,3 +94,24 @@ def test_bf16_loss_curve_C1_10_rounds(optimizer, lr):
     err = max(abs(a - b) for a, b in zip(lg, lo)) / max(lo)
     print(f"bf16 C1 {optimizer} loss curve gpu={lg} oracle={lo} err={err:.3e}")
     assert err <= 1e-2, (err, lg, lo)
+
+
+def test_bf16_block_diagonal_aggregation_rounds():
+    """SAGE in BF16 mode on small dense clusters uses the block-diagonal tensor-core
+    aggregation (intra-cluster blocks) + the sparse inter-cluster pass; q does not divide c,
+    so every epoch ends with a short batch (inert dummy rows).  Per-round mean losses and the
+    global weights after each round stay within the BF16 tolerance of the FP64 oracle."""
+    from paper_2102_10424_b200.gist import STAT_BLOCK_AGG
+    g = generate(tiny_spec(n=780, nnz=16000, d0=40, classes=6, clusters=13, f_in=0.8), seed=2)
+    gpu, ora = make_pair(g, "sage", (40, 96, 64, 6), optimizer="sgd", q=4, precision="bf16")
+    assert gpu.stat(STAT_BLOCK_AGG) == 1
+    for t in range(3):
+        gpu.partition(seed=3, m=2)
+        ora.partition(seed=3, m=2)
+        lg = gpu.subtrain(5, lr=0.1)
+        lo = ora.subtrain(5, lr=0.1)
+        assert np.max(np.abs(lg - lo)) <= BF16_TOL * max(1.0, np.max(np.abs(lo))), (t, lg, lo)
+        gpu.aggregate()
+        ora.aggregate()
+        for l in range(3):
+            assert rel_err(gpu.get_params(l), ora.theta[l]) <= BF16_TOL, (t, l)
