@@ -115,194 +115,308 @@ struct Epi {
   int64_t ldadd;
 };
 
-// Shared mainloop + epilogue of both kernels.  The tile's A rows / B columns start at
-// (a_row, b_col); K runs over [0, K) with the B operand's K coordinate offset by b_k0.
-// Output rows out_row0 + r for r < rows_valid, columns n0 + c for c < N - n0.
-template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
-__device__ __forceinline__ void gemm_tile(const CUtensorMap* mapA, const CUtensorMap* mapB, int a_row, int b_col,
-                                          int b_k0, int K, int out_row0, int rows_valid, int n0, int N,
-                                          const Epi& E) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Epilogue of one 16-column chunk of one output row: v = accumulator values.
+template <bool OUT_F32>
+__device__ __forceinline__ void epi_chunk(const Epi& E, int64_t row, int col, int N, float* v) {
+  const bool full16 = col + 16 <= N;
+  if (E.rscale) {  // per-row scale of the columns >= rs_from
+    const float sc = E.rscale[row];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col + i >= E.rs_from) v[i] *= sc;
+  }
+  if (E.add) {
+    const bf16* ap = E.add + row * E.ldadd + col;
+    if (full16 && ((((uintptr_t)ap) & 15) == 0)) {
+      float t[16];
+      ld16(ap, t);
+      ld16(ap + 8, t + 8);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += t[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < N) v[i] += __bfloat162float(ap[i]);
+    }
+  }
+  if (E.relu) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  if (E.mask) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
+    const bf16* mp = E.mask + row * E.ldm + col;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (col + i < N && !(__bfloat162float(mp[i]) > 0.f)) v[i] = 0.f;
+  }
+  if (OUT_F32) {
+    float* dst = (float*)E.C + row * E.ldc + col;
+    if (full16 && (((uintptr_t)dst & 15) == 0)) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < N) dst[i] = v[i];
+    }
+  } else {
+    bf16* dst = (bf16*)E.C + row * E.ldc + col;
+    if (full16 && (((uintptr_t)dst & 15) == 0)) {
+      st16(dst, v);
+      st16(dst + 8, v + 8);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+// One output tile of a persistent GEMM: where its operands start, where it writes.
+struct Tile {
+  bool valid;  // tile exists
+  bool mma;    // false: zero-fill only (inert dummy rows of a batch)
+  const CUtensorMap *ma, *mb;
+  int a_row, b_col, b_k0, K;  // TMA coordinates
+  int64_t out_row0;
+  int rows_valid, n0, N;
+  Epi E;
+};
+
+// Plain grouped GEMM: tiles (slot, m-tile, n-tile), n fastest.
+template <int BN>
+struct ProbPlain {
+  using Group = GemmGroupTC;
+  static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
+  static __device__ __forceinline__ Tile decode(const Group& G, int t) {
+    Tile T;
+    const int per = G.tm * G.tn;
+    const int z = t / per, r = t - z * per;
+    const GemmSlotTC& S = G.s[z];
+    const int m0 = (r / G.tn) * BM, n0 = (r % G.tn) * BN;
+    T.valid = T.mma = m0 < S.M && n0 < S.N;
+    T.ma = &S.ma;
+    T.mb = &S.mb;
+    T.a_row = m0;
+    T.b_col = n0;
+    T.b_k0 = 0;
+    T.K = S.K;
+    T.out_row0 = m0;
+    T.rows_valid = S.M - m0;
+    T.n0 = n0;
+    T.N = S.N;
+    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0};
+    return T;
+  }
+};
+
+// Block-diagonal cluster aggregation: tiles (slot, [cluster k, m-tile] | dummy tile, n-tile).
+template <int BN>
+struct ProbBd {
+  using Group = BdGroup;
+  static __device__ __forceinline__ int mt_per(const Group& G) { return (G.bs + BM - 1) / BM; }
+  static __device__ __forceinline__ int ydim(const Group& G) {
+    return G.q * mt_per(G) + (int)((G.rows + BM - 1) / BM);
+  }
+  static __device__ __forceinline__ int count(const Group& G) { return G.n * ydim(G) * G.tn; }
+  static __device__ __forceinline__ Tile decode(const Group& G, int t) {
+    Tile T;
+    const int per = ydim(G) * G.tn;
+    const int z = t / per, r = t - z * per;
+    const int y = r / G.tn, n0 = (r % G.tn) * BN;
+    const BdSlot& S = G.s[z];
+    const int q = G.q, mp = mt_per(G);
+    const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+    T.ma = &G.ma;
+    T.mb = &S.mb;
+    T.n0 = n0;
+    T.N = S.N;
+    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd};
+    T.b_col = n0;
+    T.K = G.bs;
+    if (y >= q * mp) {  // inert dummy rows [n_b, rows): zeros
+      const int64_t r0 = (int64_t)d[2 * q] + (int64_t)(y - q * mp) * BM;
+      T.mma = false;
+      T.out_row0 = r0;
+      T.rows_valid = (int)((G.rows - r0) < BM ? (G.rows - r0) : BM);
+      T.valid = T.rows_valid > 0 && n0 < S.N;
+      return T;
+    }
+    const int k = y / mp, mt = y - k * mp;
+    T.valid = T.mma = false;
+    if (k >= d[3 * q + 2]) return T;
+    const int c = d[k], r0 = d[q + k], size = d[q + k + 1] - r0;
+    if (mt * BM >= size || n0 >= S.N) return T;
+    T.valid = T.mma = true;
+    T.a_row = c * G.bs + mt * BM;
+    T.b_k0 = S.global_rows ? (int)G.cstart[c] : r0;
+    T.out_row0 = r0 + mt * BM;
+    T.rows_valid = size - mt * BM;
+    return T;
+  }
+};
+
+// Persistent warp-specialised tcgen05 GEMM: grid = min(tiles, #SMs), 192 threads.
+// warp 0: TMA producer (one lane) into an ST-deep shared-memory ring; warp 1: MMA issuer
+// (one lane) into one of two TMEM accumulators; warps 2-5: epilogue (TMEM -> registers ->
+// global), releasing the accumulator to the MMA warp, so the epilogue of tile i overlaps the
+// main loop of tile i+1 and the CTA set-up (barriers, TMEM allocation) is paid once per SM.
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+__global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__ typename Prob::Group G) {
   using CF = Cfg<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE_BYTES);
   uint64_t* empty = full + CF::STAGES;
-  uint64_t* accf = empty + CF::STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(accf + 1);
+  uint64_t* accf = empty + CF::STAGES;  // [2]
+  uint64_t* acce = accf + 2;            // [2]
+  uint32_t* tmem_slot = (uint32_t*)(acce + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (K + BK - 1) / BK;
+  constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < CF::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_map(mapA);
-    prefetch_map(mapB);
   }
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(CF::TMEM_COLS));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const int total = Prob::count(G);
 
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % CF::STAGES;
-      const uint32_t ph = (uint32_t)(kb / CF::STAGES) & 1u;
-      mbar_wait(&empty[s], ph ^ 1u);
-      uint8_t* sa = smem + s * CF::STAGE_BYTES;
-      uint8_t* sb = sa + CF::A_BYTES;
-      mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
-      const int k0 = kb * BK;
-      if (!A_MN) {
-        tma_load_2d(sa, mapA, &full[s], k0, a_row);
-      } else {
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile T = Prob::decode(G, t);
+        if (!T.mma) continue;
+        const int nk = (T.K + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % CF::STAGES;
+          const uint32_t ph = (it / CF::STAGES) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * CF::STAGE_BYTES;
+          uint8_t* sb = sa + CF::A_BYTES;
+          mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(sa, T.ma, &full[s], k0, T.a_row);
+          } else {
 #pragma unroll
-        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, mapA, &full[s], a_row + 64 * j, k0);
-      }
-      if (!B_MN) {
-        tma_load_2d(sb, mapB, &full[s], b_k0 + k0, b_col);
-      } else {
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, T.mb, &full[s], T.b_k0 + k0, T.b_col);
+          } else {
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, mapB, &full[s], b_col + 64 * j, b_k0 + k0);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(sb + j * 8192, T.mb, &full[s], T.b_col + 64 * j, T.b_k0 + k0);
+          }
+        }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                               ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % CF::STAGES;
-      const uint32_t ph = (uint32_t)(kb / CF::STAGES) & 1u;
-      mbar_wait(&full[s], ph);
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                 ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      uint32_t it = 0, tc = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile T = Prob::decode(G, t);
+        if (!T.mma) continue;
+        const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
+        mbar_wait(&acce[b], aph ^ 1u);  // the epilogue has drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem + b * BN;
+        const int nk = (T.K + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % CF::STAGES;
+          const uint32_t ph = (it / CF::STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 bytes per K16 inside the swizzled row; MN-major: +16 K-rows = 2048 bytes
+            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024) : make_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024) : make_desc(sb + k * 32, 16, 1024);
+            umma_bf16(dacc, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        umma_commit(&accf[b]);  // accumulator b complete
+        ++tc;
+      }
+    }
+  } else {  // ------------------------------------------------------------ epilogue warps 2..5
+    const int lq = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = lq * 32 + lane;
+    uint32_t tc = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const Tile T = Prob::decode(G, t);
+      if (!T.valid) continue;
+      if (!T.mma) {  // zero-fill (dummy rows)
+        const int et = threadIdx.x - 64;
+        for (int idx = et; idx < BM * BN; idx += 128) {
+          const int rr = idx / BN, cc = T.n0 + idx % BN;
+          if (rr < T.rows_valid && cc < T.N) {
+            const int64_t row = T.out_row0 + rr;
+            if (OUT_F32) ((float*)T.E.C)[row * T.E.ldc + cc] = 0.f;
+            else ((bf16*)T.E.C)[row * T.E.ldc + cc] = __float2bfloat16_rn(0.f);
+          }
+        }
+        continue;
+      }
+      const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
+      mbar_wait(&accf[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
-      const uint32_t sb = sa + CF::A_BYTES;
-#pragma unroll
-      for (int k = 0; k < BK / 16; ++k) {
-        // K-major: advance 16 elements = 32 bytes inside the swizzled row; MN-major: 16 K-rows = 2048 bytes
-        const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024) : make_desc(sa + k * 32, 16, 1024);
-        const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024) : make_desc(sb + k * 32, 16, 1024);
-        umma_bf16(tmem, ad, bd, idesc, (kb | k) != 0);
-      }
-      umma_commit(&empty[s]);  // frees the smem stage when these MMAs have read it
-    }
-    umma_commit(accf);  // accumulator complete
-  }
-  __syncwarp();
-  // ------------------------------------------------------------ epilogue (all 4 warps)
-  mbar_wait(accf, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int r = warp * 32 + lane;
-  const int64_t row = (int64_t)out_row0 + r;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+      const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
+      const int64_t row = T.out_row0 + r;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    tmem_ld16(trow + c, v);
-    const int col = n0 + c;
-    if (r < rows_valid && col < N) {
-      if (E.rscale) {  // per-row scale of the columns >= rs_from
-        const float sc = E.rscale[row];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (col + i >= E.rs_from) v[i] *= sc;
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+        if (r < T.rows_valid && T.n0 + c < T.N) epi_chunk<OUT_F32>(T.E, row, T.n0 + c, T.N, v);
       }
-      const bool full16 = col + 16 <= N;
-      if (E.add) {
-        const bf16* ap = E.add + row * E.ldadd + col;
-        if (full16 && ((((uintptr_t)ap) & 15) == 0)) {
-          float t[16];
-          ld16(ap, t);
-          ld16(ap + 8, t + 8);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += t[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (col + i < N) v[i] += __bfloat162float(ap[i]);
-        }
-      }
-      if (E.relu) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
-      }
-      if (E.mask) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
-        const bf16* mp = E.mask + row * E.ldm + col;
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (col + i < N && !(__bfloat162float(mp[i]) > 0.f)) v[i] = 0.f;
-      }
-      if (OUT_F32) {
-        float* dst = (float*)E.C + row * E.ldc + col;
-        if (full16 && (((uintptr_t)dst & 15) == 0)) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (col + i < N) dst[i] = v[i];
-        }
-      } else {
-        bf16* dst = (bf16*)E.C + row * E.ldc + col;
-        if (full16 && (((uintptr_t)dst & 15) == 0)) {
-          st16(dst, v);
-          st16(dst + 8, v + 8);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (col + i < N) dst[i] = __float2bfloat16_rn(v[i]);
-        }
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++tc;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 
-// Plain grouped GEMM: grid (N tiles, M tiles, slots).
-template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
-__global__ void __launch_bounds__(128, 1) k_gemm_tc(const __grid_constant__ GemmGroupTC G) {
-  const GemmSlotTC& S = G.s[blockIdx.z];
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  if (m0 >= S.M || n0 >= S.N) return;  // slots may be smaller than the grid (uniform exit)
-  const Epi E{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0};
-  gemm_tile<BN, ST, A_MN, B_MN, OUT_F32>(&S.ma, &S.mb, m0, n0, 0, S.K, m0, S.M - m0, n0, S.N, E);
-}
-
-// Block-diagonal aggregation (SAGE, Cluster batches): for batch cluster k of slot z,
-//   out[loff_k + r, :] = epi( sum_j A_c[r, j] * H[h0 + j, :] ),  r < |cluster|,
-// A_c = the cluster's binary intra-cluster adjacency block (bf16, BS x BS, precomputed at
-// load), h0 = loff_k (batch-local rows) or cstart[c] (global feature rows, layer 0).
-// grid (N tiles, q * M tiles per block, slots); cluster ids / offsets from the step state.
-template <int BN, int ST>
-__global__ void __launch_bounds__(128, 1) k_gemm_bd(const __grid_constant__ BdGroup G) {
-  const BdSlot& S = G.s[blockIdx.z];
-  const int q = G.q;
-  const int mt_per = (G.bs + BM - 1) / BM;
-  const int k = blockIdx.y / mt_per, mt = blockIdx.y % mt_per;
-  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
-  if (k >= d[3 * q + 2]) return;
-  const int c = d[k], r0 = d[q + k], size = d[q + k + 1] - r0;
-  if (mt * BM >= size) return;
-  const int n0 = blockIdx.x * BN;
-  if (n0 >= S.N) return;
-  const int h0 = S.global_rows ? (int)G.cstart[c] : r0;
-  const Epi E{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd};
-  gemm_tile<BN, ST, false, true, false>(&G.ma, &S.mb, c * G.bs + mt * BM, n0, h0, G.bs, r0 + mt * BM, size - mt * BM, n0,
-                                    S.N, E);
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 // ------------------------------------------------------------------ host side
@@ -337,25 +451,25 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32>
-void launch_tc(const GemmPlanTC& P, cudaStream_t s) {
-  auto kern = k_gemm_tc<BN, ST, A_MN, B_MN, OUT_F32>;
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
+  auto kern = k_gemm_persist<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
+  constexpr int SMEM = Cfg<BN, ST>::SMEM + 64;
   static bool attr = false;  // per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, ST>::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  dim3 grid((unsigned)cdiv(P.maxN, BN), (unsigned)cdiv(P.maxM, BM), (unsigned)P.G.n);
-  kern<<<grid, 128, Cfg<BN, ST>::SMEM, s>>>(P.G);
+  const int grid = total < num_sms() ? total : num_sms();
+  if (grid > 0) kern<<<grid, 192, SMEM, s>>>(G);
 }
 
-// Stage count: big single GEMMs keep the deep ring (1 CTA/SM); grouped step GEMMs use a
-// 3-stage ring at BN=128 (2 CTAs/SM, so one CTA's epilogue overlaps another's mainloop).
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
-  constexpr int ST = BN == 256 ? 4 : 3;
-  if (P.out_f32) launch_tc<BN, ST, A_MN, B_MN, true>(P, s);
-  else launch_tc<BN, ST, A_MN, B_MN, false>(P, s);
+  constexpr int ST = BN == 256 ? 4 : 6;
+  const int total = P.G.n * P.G.tm * P.G.tn;
+  if (P.out_f32) launch_persist<BN, ST, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total, s);
+  else launch_persist<BN, ST, A_MN, B_MN, false, ProbPlain<BN>>(P.G, total, s);
 }
 
 template <int BNV>
@@ -368,16 +482,9 @@ void dispatch_layout(const GemmPlanTC& P, cudaStream_t s) {
 
 template <int BN>
 void launch_bd(const BdPlan& P, cudaStream_t s) {
-  constexpr int ST = 2;  // K = cluster block size (<= 256): a short ring, 2+ CTAs per SM
-  auto kern = k_gemm_bd<BN, ST>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN, ST>::SMEM);
-    attr = true;
-  }
   const int mt_per = (P.G.bs + BM - 1) / BM;
-  dim3 grid((unsigned)cdiv(P.maxN, BN), (unsigned)(P.G.q * mt_per), (unsigned)P.G.n);
-  kern<<<grid, 128, Cfg<BN, ST>::SMEM, s>>>(P.G);
+  const int total = P.G.n * (P.G.q * mt_per + (int)cdiv(P.G.rows, BM)) * P.G.tn;
+  launch_persist<BN, 4, false, true, false, ProbBd<BN>>(P.G, total, s);
 }
 
 }  // namespace
@@ -396,8 +503,7 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     maxN = ops[i].N > maxN ? ops[i].N : maxN;
     maxM = ops[i].M > maxM ? ops[i].M : maxM;
   }
-  // wide tiles only when one GEMM alone has enough tiles to fill the GPU
-  P->bn = (maxN > 128 && n == 1 && cdiv(maxM, BM) * cdiv(maxN, 256) >= 148) ? 256 : 128;
+  P->bn = maxN > 128 ? 256 : 128;  // persistent kernel: wide tiles amortise the epilogue
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
     const GemmOp& o = ops[i];
@@ -421,6 +527,8 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     P->maxM = o.M > P->maxM ? o.M : P->maxM;
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
+  P->G.tm = (int)cdiv(P->maxM, BM);
+  P->G.tn = (int)cdiv(P->maxN, P->bn);
   return true;
 }
 
@@ -430,7 +538,7 @@ void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
   else dispatch_layout<128>(P, s);
 }
 
-bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q,
+bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q, int64_t rows,
                      const int64_t* cstart, const StepState* st, BdPlan* P) {
   if (!get_encode() || n < 1 || n > kMaxGroup || (bs % 8)) return false;
   if (!make_map(&P->G.ma, blocks, bs, (int64_t)num_clusters * bs, bs, 64, BM)) return false;
@@ -439,6 +547,7 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
   P->G.bs = bs;
   P->G.st = st;
   P->G.cstart = cstart;
+  P->G.rows = rows;
   P->maxN = 0;
   for (int i = 0; i < n; ++i) {
     const BdOp& o = ops[i];
@@ -456,7 +565,8 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.N = (int)o.N;
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
-  P->bn = 128;
+  P->bn = P->maxN > 128 ? 256 : 128;
+  P->G.tn = (int)cdiv(P->maxN, P->bn);
   return true;
 }
 

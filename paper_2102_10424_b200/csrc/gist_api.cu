@@ -908,8 +908,9 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
       g.fwd_spmm[l].n = g.count;
       g.bwd_spmm[l].n = l > 0 ? g.count : 0;
       if (bd) {
-        if (!gemm_bd_prepare(c->blocks, c->c, c->bs, bfw.data(), g.count, q, c->cstart, c->dstate, &g.fwd_bd[l]) ||
-            (l > 0 && !gemm_bd_prepare(c->blocks, c->c, c->bs, bbw.data(), g.count, q, c->cstart, c->dstate,
+        if (!gemm_bd_prepare(c->blocks, c->c, c->bs, bfw.data(), g.count, q, nb, c->cstart, c->dstate,
+                             &g.fwd_bd[l]) ||
+            (l > 0 && !gemm_bd_prepare(c->blocks, c->c, c->bs, bbw.data(), g.count, q, nb, c->cstart, c->dstate,
                                        &g.bwd_bd[l])))
           return fail(c, GIST_E_UNSUPPORTED, "block-diagonal aggregation plan failed");
       }

@@ -96,7 +96,7 @@ struct alignas(64) GemmSlotTC {
 };
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGroup];
-  int n = 0;
+  int n = 0, tm = 0, tn = 0;  // slots, M tiles, N tiles (persistent tile space)
 };
 // Host-side plan of one grouped tcgen05 GEMM (tensor maps encoded once, launched many times).
 struct GemmPlanTC {
@@ -136,7 +136,8 @@ struct alignas(64) BdSlot {
 struct BdGroup {
   CUtensorMap ma;  // all cluster blocks [num_clusters * BS, BS]
   BdSlot s[kMaxGroup];
-  int n = 0, q = 0, bs = 0;
+  int n = 0, q = 0, bs = 0, tn = 0;
+  int64_t rows = 0;  // static batch rows (nb_max): dummy rows [n_b, rows) are zero-filled
   const StepState* st = nullptr;
   const int64_t* cstart = nullptr;
 };
@@ -145,7 +146,7 @@ struct BdPlan {
   int bn = 128;
   int64_t maxN = 0;
 };
-bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q,
+bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q, int64_t rows,
                      const int64_t* cstart, const StepState* st, BdPlan* plan);
 void gemm_bd_launch(const BdPlan& plan, cudaStream_t s);
 // FP32 SIMT grouped GEMM (grid.z = slot)
