@@ -91,6 +91,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 template <int BN, int ST = (BN == 256 ? 4 : 6)>
 struct Cfg {
   static constexpr int STAGES = ST;
@@ -121,10 +136,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Epilogue of one 16-column chunk of one output row: v = accumulator values.
 template <bool OUT_F32>
-__device__ __forceinline__ void epi_chunk(const Epi& E, int64_t row, int col, int N, float* v) {
+__device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, int col, int N, float* v) {
   const bool full16 = col + 16 <= N;
-  if (E.rscale) {  // per-row scale of the columns >= rs_from
-    const float sc = E.rscale[row];
+  if (E.rscale) {  // per-row scale of the columns >= rs_from (sc = rscale[row], loaded once per tile)
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (col + i >= E.rs_from) v[i] *= sc;
@@ -192,7 +206,9 @@ template <int BN>
 struct ProbPlain {
   using Group = GemmGroupTC;
   static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
-  static __device__ __forceinline__ Tile decode(const Group& G, int t) {
+  static constexpr int kMaxDesc = 1;
+  static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
+  static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t*) {
     Tile T;
     const int per = G.tm * G.tn;
     const int z = t / per, r = t - z * per;
@@ -223,14 +239,22 @@ struct ProbBd {
     return G.q * mt_per(G) + (int)((G.rows + BM - 1) / BM);
   }
   static __device__ __forceinline__ int count(const Group& G) { return G.n * ydim(G) * G.tn; }
-  static __device__ __forceinline__ Tile decode(const Group& G, int t) {
+  // this step's descriptors of every slot, staged in shared memory once per CTA
+  static constexpr int kMaxDesc = 3 * 64 + 4;
+  static __device__ __forceinline__ void stage(const Group& G, int32_t* sdesc) {
+    const int per = 3 * G.q + 4;
+    const int z = G.st->z;
+    for (int i = threadIdx.x; i < G.n * per; i += blockDim.x)
+      sdesc[i] = G.s[i / per].desc[(size_t)z * per + (i % per)];
+  }
+  static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sdesc) {
     Tile T;
     const int per = ydim(G) * G.tn;
     const int z = t / per, r = t - z * per;
     const int y = r / G.tn, n0 = (r % G.tn) * BN;
     const BdSlot& S = G.s[z];
     const int q = G.q, mp = mt_per(G);
-    const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+    const int32_t* d = sdesc + z * (3 * q + 4);
     T.ma = &G.ma;
     T.mb = &S.mb;
     T.n0 = n0;
@@ -277,6 +301,8 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
   uint32_t* tmem_slot = (uint32_t*)(acce + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
+  __shared__ int32_t sdesc[Prob::kMaxDesc * kMaxGroup];
+  Prob::stage(G, sdesc);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < CF::STAGES; ++s) {
@@ -304,7 +330,7 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       uint32_t it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile T = Prob::decode(G, t);
+        const Tile T = Prob::decode(G, t, sdesc);
         if (!T.mma) continue;
         const int nk = (T.K + BK - 1) / BK;
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -337,7 +363,7 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
                                  ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       uint32_t it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile T = Prob::decode(G, t);
+        const Tile T = Prob::decode(G, t, sdesc);
         if (!T.mma) continue;
         const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
         mbar_wait(&acce[b], aph ^ 1u);  // the epilogue has drained this accumulator
@@ -369,7 +395,7 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
     const int r = lq * 32 + lane;
     uint32_t tc = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const Tile T = Prob::decode(G, t);
+      const Tile T = Prob::decode(G, t, sdesc);
       if (!T.valid) continue;
       if (!T.mma) {  // zero-fill (dummy rows)
         const int et = threadIdx.x - 64;
@@ -384,15 +410,20 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
         continue;
       }
       const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
+      const int64_t row = T.out_row0 + r;
+      const bool live = r < T.rows_valid;
+      const float sc = (T.E.rscale && live) ? T.E.rscale[row] : 1.f;  // before the wait: overlaps the MMA
       mbar_wait(&accf[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
-      const int64_t row = T.out_row0 + r;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(trow + c, v);
-        if (r < T.rows_valid && T.n0 + c < T.N) epi_chunk<OUT_F32>(T.E, row, T.n0 + c, T.N, v);
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(trow + c, v);
+        if (live && T.n0 + c < T.N) {
+          epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v);
+          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();

@@ -585,8 +585,10 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
     const int bs = (int)pad8(c->max_csize);
     const double bytes = (double)num_clusters * bs * bs * 2.0;
     bool want = c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->max_csize <= 256 &&
-                c->block_density >= 0.05 && bytes <= 8e9;
-    if (env) want = env[0] == '1' && c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->max_csize <= 256;
+                c->cfg.clusters_per_batch <= 64 && c->block_density >= 0.05 && bytes <= 8e9;
+    if (env)
+      want = env[0] == '1' && c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->max_csize <= 256 &&
+             c->cfg.clusters_per_batch <= 64;
     if (want) {
       c->bs = bs;
       TRY(dalloc_t(c, &c->blocks, (size_t)num_clusters * bs * bs));
