@@ -811,6 +811,11 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.bwd_bd.assign(L, BdPlan());
     g.bd_fl.assign(L, 0.0);
     const bool bd = c->bd && tc && sage;
+    if (bd) {  // the batch build copies the layer-0 self half [X_b | .] (no self_out in the sparse pass)
+      g.batch.X = (const bf16*)c->X;
+      g.batch.ldx = pad8(c->dims[0]);
+      g.batch.ldxd = c->shapes[c->slots[g0].index][0].Kp;
+    }
     g.ce.n = g.count;
     g.ce.rows = nb;
     g.ce.k = c->k;
@@ -857,6 +862,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
                              sl.scale, sl.desc_dev, l == 0 ? 1 : 0});
           a.add = C + sh.half; a.ld_add = sh.Kp;
           a.few_nnz = 1;
+          if (l == 0) { a.self_out = nullptr; g.batch.xdst[j] = (bf16*)C; }
           g.bd_fl[l] += 2.0 * q * c->bs * c->bs * sh.half;
         }
         g.fwd_by[l] += spmm_bytes(a);

@@ -187,6 +187,11 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
       out += __popc(b1);
     }
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
+    if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
+      const uint4* xs = reinterpret_cast<const uint4*>(G.X + g * G.ldx);
+      uint4* xd = reinterpret_cast<uint4*>(G.xdst[blockIdx.y] + (int64_t)v * G.ldxd);
+      for (int i = lane; i < G.ldx / 8; i += 32) xd[i] = xs[i];
+    }
     if (lane == 0) {
       S.b_end[v] = out;
       const float dg = (float)cnt;

@@ -203,6 +203,10 @@ struct BatchGroup {
   BatchSlot s[kMaxGroup];
   int n = 0, q = 0, nb_max = 0;
   const StepState* st = nullptr;
+  // optional: copy the batch rows of the feature matrix X (bf16, ldx) into xdst[slot] (ldxd)
+  const bf16* X = nullptr;
+  int64_t ldx = 0, ldxd = 0;
+  bf16* xdst[kMaxGroup] = {};
 };
 void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s);
 // skip_intra: intra-cluster edges only count towards the degree (they are aggregated by the
