@@ -28,7 +28,7 @@ __all__ = [
     "PURPOSE_PARTITION", "PURPOSE_BATCH", "PURPOSE_INIT",
     "sample_partition", "sub_index_sets", "extract", "aggregate",
     "aggregate_delta_sum", "coverage_fraction", "sub_param_count",
-    "glorot_init", "batch_schedule", "batch_nodes", "induced_subgraph",
+    "glorot_init", "glorot_block", "batch_schedule", "batch_nodes", "induced_subgraph",
     "gcn_operator", "sage_operator", "chebyshev_operator", "spmm",
     "forward", "backward", "softmax_ce", "adam_step", "sgd_step",
     "OracleGIST", "lr_step_schedule",
@@ -204,6 +204,24 @@ def glorot_init(arch: str, dims: list[int], seed: int) -> list[np.ndarray]:
         w = (tt * s).astype(np.float32)                      # one rounded fp32 multiply
         theta.append(w.astype(np.float64).reshape(rows, cols))
     return theta
+
+
+def glorot_block(arch: str, dims: list[int], seed: int, l: int, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """Theta_l[rows, cols] of glorot_init without materialising Theta_l: every entry is a
+    function of its own counter (flat index, l, 0, PURPOSE_INIT) only (R11).  Used for
+    full-size parity checks; pinned against glorot_init in tests/test_oracle_model.py."""
+    nrows = dims[l] * (2 if arch == "sage" else 1)
+    ncols = dims[l + 1]
+    s = np.sqrt(np.float32(6.0) / np.float32(nrows + ncols), dtype=np.float32)
+    r = np.asarray(rows, dtype=np.uint64)[:, None]
+    c = np.asarray(cols, dtype=np.uint64)[None, :]
+    flat = (r * np.uint64(ncols) + c).ravel()
+    ctr = np.stack([flat & MASK32, np.full_like(flat, l), flat >> np.uint64(32),
+                    np.full_like(flat, PURPOSE_INIT)], axis=1)
+    w0 = philox4x32_10(ctr, split_seed(seed))[:, 0]
+    u = (w0 >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+    tt = np.float32(2.0) * u - np.float32(1.0)
+    return (tt * s).astype(np.float32).astype(np.float64).reshape(len(rows), len(cols))
 
 
 # ---------------------------------------------------------------------------

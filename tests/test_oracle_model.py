@@ -267,3 +267,13 @@ def test_glorot_init_bounds_determinism_and_fp32():
     assert np.array_equal(big, big.astype(np.float32).astype(np.float64))   # exact fp32 values
     s = math.sqrt(6 / 500)
     assert abs(big.mean()) < 0.01 * s and abs(big.std() - s / math.sqrt(3)) < 0.01 * s
+
+
+def test_glorot_block_equals_full_init_slices():
+    rng = np.random.default_rng(0)
+    for arch, dims in [("gcn", [30, 40, 7]), ("sage", [25, 33, 9])]:
+        full = O.glorot_init(arch, dims, 13)
+        for l in range(len(dims) - 1):
+            rows = np.sort(rng.choice(full[l].shape[0], 6, replace=False))
+            cols = np.sort(rng.choice(full[l].shape[1], 5, replace=False))
+            assert np.array_equal(O.glorot_block(arch, dims, 13, l, rows, cols), full[l][np.ix_(rows, cols)])
