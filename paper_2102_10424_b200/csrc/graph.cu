@@ -116,9 +116,9 @@ __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_
   }
   if (v == 0) S.stats[0] = S.stats[1] = 0;
   if (v >= G.nb_max) return;
-  if (v >= nb) {  // inert dummy row
+  if (v >= nb) {  // inert dummy row: no neighbours, marked by a negative row start
     S.b_nodes[v] = 0;
-    S.b_beg[v] = 0;
+    S.b_beg[v] = -1;
     return;
   }
   int lo = 0, hi = qq - 1;  // largest k with loff[k] <= v
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
       S.train_b[v] = (uint8_t)tr;
     }
   } else if (v < G.nb_max && lane == 0) {  // inert dummy row
-    S.b_end[v] = 0;
+    S.b_end[v] = -1;
     S.scale[v] = 0.f;
     S.lab_b[v] = 0;
     S.train_b[v] = 0;

@@ -47,8 +47,10 @@ __global__ void __launch_bounds__(256, ((J == 1 && sizeof(TI) == 2) || UNROLL ==
   const int64_t v = gid / nchunks;
   const int chunk = (int)(gid - v * nchunks);
   if (v >= a.rows) return;           // whole group exits together
-  // inert dummy rows of a batch launch (v >= n_b): exact zeros, never a stale `add`
-  const bool dummy = a.desc && v >= a.desc[(size_t)a.st->z * (3 * a.q + 4) + 2 * a.q];
+  // inert dummy rows of a batch launch (v >= n_b, marked row_beg < 0 by the batch build):
+  // exact zeros, never a stale `add`
+  const int64_t beg = a.row_beg[v], end = a.row_end[v];
+  const bool dummy = beg < 0;
   const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
   const Off ldv = (Off)(a.ldh / V);  // row stride in 16-byte vectors
   const int64_t wv = a.w / V;        // width in vectors
@@ -80,7 +82,6 @@ __global__ void __launch_bounds__(256, ((J == 1 && sizeof(TI) == 2) || UNROLL ==
     }
   }
 
-  const int64_t beg = a.row_beg[v], end = a.row_end[v];
   for (int64_t base = beg; base < end; base += LPR) {
     const int n = (end - base) < LPR ? (int)(end - base) : LPR;
     Off ou = 0;
