@@ -143,6 +143,7 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 // per block (integer addition: deterministic).  grid (cdiv(nb_max, 8), slots).
 __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ BatchGroup G,
                                                      const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                     const int32_t* __restrict__ ccol,
                                                      const int32_t* __restrict__ cid, int arch,
                                                      const int32_t* __restrict__ labels,
                                                      const uint8_t* __restrict__ split, int skip_intra) {
@@ -165,10 +166,10 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t base = rp[g]; base < end; base += 64) {
       const int64_t e0 = base + lane, e1 = base + 32 + lane;
-      const int32_t u0 = e0 < end ? col[e0] : -1;
-      const int32_t u1 = e1 < end ? col[e1] : -1;
-      const int32_t c0 = u0 >= 0 ? cid[u0] : 0;
-      const int32_t c1 = u1 >= 0 ? cid[u1] : 0;
+      const int32_t u0 = e0 < end ? col[e0] : -1;   // col and its cluster: independent,
+      const int32_t u1 = e1 < end ? col[e1] : -1;   // coalesced loads (no cid[col] chain)
+      const int32_t c0 = e0 < end ? ccol[e0] : 0;
+      const int32_t c1 = e1 < end ? ccol[e1] : 0;
       const uint64_t m0 = u0 >= 0 ? S.map64[c0] : 0ull;
       const uint64_t m1 = u1 >= 0 ? S.map64[c1] : 0ull;
       bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
@@ -215,11 +216,22 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
     if (b) atomicAdd((unsigned long long*)&S.stats[1], (unsigned long long)b);
   }
 }
-void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
-                 const int32_t* labels, const uint8_t* split, int skip_intra, cudaStream_t s) {
+void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
+                 const int32_t* cid, int arch, const int32_t* labels, const uint8_t* split, int skip_intra,
+                 cudaStream_t s) {
   if (G.nb_max <= 0) return;
-  k_batch_build<<<dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s>>>(G, rp, col, cid, arch, labels,
-                                                                                  split, skip_intra);
+  k_batch_build<<<dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s>>>(G, rp, col, ccol, cid, arch,
+                                                                                  labels, split, skip_intra);
+}
+
+__global__ void k_edge_clusters(const int32_t* __restrict__ col, const int32_t* __restrict__ cid, int64_t nnz,
+                                int32_t* __restrict__ ccol) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    ccol[e] = cid[col[e]];
+}
+void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s) {
+  if (nnz <= 0) return;
+  k_edge_clusters<<<148 * 8, 256, 0, s>>>(col, cid, nnz, ccol);
 }
 
 // one warp per node g: its intra-cluster neighbours -> 1 in its cluster's block row

@@ -211,8 +211,11 @@ struct BatchGroup {
 void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s);
 // skip_intra: intra-cluster edges only count towards the degree (they are aggregated by the
 // block-diagonal tensor-core path); the batch CSR then holds the inter-cluster edges only.
-void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* cid, int arch,
-                 const int32_t* labels, const uint8_t* split, int skip_intra, cudaStream_t s);
+// ccol[e] = cid[col[e]] (cluster of every edge's neighbour, precomputed at load)
+void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
+                 const int32_t* cid, int arch, const int32_t* labels, const uint8_t* split, int skip_intra,
+                 cudaStream_t s);
+void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s);
 // Binary intra-cluster adjacency blocks: blocks[c][i][j] = 1 iff (cstart[c]+i, cstart[c]+j) is an
 // edge (relabelled ids), bf16 [num_clusters x bs x bs], zeroed by the caller.
 void cluster_blocks(const int64_t* rp, const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t n,
