@@ -3,7 +3,7 @@
 `python -m paper_2102_10424_b200.build` or `__graft_entry__.build()`.
 Compiles every csrc/*.cu with nvcc (-gencode arch=compute_100a,code=sm_100a
 -lineinfo -O3), links one shared library, and records `ptxas -v` output
-(registers / spills / shared memory per kernel) in build/ptxas.txt.
+(registers / spills / shared memory per kernel) in build/ptxas_<source>.txt.
 """
 from __future__ import annotations
 
@@ -62,9 +62,9 @@ def build(verbose: bool = False) -> str:
             futs = {ex.submit(_compile, s, o, inc): s for s, o in jobs}
             for f in cf.as_completed(futs):
                 logs[futs[f]] = f.result()
-        with open(os.path.join(BUILD, "ptxas.txt"), "a") as fh:
-            for s, log in sorted(logs.items()):
-                fh.write(f"==== {os.path.basename(s)}\n{log}\n")
+        for s, log in logs.items():  # one file per source, rewritten with its object
+            with open(os.path.join(BUILD, "ptxas_" + os.path.basename(s)[:-3] + ".txt"), "w") as fh:
+                fh.write(log)
     if jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", libdir, "-l:libnccl.so.2",
                "-Xlinker", f"-rpath={libdir}"]
