@@ -62,6 +62,14 @@ __device__ __forceinline__ void ld16(const float* p, float* v) {
   float4 a = *reinterpret_cast<const float4*>(p);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
 }
+__device__ __forceinline__ void unpack8(const uint4& a, float* v) {  // 8 bf16 -> fp32
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x; v[2 * i + 1] = f.y;
+  }
+}
 __device__ __forceinline__ void ld16(const __nv_bfloat16* p, float* v) {
   uint4 a = *reinterpret_cast<const uint4*>(p);
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);

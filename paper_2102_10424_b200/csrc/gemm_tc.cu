@@ -135,8 +135,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 // Epilogue of one 16-column chunk of one output row: v = accumulator values.
+// `pre`: the chunk's 16 `add` values (two 16-byte vectors) loaded ahead of time, or nullptr.
 template <bool OUT_F32>
-__device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, int col, int N, float* v) {
+__device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, int col, int N, float* v,
+                                          const uint4* pre) {
   const bool full16 = col + 16 <= N;
   if (E.rscale) {  // per-row scale of the columns >= rs_from (sc = rscale[row], loaded once per tile)
 #pragma unroll
@@ -145,7 +147,13 @@ __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, i
   }
   if (E.add) {
     const bf16* ap = E.add + row * E.ldadd + col;
-    if (full16 && ((((uintptr_t)ap) & 15) == 0)) {
+    if (pre) {
+      float t[16];
+      unpack8(pre[0], t);
+      unpack8(pre[1], t + 8);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] += t[i];
+    } else if (full16 && ((((uintptr_t)ap) & 15) == 0)) {
       float t[16];
       ld16(ap, t);
       ld16(ap + 8, t + 8);
@@ -413,17 +421,33 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
       const int64_t row = T.out_row0 + r;
       const bool live = r < T.rows_valid;
       const float sc = (T.E.rscale && live) ? T.E.rscale[row] : 1.f;  // before the wait: overlaps the MMA
+      // `add` is read one 32-column chunk ahead (the first before the accumulator wait), so its
+      // latency overlaps the MMA / the previous chunk instead of serialising the epilogue
+      const bf16* arow = T.E.add ? T.E.add + row * T.E.ldadd + T.n0 : nullptr;
+      const bool avec = arow && live && ((((uintptr_t)arow) & 15) == 0) && ((T.E.ldadd & 7) == 0);
+      uint4 cur[4], nxt[4];
+      bool cur_ok = avec && 32 <= T.N - T.n0;
+      if (cur_ok)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow) + i);
       mbar_wait(&accf[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
+        const bool nxt_ok = avec && c + 32 < BN && c + 64 <= T.N - T.n0;
+        if (nxt_ok)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
         float v[32];
         tmem_ld32(trow + c, v);
         if (live && T.n0 + c < T.N) {
-          epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v);
-          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16);
+          epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
+          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+        cur_ok = nxt_ok;
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();

@@ -859,13 +859,17 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
           else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
         }
-        if (bd) {  // intra-cluster part on tensor cores, then the sparse kernel adds the rest in place
-          bfw.push_back(BdOp{l == 0 ? (const bf16*)c->X : (const bf16*)C, l == 0 ? pad8(c->dims[0]) : sh.Kp,
-                             l == 0 ? c->n : (int64_t)nb, sh.half, (void*)(C + sh.half), sh.Kp, nullptr, 0,
-                             sl.scale, sl.desc_dev, l == 0 ? 1 : 0});
+        if (bd) {  // intra-cluster part on tensor cores, then the sparse kernel adds the rest in place.
+          // Layer 0 reads the batch-local X_b rows the batch build copied into the left half
+          // (L2-resident) rather than gathering rows of the global X from HBM.
+          bfw.push_back(BdOp{(const bf16*)C, sh.Kp, (int64_t)nb, sh.half, (void*)(C + sh.half), sh.Kp, nullptr, 0,
+                             sl.scale, sl.desc_dev, 0});
           a.add = C + sh.half; a.ld_add = sh.Kp;
           a.few_nnz = 1;
-          if (l == 0) { a.self_out = nullptr; g.batch.xdst[j] = (bf16*)C; }
+          if (l == 0) {
+            a.self_out = nullptr; a.h_index = nullptr; a.H = C; a.ldh = sh.Kp;
+            g.batch.xdst[j] = (bf16*)C;
+          }
           g.bd_fl[l] += 2.0 * q * c->bs * c->bs * sh.half;
         }
         g.fwd_by[l] += spmm_bytes(a);

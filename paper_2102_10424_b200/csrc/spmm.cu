@@ -34,7 +34,8 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
 }
 
 template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE>
-__global__ void __launch_bounds__(256, ((J == 1 && sizeof(TI) == 2) || UNROLL == 1) ? 4 : (J <= 2 ? 3 : 2))
+__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
+                                           : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
   const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
   constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
@@ -348,7 +349,7 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   const int nchunks = (int)cdiv(w, CW);
   const int64_t groups = rows * nchunks;
   const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
-  if (G.a[0].few_nnz && J <= 2) {  // few neighbours per row: occupancy over in-flight loads
+  if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
     const bool wide = G.a[0].h_index != nullptr;
     if (G.a[0].colscale) {
       if (wide) k_spmm<TI, TO, LPR, J, 1, true, true><<<grid, 256, 0, s>>>(G, nchunks);
