@@ -128,6 +128,8 @@ struct Epi {
   int rs_from;
   const bf16* add;
   int64_t ldadd;
+  uint32_t* mbits;
+  int64_t ldmb;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -233,7 +235,7 @@ struct ProbPlain {
     T.rows_valid = S.M - m0;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0};
+    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0, S.mbits, S.ldmb};
     return T;
   }
 };
@@ -267,7 +269,7 @@ struct ProbBd {
     T.mb = &S.mb;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd};
+    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0};
     T.b_col = n0;
     T.K = G.bs;
     if (y >= q * mp) {  // inert dummy rows [n_b, rows): zeros
@@ -444,6 +446,15 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
         if (live && T.n0 + c < T.N) {
           epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
           if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+          if (T.E.mbits) {  // sign bits of the values as stored (bf16-rounded on the bf16 path)
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+              bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
+            }
+            T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
+          }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
@@ -576,6 +587,8 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.relu = o.relu ? 1 : 0;
     S.rscale = o.rscale;
     S.rs_from = o.rs_from;
+    S.mbits = o.mbits;
+    S.ldmb = o.ldmb;
     S.M = (int)o.M;
     S.N = (int)o.N;
     S.K = (int)o.K;

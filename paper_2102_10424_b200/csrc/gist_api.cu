@@ -53,6 +53,7 @@ struct Slot {
   int64_t *b_beg = nullptr, *b_end = nullptr, *stats = nullptr;
   // activations (element type T of the precision mode)
   std::vector<void*> C, H, dZ;
+  std::vector<uint32_t*> mb;  // BF16: bit-packed ReLU masks of C_l / H_l (l >= 1), words [nb_max x mb_ld[l]]
   void* dC = nullptr;
   float* logits = nullptr;
   float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
@@ -125,6 +126,7 @@ struct gist_ctx {
   float *Gall = nullptr, *Mall = nullptr, *Vall = nullptr;  // same packing: gradients, Adam moments
   bf16* Wball = nullptr;                       // bf16 shadow of Wall (BF16 mode)
   int nb_max_rows = 0;                         // static row count of every batch launch
+  std::vector<int64_t> mb_ld;                  // words per row of Slot::mb[l]
   StepState* dstate = nullptr;                 // device step state (z, t, lr)
   StepState* hstate = nullptr;                 // pinned host staging for it
   cudaEvent_t hstate_ev = nullptr;
@@ -742,6 +744,13 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     s.C.assign(c->L, nullptr);
     s.H.assign(c->L, nullptr);
     s.dZ.assign(c->L, nullptr);
+    s.mb.assign(c->L, nullptr);
+    c->mb_ld.assign(c->L, 0);
+    for (int l = 1; l < c->L && c->prec == GIST_PREC_BF16; ++l) {
+      c->mb_ld[l] = cdiv(maxK[l], 32);
+      TRY(dalloc_t(c, &s.mb[l], (size_t)nbm * c->mb_ld[l]));
+      CK(cudaMemsetAsync(s.mb[l], 0, (size_t)nbm * c->mb_ld[l] * 4, c->stream));
+    }
     for (int l = 0; l < c->L; ++l) {  // zero-initialised: padding columns must read as 0
       TRY(dalloc(c, &s.C[l], (size_t)nbm * maxK[l] * E));
       CK(cudaMemsetAsync(s.C[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
@@ -878,7 +887,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         if (l + 1 < L) {
           void* out = sage ? sl.C[l + 1] : sl.H[l + 1];
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, shp[l + 1].Kp, false, true,
-                              nullptr, 0, nullptr, 0});
+                              nullptr, 0, nullptr, 0, tc ? sl.mb[l + 1] : nullptr, tc ? c->mb_ld[l + 1] : 0});
         } else {
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false,
                               nullptr, 0, nullptr, 0});
@@ -898,6 +907,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
           b.desc = sl.desc_dev; b.st = c->dstate; b.q = q; b.max_cluster = slab_max;
           b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
+          if (tc) { b.mbits = sl.mb[l]; b.ld_mbits = c->mb_ld[l]; }  // ReLU mask of C_l / H_l as bits
           if (sage && bd) {  // dZ_{l-1} = (dC_self + A_blocks dC'_neigh + A_inter dC'_neigh) * 1[H_l > 0]
             bbw.push_back(BdOp{(const bf16*)sl.dC + sh.half, sh.Kp, (int64_t)nb, sh.half, sl.dZ[l - 1],
                                shp[l - 1].Np, (const bf16*)sl.dC, sh.Kp, nullptr, sl.desc_dev, 0});

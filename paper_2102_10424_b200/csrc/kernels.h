@@ -33,6 +33,8 @@ struct SpmmArgs {
   int64_t ld_add = 0;
   const TI* mask = nullptr;
   int64_t ld_mask = 0;
+  const uint32_t* mbits = nullptr;  // bit-packed form of `mask` (GemmOp::mbits); used instead if set
+  int64_t ld_mbits = 0;
   TO* out = nullptr;
   int64_t ldo = 0;
   TI* self_out = nullptr;
@@ -82,6 +84,10 @@ struct GemmOp {
   int64_t ldm;
   const float* rscale;  // optional per-row scale of the output columns >= rs_from (BF16 path)
   int rs_from;
+  // optional (BF16 path): bit-packed ReLU mask of the stored output, bit (col % 32) of word
+  // [row * ldmb + col / 32] = 1[out[row, col] > 0] (read by the backward pass instead of out)
+  uint32_t* mbits = nullptr;
+  int64_t ldmb = 0;
 };
 }  // namespace gist
 #include <cuda.h>
@@ -91,7 +97,8 @@ struct alignas(64) GemmSlotTC {
   void* C;
   const void* mask;
   const float* rscale;
-  int64_t ldc, ldm;
+  uint32_t* mbits;
+  int64_t ldc, ldm, ldmb;
   int M, N, K, relu, rs_from;
 };
 struct GemmGroupTC {

@@ -147,7 +147,11 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
 #pragma unroll
       for (int i = 0; i < V; ++i) o[i] += t[i];
     }
-    if (a.mask) {
+    if (a.mbits) {  // bit-packed ReLU mask: 4 bytes per 32 columns instead of 2-4 bytes per column
+      const uint32_t wd = a.mbits[v * a.ld_mbits + (c >> 5)] >> (c & 31);
+#pragma unroll
+      for (int i = 0; i < V; ++i) o[i] = (wd >> i) & 1u ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
+    } else if (a.mask) {
       float t[V];
       unpack(*reinterpret_cast<const uint4*>(a.mask + v * a.ld_mask + c), t, TI());
 #pragma unroll
