@@ -2,6 +2,7 @@
 // Not shared with oracle/ (the oracle carries its own Philox; both are pinned to
 // the Random123 known-answer vectors).
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -88,6 +89,32 @@ __device__ __forceinline__ void st16(__nv_bfloat16* p, const float* v) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = a;
+}
+
+
+// ---- programmatic dependent launch (PDL) ------------------------------------------------
+// Every kernel of a subTrain step is launched with programmatic stream serialisation: it may
+// be scheduled while its predecessor drains, and calls pdl_wait() (griddepcontrol.wait:
+// the predecessor grid has completed and its writes are visible) before its first global
+// memory access, then pdl_trigger() so its own successor can be scheduled early (the
+// successor still launches only once every CTA of this grid has started).  Both are no-ops
+// for a kernel launched without the attribute.  GIST_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline void launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
 }  // namespace gist

@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
   __shared__ int32_t sdesc[Prob::kMaxDesc * kMaxGroup];
-  Prob::stage(G, sdesc);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < CF::STAGES; ++s) {
@@ -330,6 +329,11 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
                  "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // prologue above (barriers, TMEM) overlaps the predecessor kernel's tail under PDL;
+  // everything below may read what it wrote
+  pdl_wait();
+  pdl_trigger();
+  Prob::stage(G, sdesc);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -527,7 +531,7 @@ void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
     attr = true;
   }
   const int grid = total < num_sms() ? total : num_sms();
-  if (grid > 0) kern<<<grid, 192, SMEM, s>>>(G);
+  if (grid > 0) launch_pdl(kern, grid, 192, SMEM, s, G);
 }
 
 template <int BN, bool A_MN, bool B_MN>

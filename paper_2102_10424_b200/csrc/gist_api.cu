@@ -20,6 +20,11 @@
 
 using namespace gist;
 
+bool gist::pdl_enabled() {
+  static const bool on = [] { const char* e = std::getenv("GIST_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 namespace {
 
 enum State { S_CREATED = 0, S_GRAPH = 1, S_PARAMS = 2, S_PARTITIONED = 3 };

@@ -100,6 +100,8 @@ void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cud
 // grid (cdiv(nb_max, 256), slots)
 __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_t* __restrict__ cstart,
                               const int64_t* __restrict__ rp) {
+  pdl_wait();
+  pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
   const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
@@ -133,7 +135,7 @@ __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_
 }
 void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s) {
   const int n = G.nb_max > G.q ? G.nb_max : G.q;
-  k_batch_setup<<<dim3((unsigned)cdiv(n > 0 ? n : 1, 256), (unsigned)G.n), 256, 0, s>>>(G, cstart, rp);
+  launch_pdl(k_batch_setup, dim3((unsigned)cdiv(n > 0 ? n : 1, 256), (unsigned)G.n), 256, 0, s, G, cstart, rp);
 }
 
 // One warp per batch row: walk the row's global adjacency 64 entries per iteration
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
                                                      const int32_t* __restrict__ cid, int arch,
                                                      const int32_t* __restrict__ labels,
                                                      const uint8_t* __restrict__ split, int skip_intra) {
+  pdl_wait();
+  pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
   const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
@@ -220,7 +224,7 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
                  const int32_t* cid, int arch, const int32_t* labels, const uint8_t* split, int skip_intra,
                  cudaStream_t s) {
   if (G.nb_max <= 0) return;
-  k_batch_build<<<dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s>>>(G, rp, col, ccol, cid, arch,
+  launch_pdl(k_batch_build, dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s, G, rp, col, ccol, cid, arch,
                                                                                   labels, split, skip_intra);
 }
 

@@ -14,6 +14,8 @@ constexpr int BM = 128, BN = 128, BK = 8, PAD = 4;
 
 template <bool TA, bool TB, bool RELU, bool MASK>
 __global__ void __launch_bounds__(256) k_sgemm(const __grid_constant__ SgemmGroup G) {
+  pdl_wait();
+  pdl_trigger();
   const GemmOp& op = G.op[blockIdx.z];  // one sub-GCN slot per grid layer
   const int M = (int)op.M, N = (int)op.N, K = (int)op.K;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -100,10 +102,10 @@ template <bool TA, bool TB>
 void launch(const SgemmGroup& g, int64_t maxM, int64_t maxN, cudaStream_t s) {
   dim3 grid((unsigned)cdiv(maxN, BN), (unsigned)cdiv(maxM, BM), (unsigned)g.n);
   const bool relu = g.op[0].relu, mask = g.op[0].mask != nullptr;
-  if (relu && mask) k_sgemm<TA, TB, true, true><<<grid, 256, 0, s>>>(g);
-  else if (relu) k_sgemm<TA, TB, true, false><<<grid, 256, 0, s>>>(g);
-  else if (mask) k_sgemm<TA, TB, false, true><<<grid, 256, 0, s>>>(g);
-  else k_sgemm<TA, TB, false, false><<<grid, 256, 0, s>>>(g);
+  if (relu && mask) launch_pdl(k_sgemm<TA, TB, true, true>, grid, 256, 0, s, g);
+  else if (relu) launch_pdl(k_sgemm<TA, TB, true, false>, grid, 256, 0, s, g);
+  else if (mask) launch_pdl(k_sgemm<TA, TB, false, true>, grid, 256, 0, s, g);
+  else launch_pdl(k_sgemm<TA, TB, false, false>, grid, 256, 0, s, g);
 }
 }  // namespace
 

@@ -37,6 +37,8 @@ template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, boo
 __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
                                            : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
+  pdl_wait();
+  pdl_trigger();
   const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
   constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
   constexpr int GPW = 32 / LPR;      // groups per warp
@@ -181,6 +183,8 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
 template <typename TI, typename TO, int LPR, int J, bool CSCALE>
 __global__ void __launch_bounds__(512, 2)
     k_spmm_ct(const __grid_constant__ SpmmGroup<TI, TO> G, int ntiles) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint4 slab[];
   constexpr int V = Elem<TI>::kVec;
   constexpr int TV = LPR * J;  // vectors per row in the tile
@@ -343,8 +347,8 @@ void launch_ct(const SpmmGroup<TI, TO>& G, int64_t w, int maxc, cudaStream_t s) 
     attr = true;
   }
   const dim3 grid((unsigned)((G.a[0].q + 1) * ntiles), (unsigned)G.n);  // + dummy-row CTA per tile
-  if (G.a[0].colscale) k_spmm_ct<TI, TO, LPR, J, true><<<grid, 512, smem, s>>>(G, ntiles);
-  else k_spmm_ct<TI, TO, LPR, J, false><<<grid, 512, smem, s>>>(G, ntiles);
+  if (G.a[0].colscale) launch_pdl(k_spmm_ct<TI, TO, LPR, J, true>, grid, 512, smem, s, G, ntiles);
+  else launch_pdl(k_spmm_ct<TI, TO, LPR, J, false>, grid, 512, smem, s, G, ntiles);
 }
 
 template <typename TI, typename TO, int LPR, int J>
@@ -356,11 +360,11 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
     const bool wide = G.a[0].h_index != nullptr;
     if (G.a[0].colscale) {
-      if (wide) k_spmm<TI, TO, LPR, J, 1, true, true><<<grid, 256, 0, s>>>(G, nchunks);
-      else k_spmm<TI, TO, LPR, J, 1, true, false><<<grid, 256, 0, s>>>(G, nchunks);
+      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, true>, grid, 256, 0, s, G, nchunks);
+      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, false>, grid, 256, 0, s, G, nchunks);
     } else {
-      if (wide) k_spmm<TI, TO, LPR, J, 1, false, true><<<grid, 256, 0, s>>>(G, nchunks);
-      else k_spmm<TI, TO, LPR, J, 1, false, false><<<grid, 256, 0, s>>>(G, nchunks);
+      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, true>, grid, 256, 0, s, G, nchunks);
+      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, false>, grid, 256, 0, s, G, nchunks);
     }
     return;
   }
@@ -371,10 +375,10 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     const SpmmArgs<TI, TO>& a = G.a[i];
     wide |= a.h_index != nullptr || a.rows * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
   }
-  if (!wide && cs) k_spmm<TI, TO, LPR, J, UNROLL, true, false><<<grid, 256, 0, s>>>(G, nchunks);
-  else if (!wide) k_spmm<TI, TO, LPR, J, UNROLL, false, false><<<grid, 256, 0, s>>>(G, nchunks);
-  else if (cs) k_spmm<TI, TO, LPR, J, UNROLL, true, true><<<grid, 256, 0, s>>>(G, nchunks);
-  else k_spmm<TI, TO, LPR, J, UNROLL, false, true><<<grid, 256, 0, s>>>(G, nchunks);
+  if (!wide && cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, false>, grid, 256, 0, s, G, nchunks);
+  else if (!wide) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, false>, grid, 256, 0, s, G, nchunks);
+  else if (cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, true>, grid, 256, 0, s, G, nchunks);
+  else launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, true>, grid, 256, 0, s, G, nchunks);
 }
 
 }  // namespace

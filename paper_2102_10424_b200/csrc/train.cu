@@ -12,6 +12,8 @@ namespace gist {
 // padding columns [k, ld) are written as 0.
 template <typename T>
 __global__ void k_softmax_ce(const __grid_constant__ CeGroup<T> G) {
+  pdl_wait();
+  pdl_trigger();
   const CeSlot<T>& S = G.s[blockIdx.y];
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -43,7 +45,7 @@ __global__ void k_softmax_ce(const __grid_constant__ CeGroup<T> G) {
 template <typename T>
 void softmax_ce(const CeGroup<T>& G, cudaStream_t s) {
   if (G.rows <= 0 || G.n <= 0) return;
-  k_softmax_ce<T><<<dim3((unsigned)cdiv(G.rows, 8), (unsigned)G.n), 256, 0, s>>>(G);
+  launch_pdl(k_softmax_ce<T>, dim3((unsigned)cdiv(G.rows, 8), (unsigned)G.n), 256, 0, s, G);
 }
 template void softmax_ce<float>(const CeGroup<float>&, cudaStream_t);
 template void softmax_ce<bf16>(const CeGroup<bf16>&, cudaStream_t);
@@ -51,6 +53,8 @@ template void softmax_ce<bf16>(const CeGroup<bf16>&, cudaStream_t);
 // one CTA per slot, fixed-order tree: deterministic
 template <typename T>
 __global__ void __launch_bounds__(1024) k_reduce_loss(const __grid_constant__ CeGroup<T> G) {
+  pdl_wait();
+  pdl_trigger();
   const CeSlot<T>& S = G.s[blockIdx.x];
   using Red = cub::BlockReduce<float, 1024>;
   __shared__ typename Red::TempStorage tr;
@@ -67,7 +71,7 @@ __global__ void __launch_bounds__(1024) k_reduce_loss(const __grid_constant__ Ce
 template <typename T>
 void reduce_loss(const CeGroup<T>& G, cudaStream_t s) {
   if (G.n <= 0) return;
-  k_reduce_loss<T><<<(unsigned)G.n, 1024, 0, s>>>(G);
+  launch_pdl(k_reduce_loss<T>, (unsigned)G.n, 1024, 0, s, G);
 }
 template void reduce_loss<float>(const CeGroup<float>&, cudaStream_t);
 template void reduce_loss<bf16>(const CeGroup<bf16>&, cudaStream_t);
@@ -78,6 +82,8 @@ template void reduce_loss<bf16>(const CeGroup<bf16>&, cudaStream_t);
 __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float* __restrict__ M,
                        float* __restrict__ V, int64_t n, float b1, float b2, float eps,
                        const StepState* __restrict__ st, bf16* __restrict__ Wb) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float s_step, s_bc2;
   if (threadIdx.x == 0) {
     const double t = (double)(st->t + 1);
@@ -113,11 +119,13 @@ void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1
                const StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n >> 2, 256) < 148 * 8 ? cdiv(n >> 2, 256) : 148 * 8;
-  k_adam<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(W, G, M, V, n, b1, b2, eps, st, Wb);
+  launch_pdl(k_adam, (unsigned)(blocks > 0 ? blocks : 1), 256, 0, s, W, G, M, V, n, b1, b2, eps, st, Wb);
 }
 
 __global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, const StepState* st,
                       bf16* __restrict__ Wb) {
+  pdl_wait();
+  pdl_trigger();
   const float lr = st->lr;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float w = W[i] - lr * G[i];
@@ -128,14 +136,16 @@ __global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_
 void sgd_step(float* W, const float* G, int64_t n, const StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
-  k_sgd<<<(unsigned)blocks, 256, 0, s>>>(W, G, n, st, Wb);
+  launch_pdl(k_sgd, (unsigned)blocks, 256, 0, s, W, G, n, st, Wb);
 }
 
 __global__ void k_step_advance(StepState* st) {
+  pdl_wait();
+  pdl_trigger();
   st->z += 1;
   st->t += 1;
 }
-void step_advance(StepState* st, cudaStream_t s) { k_step_advance<<<1, 1, 0, s>>>(st); }
+void step_advance(StepState* st, cudaStream_t s) { launch_pdl(k_step_advance, 1, 1, 0, s, st); }
 
 __global__ void k_f32_to_bf16(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
