@@ -1102,7 +1102,7 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     int id = -1;
     if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + g.count * c->nb_max_rows * 45.0, 4.0, nnz_slot);
     batch_setup(g.batch, c->cstart, c->rp, s);
-    batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->arch, c->labels, c->split,
+    batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
                 c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, s);
     prof_end(c, s, id);
     c->nk += 2;

@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace gist {
 
 // ---------------------------------------------------------------- relabel --
@@ -138,17 +140,26 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
   launch_pdl(k_batch_setup, dim3((unsigned)cdiv(n > 0 ? n : 1, 256), (unsigned)G.n), 256, 0, s, G, cstart, rp);
 }
 
-// One warp per batch row: walk the row's global adjacency 64 entries per iteration
-// (two independent load chains col -> cid -> map64 in flight), keep the in-batch
-// neighbours (ballot compaction, original order), and write the row's normalisation
-// scale, label and train flag.  Counters are warp -> block reduced, one integer atomic
-// per block (integer addition: deterministic).  grid (cdiv(nb_max, 8), slots).
-__global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ BatchGroup G,
-                                                     const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                                     const int32_t* __restrict__ ccol,
-                                                     const int32_t* __restrict__ cid, int arch,
-                                                     const int32_t* __restrict__ labels,
-                                                     const uint8_t* __restrict__ split, int skip_intra) {
+// One warp per batch row: walk the row's global adjacency 128 entries per round (four
+// independent coalesced (col, ccol) load pairs per lane in flight), keep the in-batch
+// neighbours (ballot compaction, original order), and write the row's normalisation scale,
+// label and train flag.  SMAP: the step's cluster -> local-offset map (q entries, the rest
+// "absent") is built in shared memory from the step descriptor by every block, so the
+// per-edge membership test is a shared-memory lookup; otherwise the tagged global map64.
+// Counters are warp -> block reduced, one integer atomic per block (integer addition:
+// deterministic).  grid (cdiv(nb_max, 16), slots), 512 threads.
+constexpr int kBuildRows = 16;
+constexpr int32_t kAbsent = INT32_MIN;  // |loff - cstart| < 2^31 - 1: never a real offset
+template <bool SMAP>
+__global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ BatchGroup G,
+                                                        const int64_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ col,
+                                                        const int32_t* __restrict__ ccol,
+                                                        const int32_t* __restrict__ cid, int arch,
+                                                        const int32_t* __restrict__ labels,
+                                                        const uint8_t* __restrict__ split, int skip_intra,
+                                                        const int64_t* __restrict__ cstart, int num_clusters) {
+  extern __shared__ int32_t smap[];  // SMAP: [num_clusters]
   pdl_wait();
   pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
@@ -156,9 +167,16 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
   const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
   const int nb = d[2 * q];
   const uint32_t tag = (uint32_t)d[3 * q + 3];
-  __shared__ int s_cnt[8], s_tr[8];
+  if (SMAP) {
+    for (int i = threadIdx.x; i < num_clusters; i += blockDim.x) smap[i] = kAbsent;
+    __syncthreads();
+    const int qq = d[3 * q + 2];
+    for (int k = threadIdx.x; k < qq; k += blockDim.x) smap[d[k]] = d[q + k] - (int32_t)cstart[d[k]];
+    __syncthreads();
+  }
+  __shared__ int s_cnt[kBuildRows], s_tr[kBuildRows];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int v = blockIdx.x * 8 + w;
+  const int v = blockIdx.x * kBuildRows + w;
   int cnt = 0, tr = 0;
   if (v < nb) {
     const int64_t g = S.b_nodes[v];
@@ -168,28 +186,35 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
     int intra = 0;  // in-batch intra-cluster neighbours (skip_intra: counted, not stored)
     const int32_t cg = skip_intra ? cid[g] : -1;
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t base = rp[g]; base < end; base += 64) {
-      const int64_t e0 = base + lane, e1 = base + 32 + lane;
-      const int32_t u0 = e0 < end ? col[e0] : -1;   // col and its cluster: independent,
-      const int32_t u1 = e1 < end ? col[e1] : -1;   // coalesced loads (no cid[col] chain)
-      const int32_t c0 = e0 < end ? ccol[e0] : 0;
-      const int32_t c1 = e1 < end ? ccol[e1] : 0;
-      const uint64_t m0 = u0 >= 0 ? S.map64[c0] : 0ull;
-      const uint64_t m1 = u1 >= 0 ? S.map64[c1] : 0ull;
-      bool in0 = u0 >= 0 && (uint32_t)(m0 >> 32) == tag;
-      bool in1 = u1 >= 0 && (uint32_t)(m1 >> 32) == tag;
-      if (skip_intra) {
-        const bool i0 = in0 && c0 == cg, i1 = in1 && c1 == cg;
-        intra += __popc(__ballot_sync(0xffffffffu, i0)) + __popc(__ballot_sync(0xffffffffu, i1));
-        in0 &= !i0;
-        in1 &= !i1;
+    for (int64_t base = rp[g]; base < end; base += 128) {
+      int32_t u[4], cc[4], dl[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // col and its cluster: independent, coalesced loads
+        const int64_t e = base + r * 32 + lane;
+        u[r] = e < end ? col[e] : -1;
+        cc[r] = e < end ? ccol[e] : 0;
       }
-      const unsigned b0 = __ballot_sync(0xffffffffu, in0);
-      const unsigned b1 = __ballot_sync(0xffffffffu, in1);
-      if (in0) S.b_col[out + __popc(b0 & lt)] = u0 + (int32_t)(uint32_t)m0;
-      out += __popc(b0);
-      if (in1) S.b_col[out + __popc(b1 & lt)] = u1 + (int32_t)(uint32_t)m1;
-      out += __popc(b1);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (SMAP) {
+          dl[r] = u[r] >= 0 ? smap[cc[r]] : kAbsent;
+        } else {
+          const uint64_t m = u[r] >= 0 ? S.map64[cc[r]] : 0ull;
+          dl[r] = (u[r] >= 0 && (uint32_t)(m >> 32) == tag) ? (int32_t)(uint32_t)m : kAbsent;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        bool in = dl[r] != kAbsent;
+        if (skip_intra) {
+          const bool ii = in && cc[r] == cg;
+          intra += __popc(__ballot_sync(0xffffffffu, ii));
+          in &= !ii;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, in);
+        if (in) S.b_col[out + __popc(bm & lt)] = u[r] + dl[r];
+        out += __popc(bm);
+      }
     }
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
     if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
@@ -215,17 +240,30 @@ __global__ void __launch_bounds__(256) k_batch_build(const __grid_constant__ Bat
   __syncthreads();
   if (threadIdx.x == 0) {
     long long a = 0, b = 0;
-    for (int k = 0; k < 8; ++k) a += s_cnt[k], b += s_tr[k];
+    for (int k = 0; k < kBuildRows; ++k) a += s_cnt[k], b += s_tr[k];
     if (a) atomicAdd((unsigned long long*)&S.stats[0], (unsigned long long)a);
     if (b) atomicAdd((unsigned long long*)&S.stats[1], (unsigned long long)b);
   }
 }
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
-                 const int32_t* cid, int arch, const int32_t* labels, const uint8_t* split, int skip_intra,
-                 cudaStream_t s) {
+                 const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
+                 const uint8_t* split, int skip_intra, cudaStream_t s) {
   if (G.nb_max <= 0) return;
-  launch_pdl(k_batch_build, dim3((unsigned)cdiv(G.nb_max, 8), (unsigned)G.n), 256, 0, s, G, rp, col, ccol, cid, arch,
-                                                                                  labels, split, skip_intra);
+  const dim3 grid((unsigned)cdiv(G.nb_max, kBuildRows), (unsigned)G.n);
+  const size_t smem = (size_t)num_clusters * 4;
+  const char* force = std::getenv("GIST_BATCH_GLOBAL_MAP");  // tests: exercise the global-map path
+  if (smem <= 64 * 1024 && !(force && force[0] == '1')) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_batch_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      attr = true;
+    }
+    launch_pdl(k_batch_build<true>, grid, kBuildRows * 32, smem, s, G, rp, col, ccol, cid, arch, labels, split,
+               skip_intra, cstart, num_clusters);
+  } else {
+    launch_pdl(k_batch_build<false>, grid, kBuildRows * 32, 0, s, G, rp, col, ccol, cid, arch, labels, split,
+               skip_intra, cstart, num_clusters);
+  }
 }
 
 __global__ void k_edge_clusters(const int32_t* __restrict__ col, const int32_t* __restrict__ cid, int64_t nnz,

@@ -220,8 +220,8 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 // block-diagonal tensor-core path); the batch CSR then holds the inter-cluster edges only.
 // ccol[e] = cid[col[e]] (cluster of every edge's neighbour, precomputed at load)
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
-                 const int32_t* cid, int arch, const int32_t* labels, const uint8_t* split, int skip_intra,
-                 cudaStream_t s);
+                 const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
+                 const uint8_t* split, int skip_intra, cudaStream_t s);
 void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s);
 // Binary intra-cluster adjacency blocks: blocks[c][i][j] = 1 iff (cstart[c]+i, cstart[c]+j) is an
 // edge (relabelled ids), bf16 [num_clusters x bs x bs], zeroed by the caller.

@@ -86,6 +86,15 @@ def test_one_step_parity(name, kw, arch, dims, q, optimizer):
         assert abs(loss - tr["loss"]) <= ACT_TOL * max(1.0, abs(tr["loss"]))
 
 
+@pytest.mark.parametrize("case", [0, 1])
+def test_one_step_parity_global_cluster_map(case, monkeypatch):
+    """The batch build's global (tagged map64) membership path, taken when the cluster ->
+    offset map does not fit shared memory (> 16k clusters), forced here by env."""
+    monkeypatch.setenv("GIST_BATCH_GLOBAL_MAP", "1")
+    name, kw, arch, dims, q = CASES[case]
+    test_one_step_parity(name, kw, arch, dims, q, "sgd")
+
+
 @pytest.mark.parametrize("name,kw,arch,dims,q", CASES[:2])
 def test_rounds_parity(name, kw, arch, dims, q):
     """Several rounds (partition -> zeta steps -> aggregate): global weights <= 1e-3."""
