@@ -13,6 +13,7 @@
 // 32w..32w+31 = tile rows).  One output tile (128 x BN) per CTA.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -54,6 +55,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
+// TMA store of one staged box (shared -> global; out-of-bounds rows/columns are clipped)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // UMMA shared-memory descriptor: start, LBO, SBO in 16-byte units; version 1 (sm_100); SWIZZLE_128B.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -112,7 +123,9 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // epilogue staging for TMA stores: 4 warps x 2 buffers x (32 rows x 128 B)
+  static constexpr int EPI_BYTES = 4 * 2 * 4096;
+  static constexpr int SMEM_BASE = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
@@ -130,6 +143,8 @@ struct Epi {
   int64_t ldadd;
   uint32_t* mbits;
   int64_t ldmb;
+  const CUtensorMap* mc;  // TMA store map of C, or nullptr (direct stores)
+  int clip;               // rows >= rows_valid lie outside mc (TMA clips them): every warp may use it
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -138,7 +153,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 // Epilogue of one 16-column chunk of one output row: v = accumulator values.
 // `pre`: the chunk's 16 `add` values (two 16-byte vectors) loaded ahead of time, or nullptr.
-template <bool OUT_F32>
+template <bool OUT_F32, bool STORE = true>
 __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, int col, int N, float* v,
                                           const uint4* pre) {
   const bool full16 = col + 16 <= N;
@@ -177,6 +192,7 @@ __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, i
     for (int i = 0; i < 16; ++i)
       if (col + i < N && !(__bfloat162float(mp[i]) > 0.f)) v[i] = 0.f;
   }
+  if (!STORE) return;  // staged for a TMA store by the caller
   if (OUT_F32) {
     float* dst = (float*)E.C + row * E.ldc + col;
     if (full16 && (((uintptr_t)dst & 15) == 0)) {
@@ -215,6 +231,7 @@ struct Tile {
 template <int BN>
 struct ProbPlain {
   using Group = GemmGroupTC;
+  static constexpr bool kTmaEpi = true;  // epilogue staging + TMA stores
   static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
   static constexpr int kMaxDesc = 1;
   static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
@@ -235,7 +252,8 @@ struct ProbPlain {
     T.rows_valid = S.M - m0;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0, S.mbits, S.ldmb};
+    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0, S.mbits, S.ldmb,
+                 S.tma_store ? &S.mc : nullptr, 1};
     return T;
   }
 };
@@ -244,6 +262,9 @@ struct ProbPlain {
 template <int BN>
 struct ProbBd {
   using Group = BdGroup;
+  // direct stores: its tiles end at cluster boundaries (most warps would fall back anyway)
+  // and the 4-stage ring + descriptor staging leave no room for the staging buffers
+  static constexpr bool kTmaEpi = false;
   static __device__ __forceinline__ int mt_per(const Group& G) { return (G.bs + BM - 1) / BM; }
   static __device__ __forceinline__ int ydim(const Group& G) {
     return G.q * mt_per(G) + (int)((G.rows + BM - 1) / BM);
@@ -269,7 +290,7 @@ struct ProbBd {
     T.mb = &S.mb;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0};
+    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &S.mc : nullptr, 0};
     T.b_col = n0;
     T.K = G.bs;
     if (y >= q * mp) {  // inert dummy rows [n_b, rows): zeros
@@ -304,7 +325,8 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
   using CF = Cfg<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE_BYTES);
+  constexpr int EPI = Prob::kTmaEpi ? CF::EPI_BYTES : 0;
+  uint64_t* full = (uint64_t*)(smem + CF::STAGES * CF::STAGE_BYTES + EPI);  // after the epilogue staging
   uint64_t* empty = full + CF::STAGES;
   uint64_t* accf = empty + CF::STAGES;  // [2]
   uint64_t* acce = accf + 2;            // [2]
@@ -407,6 +429,8 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
   } else {  // ------------------------------------------------------------ epilogue warps 2..5
     const int lq = warp & 3;  // TMEM lane quarter this warp may access
     const int r = lq * 32 + lane;
+    uint8_t* epi_smem = smem + CF::STAGES * CF::STAGE_BYTES;  // [4 warps][2][32 x 128 B]
+    uint32_t tbox = 0;  // TMA-store boxes issued by this warp (buffer parity)
     uint32_t tc = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const Tile T = Prob::decode(G, t, sdesc);
@@ -439,15 +463,72 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
       mbar_wait(&accf[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
+      // TMA-store path: this warp's 32 rows are staged (128-byte rows, SWIZZLE_128B: 16-byte
+      // chunk j of row r at r*128 + ((j ^ (r & 7)) * 16), bank-conflict free) and written by
+      // one cp.async.bulk.tensor per 32 x 128 B box, so stores are full lines instead of one
+      // 16-byte piece of 32 different rows per instruction.
+      const bool tma = Prob::kTmaEpi && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
+      constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
+        // warp-uniform: the tile's remaining columns all lie beyond N (nothing to store; a
+        // staged-but-never-stored box would also break the buffer accounting below)
+        if (T.n0 + c >= T.N) break;
         const bool nxt_ok = avec && c + 32 < BN && c + 64 <= T.N - T.n0;
         if (nxt_ok)
 #pragma unroll
           for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
         float v[32];
         tmem_ld32(trow + c, v);
-        if (live && T.n0 + c < T.N) {
+        if (tma) {
+          const int cb = c % CPB;  // column of this piece inside its box
+          uint8_t* buf = epi_smem + (lq * 2 + (tbox & 1)) * 4096;
+          if (cb == 0) {  // the buffer written two boxes ago must have been read by its TMA store
+            if (lane == 0) bulk_wait_read1();
+            __syncwarp();
+          }
+          if (live && T.n0 + c < T.N) {
+            epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
+            if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+          }
+          uint8_t* rbase = buf + lane * 128;
+          if (OUT_F32) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(rbase + ((j ^ (lane & 7)) * 16)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 pk;
+              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
+              const int jj = (cb / 8) + j;  // 16-byte chunk index inside the 128-byte row
+              *reinterpret_cast<uint4*>(rbase + ((jj ^ (lane & 7)) * 16)) = pk;
+            }
+          }
+          if (cb + 32 == CPB || c + 32 == BN || T.n0 + c + 32 >= T.N) {  // box complete: store it
+            // (every box that advances tbox commits exactly one bulk group: wait_group.read 1
+            // above then guarantees the buffer about to be reused has been read)
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
+              bulk_commit();
+            }
+            ++tbox;
+          }
+          if (live && T.n0 + c < T.N && T.E.mbits) {
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+              bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
+            }
+            T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
+          }
+        } else if (live && T.n0 + c < T.N) {
           epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
           if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
           if (T.E.mbits) {  // sign bits of the values as stored (bf16-rounded on the bf16 path)
@@ -469,6 +550,8 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
       if (lane == 0) mbar_arrive(&acce[b]);
       ++tc;
     }
+    if (lane == 0) bulk_wait_all();  // every TMA store has landed before the grid completes
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -521,10 +604,28 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool tma_store_enabled() {  // GIST_TMA_STORE=0: direct epilogue stores (A/B measurements)
+  static const bool on = [] { const char* e = std::getenv("GIST_TMA_STORE"); return !(e && e[0] == '0'); }();
+  return on;
+}
+// Output store map: C [outer x inner] (ld elements), boxes of 32 rows x 128 bytes, SWIZZLE_128B.
+bool make_store_map(CUtensorMap* map, void* base, int64_t inner, int64_t outer, int64_t ld, bool f32) {
+  EncodeFn enc = get_encode();
+  const int64_t es = f32 ? 4 : 2;
+  if (!enc || ((uintptr_t)base & 15) || ((ld * es) & 15) || inner <= 0 || outer <= 0) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
+  cuuint32_t est[2] = {1, 1};
+  return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box,
+             est, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
 void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
   auto kern = k_gemm_persist<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
-  constexpr int SMEM = Cfg<BN, ST>::SMEM + 64;
+  constexpr int SMEM = Cfg<BN, ST>::SMEM_BASE + (Prob::kTmaEpi ? Cfg<BN, ST>::EPI_BYTES : 0) + 64;
   static bool attr = false;  // per instantiation
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -593,6 +694,7 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.rs_from = o.rs_from;
     S.mbits = o.mbits;
     S.ldmb = o.ldmb;
+    S.tma_store = tma_store_enabled() && make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
     S.M = (int)o.M;
     S.N = (int)o.N;
     S.K = (int)o.K;
@@ -635,6 +737,7 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.desc = o.desc;
     S.global_rows = o.global_rows;
     S.N = (int)o.N;
+    S.tma_store = 0;  // ProbBd::kTmaEpi == false
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;

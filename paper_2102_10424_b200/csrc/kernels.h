@@ -94,12 +94,13 @@ struct GemmOp {
 namespace gist {
 struct alignas(64) GemmSlotTC {
   CUtensorMap ma, mb;  // TMA descriptors (128 B each)
+  CUtensorMap mc;      // output store map (boxes of 32 rows x 128 B, SWIZZLE_128B); valid if tma_store
   void* C;
   const void* mask;
   const float* rscale;
   uint32_t* mbits;
   int64_t ldc, ldm, ldmb;
-  int M, N, K, relu, rs_from;
+  int M, N, K, relu, rs_from, tma_store;
 };
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGroup];
@@ -133,12 +134,13 @@ struct BdOp {
 };
 struct alignas(64) BdSlot {
   CUtensorMap mb;
+  CUtensorMap mc;  // output store map (see GemmSlotTC::mc); valid if tma_store
   void* C;
   const bf16* add;
   const float* rscale;
   const int32_t* desc;
   int64_t ldc, ldadd;
-  int N, global_rows;
+  int N, global_rows, tma_store;
 };
 struct BdGroup {
   CUtensorMap ma;  // all cluster blocks [num_clusters * BS, BS]

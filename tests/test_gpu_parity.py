@@ -200,3 +200,38 @@ def test_kernel_spmm_and_gemm_entry_points():
         torch.cuda.synchronize()
         ref = (a.T if ta else a).astype(np.float64) @ (b.T if tb else b).astype(np.float64)
         assert rel_err(c.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K,out_f32", [
+    (0, 0, 3120, 512, 1216, False),   # forward a3 (several tiles per persistent CTA, ragged last M tile)
+    (0, 1, 3120, 1024, 512, False),   # dX
+    (1, 0, 1216, 512, 3120, True),    # dW, fp32 out
+    (0, 0, 3120, 48, 1024, True),     # last layer, fp32 logits (N < one 128-byte box)
+    (0, 0, 777, 136, 200, False),     # N not a multiple of the tile, small
+    (0, 1, 300, 131, 64, True),       # ldc*4 not 16-byte aligned: direct-store epilogue
+    (0, 0, 12480, 512, 1024, False),  # ~3 tiles per persistent CTA (the grouped step's regime)
+    (0, 1, 12480, 1024, 512, False),
+    (1, 0, 4864, 512, 3120, True),
+    (0, 0, 24960, 48, 1024, True),    # narrow N, many tiles per CTA (logits of a grouped step)
+])
+def test_kernel_gemm_bf16_tcgen05_shapes(ta, tb, M, N, K, out_f32):
+    """tcgen05 GEMM entry point (gist_gemm dtype 1) at the subTrain step's shapes against an
+    fp64 product of the same bf16-rounded operands (fp32 out: 1e-5; bf16 out: one bf16
+    rounding of the result, 2^-8 relative)."""
+    import torch
+    from paper_2102_10424_b200 import gist
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(M * 7 + N)
+    a = torch.randn((K, M) if ta else (M, K), generator=g).to(torch.bfloat16)
+    b = torch.randn((N, K) if tb else (K, N), generator=g).to(torch.bfloat16)
+    ad, bd = a.to(dev), b.to(dev)
+    c = torch.zeros((M, N), dtype=torch.float32 if out_f32 else torch.bfloat16, device=dev)
+    gist.gemm(bool(ta), bool(tb), M, N, K, ad.data_ptr(), a.shape[1], bd.data_ptr(), b.shape[1], c.data_ptr(), N, 1,
+              out_f32=out_f32)
+    torch.cuda.synchronize()
+    A = (a.T if ta else a).double().numpy()
+    B = (b.T if tb else b).double().numpy()
+    ref = A @ B
+    got = c.float().cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref) / (np.abs(ref) + np.sqrt(K))  # |ref| ~ sqrt(K) for unit normal operands
+    assert err.max() <= (1e-5 if out_f32 else 2.0 ** -8), err.max()
