@@ -24,6 +24,9 @@ namespace gist {
 namespace {
 
 constexpr int BM = 128;
+// epilogue warps: two per TMEM lane quarter, each owning half of the tile's columns
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes: one SWIZZLE_128B row
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -62,7 +65,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // UMMA shared-memory descriptor: start, LBO, SBO in 16-byte units; version 1 (sm_100); SWIZZLE_128B.
@@ -124,7 +127,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging for TMA stores: 4 warps x 2 buffers x (32 rows x 128 B)
-  static constexpr int EPI_BYTES = 4 * 2 * 4096;
+  static constexpr int EPI_BYTES = kEpiWarps * 4096;  // one 32 x 128 B box per epilogue warp
   static constexpr int SMEM_BASE = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
 };
@@ -315,13 +318,14 @@ struct ProbBd {
   }
 };
 
-// Persistent warp-specialised tcgen05 GEMM: grid = min(tiles, #SMs), 192 threads.
+// Persistent warp-specialised tcgen05 GEMM: grid = min(tiles, #SMs), kGemmThreads threads.
 // warp 0: TMA producer (one lane) into an ST-deep shared-memory ring; warp 1: MMA issuer
-// (one lane) into one of two TMEM accumulators; warps 2-5: epilogue (TMEM -> registers ->
+// (one lane) into one of two TMEM accumulators; warps 2..9: epilogue, two per TMEM lane quarter
+// splitting the columns (TMEM -> registers ->
 // global), releasing the accumulator to the MMA warp, so the epilogue of tile i overlaps the
 // main loop of tile i+1 and the CTA set-up (barriers, TMEM allocation) is paid once per SM.
 template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
-__global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__ typename Prob::Group G) {
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_constant__ typename Prob::Group G) {
   using CF = Cfg<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 4);  // one arrival per epilogue warp
+      mbar_init(&acce[b], kEpiWarps);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -426,18 +430,20 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
         ++tc;
       }
     }
-  } else {  // ------------------------------------------------------------ epilogue warps 2..5
+  } else {  // ---------------------------------------------- epilogue warps 2 .. 1 + kEpiWarps
+    const int ew = warp - 2;
     const int lq = warp & 3;  // TMEM lane quarter this warp may access
     const int r = lq * 32 + lane;
-    uint8_t* epi_smem = smem + CF::STAGES * CF::STAGE_BYTES;  // [4 warps][2][32 x 128 B]
-    uint32_t tbox = 0;  // TMA-store boxes issued by this warp (buffer parity)
+    constexpr int CW = BN / (kEpiWarps / 4);  // columns per epilogue warp
+    const int c0w = (ew >> 2) * CW;           // this warp's first column inside the tile
+    uint8_t* stg = smem + CF::STAGES * CF::STAGE_BYTES + ew * 4096;  // this warp's staging box
     uint32_t tc = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const Tile T = Prob::decode(G, t, sdesc);
       if (!T.valid) continue;
       if (!T.mma) {  // zero-fill (dummy rows)
         const int et = threadIdx.x - 64;
-        for (int idx = et; idx < BM * BN; idx += 128) {
+        for (int idx = et; idx < BM * BN; idx += 32 * kEpiWarps) {
           const int rr = idx / BN, cc = T.n0 + idx % BN;
           if (rr < T.rows_valid && cc < T.N) {
             const int64_t row = T.out_row0 + rr;
@@ -456,10 +462,10 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
       const bf16* arow = T.E.add ? T.E.add + row * T.E.ldadd + T.n0 : nullptr;
       const bool avec = arow && live && ((((uintptr_t)arow) & 15) == 0) && ((T.E.ldadd & 7) == 0);
       uint4 cur[4], nxt[4];
-      bool cur_ok = avec && 32 <= T.N - T.n0;
+      bool cur_ok = avec && c0w + 32 <= T.N - T.n0;
       if (cur_ok)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow) + i);
+        for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow + c0w) + i);
       mbar_wait(&accf[b], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
@@ -470,11 +476,11 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
       const bool tma = Prob::kTmaEpi && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
       constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c0w; c < c0w + CW; c += 32) {
         // warp-uniform: the tile's remaining columns all lie beyond N (nothing to store; a
         // staged-but-never-stored box would also break the buffer accounting below)
         if (T.n0 + c >= T.N) break;
-        const bool nxt_ok = avec && c + 32 < BN && c + 64 <= T.N - T.n0;
+        const bool nxt_ok = avec && c + 32 < c0w + CW && c + 64 <= T.N - T.n0;
         if (nxt_ok)
 #pragma unroll
           for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
@@ -482,9 +488,9 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
         tmem_ld32(trow + c, v);
         if (tma) {
           const int cb = c % CPB;  // column of this piece inside its box
-          uint8_t* buf = epi_smem + (lq * 2 + (tbox & 1)) * 4096;
-          if (cb == 0) {  // the buffer written two boxes ago must have been read by its TMA store
-            if (lane == 0) bulk_wait_read1();
+          uint8_t* buf = stg;
+          if (cb == 0) {  // the previous box's TMA store must have finished reading the buffer
+            if (lane == 0) bulk_wait_read0();
             __syncwarp();
           }
           if (live && T.n0 + c < T.N) {
@@ -508,16 +514,13 @@ __global__ void __launch_bounds__(192, 1) k_gemm_persist(const __grid_constant__
               *reinterpret_cast<uint4*>(rbase + ((jj ^ (lane & 7)) * 16)) = pk;
             }
           }
-          if (cb + 32 == CPB || c + 32 == BN || T.n0 + c + 32 >= T.N) {  // box complete: store it
-            // (every box that advances tbox commits exactly one bulk group: wait_group.read 1
-            // above then guarantees the buffer about to be reused has been read)
+          if (cb + 32 == CPB || c + 32 == c0w + CW || T.n0 + c + 32 >= T.N) {  // box complete: store it
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
               tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
               bulk_commit();
             }
-            ++tbox;
           }
           if (live && T.n0 + c < T.N && T.E.mbits) {
             uint32_t bits = 0;
@@ -632,7 +635,7 @@ void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
     attr = true;
   }
   const int grid = total < num_sms() ? total : num_sms();
-  if (grid > 0) launch_pdl(kern, grid, 192, SMEM, s, G);
+  if (grid > 0) launch_pdl(kern, grid, kGemmThreads, SMEM, s, G);
 }
 
 template <int BN, bool A_MN, bool B_MN>
