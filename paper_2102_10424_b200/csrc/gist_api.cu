@@ -1112,8 +1112,11 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   const double per_nnz = 4.0 * g.count;
   auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
     int id = -1;
+    static const int twice = [] { const char* e = std::getenv("GIST_EXP_TWICE"); return e ? atoi(e) : 0; }();
+    if (twice == 2) spmm_group<T, T>(G, s);  // EXPERIMENT: warm every operand first (wrong results)
     if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, bytes, per_nnz, nnz_slot);
     spmm_group<T, T>(G, s);
+    if (twice == 1) spmm_group<T, T>(G, s);  // EXPERIMENT: timed twice back to back
     prof_end(c, s, id);
     ++c->nk;
   };
@@ -1539,6 +1542,8 @@ extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_
     SpmmArgs<bf16, bf16> a;
     a.row_beg = row_ptr_dev; a.row_end = row_ptr_dev + 1; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
     a.self = self; a.H = (const bf16*)H_dev; a.ldh = ld; a.out = (bf16*)out_dev; a.ldo = ld; a.w = pad8(w);
+    const char* few = std::getenv("GIST_SPMM_ENTRY_FEW");  // tools/kbench_inter.py: few-neighbour kernels
+    a.few_nnz = few && few[0] == '1';
     spmm<bf16, bf16>(a, s);
   } else {
     return GIST_E_ARG;

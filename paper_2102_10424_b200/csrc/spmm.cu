@@ -16,9 +16,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace gist {
 
 namespace {
+
+
 
 // 16 bytes -> V fp32 values
 __device__ __forceinline__ void unpack(const uint4& x, float* v, float) {
