@@ -91,6 +91,11 @@ struct gist_ctx {
   std::vector<int> dims;
   int L = 0, arch = 0, prec = 0;
   cudaStream_t stream = nullptr;
+  // GIST_STREAMS=2: the local slots run as two lockstep groups on two streams (fork / join
+  // per step) so one group's kernels fill the other's ramp-up / tail bubbles
+  int nstreams = 1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   bool own_stream = false;
   int state = S_CREATED;
   gist_status sticky = GIST_OK;
@@ -390,6 +395,14 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
     delete c;
     return GIST_E_CUDA;
   }
+  if (const char* e = std::getenv("GIST_STREAMS")) c->nstreams = atoi(e) == 2 ? 2 : 1;
+  if (c->nstreams == 2 &&
+      (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+       cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess)) {
+    delete c;
+    return GIST_E_CUDA;
+  }
   if (cfg->graph_residency != GIST_GRAPH_DEVICE) {
     delete c;
     return GIST_E_UNSUPPORTED;
@@ -424,6 +437,9 @@ extern "C" void gist_destroy(gist_ctx* c) {
   for (void* p : c->allocs) cudaFree(p);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
+  if (c->ev_join2) cudaEventDestroy(c->ev_join2);
+  if (c->side) cudaStreamDestroy(c->side);
   for (auto& r : c->prof_pending) c->ev_pool.push_back(r.a), c->ev_pool.push_back(r.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->nnz_pin) cudaFreeHost(c->nnz_pin);
@@ -803,10 +819,15 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   // on Reddit-shape batches: issue-bound, profiles/r01*_ncu_spmm_ct.txt); default off
   const char* slab_env = std::getenv("GIST_SPMM_SLAB");
   const int slab_max = (slab_env && slab_env[0] == '1') ? c->max_csize : 0;
-  for (int g0 = 0; g0 < (int)c->slots.size(); g0 += kMaxGroup) {
+  // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
+  // L2-footprint / launch-count trade-off
+  int gsz = kMaxGroup;
+  if (c->nstreams == 2) gsz = std::max(1, std::min(kMaxGroup, ((int)c->slots.size() + 1) / 2));
+  if (const char* e = std::getenv("GIST_GROUP")) gsz = std::max(1, std::min(kMaxGroup, atoi(e)));
+  for (int g0 = 0; g0 < (int)c->slots.size(); g0 += gsz) {
     typename StepPlan<T>::Group g;
     g.first = g0;
-    g.count = std::min<int>(kMaxGroup, (int)c->slots.size() - g0);
+    g.count = std::min<int>(gsz, (int)c->slots.size() - g0);
     g.batch.n = g.count;
     g.batch.q = q;
     g.batch.nb_max = nb;
@@ -1089,8 +1110,7 @@ static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp
 // One subTrain step of every slot of group g, in lockstep: every
 // kernel below is one launch over all slots of the group.
 template <typename T>
-static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z) {
-  cudaStream_t s = c->stream;
+static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t s) {
   const int L = c->L;
   for (int j = 0; j < g.count; ++j) c->slots[g.first + j].last_nb = c->slots[g.first + j].nb_of_step[z];
   int nnz_slot = -1;
@@ -1250,10 +1270,20 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
   CK(cudaEventRecord(c->hstate_ev, s));
   for (int z = 0; z < local_iters; ++z) {
     c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
-    if (c->prec == GIST_PREC_BF16) {
-      for (auto& g : c->plan_b.groups) TRY(run_group_step<bf16>(c, g, z));
-    } else {
-      for (auto& g : c->plan_f.groups) TRY(run_group_step<float>(c, g, z));
+    const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
+    const bool two = c->nstreams == 2 && ng >= 2;
+    if (two) {  // fork: the side stream sees the previous optimizer step / state advance
+      CK(cudaEventRecord(c->ev_fork2, s));
+      CK(cudaStreamWaitEvent(c->side, c->ev_fork2, 0));
+    }
+    for (size_t gi = 0; gi < ng; ++gi) {
+      cudaStream_t gs = (two && (gi & 1)) ? c->side : s;
+      if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], z, gs));
+      else TRY(run_group_step<float>(c, c->plan_f.groups[gi], z, gs));
+    }
+    if (two) {  // join before the optimizer (it updates every local slot at once)
+      CK(cudaEventRecord(c->ev_join2, c->side));
+      CK(cudaStreamWaitEvent(s, c->ev_join2, 0));
     }
     TRY(run_optimizer(c));
     c->prof_now = false;
