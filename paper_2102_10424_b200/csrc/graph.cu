@@ -271,6 +271,46 @@ __global__ void k_edge_clusters(const int32_t* __restrict__ col, const int32_t* 
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
     ccol[e] = cid[col[e]];
 }
+// Edge checks of load_graph on the device (one warp per row, original ids): out[0] = edges with
+// col out of [0, n), out[1] = self loops, out[2] = non-loop edges inside a cluster.  Block-reduced
+// integer atomics: deterministic.
+__global__ void __launch_bounds__(256) k_validate_edges(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                        const int32_t* __restrict__ cid, int64_t n,
+                                                        unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long sb[3];
+  if (threadIdx.x < 3) sb[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  unsigned long long bad = 0, self = 0, intra = 0;
+  if (v < n) {
+    const int32_t cv = cid[v];
+    for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
+      const int32_t u = col[e];
+      if (u < 0 || u >= n) { ++bad; continue; }
+      if (u == v) ++self;
+      else if (cid[u] == cv) ++intra;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    self += __shfl_xor_sync(0xffffffffu, self, o);
+    intra += __shfl_xor_sync(0xffffffffu, intra, o);
+  }
+  if (lane == 0) {
+    if (bad) atomicAdd(&sb[0], bad);
+    if (self) atomicAdd(&sb[1], self);
+    if (intra) atomicAdd(&sb[2], intra);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 && sb[threadIdx.x]) atomicAdd(&out[threadIdx.x], sb[threadIdx.x]);
+}
+void validate_edges(const int64_t* rp, const int32_t* col, const int32_t* cid, int64_t n, unsigned long long* out,
+                    cudaStream_t s) {
+  if (n <= 0) return;
+  k_validate_edges<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(rp, col, cid, n, out);
+}
+
 void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s) {
   if (nnz <= 0) return;
   k_edge_clusters<<<148 * 8, 256, 0, s>>>(col, cid, nnz, ccol);

@@ -225,6 +225,9 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
                  const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
                  const uint8_t* split, int skip_intra, cudaStream_t s);
 void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s);
+// out[3] (zeroed by the caller): edges with col outside [0, n), self loops, intra-cluster edges
+void validate_edges(const int64_t* rp, const int32_t* col, const int32_t* cid, int64_t n, unsigned long long* out,
+                    cudaStream_t s);
 // Binary intra-cluster adjacency blocks: blocks[c][i][j] = 1 iff (cstart[c]+i, cstart[c]+j) is an
 // edge (relabelled ids), bf16 [num_clusters x bs x bs], zeroed by the caller.
 void cluster_blocks(const int64_t* rp, const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t n,
