@@ -15,6 +15,7 @@
 #include "kernels.h"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace gist {
 
@@ -186,36 +187,44 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
     int intra = 0;  // in-batch intra-cluster neighbours (skip_intra: counted, not stored)
     const int32_t cg = skip_intra ? cid[g] : -1;
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t base = rp[g]; base < end; base += 128) {
-      int32_t u[4], cc[4], dl[4];
+    // R edges per round (R/32 independent (col, ccol) load pairs per lane); the degree tail
+    // (lognormal, max ~20x the mean) is what bounds this kernel, so long rows take 256 per
+    // round: the longest row's chain of dependent rounds is what the whole launch waits for
+    auto walk = [&](auto RT) {
+      constexpr int R = decltype(RT)::value;
+      for (int64_t base = rp[g]; base < end; base += R) {
+        int32_t u[R / 32], cc[R / 32], dl[R / 32];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {  // col and its cluster: independent, coalesced loads
-        const int64_t e = base + r * 32 + lane;
-        u[r] = e < end ? col[e] : -1;
-        cc[r] = e < end ? ccol[e] : 0;
-      }
+        for (int r = 0; r < R / 32; ++r) {  // col and its cluster: independent, coalesced loads
+          const int64_t e = base + r * 32 + lane;
+          u[r] = e < end ? col[e] : -1;
+          cc[r] = e < end ? ccol[e] : 0;
+        }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        if (SMAP) {
-          dl[r] = u[r] >= 0 ? smap[cc[r]] : kAbsent;
-        } else {
-          const uint64_t m = u[r] >= 0 ? S.map64[cc[r]] : 0ull;
-          dl[r] = (u[r] >= 0 && (uint32_t)(m >> 32) == tag) ? (int32_t)(uint32_t)m : kAbsent;
+        for (int r = 0; r < R / 32; ++r) {
+          if (SMAP) {
+            dl[r] = u[r] >= 0 ? smap[cc[r]] : kAbsent;
+          } else {
+            const uint64_t m = u[r] >= 0 ? S.map64[cc[r]] : 0ull;
+            dl[r] = (u[r] >= 0 && (uint32_t)(m >> 32) == tag) ? (int32_t)(uint32_t)m : kAbsent;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R / 32; ++r) {
+          bool in = dl[r] != kAbsent;
+          if (skip_intra) {
+            const bool ii = in && cc[r] == cg;
+            intra += __popc(__ballot_sync(0xffffffffu, ii));
+            in &= !ii;
+          }
+          const unsigned bm = __ballot_sync(0xffffffffu, in);
+          if (in) S.b_col[out + __popc(bm & lt)] = u[r] + dl[r];
+          out += __popc(bm);
         }
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        bool in = dl[r] != kAbsent;
-        if (skip_intra) {
-          const bool ii = in && cc[r] == cg;
-          intra += __popc(__ballot_sync(0xffffffffu, ii));
-          in &= !ii;
-        }
-        const unsigned bm = __ballot_sync(0xffffffffu, in);
-        if (in) S.b_col[out + __popc(bm & lt)] = u[r] + dl[r];
-        out += __popc(bm);
-      }
-    }
+    };
+    if (end - rp[g] > 1024) walk(std::integral_constant<int, 256>());
+    else walk(std::integral_constant<int, 128>());
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
     if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
       const uint4* xs = reinterpret_cast<const uint4*>(G.X + g * G.ldx);
