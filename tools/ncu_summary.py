@@ -4,7 +4,8 @@
   python tools/ncu_summary.py launches <launches.csv> <out.txt>
       per-kernel launch counts, summed / average device time and share of the
       captured launches (gpu__time_duration.sum pass: cold-cache, serialised).
-  python tools/ncu_summary.py report <file.ncu-rep> <out.txt> [--traffic profiles/traffic.json --key prec:class]
+  python tools/ncu_summary.py report <file.ncu-rep> <out.txt> [--filter name-substring]
+                                     [--traffic profiles/traffic.json --key prec:class]
       key metrics of a `ncu --set full` capture (time, DRAM bytes, L2/L1 hit
       rates, throughput %, tensor-pipe activity, occupancy) per captured launch;
       optionally records the mean DRAM read+write bytes per launch as `traffic`.
@@ -59,7 +60,7 @@ def launches(path, out):
     print("\n".join(lines))
 
 
-def report(path, out, traffic=None, key=None):
+def report(path, out, traffic=None, key=None, flt=None):
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, u = rows[0], rows[1]
@@ -67,6 +68,8 @@ def report(path, out, traffic=None, key=None):
     dram = []
     for r in rows[2:]:
         name = r[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        if flt and flt not in name:
+            continue
         lines.append(f"== {name}  grid={r[h.index('Grid Size')] if 'Grid Size' in h else '?'} "
                      f"block={r[h.index('Block Size')] if 'Block Size' in h else '?'}")
         b = 0.0
@@ -94,6 +97,8 @@ if __name__ == "__main__":
         launches(sys.argv[2], sys.argv[3])
     else:
         kw = {}
+        if "--filter" in sys.argv:
+            kw["flt"] = sys.argv[sys.argv.index("--filter") + 1]
         if "--traffic" in sys.argv:
             kw["traffic"] = sys.argv[sys.argv.index("--traffic") + 1]
             kw["key"] = sys.argv[sys.argv.index("--key") + 1]
