@@ -68,6 +68,63 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---- CTA-pair (cta_group::2) primitives: two CTAs of a cluster on one TPC share one
+// 256-row MMA; each holds its 128 rows of A and half of B's columns in shared memory.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-SM TMA load into this CTA's shared memory; the transaction bytes are counted on the
+// leader CTA's (rank 0) barrier at the same offset (peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// MMA completion -> arrive on the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the leader CTA's barrier at this offset (local for the leader, remote for the peer)
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\nmbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 // UMMA shared-memory descriptor: start, LBO, SBO in 16-byte units; version 1 (sm_100); SWIZZLE_128B.
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -235,15 +292,20 @@ template <int BN>
 struct ProbPlain {
   using Group = GemmGroupTC;
   static constexpr bool kTmaEpi = true;  // epilogue staging + TMA stores
+  static __device__ __forceinline__ int ydim(const Group& G) { return G.tm; }
   static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
   static constexpr int kMaxDesc = 1;
   static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
-  static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t*) {
-    Tile T;
+  static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sd) {
     const int per = G.tm * G.tn;
     const int z = t / per, r = t - z * per;
+    return decode_y(G, z, r / G.tn, r % G.tn, sd);
+  }
+  // tile (slot z, 128-row tile y, n-tile nt)
+  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t*) {
+    Tile T;
     const GemmSlotTC& S = G.s[z];
-    const int m0 = (r / G.tn) * BM, n0 = (r % G.tn) * BN;
+    const int m0 = y * BM, n0 = nt * BN;
     T.valid = T.mma = m0 < S.M && n0 < S.N;
     T.ma = &S.ma;
     T.mb = &S.mb;
@@ -282,10 +344,13 @@ struct ProbBd {
       sdesc[i] = G.s[i / per].desc[(size_t)z * per + (i % per)];
   }
   static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sdesc) {
-    Tile T;
     const int per = ydim(G) * G.tn;
     const int z = t / per, r = t - z * per;
-    const int y = r / G.tn, n0 = (r % G.tn) * BN;
+    return decode_y(G, z, r / G.tn, r % G.tn, sdesc);
+  }
+  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t* sdesc) {
+    Tile T;
+    const int n0 = nt * BN;
     const BdSlot& S = G.s[z];
     const int q = G.q, mp = mt_per(G);
     const int32_t* d = sdesc + z * (3 * q + 4);
@@ -317,6 +382,123 @@ struct ProbBd {
     return T;
   }
 };
+
+// Epilogue of one MMA tile by one epilogue warp (its TMEM lane quarter lq, columns
+// [c0w, c0w + CW)): waits for the accumulator, then TMEM -> registers -> (scale, add, ReLU,
+// mask, ReLU-mask bits) -> TMA-staged or direct stores.  Shared by the 1-CTA and CTA-pair kernels.
+template <int BN, bool OUT_F32, bool TMA_EPI>
+__device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint64_t* accf_b, uint32_t aph, int lq,
+                                         int lane, int c0w, uint8_t* stg) {
+  constexpr int CW = BN / (kEpiWarps / 4);  // columns per epilogue warp
+  const int r = lq * 32 + lane;
+    const int64_t row = T.out_row0 + r;
+    const bool live = r < T.rows_valid;
+    const float sc = (T.E.rscale && live) ? T.E.rscale[row] : 1.f;  // before the wait: overlaps the MMA
+    // `add` is read one 32-column chunk ahead (the first before the accumulator wait), so its
+    // latency overlaps the MMA / the previous chunk instead of serialising the epilogue
+    const bf16* arow = T.E.add ? T.E.add + row * T.E.ldadd + T.n0 : nullptr;
+    const bool avec = arow && live && ((((uintptr_t)arow) & 15) == 0) && ((T.E.ldadd & 7) == 0);
+    uint4 cur[4], nxt[4];
+    bool cur_ok = avec && c0w + 32 <= T.N - T.n0;
+    if (cur_ok)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow + c0w) + i);
+    mbar_wait(accf_b, aph);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t trow = tmem_acc + ((uint32_t)(lq * 32) << 16);
+    // TMA-store path: this warp's 32 rows are staged (128-byte rows, SWIZZLE_128B: 16-byte
+    // chunk j of row r at r*128 + ((j ^ (r & 7)) * 16), bank-conflict free) and written by
+    // one cp.async.bulk.tensor per 32 x 128 B box, so stores are full lines instead of one
+    // 16-byte piece of 32 different rows per instruction.
+    const bool tma = TMA_EPI && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
+    constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
+#pragma unroll 1
+    for (int c = c0w; c < c0w + CW; c += 32) {
+      // warp-uniform: the tile's remaining columns all lie beyond N (nothing to store; a
+      // staged-but-never-stored box would also break the buffer accounting below)
+      if (T.n0 + c >= T.N) break;
+      const bool nxt_ok = avec && c + 32 < c0w + CW && c + 64 <= T.N - T.n0;
+      if (nxt_ok)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
+      float v[32];
+      tmem_ld32(trow + c, v);
+      if (tma) {
+        const int cb = c % CPB;  // column of this piece inside its box
+        uint8_t* buf = stg;
+        if (cb == 0) {  // the previous box's TMA store must have finished reading the buffer
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+        if (live && T.n0 + c < T.N) {
+          epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
+          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+        }
+        uint8_t* rbase = buf + lane * 128;
+        if (OUT_F32) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(rbase + ((j ^ (lane & 7)) * 16)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 pk;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
+            const int jj = (cb / 8) + j;  // 16-byte chunk index inside the 128-byte row
+            *reinterpret_cast<uint4*>(rbase + ((jj ^ (lane & 7)) * 16)) = pk;
+          }
+        }
+        if (cb + 32 == CPB || c + 32 == c0w + CW || T.n0 + c + 32 >= T.N) {  // box complete: store it
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
+            bulk_commit();
+          }
+        }
+        if (live && T.n0 + c < T.N && T.E.mbits) {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+            bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
+          }
+          T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
+        }
+      } else if (live && T.n0 + c < T.N) {
+        epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
+        if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+        if (T.E.mbits) {  // sign bits of the values as stored (bf16-rounded on the bf16 path)
+          uint32_t bits = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+            bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
+          }
+          T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      cur_ok = nxt_ok;
+    }
+}
+
+// inert dummy rows of a batch: exact zeros (no MMA); et = thread index among the epilogue warps
+template <int BN, bool OUT_F32>
+__device__ __forceinline__ void zero_fill_tile(const Tile& T, int et) {
+  for (int idx = et; idx < BM * BN; idx += 32 * kEpiWarps) {
+    const int rr = idx / BN, cc = T.n0 + idx % BN;
+    if (rr < T.rows_valid && cc < T.N) {
+      const int64_t row = T.out_row0 + rr;
+      if (OUT_F32) ((float*)T.E.C)[row * T.E.ldc + cc] = 0.f;
+      else ((bf16*)T.E.C)[row * T.E.ldc + cc] = __float2bfloat16_rn(0.f);
+    }
+  }
+}
 
 // Persistent warp-specialised tcgen05 GEMM: grid = min(tiles, #SMs), kGemmThreads threads.
 // warp 0: TMA producer (one lane) into an ST-deep shared-memory ring; warp 1: MMA issuer
@@ -442,112 +624,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
       const Tile T = Prob::decode(G, t, sdesc);
       if (!T.valid) continue;
       if (!T.mma) {  // zero-fill (dummy rows)
-        const int et = threadIdx.x - 64;
-        for (int idx = et; idx < BM * BN; idx += 32 * kEpiWarps) {
-          const int rr = idx / BN, cc = T.n0 + idx % BN;
-          if (rr < T.rows_valid && cc < T.N) {
-            const int64_t row = T.out_row0 + rr;
-            if (OUT_F32) ((float*)T.E.C)[row * T.E.ldc + cc] = 0.f;
-            else ((bf16*)T.E.C)[row * T.E.ldc + cc] = __float2bfloat16_rn(0.f);
-          }
-        }
+        zero_fill_tile<BN, OUT_F32>(T, threadIdx.x - 64);
         continue;
       }
       const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
-      const int64_t row = T.out_row0 + r;
-      const bool live = r < T.rows_valid;
-      const float sc = (T.E.rscale && live) ? T.E.rscale[row] : 1.f;  // before the wait: overlaps the MMA
-      // `add` is read one 32-column chunk ahead (the first before the accumulator wait), so its
-      // latency overlaps the MMA / the previous chunk instead of serialising the epilogue
-      const bf16* arow = T.E.add ? T.E.add + row * T.E.ldadd + T.n0 : nullptr;
-      const bool avec = arow && live && ((((uintptr_t)arow) & 15) == 0) && ((T.E.ldadd & 7) == 0);
-      uint4 cur[4], nxt[4];
-      bool cur_ok = avec && c0w + 32 <= T.N - T.n0;
-      if (cur_ok)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow + c0w) + i);
-      mbar_wait(&accf[b], aph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t trow = tmem + b * BN + ((uint32_t)(lq * 32) << 16);
-      // TMA-store path: this warp's 32 rows are staged (128-byte rows, SWIZZLE_128B: 16-byte
-      // chunk j of row r at r*128 + ((j ^ (r & 7)) * 16), bank-conflict free) and written by
-      // one cp.async.bulk.tensor per 32 x 128 B box, so stores are full lines instead of one
-      // 16-byte piece of 32 different rows per instruction.
-      const bool tma = Prob::kTmaEpi && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
-      constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
-#pragma unroll 1
-      for (int c = c0w; c < c0w + CW; c += 32) {
-        // warp-uniform: the tile's remaining columns all lie beyond N (nothing to store; a
-        // staged-but-never-stored box would also break the buffer accounting below)
-        if (T.n0 + c >= T.N) break;
-        const bool nxt_ok = avec && c + 32 < c0w + CW && c + 64 <= T.N - T.n0;
-        if (nxt_ok)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
-        float v[32];
-        tmem_ld32(trow + c, v);
-        if (tma) {
-          const int cb = c % CPB;  // column of this piece inside its box
-          uint8_t* buf = stg;
-          if (cb == 0) {  // the previous box's TMA store must have finished reading the buffer
-            if (lane == 0) bulk_wait_read0();
-            __syncwarp();
-          }
-          if (live && T.n0 + c < T.N) {
-            epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
-            if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
-          }
-          uint8_t* rbase = buf + lane * 128;
-          if (OUT_F32) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              *reinterpret_cast<float4*>(rbase + ((j ^ (lane & 7)) * 16)) =
-                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 pk;
-              __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[8 * j + 2 * i], v[8 * j + 2 * i + 1]);
-              const int jj = (cb / 8) + j;  // 16-byte chunk index inside the 128-byte row
-              *reinterpret_cast<uint4*>(rbase + ((jj ^ (lane & 7)) * 16)) = pk;
-            }
-          }
-          if (cb + 32 == CPB || c + 32 == c0w + CW || T.n0 + c + 32 >= T.N) {  // box complete: store it
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
-              bulk_commit();
-            }
-          }
-          if (live && T.n0 + c < T.N && T.E.mbits) {
-            uint32_t bits = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
-              bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
-            }
-            T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
-          }
-        } else if (live && T.n0 + c < T.N) {
-          epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
-          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
-          if (T.E.mbits) {  // sign bits of the values as stored (bf16-rounded on the bf16 path)
-            uint32_t bits = 0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float sv = OUT_F32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
-              bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
-            }
-            T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
-        cur_ok = nxt_ok;
-      }
+      epi_tile<BN, OUT_F32, Prob::kTmaEpi>(T, tmem + b * BN, &accf[b], aph, lq, lane, c0w, stg);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[b]);
@@ -561,6 +642,181 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes 256 x BN tiles
+// (two consecutive 128-row tiles y = 2p, 2p+1 of the same slot and n-tile).  Each CTA stages
+// its own 128 rows of A and HALF of B's columns, so a ring stage is 16 + BN/4 KB instead of
+// 16 + BN/2 KB: with the same shared memory the ring is 1.5x deeper and each SM pulls 1/3
+// fewer operand bytes through L2 per FLOP.  The leader (rank 0) issues the 256-row MMA and
+// multicasts its completions to both CTAs; both CTAs' producers count their TMA bytes on the
+// leader's full barrier; both CTAs' epilogues drain their own TMEM rows and arrive on the
+// leader's accumulator-empty barrier.  Same arithmetic as k_gemm_persist.
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_constant__ typename Prob::Group G) {
+  constexpr int BNH = BN / 2;
+  constexpr int A_BYTES = BM * BK * 2, B_BYTES = BNH * BK * 2, STAGE = A_BYTES + B_BYTES;
+  constexpr int EPI = Prob::kTmaEpi ? kEpiWarps * 4096 : 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + ST * STAGE + EPI);
+  uint64_t* empty = full + ST;
+  uint64_t* accf = empty + ST;  // [2]
+  uint64_t* acce = accf + 2;    // [2]  (leader: both CTAs' epilogue warps arrive)
+  uint32_t* tmem_slot = (uint32_t*)(acce + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
+  __shared__ int32_t sdesc[Prob::kMaxDesc * kMaxGroup];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // paired TMEM allocation: same warp, same destination offset in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrival
+  pdl_wait();
+  pdl_trigger();
+  Prob::stage(G, sdesc);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const int yd = Prob::ydim(G);
+  const int yp_n = (yd + 1) / 2;
+  const int per2 = yp_n * G.tn;
+  const int total2 = G.n * per2;
+  // this CTA's 128-row tile and the leader's (which carries the pair's B operand and K)
+  auto decode2 = [&](int p, Tile& T0, Tile& Ts) {
+    const int z = p / per2, rr = p - z * per2, yp = rr / G.tn, nt = rr - yp * G.tn;
+    T0 = Prob::decode_y(G, z, 2 * yp, nt, sdesc);
+    if (leader) {
+      Ts = T0;
+    } else if (2 * yp + 1 < yd) {
+      Ts = Prob::decode_y(G, z, 2 * yp + 1, nt, sdesc);
+    } else {
+      Ts = T0;
+      Ts.valid = Ts.mma = false;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------- TMA producer (both CTAs)
+      uint32_t it = 0;
+      for (int p = pair; p < total2; p += npairs) {
+        Tile T0, Ts;
+        decode2(p, T0, Ts);
+        if (!T0.mma) continue;
+        const int a_row = Ts.mma ? Ts.a_row : T0.a_row + BM;  // rows past the tile: never stored
+        const int b_col = T0.b_col + (int)rank * BNH;
+        const int nk = (T0.K + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % ST;
+          const uint32_t ph = (it / ST) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE);  // both CTAs' bytes
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_pair(sa, T0.ma, &full[s], k0, a_row);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * 8192, T0.ma, &full[s], a_row + 64 * j, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(sb, T0.mb, &full[s], T0.b_k0 + k0, b_col);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BNH / 64; ++j)
+              tma_load_2d_pair(sb + j * 8192, T0.mb, &full[s], b_col + 64 * j, T0.b_k0 + k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ------------------------------------ MMA issuer (leader only)
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                 ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)((2 * BM) >> 4) << 24);
+      uint32_t it = 0, tc = 0;
+      for (int p = pair; p < total2; p += npairs) {
+        Tile T0, Ts;
+        decode2(p, T0, Ts);
+        if (!T0.mma) continue;
+        const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
+        mbar_wait_cluster(&acce[b], aph ^ 1u);  // both CTAs' epilogues drained accumulator b
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem + b * BN;
+        const int nk = (T0.K + BK - 1) / BK;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % ST;
+          const uint32_t ph = (it / ST) & 1u;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * STAGE);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024) : make_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024) : make_desc(sb + k * 32, 16, 1024);
+            umma_bf16_pair(dacc, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_pair(&empty[s]);  // frees stage s in both CTAs
+        }
+        umma_commit_pair(&accf[b]);  // accumulator b complete in both CTAs
+        ++tc;
+      }
+    }
+  } else {  // ---------------------------------------------- epilogue warps 2 .. 1 + kEpiWarps
+    const int ew = warp - 2;
+    const int lq = warp & 3;
+    constexpr int CW = BN / (kEpiWarps / 4);
+    const int c0w = (ew >> 2) * CW;
+    uint8_t* stg = smem + ST * STAGE + ew * 4096;
+    uint32_t tc = 0;
+    for (int p = pair; p < total2; p += npairs) {
+      Tile T0, Ts;
+      decode2(p, T0, Ts);
+      if (!T0.mma) {  // no MMA for this pair: zero-fill own dummy rows, if any
+        if (Ts.valid && !Ts.mma) zero_fill_tile<BN, OUT_F32>(Ts, threadIdx.x - 64);
+        continue;
+      }
+      const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
+      if (Ts.valid && Ts.mma) {
+        epi_tile<BN, OUT_F32, Prob::kTmaEpi>(Ts, tmem + b * BN, &accf[b], aph, lq, lane, c0w, stg);
+      } else {  // this CTA's half lies past the problem: nothing to store, still drain in order
+        mbar_wait(&accf[b], aph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&acce[b]);
+      ++tc;
+    }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();  // the peer's shared memory / TMEM may be read until the leader is done
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
   }
 }
 
@@ -638,8 +894,50 @@ void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
   if (grid > 0) launch_pdl(kern, grid, kGemmThreads, SMEM, s, G);
 }
 
+bool pair_enabled() {  // GIST_2CTA=0: never use CTA pairs (A/B measurements)
+  static const bool on = [] { const char* e = std::getenv("GIST_2CTA"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
+// CTA-pair launch: clusters of 2 (cudaLaunchAttributeClusterDimension) + PDL, grid = 2 x pairs
+template <int BN, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+void launch_pair(const typename Prob::Group& G, int total2, cudaStream_t s) {
+  constexpr int ST = BN == 256 ? 6 : 8;
+  constexpr int STAGE = BM * BK * 2 + (BN / 2) * BK * 2;
+  constexpr int SMEM = ST * STAGE + (Prob::kTmaEpi ? kEpiWarps * 4096 : 0) + 1024 + 256 + 64;
+  auto kern = k_gemm_pair<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  const int pairs = total2 < num_sms() / 2 ? total2 : num_sms() / 2;
+  if (pairs <= 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, G);
+}
+
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
+  if (P.pair) {
+    const int total2 = P.G.n * ((P.G.tm + 1) / 2) * P.G.tn;
+    if (P.out_f32) launch_pair<BN, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total2, s);
+    else launch_pair<BN, A_MN, B_MN, false, ProbPlain<BN>>(P.G, total2, s);
+    return;
+  }
   constexpr int ST = BN == 256 ? 4 : 6;
   const int total = P.G.n * P.G.tm * P.G.tn;
   if (P.out_f32) launch_persist<BN, ST, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total, s);
@@ -657,7 +955,8 @@ void dispatch_layout(const GemmPlanTC& P, cudaStream_t s) {
 template <int BN>
 void launch_bd(const BdPlan& P, cudaStream_t s) {
   const int mt_per = (P.G.bs + BM - 1) / BM;
-  const int total = P.G.n * (P.G.q * mt_per + (int)cdiv(P.G.rows, BM)) * P.G.tn;
+  const int yd = P.G.q * mt_per + (int)cdiv(P.G.rows, BM);
+  const int total = P.G.n * yd * P.G.tn;
   launch_persist<BN, 4, false, true, false, ProbBd<BN>>(P.G, total, s);
 }
 
@@ -678,6 +977,14 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     maxM = ops[i].M > maxM ? ops[i].M : maxM;
   }
   P->bn = maxN > 128 ? 256 : 128;  // persistent kernel: wide tiles amortise the epilogue
+  // CTA pairs for large GEMMs (>= 4 tiles per SM: measured 82 -> 88% of peak at width 4096);
+  // the step's small grouped GEMMs (~3 tiles per SM) and the cluster-block aggregation stay
+  // on one CTA per tile (pairs measured slower there)
+  {
+    int64_t tiles = 0;
+    for (int i = 0; i < n; ++i) tiles += cdiv(ops[i].M, BM) * cdiv(ops[i].N, P->bn);
+    P->pair = pair_enabled() && tiles >= 4 * (int64_t)num_sms();
+  }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
     const GemmOp& o = ops[i];
@@ -686,7 +993,7 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     GemmSlotTC& S = P->G.s[i];
     bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, 64, 64) : make_map(&S.ma, o.A, o.K, o.M, o.lda, 64, BM);
     ok = ok && (P->b_mn ? make_map(&S.mb, o.B, o.N, o.K, o.ldb, 64, 64)
-                        : make_map(&S.mb, o.B, o.K, o.N, o.ldb, 64, P->bn));
+                        : make_map(&S.mb, o.B, o.K, o.N, o.ldb, 64, P->pair ? P->bn / 2 : P->bn));
     if (!ok) return false;
     S.C = o.C;
     S.ldc = o.ldc;

@@ -110,6 +110,7 @@ struct GemmGroupTC {
 struct GemmPlanTC {
   GemmGroupTC G;
   bool a_mn = false, b_mn = false, out_f32 = false, relu = false, mask = false;
+  bool pair = false;  // CTA-pair (cta_group::2) kernel
   int bn = 128;
   int64_t maxM = 0, maxN = 0;
 };
