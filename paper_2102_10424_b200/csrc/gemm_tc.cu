@@ -55,6 +55,34 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// L2 eviction-priority policies (createpolicy; used as .L2::cache_hint operands)
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st16_hint(bf16* p, const float* v, uint64_t pol) {
+  uint4 a;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -62,6 +90,11 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int x, int y, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "l"(pol)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -205,6 +238,7 @@ struct Epi {
   int64_t ldmb;
   const CUtensorMap* mc;  // TMA store map of C, or nullptr (direct stores)
   int clip;               // rows >= rows_valid lie outside mc (TMA clips them): every warp may use it
+  int keep;               // L2 evict_last hint on the output stores
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -266,8 +300,14 @@ __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, i
   } else {
     bf16* dst = (bf16*)E.C + row * E.ldc + col;
     if (full16 && (((uintptr_t)dst & 15) == 0)) {
-      st16(dst, v);
-      st16(dst + 8, v + 8);
+      if (E.keep) {
+        const uint64_t pol = policy_evict_last();
+        st16_hint(dst, v, pol);
+        st16_hint(dst + 8, v + 8, pol);
+      } else {
+        st16(dst, v);
+        st16(dst + 8, v + 8);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
@@ -284,6 +324,7 @@ struct Tile {
   int a_row, b_col, b_k0, K;  // TMA coordinates
   int64_t out_row0;
   int rows_valid, n0, N;
+  int stream_a;  // evict_first hint on the A loads
   Epi E;
 };
 
@@ -318,7 +359,8 @@ struct ProbPlain {
     T.n0 = n0;
     T.N = S.N;
     T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0, S.mbits, S.ldmb,
-                 S.tma_store ? &S.mc : nullptr, 1};
+                 S.tma_store ? &S.mc : nullptr, 1, S.keep_out};
+    T.stream_a = S.stream_a;
     return T;
   }
 };
@@ -358,7 +400,9 @@ struct ProbBd {
     T.mb = &S.mb;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &S.mc : nullptr, 0};
+    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &S.mc : nullptr, 0,
+              S.keep_out};
+    T.stream_a = 0;
     T.b_col = n0;
     T.K = G.bs;
     if (y >= q * mp) {  // inert dummy rows [n_b, rows): zeros
@@ -455,7 +499,8 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
+            if (T.E.keep) tma_store_2d_hint(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32), policy_evict_last());
+            else tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
             bulk_commit();
           }
         }
@@ -563,7 +608,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           uint8_t* sb = sa + CF::A_BYTES;
           mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
           const int k0 = kb * BK;
-          if (!A_MN) {
+          if (T.stream_a) {  // last read of A for a while: evict first
+            const uint64_t pol = policy_evict_first();
+            if (!A_MN) {
+              tma_load_2d_hint(sa, T.ma, &full[s], k0, T.a_row, pol);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0, pol);
+            }
+          } else if (!A_MN) {
             tma_load_2d(sa, T.ma, &full[s], k0, T.a_row);
           } else {
 #pragma unroll
@@ -863,6 +917,10 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool l2hint_enabled() {  // GIST_L2HINT=0: no L2 eviction-priority hints (A/B measurements)
+  static const bool on = [] { const char* e = std::getenv("GIST_L2HINT"); return !(e && e[0] == '0'); }();
+  return on;
+}
 bool tma_store_enabled() {  // GIST_TMA_STORE=0: direct epilogue stores (A/B measurements)
   static const bool on = [] { const char* e = std::getenv("GIST_TMA_STORE"); return !(e && e[0] == '0'); }();
   return on;
@@ -1004,6 +1062,8 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.rs_from = o.rs_from;
     S.mbits = o.mbits;
     S.ldmb = o.ldmb;
+    S.keep_out = l2hint_enabled() ? o.keep_out : 0;
+    S.stream_a = l2hint_enabled() ? o.stream_a : 0;
     S.tma_store = tma_store_enabled() && make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
     S.M = (int)o.M;
     S.N = (int)o.N;
@@ -1048,6 +1108,7 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.global_rows = o.global_rows;
     S.N = (int)o.N;
     S.tma_store = 0;  // ProbBd::kTmaEpi == false
+    S.keep_out = l2hint_enabled() ? o.keep_out : 0;
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;

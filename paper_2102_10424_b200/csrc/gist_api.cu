@@ -929,7 +929,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           // Layer 0 reads the batch-local X_b rows the batch build copied into the left half
           // (L2-resident) rather than gathering rows of the global X from HBM.
           bfw.push_back(BdOp{(const bf16*)C, sh.Kp, (int64_t)nb, sh.half, (void*)(C + sh.half), sh.Kp, nullptr, 0,
-                             sl.scale, sl.desc_dev, 0});
+                             sl.scale, sl.desc_dev, 0, /*keep_out*/ 1});
           a.add = C + sh.half; a.ld_add = sh.Kp;
           a.few_nnz = 1;
           if (l == 0) {
@@ -944,7 +944,8 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         if (l + 1 < L) {
           void* out = sage ? sl.C[l + 1] : sl.H[l + 1];
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, shp[l + 1].Kp, false, true,
-                              nullptr, 0, nullptr, 0, tc ? sl.mb[l + 1] : nullptr, tc ? c->mb_ld[l + 1] : 0});
+                              nullptr, 0, nullptr, 0, tc ? sl.mb[l + 1] : nullptr, tc ? c->mb_ld[l + 1] : 0,
+                              /*keep_out: read by the next aggregation + GEMM*/ 1, /*stream_a*/ 1});
         } else {
           fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false,
                               nullptr, 0, nullptr, 0});
@@ -952,13 +953,13 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
         // backward: dW_l = C_l^T dZ_l (fp32 into the packed gradient buffer)
         dw.push_back(GemmOp{true, false, sh.Kp, sh.Np, nb, C, sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
-                            nullptr, 0, nullptr, 0});
+                            nullptr, 0, nullptr, 0, nullptr, 0, 0, /*stream_a: C_l's last read*/ 1});
         g.dw_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
         if (l > 0) {
           // dC_l = dZ_l W_l^T
           // (bd: the epilogue pre-scales the neighbour half by 1/deg of the row: N^T = A diag(1/deg))
           dx.push_back(GemmOp{false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false,
-                              nullptr, 0, bd ? sl.scale : nullptr, sh.half});
+                              nullptr, 0, bd ? sl.scale : nullptr, sh.half, nullptr, 0, /*keep_out*/ 1, 0});
           g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
           SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
           b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
@@ -967,7 +968,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           if (tc) { b.mbits = sl.mb[l]; b.ld_mbits = c->mb_ld[l]; }  // ReLU mask of C_l / H_l as bits
           if (sage && bd) {  // dZ_{l-1} = (dC_self + A_blocks dC'_neigh + A_inter dC'_neigh) * 1[H_l > 0]
             bbw.push_back(BdOp{(const bf16*)sl.dC + sh.half, sh.Kp, (int64_t)nb, sh.half, sl.dZ[l - 1],
-                               shp[l - 1].Np, (const bf16*)sl.dC, sh.Kp, nullptr, sl.desc_dev, 0});
+                               shp[l - 1].Np, (const bf16*)sl.dC, sh.Kp, nullptr, sl.desc_dev, 0, /*keep_out*/ 1});
             b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
             b.add = (const T*)sl.dZ[l - 1]; b.ld_add = shp[l - 1].Np;
             b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;

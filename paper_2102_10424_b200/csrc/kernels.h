@@ -88,6 +88,9 @@ struct GemmOp {
   // [row * ldmb + col / 32] = 1[out[row, col] > 0] (read by the backward pass instead of out)
   uint32_t* mbits = nullptr;
   int64_t ldmb = 0;
+  // L2 residency hints: keep_out = the output is read again by the next kernels (evict_last);
+  // stream_a = this is the last read of A for a while (evict_first)
+  int keep_out = 0, stream_a = 0;
 };
 }  // namespace gist
 #include <cuda.h>
@@ -100,7 +103,7 @@ struct alignas(64) GemmSlotTC {
   const float* rscale;
   uint32_t* mbits;
   int64_t ldc, ldm, ldmb;
-  int M, N, K, relu, rs_from, tma_store;
+  int M, N, K, relu, rs_from, tma_store, keep_out, stream_a;
 };
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGroup];
@@ -132,6 +135,7 @@ struct BdOp {
   const float* rscale;
   const int32_t* desc;
   int global_rows;
+  int keep_out = 0;  // L2 hint for the output (see GemmOp)
 };
 struct alignas(64) BdSlot {
   CUtensorMap mb;
@@ -141,7 +145,7 @@ struct alignas(64) BdSlot {
   const float* rscale;
   const int32_t* desc;
   int64_t ldc, ldadd;
-  int N, global_rows, tma_store;
+  int N, global_rows, tma_store, keep_out;
 };
 struct BdGroup {
   CUtensorMap ma;  // all cluster blocks [num_clusters * BS, BS]
