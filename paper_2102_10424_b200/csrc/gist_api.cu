@@ -1606,6 +1606,8 @@ extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_
     a.self = self; a.H = (const bf16*)H_dev; a.ldh = ld; a.out = (bf16*)out_dev; a.ldo = ld; a.w = pad8(w);
     const char* few = std::getenv("GIST_SPMM_ENTRY_FEW");  // tools/kbench_inter.py: few-neighbour kernels
     a.few_nnz = few && few[0] == '1';
+    const char* add = std::getenv("GIST_SPMM_ENTRY_ADD");  // tools/kbench_inter.py: in-place add (out += ...)
+    if (add && add[0] == '1') { a.add = (const bf16*)out_dev; a.ld_add = ld; }
     spmm<bf16, bf16>(a, s);
   } else {
     return GIST_E_ARG;
