@@ -63,6 +63,7 @@ struct Slot {
   void* dC = nullptr;
   float* logits = nullptr;
   float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
+  uint32_t* ce_done = nullptr;  // softmax-CE last-CTA counter
   int last_nb = 0;
 };
 
@@ -818,6 +819,8 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     TRY(dalloc_t(c, &s.logits, (size_t)nbm * maxN[c->L - 1]));
     CK(cudaMemsetAsync(s.logits, 0, (size_t)nbm * maxN[c->L - 1] * 4, c->stream));
     TRY(dalloc_t(c, &s.row_loss, nbm));
+    TRY(dalloc_t(c, &s.ce_done, 1));
+    CK(cudaMemsetAsync(s.ce_done, 0, 4, c->stream));
     TRY(dalloc_t(c, &s.step_loss, 1));
     TRY(dalloc_t(c, &s.loss_acc, 1));
   }
@@ -903,6 +906,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           CeSlot<T>& e = g.ce.s[j];
           e.logits = sl.logits; e.dlog = (T*)sl.dZ[L - 1]; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
           e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
+          e.done = sl.ce_done;
         }
         T* C = (T*)sl.C[l];
         // forward aggregation (a2)
@@ -1189,10 +1193,9 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   {
     const double bytes = (double)g.count * c->nb_max_rows * (g.ce.ld * (4.0 + sizeof(T)) + 17.0);
     const int id = prof_begin(c, s, GIST_PROF_LOSS, bytes);
-    softmax_ce<T>(g.ce, s);
-    reduce_loss<T>(g.ce, s);
+    softmax_ce<T>(g.ce, s);  // (its last CTA per slot also reduces the step loss)
     prof_end(c, s, id);
-    c->nk += 2;
+    c->nk += 1;
   }
   // ---- a5/a6: backward
   for (int l = L - 1; l >= 0; --l) {
@@ -1216,7 +1219,7 @@ static gist_status run_optimizer(gist_ctx* c) {
   else
     PL(GIST_PROF_OPTIM, (double)n * (12.0 + (c->Wball ? 2.0 : 0.0)), s,
        sgd_step(c->Wall, c->Gall, n, c->dstate, c->Wball, s));
-  LK(step_advance(c->dstate, s));
+  ++c->nk;  // (no step_advance launch: the optimizer's last CTA advances the step state)
   return GIST_OK;
 }
 
@@ -1297,7 +1300,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
     c->h2d += (int64_t)local_iters * per * 4;
     CK(cudaMemsetAsync(sl.loss_acc, 0, 4, s));
   }
-  *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0.f};
+  *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0u};
   CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
   CK(cudaEventRecord(c->hstate_ev, s));
   for (int z = 0; z < local_iters; ++z) {

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
         }
       }
     };
-    if (end - rp[g] > 1024) walk(std::integral_constant<int, 256>());
+    if (end - rp[g] > 128) walk(std::integral_constant<int, 256>());
     else walk(std::integral_constant<int, 128>());
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
     if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)

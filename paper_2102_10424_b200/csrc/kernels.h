@@ -192,7 +192,8 @@ void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cud
 // t = optimizer steps taken since the last partition, lr = learning rate of the call.
 struct StepState {
   int32_t z, t;
-  float lr, pad_;
+  float lr;
+  uint32_t done;  // optimizer CTAs finished this step (the last one advances z, t and resets it)
 };
 // Per-step batch descriptor (host-built, R7), 3q+4 int32:
 //   [bcl(q) | loff(q+1) | voff(q+1) | qq | tag]
@@ -250,6 +251,7 @@ struct CeSlot {
   const uint8_t* train;
   const int64_t* stats;
   float *step_loss, *loss_acc;
+  uint32_t* done;  // CTAs of this slot finished (the last one reduces the loss and resets it)
 };
 template <typename T>
 struct CeGroup {
@@ -260,11 +262,11 @@ struct CeGroup {
 // per slot: dlogits = (softmax - onehot)/n_train on train rows (else 0), row losses
 template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);
 // per slot: step_loss = sum(row_loss)/n_train (0 if none); loss_acc += step_loss
-template <typename T> void reduce_loss(const CeGroup<T>& G, cudaStream_t s);
 // Adam (R8) over n packed parameters; bias corrections from st->t (device), lr from st->lr
 void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
-               const StepState* st, bf16* Wb, cudaStream_t s);
-void sgd_step(float* W, const float* G, int64_t n, const StepState* st, bf16* Wb, cudaStream_t s);
+               StepState* st, bf16* Wb, cudaStream_t s);
+void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s);
+// (the optimizer kernels advance the step state themselves: their last CTA increments z, t)
 void step_advance(StepState* st, cudaStream_t s);
 void f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
 

@@ -9,37 +9,59 @@ namespace gist {
 
 // One warp per batch row (grid.y = slot).  loss_v = logsumexp(z_v) - z_v[y_v] on train
 // rows; dlogits_v = (softmax(z_v) - onehot(y_v)) / n_train on train rows, else 0;
-// padding columns [k, ld) are written as 0.
+// padding columns [k, ld) are written as 0.  The last CTA of each slot to finish sums the
+// row losses in a fixed order (deterministic) into step_loss / loss_acc.
 template <typename T>
-__global__ void k_softmax_ce(const __grid_constant__ CeGroup<T> G) {
+__global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGroup<T> G) {
   pdl_wait();
   pdl_trigger();
   const CeSlot<T>& S = G.s[blockIdx.y];
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (v >= G.rows) return;
-  const int64_t ld = G.ld;
-  const int k = G.k;
-  const float* z = S.logits + (int64_t)v * ld;
   const int64_t nt = S.stats[1];
-  const bool tr = S.train[v] && nt > 0;
-  float mx = -INFINITY;
-  for (int c = lane; c < k; c += 32) mx = fmaxf(mx, z[c]);
+  if (v < G.rows) {
+    const int64_t ld = G.ld;
+    const int k = G.k;
+    const float* z = S.logits + (int64_t)v * ld;
+    const bool tr = S.train[v] && nt > 0;
+    float mx = -INFINITY;
+    for (int c = lane; c < k; c += 32) mx = fmaxf(mx, z[c]);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float se = 0.f;
-  for (int c = lane; c < k; c += 32) se += expf(z[c] - mx);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f;
+    for (int c = lane; c < k; c += 32) se += expf(z[c] - mx);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-  const float lse = mx + logf(se);
-  const int y = S.lab[v];
-  const float inv = tr ? 1.0f / (float)nt : 0.f;
-  for (int c = lane; c < ld; c += 32) {
-    float g = 0.f;
-    if (tr && c < k) g = (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) * inv;
-    S.dlog[(int64_t)v * ld + c] = Elem<T>::from_f(g);
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float lse = mx + logf(se);
+    const int y = S.lab[v];
+    const float inv = tr ? 1.0f / (float)nt : 0.f;
+    for (int c = lane; c < ld; c += 32) {
+      float g = 0.f;
+      if (tr && c < k) g = (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) * inv;
+      S.dlog[(int64_t)v * ld + c] = Elem<T>::from_f(g);
+    }
+    if (lane == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
   }
-  if (lane == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(S.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  using Red = cub::BlockReduce<float, 256>;
+  __shared__ typename Red::TempStorage tr;
+  float acc = 0.f;
+  for (int r = threadIdx.x; r < G.rows; r += blockDim.x) acc += __ldcg(S.row_loss + r);
+  const float tot = Red(tr).Sum(acc);
+  if (threadIdx.x == 0) {
+    const float l = nt > 0 ? tot / (float)nt : 0.f;
+    S.step_loss[0] = l;
+    S.loss_acc[0] += l;
+    *S.done = 0;
+  }
 }
 
 template <typename T>
@@ -50,38 +72,29 @@ void softmax_ce(const CeGroup<T>& G, cudaStream_t s) {
 template void softmax_ce<float>(const CeGroup<float>&, cudaStream_t);
 template void softmax_ce<bf16>(const CeGroup<bf16>&, cudaStream_t);
 
-// one CTA per slot, fixed-order tree: deterministic
-template <typename T>
-__global__ void __launch_bounds__(1024) k_reduce_loss(const __grid_constant__ CeGroup<T> G) {
-  pdl_wait();
-  pdl_trigger();
-  const CeSlot<T>& S = G.s[blockIdx.x];
-  using Red = cub::BlockReduce<float, 1024>;
-  __shared__ typename Red::TempStorage tr;
-  float acc = 0.f;
-  for (int v = threadIdx.x; v < G.rows; v += 1024) acc += S.row_loss[v];
-  const float tot = Red(tr).Sum(acc);
+
+// Called by every CTA of an optimizer launch after its last read of *st: the last CTA to
+// finish advances the step state for the next step (replaces a separate 1-thread launch).
+__device__ __forceinline__ void advance_if_last(StepState* st) {
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const int64_t nt = S.stats[1];
-    const float l = nt > 0 ? tot / (float)nt : 0.f;
-    S.step_loss[0] = l;
-    S.loss_acc[0] += l;
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->done, 1u);
+    if (prev == gridDim.x - 1) {
+      st->z += 1;
+      st->t += 1;
+      st->done = 0;
+      __threadfence();
+    }
   }
 }
-template <typename T>
-void reduce_loss(const CeGroup<T>& G, cudaStream_t s) {
-  if (G.n <= 0) return;
-  launch_pdl(k_reduce_loss<T>, (unsigned)G.n, 1024, 0, s, G);
-}
-template void reduce_loss<float>(const CeGroup<float>&, cudaStream_t);
-template void reduce_loss<bf16>(const CeGroup<bf16>&, cudaStream_t);
 
 // Adam, PyTorch form (R8): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
 // w -= (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps), bc_i = 1 - b_i^t, t from the device
 // step state (so the launch is identical every step).  Optionally refreshes the bf16 shadow.
 __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float* __restrict__ M,
-                       float* __restrict__ V, int64_t n, float b1, float b2, float eps,
-                       const StepState* __restrict__ st, bf16* __restrict__ Wb) {
+                       float* __restrict__ V, int64_t n, float b1, float b2, float eps, StepState* st,
+                       bf16* __restrict__ Wb) {
   pdl_wait();
   pdl_trigger();
   __shared__ float s_step, s_bc2;
@@ -114,15 +127,16 @@ __global__ void k_adam(float* __restrict__ W, const float* __restrict__ G, float
       reinterpret_cast<__nv_bfloat162*>(Wb)[2 * i + 1] = __floats2bfloat162_rn(w.z, w.w);
     }
   }
+  advance_if_last(st);
 }
 void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
-               const StepState* st, bf16* Wb, cudaStream_t s) {
+               StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n >> 2, 256) < 148 * 8 ? cdiv(n >> 2, 256) : 148 * 8;
   launch_pdl(k_adam, (unsigned)(blocks > 0 ? blocks : 1), 256, 0, s, W, G, M, V, n, b1, b2, eps, st, Wb);
 }
 
-__global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, const StepState* st,
+__global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, StepState* st,
                       bf16* __restrict__ Wb) {
   pdl_wait();
   pdl_trigger();
@@ -132,8 +146,9 @@ __global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_
     W[i] = w;
     if (Wb) Wb[i] = __float2bfloat16_rn(w);
   }
+  advance_if_last(st);
 }
-void sgd_step(float* W, const float* G, int64_t n, const StepState* st, bf16* Wb, cudaStream_t s) {
+void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
   launch_pdl(k_sgd, (unsigned)blocks, 256, 0, s, W, G, n, st, Wb);
