@@ -239,6 +239,8 @@ struct Epi {
   const CUtensorMap* mc;  // TMA store map of C, or nullptr (direct stores)
   int clip;               // rows >= rows_valid lie outside mc (TMA clips them): every warp may use it
   int keep;               // L2 evict_last hint on the output stores
+  const uint32_t* mbits_in;  // bit-packed ReLU mask applied after add (words [row * ldmbi + col / 32])
+  int64_t ldmbi;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -279,6 +281,12 @@ __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, i
   if (E.relu) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
+  }
+  if (E.mbits_in) {  // ReLU'(0) = 0 of the layer below (R3), bit-packed (col % 16 == 0 here)
+    const uint32_t wd = E.mbits_in[row * E.ldmbi + (col >> 5)] >> (col & 31);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (!((wd >> i) & 1u)) v[i] = 0.f;
   }
   if (E.mask) {  // ReLU'(0) = 0 of the layer below (R3): out = acc * 1[mask > 0]
     const bf16* mp = E.mask + row * E.ldm + col;
@@ -358,8 +366,8 @@ struct ProbPlain {
     T.rows_valid = S.M - m0;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, nullptr, 0, S.mbits, S.ldmb,
-                 S.tma_store ? &S.mc : nullptr, 1, S.keep_out};
+    T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, S.add, S.ldadd, S.mbits, S.ldmb,
+                 S.tma_store ? &S.mc : nullptr, 1, S.keep_out, S.mbits_in, S.ldmbi};
     T.stream_a = S.stream_a;
     return T;
   }
@@ -401,7 +409,7 @@ struct ProbBd {
     T.n0 = n0;
     T.N = S.N;
     T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &S.mc : nullptr, 0,
-              S.keep_out};
+              S.keep_out, nullptr, 0};
     T.stream_a = 0;
     T.b_col = n0;
     T.K = G.bs;
@@ -1021,7 +1029,7 @@ void launch_bd(const BdPlan& P, cudaStream_t s) {
 }  // namespace
 
 bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
-  if (!get_encode() || n < 1 || n > kMaxGroup) return false;
+  if (!get_encode() || n < 1 || n > kMaxGemmOps) return false;
   const GemmOp& o0 = ops[0];
   P->a_mn = o0.transA;     // A stored K x M
   P->b_mn = !o0.transB;    // B stored K x N
@@ -1062,6 +1070,10 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.rs_from = o.rs_from;
     S.mbits = o.mbits;
     S.ldmb = o.ldmb;
+    S.add = o.add;
+    S.ldadd = o.ldadd;
+    S.mbits_in = o.mbits_in;
+    S.ldmbi = o.ldmbi;
     S.keep_out = l2hint_enabled() ? o.keep_out : 0;
     S.stream_a = l2hint_enabled() ? o.stream_a : 0;
     S.tma_store = tma_store_enabled() && make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;

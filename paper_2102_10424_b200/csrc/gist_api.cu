@@ -64,6 +64,9 @@ struct Slot {
   float* logits = nullptr;
   float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
   uint32_t* ce_done = nullptr;  // softmax-CE last-CTA counter
+  // re-associated last layer (BF16 GraphSAGE): P = H W_bot, AGG = N P, DQ = [dZ | Q = N^T dZ],
+  // DZs = dZ / deg (block-diagonal path)
+  void *rP = nullptr, *rAGG = nullptr, *rDQ = nullptr, *rDZs = nullptr;
   int last_nb = 0;
 };
 
@@ -82,6 +85,12 @@ struct StepPlan {
     std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
     std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
     CeGroup<T> ce;
+    // re-associated last layer: Z = H W_top + N (H W_bot); backward via Q = N^T dZ
+    bool reassoc = false;
+    GemmPlanTC ra_p, ra_z, ra_dw, ra_dha, ra_dhb;
+    BdPlan ra_fbd, ra_bbd;
+    SpmmGroup<T, T> ra_fsp, ra_bsp;
+    double ra_gemm_fl = 0.0, ra_bd_fl = 0.0, ra_fby = 0.0, ra_bby = 0.0;
   };
   std::vector<Group> groups;
 };
@@ -139,6 +148,7 @@ struct gist_ctx {
   bf16* Wball = nullptr;                       // bf16 shadow of Wall (BF16 mode)
   int nb_max_rows = 0;                         // static row count of every batch launch
   std::vector<int64_t> mb_ld;                  // words per row of Slot::mb[l]
+  bool reassoc = false;                        // last SAGE layer re-associated (BF16, L >= 2)
   StepState* dstate = nullptr;                 // device step state (z, t, lr)
   StepState* hstate = nullptr;                 // pinned host staging for it
   cudaEvent_t hstate_ev = nullptr;
@@ -814,6 +824,19 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
       CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
     }
+    c->reassoc = c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->L >= 2;
+    if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->reassoc && e[0] != '0';
+    if (c->reassoc) {
+      const size_t npl = (size_t)maxN[c->L - 1];
+      TRY(dalloc(c, &s.rP, (size_t)nbm * npl * E));
+      TRY(dalloc(c, &s.rAGG, (size_t)nbm * npl * E));
+      TRY(dalloc(c, &s.rDQ, (size_t)nbm * 2 * npl * E));
+      TRY(dalloc(c, &s.rDZs, (size_t)nbm * 2 * npl * E));
+      CK(cudaMemsetAsync(s.rP, 0, (size_t)nbm * npl * E, c->stream));
+      CK(cudaMemsetAsync(s.rAGG, 0, (size_t)nbm * npl * E, c->stream));
+      CK(cudaMemsetAsync(s.rDQ, 0, (size_t)nbm * 2 * npl * E, c->stream));
+      CK(cudaMemsetAsync(s.rDZs, 0, (size_t)nbm * 2 * npl * E, c->stream));
+    }
     TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
     CK(cudaMemsetAsync(s.dC, 0, (size_t)nbm * maxKall * E, c->stream));
     TRY(dalloc_t(c, &s.logits, (size_t)nbm * maxN[c->L - 1]));
@@ -892,9 +915,88 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.ce.rows = nb;
     g.ce.k = c->k;
     g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
+    g.reassoc = c->reassoc && tc && sage && L >= 2;
     for (int l = 0; l < L; ++l) {
       std::vector<GemmOp> fw, dw, dx;
       std::vector<BdOp> bfw, bbw;
+      if (g.reassoc && l == L - 1) {
+        // Re-associated last GraphSAGE layer (exact algebra of Eq. (2), with the
+        // class width far below the hidden width): Z = H W_top + N (H W_bot), so the
+        // aggregation runs at the class width Np instead of the hidden width; backward:
+        // Q = N^T dZ (width Np), dW_top = H^T dZ, dW_bot = H^T Q, dH = dZ W_top^T + Q W_bot^T.
+        std::vector<GemmOp> op_p, op_z, op_w, op_ha, op_hb;
+        std::vector<BdOp> fb, bb;
+        for (int j = 0; j < g.count; ++j) {
+          Slot& sl = c->slots[g0 + j];
+          const auto& shp = c->shapes[sl.index];
+          const LayerShape& sh = shp[l];
+          const int64_t Np = sh.Np, half = sh.half, Kp = sh.Kp;
+          const bf16* Wl = sl.Wb + sh.off;  // [W_top; W_bot], Kp x Np
+          const bf16* H = (const bf16*)sl.C[l];  // left half of C_l (written by GEMM l-1)
+          bf16 *P = (bf16*)sl.rP, *AGG = (bf16*)sl.rAGG, *DQ = (bf16*)sl.rDQ, *DZs = (bf16*)sl.rDZs;
+          op_p.push_back(GemmOp{false, false, nb, Np, half, H, Kp, Wl + half * Np, Np, P, Np, false, false, nullptr, 0,
+                                nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0});
+          GemmOp z{false, false, nb, Np, half, H, Kp, Wl, Np, sl.logits, Np, true, false, nullptr, 0, nullptr, 0};
+          z.add = AGG; z.ldadd = Np;
+          op_z.push_back(z);
+          // forward aggregation of P
+          SpmmArgs<T, T>& a = g.ra_fsp.a[j];
+          a = SpmmArgs<T, T>();
+          a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
+          a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
+          a.rowscale = sl.scale; a.H = (const T*)P; a.ldh = Np; a.w = Np; a.out = (T*)AGG; a.ldo = Np;
+          if (bd) {
+            fb.push_back(BdOp{P, Np, (int64_t)nb, Np, (void*)AGG, Np, nullptr, 0, sl.scale, sl.desc_dev, 0, 1});
+            a.add = (const T*)AGG; a.ld_add = Np; a.few_nnz = 1;
+          }
+          g.ra_fby += spmm_bytes(a);
+          // backward: Q = N^T dZ into DQ[:, Np:2Np) (dZ in DQ[:, 0:Np) from the loss kernel)
+          SpmmArgs<T, T>& b = g.ra_bsp.a[j];
+          b = SpmmArgs<T, T>();
+          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
+          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
+          b.w = Np; b.out = (T*)(DQ + Np); b.ldo = 2 * Np;
+          if (bd) {  // N^T = A diag(1/deg): aggregate DZs = dZ / deg (written by the loss kernel)
+            bb.push_back(BdOp{DZs, 2 * Np, (int64_t)nb, Np, (void*)(DQ + Np), 2 * Np, nullptr, 0, nullptr, sl.desc_dev, 0, 1});
+            b.H = (const T*)DZs; b.ldh = 2 * Np;
+            b.add = (const T*)(DQ + Np); b.ld_add = 2 * Np; b.few_nnz = 1;
+          } else {
+            b.colscale = sl.scale; b.H = (const T*)DQ; b.ldh = 2 * Np;
+          }
+          g.ra_bby += spmm_bytes(b);
+          op_w.push_back(GemmOp{true, false, half, Np, nb, H, Kp, DQ, 2 * Np, sl.G + sh.off, Np, true, false, nullptr, 0,
+                                nullptr, 0, nullptr, 0, 0, /*stream_a*/ 1});
+          op_w.push_back(GemmOp{true, false, half, Np, nb, H, Kp, DQ + Np, 2 * Np, sl.G + sh.off + half * Np, Np, true,
+                                false, nullptr, 0, nullptr, 0, nullptr, 0, 0, 1});
+          // dH = dZ W_top^T (T, in dC) then Q W_bot^T + T, masked by ReLU'(H) -> dZ_{l-1}
+          op_ha.push_back(GemmOp{false, true, nb, half, Np, DQ, 2 * Np, Wl, Np, sl.dC, Kp, false, false, nullptr, 0,
+                                 nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0});
+          GemmOp hb{false, true, nb, half, Np, DQ + Np, 2 * Np, Wl + half * Np, Np, sl.dZ[l - 1], shp[l - 1].Np, false,
+                    false, nullptr, 0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
+          hb.add = (const bf16*)sl.dC; hb.ldadd = Kp;
+          hb.mbits_in = sl.mb[l]; hb.ldmbi = c->mb_ld[l];
+          op_hb.push_back(hb);
+          g.ra_gemm_fl += 2.0 * nb * Np * half * 6;
+          if (bd) g.ra_bd_fl += 2.0 * q * c->bs * c->bs * Np;
+        }
+        g.ra_fsp.n = g.ra_bsp.n = g.count;
+        if (bd && (!gemm_bd_prepare(c->blocks, c->c, c->bs, fb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_fbd) ||
+                   !gemm_bd_prepare(c->blocks, c->c, c->bs, bb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_bbd)))
+          return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: block-diagonal plan failed");
+        if (!gemm_bf16_prepare(op_p.data(), g.count, &g.ra_p) || !gemm_bf16_prepare(op_z.data(), g.count, &g.ra_z) ||
+            !gemm_bf16_prepare(op_w.data(), 2 * g.count, &g.ra_dw) ||
+            !gemm_bf16_prepare(op_ha.data(), g.count, &g.ra_dha) || !gemm_bf16_prepare(op_hb.data(), g.count, &g.ra_dhb))
+          return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: tcgen05 GEMM plan failed");
+        // the loss kernel writes dZ into DQ[:, 0:Np) (and dZ / deg for the block-diagonal path)
+        g.ce.ld_dlog = 2 * (int64_t)c->shapes[c->slots[g0].index][l].Np;
+        for (int j = 0; j < g.count; ++j) {
+          Slot& sl = c->slots[g0 + j];
+          g.ce.s[j].dlog = (T*)sl.rDQ;
+          g.ce.s[j].dlog_s = bd ? (T*)sl.rDZs : nullptr;
+          g.ce.s[j].scale_s = sl.scale;
+        }
+        continue;
+      }
       for (int j = 0; j < g.count; ++j) {
         Slot& sl = c->slots[g0 + j];
         const auto& shp = c->shapes[sl.index];
@@ -1183,8 +1285,21 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     ++c->nk;
   };
   const bool bd = c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE;
+  auto tc_l = [&](const GemmPlanTC& P, double fl) {  // one tcgen05 GEMM launch (BF16 plans only)
+    const int id = prof_begin(c, s, GIST_PROF_GEMM, fl);
+    gemm_bf16_launch(P, s);
+    prof_end(c, s, id);
+    ++c->nk;
+  };
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
+    if (g.reassoc && l == L - 1) {  // Z = H W_top + N (H W_bot)
+      tc_l(g.ra_p, g.ra_gemm_fl / 6);
+      if (bd) bd_l(g.ra_fbd, g.ra_bd_fl / 2);
+      spmm_l(g.ra_fsp, g.ra_fby);
+      tc_l(g.ra_z, g.ra_gemm_fl / 6);
+      continue;
+    }
     if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
     spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
     launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
@@ -1199,6 +1314,14 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   }
   // ---- a5/a6: backward
   for (int l = L - 1; l >= 0; --l) {
+    if (g.reassoc && l == L - 1) {  // Q = N^T dZ; dW = [H^T dZ; H^T Q]; dZ_{l-1} = (dZ W_top^T + Q W_bot^T) * ReLU'
+      if (bd) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
+      spmm_l(g.ra_bsp, g.ra_bby);
+      tc_l(g.ra_dw, g.ra_gemm_fl / 3);
+      tc_l(g.ra_dha, g.ra_gemm_fl / 6);
+      tc_l(g.ra_dhb, g.ra_gemm_fl / 6);
+      continue;
+    }
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
     if (l == 0) break;
     launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);

@@ -54,6 +54,8 @@ template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStr
 
 // Grouped launch: the same SpMM for up to kMaxGroup sub-GCN slots in one grid (grid.y = slot).
 constexpr int kMaxGroup = 8;
+// a grouped tcgen05 GEMM launch may carry two operand sets per slot (re-associated last layer)
+constexpr int kMaxGemmOps = 2 * kMaxGroup;
 template <typename TI, typename TO = TI>
 struct SpmmGroup {
   SpmmArgs<TI, TO> a[kMaxGroup];
@@ -91,6 +93,12 @@ struct GemmOp {
   // L2 residency hints: keep_out = the output is read again by the next kernels (evict_last);
   // stream_a = this is the last read of A for a while (evict_first)
   int keep_out = 0, stream_a = 0;
+  // optional (BF16 path): out += add (bf16, ldadd), then out *= 1[bit] with the bit-packed
+  // ReLU mask mbits_in (words [row * ldmbi + col / 32]) of the layer below
+  const bf16* add = nullptr;
+  int64_t ldadd = 0;
+  const uint32_t* mbits_in = nullptr;
+  int64_t ldmbi = 0;
 };
 }  // namespace gist
 #include <cuda.h>
@@ -102,11 +110,13 @@ struct alignas(64) GemmSlotTC {
   const void* mask;
   const float* rscale;
   uint32_t* mbits;
-  int64_t ldc, ldm, ldmb;
+  const bf16* add;
+  const uint32_t* mbits_in;
+  int64_t ldc, ldm, ldmb, ldadd, ldmbi;
   int M, N, K, relu, rs_from, tma_store, keep_out, stream_a;
 };
 struct GemmGroupTC {
-  GemmSlotTC s[kMaxGroup];
+  GemmSlotTC s[kMaxGemmOps];
   int n = 0, tm = 0, tn = 0;  // slots, M tiles, N tiles (persistent tile space)
 };
 // Host-side plan of one grouped tcgen05 GEMM (tensor maps encoded once, launched many times).
@@ -252,12 +262,15 @@ struct CeSlot {
   const int64_t* stats;
   float *step_loss, *loss_acc;
   uint32_t* done;  // CTAs of this slot finished (the last one reduces the loss and resets it)
+  T* dlog_s = nullptr;              // optional second output: dlogits * scale[v] (row scale)
+  const float* scale_s = nullptr;
 };
 template <typename T>
 struct CeGroup {
   CeSlot<T> s[kMaxGroup];
   int n = 0, rows = 0, k = 0;
-  int64_t ld = 0;
+  int64_t ld = 0;       // logits row stride
+  int64_t ld_dlog = 0;  // dlogits (and dlog_s) row stride; 0 = ld
 };
 // per slot: dlogits = (softmax - onehot)/n_train on train rows (else 0), row losses
 template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);

@@ -35,10 +35,13 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
     const float lse = mx + logf(se);
     const int y = S.lab[v];
     const float inv = tr ? 1.0f / (float)nt : 0.f;
+    const int64_t ldd = G.ld_dlog ? G.ld_dlog : ld;
+    const float sv = S.dlog_s ? S.scale_s[v] : 0.f;
     for (int c = lane; c < ld; c += 32) {
       float g = 0.f;
       if (tr && c < k) g = (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) * inv;
-      S.dlog[(int64_t)v * ld + c] = Elem<T>::from_f(g);
+      S.dlog[(int64_t)v * ldd + c] = Elem<T>::from_f(g);
+      if (S.dlog_s) S.dlog_s[(int64_t)v * ldd + c] = Elem<T>::from_f(g * sv);
     }
     if (lane == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
   }

@@ -77,6 +77,17 @@ def test_bf16_one_step(name, kw, arch, dims, q):
             assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= BF16_TOL, l
 
 
+@pytest.mark.parametrize("bd,reassoc", [("0", "1"), ("1", "0"), ("0", "0")])
+@pytest.mark.parametrize("name,kw,arch,dims,q", [c for c in CASES if c[2] == "sage"])
+def test_bf16_one_step_sage_aggregation_variants(name, kw, arch, dims, q, bd, reassoc, monkeypatch):
+    """GraphSAGE BF16 with and without the block-diagonal tensor-core aggregation (GIST_BD) and
+    with and without the re-associated last layer (GIST_REASSOC: Z = H W_top + N (H W_bot),
+    Q = N^T dZ at the class width); the default (both on) is covered above."""
+    monkeypatch.setenv("GIST_BD", bd)
+    monkeypatch.setenv("GIST_REASSOC", reassoc)
+    test_bf16_one_step(name, kw, arch, dims, q)
+
+
 @pytest.mark.parametrize("optimizer,lr", [("sgd", 0.1), ("adam", 0.001)])  # well-conditioned trajectories (DESIGN.md)
 def test_bf16_loss_curve_C1_10_rounds(optimizer, lr):
     """north_star: BF16 mode loss curve within 1% after 10 rounds (C1 = Cora-shaped, m=2,
