@@ -1043,13 +1043,16 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     maxM = ops[i].M > maxM ? ops[i].M : maxM;
   }
   P->bn = maxN > 128 ? 256 : 128;  // persistent kernel: wide tiles amortise the epilogue
-  // CTA pairs for large GEMMs (>= 4 tiles per SM: measured 82 -> 88% of peak at width 4096);
-  // the step's small grouped GEMMs (~3 tiles per SM) and the cluster-block aggregation stay
-  // on one CTA per tile (pairs measured slower there)
+  // CTA pairs for large, long-K GEMMs (>= 4 tiles per SM and K >= 2048: measured 82 -> 88% of
+  // peak at width 4096); short-K GEMMs (the C3 step's dX, K = 512: 27 -> 41 us as pairs) and
+  // the cluster-block aggregation stay on one CTA per tile
   {
-    int64_t tiles = 0;
-    for (int i = 0; i < n; ++i) tiles += cdiv(ops[i].M, BM) * cdiv(ops[i].N, P->bn);
-    P->pair = pair_enabled() && tiles >= 4 * (int64_t)num_sms();
+    int64_t tiles = 0, kmin = INT64_MAX;
+    for (int i = 0; i < n; ++i) {
+      tiles += cdiv(ops[i].M, BM) * cdiv(ops[i].N, P->bn);
+      kmin = ops[i].K < kmin ? ops[i].K : kmin;
+    }
+    P->pair = pair_enabled() && tiles >= 4 * (int64_t)num_sms() && kmin >= 2048;
   }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
