@@ -37,8 +37,8 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
   }
 }
 
-template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE>
-__global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
+template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE, bool PRED = false>
+__global__ void __launch_bounds__(256, PRED ? 3 : (J == 1 && sizeof(TI) == 2) ? 4
                                            : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
   pdl_wait();
@@ -100,39 +100,64 @@ __global__ void __launch_bounds__(256, (J == 1 && sizeof(TI) == 2) ? 4
       ou = (Off)(a.h_index ? (int64_t)a.h_index[u] : (int64_t)u) * ldv;
     }
     int jj = 0;
-    for (; jj + UNROLL <= n; jj += UNROLL) {
-      uint4 x[UNROLL][J];
-      float s[UNROLL];
+    if constexpr (PRED) {  // all UNROLL gathers of a round in flight, predicated (no serial tail)
+      for (; jj < n; jj += UNROLL) {
+        uint4 x[UNROLL][J];
 #pragma unroll
-      for (int q = 0; q < UNROLL; ++q) {
-        const Off r = __shfl_sync(gmask, ou, jj + q, LPR);
-        s[q] = CSCALE ? __shfl_sync(gmask, su, jj + q, LPR) : 1.f;
+        for (int q = 0; q < UNROLL; ++q) {
+          const bool on = jj + q < n;  // uniform over the group
+          const Off r = __shfl_sync(gmask, ou, on ? jj + q : 0, LPR);
 #pragma unroll
-        for (int j = 0; j < J; ++j)
-          if (act[j]) x[q][j] = __ldg(H4 + r + vbase + j * LPR);
+          for (int j = 0; j < J; ++j)
+            if (act[j] && on) x[q][j] = __ldg(H4 + r + vbase + j * LPR);
+        }
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q)
+          if (jj + q < n)
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+              if (act[j]) {
+                float t[V];
+                unpack(x[q][j], t, TI());
+#pragma unroll
+                for (int i = 0; i < V; ++i) acc[j][i] += t[i];
+              }
       }
+    } else {
+      for (; jj + UNROLL <= n; jj += UNROLL) {
+        uint4 x[UNROLL][J];
+        float s[UNROLL];
 #pragma unroll
-      for (int q = 0; q < UNROLL; ++q)
+        for (int q = 0; q < UNROLL; ++q) {
+          const Off r = __shfl_sync(gmask, ou, jj + q, LPR);
+          s[q] = CSCALE ? __shfl_sync(gmask, su, jj + q, LPR) : 1.f;
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+            if (act[j]) x[q][j] = __ldg(H4 + r + vbase + j * LPR);
+        }
+#pragma unroll
+        for (int q = 0; q < UNROLL; ++q)
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+            if (act[j]) {
+              float t[V];
+              unpack(x[q][j], t, TI());
+#pragma unroll
+              for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s[q], t[i], acc[j][i]) : acc[j][i] + t[i];
+            }
+      }
+      for (; jj < n; ++jj) {
+        const Off r = __shfl_sync(gmask, ou, jj, LPR);
+        const float s = CSCALE ? __shfl_sync(gmask, su, jj, LPR) : 1.f;
 #pragma unroll
         for (int j = 0; j < J; ++j)
           if (act[j]) {
             float t[V];
-            unpack(x[q][j], t, TI());
+            unpack(__ldg(H4 + r + vbase + j * LPR), t, TI());
 #pragma unroll
-            for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s[q], t[i], acc[j][i]) : acc[j][i] + t[i];
+            for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s, t[i], acc[j][i]) : acc[j][i] + t[i];
           }
-    }
-    for (; jj < n; ++jj) {
-      const Off r = __shfl_sync(gmask, ou, jj, LPR);
-      const float s = CSCALE ? __shfl_sync(gmask, su, jj, LPR) : 1.f;
-#pragma unroll
-      for (int j = 0; j < J; ++j)
-        if (act[j]) {
-          float t[V];
-          unpack(__ldg(H4 + r + vbase + j * LPR), t, TI());
-#pragma unroll
-          for (int i = 0; i < V; ++i) acc[j][i] = CSCALE ? fmaf(s, t[i], acc[j][i]) : acc[j][i] + t[i];
-        }
+      }
     }
   }
   const float rs = a.rowscale ? a.rowscale[v] : 1.f;
@@ -361,6 +386,13 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   const int nchunks = (int)cdiv(w, CW);
   const int64_t groups = rows * nchunks;
   const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
+  if (G.a[0].few_nnz && J == 1 && !G.a[0].colscale) {  // few neighbours, narrow rows: the row's
+    // dependency chain dominates (not bytes), so every round keeps 8 gathers in flight
+    const bool wide = G.a[0].h_index != nullptr;
+    if (wide) launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, true, true>, grid, 256, 0, s, G, nchunks);
+    else launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, false, true>, grid, 256, 0, s, G, nchunks);
+    return;
+  }
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
     const bool wide = G.a[0].h_index != nullptr;
     if (G.a[0].colscale) {
