@@ -67,6 +67,7 @@ struct Slot {
   // re-associated last layer (BF16 GraphSAGE): P = H W_bot, AGG = N P, DQ = [dZ | Q = N^T dZ],
   // DZs = dZ / deg (block-diagonal path)
   void *rP = nullptr, *rAGG = nullptr, *rDQ = nullptr, *rDZs = nullptr;
+  void* rWc = nullptr;  // [W_top | W_bot] of the last layer, half x 2Np bf16 (refreshed every step)
   int last_nb = 0;
 };
 
@@ -87,7 +88,8 @@ struct StepPlan {
     CeGroup<T> ce;
     // re-associated last layer: Z = H W_top + N (H W_bot); backward via Q = N^T dZ
     bool reassoc = false;
-    GemmPlanTC ra_p, ra_z, ra_dw, ra_dha, ra_dhb;
+    GemmPlanTC ra_p, ra_z, ra_dw, ra_dh;
+    RelayoutGroup ra_wc;
     BdPlan ra_fbd, ra_bbd;
     SpmmGroup<T, T> ra_fsp, ra_bsp;
     double ra_gemm_fl = 0.0, ra_bd_fl = 0.0, ra_fby = 0.0, ra_bby = 0.0;
@@ -832,6 +834,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
       TRY(dalloc(c, &s.rAGG, (size_t)nbm * npl * E));
       TRY(dalloc(c, &s.rDQ, (size_t)nbm * 2 * npl * E));
       TRY(dalloc(c, &s.rDZs, (size_t)nbm * 2 * npl * E));
+      TRY(dalloc(c, &s.rWc, (size_t)maxK[c->L - 1] * npl * E));
       CK(cudaMemsetAsync(s.rP, 0, (size_t)nbm * npl * E, c->stream));
       CK(cudaMemsetAsync(s.rAGG, 0, (size_t)nbm * npl * E, c->stream));
       CK(cudaMemsetAsync(s.rDQ, 0, (size_t)nbm * 2 * npl * E, c->stream));
@@ -924,7 +927,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         // class width far below the hidden width): Z = H W_top + N (H W_bot), so the
         // aggregation runs at the class width Np instead of the hidden width; backward:
         // Q = N^T dZ (width Np), dW_top = H^T dZ, dW_bot = H^T Q, dH = dZ W_top^T + Q W_bot^T.
-        std::vector<GemmOp> op_p, op_z, op_w, op_ha, op_hb;
+        std::vector<GemmOp> op_p, op_z, op_w, op_hb;
         std::vector<BdOp> fb, bb;
         for (int j = 0; j < g.count; ++j) {
           Slot& sl = c->slots[g0 + j];
@@ -968,24 +971,27 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
                                 nullptr, 0, nullptr, 0, 0, /*stream_a*/ 1});
           op_w.push_back(GemmOp{true, false, half, Np, nb, H, Kp, DQ + Np, 2 * Np, sl.G + sh.off + half * Np, Np, true,
                                 false, nullptr, 0, nullptr, 0, nullptr, 0, 0, 1});
-          // dH = dZ W_top^T (T, in dC) then Q W_bot^T + T, masked by ReLU'(H) -> dZ_{l-1}
-          op_ha.push_back(GemmOp{false, true, nb, half, Np, DQ, 2 * Np, Wl, Np, sl.dC, Kp, false, false, nullptr, 0,
-                                 nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0});
-          GemmOp hb{false, true, nb, half, Np, DQ + Np, 2 * Np, Wl + half * Np, Np, sl.dZ[l - 1], shp[l - 1].Np, false,
-                    false, nullptr, 0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
-          hb.add = (const bf16*)sl.dC; hb.ldadd = Kp;
+          // dH = [dZ | Q] [W_top | W_bot]^T (one K = 2 Np GEMM), masked by ReLU'(H) -> dZ_{l-1}
+          GemmOp hb{false, true, nb, half, 2 * Np, DQ, 2 * Np, (const bf16*)sl.rWc, 2 * Np, sl.dZ[l - 1],
+                    shp[l - 1].Np, false, false, nullptr, 0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
           hb.mbits_in = sl.mb[l]; hb.ldmbi = c->mb_ld[l];
           op_hb.push_back(hb);
+          g.ra_wc.src[j] = Wl;
+          g.ra_wc.dst[j] = (bf16*)sl.rWc;
+          g.ra_wc.half[j] = (int)half;
+          g.ra_wc.Np = (int)Np;
+          g.ra_wc.max_half = std::max<int>(g.ra_wc.max_half, (int)half);
           g.ra_gemm_fl += 2.0 * nb * Np * half * 6;
           if (bd) g.ra_bd_fl += 2.0 * q * c->bs * c->bs * Np;
         }
         g.ra_fsp.n = g.ra_bsp.n = g.count;
+        g.ra_wc.n = g.count;
         if (bd && (!gemm_bd_prepare(c->blocks, c->c, c->bs, fb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_fbd) ||
                    !gemm_bd_prepare(c->blocks, c->c, c->bs, bb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_bbd)))
           return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: block-diagonal plan failed");
         if (!gemm_bf16_prepare(op_p.data(), g.count, &g.ra_p) || !gemm_bf16_prepare(op_z.data(), g.count, &g.ra_z) ||
             !gemm_bf16_prepare(op_w.data(), 2 * g.count, &g.ra_dw) ||
-            !gemm_bf16_prepare(op_ha.data(), g.count, &g.ra_dha) || !gemm_bf16_prepare(op_hb.data(), g.count, &g.ra_dhb))
+            !gemm_bf16_prepare(op_hb.data(), g.count, &g.ra_dh))
           return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: tcgen05 GEMM plan failed");
         // the loss kernel writes dZ into DQ[:, 0:Np) (and dZ / deg for the block-diagonal path)
         g.ce.ld_dlog = 2 * (int64_t)c->shapes[c->slots[g0].index][l].Np;
@@ -1294,6 +1300,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
     if (g.reassoc && l == L - 1) {  // Z = H W_top + N (H W_bot)
+      LK(relayout_last(g.ra_wc, s));  // [W_top | W_bot] of this step's weights, for dH below
+      ++c->nk;
       tc_l(g.ra_p, g.ra_gemm_fl / 6);
       if (bd) bd_l(g.ra_fbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_fsp, g.ra_fby);
@@ -1318,8 +1326,7 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       if (bd) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_bsp, g.ra_bby);
       tc_l(g.ra_dw, g.ra_gemm_fl / 3);
-      tc_l(g.ra_dha, g.ra_gemm_fl / 6);
-      tc_l(g.ra_dhb, g.ra_gemm_fl / 6);
+      tc_l(g.ra_dh, g.ra_gemm_fl / 3);
       continue;
     }
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);

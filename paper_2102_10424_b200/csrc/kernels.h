@@ -281,6 +281,15 @@ void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1
 void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s);
 // (the optimizer kernels advance the step state themselves: their last CTA increments z, t)
 void step_advance(StepState* st, cudaStream_t s);
+// Re-associated last layer: Wcat[r][c2] = [W_top | W_bot] (half x 2Np, row-major) from the
+// bf16 shadow W = [W_top; W_bot] (2 half x Np), so dH = [dZ | Q] Wcat^T is one K = 2 Np GEMM.
+struct RelayoutGroup {
+  const bf16* src[kMaxGroup];
+  bf16* dst[kMaxGroup];
+  int half[kMaxGroup];
+  int n = 0, Np = 0, max_half = 0;
+};
+void relayout_last(const RelayoutGroup& G, cudaStream_t s);
 void f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
 
 // --------------------------------------------------------------------------

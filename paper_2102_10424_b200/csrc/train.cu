@@ -165,6 +165,22 @@ __global__ void k_step_advance(StepState* st) {
 }
 void step_advance(StepState* st, cudaStream_t s) { launch_pdl(k_step_advance, 1, 1, 0, s, st); }
 
+__global__ void k_relayout_last(const __grid_constant__ RelayoutGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  const int j = blockIdx.y;
+  const int half = G.half[j], Np = G.Np, w2 = 2 * Np;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)half * w2) return;
+  const int r = (int)(idx / w2), c2 = (int)(idx - (int64_t)r * w2);
+  const int srow = c2 < Np ? r : half + r, c = c2 < Np ? c2 : c2 - Np;
+  G.dst[j][idx] = G.src[j][(int64_t)srow * Np + c];
+}
+void relayout_last(const RelayoutGroup& G, cudaStream_t s) {
+  if (G.n <= 0 || G.max_half <= 0) return;
+  launch_pdl(k_relayout_last, dim3((unsigned)cdiv((int64_t)G.max_half * 2 * G.Np, 256), (unsigned)G.n), 256, 0, s, G);
+}
+
 __global__ void k_f32_to_bf16(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
