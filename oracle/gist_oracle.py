@@ -407,6 +407,11 @@ class OracleGIST:
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
+    # Adam state across rounds: "reset" = moments and step counter restart at every
+    # partition (R8, the default); "persistent" = SURVEY §8 f3: the global first
+    # and second moments are shaped like Theta, partitioned / extracted / aggregated with the
+    # weights, and the step counter carries over (the paper is silent)
+    opt_state: str = "reset"
     # state
     theta: list = field(default_factory=list)
     round: int = 0
@@ -432,9 +437,18 @@ class OracleGIST:
 
     def init_params(self, seed: int):
         self.theta = glorot_init(self.arch, self.dims, seed)
+        self.reset_moments()
+
+    def reset_moments(self):
+        """Global Adam moments (zero) and step counter for opt_state == "persistent"."""
+        self.mom = [np.zeros_like(w) for w in self.theta]
+        self.vel = [np.zeros_like(w) for w in self.theta]
+        self.t_global = 0
 
     def set_params(self, theta):
         self.theta = [np.asarray(w, dtype=np.float64).copy() for w in theta]
+        if not hasattr(self, "mom"):
+            self.reset_moments()
 
     # subGCNs (Alg. 1 line "subGCNs"; PAPER.md:111, 147-161)
     def partition(self, seed: int, m: int):
@@ -442,7 +456,11 @@ class OracleGIST:
         self.blocks = sample_partition(self.dims, m, seed, self.round)
         self.index_sets = [sub_index_sets(self.arch, self.dims, self.blocks, i) for i in range(m)]
         self.sub = [extract(self.theta, s) for s in self.index_sets]
-        self.opt = [[{} for _ in self.theta] for _ in range(m)]   # reset per round (R8)
+        if self.opt_state == "persistent":      # f3: slice the global moments like the weights
+            self.opt = [[{"m": mm, "v": vv, "t": self.t_global}
+                         for mm, vv in zip(extract(self.mom, s), extract(self.vel, s))] for s in self.index_sets]
+        else:
+            self.opt = [[{} for _ in self.theta] for _ in range(m)]   # reset per round (R8)
 
     def make_batch(self, slot: int, step: int):
         chosen = batch_schedule(self.num_clusters, self.clusters_per_batch, self.batch_seed, slot, step)
@@ -482,6 +500,10 @@ class OracleGIST:
     # subAgg
     def aggregate(self):
         aggregate(self.theta, self.sub, self.index_sets)
+        if self.opt_state == "persistent" and self.optimizer == "adam":  # f3: moments written back too
+            aggregate(self.mom, [[st["m"] for st in o] for o in self.opt], self.index_sets)
+            aggregate(self.vel, [[st["v"] for st in o] for o in self.opt], self.index_sets)
+            self.t_global = self.opt[0][0].get("t", self.t_global)
         self.round += 1
         self.sub = None
 

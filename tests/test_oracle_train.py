@@ -47,6 +47,60 @@ def test_m1_reduces_to_plain_training(arch, optimizer):
     assert all(np.array_equal(a, b) for a, b in zip(theta, o.theta))
 
 
+@pytest.mark.parametrize("arch", ["gcn", "sage"])
+def test_m1_persistent_adam_reduces_to_plain_adam(arch):
+    """SURVEY §8 f3 (persistent sliced optimizer state): with m = 1 every slice is the whole
+    model, so GIST with persistent Adam state is plain Adam training WITHOUT restarts: the
+    plain loop below keeps one Adam state for the whole run (bit-exact)."""
+    dims, zeta, rounds = (8, 10, 6, 4), 3, 3
+    o, _ = make(arch, dims, "adam")
+    o.opt_state = "persistent"
+    theta = [w.copy() for w in o.theta]
+    for t in range(rounds):
+        o.partition(seed=1, m=1)
+        o.subtrain(zeta, lr=0.05)
+        o.aggregate()
+    p, _ = make(arch, dims, "adam")
+    state = [{} for _ in theta]
+    step = 0
+    for t in range(rounds * zeta):
+        nodes, rp, ci = p.make_batch(0, step)
+        op = p.operator(rp, ci, len(nodes))
+        tape = O.forward(arch, theta, op, p.X[nodes])
+        _, dl = O.softmax_ce(tape["logits"], p.labels[nodes], p.split[nodes] == 0)
+        gr = O.backward(arch, theta, op, tape, dl)
+        for l in range(len(theta)):
+            theta[l] = O.adam_step(theta[l], gr[l], state[l], 0.05)
+        step += 1
+    assert all(np.array_equal(a, b) for a, b in zip(theta, o.theta))
+    assert o.t_global == rounds * zeta
+
+
+def test_persistent_moments_slice_like_the_weights():
+    """f3: after a round with m = 2 the global moments are nonzero exactly on the entries the
+    sub-GCNs own (write-back by replacement), zero elsewhere; the step counter advanced by zeta;
+    and with opt_state = "reset" (default) the second round restarts from t = 0."""
+    dims = (8, 12, 10, 4)
+    o, _ = make("sage", dims, "adam")
+    o.opt_state = "persistent"
+    o.partition(seed=3, m=2)
+    sets = o.index_sets
+    o.subtrain(4, lr=0.01)
+    o.aggregate()
+    assert o.t_global == 4
+    for l in range(3):
+        cov = np.zeros_like(o.theta[l], dtype=bool)
+        for s in sets:
+            cov[np.ix_(*s[l])] = True
+        assert np.all(o.vel[l][~cov] == 0) and np.all(o.mom[l][~cov] == 0)
+        assert np.mean(o.vel[l][cov] > 0) > 0.5      # second moments of trained entries
+    o.partition(seed=4, m=2)
+    assert all(st["t"] == 4 for so in o.opt for st in so)   # counter carried into the new round
+    r, _ = make("sage", dims, "adam")
+    r.partition(seed=3, m=2)
+    assert all(st == {} for so in r.opt for st in so)        # default: reset per round (R8)
+
+
 def test_only_covered_entries_change_after_a_round():
     dims = (8, 12, 10, 4)
     o, _ = make("gcn", dims, "adam")
