@@ -58,6 +58,13 @@ enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1 };      /* Eq. (1)
 enum { GIST_OPT_SGD = 0, GIST_OPT_ADAM = 1 };        /* subTrain = SGD step PAPER.md:168; Adam PAPER.md:660,680,690 */
 enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1 };     /* FP32 parity mode / BF16 tensor-core mode (R13) */
 enum { GIST_GRAPH_DEVICE = 0, GIST_GRAPH_HOST = 1 }; /* graph resident in HBM / in pinned host memory (streamed per step) */
+/* Adam state across rounds: RESET = moments and step counter restart at every gist_partition
+ * (R8; the default).  PERSISTENT = SURVEY.md §8 f3: global first / second moments
+ * shaped like Theta are partitioned, extracted and aggregated with the weights (and
+ * all-gathered with them when world_size > 1: 3x subAgg bytes), the step counter carries
+ * over; GIST with m = 1 is then plain Adam training without restarts (the paper is silent,
+ * PAPER.md:660).  Ignored for SGD. */
+enum { GIST_OPT_STATE_RESET = 0, GIST_OPT_STATE_PERSISTENT = 1 };
 
 typedef struct {
   int32_t arch;               /* GIST_ARCH_* */
@@ -73,6 +80,7 @@ typedef struct {
   int32_t device;             /* CUDA device ordinal */
   const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0 when world_size > 1, else NULL */
   void* stream;               /* optional cudaStream_t to order work on; NULL = library-owned */
+  int32_t opt_state;          /* GIST_OPT_STATE_* (default RESET) */
 } gist_config;
 
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */

@@ -21,6 +21,9 @@
 
 using namespace gist;
 
+struct gist_ctx;
+static bool persistent_adam(const gist_ctx* c);
+
 bool gist::pdl_enabled() {
   static const bool on = [] { const char* e = std::getenv("GIST_PDL"); return !(e && e[0] == '0'); }();
   return on;
@@ -147,6 +150,7 @@ struct gist_ctx {
   std::vector<Slot> slots;                     // local slots
   float* Wall = nullptr;                       // slots_per_rank * S_max (local slot weights, contiguous)
   float *Gall = nullptr, *Mall = nullptr, *Vall = nullptr;  // same packing: gradients, Adam moments
+  std::vector<float*> theta_m, theta_v;  // GIST_OPT_STATE_PERSISTENT: global Adam moments (Theta layout)
   bf16* Wball = nullptr;                       // bf16 shadow of Wall (BF16 mode)
   int nb_max_rows = 0;                         // static row count of every batch launch
   std::vector<int64_t> mb_ld;                  // words per row of Slot::mb[l]
@@ -346,6 +350,10 @@ void epoch_perm(const gist_ctx* c, int slot, int64_t e, std::vector<int32_t>& ou
 }  // namespace
 
 // ============================================================ lifecycle ====
+static bool persistent_adam(const gist_ctx* c) {
+  return c->cfg.optimizer == GIST_OPT_ADAM && c->cfg.opt_state == GIST_OPT_STATE_PERSISTENT;
+}
+
 extern "C" void gist_config_default(gist_config* cfg) {
   std::memset(cfg, 0, sizeof(*cfg));
   cfg->arch = GIST_ARCH_GCN;
@@ -395,6 +403,7 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (cfg->arch != GIST_ARCH_GCN && cfg->arch != GIST_ARCH_SAGE) return GIST_E_ARG;
   if (cfg->optimizer != GIST_OPT_SGD && cfg->optimizer != GIST_OPT_ADAM) return GIST_E_ARG;
   if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
+  if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
   if (cfg->clusters_per_batch < 1 || cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
     return GIST_E_ARG;
   for (int l = 0; l <= cfg->num_layers; ++l)
@@ -684,6 +693,12 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
     c->th_N[l] = pad8(c->dims[l + 1]);
     TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
     CK(cudaMemsetAsync(c->theta[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, s));
+    if (persistent_adam(c)) {  // f3: global moments, same physical layout as Theta
+      c->theta_m.resize(c->L, nullptr);
+      c->theta_v.resize(c->L, nullptr);
+      TRY(dalloc_t(c, &c->theta_m[l], (size_t)c->th_K[l] * c->th_N[l]));
+      TRY(dalloc_t(c, &c->theta_v[l], (size_t)c->th_K[l] * c->th_N[l]));
+    }
   }
   c->state = S_GRAPH;
   return GIST_OK;
@@ -693,6 +708,11 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
 extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
   PRE(c);
   if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "init_params: bad state");
+  for (int l = 0; l < (int)c->theta_m.size(); ++l) {  // f3: moments restart with the parameters
+    CK(cudaMemsetAsync(c->theta_m[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, c->stream));
+    CK(cudaMemsetAsync(c->theta_v[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, c->stream));
+  }
+  c->adam_t = 0;
   for (int l = 0; l < c->L; ++l) {
     const int rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[l] : c->dims[l];
     const int cols = c->dims[l + 1];
@@ -1207,10 +1227,14 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
       mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
       mp.ldg = c->th_N[l];
       PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta[l], mp, sl.W + sh.off, s));
+      if (persistent_adam(c)) {  // f3: slice the global moments exactly like the weights
+        PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta_m[l], mp, sl.M + sh.off, s));
+        PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta_v[l], mp, sl.V + sh.off, s));
+      }
     }
   }
   const int64_t tot_local = (int64_t)c->slots.size() * c->S_max;
-  if (c->Mall && tot_local > 0) {
+  if (c->Mall && tot_local > 0 && !persistent_adam(c)) {  // R8: reset per round
     CK(cudaMemsetAsync(c->Mall, 0, (size_t)tot_local * 4, s));
     CK(cudaMemsetAsync(c->Vall, 0, (size_t)tot_local * 4, s));
   }
@@ -1219,7 +1243,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
   else TRY(build_plan<float>(c, c->plan_f));
   c->prof_now = false;
   TRY(check_launch(c, "partition"));
-  c->adam_t = 0;
+  if (!persistent_adam(c)) c->adam_t = 0;  // R8 (f3: the counter carries over)
   c->state = S_PARTITIONED;
   return GIST_OK;
 }
@@ -1476,25 +1500,32 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "aggregate: no open round");
   cudaStream_t s = c->stream;
   const int W = c->cfg.world_size;
-  const float* src = c->Wall;
   c->prof_now = c->prof_stride > 0;
-  if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
-    const int id = prof_begin(c, s, GIST_PROF_AGGREGATE, (double)W * c->slots_per_rank * c->S_max * 4.0);
-    NK(ncclAllGather(c->Wall, c->Wrecv, (size_t)c->slots_per_rank * c->S_max, ncclFloat, c->comm, s));
-    prof_end(c, s, id);
-    src = c->Wrecv;
-  }
-  for (int i = 0; i < c->m; ++i) {
-    const int rank = gist_slot_owner(i, W), j = i / W;
-    const float* w = src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
-    if (W == 1) w = c->Wall + (size_t)j * c->S_max;
-    for (int l = 0; l < c->L; ++l) {
-      const LayerShape& sh = c->shapes[i][l];
-      LayerMap mp;
-      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
-      mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
-      mp.ldg = c->th_N[l];
-      PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 12.0, s, scatter_sub(c->theta[l], mp, w + sh.off, s));
+  // the weights, and with persistent Adam state (f3) the two moments, travel the same way
+  struct Part { float* local; std::vector<float*>* global; };
+  std::vector<float*> wvec(c->theta.begin(), c->theta.end());
+  std::vector<Part> parts = {{c->Wall, &wvec}};
+  if (persistent_adam(c)) parts.push_back({c->Mall, &c->theta_m}), parts.push_back({c->Vall, &c->theta_v});
+  for (const Part& pt : parts) {
+    const float* src = pt.local;
+    if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
+      const int id = prof_begin(c, s, GIST_PROF_AGGREGATE, (double)W * c->slots_per_rank * c->S_max * 4.0);
+      NK(ncclAllGather(pt.local, c->Wrecv, (size_t)c->slots_per_rank * c->S_max, ncclFloat, c->comm, s));
+      prof_end(c, s, id);
+      src = c->Wrecv;
+    }
+    for (int i = 0; i < c->m; ++i) {
+      const int rank = gist_slot_owner(i, W), j = i / W;
+      const float* w = src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
+      if (W == 1) w = pt.local + (size_t)j * c->S_max;
+      for (int l = 0; l < c->L; ++l) {
+        const LayerShape& sh = c->shapes[i][l];
+        LayerMap mp;
+        mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
+        mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
+        mp.ldg = c->th_N[l];
+        PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 12.0, s, scatter_sub((*pt.global)[l], mp, w + sh.off, s));
+      }
     }
   }
   c->prof_now = false;

@@ -32,6 +32,9 @@ EXPORTS = [
 PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc"]
 
 
+GIST_OPT_STATE_RESET, GIST_OPT_STATE_PERSISTENT = 0, 1
+
+
 class GistConfig(C.Structure):
     _fields_ = [
         ("arch", C.c_int32), ("num_layers", C.c_int32), ("dims", C.POINTER(C.c_int32)),
@@ -39,6 +42,7 @@ class GistConfig(C.Structure):
         ("precision", C.c_int32), ("clusters_per_batch", C.c_int32), ("batch_seed", C.c_uint64),
         ("graph_residency", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("device", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
+        ("opt_state", C.c_int32),
     ]
 
 
@@ -105,7 +109,7 @@ class Gist:
     def __init__(self, arch: str, dims, optimizer: str = "adam", precision: str = "fp32",
                  clusters_per_batch: int = 1, batch_seed: int = 0, rank: int = 0, world_size: int = 1,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream: int | None = None,
-                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8):
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset"):
         L = lib()
         self.arch = arch
         self.dims = [int(d) for d in dims]
@@ -126,6 +130,7 @@ class Gist:
             self._uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         cfg.stream = stream
+        cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
         self._cfg = cfg
         h = C.c_void_p()
         self._check(L.gist_create(C.byref(cfg), C.byref(h)), None)

@@ -31,9 +31,10 @@ def free_port():
     return p
 
 
-def make():
+def make(opt_state="reset"):
     g = generate(tiny_spec(n=240, nnz=1500, d0=12, classes=4, clusters=8), seed=3)
-    o = O.OracleGIST(arch="sage", dims=list(DIMS), optimizer="adam", clusters_per_batch=2, batch_seed=9)
+    o = O.OracleGIST(arch="sage", dims=list(DIMS), optimizer="adam", clusters_per_batch=2, batch_seed=9,
+                     opt_state=opt_state)
     o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
                  g["cluster_ids"], g["num_clusters"])
     o.init_params(5)
@@ -57,9 +58,9 @@ def unpack(flat, shapes):
     return out
 
 
-def sharded_run(rank, world):
+def sharded_run(rank, world, opt_state="reset"):
     from paper_2102_10424_b200 import gist
-    o = make()
+    o = make(opt_state)
     spr = gist.slots_per_rank(M, world)
     mine = gist.local_slots(M, world, rank)
     history = []
@@ -71,39 +72,53 @@ def sharded_run(rank, world):
             for z in range(ZETA):
                 o.train_step(i, o.step + z, 0.01)
         o.step += ZETA
-        send = torch.from_numpy(pack(o.sub, mine, spr, smax))
-        recv = [torch.zeros_like(send) for _ in range(world)]
-        dist.all_gather(recv, send)                   # the one exchange of the round
-        for r in range(world):
-            for j in range(spr):
-                i = r + world * j
-                if i >= M:
-                    continue
-                assert gist.slot_owner(i, world) == r
-                o.sub[i] = unpack(recv[r].numpy()[j * smax:(j + 1) * smax], shapes[i])
+        # the one exchange of the round: the packed slot weights (and, with persistent Adam
+        # state, the two moment slices the same way)
+        tensors = [("w", o.sub)]
+        if opt_state == "persistent":
+            tensors += [(k, [[st[k] for st in so] for so in o.opt]) for k in ("m", "v")]
+        for name, blocks in tensors:
+            send = torch.from_numpy(pack(blocks, mine, spr, smax))
+            recv = [torch.zeros_like(send) for _ in range(world)]
+            dist.all_gather(recv, send)
+            for r in range(world):
+                for j in range(spr):
+                    i = r + world * j
+                    if i >= M:
+                        continue
+                    assert gist.slot_owner(i, world) == r
+                    got = unpack(recv[r].numpy()[j * smax:(j + 1) * smax], shapes[i])
+                    if name == "w":
+                        o.sub[i] = got
+                    else:
+                        for l in range(len(got)):
+                            o.opt[i][l][name] = got[l]
+                            o.opt[i][l]["t"] = o.t_global + ZETA   # every slot took ZETA steps
         o.aggregate()
-        history.append([w.copy() for w in o.theta])
+        history.append([w.copy() for w in o.theta] +
+                       ([m.copy() for m in o.mom] + [v.copy() for v in o.vel] if opt_state == "persistent" else []))
     return history
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, opt_state="reset"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        hist = sharded_run(rank, world)
+        hist = sharded_run(rank, world, opt_state)
         q.put((rank, [[w.tobytes() for w in th] for th in hist]))
     finally:
         dist.destroy_process_group()
 
 
-def reference():
-    o = make()
+def reference(opt_state="reset"):
+    o = make(opt_state)
     hist = []
     for t in range(ROUNDS):
         o.partition(seed=77, m=M)
         o.subtrain(ZETA, 0.01)
         o.aggregate()
-        hist.append([w.copy() for w in o.theta])
+        hist.append([w.copy() for w in o.theta] +
+                    ([m.copy() for m in o.mom] + [v.copy() for v in o.vel] if opt_state == "persistent" else []))
     return hist
 
 
@@ -118,19 +133,21 @@ def test_layout_functions():
 
 
 @pytest.mark.timeout(300)
-def test_world2_gloo_bit_identical_to_world1():
+@pytest.mark.parametrize("opt_state", ["reset", "persistent"])
+def test_world2_gloo_bit_identical_to_world1(opt_state):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, opt_state)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ref = reference()
+    ref = reference(opt_state)
     for t in range(ROUNDS):
-        for l in range(len(DIMS) - 1):
+        assert len(ref[t]) == len(res[0][t]) == (len(DIMS) - 1) * (3 if opt_state == "persistent" else 1)
+        for l in range(len(ref[t])):        # weights (and global moments) per layer
             want = ref[t][l].tobytes()
             assert res[0][t][l] == want and res[1][t][l] == want, (t, l)

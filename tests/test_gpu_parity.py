@@ -235,3 +235,35 @@ def test_kernel_gemm_bf16_tcgen05_shapes(ta, tb, M, N, K, out_f32):
     got = c.float().cpu().numpy().astype(np.float64)
     err = np.abs(got - ref) / (np.abs(ref) + np.sqrt(K))  # |ref| ~ sqrt(K) for unit normal operands
     assert err.max() <= (1e-5 if out_f32 else 2.0 ** -8), err.max()
+
+
+@pytest.mark.parametrize("arch,dims,m", [("sage", (23, 40, 33, 7), 2), ("gcn", (37, 45, 29, 5), 3),
+                                         ("sage", (23, 40, 33, 7), 1)])
+def test_persistent_adam_state_rounds(arch, dims, m):
+    """persistent sliced Adam state (GIST_OPT_STATE_PERSISTENT) against the
+    oracle's persistent mode over 3 rounds (FP32).  After the first step the moments are no
+    longer sign-like, so the weights stay within 1e-3 across rounds; m = 1
+    is plain Adam without restarts."""
+    kw = CASES[1][1] if arch == "sage" else CASES[0][1]
+    q = CASES[1][4] if arch == "sage" else CASES[0][4]
+    g = graph(kw, seed=2)
+    from paper_2102_10424_b200.gist import Gist
+    gpu = Gist(arch, dims, optimizer="adam", precision="fp32", clusters_per_batch=q, batch_seed=3,
+               opt_state="persistent")
+    gpu.load_graph(g)
+    gpu.init_params(7)
+    ora = O.OracleGIST(arch=arch, dims=list(dims), optimizer="adam", clusters_per_batch=q, batch_seed=3,
+                       opt_state="persistent")
+    ora.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
+                   g["cluster_ids"], g["num_clusters"])
+    ora.init_params(7)
+    for t in range(3):
+        gpu.partition(seed=21, m=m)
+        ora.partition(seed=21, m=m)
+        lg = gpu.subtrain(4, lr=0.002)
+        lo = ora.subtrain(4, lr=0.002)
+        assert np.max(np.abs(lg - lo)) <= 1e-4 * max(1.0, np.max(np.abs(lo))), (t, lg, lo)
+        gpu.aggregate()
+        ora.aggregate()
+        for l in range(len(dims) - 1):
+            assert rel_err(gpu.get_params(l), ora.theta[l]) <= GRAD_TOL, (t, l)
