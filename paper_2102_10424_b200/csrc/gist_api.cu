@@ -95,6 +95,7 @@ struct StepPlan {
     RelayoutGroup ra_wc;
     BdPlan ra_fbd, ra_bbd;
     SpmmGroup<T, T> ra_fsp, ra_bsp;
+    SpmmGroup<T, float> ra_fsp_f;  // GCN: logits = A_hat P straight into the fp32 logits
     double ra_gemm_fl = 0.0, ra_bd_fl = 0.0, ra_fby = 0.0, ra_bby = 0.0;
   };
   std::vector<Group> groups;
@@ -846,7 +847,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
       CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
     }
-    c->reassoc = c->arch == GIST_ARCH_SAGE && c->prec == GIST_PREC_BF16 && c->L >= 2;
+    c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2;
     if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->reassoc && e[0] != '0';
     if (c->reassoc) {
       const size_t npl = (size_t)maxN[c->L - 1];
@@ -938,10 +939,55 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.ce.rows = nb;
     g.ce.k = c->k;
     g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
-    g.reassoc = c->reassoc && tc && sage && L >= 2;
+    g.reassoc = c->reassoc && tc && L >= 2;
     for (int l = 0; l < L; ++l) {
       std::vector<GemmOp> fw, dw, dx;
       std::vector<BdOp> bfw, bbw;
+      if (g.reassoc && l == L - 1 && !sage) {
+        // Re-associated last GCN layer (Eq. (1): Z = A_hat (H W), width Np instead of
+        // the hidden width; A_hat symmetric): forward P = H W, logits = A_hat P; backward
+        // Q = A_hat dZ, dW = H^T Q, dH = Q W^T * ReLU'(H).
+        std::vector<GemmOp> op_p, op_w, op_h;
+        for (int j = 0; j < g.count; ++j) {
+          Slot& sl = c->slots[g0 + j];
+          const auto& shp = c->shapes[sl.index];
+          const LayerShape& sh = shp[l];
+          const int64_t Np = sh.Np, Kp = sh.Kp;
+          const bf16* Wl = sl.Wb + sh.off;
+          const bf16* H = (const bf16*)sl.H[l];
+          bf16 *P = (bf16*)sl.rP, *DQ = (bf16*)sl.rDQ;
+          op_p.push_back(GemmOp{false, false, nb, Np, Kp, H, Kp, Wl, Np, P, Np, false, false, nullptr, 0, nullptr, 0,
+                                nullptr, 0, /*keep_out*/ 1, 0});
+          SpmmArgs<T, float>& a = g.ra_fsp_f.a[j];
+          a = SpmmArgs<T, float>();
+          a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
+          a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
+          a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;
+          a.H = (const T*)P; a.ldh = Np; a.w = Np; a.out = sl.logits; a.ldo = Np;
+          SpmmArgs<T, T>& b = g.ra_bsp.a[j];
+          b = SpmmArgs<T, T>();
+          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
+          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
+          b.rowscale = sl.scale; b.colscale = sl.scale; b.self = 1;
+          b.H = (const T*)DQ; b.ldh = 2 * Np; b.w = Np; b.out = (T*)(DQ + Np); b.ldo = 2 * Np;
+          g.ra_fby += (double)nb * Np * 6.0 + nb * 16.0;
+          g.ra_bby += spmm_bytes(b);
+          op_w.push_back(GemmOp{true, false, Kp, Np, nb, H, Kp, DQ + Np, 2 * Np, sl.G + sh.off, Np, true, false, nullptr,
+                                0, nullptr, 0, nullptr, 0, 0, /*stream_a*/ 1});
+          GemmOp h{false, true, nb, Kp, Np, DQ + Np, 2 * Np, Wl, Np, sl.dZ[l - 1], shp[l - 1].Np, false, false, nullptr,
+                   0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
+          h.mbits_in = sl.mb[l]; h.ldmbi = c->mb_ld[l];
+          op_h.push_back(h);
+          g.ra_gemm_fl += 2.0 * nb * Np * Kp * 3;
+        }
+        g.ra_fsp_f.n = g.ra_bsp.n = g.count;
+        if (!gemm_bf16_prepare(op_p.data(), g.count, &g.ra_p) || !gemm_bf16_prepare(op_w.data(), g.count, &g.ra_dw) ||
+            !gemm_bf16_prepare(op_h.data(), g.count, &g.ra_dh))
+          return fail(c, GIST_E_UNSUPPORTED, "re-associated GCN layer: tcgen05 GEMM plan failed");
+        g.ce.ld_dlog = 2 * (int64_t)c->shapes[c->slots[g0].index][l].Np;
+        for (int j = 0; j < g.count; ++j) g.ce.s[j].dlog = (T*)c->slots[g0 + j].rDQ;
+        continue;
+      }
       if (g.reassoc && l == L - 1) {
         // Re-associated last GraphSAGE layer (exact algebra of Eq. (2), with the
         // class width far below the hidden width): Z = H W_top + N (H W_bot), so the
@@ -1323,6 +1369,14 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   };
   // ---- a2/a3: forward
   for (int l = 0; l < L; ++l) {
+    if (g.reassoc && l == L - 1 && c->arch != GIST_ARCH_SAGE) {  // GCN: logits = A_hat (H W)
+      tc_l(g.ra_p, g.ra_gemm_fl / 3);
+      const int id = prof_begin(c, s, GIST_PROF_SPMM, g.ra_fby, per_nnz, nnz_slot);
+      spmm_group<T, float>(g.ra_fsp_f, s);
+      prof_end(c, s, id);
+      ++c->nk;
+      continue;
+    }
     if (g.reassoc && l == L - 1) {  // Z = H W_top + N (H W_bot)
       LK(relayout_last(g.ra_wc, s));  // [W_top | W_bot] of this step's weights, for dH below
       ++c->nk;
@@ -1346,6 +1400,12 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   }
   // ---- a5/a6: backward
   for (int l = L - 1; l >= 0; --l) {
+    if (g.reassoc && l == L - 1 && c->arch != GIST_ARCH_SAGE) {  // GCN: Q = A_hat dZ; dW = H^T Q; dH = Q W^T
+      spmm_l(g.ra_bsp, g.ra_bby);
+      tc_l(g.ra_dw, g.ra_gemm_fl / 3);
+      tc_l(g.ra_dh, g.ra_gemm_fl / 3);
+      continue;
+    }
     if (g.reassoc && l == L - 1) {  // Q = N^T dZ; dW = [H^T dZ; H^T Q]; dZ_{l-1} = (dZ W_top^T + Q W_bot^T) * ReLU'
       if (bd) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_bsp, g.ra_bby);

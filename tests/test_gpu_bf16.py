@@ -88,6 +88,14 @@ def test_bf16_one_step_sage_aggregation_variants(name, kw, arch, dims, q, bd, re
     test_bf16_one_step(name, kw, arch, dims, q)
 
 
+def test_bf16_one_step_gcn_paper_order(monkeypatch):
+    """GCN BF16 with the paper's association order for the last layer (GIST_REASSOC=0);
+    the default re-associated form A_hat (H W) is covered by test_bf16_one_step."""
+    monkeypatch.setenv("GIST_REASSOC", "0")
+    name, kw, arch, dims, q = CASES[0]
+    test_bf16_one_step(name, kw, arch, dims, q)
+
+
 @pytest.mark.parametrize("optimizer,lr", [("sgd", 0.1), ("adam", 0.001)])  # well-conditioned trajectories (DESIGN.md)
 def test_bf16_loss_curve_C1_10_rounds(optimizer, lr):
     """north_star: BF16 mode loss curve within 1% after 10 rounds (C1 = Cora-shaped, m=2,
