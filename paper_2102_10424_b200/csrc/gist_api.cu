@@ -847,8 +847,12 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
       CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
     }
-    c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2;
-    if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->reassoc && e[0] != '0';
+    // (only where it pays: the last layer's input slice is >= 256 wide; measured neutral to
+    // slightly negative on the Cora-shaped C1 with a 128-wide slice)
+    // GIST_REASSOC=1 / 0 forces it on / off (tests exercise both on small shapes)
+    const int last_in = c->arch == GIST_ARCH_SAGE ? maxK[c->L - 1] / 2 : maxK[c->L - 1];
+    c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && last_in >= 256;
+    if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && e[0] == '1';
     if (c->reassoc) {
       const size_t npl = (size_t)maxN[c->L - 1];
       TRY(dalloc(c, &s.rP, (size_t)nbm * npl * E));

@@ -77,21 +77,22 @@ def test_bf16_one_step(name, kw, arch, dims, q):
             assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= BF16_TOL, l
 
 
-@pytest.mark.parametrize("bd,reassoc", [("0", "1"), ("1", "0"), ("0", "0")])
+@pytest.mark.parametrize("bd,reassoc", [("1", "1"), ("0", "1"), ("1", "0"), ("0", "0")])
 @pytest.mark.parametrize("name,kw,arch,dims,q", [c for c in CASES if c[2] == "sage"])
 def test_bf16_one_step_sage_aggregation_variants(name, kw, arch, dims, q, bd, reassoc, monkeypatch):
     """GraphSAGE BF16 with and without the block-diagonal tensor-core aggregation (GIST_BD) and
-    with and without the re-associated last layer (GIST_REASSOC: Z = H W_top + N (H W_bot),
-    Q = N^T dZ at the class width); the default (both on) is covered above."""
+    with the re-associated last layer forced on / off (GIST_REASSOC: Z = H W_top + N (H W_bot),
+    Q = N^T dZ at the class width, R19; by default only for slices >= 256 wide)."""
     monkeypatch.setenv("GIST_BD", bd)
     monkeypatch.setenv("GIST_REASSOC", reassoc)
     test_bf16_one_step(name, kw, arch, dims, q)
 
 
-def test_bf16_one_step_gcn_paper_order(monkeypatch):
-    """GCN BF16 with the paper's association order for the last layer (GIST_REASSOC=0);
-    the default re-associated form A_hat (H W) is covered by test_bf16_one_step."""
-    monkeypatch.setenv("GIST_REASSOC", "0")
+def test_bf16_one_step_gcn_reassociated(monkeypatch):
+    """GCN BF16 with the re-associated last layer forced on (GIST_REASSOC=1; by default it
+    is used only when the layer's input slice is >= 256 wide): logits = A_hat (H W),
+    Q = A_hat dZ, dW = H^T Q, dH = Q W^T."""
+    monkeypatch.setenv("GIST_REASSOC", "1")
     name, kw, arch, dims, q = CASES[0]
     test_bf16_one_step(name, kw, arch, dims, q)
 
