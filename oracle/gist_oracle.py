@@ -4,7 +4,7 @@ Plain, slow, obviously-correct CPU implementation of the GIST training loop
 (Algorithm 1) restricted to the hot path named by
 BASELINE.json's north_star: subGCNs (partition + extract), subTrain (Cluster
 mini-batch, GCN / GraphSAGE forward + backward, softmax-CE, Adam/SGD) and
-subAgg (replacement write-back), plus full-graph evaluation.
+subAgg (replacement write-back), plus full-graph and partition-wise (R20) evaluation.
 
 Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
 `--impl reference`) may import this module.  It shares no code with the CUDA
@@ -515,3 +515,33 @@ class OracleGIST:
         loss, _ = softmax_ce(logits, self.labels, rows)
         acc = float(np.mean(np.argmax(logits[rows], axis=1) == self.labels[rows])) if rows.any() else 0.0
         return loss, acc, logits
+
+    def eval_partitions(self, split_code: int, part_ids, num_parts: int, parts=None):
+        """Partition-wise evaluation (PAPER.md:696-697, Appendix "Training Ultra-Wide GCNs";
+        reading R20): the graph is cut into `num_parts` partitions (part_ids[v] in
+        [0, num_parts)); every partition is evaluated on its own induced subgraph with the
+        training batch operator (R1/R2 on that subgraph, R10 no output scaling), and the
+        score measured on each partition is averaged over the partitions that hold at least
+        one node with split == split_code.  Single-label F1 (micro) = accuracy.
+        `parts`: evaluate only these partition ids (the means then cover only them).
+        Returns (mean loss, mean acc, per-partition loss, per-partition acc; NaN = no
+        evaluated node)."""
+        part = np.asarray(part_ids, dtype=np.int64)
+        assert part.shape == (self.n,) and (num_parts == 0 or (part.min() >= 0 and part.max() < num_parts))
+        loss_p = np.full(num_parts, np.nan)
+        acc_p = np.full(num_parts, np.nan)
+        for p in (range(num_parts) if parts is None else parts):
+            nodes = np.nonzero(part == p)[0]              # ascending global id
+            rows = self.split[nodes] == split_code
+            if not rows.any():
+                continue
+            rp, ci = induced_subgraph(self.row_ptr, self.col_idx, nodes)
+            op = self.operator(rp, ci, len(nodes))
+            logits = forward(self.arch, self.theta, op, self.X[nodes])["logits"]
+            y = self.labels[nodes]
+            loss_p[p], _ = softmax_ce(logits, y, rows)
+            acc_p[p] = float(np.mean(np.argmax(logits[rows], axis=1) == y[rows]))
+        ok = ~np.isnan(acc_p)
+        if not ok.any():
+            return 0.0, 0.0, loss_p, acc_p
+        return float(np.mean(loss_p[ok])), float(np.mean(acc_p[ok])), loss_p, acc_p
