@@ -137,6 +137,25 @@ gist_status gist_aggregate(gist_ctx* ctx);
  * split == split_code.  Either output may be NULL. */
 gist_status gist_eval(gist_ctx* ctx, int32_t split_code, float* loss, float* acc);
 
+/* Partition-wise evaluation of the global model ("for d_i > 4096
+ * evaluation must be performed on graph partitions ... F1 score is measured over each
+ * partition and averaged"; reading R20).  Every partition is evaluated on its own induced
+ * subgraph (cut edges dropped, R1/R2 normalisation inside the partition, R10 no output
+ * scaling); its score is the mean CE / accuracy (= single-label micro-F1) over its nodes with
+ * split == split_code, and *loss / *acc are the unweighted means over the partitions holding
+ * at least one such node (0 if none).
+ *   part_ids   host int32[n], ORIGINAL node ids -> partition in [0, num_parts); NULL = the
+ *              training clusters of gist_load_graph (num_parts must then be 0 or their count).
+ *   max_rows   rows per evaluation chunk (whole partitions per chunk; a partition larger
+ *              than max_rows forms its own chunk); <= 0 = sized from free device memory.
+ *   part_loss, part_acc  optional host float[num_parts]; NaN for partitions without
+ *              evaluated nodes.  Any output may be NULL.
+ * World > 1: collective; partition p is evaluated by rank p mod world_size and the
+ * per-partition sums are combined with one ncclAllReduce; every rank gets all outputs.
+ * Errors: GIST_E_STATE (open round / no params), GIST_E_ARG (bad split code or ids). */
+gist_status gist_eval_parts(gist_ctx* ctx, int32_t split_code, const int32_t* part_ids, int32_t num_parts,
+                            int64_t max_rows, float* loss, float* acc, float* part_loss, float* part_acc);
+
 /* ---------------- inspection / parity hooks ---------------- */
 /* Global Theta_l, logical row-major: rows = d_l (GCN) or 2*d_l (SAGE: self rows then
  * neighbour rows), cols = d_{l+1}.  out / in: float[rows*cols]. */

@@ -1682,6 +1682,203 @@ extern "C" gist_status gist_eval(gist_ctx* c, int32_t split_code, float* loss, f
   return eval_t<float>(c, split_code, loss, acc);
 }
 
+// ==================================================== partition-wise eval (R20) ===
+// for wide models the global model is evaluated partition by partition.
+// Every partition is a closed subgraph (cut edges dropped), so the local partitions of this
+// rank are laid out contiguously (partition order) and processed in row chunks of whole
+// partitions: per layer one SpMM over the chunk's partition-induced CSR (layer 0 reads X
+// through a row index, no copy) and one GEMM, all buffers chunk-sized.  World > 1:
+// partition p is evaluated by rank p mod W and the per-partition sums are all-reduced.
+template <typename T>
+static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t>& part, int np, int64_t max_rows,
+                                std::vector<double>& sums) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->n;
+  const bool sage = c->arch == GIST_ARCH_SAGE;
+  const int W = c->cfg.world_size, rank = c->cfg.rank;
+  // local partitions (p mod W == rank) in partition order, nodes ascending (internal ids)
+  std::vector<int64_t> cnt(np + 1, 0);
+  for (int64_t g = 0; g < n; ++g) ++cnt[part[g] + 1];
+  std::vector<int32_t> lparts;
+  for (int p = rank; p < np; p += W) lparts.push_back(p);
+  const int nlp = (int)lparts.size();
+  std::vector<int64_t> lbeg(nlp + 1, 0);
+  std::vector<int64_t> fill(np, -1);
+  for (int j = 0; j < nlp; ++j) {
+    fill[lparts[j]] = lbeg[j];
+    lbeg[j + 1] = lbeg[j] + cnt[lparts[j] + 1];
+  }
+  const int64_t nl = lbeg[nlp];
+  std::vector<int32_t> pnode(std::max<int64_t>(nl, 1)), pos(n, -1), rowbase(std::max<int64_t>(nl, 1));
+  for (int64_t g = 0; g < n; ++g) {
+    const int p = part[g];
+    if (fill[p] < 0) continue;
+    pos[g] = (int32_t)fill[p];
+    pnode[fill[p]++] = (int32_t)g;
+  }
+  // buffers and chunking
+  int64_t maxK = 0;
+  for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
+  const int64_t Nl = c->th_N[c->L - 1];
+  std::vector<void*> wl(c->L, nullptr);
+  if (sizeof(T) == 2)
+    for (int l = 0; l < c->L; ++l) {
+      TRY(dalloc(c, &wl[l], (size_t)c->th_K[l] * c->th_N[l] * 2));
+      LK(f32_to_bf16(c->theta[l], (bf16*)wl[l], c->th_K[l] * c->th_N[l], s));
+    }
+  const int64_t row_bytes = 2 * maxK * (int64_t)sizeof(T) + Nl * 4;
+  if (max_rows <= 0) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    max_rows = std::max<int64_t>(1, (int64_t)(fr / 2) / row_bytes);
+  }
+  std::vector<int> chunk_first{0};  // chunk j = local partitions chunk_first[j] .. chunk_first[j+1]
+  for (int j = 0; j < nlp; ++j) {
+    const int f = chunk_first.back();
+    if (j > f && lbeg[j + 1] - lbeg[f] > max_rows) chunk_first.push_back(j);
+  }
+  chunk_first.push_back(nlp);
+  int64_t max_chunk = 0;
+  for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
+    const int64_t k0 = lbeg[chunk_first[j]], k1 = lbeg[chunk_first[j + 1]];
+    max_chunk = std::max(max_chunk, k1 - k0);
+    for (int64_t r = k0; r < k1; ++r) rowbase[r] = (int32_t)k0;
+  }
+  // partition-induced CSR (device)
+  int32_t *pnode_d = nullptr, *pos_d = nullptr, *part_d = nullptr, *rb_d = nullptr, *pcol = nullptr;
+  int64_t *deg = nullptr, *prp = nullptr, *lbeg_d = nullptr;
+  float* pscale = nullptr;
+  double* out3 = nullptr;
+  TRY(dalloc_t(c, &pnode_d, std::max<int64_t>(nl, 1)));
+  TRY(dalloc_t(c, &pos_d, n));
+  TRY(dalloc_t(c, &part_d, n));
+  TRY(dalloc_t(c, &rb_d, std::max<int64_t>(nl, 1)));
+  TRY(dalloc_t(c, &deg, nl + 1));
+  TRY(dalloc_t(c, &prp, nl + 1));
+  TRY(dalloc_t(c, &lbeg_d, nlp + 1));
+  TRY(dalloc_t(c, &pscale, std::max<int64_t>(nl, 1)));
+  TRY(dalloc_t(c, &out3, 3 * (size_t)std::max(nlp, 1)));
+  CK(cudaMemcpyAsync(pnode_d, pnode.data(), nl * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(pos_d, pos.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(part_d, part.data(), n * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(rb_d, rowbase.data(), nl * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(lbeg_d, lbeg.data(), (nlp + 1) * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(deg, 0, (nl + 1) * 8, s));
+  LK(part_count(c->rp, c->col, pnode_d, part_d, nl, deg, s));
+  {
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, prp, nl + 1, s);
+    void* tmp = nullptr;
+    TRY(dalloc(c, &tmp, tb));
+    cub::DeviceScan::ExclusiveSum(tmp, tb, deg, prp, nl + 1, s);
+    ++c->nk;
+    CK(cudaStreamSynchronize(s));
+    dfree(c, tmp);
+  }
+  int64_t pnnz = 0;
+  CK(cudaMemcpy(&pnnz, prp + nl, 8, cudaMemcpyDeviceToHost));
+  TRY(dalloc_t(c, &pcol, std::max<int64_t>(pnnz, 1)));
+  LK(part_fill(c->rp, c->col, pnode_d, pos_d, part_d, rb_d, prp, nl, pcol, s));
+  LK(full_graph_scales(prp, nl, c->arch, pscale, s));
+  void *bufA = nullptr, *bufB = nullptr;
+  float* logits = nullptr;
+  TRY(dalloc(c, &bufA, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
+  TRY(dalloc(c, &bufB, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
+  TRY(dalloc_t(c, &logits, (size_t)std::max<int64_t>(max_chunk, 1) * Nl));
+  for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
+    const int f = chunk_first[j], e = chunk_first[j + 1];
+    const int64_t k0 = lbeg[f], rows = lbeg[e] - k0;
+    if (rows == 0) continue;
+    T* Cb = (T*)bufA;
+    T* Hn = (T*)bufB;
+    for (int l = 0; l < c->L; ++l) {
+      const int64_t K = c->th_K[l], N = c->th_N[l];
+      const int64_t half = pad8(c->dims[l]);
+      SpmmArgs<T, T> a;
+      a.row_beg = prp + k0; a.row_end = prp + k0 + 1; a.col = pcol; a.rows = rows; a.rowscale = pscale + k0;
+      const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
+      if (l == 0) a.h_index = pnode_d + k0;  // chunk row -> internal node id (rows of X)
+      if (sage) {
+        if (l == 0) { a.self_out = Cb; a.ld_self = K; }
+        a.H = l == 0 ? Hin : Cb; a.ldh = l == 0 ? half : K;
+        a.out = Cb + half; a.ldo = K; a.w = half;
+      } else {
+        a.colscale = pscale + k0; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
+      }
+      LK((spmm<T, T>(a, s)));
+      const void* Wl = sizeof(T) == 2 ? wl[l] : (const void*)c->theta[l];
+      if (l + 1 < c->L) {
+        TRY(gemm_any(c, false, false, rows, N, K, Cb, K, Wl, N, Hn, c->th_K[l + 1], false, true, s));
+        if (sage) std::swap(Cb, Hn);
+      } else {
+        TRY(gemm_any(c, false, false, rows, N, K, Cb, K, Wl, N, logits, N, true, false, s));
+      }
+    }
+    LK(eval_parts(logits, Nl, c->k, lbeg_d + f, k0, e - f, pnode_d, c->labels, c->split, code, out3 + 3 * f, s));
+  }
+  std::vector<double> loc(3 * (size_t)std::max(nlp, 1));
+  CK(cudaMemcpyAsync(loc.data(), out3, loc.size() * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  TRY(check_launch(c, "eval_parts"));
+  sums.assign(3 * (size_t)np, 0.0);
+  for (int j = 0; j < nlp; ++j)
+    for (int q = 0; q < 3; ++q) sums[3 * (size_t)lparts[j] + q] = loc[3 * (size_t)j + q];
+  if (W > 1) {  // every partition was evaluated by exactly one rank: a sum-all-reduce assembles them
+    double* red = nullptr;
+    TRY(dalloc_t(c, &red, sums.size()));
+    CK(cudaMemcpyAsync(red, sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, s));
+    NK(ncclAllReduce(red, red, sums.size(), ncclDouble, ncclSum, c->comm, s));
+    CK(cudaMemcpyAsync(sums.data(), red, sums.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(c, red);
+  }
+  for (void* p : wl) if (p) dfree(c, p);
+  for (void* p : {(void*)pnode_d, (void*)pos_d, (void*)part_d, (void*)rb_d, (void*)pcol, (void*)deg, (void*)prp,
+                  (void*)lbeg_d, (void*)pscale, (void*)out3, bufA, bufB, (void*)logits})
+    dfree(c, p);
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const int32_t* part_ids, int32_t num_parts,
+                                       int64_t max_rows, float* loss, float* acc, float* part_loss,
+                                       float* part_acc) {
+  PRE(c);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_parts: needs params and no open round");
+  if (split_code < 0 || split_code > 3) return GIST_E_ARG;
+  const int64_t n = c->n;
+  std::vector<int32_t> part(n);
+  int np = num_parts;
+  if (part_ids) {
+    if (num_parts < 1) return fail(c, GIST_E_ARG, "eval_parts: num_parts < 1");
+    for (int64_t g = 0; g < n; ++g) {
+      const int32_t p = part_ids[c->perm_h[g]];
+      if (p < 0 || p >= num_parts) return fail(c, GIST_E_ARG, "eval_parts: partition id out of range");
+      part[g] = p;
+    }
+  } else {  // the training clusters (contiguous internal id ranges after relabelling)
+    np = (int)c->cstart_h.size() - 1;
+    if (num_parts != 0 && num_parts != np) return fail(c, GIST_E_ARG, "eval_parts: num_parts != clusters");
+    for (int p = 0; p < np; ++p)
+      for (int64_t g = c->cstart_h[p]; g < c->cstart_h[p + 1]; ++g) part[g] = p;
+  }
+  std::vector<double> sums;
+  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, split_code, part, np, max_rows, sums)
+                                : eval_parts_t<float>(c, split_code, part, np, max_rows, sums));
+  double ls = 0.0, as = 0.0;
+  int cntp = 0;
+  for (int p = 0; p < np; ++p) {
+    const double k = sums[3 * (size_t)p + 2];
+    const float lp = k > 0 ? (float)(sums[3 * (size_t)p] / k) : NAN;
+    const float ap = k > 0 ? (float)(sums[3 * (size_t)p + 1] / k) : NAN;
+    if (part_loss) part_loss[p] = lp;
+    if (part_acc) part_acc[p] = ap;
+    if (k > 0) ls += sums[3 * (size_t)p] / k, as += sums[3 * (size_t)p + 1] / k, ++cntp;
+  }
+  if (loss) *loss = cntp ? (float)(ls / cntp) : 0.f;
+  if (acc) *acc = cntp ? (float)(as / cntp) : 0.f;
+  return GIST_OK;
+}
+
 // ====================================================== inspection hooks ===
 extern "C" gist_status gist_sub_shape(gist_ctx* c, int32_t slot, int32_t layer, int64_t* rows, int64_t* cols) {
   PRE(c);

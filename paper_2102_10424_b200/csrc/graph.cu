@@ -87,6 +87,60 @@ template void gather_rows_f32<float>(const float*, int64_t, const int32_t*, int6
 template void gather_rows_f32<bf16>(const float*, int64_t, const int32_t*, int64_t, int64_t, bf16*, int64_t,
                                     cudaStream_t);
 
+// ------------------------------------------------ partition-wise eval (R20) --
+// Partition-induced graph in partition order: position g holds internal node pnode[g];
+// only neighbours in the same partition are kept, as positions relative to the first
+// position of g's evaluation chunk (rowbase[g]), so one chunk's rows form a closed CSR.
+__global__ void k_part_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ pnode, const int32_t* __restrict__ part, int64_t n,
+                             int64_t* __restrict__ deg_new) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= n) return;
+  const int64_t v = pnode[g];
+  const int32_t pv = part[v];
+  int cnt = 0;
+  for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
+    const int32_t u = col[e];
+    cnt += (u != v) && part[u] == pv;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) deg_new[g] = cnt;
+}
+
+__global__ void k_part_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ pnode, const int32_t* __restrict__ pos,
+                            const int32_t* __restrict__ part, const int32_t* __restrict__ rowbase,
+                            const int64_t* __restrict__ rp_new, int64_t n, int32_t* __restrict__ col_new) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= n) return;
+  const int64_t v = pnode[g];
+  const int32_t pv = part[v], base = rowbase[g];
+  int64_t out = rp_new[g];
+  for (int64_t b = rp[v]; b < rp[v + 1]; b += 32) {
+    const int64_t e = b + lane;
+    const bool in = e < rp[v + 1];
+    const int32_t u = in ? col[e] : 0;
+    const bool keep = in && u != v && part[u] == pv;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) col_new[out + __popc(bal & ((1u << lane) - 1))] = pos[u] - base;
+    out += __popc(bal);
+  }
+}
+
+void part_count(const int64_t* rp, const int32_t* col, const int32_t* pnode, const int32_t* part, int64_t n,
+                int64_t* deg_new, cudaStream_t s) {
+  if (n <= 0) return;
+  k_part_count<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(rp, col, pnode, part, n, deg_new);
+}
+void part_fill(const int64_t* rp, const int32_t* col, const int32_t* pnode, const int32_t* pos, const int32_t* part,
+               const int32_t* rowbase, const int64_t* rp_new, int64_t n, int32_t* col_new, cudaStream_t s) {
+  if (n <= 0) return;
+  k_part_fill<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(rp, col, pnode, pos, part, rowbase, rp_new, n, col_new);
+}
+
 // full-graph normalisation scales (R1: (deg+1)^{-1/2}; R2: 1/deg or 0)
 __global__ void k_full_scales(const int64_t* __restrict__ rp, int64_t n, int arch, float* __restrict__ scale) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -194,6 +194,11 @@ void relabel_fill(const int64_t* rp, const int32_t* col, const int32_t* perm, co
 template <typename T>
 void gather_rows_f32(const float* src, int64_t ld_src, const int32_t* idx, int64_t n, int64_t w, T* dst,
                      int64_t ld_dst, cudaStream_t s);
+// partition-wise eval (R20): partition-induced CSR in partition order, chunk-relative columns
+void part_count(const int64_t* rp, const int32_t* col, const int32_t* pnode, const int32_t* part, int64_t n,
+                int64_t* deg_new, cudaStream_t s);
+void part_fill(const int64_t* rp, const int32_t* col, const int32_t* pnode, const int32_t* pos, const int32_t* part,
+               const int32_t* rowbase, const int64_t* rp_new, int64_t n, int32_t* col_new, cudaStream_t s);
 void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cudaStream_t s);
 
 // Device-resident step state: the kernels of one subTrain step read everything that
@@ -321,5 +326,11 @@ void glorot_init(float* theta, int rows_logical, int cols, int sage, int d_l, in
 // eval: per-row CE / argmax correctness over rows with split == code; reduce (deterministic)
 void eval_rows(const float* logits, int64_t ld, int64_t n, int k, const int32_t* labels, const uint8_t* split,
                int code, double* out3, cudaStream_t s);
+
+// partition-wise eval: one CTA per partition of a chunk (positions pbeg[p]..pbeg[p+1]; logits row
+// = position - k0); out3[3p..3p+2] = (sum CE, correct, count) over rows with split == code
+void eval_parts(const float* logits, int64_t ld, int k, const int64_t* pbeg, int64_t k0, int nparts,
+                const int32_t* pnode,
+                const int32_t* labels, const uint8_t* split, int code, double* out3, cudaStream_t s);
 
 }  // namespace gist

@@ -224,4 +224,42 @@ void eval_rows(const float* logits, int64_t ld, int64_t n, int k, const int32_t*
   k_eval_rows<<<1, 1024, 0, s>>>(logits, ld, n, k, labels, split, code, out3);
 }
 
+__global__ void __launch_bounds__(256) k_eval_parts(const float* __restrict__ logits, int64_t ld, int k,
+                                                    const int64_t* __restrict__ pbeg, int64_t k0,
+                                                    const int32_t* __restrict__ pnode,
+                                                    const int32_t* __restrict__ labels,
+                                                    const uint8_t* __restrict__ split, int code,
+                                                    double* __restrict__ out3) {
+  using Red = cub::BlockReduce<double, 256>;
+  __shared__ typename Red::TempStorage tr;
+  const int p = blockIdx.x;
+  double loss = 0.0, corr = 0.0, cnt = 0.0;
+  for (int64_t r = pbeg[p] + threadIdx.x; r < pbeg[p + 1]; r += 256) {
+    const int32_t v = pnode[r];
+    if (split[v] != code) continue;
+    const float* z = logits + (r - k0) * ld;
+    float mx = -INFINITY;
+    int am = 0;
+    for (int c = 0; c < k; ++c)
+      if (z[c] > mx) { mx = z[c]; am = c; }
+    float se = 0.f;
+    for (int c = 0; c < k; ++c) se += expf(z[c] - mx);
+    loss += (double)(mx + logf(se) - z[labels[v]]);
+    corr += am == labels[v];
+    cnt += 1.0;
+  }
+  double a = Red(tr).Sum(loss);
+  __syncthreads();
+  double b = Red(tr).Sum(corr);
+  __syncthreads();
+  double c = Red(tr).Sum(cnt);
+  if (threadIdx.x == 0) { out3[3 * p] = a; out3[3 * p + 1] = b; out3[3 * p + 2] = c; }
+}
+void eval_parts(const float* logits, int64_t ld, int k, const int64_t* pbeg, int64_t k0, int nparts,
+                const int32_t* pnode, const int32_t* labels, const uint8_t* split, int code, double* out3,
+                cudaStream_t s) {
+  if (nparts <= 0) return;
+  k_eval_parts<<<nparts, 256, 0, s>>>(logits, ld, k, pbeg, k0, pnode, labels, split, code, out3);
+}
+
 }  // namespace gist

@@ -24,7 +24,7 @@ TRACE_NODES, TRACE_ACT, TRACE_LOGITS, TRACE_GRAD, TRACE_LOSS = range(5)
 # every symbol include/gist.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "gist_config_default", "gist_create", "gist_load_graph", "gist_init_params", "gist_partition",
-    "gist_subtrain", "gist_aggregate", "gist_eval", "gist_get_params", "gist_set_params",
+    "gist_subtrain", "gist_aggregate", "gist_eval", "gist_eval_parts", "gist_get_params", "gist_set_params",
     "gist_get_partition", "gist_sub_shape", "gist_get_sub_params", "gist_get_trace", "gist_stat",
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
     "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
@@ -68,6 +68,7 @@ def lib() -> C.CDLL:
         "gist_subtrain": (i32, [vp, i32, f32, vp]),
         "gist_aggregate": (i32, [vp]),
         "gist_eval": (i32, [vp, i32, P(f32), P(f32)]),
+        "gist_eval_parts": (i32, [vp, i32, vp, i32, i64, P(f32), P(f32), vp, vp]),
         "gist_get_params": (i32, [vp, i32, vp]),
         "gist_set_params": (i32, [vp, i32, vp]),
         "gist_get_partition": (i32, [vp, i32, vp, vp]),
@@ -165,6 +166,7 @@ class Gist:
         n = len(rp) - 1
         self._check(lib().gist_load_graph(self.h, n, _ptr(rp), _ptr(ci), int(rp[-1]), _ptr(X), _ptr(lab),
                                           int(g["num_classes"]), _ptr(sp), _ptr(cl), int(g["num_clusters"])))
+        self.num_clusters = int(g["num_clusters"])
 
     def init_params(self, seed: int):
         self._check(lib().gist_init_params(self.h, seed))
@@ -185,6 +187,22 @@ class Gist:
         loss, acc = C.c_float(), C.c_float()
         self._check(lib().gist_eval(self.h, split_code, C.byref(loss), C.byref(acc)))
         return loss.value, acc.value
+
+    def eval_parts(self, split_code: int, part_ids=None, num_parts: int = 0, max_rows: int = 0):
+        """Partition-wise evaluation (gist_eval_parts); part_ids indexed by original node id,
+        None = the training clusters.  Returns (loss, acc, per-partition loss, per-partition acc)."""
+        if part_ids is not None:
+            part_ids = np.ascontiguousarray(part_ids, dtype=np.int32)
+            npart = int(num_parts)
+        else:
+            npart = int(self.num_clusters)
+        loss, acc = C.c_float(), C.c_float()
+        lp = np.zeros(npart, dtype=np.float32)
+        ap = np.zeros(npart, dtype=np.float32)
+        self._check(lib().gist_eval_parts(self.h, split_code, _ptr(part_ids) if part_ids is not None else None,
+                                          num_parts if part_ids is not None else 0, max_rows,
+                                          C.byref(loss), C.byref(acc), _ptr(lp), _ptr(ap)))
+        return loss.value, acc.value, lp, ap
 
     def param_shape(self, layer: int):
         f = 2 if self.arch == "sage" else 1
