@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--profile-stride", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-eval", action="store_true", help="skip the (untimed-for-value) evaluation timings")
+    ap.add_argument("--eval-parts", type=int, default=5000, help="partitions of the partition-wise eval (P:697)")
     args = ap.parse_args()
     spec = MODELS[args.config]
     rank, world, local = dist_env()
@@ -244,6 +246,25 @@ def main():
     block_agg = gx.stat(G.STAT_BLOCK_AGG)
     block_density = gx.stat(G.STAT_BLOCK_DENSITY_PPM) / 1e6
     nnzb_last = gx.stat(G.STAT_LAST_NNZ_B)
+    # ------------------------------------------------ evaluation (not part of `value`)
+    ev = None
+    if not args.no_eval:
+        n = g["n"]
+        order = np.argsort(g["cluster_ids"], kind="stable")
+        part = np.empty(n, np.int32)
+        part[order] = (np.arange(n) * args.eval_parts) // n     # METIS stand-in: cluster-sorted order cut
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        lf, af = gx.eval(2)
+        t_full = time.perf_counter() - t0
+        barrier()
+        t0 = time.perf_counter()
+        lp, apc, _, _ = gx.eval_parts(2, part, args.eval_parts)
+        t_parts = time.perf_counter() - t0
+        ev = {"split": "test", "full_graph_s": t_full, "full_graph_loss": lf, "full_graph_acc": af,
+              "parts": args.eval_parts, "parts_s": t_parts, "parts_loss": lp, "parts_acc": apc,
+              "note": "after the timed rounds; wall clock around each ABI call (host setup included)"}
     total_ms = float(sum(times))
     if world > 1:
         t = torch.tensor([total_ms], device=f"cuda:{local}")
@@ -318,6 +339,7 @@ def main():
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernel_profile": {k: {"ms": v["ms"], "launches": v["launches"]} for k, v in prof.items()},
+        "eval": ev,
         "e2e": {"value": steps_total / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": h2d / args.steps,
                 "d2h_bytes_per_step": d2h / args.steps,
                 "includes": "gist_load_graph from host arrays + init + K rounds with per-round loss readback"},

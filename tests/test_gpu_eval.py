@@ -84,29 +84,35 @@ def test_eval_parts_bad_ids():
         gpu.eval_parts(7, part, 5)
 
 
-@pytest.mark.slow
-@pytest.mark.parametrize("precision", ["bf16", "fp32"])
-def test_eval_parts_c3_full_size_sampled(precision):
-    """C3 graph (232,965 nodes, 114.6M nnz), global 4-layer GraphSAGE at width 4096 — the
-    regime where the paper evaluates on 5,000 partitions.  Partitions: the cluster-sorted
-    node order cut into 5,000 contiguous pieces (≈ 47 nodes, mostly inside one cluster).
-    The oracle recomputes 12 sampled partitions in FP64."""
+@pytest.fixture(scope="module")
+def c3():
     spec = MODELS["C3"]
     g = generate(GRAPHS["reddit"], seed=0, device="cuda")
     dims = list(spec.dims)
-    from paper_2102_10424_b200.gist import Gist
-    gpu = Gist(spec.arch, dims, precision=precision, clusters_per_batch=spec.q)
-    gpu.load_graph(g)
-    gpu.init_params(11)
     n = len(g["labels"])
     order = np.argsort(g["cluster_ids"], kind="stable")
     part = np.empty(n, np.int32)
     part[order] = (np.arange(n) * 5000) // n
-    lg, ag, lpg, apg = gpu.eval_parts(2, part, 5000)
     ora = O.OracleGIST(arch=spec.arch, dims=dims)
     ora.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
                    g["cluster_ids"], g["num_clusters"])
     ora.init_params(11)     # the same counter-based Glorot init (R11), computed on the host
+    return spec, g, part, ora
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_eval_parts_c3_full_size_sampled(c3, precision):
+    """C3 graph (232,965 nodes, 114.6M nnz), global 4-layer GraphSAGE at width 4096 — the
+    regime where the paper evaluates on 5,000 partitions.  Partitions: the cluster-sorted
+    node order cut into 5,000 contiguous pieces (≈ 47 nodes, mostly inside one cluster).
+    The oracle recomputes 12 sampled partitions in FP64."""
+    from paper_2102_10424_b200.gist import Gist
+    spec, g, part, ora = c3
+    gpu = Gist(spec.arch, list(spec.dims), precision=precision, clusters_per_batch=spec.q)
+    gpu.load_graph(g)
+    gpu.init_params(11)
+    lg, ag, lpg, apg = gpu.eval_parts(2, part, 5000)
     sample = np.random.default_rng(0).choice(5000, 12, replace=False)
     _, _, lpo, apo = ora.eval_partitions(2, part, 5000, parts=sample)
     ok = ~np.isnan(apo[sample])
