@@ -125,7 +125,8 @@ struct gist_ctx {
   int64_t self_loops = 0;
   int64_t *rp = nullptr, *cstart = nullptr;
   int32_t *col = nullptr, *cid = nullptr, *labels = nullptr;
-  int32_t* ccol = nullptr;  // cluster of every edge's neighbour (batch build)
+  int32_t* ccol = nullptr;  // cluster of every edge's neighbour (batch build), or packed codes (pack_ob > 0)
+  int pack_ob = 0;          // offset bits of the packed edge codes (0: plain cluster ids)
   uint8_t* split = nullptr;
   void* X = nullptr;  // n x pad8(d0), T
   float* full_scale = nullptr;
@@ -656,7 +657,11 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   c->h2d += n * 9 + (num_clusters + 1) * 8;
   LK(full_graph_scales(c->rp, n, c->arch, c->full_scale, s));
   TRY(dalloc_t(c, &c->ccol, std::max<int64_t>(c->nnz, 1)));
-  LK(edge_clusters(c->col, c->cid, c->nnz, c->ccol, s));
+  c->pack_ob = pack_bits(num_clusters, c->max_csize);
+  if (c->pack_ob)
+    LK(edge_codes(c->col, c->cid, c->cstart, c->nnz, c->pack_ob, c->ccol, s));
+  else
+    LK(edge_clusters(c->col, c->cid, c->nnz, c->ccol, s));
   // Block-diagonal tensor-core aggregation: GraphSAGE in BF16 mode when the
   // clusters are small (<= 256 rows) and their intra-cluster blocks dense enough (>= 5%).
   // GIST_BD=0/1 overrides the choice.
@@ -1338,10 +1343,12 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     double vol = 0.0;
     for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
     int id = -1;
-    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_BATCH, vol * 16.0 + g.count * c->nb_max_rows * 45.0, 4.0, nnz_slot);
+    if (c->prof_now)
+      id = prof_begin(c, s, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0, 4.0,
+                      nnz_slot);
     batch_setup(g.batch, c->cstart, c->rp, s);
     batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
-                c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, s);
+                c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, s);
     prof_end(c, s, id);
     c->nk += 2;
     if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size

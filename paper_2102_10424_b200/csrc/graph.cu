@@ -205,7 +205,7 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 // deterministic).  grid (cdiv(nb_max, 16), slots), 512 threads.
 constexpr int kBuildRows = 16;
 constexpr int32_t kAbsent = INT32_MIN;  // |loff - cstart| < 2^31 - 1: never a real offset
-template <bool SMAP>
+template <bool SMAP, bool PACK>
 __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ BatchGroup G,
                                                         const int64_t* __restrict__ rp,
                                                         const int32_t* __restrict__ col,
@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
                                                         const int32_t* __restrict__ cid, int arch,
                                                         const int32_t* __restrict__ labels,
                                                         const uint8_t* __restrict__ split, int skip_intra,
-                                                        const int64_t* __restrict__ cstart, int num_clusters) {
+                                                        const int64_t* __restrict__ cstart, int num_clusters,
+                                                        int ob) {
   extern __shared__ int32_t smap[];  // SMAP: [num_clusters]
   pdl_wait();
   pdl_trigger();
@@ -226,7 +227,8 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
     for (int i = threadIdx.x; i < num_clusters; i += blockDim.x) smap[i] = kAbsent;
     __syncthreads();
     const int qq = d[3 * q + 2];
-    for (int k = threadIdx.x; k < qq; k += blockDim.x) smap[d[k]] = d[q + k] - (int32_t)cstart[d[k]];
+    // PACK: local id = local start of the cluster + offset inside it; else u + (loff - cstart)
+    for (int k = threadIdx.x; k < qq; k += blockDim.x) smap[d[k]] = d[q + k] - (PACK ? 0 : (int32_t)cstart[d[k]]);
     __syncthreads();
   }
   __shared__ int s_cnt[kBuildRows], s_tr[kBuildRows];
@@ -247,17 +249,23 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
     auto walk = [&](auto RT) {
       constexpr int R = decltype(RT)::value;
       for (int64_t base = rp[g]; base < end; base += R) {
+        // PACK: u holds the edge code (neighbour cluster << ob) | offset inside it, cc is unused
         int32_t u[R / 32], cc[R / 32], dl[R / 32];
 #pragma unroll
-        for (int r = 0; r < R / 32; ++r) {  // col and its cluster: independent, coalesced loads
+        for (int r = 0; r < R / 32; ++r) {  // independent, coalesced loads
           const int64_t e = base + r * 32 + lane;
-          u[r] = e < end ? col[e] : -1;
-          cc[r] = e < end ? ccol[e] : 0;
+          if (PACK) {
+            u[r] = e < end ? ccol[e] : -1;
+          } else {
+            u[r] = e < end ? col[e] : -1;
+            cc[r] = e < end ? ccol[e] : 0;
+          }
         }
+        auto clus = [&](int r) { return PACK ? (u[r] >> ob) : cc[r]; };
 #pragma unroll
         for (int r = 0; r < R / 32; ++r) {
           if (SMAP) {
-            dl[r] = u[r] >= 0 ? smap[cc[r]] : kAbsent;
+            dl[r] = u[r] >= 0 ? smap[clus(r)] : kAbsent;
           } else {
             const uint64_t m = u[r] >= 0 ? S.map64[cc[r]] : 0ull;
             dl[r] = (u[r] >= 0 && (uint32_t)(m >> 32) == tag) ? (int32_t)(uint32_t)m : kAbsent;
@@ -267,17 +275,18 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
         for (int r = 0; r < R / 32; ++r) {
           bool in = dl[r] != kAbsent;
           if (skip_intra) {
-            const bool ii = in && cc[r] == cg;
+            const bool ii = in && clus(r) == cg;
             intra += __popc(__ballot_sync(0xffffffffu, ii));
             in &= !ii;
           }
           const unsigned bm = __ballot_sync(0xffffffffu, in);
-          if (in) S.b_col[out + __popc(bm & lt)] = u[r] + dl[r];
+          if (in) S.b_col[out + __popc(bm & lt)] = (PACK ? (u[r] & ((1 << ob) - 1)) : u[r]) + dl[r];
           out += __popc(bm);
         }
       }
     };
-    if (end - rp[g] > 128) walk(std::integral_constant<int, 256>());
+    if (PACK && end - rp[g] > 256) walk(std::integral_constant<int, PACK ? 512 : 256>());
+    else if (end - rp[g] > 128) walk(std::integral_constant<int, 256>());
     else walk(std::integral_constant<int, 128>());
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
     if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
 }
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
                  const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
-                 const uint8_t* split, int skip_intra, cudaStream_t s) {
+                 const uint8_t* split, int skip_intra, int ob, cudaStream_t s) {
   if (G.nb_max <= 0) return;
   const dim3 grid((unsigned)cdiv(G.nb_max, kBuildRows), (unsigned)G.n);
   const size_t smem = (size_t)num_clusters * 4;
@@ -318,15 +327,44 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
   if (smem <= 64 * 1024 && !(force && force[0] == '1')) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_batch_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_batch_build<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+      cudaFuncSetAttribute(k_batch_build<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       attr = true;
     }
-    launch_pdl(k_batch_build<true>, grid, kBuildRows * 32, smem, s, G, rp, col, ccol, cid, arch, labels, split,
-               skip_intra, cstart, num_clusters);
-  } else {
-    launch_pdl(k_batch_build<false>, grid, kBuildRows * 32, 0, s, G, rp, col, ccol, cid, arch, labels, split,
-               skip_intra, cstart, num_clusters);
+    if (ob > 0)
+      launch_pdl(k_batch_build<true, true>, grid, kBuildRows * 32, smem, s, G, rp, col, ccol, cid, arch, labels,
+                 split, skip_intra, cstart, num_clusters, ob);
+    else
+      launch_pdl(k_batch_build<true, false>, grid, kBuildRows * 32, smem, s, G, rp, col, ccol, cid, arch, labels,
+                 split, skip_intra, cstart, num_clusters, 0);
+  } else {  // the packed codes are only built when the shared-memory map applies (pack_bits)
+    launch_pdl(k_batch_build<false, false>, grid, kBuildRows * 32, 0, s, G, rp, col, ccol, cid, arch, labels, split,
+               skip_intra, cstart, num_clusters, 0);
   }
+}
+
+// ob > 0: packed per-edge codes (cid[u] << ob) | (u - cstart[cid[u]]) (one array instead of col +
+// ccol for the batch build); ob == 0: ccol[e] = cid[col[e]]
+__global__ void k_edge_codes(const int32_t* __restrict__ col, const int32_t* __restrict__ cid,
+                             const int64_t* __restrict__ cstart, int64_t nnz, int ob, int32_t* __restrict__ code) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = col[e], k = cid[u];
+    code[e] = (k << ob) | (int32_t)(u - cstart[k]);
+  }
+}
+void edge_codes(const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t nnz, int ob, int32_t* code,
+                cudaStream_t s) {
+  if (nnz <= 0) return;
+  k_edge_codes<<<148 * 8, 256, 0, s>>>(col, cid, cstart, nnz, ob, code);
+}
+int pack_bits(int num_clusters, int64_t max_csize) {
+  if ((size_t)num_clusters * 4 > 64 * 1024 || std::getenv("GIST_BATCH_GLOBAL_MAP")) return 0;
+  const char* env = std::getenv("GIST_PACK_EDGES");
+  if (env && env[0] == '0') return 0;
+  int ob = 1, cb = 1;
+  while (((int64_t)1 << ob) < max_csize) ++ob;
+  while ((1 << cb) < num_clusters) ++cb;
+  return ob + cb <= 31 ? ob : 0;
 }
 
 __global__ void k_edge_clusters(const int32_t* __restrict__ col, const int32_t* __restrict__ cid, int64_t nnz,

@@ -244,7 +244,11 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 // ccol[e] = cid[col[e]] (cluster of every edge's neighbour, precomputed at load)
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
                  const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
-                 const uint8_t* split, int skip_intra, cudaStream_t s);
+                 const uint8_t* split, int skip_intra, int ob, cudaStream_t s);
+// packed edge codes for the batch build: offset bits ob (0 = packing does not apply: use ccol)
+int pack_bits(int num_clusters, int64_t max_csize);
+void edge_codes(const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t nnz, int ob, int32_t* code,
+                cudaStream_t s);
 void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s);
 // out[3] (zeroed by the caller): edges with col outside [0, n), self loops, intra-cluster edges
 void validate_edges(const int64_t* rp, const int32_t* col, const int32_t* cid, int64_t n, unsigned long long* out,
