@@ -828,7 +828,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     TRY(dalloc_t(c, &s.scale, nbm));
     TRY(dalloc_t(c, &s.b_beg, nbm));
     TRY(dalloc_t(c, &s.b_end, nbm));
-    TRY(dalloc_t(c, &s.stats, 2));
+    TRY(dalloc_t(c, &s.stats, 4));  // [0] nnz_b, [1] train rows, [2] batch-build row counter
     TRY(dalloc_t(c, &s.b_col, std::max<int64_t>(c->nnzb_max, 1)));
     TRY(dalloc_t(c, &s.map64, c->c));
     CK(cudaMemsetAsync(s.map64, 0, (size_t)c->c * 8, c->stream));  // tag 0 = never in a batch

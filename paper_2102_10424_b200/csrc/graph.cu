@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -173,7 +174,7 @@ __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_
     const int32_t c = bcl[v];
     S.map64[c] = ((uint64_t)tag << 32) | (uint32_t)(loff[v] - (int32_t)cstart[c]);
   }
-  if (v == 0) S.stats[0] = S.stats[1] = 0;
+  if (v == 0) S.stats[0] = S.stats[1] = S.stats[2] = 0;
   if (v >= G.nb_max) return;
   if (v >= nb) {  // inert dummy row: no neighbours, marked by a negative row start
     S.b_nodes[v] = 0;
@@ -202,7 +203,7 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 // "absent") is built in shared memory from the step descriptor by every block, so the
 // per-edge membership test is a shared-memory lookup; otherwise the tagged global map64.
 // Counters are warp -> block reduced, one integer atomic per block (integer addition:
-// deterministic).  grid (cdiv(nb_max, 16), slots), 512 threads.
+// deterministic).  grid (<= 2 x 148 / slots, slots), 512 threads; rows dealt by an atomic counter.
 constexpr int kBuildRows = 16;
 constexpr int32_t kAbsent = INT32_MIN;  // |loff - cstart| < 2^31 - 1: never a real offset
 template <bool SMAP, bool PACK>
@@ -233,7 +234,15 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
   }
   __shared__ int s_cnt[kBuildRows], s_tr[kBuildRows];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int v = blockIdx.x * kBuildRows + w;
+  // rows are handed out by a per-slot counter (reset by k_batch_setup): a warp that finishes a
+  // short row takes the next one instead of idling until the longest row of its block is done
+  int* next_row = reinterpret_cast<int*>(S.stats + 2);
+  int cnt_sum = 0, tr_sum = 0;
+  for (;;) {
+  int v = 0;
+  if (lane == 0) v = atomicAdd(next_row, 1);
+  v = __shfl_sync(0xffffffffu, v, 0);
+  if (v >= G.nb_max) break;
   int cnt = 0, tr = 0;
   if (v < nb) {
     const int64_t g = S.b_nodes[v];
@@ -302,13 +311,16 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
       tr = split[g] == 0;
       S.train_b[v] = (uint8_t)tr;
     }
-  } else if (v < G.nb_max && lane == 0) {  // inert dummy row
+  } else if (lane == 0) {  // inert dummy row
     S.b_end[v] = -1;
     S.scale[v] = 0.f;
     S.lab_b[v] = 0;
     S.train_b[v] = 0;
   }
-  if (lane == 0) { s_cnt[w] = cnt; s_tr[w] = tr; }
+  cnt_sum += cnt;
+  tr_sum += tr;
+  }
+  if (lane == 0) { s_cnt[w] = cnt_sum; s_tr[w] = tr_sum; }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long a = 0, b = 0;
@@ -321,7 +333,9 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
                  const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
                  const uint8_t* split, int skip_intra, int ob, cudaStream_t s) {
   if (G.nb_max <= 0) return;
-  const dim3 grid((unsigned)cdiv(G.nb_max, kBuildRows), (unsigned)G.n);
+  // two 512-thread CTAs per SM (launch bounds) shared by the slots; rows are dealt dynamically
+  const int per_slot = std::max(1, std::min((int)cdiv(G.nb_max, kBuildRows), 2 * 148 / std::max(G.n, 1)));
+  const dim3 grid((unsigned)per_slot, (unsigned)G.n);
   const size_t smem = (size_t)num_clusters * 4;
   const char* force = std::getenv("GIST_BATCH_GLOBAL_MAP");  // tests: exercise the global-map path
   if (smem <= 64 * 1024 && !(force && force[0] == '1')) {

@@ -227,7 +227,7 @@ struct BatchSlot {
   float* scale;
   int32_t* lab_b;
   uint8_t* train_b;
-  int64_t* stats;  // [0] nnz_b, [1] train rows
+  int64_t* stats;  // [0] nnz_b, [1] train rows, [2] batch-build row counter (int)
 };
 struct BatchGroup {
   BatchSlot s[kMaxGroup];

@@ -16,8 +16,12 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
   pdl_wait();
   pdl_trigger();
   const CeSlot<T>& S = G.s[blockIdx.y];
-  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  // 8 lanes per row (4 rows per warp): the class count is small (7..47), so a full warp per
+  // row left most lanes idle and made the launch instruction-bound
+  constexpr int LPR = 8;
+  const int gl = threadIdx.x & (LPR - 1);
+  const unsigned gmask = ((1u << LPR) - 1u) << ((threadIdx.x & 31) - gl);  // this row's lanes
+  const int v = (blockIdx.x * blockDim.x + threadIdx.x) / LPR;
   const int64_t nt = S.stats[1];
   if (v < G.rows) {
     const int64_t ld = G.ld;
@@ -25,25 +29,25 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
     const float* z = S.logits + (int64_t)v * ld;
     const bool tr = S.train[v] && nt > 0;
     float mx = -INFINITY;
-    for (int c = lane; c < k; c += 32) mx = fmaxf(mx, z[c]);
+    for (int c = gl; c < k; c += LPR) mx = fmaxf(mx, z[c]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = LPR / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o, LPR));
     float se = 0.f;
-    for (int c = lane; c < k; c += 32) se += expf(z[c] - mx);
+    for (int c = gl; c < k; c += LPR) se += expf(z[c] - mx);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    for (int o = LPR / 2; o; o >>= 1) se += __shfl_xor_sync(gmask, se, o, LPR);
     const float lse = mx + logf(se);
     const int y = S.lab[v];
     const float inv = tr ? 1.0f / (float)nt : 0.f;
     const int64_t ldd = G.ld_dlog ? G.ld_dlog : ld;
     const float sv = S.dlog_s ? S.scale_s[v] : 0.f;
-    for (int c = lane; c < ld; c += 32) {
+    for (int c = gl; c < ld; c += LPR) {
       float g = 0.f;
       if (tr && c < k) g = (expf(z[c] - lse) - (c == y ? 1.f : 0.f)) * inv;
       S.dlog[(int64_t)v * ldd + c] = Elem<T>::from_f(g);
       if (S.dlog_s) S.dlog_s[(int64_t)v * ldd + c] = Elem<T>::from_f(g * sv);
     }
-    if (lane == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
+    if (gl == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
   }
   __shared__ bool s_last;
   __syncthreads();
@@ -70,7 +74,7 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
 template <typename T>
 void softmax_ce(const CeGroup<T>& G, cudaStream_t s) {
   if (G.rows <= 0 || G.n <= 0) return;
-  launch_pdl(k_softmax_ce<T>, dim3((unsigned)cdiv(G.rows, 8), (unsigned)G.n), 256, 0, s, G);
+  launch_pdl(k_softmax_ce<T>, dim3((unsigned)cdiv(G.rows, 32), (unsigned)G.n), 256, 0, s, G);
 }
 template void softmax_ce<float>(const CeGroup<float>&, cudaStream_t);
 template void softmax_ce<bf16>(const CeGroup<bf16>&, cudaStream_t);
