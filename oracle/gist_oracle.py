@@ -29,7 +29,8 @@ __all__ = [
     "sample_partition", "sub_index_sets", "extract", "aggregate",
     "aggregate_delta_sum", "coverage_fraction", "sub_param_count",
     "glorot_init", "glorot_block", "batch_schedule", "batch_nodes", "induced_subgraph",
-    "gcn_operator", "sage_operator", "chebyshev_operator", "spmm",
+    "gcn_operator", "sage_operator", "chebyshev_operator", "spmm", "gat_structure", "gat_attention",
+    "weight_rows",
     "forward", "backward", "softmax_ce", "adam_step", "sgd_step",
     "OracleGIST", "lr_step_schedule",
 ]
@@ -128,13 +129,17 @@ def sub_index_sets(arch: str, dims: list[int], blocks, i: int):
     """Row/column index sets of Theta_l^(i) = [Theta_l]_{D_l^(i) x D_{l+1}^(i)}.
 
     GraphSAGE weights act on [H || N H] (R2), so their rows are D_l^(i) followed by
-    d_l + D_l^(i) (self block, then neighbour block; R6).
+    d_l + D_l^(i) (self block, then neighbour block; R6).  GAT weights carry the two
+    attention vectors as rows d_l (a_src) and d_l + 1 (a_dst) (R21); every sub-GCN keeps
+    both rows, sliced to its output units.
     """
     out = []
     for l in range(len(dims) - 1):
         rows = blocks[l][i]
         if arch == "sage":
             rows = np.concatenate([rows, dims[l] + rows])
+        elif arch == "gat":      # R21: the attention vectors (rows d_l, d_l + 1) follow the output units
+            rows = np.concatenate([rows, [dims[l], dims[l] + 1]])
         out.append((rows, blocks[l + 1][i]))
     return out
 
@@ -162,9 +167,14 @@ def aggregate_delta_sum(theta, subs_start, subs_end, all_index_sets):
     return out
 
 
+def weight_rows(arch: str, d: int) -> int:
+    """Logical rows of Theta_l for input width d: GCN d, GraphSAGE 2d (R2), GAT d + 2 (R21)."""
+    return 2 * d if arch == "sage" else (d + 2 if arch == "gat" else d)
+
+
 def coverage_fraction(dims, blocks, l: int, m: int, arch: str = "gcn") -> float:
     """Fraction of Theta_l entries inside the union of the m diagonal blocks."""
-    rows = dims[l] * (2 if arch == "sage" else 1)
+    rows = weight_rows(arch, dims[l])
     mask = np.zeros((rows, dims[l + 1]), dtype=bool)
     for i in range(m):
         r, c = sub_index_sets(arch, dims, blocks, i)[l]
@@ -181,8 +191,7 @@ def sub_param_count(arch: str, dims, m: int, i: int = 0) -> int:
             return dims[l]
         base, extra = divmod(dims[l], m)
         return base + (1 if i < extra else 0)
-    f = 2 if arch == "sage" else 1
-    return sum(f * size(l) * size(l + 1) for l in range(L))
+    return sum(weight_rows(arch, size(l)) * size(l + 1) for l in range(L))
 
 
 # ---------------------------------------------------------------------------
@@ -192,9 +201,10 @@ def sub_param_count(arch: str, dims, m: int, i: int = 0) -> int:
 def glorot_init(arch: str, dims: list[int], seed: int) -> list[np.ndarray]:
     theta = []
     for l in range(len(dims) - 1):
-        rows = dims[l] * (2 if arch == "sage" else 1)
+        rows = weight_rows(arch, dims[l])
         cols = dims[l + 1]
-        s = np.sqrt(np.float32(6.0) / np.float32(rows + cols), dtype=np.float32)
+        fan_in = dims[l] if arch == "gat" else rows       # R21: GAT fan_in = d_l
+        s = np.sqrt(np.float32(6.0) / np.float32(fan_in + cols), dtype=np.float32)
         flat = np.arange(rows * cols, dtype=np.uint64)
         ctr = np.stack([flat & MASK32, np.full_like(flat, l), flat >> np.uint64(32),
                         np.full_like(flat, PURPOSE_INIT)], axis=1)
@@ -210,9 +220,10 @@ def glorot_block(arch: str, dims: list[int], seed: int, l: int, rows: np.ndarray
     """Theta_l[rows, cols] of glorot_init without materialising Theta_l: every entry is a
     function of its own counter (flat index, l, 0, PURPOSE_INIT) only (R11).  Used for
     full-size parity checks; pinned against glorot_init in tests/test_oracle_model.py."""
-    nrows = dims[l] * (2 if arch == "sage" else 1)
+    nrows = weight_rows(arch, dims[l])
     ncols = dims[l + 1]
-    s = np.sqrt(np.float32(6.0) / np.float32(nrows + ncols), dtype=np.float32)
+    fan_in = dims[l] if arch == "gat" else nrows
+    s = np.sqrt(np.float32(6.0) / np.float32(fan_in + ncols), dtype=np.float32)
     r = np.asarray(rows, dtype=np.uint64)[:, None]
     c = np.asarray(cols, dtype=np.uint64)[None, :]
     flat = (r * np.uint64(ncols) + c).ravel()
@@ -295,6 +306,31 @@ def sage_operator(row_ptr, col_idx, n) -> sp.csr_matrix:
     return (sp.diags(inv) @ A).tocsr()
 
 
+def gat_structure(row_ptr, col_idx, n) -> sp.csr_matrix:
+    """GAT attends over N(i) and i itself (R21): the 0/1 pattern of A + I."""
+    S = (_adjacency(row_ptr, col_idx, n) + sp.identity(n, format="csr")).tocsr()
+    S.data[:] = 1.0
+    S.sort_indices()
+    return S
+
+
+def gat_attention(S: sp.csr_matrix, Z: np.ndarray, a_src: np.ndarray, a_dst: np.ndarray, slope: float = 0.2):
+    """Attention of one GAT layer (Velickovic et al., R21): s = Z a_src, t = Z a_dst,
+    e_ij = LeakyReLU(t_i + s_j) on the pattern S, alpha_ij = softmax_j(e_ij) per row.
+    Returns (alpha as a CSR matrix with S's pattern, pre-activation e per stored entry)."""
+    s = Z @ a_src
+    t = Z @ a_dst
+    rows = np.repeat(np.arange(S.shape[0]), np.diff(S.indptr))
+    pre = t[rows] + s[S.indices]
+    e = np.where(pre > 0, pre, slope * pre)
+    alpha = np.empty_like(e)
+    for i in range(S.shape[0]):
+        a, b = S.indptr[i], S.indptr[i + 1]
+        x = np.exp(e[a:b] - e[a:b].max())
+        alpha[a:b] = x / x.sum()
+    return sp.csr_matrix((alpha, S.indices.copy(), S.indptr.copy()), shape=S.shape), pre
+
+
 def spmm(op: sp.csr_matrix, H: np.ndarray) -> np.ndarray:
     """Sparse (n x n) times dense (n x w), FP64 (library primitive)."""
     return np.asarray(op @ H)
@@ -311,11 +347,17 @@ def forward(arch: str, theta: list[np.ndarray], op: sp.csr_matrix, X: np.ndarray
     agg, Z = [], []
     L = len(theta)
     for l in range(L):
-        if arch == "gcn":
+        if arch == "gat":                               # R21: out = alpha(Z) Z, Z = H W
+            d = H[l].shape[1]
+            C = H[l] @ theta[l][:d]
+            alpha, _ = gat_attention(op, C, theta[l][d], theta[l][d + 1])
+            z = spmm(alpha, C)
+        elif arch == "gcn":
             C = spmm(op, H[l])                          # A_bar H_l
+            z = C @ theta[l]
         else:
             C = np.concatenate([H[l], spmm(op, H[l])], axis=1)   # [H_l || N H_l]
-        z = C @ theta[l]
+            z = C @ theta[l]
         agg.append(C)
         Z.append(z)
         if l < L - 1:
@@ -331,6 +373,27 @@ def backward(arch: str, theta, op: sp.csr_matrix, tape: dict, dlogits: np.ndarra
     G = np.asarray(dlogits, dtype=np.float64)            # dL/dZ_{L-1}
     opT = op.T.tocsr()
     for l in range(L - 1, -1, -1):
+        if arch == "gat":                                  # R21, chain rule through the attention
+            H_l, Zl = tape["H"][l], tape["C"][l]
+            d = H_l.shape[1]
+            a_src, a_dst = theta[l][d], theta[l][d + 1]
+            alpha, pre = gat_attention(op, Zl, a_src, a_dst)
+            rows = np.repeat(np.arange(op.shape[0]), np.diff(op.indptr))
+            cols = op.indices
+            dZ = spmm(alpha.T.tocsr(), G)                  # through out_i = sum_j alpha_ij Z_j
+            dal = np.einsum("ek,ek->e", G[rows], Zl[cols])  # d alpha_ij = G_i . Z_j
+            Srow = np.bincount(rows, weights=alpha.data * dal, minlength=op.shape[0])
+            de = alpha.data * (dal - Srow[rows])           # softmax backward
+            dpre = de * np.where(pre > 0, 1.0, 0.2)        # LeakyReLU backward
+            dt = np.bincount(rows, weights=dpre, minlength=op.shape[0])
+            ds = np.bincount(cols, weights=dpre, minlength=op.shape[0])
+            dZ = dZ + np.outer(ds, a_src) + np.outer(dt, a_dst)
+            grads[l] = np.vstack([H_l.T @ dZ, (Zl.T @ ds)[None, :], (Zl.T @ dt)[None, :]])
+            if l == 0:
+                break
+            dH = dZ @ theta[l][:d].T
+            G = dH * (tape["Z"][l - 1] > 0.0)
+            continue
         grads[l] = tape["C"][l].T @ G                      # dTheta_l = C_l^T G
         if l == 0:
             break
@@ -399,7 +462,7 @@ def lr_step_schedule(base_lr: float, epoch: int, total: int) -> float:
 # ---------------------------------------------------------------------------
 @dataclass
 class OracleGIST:
-    arch: str                    # "gcn" or "sage"
+    arch: str                    # "gcn", "sage" or "gat" (R21)
     dims: list
     optimizer: str = "adam"      # "adam" or "sgd"
     clusters_per_batch: int = 1  # q
@@ -469,6 +532,8 @@ class OracleGIST:
         return nodes, rp, ci
 
     def operator(self, rp, ci, n):
+        if self.arch == "gat":
+            return gat_structure(rp, ci, n)
         return gcn_operator(rp, ci, n) if self.arch == "gcn" else sage_operator(rp, ci, n)
 
     def train_step(self, slot: int, step: int, lr: float) -> float:
@@ -500,12 +565,25 @@ class OracleGIST:
     # subAgg
     def aggregate(self):
         aggregate(self.theta, self.sub, self.index_sets)
+        if self.arch == "gat":   # R21: the output layer's attention rows are shared by all m sub-GCNs
+            self._mean_shared_rows(self.theta, self.sub)
         if self.opt_state == "persistent" and self.optimizer == "adam":  # f3: moments written back too
             aggregate(self.mom, [[st["m"] for st in o] for o in self.opt], self.index_sets)
             aggregate(self.vel, [[st["v"] for st in o] for o in self.opt], self.index_sets)
+            if self.arch == "gat":
+                self._mean_shared_rows(self.mom, [[st["m"] for st in o] for o in self.opt])
+                self._mean_shared_rows(self.vel, [[st["v"] for st in o] for o in self.opt])
             self.t_global = self.opt[0][0].get("t", self.t_global)
         self.round += 1
         self.sub = None
+
+    def _mean_shared_rows(self, theta, subs):
+        """GAT (R21): the class dimension d_L is not partitioned, so the attention vectors of
+        the last layer (its rows d_{L-1}, d_{L-1} + 1) are trained by every sub-GCN; subAgg sets
+        them to the mean of the m trained copies (replacement stays for every disjoint entry)."""
+        L = len(self.dims) - 1
+        d = self.dims[L - 1]
+        theta[L - 1][d:d + 2] = np.mean([sub[L - 1][-2:] for sub in subs], axis=0)
 
     def eval(self, split_code: int):
         """Forward of the global model on the full graph (R10: no output scaling)."""

@@ -1052,7 +1052,9 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
       tiles += cdiv(ops[i].M, BM) * cdiv(ops[i].N, P->bn);
       kmin = ops[i].K < kmin ? ops[i].K : kmin;
     }
-    P->pair = pair_enabled() && tiles >= 4 * (int64_t)num_sms() && kmin >= 2048;
+    static const int64_t kmin_pair = [] { const char* e = std::getenv("GIST_PAIR_KMIN"); return e ? atoll(e) : 2048; }();
+    static const int64_t tiles_pair = [] { const char* e = std::getenv("GIST_PAIR_TILES"); return e ? atoll(e) : 4; }();
+    P->pair = pair_enabled() && tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
   }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
