@@ -54,7 +54,9 @@ typedef enum {
   GIST_E_UNSUPPORTED = -7  /* no sm_100 device / feature not built */
 } gist_status;
 
-enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1 };      /* Eq. (1); GraphSAGE-mean PAPER.md:246 (R2) */
+/* Eq. (1); GraphSAGE-mean PAPER.md:246 (R2); GAT PAPER.md:204, 632 (R21: single
+ * head, Theta_l = [W; a_src^T; a_dst^T] with logical rows d_l + 2, self loops added, ReLU hidden) */
+enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1, GIST_ARCH_GAT = 2 };
 enum { GIST_OPT_SGD = 0, GIST_OPT_ADAM = 1 };        /* subTrain = SGD step PAPER.md:168; Adam PAPER.md:660,680,690 */
 enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1 };     /* FP32 parity mode / BF16 tensor-core mode (R13) */
 enum { GIST_GRAPH_DEVICE = 0, GIST_GRAPH_HOST = 1 }; /* graph resident in HBM / in pinned host memory (streamed per step) */
@@ -157,8 +159,9 @@ gist_status gist_eval_parts(gist_ctx* ctx, int32_t split_code, const int32_t* pa
                             int64_t max_rows, float* loss, float* acc, float* part_loss, float* part_acc);
 
 /* ---------------- inspection / parity hooks ---------------- */
-/* Global Theta_l, logical row-major: rows = d_l (GCN) or 2*d_l (SAGE: self rows then
- * neighbour rows), cols = d_{l+1}.  out / in: float[rows*cols]. */
+/* Global Theta_l, logical row-major: rows = d_l (GCN), 2*d_l (SAGE: self rows then
+ * neighbour rows) or d_l + 2 (GAT: W rows, then a_src, a_dst), cols = d_{l+1}.
+ * out / in: float[rows*cols]. */
 gist_status gist_get_params(gist_ctx* ctx, int32_t layer, float* out);
 gist_status gist_set_params(gist_ctx* ctx, int32_t layer, const float* in);
 

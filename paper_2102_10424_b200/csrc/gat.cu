@@ -1,0 +1,383 @@
+// gat.cu -- GAT sub-GCN layer kernels (reading R21).
+//
+// One single-head GAT layer on a batch (or full / partition) CSR without self loops:
+//   Z = H W (tcgen05 / SIMT GEMM, outside), s = Z a_src, t = Z a_dst          (k_gat_scores)
+//   e_ij = LeakyReLU(t_i + s_j), j in N(i) u {i}; alpha = row softmax;
+//   out_i = sum_j alpha_ij Z_j, ReLU on hidden layers                          (k_gat_fwd)
+// Backward, with G = dL/dout (ReLU mask of the next layer's input applied on read):
+//   S_i = sum_j alpha_ij (G_i . Z_j),  dt_i = sum_j alpha_ij slope_ij (G_i . Z_j - S_i)  (k_gat_bwd_rows)
+//   dZ_j = sum_i alpha_ij G_i + ds_j a_src + dt_j a_dst,
+//   ds_j = sum_i alpha_ij slope_ij (G_i . Z_j - S_i)      over i in N(j) u {j}   (k_gat_bwd_cols)
+// (the adjacency is symmetric, so the column pass walks row j's own neighbour list and
+// recomputes alpha_ij from the per-node scalars t_i, s_j, lse_i: no atomics, no transpose);
+//   d a_src = Z^T ds, d a_dst = Z^T dt                                          (k_gat_da)
+// One warp per row; a lane holds 4 consecutive columns of each 128-column chunk (NV chunks).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gist {
+namespace {
+
+constexpr float kSlope = 0.2f;  // LeakyReLU negative slope (GAT)
+
+__device__ __forceinline__ void ld4(const float* p, float* v) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+__device__ __forceinline__ void ld4(const bf16* p, float* v) {
+  const uint2 x = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&x.y));
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+__device__ __forceinline__ void st4(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void st4(bf16* p, const float* v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 x;
+  x.x = *reinterpret_cast<uint32_t*>(&a);
+  x.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = x;
+}
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ float lrelu(float x) { return x > 0.f ? x : kSlope * x; }
+
+// G_i (masked by mask_i > 0 when a mask is given) into registers; columns >= w read as 0
+template <typename T, int NV, typename TM = T>
+__device__ __forceinline__ void load_row(const T* base, int64_t ld, int64_t r, int64_t w, int lane, float (&x)[NV][4],
+                                         const TM* mask = nullptr, int64_t ldm = 0) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t c = (int64_t)k * 128 + lane * 4;
+    if (c < w) {
+      ld4(base + r * ld + c, x[k]);
+      if (mask) {
+        float m[4];
+        ld4(mask + r * ldm + c, m);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[k][q] = m[q] > 0.f ? x[k][q] : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[k][q] = 0.f;
+    }
+  }
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_scores(const __grid_constant__ GatLayer<T> a) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.rows) return;
+  float z[NV][4];
+  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+  float ps = 0.f, pt = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t c = (int64_t)k * 128 + lane * 4;
+    if (c < a.w)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps += z[k][q] * a.a_src[c + q], pt += z[k][q] * a.a_dst[c + q];
+  }
+  ps = warp_sum(ps);
+  pt = warp_sum(pt);
+  if (lane == 0) a.s[v] = ps, a.t[v] = pt;
+}
+
+// wa[k] = W32[k, :] . a_src, wa[kw + k] = W32[k, :] . a_dst (fp32; one warp per row of W)
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_wa(const __grid_constant__ GatLayer<T> a) {
+  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= a.kw) return;
+  float x[NV][4];
+  load_row<float, NV>(a.W32, a.ldw, k, a.w, lane, x);
+  float ps = 0.f, pt = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int64_t c = (int64_t)j * 128 + lane * 4;
+    if (c < a.w)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps += x[j][q] * a.a_src[c + q], pt += x[j][q] * a.a_dst[c + q];
+  }
+  ps = warp_sum(ps);
+  pt = warp_sum(pt);
+  if (lane == 0) a.wa[k] = ps, a.wa[a.kw + k] = pt;
+}
+
+// s[v] = H[v, :] . wa[0:kw], t[v] = H[v, :] . wa[kw:2kw]
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_scores_h(const __grid_constant__ GatLayer<T> a) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.rows) return;
+  float h[NV][4];
+  load_row<T, NV>(a.H, a.ldh, v, a.kw, lane, h);
+  float ps = 0.f, pt = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int64_t c = (int64_t)j * 128 + lane * 4;
+    if (c < a.kw)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps += h[j][q] * a.wa[c + q], pt += h[j][q] * a.wa[a.kw + c + q];
+  }
+  ps = warp_sum(ps);
+  pt = warp_sum(pt);
+  if (lane == 0) a.s[v] = ps, a.t[v] = pt;
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLayer<T> a) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.rows) return;
+  const int64_t beg = a.row_beg[v], end = a.row_end[v];  // dummy batch rows: beg = end = -1 (self only)
+  const float tv = a.t[v];
+  float acc[NV][4];
+  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, acc);  // self loop first: m = e_vv, l = 1
+  float m = lrelu(tv + a.s[v]), l = 1.f;
+  for (int64_t b0 = beg; b0 < end; b0 += 32) {
+    const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
+    int32_t u = 0;
+    float su = 0.f;
+    if (lane < n) u = a.col[b0 + lane], su = a.s[u];
+    for (int jj = 0; jj < n; ++jj) {
+      const int32_t uj = __shfl_sync(0xffffffffu, u, jj);
+      const float e = lrelu(tv + __shfl_sync(0xffffffffu, su, jj));
+      float z[NV][4];
+      load_row<float, NV>(a.Z, a.ldz, uj, a.w, lane, z);
+      if (e > m) {  // online softmax: rescale the running sum (warp-uniform branch)
+        const float sc = expf(m - e);
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[k][q] = acc[k][q] * sc + z[k][q];
+        l = l * sc + 1.f;
+        m = e;
+      } else {
+        const float p = expf(e - m);
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[k][q] += p * z[k][q];
+        l += p;
+      }
+    }
+  }
+  const float inv = 1.f / l;
+  if (lane == 0) a.lse[v] = m + logf(l);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t c = (int64_t)k * 128 + lane * 4;
+    if (c >= a.w) continue;
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = a.relu ? fmaxf(acc[k][q] * inv, 0.f) : acc[k][q] * inv;
+    if (a.out_f32) st4(a.out_f32 + v * a.ldo + c, o);
+    else st4(a.out + v * a.ldo + c, o);
+  }
+}
+
+// per row i: S_i and dt_i (see the file header)
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ GatLayer<T> a) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.rows) return;
+  const int64_t beg = a.row_beg[v], end = a.row_end[v];
+  const float tv = a.t[v], lv = a.lse[v];
+  float g[NV][4];
+  load_row<float, NV, T>(a.G, a.ldg, v, a.w, lane, g, a.mask, a.ldm);
+  float S = 0.f, U = 0.f, V = 0.f;
+  auto edge = [&](int64_t u, float su) {
+    float z[NV][4];
+    load_row<float, NV>(a.Z, a.ldz, u, a.w, lane, z);
+    float d = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d += g[k][q] * z[k][q];
+    d = warp_sum(d);
+    const float pre = tv + su;
+    const float al = expf(lrelu(pre) - lv);
+    const float sl = pre > 0.f ? 1.f : kSlope;
+    S += al * d;
+    U += al * d * sl;
+    V += al * sl;
+  };
+  edge(v, a.s[v]);
+  for (int64_t b0 = beg; b0 < end; b0 += 32) {
+    const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
+    int32_t u = 0;
+    float su = 0.f;
+    if (lane < n) u = a.col[b0 + lane], su = a.s[u];
+    for (int jj = 0; jj < n; ++jj) edge(__shfl_sync(0xffffffffu, u, jj), __shfl_sync(0xffffffffu, su, jj));
+  }
+  if (lane == 0) a.Srow[v] = S, a.dt[v] = U - S * V;
+}
+
+// per row j: dZ_j and ds_j (see the file header)
+template <typename T, int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ GatLayer<T> a) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.rows) return;
+  const int64_t beg = a.row_beg[v], end = a.row_end[v];
+  const float sv = a.s[v];
+  float z[NV][4], acc[NV][4];
+  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[k][q] = 0.f;
+  float ds = 0.f;
+  auto edge = [&](int64_t i, float ti, float li, float Si) {
+    float g[NV][4];
+    load_row<float, NV, T>(a.G, a.ldg, i, a.w, lane, g, a.mask, a.ldm);
+    const float pre = ti + sv;
+    const float al = expf(lrelu(pre) - li);
+    float d = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) d += g[k][q] * z[k][q], acc[k][q] += al * g[k][q];
+    d = warp_sum(d);
+    ds += al * (d - Si) * (pre > 0.f ? 1.f : kSlope);
+  };
+  edge(v, a.t[v], a.lse[v], a.Srow[v]);
+  for (int64_t b0 = beg; b0 < end; b0 += 32) {
+    const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
+    int32_t u = 0;
+    float tu = 0.f, lu = 0.f, Su = 0.f;
+    if (lane < n) u = a.col[b0 + lane], tu = a.t[u], lu = a.lse[u], Su = a.Srow[u];
+    for (int jj = 0; jj < n; ++jj)
+      edge(__shfl_sync(0xffffffffu, u, jj), __shfl_sync(0xffffffffu, tu, jj), __shfl_sync(0xffffffffu, lu, jj),
+           __shfl_sync(0xffffffffu, Su, jj));
+  }
+  const float dtv = a.dt[v];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t c = (int64_t)k * 128 + lane * 4;
+    if (c >= a.w) continue;
+    float o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = acc[k][q] + ds * a.a_src[c + q] + dtv * a.a_dst[c + q];
+    st4(a.dZ + v * a.ldd + c, o);
+  }
+  if (lane == 0) a.ds[v] = ds;
+}
+
+// d a_src[c] = sum_r ds[r] Z[r, c], d a_dst[c] = sum_r dt[r] Z[r, c]: one thread per column,
+// rows in order (deterministic); written into the fp32 gradient rows of the sub weight
+template <typename T>
+__global__ void __launch_bounds__(128) k_gat_da(const __grid_constant__ GatLayer<T> a) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.w) return;
+  float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f;
+  int64_t r = 0;
+  for (; r + 1 < a.rows; r += 2) {
+    const float z0 = a.Z[r * a.ldz + c], z1 = a.Z[(r + 1) * a.ldz + c];
+    x0 += a.ds[r] * z0, y0 += a.dt[r] * z0;
+    x1 += a.ds[r + 1] * z1, y1 += a.dt[r + 1] * z1;
+  }
+  if (r < a.rows) {
+    const float z0 = a.Z[r * a.ldz + c];
+    x0 += a.ds[r] * z0, y0 += a.dt[r] * z0;
+  }
+  a.da_src[c] = x0 + x1;
+  a.da_dst[c] = y0 + y1;
+}
+
+}  // namespace
+
+#define GAT_DISPATCH(KERNEL)                                                                    \
+  do {                                                                                          \
+    if (a.rows <= 0) return;                                                                    \
+    const dim3 grid((unsigned)cdiv(a.rows, 8));                                                 \
+    if (a.w <= 128) KERNEL<T, 1><<<grid, 256, 0, s>>>(a);                                       \
+    else if (a.w <= 256) KERNEL<T, 2><<<grid, 256, 0, s>>>(a);                                  \
+    else if (a.w <= 512) KERNEL<T, 4><<<grid, 256, 0, s>>>(a);                                  \
+    else if (a.w <= 1024) KERNEL<T, 8><<<grid, 256, 0, s>>>(a);                                 \
+    else KERNEL<T, 16><<<grid, 256, 0, s>>>(a);                                                 \
+  } while (0)
+
+template <typename T>
+void gat_scores(const GatLayer<T>& a, cudaStream_t s) {
+  if (!a.H) {
+    GAT_DISPATCH(k_gat_scores);
+    return;
+  }
+  if (a.rows <= 0) return;
+  const dim3 gk((unsigned)cdiv(a.kw, 8)), gr((unsigned)cdiv(a.rows, 8));
+  if (a.w <= 128) k_gat_wa<T, 1><<<gk, 256, 0, s>>>(a);
+  else if (a.w <= 256) k_gat_wa<T, 2><<<gk, 256, 0, s>>>(a);
+  else if (a.w <= 512) k_gat_wa<T, 4><<<gk, 256, 0, s>>>(a);
+  else if (a.w <= 1024) k_gat_wa<T, 8><<<gk, 256, 0, s>>>(a);
+  else k_gat_wa<T, 16><<<gk, 256, 0, s>>>(a);
+  if (a.kw <= 128) k_gat_scores_h<T, 1><<<gr, 256, 0, s>>>(a);
+  else if (a.kw <= 256) k_gat_scores_h<T, 2><<<gr, 256, 0, s>>>(a);
+  else if (a.kw <= 512) k_gat_scores_h<T, 4><<<gr, 256, 0, s>>>(a);
+  else if (a.kw <= 1024) k_gat_scores_h<T, 8><<<gr, 256, 0, s>>>(a);
+  else k_gat_scores_h<T, 16><<<gr, 256, 0, s>>>(a);
+}
+template <typename T>
+void gat_forward(const GatLayer<T>& a, cudaStream_t s) { GAT_DISPATCH(k_gat_fwd); }
+template <typename T>
+void gat_backward(const GatLayer<T>& a, cudaStream_t s) {
+  GAT_DISPATCH(k_gat_bwd_rows);
+  GAT_DISPATCH(k_gat_bwd_cols);
+  k_gat_da<T><<<(unsigned)cdiv(a.w, 128), 128, 0, s>>>(a);
+}
+#undef GAT_DISPATCH
+
+// dst[r, :] = src[idx[r], :] (T rows, 16-byte vectors; ld multiples of 8 elements)
+template <typename T>
+__global__ void k_gather_t(const T* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx, int64_t rows,
+                           int64_t vecs, T* __restrict__ dst, int64_t ldd) {
+  const int64_t r = blockIdx.y + (int64_t)blockIdx.z * 65535;
+  if (r >= rows) return;
+  const uint4* s = reinterpret_cast<const uint4*>(src + (int64_t)idx[r] * lds);
+  uint4* d = reinterpret_cast<uint4*>(dst + r * ldd);
+  for (int64_t i = threadIdx.x; i < vecs; i += blockDim.x) d[i] = s[i];
+}
+template <typename T>
+void gather_rows_t(const T* src, int64_t lds, const int32_t* idx, int64_t rows, int64_t w, T* dst, int64_t ldd,
+                   cudaStream_t s) {
+  if (rows <= 0) return;
+  const int64_t vecs = w / Elem<T>::kVec;
+  const dim3 grid(1, (unsigned)std::min<int64_t>(rows, 65535), (unsigned)cdiv(rows, 65535));
+  k_gather_t<T><<<grid, 128, 0, s>>>(src, lds, idx, rows, vecs, dst, ldd);
+}
+
+// dst[c] = mean over k of srcs[k][c] (sum in slot order, then / n): the last GAT layer's
+// shared attention rows at subAgg (R21)
+__global__ void k_mean_rows(float* __restrict__ dst, const __grid_constant__ MeanRows m) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.cols) return;
+  const int r = blockIdx.y;
+  float acc = 0.f;
+  for (int k = 0; k < m.n; ++k) acc += m.src[k][(int64_t)r * m.ld_src[k] + c];
+  dst[(int64_t)r * m.ld_dst + c] = acc / (float)m.n;
+}
+void mean_rows(float* dst, const MeanRows& m, int rows, cudaStream_t s) {
+  if (m.n <= 0 || m.cols <= 0 || rows <= 0) return;
+  k_mean_rows<<<dim3((unsigned)cdiv(m.cols, 128), (unsigned)rows), 128, 0, s>>>(dst, m);
+}
+
+template void gat_scores<float>(const GatLayer<float>&, cudaStream_t);
+template void gat_scores<bf16>(const GatLayer<bf16>&, cudaStream_t);
+template void gat_forward<float>(const GatLayer<float>&, cudaStream_t);
+template void gat_forward<bf16>(const GatLayer<bf16>&, cudaStream_t);
+template void gat_backward<float>(const GatLayer<float>&, cudaStream_t);
+template void gat_backward<bf16>(const GatLayer<bf16>&, cudaStream_t);
+template void gather_rows_t<float>(const float*, int64_t, const int32_t*, int64_t, int64_t, float*, int64_t,
+                                   cudaStream_t);
+template void gather_rows_t<bf16>(const bf16*, int64_t, const int32_t*, int64_t, int64_t, bf16*, int64_t,
+                                  cudaStream_t);
+
+}  // namespace gist

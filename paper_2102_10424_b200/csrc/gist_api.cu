@@ -71,6 +71,11 @@ struct Slot {
   // DZs = dZ / deg (block-diagonal path)
   void *rP = nullptr, *rAGG = nullptr, *rDQ = nullptr, *rDZs = nullptr;
   void* rWc = nullptr;  // [W_top | W_bot] of the last layer, half x 2Np bf16 (refreshed every step)
+  // GAT (R21): Z_l = H_l W_l per layer, per-row scalars [s | t | lse | S | dt | ds] (6 x nb_max),
+  // and the backward operand G (dlogits, then dH_l of each layer)
+  std::vector<void*> gZ;
+  std::vector<float*> gsc;
+  void* gG = nullptr;
   int last_nb = 0;
 };
 
@@ -89,6 +94,7 @@ struct StepPlan {
     std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
     std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
     CeGroup<T> ce;
+    CeGroup<float> ce_f;  // GAT: fp32 dlogits in both modes
     // re-associated last layer: Z = H W_top + N (H W_bot); backward via Q = N^T dZ
     bool reassoc = false;
     GemmPlanTC ra_p, ra_z, ra_dw, ra_dh;
@@ -402,7 +408,7 @@ extern "C" gist_status gist_nccl_unique_id(void* out128) {
 extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (!cfg || !out || !cfg->dims || cfg->num_layers < 1) return GIST_E_ARG;
   *out = nullptr;
-  if (cfg->arch != GIST_ARCH_GCN && cfg->arch != GIST_ARCH_SAGE) return GIST_E_ARG;
+  if (cfg->arch != GIST_ARCH_GCN && cfg->arch != GIST_ARCH_SAGE && cfg->arch != GIST_ARCH_GAT) return GIST_E_ARG;
   if (cfg->optimizer != GIST_OPT_SGD && cfg->optimizer != GIST_OPT_ADAM) return GIST_E_ARG;
   if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
   if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
@@ -465,6 +471,16 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   *out = c;
   return GIST_OK;
 }
+
+// Logical rows of Theta_l for input width d (GCN d, GraphSAGE 2d (R2), GAT d + 2 (R21)) and the
+// physical rows (second block at pad8(d): SAGE neighbour rows, GAT the two attention rows)
+static int wrows(const gist_ctx* c, int d) {
+  return c->arch == GIST_ARCH_SAGE ? 2 * d : (c->arch == GIST_ARCH_GAT ? d + 2 : d);
+}
+static int64_t kphys(const gist_ctx* c, int64_t d) {
+  return c->arch == GIST_ARCH_SAGE ? 2 * pad8(d) : (c->arch == GIST_ARCH_GAT ? pad8(d) + 8 : pad8(d));
+}
+static bool two_blocks(const gist_ctx* c) { return c->arch != GIST_ARCH_GCN; }
 
 static void free_slots(gist_ctx* c) {
   for (auto& s : c->slots)
@@ -695,7 +711,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   c->th_K.assign(c->L, 0);
   c->th_N.assign(c->L, 0);
   for (int l = 0; l < c->L; ++l) {
-    c->th_K[l] = c->arch == GIST_ARCH_SAGE ? 2 * pad8(c->dims[l]) : pad8(c->dims[l]);
+    c->th_K[l] = kphys(c, c->dims[l]);
     c->th_N[l] = pad8(c->dims[l + 1]);
     TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
     CK(cudaMemsetAsync(c->theta[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, s));
@@ -720,10 +736,11 @@ extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
   }
   c->adam_t = 0;
   for (int l = 0; l < c->L; ++l) {
-    const int rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[l] : c->dims[l];
+    const int rows = wrows(c, c->dims[l]);
     const int cols = c->dims[l + 1];
-    const float sc = std::sqrt(6.0f / (float)(rows + cols));  // fp32, correctly rounded (R11)
-    LK(glorot_init(c->theta[l], rows, cols, c->arch == GIST_ARCH_SAGE, c->dims[l], (int)pad8(c->dims[l]),
+    const int fan_in = c->arch == GIST_ARCH_GAT ? c->dims[l] : rows;  // R21: GAT fan_in = d_l
+    const float sc = std::sqrt(6.0f / (float)(fan_in + cols));  // fp32, correctly rounded (R11)
+    LK(glorot_init(c->theta[l], rows, cols, two_blocks(c), c->dims[l], (int)pad8(c->dims[l]),
                    c->th_N[l], (uint32_t)l, seed, sc, c->stream));
   }
   TRY(check_launch(c, "init_params"));
@@ -732,7 +749,7 @@ extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
 }
 
 static int64_t logical_to_phys_row(const gist_ctx* c, int l, int64_t r) {
-  if (c->arch == GIST_ARCH_SAGE && r >= c->dims[l]) return pad8(c->dims[l]) + (r - c->dims[l]);
+  if (two_blocks(c) && r >= c->dims[l]) return pad8(c->dims[l]) + (r - c->dims[l]);
   return r;
 }
 
@@ -744,7 +761,7 @@ extern "C" gist_status gist_get_params(gist_ctx* c, int32_t layer, float* out) {
   std::vector<float> buf(K * N);
   CK(cudaMemcpyAsync(buf.data(), c->theta[layer], K * N * 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  const int64_t rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[layer] : c->dims[layer];
+  const int64_t rows = wrows(c, c->dims[layer]);
   const int64_t cols = c->dims[layer + 1];
   for (int64_t r = 0; r < rows; ++r)
     std::memcpy(out + r * cols, buf.data() + logical_to_phys_row(c, layer, r) * N, cols * 4);
@@ -757,7 +774,7 @@ extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* 
   if (layer < 0 || layer >= c->L || !in) return GIST_E_ARG;
   const int64_t K = c->th_K[layer], N = c->th_N[layer];
   std::vector<float> buf(K * N, 0.f);
-  const int64_t rows = c->arch == GIST_ARCH_SAGE ? 2 * c->dims[layer] : c->dims[layer];
+  const int64_t rows = wrows(c, c->dims[layer]);
   const int64_t cols = c->dims[layer + 1];
   for (int64_t r = 0; r < rows; ++r)
     std::memcpy(buf.data() + logical_to_phys_row(c, layer, r) * N, in + r * cols, cols * 4);
@@ -785,7 +802,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
   for (int l = 0; l < c->L; ++l) {
     const int nr = (l == 0) ? c->dims[0] : hidden_block_max(c, l, m);
     const int nc = (l + 1 == c->L) ? c->dims[c->L] : hidden_block_max(c, l + 1, m);
-    maxK[l] = (int)(c->arch == GIST_ARCH_SAGE ? 2 * pad8(nr) : pad8(nr));
+    maxK[l] = (int)kphys(c, nr);
     maxN[l] = (int)pad8(nc);
     smax += (int64_t)maxK[l] * maxN[l];
   }
@@ -849,6 +866,16 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
         TRY(dalloc(c, &s.H[l], (size_t)nbm * maxK[l] * E));
         CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
       }
+      if (c->arch == GIST_ARCH_GAT) {  // H_l (layer 0: the gathered X_b rows), Z_l, scalars
+        const size_t kw = (size_t)(maxK[l] - 8);  // pad8 of the widest input slice
+        TRY(dalloc(c, &s.H[l], (size_t)nbm * kw * E));
+        CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * kw * E, c->stream));
+        s.gZ.resize(c->L, nullptr);
+        s.gsc.resize(c->L, nullptr);
+        TRY(dalloc(c, &s.gZ[l], (size_t)nbm * maxN[l] * 4));  // fp32: attention operand
+        CK(cudaMemsetAsync(s.gZ[l], 0, (size_t)nbm * maxN[l] * 4, c->stream));
+        TRY(dalloc_t(c, &s.gsc[l], (size_t)6 * nbm + 2 * kw));
+      }
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
       CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
     }
@@ -858,6 +885,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     const int last_in = c->arch == GIST_ARCH_SAGE ? maxK[c->L - 1] / 2 : maxK[c->L - 1];
     c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && last_in >= 256;
     if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && e[0] == '1';
+    if (c->arch == GIST_ARCH_GAT) c->reassoc = false;
     if (c->reassoc) {
       const size_t npl = (size_t)maxN[c->L - 1];
       TRY(dalloc(c, &s.rP, (size_t)nbm * npl * E));
@@ -869,6 +897,12 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
       CK(cudaMemsetAsync(s.rAGG, 0, (size_t)nbm * npl * E, c->stream));
       CK(cudaMemsetAsync(s.rDQ, 0, (size_t)nbm * 2 * npl * E, c->stream));
       CK(cudaMemsetAsync(s.rDZs, 0, (size_t)nbm * 2 * npl * E, c->stream));
+    }
+    if (c->arch == GIST_ARCH_GAT) {
+      int gw = 0;
+      for (int l = 0; l < c->L; ++l) gw = std::max(gw, maxN[l]);
+      TRY(dalloc(c, &s.gG, (size_t)nbm * gw * 4));  // fp32 dlogits / dH
+      CK(cudaMemsetAsync(s.gG, 0, (size_t)nbm * gw * 4, c->stream));
     }
     TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
     CK(cudaMemsetAsync(s.dC, 0, (size_t)nbm * maxKall * E, c->stream));
@@ -949,6 +983,21 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.ce.k = c->k;
     g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
     g.reassoc = c->reassoc && tc && L >= 2;
+    if (c->arch == GIST_ARCH_GAT) {  // R21: batch build and loss are grouped; the layers run per slot
+      for (int j = 0; j < g.count; ++j) {
+        Slot& sl = c->slots[g0 + j];
+        BatchSlot& b = g.batch.s[j];
+        b.desc = sl.desc_dev; b.map64 = sl.map64; b.b_nodes = sl.b_nodes; b.b_beg = sl.b_beg; b.b_end = sl.b_end;
+        b.b_col = sl.b_col; b.scale = sl.scale; b.lab_b = sl.lab_b; b.train_b = sl.train_b; b.stats = sl.stats;
+        CeSlot<float>& e = g.ce_f.s[j];
+        e.logits = sl.logits; e.dlog = (float*)sl.gG; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
+        e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
+        e.done = sl.ce_done;
+      }
+      g.ce_f.n = g.ce.n; g.ce_f.rows = g.ce.rows; g.ce_f.k = g.ce.k; g.ce_f.ld = g.ce.ld;
+      P.groups.push_back(g);
+      continue;
+    }
     for (int l = 0; l < L; ++l) {
       std::vector<GemmOp> fw, dw, dx;
       std::vector<BdOp> bfw, bbw;
@@ -1208,6 +1257,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
   PRE(c);
   if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "partition: needs params and no open round");
   if (m < 1) return fail(c, GIST_E_ARG, "partition: m < 1");
+  if (c->arch == GIST_ARCH_GAT && m > kMaxMean) return fail(c, GIST_E_ARG, "partition: GAT supports m <= 128");
   for (int l = 1; l < c->L; ++l)
     if (m > c->dims[l]) return fail(c, GIST_E_ARG, "partition: m exceeds hidden dim " + std::to_string(l));
   cudaStream_t s = c->stream;
@@ -1264,7 +1314,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
       LayerShape& sh = c->shapes[i][l];
       sub_logical(c, i, l, &sh.nrows, &sh.ncols);
       sh.half = (int)pad8(sh.nrows);
-      sh.Kp = (int)(c->arch == GIST_ARCH_SAGE ? 2 * pad8(sh.nrows) : pad8(sh.nrows));
+      sh.Kp = (int)kphys(c, sh.nrows);
       sh.Np = (int)pad8(sh.ncols);
       sh.off = off;
       off += (int64_t)sh.Kp * sh.Np;
@@ -1278,7 +1328,7 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
     for (int l = 0; l < c->L; ++l) {
       const LayerShape& sh = shp[l];
       LayerMap mp;
-      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
+      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = c->arch == GIST_ARCH_GAT; mp.half = sh.half;
       mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
       mp.ldg = c->th_N[l];
       PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta[l], mp, sl.W + sh.off, s));
@@ -1330,6 +1380,88 @@ static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp
   ++c->nk;
 }
 
+static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
+                            cudaStream_t s);
+
+// One GAT subTrain step (R21) of every slot of group g after the grouped batch build: per slot
+// and layer Z = H W (GEMM), attention scores and aggregation; the grouped softmax-CE; then per
+// slot and layer the two attention backward passes, dW = H^T dZ (plus the attention rows) and
+// dH = dZ W^T.  Dummy batch rows (v >= n_b) carry no neighbours and a zero loss gradient.
+template <typename T>
+static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, cudaStream_t s) {
+  const int L = c->L;
+  const int64_t nb = c->nb_max_rows;
+  const bool tc = c->prec == GIST_PREC_BF16;
+  auto layer_args = [&](Slot& sl, int l) {
+    const LayerShape& sh = c->shapes[sl.index][l];
+    GatLayer<T> a;
+    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb; a.w = sh.Np;
+    a.Z = (const float*)sl.gZ[l]; a.ldz = sh.Np;
+    a.a_src = sl.W + sh.off + (int64_t)sh.half * sh.Np;
+    a.a_dst = a.a_src + sh.Np;
+    float* sc = sl.gsc[l];
+    a.s = sc; a.t = sc + nb; a.lse = sc + 2 * nb; a.Srow = sc + 3 * nb; a.dt = sc + 4 * nb; a.ds = sc + 5 * nb;
+    return a;
+  };
+  for (int j = 0; j < g.count; ++j) {  // ---- a2/a3: forward
+    Slot& sl = c->slots[g.first + j];
+    const auto& shp = c->shapes[sl.index];
+    const int64_t d0p = pad8(c->dims[0]);
+    LK(gather_rows_t<T>((const T*)c->X, d0p, sl.b_nodes, nb, d0p, (T*)sl.H[0], d0p, s));
+    ++c->nk;
+    for (int l = 0; l < L; ++l) {
+      const LayerShape& sh = shp[l];
+      const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
+      int id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * nb * sh.Np * sh.half);
+      TRY(gemm_any(c, false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, true, false, s));
+      prof_end(c, s, id);
+      GatLayer<T> a = layer_args(sl, l);
+      a.H = (const T*)sl.H[l]; a.ldh = sh.half; a.kw = sh.half;  // scores = H (W a), fp32 W a
+      a.W32 = sl.W + sh.off; a.ldw = sh.Np; a.wa = sl.gsc[l] + 6 * nb;
+      if (l + 1 < L) { a.out = (T*)sl.H[l + 1]; a.ldo = shp[l + 1].half; a.relu = 1; }
+      else { a.out_f32 = sl.logits; a.ldo = sh.Np; }
+      id = prof_begin(c, s, GIST_PROF_SPMM, (double)nb * sh.Np * sizeof(T) * 3.0);
+      LK(gat_scores<T>(a, s));
+      LK(gat_forward<T>(a, s));
+      prof_end(c, s, id);
+      c->nk += 2;
+    }
+  }
+  {  // ---- a4: softmax cross-entropy (grouped), dlogits into gG
+    const int id = prof_begin(c, s, GIST_PROF_LOSS, (double)g.count * nb * (g.ce.ld * 8.0 + 17.0));
+    softmax_ce<float>(g.ce_f, s);
+    prof_end(c, s, id);
+    ++c->nk;
+  }
+  for (int j = 0; j < g.count; ++j) {  // ---- a5/a6: backward
+    Slot& sl = c->slots[g.first + j];
+    const auto& shp = c->shapes[sl.index];
+    for (int l = L - 1; l >= 0; --l) {
+      const LayerShape& sh = shp[l];
+      GatLayer<T> a = layer_args(sl, l);
+      a.G = (const float*)sl.gG; a.ldg = sh.Np;  // dlogits (last layer) or dH_{l+1} (width Np_l)
+      if (l + 1 < L) { a.mask = (const T*)sl.H[l + 1]; a.ldm = shp[l + 1].half; }
+      a.dZ = (T*)sl.dZ[l]; a.ldd = sh.Np;
+      a.da_src = sl.G + sh.off + (int64_t)sh.half * sh.Np;
+      a.da_dst = a.da_src + sh.Np;
+      int id = prof_begin(c, s, GIST_PROF_SPMM, (double)nb * sh.Np * sizeof(T) * 6.0);
+      LK(gat_backward<T>(a, s));
+      prof_end(c, s, id);
+      c->nk += 3;
+      id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * nb * sh.Np * sh.half * (l > 0 ? 2 : 1));
+      TRY(gemm_any(c, true, false, sh.half, sh.Np, nb, sl.H[l], sh.half, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true,
+                   false, s));
+      if (l > 0) {
+        const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
+        TRY(gemm_any(c, false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, true, false, s));
+      }
+      prof_end(c, s, id);
+    }
+  }
+  return GIST_OK;
+}
+
 // One subTrain step of every slot of group g, in lockstep: every
 // kernel below is one launch over all slots of the group.
 template <typename T>
@@ -1354,6 +1486,7 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
       CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
   }
+  if (c->arch == GIST_ARCH_GAT) return gat_group_step<T>(c, g, s);
   const double per_nnz = 4.0 * g.count;
   auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
     int id = -1;
@@ -1592,11 +1725,28 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
       for (int l = 0; l < c->L; ++l) {
         const LayerShape& sh = c->shapes[i][l];
         LayerMap mp;
-        mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.half = sh.half;
+        mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = c->arch == GIST_ARCH_GAT; mp.half = sh.half;
         mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
         mp.ldg = c->th_N[l];
         PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 12.0, s, scatter_sub((*pt.global)[l], mp, w + sh.off, s));
       }
+    }
+    if (c->arch == GIST_ARCH_GAT) {  // R21: the last layer's attention rows = mean of the m copies
+      const int l = c->L - 1;
+      MeanRows mr;
+      mr.n = c->m;
+      mr.cols = c->dims[c->L];
+      mr.ld_dst = c->th_N[l];
+      for (int i = 0; i < c->m; ++i) {
+        const int rank = gist_slot_owner(i, W), j = i / W;
+        const float* w = W == 1 ? pt.local + (size_t)j * c->S_max
+                                : src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
+        const LayerShape& sh = c->shapes[i][l];
+        mr.src[i] = w + sh.off + (int64_t)sh.half * sh.Np;
+        mr.ld_src[i] = sh.Np;
+      }
+      PL(GIST_PROF_AGGREGATE, 2.0 * c->m * mr.cols * 4.0, s,
+         mean_rows((*pt.global)[l] + pad8(c->dims[l]) * c->th_N[l], mr, 2, s));
     }
   }
   c->prof_now = false;
@@ -1619,6 +1769,36 @@ static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N,
   return GIST_OK;
 }
 
+// GAT forward of the global model over `rows` rows of a CSR without self loops (R21): layer 0
+// reads X0 (ld pad8(d_0)); hidden outputs alternate between bufA / bufB; fp32 logits (ld th_N).
+template <typename T>
+static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* row_beg, const int64_t* row_end,
+                                    const int32_t* col, const T* X0, const std::vector<void*>& wl, T* bufA, T* bufB,
+                                    float* Z, float* sc, float* logits, cudaStream_t s) {
+  const T* Hin = X0;
+  int64_t ldin = pad8(c->dims[0]);
+  T* Hout = bufA;
+  for (int l = 0; l < c->L; ++l) {
+    const int64_t K = pad8(c->dims[l]), N = c->th_N[l];
+    const void* Wl = sizeof(T) == 2 ? wl[l] : (const void*)c->theta[l];
+    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, Wl, N, Z, N, true, false, s));
+    GatLayer<T> a;
+    a.row_beg = row_beg; a.row_end = row_end; a.col = col; a.rows = rows; a.w = N;
+    a.Z = Z; a.ldz = N;
+    a.a_src = c->theta[l] + K * N; a.a_dst = a.a_src + N;
+    a.s = sc; a.t = sc + rows; a.lse = sc + 2 * rows;
+    a.H = Hin; a.ldh = ldin; a.kw = K; a.W32 = c->theta[l]; a.ldw = N; a.wa = sc + 3 * rows;
+    if (l + 1 < c->L) { a.out = Hout; a.ldo = N; a.relu = 1; }
+    else { a.out_f32 = logits; a.ldo = N; }
+    LK(gat_scores<T>(a, s));
+    LK(gat_forward<T>(a, s));
+    Hin = Hout;
+    ldin = N;
+    Hout = Hout == bufA ? bufB : bufA;
+  }
+  return GIST_OK;
+}
+
 // ================================================================ eval ====
 template <typename T>
 static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
@@ -1636,7 +1816,26 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
   TRY(dalloc_t(c, &out3, 3));
   T* Cb = (T*)bufA;
   T* Hn = (T*)bufB;
-  for (int l = 0; l < c->L; ++l) {
+  if (c->arch == GIST_ARCH_GAT) {
+    std::vector<void*> wl(c->L, nullptr);
+    int64_t maxN = 0;
+    for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
+    void* Z = nullptr;
+    float* sc = nullptr;
+    TRY(dalloc(c, &Z, (size_t)n * maxN * 4));
+    TRY(dalloc_t(c, &sc, (size_t)3 * std::max<int64_t>(n, 1) + 2 * maxK));
+    if (sizeof(T) == 2)
+      for (int l = 0; l < c->L; ++l) {
+        TRY(dalloc(c, &wl[l], (size_t)c->th_K[l] * c->th_N[l] * 2));
+        LK(f32_to_bf16(c->theta[l], (bf16*)wl[l], c->th_K[l] * c->th_N[l], s));
+      }
+    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, wl, Cb, Hn, (float*)Z, sc, logits, s));
+    CK(cudaStreamSynchronize(s));
+    for (void* p : wl) if (p) dfree(c, p);
+    dfree(c, Z);
+    dfree(c, sc);
+  }
+  for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {
     const int64_t K = c->th_K[l], N = c->th_N[l];
     const int64_t half = pad8(c->dims[l]);
     SpmmArgs<T, T> a;
@@ -1792,13 +1991,28 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
   TRY(dalloc(c, &bufA, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
   TRY(dalloc(c, &bufB, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
   TRY(dalloc_t(c, &logits, (size_t)std::max<int64_t>(max_chunk, 1) * Nl));
+  void *gX = nullptr, *gZ = nullptr;
+  float* gsc = nullptr;
+  if (c->arch == GIST_ARCH_GAT) {
+    int64_t maxN = 0;
+    for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
+    TRY(dalloc(c, &gX, (size_t)std::max<int64_t>(max_chunk, 1) * pad8(c->dims[0]) * sizeof(T)));
+    TRY(dalloc(c, &gZ, (size_t)std::max<int64_t>(max_chunk, 1) * maxN * 4));
+    TRY(dalloc_t(c, &gsc, (size_t)3 * std::max<int64_t>(max_chunk, 1) + 2 * maxK));
+  }
   for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
     const int f = chunk_first[j], e = chunk_first[j + 1];
     const int64_t k0 = lbeg[f], rows = lbeg[e] - k0;
     if (rows == 0) continue;
     T* Cb = (T*)bufA;
     T* Hn = (T*)bufB;
-    for (int l = 0; l < c->L; ++l) {
+    if (c->arch == GIST_ARCH_GAT) {  // X rows of the chunk gathered, then the GAT layers
+      const int64_t d0p = pad8(c->dims[0]);
+      LK(gather_rows_t<T>((const T*)c->X, d0p, pnode_d + k0, rows, d0p, (T*)gX, d0p, s));
+      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, wl, Cb, Hn, (float*)gZ, gsc, logits,
+                              s));
+    }
+    for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {
       const int64_t K = c->th_K[l], N = c->th_N[l];
       const int64_t half = pad8(c->dims[l]);
       SpmmArgs<T, T> a;
@@ -1840,6 +2054,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
     dfree(c, red);
   }
   for (void* p : wl) if (p) dfree(c, p);
+  for (void* p : {gX, gZ, (void*)gsc}) if (p) dfree(c, p);
   for (void* p : {(void*)pnode_d, (void*)pos_d, (void*)part_d, (void*)rb_d, (void*)pcol, (void*)deg, (void*)prp,
                   (void*)lbeg_d, (void*)pscale, (void*)out3, bufA, bufB, (void*)logits})
     dfree(c, p);
@@ -1892,7 +2107,7 @@ extern "C" gist_status gist_sub_shape(gist_ctx* c, int32_t slot, int32_t layer, 
   if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "sub_shape: no open round");
   if (slot < 0 || slot >= c->m || layer < 0 || layer >= c->L) return GIST_E_ARG;
   const LayerShape& sh = c->shapes[slot][layer];
-  if (rows) *rows = c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows;
+  if (rows) *rows = wrows(c, sh.nrows);
   if (cols) *cols = sh.ncols;
   return GIST_OK;
 }
@@ -1905,9 +2120,9 @@ static Slot* local_slot(gist_ctx* c, int slot) {
 
 // physical packed block -> logical row-major
 static void phys_to_logical(const gist_ctx* c, const LayerShape& sh, const std::vector<float>& buf, float* out) {
-  const int rows = c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows;
+  const int rows = wrows(c, sh.nrows);
   for (int r = 0; r < rows; ++r) {
-    const int p = (c->arch == GIST_ARCH_SAGE && r >= sh.nrows) ? sh.half + (r - sh.nrows) : r;
+    const int p = (two_blocks(c) && r >= sh.nrows) ? sh.half + (r - sh.nrows) : r;
     std::memcpy(out + (size_t)r * sh.ncols, buf.data() + (size_t)p * sh.Np, (size_t)sh.ncols * 4);
   }
 }
@@ -1963,8 +2178,9 @@ extern "C" gist_status gist_get_trace(gist_ctx* c, int32_t slot, int32_t what, i
       cnt = (int64_t)nb * sh.nrows;
       if (out) {
         const void* src = c->arch == GIST_ARCH_SAGE ? sl->C[layer] : sl->H[layer];
-        if (c->prec == GIST_PREC_BF16) copy_rows_out<bf16>(src, nb, sh.Kp, sh.nrows, (float*)out);
-        else copy_rows_out<float>(src, nb, sh.Kp, sh.nrows, (float*)out);
+        const int64_t ld = c->arch == GIST_ARCH_GAT ? sh.half : sh.Kp;
+        if (c->prec == GIST_PREC_BF16) copy_rows_out<bf16>(src, nb, ld, sh.nrows, (float*)out);
+        else copy_rows_out<float>(src, nb, ld, sh.nrows, (float*)out);
       }
       break;
     }
@@ -1977,7 +2193,7 @@ extern "C" gist_status gist_get_trace(gist_ctx* c, int32_t slot, int32_t what, i
     case GIST_TRACE_GRAD: {
       if (layer < 0 || layer >= c->L) return GIST_E_ARG;
       const LayerShape& sh = shp[layer];
-      cnt = (int64_t)(c->arch == GIST_ARCH_SAGE ? 2 * sh.nrows : sh.nrows) * sh.ncols;
+      cnt = (int64_t)wrows(c, sh.nrows) * sh.ncols;
       if (out) {
         std::vector<float> buf((size_t)sh.Kp * sh.Np);
         CK(cudaMemcpy(buf.data(), sl->G + sh.off, buf.size() * 4, cudaMemcpyDeviceToHost));

@@ -315,6 +315,7 @@ struct LayerMap {
   const int32_t* rows = nullptr;  // sub row units (nullptr: identity)
   int nrows = 0;                  // logical rows of the sub block (self block for SAGE)
   int sage = 0;
+  int gat = 0;                    // GAT (R21): the second block is the two attention rows
   int half = 0;                   // physical offset of the neighbour block in the sub weight (SAGE)
   int glob_half = 0;              // physical offset of the neighbour block in the global weight (SAGE)
   const int32_t* cols = nullptr;  // sub column units (nullptr: identity)
@@ -336,5 +337,56 @@ void eval_rows(const float* logits, int64_t ld, int64_t n, int k, const int32_t*
 void eval_parts(const float* logits, int64_t ld, int k, const int64_t* pbeg, int64_t k0, int nparts,
                 const int32_t* pnode,
                 const int32_t* labels, const uint8_t* split, int code, double* out3, cudaStream_t s);
+
+// --------------------------------------------------------------------------
+// GAT sub-GCN layer (reading R21; gat.cu).  CSR without self loops (the self
+// loop is added by the kernels); dummy batch rows have row_beg = row_end = -1.
+// --------------------------------------------------------------------------
+template <typename T>
+struct GatLayer {
+  const int64_t* row_beg = nullptr;
+  const int64_t* row_end = nullptr;
+  const int32_t* col = nullptr;
+  int64_t rows = 0, w = 0;            // rows; padded width (multiple of 8)
+  const float* Z = nullptr;           // Z = H W (rows x w), fp32 in both modes (attention operand)
+  int64_t ldz = 0;
+  const float* a_src = nullptr;       // attention vectors (fp32 master rows of the weight)
+  const float* a_dst = nullptr;
+  float *s = nullptr, *t = nullptr, *lse = nullptr;  // per-row scores / log-sum-exp (forward)
+  float *Srow = nullptr, *dt = nullptr, *ds = nullptr;  // backward per-row scalars
+  T* out = nullptr;                   // forward output (hidden, ReLU if relu) ...
+  float* out_f32 = nullptr;           // ... or fp32 logits
+  int64_t ldo = 0;
+  int relu = 0;
+  const float* G = nullptr;           // backward: dL/dout, fp32 (masked by mask > 0 if mask)
+  int64_t ldg = 0;
+  const T* mask = nullptr;
+  int64_t ldm = 0;
+  T* dZ = nullptr;                    // backward output dL/dZ
+  int64_t ldd = 0;
+  float *da_src = nullptr, *da_dst = nullptr;  // backward output: gradient rows of a_src / a_dst
+  // scores re-associated as s = H (W a_src), t = H (W a_dst) (fp32 W a from the fp32 master W), so
+  // they do not inherit the rounding of a bf16 Z: layer input H (ld ldh, width kw = padded rows of
+  // W), W32 (kw x w, ld ldw) and a 2*kw scratch for [W a_src | W a_dst].  H == nullptr: s = Z a_src.
+  const T* H = nullptr;
+  int64_t ldh = 0, kw = 0;
+  const float* W32 = nullptr;
+  int64_t ldw = 0;
+  float* wa = nullptr;
+};
+template <typename T> void gat_scores(const GatLayer<T>& a, cudaStream_t s);
+template <typename T> void gat_forward(const GatLayer<T>& a, cudaStream_t s);
+template <typename T> void gat_backward(const GatLayer<T>& a, cudaStream_t s);
+template <typename T>
+void gather_rows_t(const T* src, int64_t lds, const int32_t* idx, int64_t rows, int64_t w, T* dst, int64_t ldd,
+                   cudaStream_t s);
+constexpr int kMaxMean = 128;
+struct MeanRows {
+  const float* src[kMaxMean];
+  int64_t ld_src[kMaxMean];
+  int n = 0, cols = 0;
+  int64_t ld_dst = 0;
+};
+void mean_rows(float* dst, const MeanRows& m, int rows, cudaStream_t s);
 
 }  // namespace gist

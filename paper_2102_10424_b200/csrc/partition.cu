@@ -69,6 +69,11 @@ void partition_compact(const int32_t* blk, int d, int m, const int32_t* offs, in
 
 // physical row of the global weight for sub-weight physical row p (-1 = padding)
 __device__ __forceinline__ int64_t glob_row(const LayerMap& m, int p) {
+  if (m.gat) {  // R21: rows D_l^(i), then the two attention rows (global rows glob_half, glob_half + 1)
+    if (p < m.nrows) return m.rows ? m.rows[p] : p;
+    if (p >= m.half && p < m.half + 2) return (int64_t)m.glob_half + (p - m.half);
+    return -1;
+  }
   if (!m.sage) {
     if (p >= m.nrows) return -1;
     return m.rows ? m.rows[p] : p;

@@ -13,7 +13,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgist.so")
 
-GIST_ARCH_GCN, GIST_ARCH_SAGE = 0, 1
+GIST_ARCH_GCN, GIST_ARCH_SAGE, GIST_ARCH_GAT = 0, 1, 2
+ARCHS = {"gcn": GIST_ARCH_GCN, "sage": GIST_ARCH_SAGE, "gat": GIST_ARCH_GAT}
 GIST_OPT_SGD, GIST_OPT_ADAM = 0, 1
 GIST_PREC_FP32, GIST_PREC_BF16 = 0, 1
 GIST_GRAPH_DEVICE, GIST_GRAPH_HOST = 0, 1
@@ -117,7 +118,7 @@ class Gist:
         self._dims = (C.c_int32 * len(self.dims))(*self.dims)
         cfg = GistConfig()
         L.gist_config_default(C.byref(cfg))
-        cfg.arch = GIST_ARCH_SAGE if arch == "sage" else GIST_ARCH_GCN
+        cfg.arch = ARCHS[arch]
         cfg.num_layers = len(self.dims) - 1
         cfg.dims = self._dims
         cfg.optimizer = GIST_OPT_ADAM if optimizer == "adam" else GIST_OPT_SGD
@@ -205,8 +206,9 @@ class Gist:
         return loss.value, acc.value, lp, ap
 
     def param_shape(self, layer: int):
-        f = 2 if self.arch == "sage" else 1
-        return f * self.dims[layer], self.dims[layer + 1]
+        d = self.dims[layer]
+        rows = 2 * d if self.arch == "sage" else (d + 2 if self.arch == "gat" else d)
+        return rows, self.dims[layer + 1]
 
     def get_params(self, layer: int) -> np.ndarray:
         out = np.zeros(self.param_shape(layer), dtype=np.float32)
