@@ -40,7 +40,8 @@ def metric_for(spec):
     if spec.graph == "reddit" and spec.arch == "sage":
         return METRIC
     shape = {"cora": "Cora", "arxiv": "arxiv", "reddit": "Reddit", "amazon2m": "Amazon2M"}.get(spec.graph, spec.graph)
-    return f"sub-GCN train steps/s (box-level), {shape}-shape {'GraphSAGE' if spec.arch == 'sage' else 'GCN'}"
+    fam = {"sage": "GraphSAGE", "gat": "GAT"}.get(spec.arch, "GCN")
+    return f"sub-GCN train steps/s (box-level), {shape}-shape {fam}"
 
 
 def peaks():

@@ -995,6 +995,38 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         e.done = sl.ce_done;
       }
       g.ce_f.n = g.ce.n; g.ce_f.rows = g.ce.rows; g.ce_f.k = g.ce.k; g.ce_f.ld = g.ce.ld;
+      // the GEMMs of every layer are grouped over the slots: Z = H W, dW = H^T dZ, dH = dZ W^T
+      for (int l = 0; l < L; ++l) {
+        std::vector<GemmOp> fw, dw, dx;
+        for (int j = 0; j < g.count; ++j) {
+          Slot& sl = c->slots[g0 + j];
+          const LayerShape& sh = c->shapes[sl.index][l];
+          const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
+          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, true,
+                              false, nullptr, 0, nullptr, 0});
+          dw.push_back(GemmOp{true, false, sh.half, sh.Np, nb, sl.H[l], sh.half, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np,
+                              true, false, nullptr, 0, nullptr, 0});
+          if (l > 0)
+            dx.push_back(GemmOp{false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, true, false,
+                                nullptr, 0, nullptr, 0});
+          g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.half;
+          g.dw_fl[l] += 2.0 * nb * sh.Np * sh.half;
+          if (l > 0) g.dx_fl[l] += 2.0 * nb * sh.Np * sh.half;
+        }
+        if (tc) {
+          if (!gemm_bf16_prepare(fw.data(), g.count, &g.fwd_tc[l]) || !gemm_bf16_prepare(dw.data(), g.count, &g.dw_tc[l]) ||
+              (l > 0 && !gemm_bf16_prepare(dx.data(), g.count, &g.dx_tc[l])))
+            return fail(c, GIST_E_UNSUPPORTED, "GAT: tcgen05 GEMM plan failed");
+        } else {
+          for (int j = 0; j < g.count; ++j) {
+            g.fwd_f[l].op[j] = fw[j];
+            g.dw_f[l].op[j] = dw[j];
+            if (l > 0) g.dx_f[l].op[j] = dx[j];
+          }
+          g.fwd_f[l].n = g.dw_f[l].n = g.count;
+          g.dx_f[l].n = l > 0 ? g.count : 0;
+        }
+      }
       P.groups.push_back(g);
       continue;
     }
@@ -1380,10 +1412,6 @@ static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp
   ++c->nk;
 }
 
-static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
-                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
-                            cudaStream_t s);
-
 // One GAT subTrain step (R21) of every slot of group g after the grouped batch build: per slot
 // and layer Z = H W (GEMM), attention scores and aggregation; the grouped softmax-CE; then per
 // slot and layer the two attention backward passes, dW = H^T dZ (plus the attention rows) and
@@ -1392,7 +1420,6 @@ template <typename T>
 static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, cudaStream_t s) {
   const int L = c->L;
   const int64_t nb = c->nb_max_rows;
-  const bool tc = c->prec == GIST_PREC_BF16;
   auto layer_args = [&](Slot& sl, int l) {
     const LayerShape& sh = c->shapes[sl.index][l];
     GatLayer<T> a;
@@ -1404,40 +1431,44 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, c
     a.s = sc; a.t = sc + nb; a.lse = sc + 2 * nb; a.Srow = sc + 3 * nb; a.dt = sc + 4 * nb; a.ds = sc + 5 * nb;
     return a;
   };
-  for (int j = 0; j < g.count; ++j) {  // ---- a2/a3: forward
+  const int64_t d0p = pad8(c->dims[0]);
+  for (int j = 0; j < g.count; ++j) {  // layer-0 input: the batch rows of X
     Slot& sl = c->slots[g.first + j];
-    const auto& shp = c->shapes[sl.index];
-    const int64_t d0p = pad8(c->dims[0]);
     LK(gather_rows_t<T>((const T*)c->X, d0p, sl.b_nodes, nb, d0p, (T*)sl.H[0], d0p, s));
-    ++c->nk;
-    for (int l = 0; l < L; ++l) {
+  }
+  for (int l = 0; l < L; ++l) {  // ---- a2/a3: forward
+    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);  // Z = H W (grouped, fp32 out)
+    double by = 0.0;
+    for (int j = 0; j < g.count; ++j) by += (double)nb * c->shapes[c->slots[g.first + j].index][l].Np * 4.0 * 2.0;
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by);
+    for (int j = 0; j < g.count; ++j) {
+      Slot& sl = c->slots[g.first + j];
+      const auto& shp = c->shapes[sl.index];
       const LayerShape& sh = shp[l];
-      const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
-      int id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * nb * sh.Np * sh.half);
-      TRY(gemm_any(c, false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, true, false, s));
-      prof_end(c, s, id);
       GatLayer<T> a = layer_args(sl, l);
       a.H = (const T*)sl.H[l]; a.ldh = sh.half; a.kw = sh.half;  // scores = H (W a), fp32 W a
       a.W32 = sl.W + sh.off; a.ldw = sh.Np; a.wa = sl.gsc[l] + 6 * nb;
       if (l + 1 < L) { a.out = (T*)sl.H[l + 1]; a.ldo = shp[l + 1].half; a.relu = 1; }
       else { a.out_f32 = sl.logits; a.ldo = sh.Np; }
-      id = prof_begin(c, s, GIST_PROF_SPMM, (double)nb * sh.Np * sizeof(T) * 3.0);
       LK(gat_scores<T>(a, s));
       LK(gat_forward<T>(a, s));
-      prof_end(c, s, id);
-      c->nk += 2;
+      ++c->nk;
     }
+    prof_end(c, s, id);
   }
-  {  // ---- a4: softmax cross-entropy (grouped), dlogits into gG
+  {  // ---- a4: softmax cross-entropy (grouped), fp32 dlogits into gG
     const int id = prof_begin(c, s, GIST_PROF_LOSS, (double)g.count * nb * (g.ce.ld * 8.0 + 17.0));
     softmax_ce<float>(g.ce_f, s);
     prof_end(c, s, id);
     ++c->nk;
   }
-  for (int j = 0; j < g.count; ++j) {  // ---- a5/a6: backward
-    Slot& sl = c->slots[g.first + j];
-    const auto& shp = c->shapes[sl.index];
-    for (int l = L - 1; l >= 0; --l) {
+  for (int l = L - 1; l >= 0; --l) {  // ---- a5/a6: backward
+    double by = 0.0;
+    for (int j = 0; j < g.count; ++j) by += (double)nb * c->shapes[c->slots[g.first + j].index][l].Np * 4.0 * 4.0;
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by);
+    for (int j = 0; j < g.count; ++j) {
+      Slot& sl = c->slots[g.first + j];
+      const auto& shp = c->shapes[sl.index];
       const LayerShape& sh = shp[l];
       GatLayer<T> a = layer_args(sl, l);
       a.G = (const float*)sl.gG; a.ldg = sh.Np;  // dlogits (last layer) or dH_{l+1} (width Np_l)
@@ -1445,19 +1476,12 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, c
       a.dZ = (T*)sl.dZ[l]; a.ldd = sh.Np;
       a.da_src = sl.G + sh.off + (int64_t)sh.half * sh.Np;
       a.da_dst = a.da_src + sh.Np;
-      int id = prof_begin(c, s, GIST_PROF_SPMM, (double)nb * sh.Np * sizeof(T) * 6.0);
       LK(gat_backward<T>(a, s));
-      prof_end(c, s, id);
-      c->nk += 3;
-      id = prof_begin(c, s, GIST_PROF_GEMM, 2.0 * nb * sh.Np * sh.half * (l > 0 ? 2 : 1));
-      TRY(gemm_any(c, true, false, sh.half, sh.Np, nb, sl.H[l], sh.half, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true,
-                   false, s));
-      if (l > 0) {
-        const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
-        TRY(gemm_any(c, false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, true, false, s));
-      }
-      prof_end(c, s, id);
+      c->nk += 2;
     }
+    prof_end(c, s, id);
+    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);            // dW = H^T dZ (rows [0, half))
+    if (l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);  // dH = dZ W^T -> gG (fp32)
   }
   return GIST_OK;
 }

@@ -57,7 +57,7 @@ GRAPHS = {
 class ModelSpec:
     name: str
     graph: str
-    arch: str                # "gcn" | "sage"
+    arch: str                # "gcn" | "sage" | "gat"
     dims: tuple
     m: int
     q: int                   # clusters per mini-batch
@@ -72,6 +72,9 @@ MODELS = {
     "C3": ModelSpec("C3-reddit-sage4-4096", "reddit", "sage", (602, 4096, 4096, 4096, 41), 8, 20, 500),
     "C4": ModelSpec("C4-amazon2m-sage3-8192", "amazon2m", "sage", (100, 8192, 8192, 47), 8, 10, 5000),
     "C5": ModelSpec("C5-amazon2m-sage3-32768", "amazon2m", "sage", (100, 32768, 32768, 47), 8, 10, 5000),
+    # the paper's Reddit GAT (256-dimensional, two to four layers;
+    # m = 2 gives its best F1), on the C3 graph and batching (R21)
+    "C3G": ModelSpec("C3G-reddit-gat2-256", "reddit", "gat", (602, 256, 41), 2, 20, 500),
 }
 
 
