@@ -5,7 +5,8 @@
 //   e_ij = LeakyReLU(t_i + s_j), j in N(i) u {i}; alpha = row softmax;
 //   out_i = sum_j alpha_ij Z_j, ReLU on hidden layers                          (k_gat_fwd)
 // Backward, with G = dL/dout (ReLU mask of the next layer's input applied on read):
-//   S_i = sum_j alpha_ij (G_i . Z_j),  dt_i = sum_j alpha_ij slope_ij (G_i . Z_j - S_i)  (k_gat_bwd_rows)
+//   S_i = sum_j alpha_ij (G_i . Z_j),  dt_i = sum_j alpha_ij slope_ij (G_i . Z_j - S_i)  (k_gat_bwd_rows,
+//   which also stores the masked G_i back in place for the column pass)
 //   dZ_j = sum_i alpha_ij G_i + ds_j a_src + dt_j a_dst,
 //   ds_j = sum_i alpha_ij slope_ij (G_i . Z_j - S_i)      over i in N(j) u {j}   (k_gat_bwd_cols)
 // (the adjacency is symmetric, so the column pass walks row j's own neighbour list and
@@ -131,61 +132,91 @@ __global__ void __launch_bounds__(256) k_gat_scores_h(const __grid_constant__ Ga
   if (lane == 0) a.s[v] = ps, a.t[v] = pt;
 }
 
+// neighbours gathered per unrolled round (independent row loads in flight per warp)
+template <int NV>
+struct Unroll {
+  static constexpr int U = NV == 1 ? 8 : (NV == 2 ? 4 : (NV == 4 ? 2 : 1));
+};
+
+// lse_i = log sum_{j in N(i) u {i}} exp(e_ij): lane-parallel over the neighbour list (scalars only)
+template <typename T>
+__device__ __forceinline__ float row_lse(const GatLayer<T>& a, int64_t v, int64_t beg, int64_t end, float tv,
+                                         int lane) {
+  float m = lane == 0 ? lrelu(tv + a.s[v]) : -INFINITY, l = lane == 0 ? 1.f : 0.f;
+  for (int64_t e = beg + lane; e < end; e += 32) {
+    const float x = lrelu(tv + a.s[a.col[e]]);
+    if (x > m) l = l * expf(m - x) + 1.f, m = x;
+    else l += expf(x - m);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    const float mm = fmaxf(m, m2);
+    l = (m == -INFINITY ? 0.f : l * expf(m - mm)) + (m2 == -INFINITY ? 0.f : l2 * expf(m2 - mm));
+    m = mm;
+  }
+  return m + logf(l);
+}
+
+// forward: pass 1 the row's log-sum-exp from the per-node scalars, pass 2 the alpha-weighted
+// gather of Z rows, U rows in flight per round
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLayer<T> a) {
+  constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
   const int64_t beg = a.row_beg[v], end = a.row_end[v];  // dummy batch rows: beg = end = -1 (self only)
   const float tv = a.t[v];
+  const float lse = row_lse(a, v, beg, end, tv, lane);
   float acc[NV][4];
-  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, acc);  // self loop first: m = e_vv, l = 1
-  float m = lrelu(tv + a.s[v]), l = 1.f;
+  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, acc);
+  {
+    const float a0 = expf(lrelu(tv + a.s[v]) - lse);
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[k][q] *= a0;
+  }
   for (int64_t b0 = beg; b0 < end; b0 += 32) {
     const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
     int32_t u = 0;
-    float su = 0.f;
-    if (lane < n) u = a.col[b0 + lane], su = a.s[u];
-    for (int jj = 0; jj < n; ++jj) {
-      const int32_t uj = __shfl_sync(0xffffffffu, u, jj);
-      const float e = lrelu(tv + __shfl_sync(0xffffffffu, su, jj));
-      float z[NV][4];
-      load_row<float, NV>(a.Z, a.ldz, uj, a.w, lane, z);
-      if (e > m) {  // online softmax: rescale the running sum (warp-uniform branch)
-        const float sc = expf(m - e);
+    float al = 0.f;
+    if (lane < n) u = a.col[b0 + lane], al = expf(lrelu(tv + a.s[u]) - lse);
+    for (int jj = 0; jj < n; jj += U) {
+      float z[U][NV][4], w[U];
 #pragma unroll
-        for (int k = 0; k < NV; ++k)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[k][q] = acc[k][q] * sc + z[k][q];
-        l = l * sc + 1.f;
-        m = e;
-      } else {
-        const float p = expf(e - m);
-#pragma unroll
-        for (int k = 0; k < NV; ++k)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[k][q] += p * z[k][q];
-        l += p;
+      for (int r = 0; r < U; ++r) {
+        const int src = jj + r < n ? jj + r : jj;
+        const int32_t uj = __shfl_sync(0xffffffffu, u, src);
+        w[r] = jj + r < n ? __shfl_sync(0xffffffffu, al, src) : 0.f;
+        load_row<float, NV>(a.Z, a.ldz, uj, a.w, lane, z[r]);
       }
+#pragma unroll
+      for (int r = 0; r < U; ++r)
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[k][q] += w[r] * z[r][k][q];
     }
   }
-  const float inv = 1.f / l;
-  if (lane == 0) a.lse[v] = m + logf(l);
+  if (lane == 0) a.lse[v] = lse;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const int64_t c = (int64_t)k * 128 + lane * 4;
     if (c >= a.w) continue;
     float o[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) o[q] = a.relu ? fmaxf(acc[k][q] * inv, 0.f) : acc[k][q] * inv;
+    for (int q = 0; q < 4; ++q) o[q] = a.relu ? fmaxf(acc[k][q], 0.f) : acc[k][q];
     if (a.out_f32) st4(a.out_f32 + v * a.ldo + c, o);
     else st4(a.out + v * a.ldo + c, o);
   }
 }
 
-// per row i: S_i and dt_i (see the file header)
+// per row i: S_i and dt_i (see the file header); U neighbour rows of Z in flight per round
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ GatLayer<T> a) {
+  constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
@@ -193,37 +224,71 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
   const float tv = a.t[v], lv = a.lse[v];
   float g[NV][4];
   load_row<float, NV, T>(a.G, a.ldg, v, a.w, lane, g, a.mask, a.ldm);
-  float S = 0.f, U = 0.f, V = 0.f;
-  auto edge = [&](int64_t u, float su) {
-    float z[NV][4];
-    load_row<float, NV>(a.Z, a.ldz, u, a.w, lane, z);
+  float S = 0.f, Uu = 0.f, V = 0.f;
+  auto dot = [&](const float (&z)[NV][4]) {
     float d = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
       for (int q = 0; q < 4; ++q) d += g[k][q] * z[k][q];
-    d = warp_sum(d);
-    const float pre = tv + su;
-    const float al = expf(lrelu(pre) - lv);
-    const float sl = pre > 0.f ? 1.f : kSlope;
-    S += al * d;
-    U += al * d * sl;
-    V += al * sl;
+    return d;
   };
-  edge(v, a.s[v]);
+  {  // self loop
+    float z[NV][4];
+    load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+    const float d = warp_sum(dot(z));
+    const float pre = tv + a.s[v];
+    const float al = expf(lrelu(pre) - lv), sl = pre > 0.f ? 1.f : kSlope;
+    S += al * d, Uu += al * d * sl, V += al * sl;
+  }
   for (int64_t b0 = beg; b0 < end; b0 += 32) {
     const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
     int32_t u = 0;
-    float su = 0.f;
-    if (lane < n) u = a.col[b0 + lane], su = a.s[u];
-    for (int jj = 0; jj < n; ++jj) edge(__shfl_sync(0xffffffffu, u, jj), __shfl_sync(0xffffffffu, su, jj));
+    float al = 0.f, sl = 0.f;
+    if (lane < n) {
+      u = a.col[b0 + lane];
+      const float pre = tv + a.s[u];
+      al = expf(lrelu(pre) - lv);
+      sl = pre > 0.f ? 1.f : kSlope;
+    }
+    for (int jj = 0; jj < n; jj += U) {
+      float z[U][NV][4], d[U];
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int src = jj + r < n ? jj + r : jj;
+        load_row<float, NV>(a.Z, a.ldz, __shfl_sync(0xffffffffu, u, src), a.w, lane, z[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < U; ++r) d[r] = dot(z[r]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < U; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int src = jj + r < n ? jj + r : jj;
+        const float alr = jj + r < n ? __shfl_sync(0xffffffffu, al, src) : 0.f;
+        const float slr = __shfl_sync(0xffffffffu, sl, src);
+        S += alr * d[r], Uu += alr * d[r] * slr, V += alr * slr;
+      }
+    }
   }
-  if (lane == 0) a.Srow[v] = S, a.dt[v] = U - S * V;
+  if (lane == 0) a.Srow[v] = S, a.dt[v] = Uu - S * V;
+  if (a.mask) {  // store G_v masked in place (only this warp reads row v here): the column pass
+    // then gathers G rows without their masks
+    float* gw = const_cast<float*>(a.G) + v * a.ldg;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int64_t c = (int64_t)k * 128 + lane * 4;
+      if (c < a.w) st4(gw + c, g[k]);
+    }
+  }
 }
 
-// per row j: dZ_j and ds_j (see the file header)
+// per row j: dZ_j and ds_j (see the file header); U neighbour rows of G in flight per round
 template <typename T, int NV>
 __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ GatLayer<T> a) {
+  constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
@@ -236,28 +301,63 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[k][q] = 0.f;
   float ds = 0.f;
-  auto edge = [&](int64_t i, float ti, float li, float Si) {
-    float g[NV][4];
-    load_row<float, NV, T>(a.G, a.ldg, i, a.w, lane, g, a.mask, a.ldm);
-    const float pre = ti + sv;
-    const float al = expf(lrelu(pre) - li);
+  auto dot = [&](const float (&g)[NV][4]) {
     float d = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) d += g[k][q] * z[k][q], acc[k][q] += al * g[k][q];
-    d = warp_sum(d);
-    ds += al * (d - Si) * (pre > 0.f ? 1.f : kSlope);
+      for (int q = 0; q < 4; ++q) d += g[k][q] * z[k][q];
+    return d;
   };
-  edge(v, a.t[v], a.lse[v], a.Srow[v]);
+  {  // self loop
+    float g[NV][4];
+    load_row<float, NV>(a.G, a.ldg, v, a.w, lane, g);  // masked by the row pass
+    const float pre = a.t[v] + sv;
+    const float al = expf(lrelu(pre) - a.lse[v]);
+    const float d = warp_sum(dot(g));
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[k][q] += al * g[k][q];
+    ds += al * (d - a.Srow[v]) * (pre > 0.f ? 1.f : kSlope);
+  }
   for (int64_t b0 = beg; b0 < end; b0 += 32) {
     const int n = (end - b0) < 32 ? (int)(end - b0) : 32;
     int32_t u = 0;
-    float tu = 0.f, lu = 0.f, Su = 0.f;
-    if (lane < n) u = a.col[b0 + lane], tu = a.t[u], lu = a.lse[u], Su = a.Srow[u];
-    for (int jj = 0; jj < n; ++jj)
-      edge(__shfl_sync(0xffffffffu, u, jj), __shfl_sync(0xffffffffu, tu, jj), __shfl_sync(0xffffffffu, lu, jj),
-           __shfl_sync(0xffffffffu, Su, jj));
+    float al = 0.f, sl = 0.f, Su = 0.f;
+    if (lane < n) {
+      u = a.col[b0 + lane];
+      const float pre = a.t[u] + sv;
+      al = expf(lrelu(pre) - a.lse[u]);
+      sl = pre > 0.f ? 1.f : kSlope;
+      Su = a.Srow[u];
+    }
+    for (int jj = 0; jj < n; jj += U) {
+      float g[U][NV][4], d[U];
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int src = jj + r < n ? jj + r : jj;
+        load_row<float, NV>(a.G, a.ldg, __shfl_sync(0xffffffffu, u, src), a.w, lane, g[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < U; ++r) d[r] = dot(g[r]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < U; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int src = jj + r < n ? jj + r : jj;
+        const float alr = jj + r < n ? __shfl_sync(0xffffffffu, al, src) : 0.f;
+        const float slr = __shfl_sync(0xffffffffu, sl, src);
+        const float Sr = __shfl_sync(0xffffffffu, Su, src);
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[k][q] += alr * g[r][k][q];
+        ds += alr * (d[r] - Sr) * slr;
+      }
+    }
   }
   const float dtv = a.dt[v];
 #pragma unroll
@@ -272,25 +372,40 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
   if (lane == 0) a.ds[v] = ds;
 }
 
-// d a_src[c] = sum_r ds[r] Z[r, c], d a_dst[c] = sum_r dt[r] Z[r, c]: one thread per column,
-// rows in order (deterministic); written into the fp32 gradient rows of the sub weight
+// d a_src[c] = sum_r ds[r] Z[r, c], d a_dst[c] = sum_r dt[r] Z[r, c], in two deterministic
+// phases: k_gat_da_part sums a chunk of rows per CTA (32 columns x 8 row phases, smem-reduced)
+// into da_part[chunk][2][w]; k_gat_da_sum adds the chunks in order into the fp32 gradient rows.
 template <typename T>
-__global__ void __launch_bounds__(128) k_gat_da(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_da_part(const __grid_constant__ GatLayer<T> a) {
+  __shared__ float sx[8][32], sy[8][32];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t per = (a.rows + kGatDaChunks - 1) / kGatDaChunks;
+  const int64_t r0 = blockIdx.y * per, r1 = r0 + per < a.rows ? r0 + per : a.rows;
+  float x = 0.f, y = 0.f;
+  if (c < a.w)
+    for (int64_t r = r0 + wp; r < r1; r += 8) {
+      const float z = a.Z[r * a.ldz + c];
+      x += a.ds[r] * z, y += a.dt[r] * z;
+    }
+  sx[wp][lane] = x, sy[wp][lane] = y;
+  __syncthreads();
+  if (wp == 0 && c < a.w) {
+    float xs = 0.f, ys = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xs += sx[k][lane], ys += sy[k][lane];
+    a.da_part[(int64_t)blockIdx.y * 2 * a.w + c] = xs;
+    a.da_part[(int64_t)blockIdx.y * 2 * a.w + a.w + c] = ys;
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(128) k_gat_da_sum(const __grid_constant__ GatLayer<T> a) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.w) return;
-  float x0 = 0.f, y0 = 0.f, x1 = 0.f, y1 = 0.f;
-  int64_t r = 0;
-  for (; r + 1 < a.rows; r += 2) {
-    const float z0 = a.Z[r * a.ldz + c], z1 = a.Z[(r + 1) * a.ldz + c];
-    x0 += a.ds[r] * z0, y0 += a.dt[r] * z0;
-    x1 += a.ds[r + 1] * z1, y1 += a.dt[r + 1] * z1;
-  }
-  if (r < a.rows) {
-    const float z0 = a.Z[r * a.ldz + c];
-    x0 += a.ds[r] * z0, y0 += a.dt[r] * z0;
-  }
-  a.da_src[c] = x0 + x1;
-  a.da_dst[c] = y0 + y1;
+  float x = 0.f, y = 0.f;
+  for (int k = 0; k < kGatDaChunks; ++k) x += a.da_part[(int64_t)k * 2 * a.w + c], y += a.da_part[(int64_t)k * 2 * a.w + a.w + c];
+  a.da_src[c] = x;
+  a.da_dst[c] = y;
 }
 
 }  // namespace
@@ -331,7 +446,8 @@ template <typename T>
 void gat_backward(const GatLayer<T>& a, cudaStream_t s) {
   GAT_DISPATCH(k_gat_bwd_rows);
   GAT_DISPATCH(k_gat_bwd_cols);
-  k_gat_da<T><<<(unsigned)cdiv(a.w, 128), 128, 0, s>>>(a);
+  k_gat_da_part<T><<<dim3((unsigned)cdiv(a.w, 32), kGatDaChunks), 256, 0, s>>>(a);
+  k_gat_da_sum<T><<<(unsigned)cdiv(a.w, 128), 128, 0, s>>>(a);
 }
 #undef GAT_DISPATCH
 

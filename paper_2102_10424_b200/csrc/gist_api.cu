@@ -874,7 +874,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
         s.gsc.resize(c->L, nullptr);
         TRY(dalloc(c, &s.gZ[l], (size_t)nbm * maxN[l] * 4));  // fp32: attention operand
         CK(cudaMemsetAsync(s.gZ[l], 0, (size_t)nbm * maxN[l] * 4, c->stream));
-        TRY(dalloc_t(c, &s.gsc[l], (size_t)6 * nbm + 2 * kw));
+        TRY(dalloc_t(c, &s.gsc[l], (size_t)6 * nbm + 2 * kw + (size_t)2 * kGatDaChunks * maxN[l]));
       }
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
       CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
@@ -1417,7 +1417,7 @@ static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp
 // slot and layer the two attention backward passes, dW = H^T dZ (plus the attention rows) and
 // dH = dZ W^T.  Dummy batch rows (v >= n_b) carry no neighbours and a zero loss gradient.
 template <typename T>
-static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, cudaStream_t s) {
+static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int nnz_slot, cudaStream_t s) {
   const int L = c->L;
   const int64_t nb = c->nb_max_rows;
   auto layer_args = [&](Slot& sl, int l) {
@@ -1438,9 +1438,14 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, c
   }
   for (int l = 0; l < L; ++l) {  // ---- a2/a3: forward
     launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);  // Z = H W (grouped, fp32 out)
+    // compulsory bytes: Z read once (fp32), H (scores) and the output written once, per-row scalars,
+    // 4 B per edge of the batch CSR (the gathered Z rows are served from L2, as for k_spmm)
     double by = 0.0;
-    for (int j = 0; j < g.count; ++j) by += (double)nb * c->shapes[c->slots[g.first + j].index][l].Np * 4.0 * 2.0;
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by);
+    for (int j = 0; j < g.count; ++j) {
+      const LayerShape& sh = c->shapes[c->slots[g.first + j].index][l];
+      by += (double)nb * (sh.Np * (4.0 + sizeof(T)) + sh.half * sizeof(T) + 32.0);
+    }
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 4.0 * g.count, nnz_slot);
     for (int j = 0; j < g.count; ++j) {
       Slot& sl = c->slots[g.first + j];
       const auto& shp = c->shapes[sl.index];
@@ -1463,9 +1468,12 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, c
     ++c->nk;
   }
   for (int l = L - 1; l >= 0; --l) {  // ---- a5/a6: backward
-    double by = 0.0;
-    for (int j = 0; j < g.count; ++j) by += (double)nb * c->shapes[c->slots[g.first + j].index][l].Np * 4.0 * 4.0;
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by);
+    double by = 0.0;  // Z, G (+ mask), dZ once; scalars; two passes over the batch CSR
+    for (int j = 0; j < g.count; ++j) {
+      const LayerShape& sh = c->shapes[c->slots[g.first + j].index][l];
+      by += (double)nb * (sh.Np * (8.0 + 2.0 * sizeof(T)) + 48.0);
+    }
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 8.0 * g.count, nnz_slot);
     for (int j = 0; j < g.count; ++j) {
       Slot& sl = c->slots[g.first + j];
       const auto& shp = c->shapes[sl.index];
@@ -1476,6 +1484,7 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, c
       a.dZ = (T*)sl.dZ[l]; a.ldd = sh.Np;
       a.da_src = sl.G + sh.off + (int64_t)sh.half * sh.Np;
       a.da_dst = a.da_src + sh.Np;
+      a.da_part = sl.gsc[l] + 6 * nb + 2 * sh.half;
       LK(gat_backward<T>(a, s));
       c->nk += 2;
     }
@@ -1510,7 +1519,7 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
       CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
   }
-  if (c->arch == GIST_ARCH_GAT) return gat_group_step<T>(c, g, s);
+  if (c->arch == GIST_ARCH_GAT) return gat_group_step<T>(c, g, nnz_slot, s);
   const double per_nnz = 4.0 * g.count;
   auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
     int id = -1;

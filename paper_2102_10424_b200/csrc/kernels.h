@@ -365,6 +365,7 @@ struct GatLayer {
   T* dZ = nullptr;                    // backward output dL/dZ
   int64_t ldd = 0;
   float *da_src = nullptr, *da_dst = nullptr;  // backward output: gradient rows of a_src / a_dst
+  float* da_part = nullptr;                    // scratch: 64 x 2 x w partial sums of the above
   // scores re-associated as s = H (W a_src), t = H (W a_dst) (fp32 W a from the fp32 master W), so
   // they do not inherit the rounding of a bf16 Z: layer input H (ld ldh, width kw = padded rows of
   // W), W32 (kw x w, ld ldw) and a 2*kw scratch for [W a_src | W a_dst].  H == nullptr: s = Z a_src.
@@ -377,6 +378,7 @@ struct GatLayer {
 template <typename T> void gat_scores(const GatLayer<T>& a, cudaStream_t s);
 template <typename T> void gat_forward(const GatLayer<T>& a, cudaStream_t s);
 template <typename T> void gat_backward(const GatLayer<T>& a, cudaStream_t s);
+constexpr int kGatDaChunks = 64;
 template <typename T>
 void gather_rows_t(const T* src, int64_t lds, const int32_t* idx, int64_t rows, int64_t w, T* dst, int64_t ldd,
                    cudaStream_t s);
