@@ -123,7 +123,7 @@ def oracle_steps_per_s(spec, g, seconds: float, max_steps: int, min_steps: int =
     rng = np.random.default_rng(seed)   # timing only: random weights instead of the (slow) Philox init
     th = []
     for l in range(len(spec.dims) - 1):
-        rows = spec.dims[l] * (2 if spec.arch == "sage" else 1)
+        rows = O.weight_rows(spec.arch, spec.dims[l])
         th.append(rng.uniform(-0.05, 0.05, size=(rows, spec.dims[l + 1])))
     o.set_params(th)
     o.partition(seed=1, m=spec.m)
@@ -256,9 +256,11 @@ def main():
         part[order] = (np.arange(n) * args.eval_parts) // n     # METIS stand-in: cluster-sorted order cut
         torch.cuda.synchronize()
         barrier()
-        t0 = time.perf_counter()
-        lf, af = gx.eval(2)
-        t_full = time.perf_counter() - t0
+        lf = af = t_full = None
+        if max(spec.dims[1:-1]) <= 4096:   # wider models are evaluated on partitions only
+            t0 = time.perf_counter()
+            lf, af = gx.eval(2)
+            t_full = time.perf_counter() - t0
         barrier()
         t0 = time.perf_counter()
         lp, apc, _, _ = gx.eval_parts(2, part, args.eval_parts)
