@@ -13,6 +13,8 @@
 // recomputes alpha_ij from the per-node scalars t_i, s_j, lse_i: no atomics, no transpose);
 //   d a_src = Z^T ds, d a_dst = Z^T dt                                          (k_gat_da)
 // One warp per row; a lane holds 4 consecutive columns of each 128-column chunk (NV chunks).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,12 +73,13 @@ __device__ __forceinline__ void load_row(const T* base, int64_t ld, int64_t r, i
 }
 
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_scores(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_scores(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
   float z[NV][4];
-  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+  load_row<T, NV>(a.Z, a.ldz, v, a.w, lane, z);
   float ps = 0.f, pt = 0.f;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -92,7 +95,8 @@ __global__ void __launch_bounds__(256) k_gat_scores(const __grid_constant__ GatL
 
 // wa[k] = W32[k, :] . a_src, wa[kw + k] = W32[k, :] . a_dst (fp32; one warp per row of W)
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_wa(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_wa(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (k >= a.kw) return;
@@ -113,7 +117,8 @@ __global__ void __launch_bounds__(256) k_gat_wa(const __grid_constant__ GatLayer
 
 // s[v] = H[v, :] . wa[0:kw], t[v] = H[v, :] . wa[kw:2kw]
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_scores_h(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_scores_h(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
@@ -161,7 +166,8 @@ __device__ __forceinline__ float row_lse(const GatLayer<T>& a, int64_t v, int64_
 // forward: pass 1 the row's log-sum-exp from the per-node scalars, pass 2 the alpha-weighted
 // gather of Z rows, U rows in flight per round
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLaye
   const float tv = a.t[v];
   const float lse = row_lse(a, v, beg, end, tv, lane);
   float acc[NV][4];
-  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, acc);
+  load_row<T, NV>(a.Z, a.ldz, v, a.w, lane, acc);
   {
     const float a0 = expf(lrelu(tv + a.s[v]) - lse);
 #pragma unroll
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLaye
         const int src = jj + r < n ? jj + r : jj;
         const int32_t uj = __shfl_sync(0xffffffffu, u, src);
         w[r] = jj + r < n ? __shfl_sync(0xffffffffu, al, src) : 0.f;
-        load_row<float, NV>(a.Z, a.ldz, uj, a.w, lane, z[r]);
+        load_row<T, NV>(a.Z, a.ldz, uj, a.w, lane, z[r]);
       }
 #pragma unroll
       for (int r = 0; r < U; ++r)
@@ -215,7 +221,8 @@ __global__ void __launch_bounds__(256) k_gat_fwd(const __grid_constant__ GatLaye
 
 // per row i: S_i and dt_i (see the file header); U neighbour rows of Z in flight per round
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
   const int64_t beg = a.row_beg[v], end = a.row_end[v];
   const float tv = a.t[v], lv = a.lse[v];
   float g[NV][4];
-  load_row<float, NV, T>(a.G, a.ldg, v, a.w, lane, g, a.mask, a.ldm);
+  load_row<T, NV>(a.G, a.ldg, v, a.w, lane, g, a.mask, a.ldm);
   float S = 0.f, Uu = 0.f, V = 0.f;
   auto dot = [&](const float (&z)[NV][4]) {
     float d = 0.f;
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
   };
   {  // self loop
     float z[NV][4];
-    load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+    load_row<T, NV>(a.Z, a.ldz, v, a.w, lane, z);
     const float d = warp_sum(dot(z));
     const float pre = tv + a.s[v];
     const float al = expf(lrelu(pre) - lv), sl = pre > 0.f ? 1.f : kSlope;
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
 #pragma unroll
       for (int r = 0; r < U; ++r) {
         const int src = jj + r < n ? jj + r : jj;
-        load_row<float, NV>(a.Z, a.ldz, __shfl_sync(0xffffffffu, u, src), a.w, lane, z[r]);
+        load_row<T, NV>(a.Z, a.ldz, __shfl_sync(0xffffffffu, u, src), a.w, lane, z[r]);
       }
 #pragma unroll
       for (int r = 0; r < U; ++r) d[r] = dot(z[r]);
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
   if (lane == 0) a.Srow[v] = S, a.dt[v] = Uu - S * V;
   if (a.mask) {  // store G_v masked in place (only this warp reads row v here): the column pass
     // then gathers G rows without their masks
-    float* gw = const_cast<float*>(a.G) + v * a.ldg;
+    T* gw = const_cast<T*>(a.G) + v * a.ldg;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int64_t c = (int64_t)k * 128 + lane * 4;
@@ -287,7 +294,8 @@ __global__ void __launch_bounds__(256) k_gat_bwd_rows(const __grid_constant__ Ga
 
 // per row j: dZ_j and ds_j (see the file header); U neighbour rows of G in flight per round
 template <typename T, int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   constexpr int U = Unroll<NV>::U;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
   const int64_t beg = a.row_beg[v], end = a.row_end[v];
   const float sv = a.s[v];
   float z[NV][4], acc[NV][4];
-  load_row<float, NV>(a.Z, a.ldz, v, a.w, lane, z);
+  load_row<T, NV>(a.Z, a.ldz, v, a.w, lane, z);
 #pragma unroll
   for (int k = 0; k < NV; ++k)
 #pragma unroll
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
   };
   {  // self loop
     float g[NV][4];
-    load_row<float, NV>(a.G, a.ldg, v, a.w, lane, g);  // masked by the row pass
+    load_row<T, NV>(a.G, a.ldg, v, a.w, lane, g);  // masked by the row pass
     const float pre = a.t[v] + sv;
     const float al = expf(lrelu(pre) - a.lse[v]);
     const float d = warp_sum(dot(g));
@@ -337,7 +345,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
 #pragma unroll
       for (int r = 0; r < U; ++r) {
         const int src = jj + r < n ? jj + r : jj;
-        load_row<float, NV>(a.G, a.ldg, __shfl_sync(0xffffffffu, u, src), a.w, lane, g[r]);
+        load_row<T, NV>(a.G, a.ldg, __shfl_sync(0xffffffffu, u, src), a.w, lane, g[r]);
       }
 #pragma unroll
       for (int r = 0; r < U; ++r) d[r] = dot(g[r]);
@@ -376,7 +384,8 @@ __global__ void __launch_bounds__(256) k_gat_bwd_cols(const __grid_constant__ Ga
 // phases: k_gat_da_part sums a chunk of rows per CTA (32 columns x 8 row phases, smem-reduced)
 // into da_part[chunk][2][w]; k_gat_da_sum adds the chunks in order into the fp32 gradient rows.
 template <typename T>
-__global__ void __launch_bounds__(256) k_gat_da_part(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(256) k_gat_da_part(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.z];
   __shared__ float sx[8][32], sy[8][32];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
@@ -385,7 +394,7 @@ __global__ void __launch_bounds__(256) k_gat_da_part(const __grid_constant__ Gat
   float x = 0.f, y = 0.f;
   if (c < a.w)
     for (int64_t r = r0 + wp; r < r1; r += 8) {
-      const float z = a.Z[r * a.ldz + c];
+      const float z = Elem<T>::to_f(a.Z[r * a.ldz + c]);
       x += a.ds[r] * z, y += a.dt[r] * z;
     }
   sx[wp][lane] = x, sy[wp][lane] = y;
@@ -399,7 +408,8 @@ __global__ void __launch_bounds__(256) k_gat_da_part(const __grid_constant__ Gat
   }
 }
 template <typename T>
-__global__ void __launch_bounds__(128) k_gat_da_sum(const __grid_constant__ GatLayer<T> a) {
+__global__ void __launch_bounds__(128) k_gat_da_sum(const __grid_constant__ GatGroup<T> Gp) {
+  const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= a.w) return;
   float x = 0.f, y = 0.f;
@@ -410,44 +420,52 @@ __global__ void __launch_bounds__(128) k_gat_da_sum(const __grid_constant__ GatL
 
 }  // namespace
 
-#define GAT_DISPATCH(KERNEL)                                                                    \
+#define GAT_DISPATCH(KERNEL, W, ROWS)                                                            \
   do {                                                                                          \
-    if (a.rows <= 0) return;                                                                    \
-    const dim3 grid((unsigned)cdiv(a.rows, 8));                                                 \
-    if (a.w <= 128) KERNEL<T, 1><<<grid, 256, 0, s>>>(a);                                       \
-    else if (a.w <= 256) KERNEL<T, 2><<<grid, 256, 0, s>>>(a);                                  \
-    else if (a.w <= 512) KERNEL<T, 4><<<grid, 256, 0, s>>>(a);                                  \
-    else if (a.w <= 1024) KERNEL<T, 8><<<grid, 256, 0, s>>>(a);                                 \
-    else KERNEL<T, 16><<<grid, 256, 0, s>>>(a);                                                 \
+    if ((ROWS) <= 0 || G.n <= 0) return;                                                        \
+    const dim3 grid((unsigned)cdiv((ROWS), 8), (unsigned)G.n);                                  \
+    if ((W) <= 128) KERNEL<T, 1><<<grid, 256, 0, s>>>(G);                                       \
+    else if ((W) <= 256) KERNEL<T, 2><<<grid, 256, 0, s>>>(G);                                  \
+    else if ((W) <= 512) KERNEL<T, 4><<<grid, 256, 0, s>>>(G);                                  \
+    else if ((W) <= 1024) KERNEL<T, 8><<<grid, 256, 0, s>>>(G);                                 \
+    else KERNEL<T, 16><<<grid, 256, 0, s>>>(G);                                                 \
   } while (0)
 
 template <typename T>
-void gat_scores(const GatLayer<T>& a, cudaStream_t s) {
-  if (!a.H) {
-    GAT_DISPATCH(k_gat_scores);
+static void group_max(const GatGroup<T>& G, int64_t& w, int64_t& rows, int64_t& kw) {
+  w = rows = kw = 0;
+  for (int i = 0; i < G.n; ++i) {
+    w = std::max(w, G.a[i].w);
+    rows = std::max(rows, G.a[i].rows);
+    kw = std::max(kw, G.a[i].kw);
+  }
+}
+
+template <typename T>
+void gat_scores(const GatGroup<T>& G, cudaStream_t s) {
+  int64_t w, rows, kw;
+  group_max(G, w, rows, kw);
+  if (!G.a[0].H) {
+    GAT_DISPATCH(k_gat_scores, w, rows);
     return;
   }
-  if (a.rows <= 0) return;
-  const dim3 gk((unsigned)cdiv(a.kw, 8)), gr((unsigned)cdiv(a.rows, 8));
-  if (a.w <= 128) k_gat_wa<T, 1><<<gk, 256, 0, s>>>(a);
-  else if (a.w <= 256) k_gat_wa<T, 2><<<gk, 256, 0, s>>>(a);
-  else if (a.w <= 512) k_gat_wa<T, 4><<<gk, 256, 0, s>>>(a);
-  else if (a.w <= 1024) k_gat_wa<T, 8><<<gk, 256, 0, s>>>(a);
-  else k_gat_wa<T, 16><<<gk, 256, 0, s>>>(a);
-  if (a.kw <= 128) k_gat_scores_h<T, 1><<<gr, 256, 0, s>>>(a);
-  else if (a.kw <= 256) k_gat_scores_h<T, 2><<<gr, 256, 0, s>>>(a);
-  else if (a.kw <= 512) k_gat_scores_h<T, 4><<<gr, 256, 0, s>>>(a);
-  else if (a.kw <= 1024) k_gat_scores_h<T, 8><<<gr, 256, 0, s>>>(a);
-  else k_gat_scores_h<T, 16><<<gr, 256, 0, s>>>(a);
+  GAT_DISPATCH(k_gat_wa, w, kw);
+  GAT_DISPATCH(k_gat_scores_h, kw, rows);
 }
 template <typename T>
-void gat_forward(const GatLayer<T>& a, cudaStream_t s) { GAT_DISPATCH(k_gat_fwd); }
+void gat_forward(const GatGroup<T>& G, cudaStream_t s) {
+  int64_t w, rows, kw;
+  group_max(G, w, rows, kw);
+  GAT_DISPATCH(k_gat_fwd, w, rows);
+}
 template <typename T>
-void gat_backward(const GatLayer<T>& a, cudaStream_t s) {
-  GAT_DISPATCH(k_gat_bwd_rows);
-  GAT_DISPATCH(k_gat_bwd_cols);
-  k_gat_da_part<T><<<dim3((unsigned)cdiv(a.w, 32), kGatDaChunks), 256, 0, s>>>(a);
-  k_gat_da_sum<T><<<(unsigned)cdiv(a.w, 128), 128, 0, s>>>(a);
+void gat_backward(const GatGroup<T>& G, cudaStream_t s) {
+  int64_t w, rows, kw;
+  group_max(G, w, rows, kw);
+  GAT_DISPATCH(k_gat_bwd_rows, w, rows);
+  GAT_DISPATCH(k_gat_bwd_cols, w, rows);
+  k_gat_da_part<T><<<dim3((unsigned)cdiv(w, 32), kGatDaChunks, (unsigned)G.n), 256, 0, s>>>(G);
+  k_gat_da_sum<T><<<dim3((unsigned)cdiv(w, 128), (unsigned)G.n), 128, 0, s>>>(G);
 }
 #undef GAT_DISPATCH
 
@@ -485,12 +503,12 @@ void mean_rows(float* dst, const MeanRows& m, int rows, cudaStream_t s) {
   k_mean_rows<<<dim3((unsigned)cdiv(m.cols, 128), (unsigned)rows), 128, 0, s>>>(dst, m);
 }
 
-template void gat_scores<float>(const GatLayer<float>&, cudaStream_t);
-template void gat_scores<bf16>(const GatLayer<bf16>&, cudaStream_t);
-template void gat_forward<float>(const GatLayer<float>&, cudaStream_t);
-template void gat_forward<bf16>(const GatLayer<bf16>&, cudaStream_t);
-template void gat_backward<float>(const GatLayer<float>&, cudaStream_t);
-template void gat_backward<bf16>(const GatLayer<bf16>&, cudaStream_t);
+template void gat_scores<float>(const GatGroup<float>&, cudaStream_t);
+template void gat_scores<bf16>(const GatGroup<bf16>&, cudaStream_t);
+template void gat_forward<float>(const GatGroup<float>&, cudaStream_t);
+template void gat_forward<bf16>(const GatGroup<bf16>&, cudaStream_t);
+template void gat_backward<float>(const GatGroup<float>&, cudaStream_t);
+template void gat_backward<bf16>(const GatGroup<bf16>&, cudaStream_t);
 template void gather_rows_t<float>(const float*, int64_t, const int32_t*, int64_t, int64_t, float*, int64_t,
                                    cudaStream_t);
 template void gather_rows_t<bf16>(const bf16*, int64_t, const int32_t*, int64_t, int64_t, bf16*, int64_t,

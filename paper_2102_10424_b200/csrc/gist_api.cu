@@ -94,7 +94,6 @@ struct StepPlan {
     std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
     std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
     CeGroup<T> ce;
-    CeGroup<float> ce_f;  // GAT: fp32 dlogits in both modes
     // re-associated last layer: Z = H W_top + N (H W_bot); backward via Q = N^T dZ
     bool reassoc = false;
     GemmPlanTC ra_p, ra_z, ra_dw, ra_dh;
@@ -872,8 +871,8 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
         CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * kw * E, c->stream));
         s.gZ.resize(c->L, nullptr);
         s.gsc.resize(c->L, nullptr);
-        TRY(dalloc(c, &s.gZ[l], (size_t)nbm * maxN[l] * 4));  // fp32: attention operand
-        CK(cudaMemsetAsync(s.gZ[l], 0, (size_t)nbm * maxN[l] * 4, c->stream));
+        TRY(dalloc(c, &s.gZ[l], (size_t)nbm * maxN[l] * E));
+        CK(cudaMemsetAsync(s.gZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
         TRY(dalloc_t(c, &s.gsc[l], (size_t)6 * nbm + 2 * kw + (size_t)2 * kGatDaChunks * maxN[l]));
       }
       TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
@@ -901,8 +900,8 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     if (c->arch == GIST_ARCH_GAT) {
       int gw = 0;
       for (int l = 0; l < c->L; ++l) gw = std::max(gw, maxN[l]);
-      TRY(dalloc(c, &s.gG, (size_t)nbm * gw * 4));  // fp32 dlogits / dH
-      CK(cudaMemsetAsync(s.gG, 0, (size_t)nbm * gw * 4, c->stream));
+      TRY(dalloc(c, &s.gG, (size_t)nbm * gw * E));  // dlogits, then dH of each layer
+      CK(cudaMemsetAsync(s.gG, 0, (size_t)nbm * gw * E, c->stream));
     }
     TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
     CK(cudaMemsetAsync(s.dC, 0, (size_t)nbm * maxKall * E, c->stream));
@@ -989,12 +988,11 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         BatchSlot& b = g.batch.s[j];
         b.desc = sl.desc_dev; b.map64 = sl.map64; b.b_nodes = sl.b_nodes; b.b_beg = sl.b_beg; b.b_end = sl.b_end;
         b.b_col = sl.b_col; b.scale = sl.scale; b.lab_b = sl.lab_b; b.train_b = sl.train_b; b.stats = sl.stats;
-        CeSlot<float>& e = g.ce_f.s[j];
-        e.logits = sl.logits; e.dlog = (float*)sl.gG; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
+        CeSlot<T>& e = g.ce.s[j];
+        e.logits = sl.logits; e.dlog = (T*)sl.gG; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
         e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
         e.done = sl.ce_done;
       }
-      g.ce_f.n = g.ce.n; g.ce_f.rows = g.ce.rows; g.ce_f.k = g.ce.k; g.ce_f.ld = g.ce.ld;
       // the GEMMs of every layer are grouped over the slots: Z = H W, dW = H^T dZ, dH = dZ W^T
       for (int l = 0; l < L; ++l) {
         std::vector<GemmOp> fw, dw, dx;
@@ -1002,12 +1000,12 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           Slot& sl = c->slots[g0 + j];
           const LayerShape& sh = c->shapes[sl.index][l];
           const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
-          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, true,
+          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, !tc,
                               false, nullptr, 0, nullptr, 0});
           dw.push_back(GemmOp{true, false, sh.half, sh.Np, nb, sl.H[l], sh.half, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np,
                               true, false, nullptr, 0, nullptr, 0});
           if (l > 0)
-            dx.push_back(GemmOp{false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, true, false,
+            dx.push_back(GemmOp{false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, !tc, false,
                                 nullptr, 0, nullptr, 0});
           g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.half;
           g.dw_fl[l] += 2.0 * nb * sh.Np * sh.half;
@@ -1424,7 +1422,7 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     const LayerShape& sh = c->shapes[sl.index][l];
     GatLayer<T> a;
     a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb; a.w = sh.Np;
-    a.Z = (const float*)sl.gZ[l]; a.ldz = sh.Np;
+    a.Z = (const T*)sl.gZ[l]; a.ldz = sh.Np;
     a.a_src = sl.W + sh.off + (int64_t)sh.half * sh.Np;
     a.a_dst = a.a_src + sh.Np;
     float* sc = sl.gsc[l];
@@ -1437,60 +1435,60 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     LK(gather_rows_t<T>((const T*)c->X, d0p, sl.b_nodes, nb, d0p, (T*)sl.H[0], d0p, s));
   }
   for (int l = 0; l < L; ++l) {  // ---- a2/a3: forward
-    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);  // Z = H W (grouped, fp32 out)
-    // compulsory bytes: Z read once (fp32), H (scores) and the output written once, per-row scalars,
+    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);  // Z = H W (grouped)
+    // compulsory bytes: Z read once, H (scores) and the output written once, per-row scalars,
     // 4 B per edge of the batch CSR (the gathered Z rows are served from L2, as for k_spmm)
     double by = 0.0;
-    for (int j = 0; j < g.count; ++j) {
-      const LayerShape& sh = c->shapes[c->slots[g.first + j].index][l];
-      by += (double)nb * (sh.Np * (4.0 + sizeof(T)) + sh.half * sizeof(T) + 32.0);
-    }
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 4.0 * g.count, nnz_slot);
+    GatGroup<T> G;
+    G.n = g.count;
     for (int j = 0; j < g.count; ++j) {
       Slot& sl = c->slots[g.first + j];
       const auto& shp = c->shapes[sl.index];
       const LayerShape& sh = shp[l];
-      GatLayer<T> a = layer_args(sl, l);
+      by += (double)nb * (sh.Np * 2.0 * sizeof(T) + sh.half * sizeof(T) + 32.0);
+      GatLayer<T>& a = G.a[j];
+      a = layer_args(sl, l);
       a.H = (const T*)sl.H[l]; a.ldh = sh.half; a.kw = sh.half;  // scores = H (W a), fp32 W a
       a.W32 = sl.W + sh.off; a.ldw = sh.Np; a.wa = sl.gsc[l] + 6 * nb;
       if (l + 1 < L) { a.out = (T*)sl.H[l + 1]; a.ldo = shp[l + 1].half; a.relu = 1; }
       else { a.out_f32 = sl.logits; a.ldo = sh.Np; }
-      LK(gat_scores<T>(a, s));
-      LK(gat_forward<T>(a, s));
-      ++c->nk;
     }
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 4.0 * g.count, nnz_slot);
+    LK(gat_scores<T>(G, s));
+    LK(gat_forward<T>(G, s));
+    ++c->nk;
     prof_end(c, s, id);
   }
-  {  // ---- a4: softmax cross-entropy (grouped), fp32 dlogits into gG
-    const int id = prof_begin(c, s, GIST_PROF_LOSS, (double)g.count * nb * (g.ce.ld * 8.0 + 17.0));
-    softmax_ce<float>(g.ce_f, s);
+  {  // ---- a4: softmax cross-entropy (grouped), dlogits into gG
+    const int id = prof_begin(c, s, GIST_PROF_LOSS, (double)g.count * nb * (g.ce.ld * (4.0 + sizeof(T)) + 17.0));
+    softmax_ce<T>(g.ce, s);
     prof_end(c, s, id);
     ++c->nk;
   }
   for (int l = L - 1; l >= 0; --l) {  // ---- a5/a6: backward
     double by = 0.0;  // Z, G (+ mask), dZ once; scalars; two passes over the batch CSR
-    for (int j = 0; j < g.count; ++j) {
-      const LayerShape& sh = c->shapes[c->slots[g.first + j].index][l];
-      by += (double)nb * (sh.Np * (8.0 + 2.0 * sizeof(T)) + 48.0);
-    }
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 8.0 * g.count, nnz_slot);
+    GatGroup<T> G;
+    G.n = g.count;
     for (int j = 0; j < g.count; ++j) {
       Slot& sl = c->slots[g.first + j];
       const auto& shp = c->shapes[sl.index];
       const LayerShape& sh = shp[l];
-      GatLayer<T> a = layer_args(sl, l);
-      a.G = (const float*)sl.gG; a.ldg = sh.Np;  // dlogits (last layer) or dH_{l+1} (width Np_l)
+      by += (double)nb * (sh.Np * 4.0 * sizeof(T) + 48.0);
+      GatLayer<T>& a = G.a[j];
+      a = layer_args(sl, l);
+      a.G = (const T*)sl.gG; a.ldg = sh.Np;  // dlogits (last layer) or dH_{l+1} (width Np_l)
       if (l + 1 < L) { a.mask = (const T*)sl.H[l + 1]; a.ldm = shp[l + 1].half; }
       a.dZ = (T*)sl.dZ[l]; a.ldd = sh.Np;
       a.da_src = sl.G + sh.off + (int64_t)sh.half * sh.Np;
       a.da_dst = a.da_src + sh.Np;
       a.da_part = sl.gsc[l] + 6 * nb + 2 * sh.half;
-      LK(gat_backward<T>(a, s));
-      c->nk += 2;
     }
+    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 8.0 * g.count, nnz_slot);
+    LK(gat_backward<T>(G, s));
+    c->nk += 3;
     prof_end(c, s, id);
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);            // dW = H^T dZ (rows [0, half))
-    if (l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);  // dH = dZ W^T -> gG (fp32)
+    if (l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);  // dH = dZ W^T -> gG
   }
   return GIST_OK;
 }
@@ -1807,15 +1805,17 @@ static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N,
 template <typename T>
 static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* row_beg, const int64_t* row_end,
                                     const int32_t* col, const T* X0, const std::vector<void*>& wl, T* bufA, T* bufB,
-                                    float* Z, float* sc, float* logits, cudaStream_t s) {
+                                    T* Z, float* sc, float* logits, cudaStream_t s) {
   const T* Hin = X0;
   int64_t ldin = pad8(c->dims[0]);
   T* Hout = bufA;
   for (int l = 0; l < c->L; ++l) {
     const int64_t K = pad8(c->dims[l]), N = c->th_N[l];
     const void* Wl = sizeof(T) == 2 ? wl[l] : (const void*)c->theta[l];
-    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, Wl, N, Z, N, true, false, s));
-    GatLayer<T> a;
+    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, Wl, N, Z, N, sizeof(T) == 4, false, s));
+    GatGroup<T> G;
+    G.n = 1;
+    GatLayer<T>& a = G.a[0];
     a.row_beg = row_beg; a.row_end = row_end; a.col = col; a.rows = rows; a.w = N;
     a.Z = Z; a.ldz = N;
     a.a_src = c->theta[l] + K * N; a.a_dst = a.a_src + N;
@@ -1823,8 +1823,8 @@ static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* ro
     a.H = Hin; a.ldh = ldin; a.kw = K; a.W32 = c->theta[l]; a.ldw = N; a.wa = sc + 3 * rows;
     if (l + 1 < c->L) { a.out = Hout; a.ldo = N; a.relu = 1; }
     else { a.out_f32 = logits; a.ldo = N; }
-    LK(gat_scores<T>(a, s));
-    LK(gat_forward<T>(a, s));
+    LK(gat_scores<T>(G, s));
+    LK(gat_forward<T>(G, s));
     Hin = Hout;
     ldin = N;
     Hout = Hout == bufA ? bufB : bufA;
@@ -1855,14 +1855,14 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
     for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
     void* Z = nullptr;
     float* sc = nullptr;
-    TRY(dalloc(c, &Z, (size_t)n * maxN * 4));
+    TRY(dalloc(c, &Z, (size_t)n * maxN * sizeof(T)));
     TRY(dalloc_t(c, &sc, (size_t)3 * std::max<int64_t>(n, 1) + 2 * maxK));
     if (sizeof(T) == 2)
       for (int l = 0; l < c->L; ++l) {
         TRY(dalloc(c, &wl[l], (size_t)c->th_K[l] * c->th_N[l] * 2));
         LK(f32_to_bf16(c->theta[l], (bf16*)wl[l], c->th_K[l] * c->th_N[l], s));
       }
-    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, wl, Cb, Hn, (float*)Z, sc, logits, s));
+    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, wl, Cb, Hn, (T*)Z, sc, logits, s));
     CK(cudaStreamSynchronize(s));
     for (void* p : wl) if (p) dfree(c, p);
     dfree(c, Z);
@@ -2030,7 +2030,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
     int64_t maxN = 0;
     for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
     TRY(dalloc(c, &gX, (size_t)std::max<int64_t>(max_chunk, 1) * pad8(c->dims[0]) * sizeof(T)));
-    TRY(dalloc(c, &gZ, (size_t)std::max<int64_t>(max_chunk, 1) * maxN * 4));
+    TRY(dalloc(c, &gZ, (size_t)std::max<int64_t>(max_chunk, 1) * maxN * sizeof(T)));
     TRY(dalloc_t(c, &gsc, (size_t)3 * std::max<int64_t>(max_chunk, 1) + 2 * maxK));
   }
   for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
@@ -2042,7 +2042,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
     if (c->arch == GIST_ARCH_GAT) {  // X rows of the chunk gathered, then the GAT layers
       const int64_t d0p = pad8(c->dims[0]);
       LK(gather_rows_t<T>((const T*)c->X, d0p, pnode_d + k0, rows, d0p, (T*)gX, d0p, s));
-      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, wl, Cb, Hn, (float*)gZ, gsc, logits,
+      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, wl, Cb, Hn, (T*)gZ, gsc, logits,
                               s));
     }
     for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {

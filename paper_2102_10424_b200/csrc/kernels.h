@@ -348,7 +348,7 @@ struct GatLayer {
   const int64_t* row_end = nullptr;
   const int32_t* col = nullptr;
   int64_t rows = 0, w = 0;            // rows; padded width (multiple of 8)
-  const float* Z = nullptr;           // Z = H W (rows x w), fp32 in both modes (attention operand)
+  const T* Z = nullptr;               // Z = H W (rows x w)
   int64_t ldz = 0;
   const float* a_src = nullptr;       // attention vectors (fp32 master rows of the weight)
   const float* a_dst = nullptr;
@@ -358,7 +358,7 @@ struct GatLayer {
   float* out_f32 = nullptr;           // ... or fp32 logits
   int64_t ldo = 0;
   int relu = 0;
-  const float* G = nullptr;           // backward: dL/dout, fp32 (masked by mask > 0 if mask)
+  const T* G = nullptr;               // backward: dL/dout (masked by mask > 0 if mask)
   int64_t ldg = 0;
   const T* mask = nullptr;
   int64_t ldm = 0;
@@ -375,9 +375,15 @@ struct GatLayer {
   int64_t ldw = 0;
   float* wa = nullptr;
 };
-template <typename T> void gat_scores(const GatLayer<T>& a, cudaStream_t s);
-template <typename T> void gat_forward(const GatLayer<T>& a, cudaStream_t s);
-template <typename T> void gat_backward(const GatLayer<T>& a, cudaStream_t s);
+// one launch per kernel for up to kMaxGroup slots (grid.y = slot)
+template <typename T>
+struct GatGroup {
+  GatLayer<T> a[kMaxGroup];
+  int n = 0;
+};
+template <typename T> void gat_scores(const GatGroup<T>& G, cudaStream_t s);
+template <typename T> void gat_forward(const GatGroup<T>& G, cudaStream_t s);
+template <typename T> void gat_backward(const GatGroup<T>& G, cudaStream_t s);
 constexpr int kGatDaChunks = 64;
 template <typename T>
 void gather_rows_t(const T* src, int64_t lds, const int32_t* idx, int64_t rows, int64_t w, T* dst, int64_t ldd,
