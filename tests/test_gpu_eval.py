@@ -126,3 +126,26 @@ def test_eval_parts_c3_full_size_sampled(c3, precision):
     okg = ~np.isnan(apg)
     assert lg == pytest.approx(float(np.mean(lpg[okg].astype(np.float64))), rel=1e-5)
     assert ag == pytest.approx(float(np.mean(apg[okg].astype(np.float64))), rel=1e-5)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_full_graph_eval_c2_full_size(precision):
+    """C2 (ogbn-arxiv-shaped, 169,343 nodes, 1.17 M edges), 3-layer GCN hidden 1024: the
+    full-graph eval operator runs in L2-sized column slabs (n >= 65,536), GCN scalings and the
+    self term included; the FP64 oracle computes the whole forward."""
+    spec = MODELS["C2"]
+    g = generate(GRAPHS["arxiv"], seed=0, device="cuda")
+    dims = list(spec.dims)
+    gpu, ora = make_pair(g, spec.arch, dims, precision=precision, q=spec.q)
+    t = TOL[precision]
+    for code in (1, 2):
+        lg, ag = gpu.eval(code)
+        lo, ao, _ = ora.eval(code)
+        assert abs(lg - lo) <= t * max(1.0, abs(lo)), (code, lg, lo)
+        assert abs(ag - ao) <= (1e-5 if precision == "fp32" else 5e-3), (code, ag, ao)
+    # partition-wise over the training clusters, checked on every partition
+    lg, ag, lpg, apg = gpu.eval_parts(2)
+    lo, ao, lpo, apo = ora.eval_partitions(2, g["cluster_ids"], g["num_clusters"])
+    ok = ~np.isnan(apo)
+    assert np.max(np.abs(lpg[ok] - lpo[ok])) <= t * max(1.0, np.max(np.abs(lpo[ok])))

@@ -149,3 +149,30 @@ def test_gat_bf16_loss_curve_10_rounds():
     err = max(abs(a - b) for a, b in zip(lg, lo)) / max(lo)
     print(f"bf16 GAT loss curve gpu={lg} oracle={lo} err={err:.3e}")
     assert err <= 1e-2, (err, lg, lo)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_gat_c3g_full_size_one_step(precision):
+    """The bench's C3G configuration at full size (Reddit-shaped graph, 232,965 nodes / 114.6 M
+    nnz, 20-cluster batches of ~3,100 rows and ~180 k edges, 2-layer GAT hidden 256, m = 2):
+    one subTrain step of both slots on the GPU; the oracle recomputes every slot's step."""
+    from synth.planted import MODELS
+    spec = MODELS["C3G"]
+    g = generate(GRAPHS["reddit"], seed=0, device="cuda")
+    dims = list(spec.dims)
+    gpu, ora = make_pair(g, "gat", dims, optimizer="adam", q=spec.q, precision=precision)
+    act_tol, grad_tol = TOL[precision]
+    gpu.partition(seed=5, m=spec.m)
+    ora.partition(seed=5, m=spec.m)
+    gpu.subtrain(1, lr=0.01)
+    for i in range(spec.m):
+        ora.train_step(i, 0, 0.01)
+        tr = ora.last_trace[i]
+        nodes = gpu.trace(i, 0)
+        p = align(nodes, tr["nodes"])
+        nb = len(nodes)
+        assert rel_err(gpu.trace(i, 2).reshape(nb, -1), tr["tape"]["logits"][p]) <= act_tol
+        assert rel_err(gpu.trace(i, 1, 1).reshape(nb, -1), tr["tape"]["H"][1][p]) <= act_tol
+        for l in range(len(dims) - 1):
+            assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= grad_tol, (i, l)
