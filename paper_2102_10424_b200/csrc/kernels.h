@@ -288,6 +288,15 @@ template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);
 void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
                StepState* st, bf16* Wb, cudaStream_t s);
 void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s);
+// per-layer optimizer step over one block per slot (offsets / lengths in floats, multiples of 4)
+struct OptRanges {
+  int64_t off[kMaxGroup];
+  int64_t len[kMaxGroup];
+  int n = 0;
+  int64_t total = 0;
+};
+void opt_ranges_step(bool adam, float* W, const float* G, float* M, float* V, const OptRanges& R, float b1, float b2,
+                     float eps, StepState* st, bf16* Wb, bool advance, cudaStream_t s);
 // (the optimizer kernels advance the step state themselves: their last CTA increments z, t)
 void step_advance(StepState* st, cudaStream_t s);
 // Re-associated last layer: Wcat[r][c2] = [W_top | W_bot] (half x 2Np, row-major) from the
