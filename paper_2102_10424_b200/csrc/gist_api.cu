@@ -126,6 +126,8 @@ struct gist_ctx {
   // set per step: the optimizer runs per layer on the dW stream right after that layer's last
   // reader of W (single lockstep group only), instead of one launch after the step
   bool opt_per_layer = false;
+  // the next step's batch was built on the dW stream, overlapping this step's optimizer
+  bool batch_prefetched = false;
   bool own_stream = false;
   int state = S_CREATED;
   gist_status sticky = GIST_OK;
@@ -1530,8 +1532,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   for (int j = 0; j < g.count; ++j) c->slots[g.first + j].last_nb = c->slots[g.first + j].nb_of_step[z];
   int nnz_slot = -1;
   if (c->prof_now && c->nnz_pin_used < c->nnz_pin_cap) nnz_slot = c->nnz_pin_used++;
-  // ---- a1: Cluster mini-batch build
-  {
+  // ---- a1: Cluster mini-batch build (unless prefetched during the previous step's optimizer)
+  if (!c->batch_prefetched) {
     double vol = 0.0;
     for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
     int id = -1;
@@ -1543,9 +1545,9 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
                 c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, s);
     prof_end(c, s, id);
     c->nk += 2;
-    if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
-      CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
   }
+  if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
+    CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
   if (c->arch == GIST_ARCH_GAT) return gat_group_step<T>(c, g, nnz_slot, s);
   const double per_nnz = 4.0 * g.count;
   auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
@@ -1670,6 +1672,23 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   return GIST_OK;
 }
 
+// a1 of step z for group g on stream bs with an explicit step index (the device step state
+// still points at the previous step while its optimizer runs on the main stream)
+template <typename T>
+static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs) {
+  BatchGroup B = g.batch;
+  B.zfix = z;
+  double vol = 0.0;
+  for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
+  const int id = prof_begin(c, bs, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0);
+  batch_setup(B, c->cstart, c->rp, bs);
+  batch_build(B, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
+              c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, bs);
+  prof_end(c, bs, id);
+  c->nk += 2;
+  return GIST_OK;
+}
+
 // a7 over every local slot at once (the packed buffers are contiguous), then advance the step state
 static gist_status run_optimizer(gist_ctx* c) {
   cudaStream_t s = c->stream;
@@ -1765,6 +1784,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
   *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0u};
   CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
   CK(cudaEventRecord(c->hstate_ev, s));
+  c->batch_prefetched = false;
   for (int z = 0; z < local_iters; ++z) {
     c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
     const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
@@ -1787,7 +1807,23 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
       CK(cudaEventRecord(c->ev_join2, c->side));
       CK(cudaStreamWaitEvent(s, c->ev_join2, 0));
     }
+    // prefetch: step z+1's batch build (it only needs the graph and the schedule) runs on the dW
+    // stream while the optimizer of step z runs here; every reader of the batch buffers of
+    // step z (the backward, dW included) is done by now.  One lockstep group only.
+    static const bool prefetch_on = [] { const char* e = std::getenv("GIST_BATCH_PREFETCH"); return !(e && e[0] == '0'); }();
+    const bool pf = prefetch_on && c->dws && ng == 1 && !two && z + 1 < local_iters;
+    if (pf) {
+      CK(cudaEventRecord(c->ev_dw_fork, s));
+      CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
+      if (c->prec == GIST_PREC_BF16) TRY(prefetch_batch<bf16>(c, c->plan_b.groups[0], z + 1, c->dws));
+      else TRY(prefetch_batch<float>(c, c->plan_f.groups[0], z + 1, c->dws));
+    }
     if (!c->opt_per_layer) TRY(run_optimizer(c));
+    if (pf) {
+      CK(cudaEventRecord(c->ev_dw_join, c->dws));
+      CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
+    }
+    c->batch_prefetched = pf;
     c->prof_now = false;
   }
   c->adam_t += local_iters;

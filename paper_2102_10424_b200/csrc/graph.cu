@@ -162,7 +162,7 @@ __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_
   pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
-  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+  const int32_t* d = S.desc + (size_t)(G.zfix >= 0 ? G.zfix : G.st->z) * (3 * q + 4);
   const int32_t* bcl = d;
   const int32_t* loff = d + q;
   const int32_t* voff = d + 2 * q + 1;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
   pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
-  const int32_t* d = S.desc + (size_t)G.st->z * (3 * q + 4);
+  const int32_t* d = S.desc + (size_t)(G.zfix >= 0 ? G.zfix : G.st->z) * (3 * q + 4);
   const int nb = d[2 * q];
   const uint32_t tag = (uint32_t)d[3 * q + 3];
   if (SMAP) {

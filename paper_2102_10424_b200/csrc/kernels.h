@@ -233,6 +233,7 @@ struct BatchGroup {
   BatchSlot s[kMaxGroup];
   int n = 0, q = 0, nb_max = 0;
   const StepState* st = nullptr;
+  int zfix = -1;  // >= 0: build the batch of step zfix (prefetch), not of the device step state's z
   // optional: copy the batch rows of the feature matrix X (bf16, ldx) into xdst[slot] (ldxd)
   const bf16* X = nullptr;
   int64_t ldx = 0, ldxd = 0;
