@@ -128,6 +128,7 @@ struct gist_ctx {
   bool opt_per_layer = false;
   // the next step's batch was built on the dW stream, overlapping this step's optimizer
   bool batch_prefetched = false;
+  bool agg0_prefetched = false;  // ... and its layer-0 aggregation
   bool own_stream = false;
   int state = S_CREATED;
   gist_status sticky = GIST_OK;
@@ -1592,8 +1593,10 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       tc_l(g.ra_z, g.ra_gemm_fl / 6);
       continue;
     }
-    if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
-    spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
+    if (!(l == 0 && c->batch_prefetched && c->agg0_prefetched)) {
+      if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
+      spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
+    }
     launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
   }
   // ---- a4: softmax cross-entropy
@@ -1686,6 +1689,26 @@ static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, i
               c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, bs);
   prof_end(c, bs, id);
   c->nk += 2;
+  // layer-0 aggregation [X_b | N X_b] needs only the batch: opt-in GIST_AGG0_PREFETCH=1 runs it
+  // here too (C3: 8,214-8,231 vs 8,260-8,266 steps/s without: it competes with the HBM-bound
+  // optimizer instead of filling idle SMs)
+  static const bool agg0 = [] { const char* e = std::getenv("GIST_AGG0_PREFETCH"); return e && e[0] == '1'; }();
+  if (agg0 && c->arch != GIST_ARCH_GAT && !(g.reassoc && c->L == 1)) {
+    const bool bd = c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE;
+    if (bd) {
+      BdPlan P = g.fwd_bd[0];
+      P.G.zfix = z;
+      const int id2 = prof_begin(c, bs, GIST_PROF_AGG_TC, g.bd_fl[0]);
+      gemm_bd_launch(P, bs);
+      prof_end(c, bs, id2);
+      ++c->nk;
+    }
+    const int id3 = prof_begin(c, bs, GIST_PROF_SPMM, g.fwd_by[0], 4.0 * g.count, -1);
+    spmm_group<T, T>(g.fwd_spmm[0], bs);
+    prof_end(c, bs, id3);
+    ++c->nk;
+    c->agg0_prefetched = true;
+  }
   return GIST_OK;
 }
 
@@ -1784,7 +1807,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
   *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0u};
   CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
   CK(cudaEventRecord(c->hstate_ev, s));
-  c->batch_prefetched = false;
+  c->batch_prefetched = c->agg0_prefetched = false;
   for (int z = 0; z < local_iters; ++z) {
     c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
     const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
@@ -1812,6 +1835,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
     // step z (the backward, dW included) is done by now.  One lockstep group only.
     static const bool prefetch_on = [] { const char* e = std::getenv("GIST_BATCH_PREFETCH"); return !(e && e[0] == '0'); }();
     const bool pf = prefetch_on && c->dws && ng == 1 && !two && z + 1 < local_iters;
+    c->agg0_prefetched = false;
     if (pf) {
       CK(cudaEventRecord(c->ev_dw_fork, s));
       CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
@@ -1824,6 +1848,7 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
       CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
     }
     c->batch_prefetched = pf;
+    if (!pf) c->agg0_prefetched = false;
     c->prof_now = false;
   }
   c->adam_t += local_iters;

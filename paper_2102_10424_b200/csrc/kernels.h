@@ -164,6 +164,7 @@ struct BdGroup {
   int64_t rows = 0;  // static batch rows (nb_max): dummy rows [n_b, rows) are zero-filled
   const StepState* st = nullptr;
   const int64_t* cstart = nullptr;
+  int zfix = -1;  // >= 0: descriptors of step zfix (prefetched layer-0 aggregation), not st->z
 };
 struct BdPlan {
   BdGroup G;
