@@ -195,13 +195,14 @@ def main():
     t_gen = time.perf_counter()
     g = generate(GRAPHS[spec.graph], seed=args.seed, device=f"cuda:{local}")
     t_gen = time.perf_counter() - t_gen
-    uid = None
-    if world > 1:
-        obj = [G.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-
     def make():
+        # every context builds its own NCCL communicator, so every one needs a fresh unique id
+        # (an ncclUniqueId's bootstrap root serves exactly one communicator init)
+        uid = None
+        if world > 1:
+            obj = [G.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
         return G.Gist(spec.arch, spec.dims, optimizer="adam", precision=args.precision, clusters_per_batch=spec.q,
                       batch_seed=1, rank=rank, world_size=world, device=local, nccl_unique_id=uid)
 
