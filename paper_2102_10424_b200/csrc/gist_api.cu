@@ -122,6 +122,10 @@ struct gist_ctx {
   // lockstep group, the per-layer optimizer steps) run on a side stream, overlapping the rest
   // of the backward chain (dX -> aggregation); joined at the end of the step
   cudaStream_t dws = nullptr;
+  // the side stream for this step: dws, except in profiled steps (every prof_stride-th), which
+  // run serialised so that the per-kernel event times of the live roofline are not inflated by
+  // overlap (ncu's launch list is serialised too)
+  cudaStream_t side_now = nullptr;
   cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr, ev_dw_wread = nullptr;
   // set per step: the optimizer runs per layer on the dW stream right after that layer's last
   // reader of W (single lockstep group only), instead of one launch after the step
@@ -1511,15 +1515,15 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     LK(gat_backward<T>(G, s));
     c->nk += 3;
     prof_end(c, s, id);
-    if (c->dws) {  // dW_l only feeds the optimizer: overlap it with the rest of the backward chain
+    if (c->side_now) {  // dW_l only feeds the optimizer: overlap it with the rest of the backward chain
       CK(cudaEventRecord(c->ev_dw_fork, s));
-      CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
+      CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
     }
-    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->dws ? c->dws : s);  // dW = H^T dZ (rows [0, half))
+    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->side_now ? c->side_now : s);  // dW = H^T dZ (rows [0, half))
     if (l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);          // dH = dZ W^T -> gG
   }
-  if (c->dws) {
-    CK(cudaEventRecord(c->ev_dw_join, c->dws));
+  if (c->side_now) {
+    CK(cudaEventRecord(c->ev_dw_join, c->side_now));
     CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
   }
   return GIST_OK;
@@ -1612,13 +1616,13 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   // stream once the main stream's last reader of W_l (the dX / dH GEMM) is done.
   auto fork = [&]() {
     CK(cudaEventRecord(c->ev_dw_fork, s));
-    CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
+    CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
     return GIST_OK;
   };
   auto opt_layer = [&](int l) {
     if (!c->opt_per_layer) return GIST_OK;
     CK(cudaEventRecord(c->ev_dw_wread, s));
-    CK(cudaStreamWaitEvent(c->dws, c->ev_dw_wread, 0));
+    CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_wread, 0));
     OptRanges R;
     R.n = g.count;
     for (int j = 0; j < g.count; ++j) {
@@ -1629,9 +1633,9 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       R.total += R.len[j];
     }
     const bool adam = c->cfg.optimizer == GIST_OPT_ADAM;
-    PL(GIST_PROF_OPTIM, (double)R.total * ((adam ? 28.0 : 12.0) + (c->Wball ? 2.0 : 0.0)), c->dws,
+    PL(GIST_PROF_OPTIM, (double)R.total * ((adam ? 28.0 : 12.0) + (c->Wball ? 2.0 : 0.0)), c->side_now,
        opt_ranges_step(adam, c->Wall, c->Gall, c->Mall, c->Vall, R, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate,
-                       c->Wball, l == 0, c->dws));
+                       c->Wball, l == 0, c->side_now));
     return GIST_OK;
   };
   for (int l = L - 1; l >= 0; --l) {
@@ -1640,11 +1644,11 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       // dZ_{l-1} = (dZ W_top^T + Q W_bot^T) * ReLU'
       if (bd && c->arch == GIST_ARCH_SAGE) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_bsp, g.ra_bby);
-      if (c->dws) {
+      if (c->side_now) {
         TRY(fork());
-        const int id = prof_begin(c, c->dws, GIST_PROF_GEMM, g.ra_gemm_fl / 3);
-        gemm_bf16_launch(g.ra_dw, c->dws);
-        prof_end(c, c->dws, id);
+        const int id = prof_begin(c, c->side_now, GIST_PROF_GEMM, g.ra_gemm_fl / 3);
+        gemm_bf16_launch(g.ra_dw, c->side_now);
+        prof_end(c, c->side_now, id);
         ++c->nk;
       } else {
         tc_l(g.ra_dw, g.ra_gemm_fl / 3);
@@ -1653,9 +1657,9 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       TRY(opt_layer(l));
       continue;
     }
-    if (c->dws) {
+    if (c->side_now) {
       TRY(fork());
-      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->dws);
+      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->side_now);
     } else {
       launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
     }
@@ -1668,8 +1672,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
     spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
   }
-  if (c->dws) {  // join: the optimizer (or the next step) reads every gradient / weight
-    CK(cudaEventRecord(c->ev_dw_join, c->dws));
+  if (c->side_now) {  // join: the optimizer (or the next step) reads every gradient / weight
+    CK(cudaEventRecord(c->ev_dw_join, c->side_now));
     CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
   }
   return GIST_OK;
@@ -1816,7 +1820,8 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
     // GCN / GraphSAGE): measured 8,033 vs 8,078 steps/s for dW-only overlap on C3 -- four
     // HBM-bound launches competing with the backward chain cost more than they hide
     static const bool per_layer = [] { const char* e = std::getenv("GIST_OPT_PER_LAYER"); return e && e[0] == '1'; }();
-    c->opt_per_layer = per_layer && c->dws && ng == 1 && c->arch != GIST_ARCH_GAT;
+    c->side_now = c->prof_now ? nullptr : c->dws;
+    c->opt_per_layer = per_layer && c->side_now && ng == 1 && c->arch != GIST_ARCH_GAT;
     if (two) {  // fork: the side stream sees the previous optimizer step / state advance
       CK(cudaEventRecord(c->ev_fork2, s));
       CK(cudaStreamWaitEvent(c->side, c->ev_fork2, 0));
@@ -1834,7 +1839,8 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
     // stream while the optimizer of step z runs here; every reader of the batch buffers of
     // step z (the backward, dW included) is done by now.  One lockstep group only.
     static const bool prefetch_on = [] { const char* e = std::getenv("GIST_BATCH_PREFETCH"); return !(e && e[0] == '0'); }();
-    const bool pf = prefetch_on && c->dws && ng == 1 && !two && z + 1 < local_iters;
+    const bool next_prof = c->prof_stride > 0 && ((c->step + z + 1) % c->prof_stride) == 0;
+    const bool pf = prefetch_on && c->dws && ng == 1 && !two && z + 1 < local_iters && !c->prof_now && !next_prof;
     c->agg0_prefetched = false;
     if (pf) {
       CK(cudaEventRecord(c->ev_dw_fork, s));
