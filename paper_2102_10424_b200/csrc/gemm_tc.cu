@@ -330,6 +330,8 @@ struct Tile {
   bool mma;    // false: zero-fill only (inert dummy rows of a batch)
   const CUtensorMap *ma, *mb;
   int a_row, b_col, b_k0, K;  // TMA coordinates
+  int a_k0 = 0;                // K offset of A (split-K chunk)
+  bool split = false;          // split-K chunk: the epilogue adds into the output (fp32 atomics)
   int64_t out_row0;
   int rows_valid, n0, N;
   int stream_a;  // evict_first hint on the A loads
@@ -342,13 +344,24 @@ struct ProbPlain {
   using Group = GemmGroupTC;
   static constexpr bool kTmaEpi = true;  // epilogue staging + TMA stores
   static __device__ __forceinline__ int ydim(const Group& G) { return G.tm; }
-  static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
+  static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn * G.ksplit; }
   static constexpr int kMaxDesc = 1;
   static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
   static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sd) {
+    const int ks = t % G.ksplit;  // the split-K chunks of one tile go to consecutive CTAs
+    t /= G.ksplit;
     const int per = G.tm * G.tn;
     const int z = t / per, r = t - z * per;
-    return decode_y(G, z, r / G.tn, r % G.tn, sd);
+    Tile T = decode_y(G, z, r / G.tn, r % G.tn, sd);
+    if (G.ksplit > 1) {
+      const int k0 = ks * G.kchunk;
+      T.split = true;
+      T.a_k0 = k0;
+      T.b_k0 = k0;
+      T.K = T.K - k0 < G.kchunk ? T.K - k0 : G.kchunk;
+      if (T.K <= 0) T.valid = T.mma = false;
+    }
+    return T;
   }
   // tile (slot z, 128-row tile y, n-tile nt)
   static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t*) {
@@ -462,7 +475,7 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
     // chunk j of row r at r*128 + ((j ^ (r & 7)) * 16), bank-conflict free) and written by
     // one cp.async.bulk.tensor per 32 x 128 B box, so stores are full lines instead of one
     // 16-byte piece of 32 different rows per instruction.
-    const bool tma = TMA_EPI && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
+    const bool tma = TMA_EPI && T.E.mc && !T.split && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
     constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
 #pragma unroll 1
     for (int c = c0w; c < c0w + CW; c += 32) {
@@ -520,6 +533,19 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
             bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
           }
           T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
+        }
+      } else if (OUT_F32 && T.split) {  // split-K chunk: add into the zeroed fp32 output
+        if (live && T.n0 + c < T.N) {
+          float* dst = (float*)T.E.C + row * T.E.ldc + T.n0 + c;
+          if (T.n0 + c + 32 <= T.N && (((uintptr_t)dst & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              atomicAdd(reinterpret_cast<float4*>(dst + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (T.n0 + c + i < T.N) atomicAdd(dst + i, v[i]);
+          }
         }
       } else if (live && T.n0 + c < T.N) {
         epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
@@ -619,17 +645,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           if (T.stream_a) {  // last read of A for a while: evict first
             const uint64_t pol = policy_evict_first();
             if (!A_MN) {
-              tma_load_2d_hint(sa, T.ma, &full[s], k0, T.a_row, pol);
+              tma_load_2d_hint(sa, T.ma, &full[s], T.a_k0 + k0, T.a_row, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0, pol);
+                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, T.a_k0 + k0, pol);
             }
           } else if (!A_MN) {
-            tma_load_2d(sa, T.ma, &full[s], k0, T.a_row);
+            tma_load_2d(sa, T.ma, &full[s], T.a_k0 + k0, T.a_row);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, T.a_k0 + k0);
           }
           if (!B_MN) {
             tma_load_2d(sb, T.mb, &full[s], T.b_k0 + k0, T.b_col);
@@ -1090,11 +1117,48 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
   }
   P->G.tm = (int)cdiv(P->maxM, BM);
   P->G.tn = (int)cdiv(P->maxN, P->bn);
+  // split-K when the tile space leaves most SMs idle (few, long-K tiles: the step's dW GEMMs,
+  // K = batch rows): fp32 outputs without epilogue operands only.  Opt-in (GIST_SPLITK=1):
+  // measured slower -- C3 8,265 vs 8,386 steps/s, single-slot groups 2,025 vs 2,779 (the chunks
+  // of one tile add into the same addresses at the same time, and each short chunk pays the
+  // pipeline fill and a full-tile epilogue)
+  P->G.ksplit = 1;
+  P->G.kchunk = 0;
+  static const bool splitk = [] { const char* e = std::getenv("GIST_SPLITK"); return e && e[0] == '1'; }();
+  bool plain = splitk && !P->pair && o0.out_f32;
+  int64_t tiles = 0, kmax = 0;
+  for (int i = 0; i < n; ++i) {
+    const GemmOp& o = ops[i];
+    plain = plain && !o.relu && !o.mask && !o.rscale && !o.add && !o.mbits && !o.mbits_in;
+    tiles += cdiv(o.M, BM) * cdiv(o.N, P->bn);
+    kmax = o.K > kmax ? o.K : kmax;
+  }
+  if (plain) {
+    const int64_t nkb = cdiv(kmax, BK);
+    int64_t ks = (2 * (int64_t)num_sms()) / (tiles > 0 ? tiles : 1);
+    ks = ks < 8 ? ks : 8;
+    ks = ks < nkb / 4 ? ks : nkb / 4;
+    if (ks >= 2) {
+      P->G.ksplit = (int)ks;
+      P->G.kchunk = (int)(cdiv(nkb, ks) * BK);
+      for (int i = 0; i < n; ++i) P->G.s[i].tma_store = 0;
+    }
+  }
   return true;
+}
+
+// split-K outputs start at zero: one launch zeroes every op's M x N block (row stride ldc)
+__global__ void k_zero_ops(const __grid_constant__ GemmGroupTC G) {
+  const GemmSlotTC& S = G.s[blockIdx.y];
+  float* C = (float*)S.C;
+  const int64_t total = (int64_t)S.M * S.N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    C[(i / S.N) * S.ldc + (i % S.N)] = 0.f;
 }
 
 void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
   if (P.G.n <= 0 || P.maxM <= 0 || P.maxN <= 0) return;
+  if (P.G.ksplit > 1) k_zero_ops<<<dim3(64, (unsigned)P.G.n), 256, 0, s>>>(P.G);
   if (P.bn == 256) dispatch_layout<256>(P, s);
   else dispatch_layout<128>(P, s);
 }

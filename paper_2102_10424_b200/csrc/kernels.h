@@ -118,6 +118,9 @@ struct alignas(64) GemmSlotTC {
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGemmOps];
   int n = 0, tm = 0, tn = 0;  // slots, M tiles, N tiles (persistent tile space)
+  // split-K (fp32 outputs without epilogue operands, few tiles): every tile's K range is cut into
+  // ksplit chunks of kchunk (multiple of 64) reduced with fp32 atomics into a zeroed output
+  int ksplit = 1, kchunk = 0;
 };
 // Host-side plan of one grouped tcgen05 GEMM (tensor maps encoded once, launched many times).
 struct GemmPlanTC {

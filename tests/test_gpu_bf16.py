@@ -135,3 +135,17 @@ def test_bf16_block_diagonal_aggregation_rounds():
         ora.aggregate()
         for l in range(3):
             assert rel_err(gpu.get_params(l), ora.theta[l]) <= BF16_TOL, (t, l)
+
+
+def test_tc_gemm_split_k_opt_in():
+    """The opt-in split-K path of the tcgen05 GEMM (GIST_SPLITK=1; fp32 outputs without epilogue
+    operands, few long-K tiles, fp32 atomics into a zeroed output): the layout tests again in a
+    process with it enabled (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GIST_SPLITK="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "test_tc_gemm_layouts and True-False"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
