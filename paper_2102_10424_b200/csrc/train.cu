@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
   const unsigned gmask = ((1u << LPR) - 1u) << ((threadIdx.x & 31) - gl);  // this row's lanes
   const int v = (blockIdx.x * blockDim.x + threadIdx.x) / LPR;
   const int64_t nt = S.stats[1];
+  float my_loss = 0.f;  // this row's CE (lane 0 of the row's group)
   if (v < G.rows) {
     const int64_t ld = G.ld;
     const int k = G.k;
@@ -47,21 +48,23 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
       S.dlog[(int64_t)v * ldd + c] = Elem<T>::from_f(g);
       if (S.dlog_s) S.dlog_s[(int64_t)v * ldd + c] = Elem<T>::from_f(g * sv);
     }
-    if (gl == 0) S.row_loss[v] = tr ? lse - z[y] : 0.f;
+    if (gl == 0 && tr) my_loss = lse - z[y];
   }
+  // per-CTA partial sums (fixed order), then the last CTA of the slot adds the gridDim.x partials
+  using Red = cub::BlockReduce<float, 256>;
+  __shared__ typename Red::TempStorage tr;
+  const float part = Red(tr).Sum(my_loss);
   __shared__ bool s_last;
-  __syncthreads();
   if (threadIdx.x == 0) {
+    S.row_loss[blockIdx.x] = part;
     __threadfence();
     s_last = atomicAdd(S.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  using Red = cub::BlockReduce<float, 256>;
-  __shared__ typename Red::TempStorage tr;
   float acc = 0.f;
-  for (int r = threadIdx.x; r < G.rows; r += blockDim.x) acc += __ldcg(S.row_loss + r);
+  for (int r = threadIdx.x; r < (int)gridDim.x; r += blockDim.x) acc += __ldcg(S.row_loss + r);
   const float tot = Red(tr).Sum(acc);
   if (threadIdx.x == 0) {
     const float l = nt > 0 ? tot / (float)nt : 0.f;
