@@ -31,9 +31,9 @@ def free_port():
     return p
 
 
-def make(opt_state="reset"):
+def make(opt_state="reset", arch="sage"):
     g = generate(tiny_spec(n=240, nnz=1500, d0=12, classes=4, clusters=8), seed=3)
-    o = O.OracleGIST(arch="sage", dims=list(DIMS), optimizer="adam", clusters_per_batch=2, batch_seed=9,
+    o = O.OracleGIST(arch=arch, dims=list(DIMS), optimizer="adam", clusters_per_batch=2, batch_seed=9,
                      opt_state=opt_state)
     o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
                  g["cluster_ids"], g["num_clusters"])
@@ -58,9 +58,9 @@ def unpack(flat, shapes):
     return out
 
 
-def sharded_run(rank, world, opt_state="reset"):
+def sharded_run(rank, world, opt_state="reset", arch="sage"):
     from paper_2102_10424_b200 import gist
-    o = make(opt_state)
+    o = make(opt_state, arch)
     spr = gist.slots_per_rank(M, world)
     mine = gist.local_slots(M, world, rank)
     history = []
@@ -100,18 +100,18 @@ def sharded_run(rank, world, opt_state="reset"):
     return history
 
 
-def worker(rank, world, port, q, opt_state="reset"):
+def worker(rank, world, port, q, opt_state="reset", arch="sage"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        hist = sharded_run(rank, world, opt_state)
+        hist = sharded_run(rank, world, opt_state, arch)
         q.put((rank, [[w.tobytes() for w in th] for th in hist]))
     finally:
         dist.destroy_process_group()
 
 
-def reference(opt_state="reset"):
-    o = make(opt_state)
+def reference(opt_state="reset", arch="sage"):
+    o = make(opt_state, arch)
     hist = []
     for t in range(ROUNDS):
         o.partition(seed=77, m=M)
@@ -133,21 +133,68 @@ def test_layout_functions():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("opt_state", ["reset", "persistent"])
-def test_world2_gloo_bit_identical_to_world1(opt_state):
+@pytest.mark.parametrize("opt_state,arch", [("reset", "sage"), ("persistent", "sage"), ("reset", "gat")])
+def test_world2_gloo_bit_identical_to_world1(opt_state, arch):
+    """(GAT, R21: the last layer's attention rows are the mean of all m copies, so every rank
+    needs every slot's copy -- the same all-gather delivers them.)"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q, opt_state)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, opt_state, arch)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ref = reference(opt_state)
+    ref = reference(opt_state, arch)
     for t in range(ROUNDS):
         assert len(ref[t]) == len(res[0][t]) == (len(DIMS) - 1) * (3 if opt_state == "persistent" else 1)
         for l in range(len(ref[t])):        # weights (and global moments) per layer
             want = ref[t][l].tobytes()
             assert res[0][t][l] == want and res[1][t][l] == want, (t, l)
+
+
+def eval_worker(rank, world, port, q):
+    """Partition-wise eval protocol of gist_eval_parts for world > 1 (R20): rank r evaluates the
+    partitions p with p mod W == r, the per-partition (CE sum, correct, count) triples are summed
+    across ranks (the library's one ncclAllReduce; gloo here), every rank averages."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o = make()
+        n = len(o.labels)
+        part = (np.arange(n) * 5) % 7
+        mine = [p for p in range(7) if p % world == rank]
+        _, _, lp, ap = o.eval_partitions(0, part, 7, parts=mine)
+        sums = np.zeros((7, 3))
+        for p in mine:
+            cnt = float(np.sum((part == p) & (o.split == 0)))
+            if cnt:
+                sums[p] = [lp[p] * cnt, ap[p] * cnt, cnt]
+        t = torch.from_numpy(sums)
+        dist.all_reduce(t)
+        s = t.numpy()
+        ok = s[:, 2] > 0
+        q.put((rank, float(np.mean(s[ok, 0] / s[ok, 2])), float(np.mean(s[ok, 1] / s[ok, 2]))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_world2_gloo_partition_eval_protocol():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=eval_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (l, a)) for r, l, a in (q.get(timeout=240) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    o = make()
+    n = len(o.labels)
+    lw, aw, _, _ = o.eval_partitions(0, (np.arange(n) * 5) % 7, 7)
+    for r in (0, 1):
+        assert res[r][0] == pytest.approx(lw, rel=1e-12) and res[r][1] == pytest.approx(aw, rel=1e-12)
