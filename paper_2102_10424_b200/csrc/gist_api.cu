@@ -1557,11 +1557,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   const double per_nnz = 4.0 * g.count;
   auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
     int id = -1;
-    static const int twice = [] { const char* e = std::getenv("GIST_EXP_TWICE"); return e ? atoi(e) : 0; }();
-    if (twice == 2) spmm_group<T, T>(G, s);  // EXPERIMENT: warm every operand first (wrong results)
     if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, bytes, per_nnz, nnz_slot);
     spmm_group<T, T>(G, s);
-    if (twice == 1) spmm_group<T, T>(G, s);  // EXPERIMENT: timed twice back to back
     prof_end(c, s, id);
     ++c->nk;
   };
