@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--zeta", type=int, default=0, help="local iterations per round (0 = paper's zeta, capped)")
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--agg", default="allgather", choices=["allgather", "p2p"],
+                    help="subAgg transport (gist_config.agg_mode; p2p = SURVEY §8 f2 peer stores)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--profile-stride", type=int, default=32,
                     help="every N-th step is profiled per kernel class (serialised: no side-stream overlap)")
@@ -205,7 +207,8 @@ def main():
             dist.broadcast_object_list(obj, src=0)
             uid = obj[0]
         return G.Gist(spec.arch, spec.dims, optimizer="adam", precision=args.precision, clusters_per_batch=spec.q,
-                      batch_seed=1, rank=rank, world_size=world, device=local, nccl_unique_id=uid)
+                      batch_seed=1, rank=rank, world_size=world, device=local, nccl_unique_id=uid,
+                      agg_mode=args.agg)
 
     def barrier():
         if world > 1:
@@ -350,6 +353,7 @@ def main():
                    f"(n={g['n']}, nnz={int(g['row_ptr'][-1])})", "arch": spec.arch, "dims": list(spec.dims),
                    "m": spec.m, "q": spec.q, "zeta": zeta, "step": "one GIST round (partition + zeta subTrain "
                    "steps of all m sub-GCNs + aggregate)", "parallelism": f"gist-m{spec.m}-over-{world}gpu",
+                   "agg": args.agg,
                    "precision": args.precision, "l2": "256 MiB buffer written between timed rounds",
                    "epoch_s": spec.m * B / value, "batches_per_epoch": B, "last_n_b": nb_last,
                    "last_nnz_b": nnzb_last, "gen_s": t_gen, "profile_stride": args.profile_stride,

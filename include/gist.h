@@ -67,6 +67,17 @@ enum { GIST_GRAPH_DEVICE = 0, GIST_GRAPH_HOST = 1 }; /* graph resident in HBM / 
  * over; GIST with m = 1 is then plain Adam training without restarts (the paper is silent,
  * PAPER.md:660).  Ignored for SGD. */
 enum { GIST_OPT_STATE_RESET = 0, GIST_OPT_STATE_PERSISTENT = 1 };
+/* subAgg transport.  ALLGATHER (default): one
+ * ncclAllGather of the packed slot buffers, then every rank scatters all m slots into its
+ * own replica of Theta.  P2P: Theta (and the f3 moments) live in one cudaMalloc region
+ * whose CUDA IPC handle every rank opens at gist_load_graph; gist_aggregate has each owner
+ * write its own slots' blocks straight into every rank's replica over NVLink peer stores
+ * (one kernel per layer reads a block once and stores it W times), bracketed by two
+ * one-word NCCL all-reduces used as barriers (no rank still reads its replica while peers
+ * write; no rank reads it before every peer's stores completed).  No receive buffer, no
+ * second pass over the gathered bytes.  Not available for GAT (R21 averages the m copies
+ * of the attention rows, which needs every copy on every rank): GIST_E_UNSUPPORTED. */
+enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1 };
 
 typedef struct {
   int32_t arch;               /* GIST_ARCH_* */
@@ -83,6 +94,7 @@ typedef struct {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0 when world_size > 1, else NULL */
   void* stream;               /* optional cudaStream_t to order work on; NULL = library-owned */
   int32_t opt_state;          /* GIST_OPT_STATE_* (default RESET) */
+  int32_t agg_mode;           /* GIST_AGG_* (default ALLGATHER) */
 } gist_config;
 
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
@@ -130,8 +142,9 @@ gist_status gist_subtrain(gist_ctx* ctx, int32_t local_iters, float lr, float* m
 
 /* subAgg: every slot's block replaces its entries of the
  * global Theta (bitwise copy, R9); entries outside all blocks are untouched.
- * Collective: one ncclAllGather of the packed slot buffers when world_size > 1.
- * Increments the round counter t. */
+ * Collective: one ncclAllGather of the packed slot buffers when world_size > 1
+ * (agg_mode ALLGATHER), or peer stores into every replica between two barriers
+ * (agg_mode P2P).  Both give bit-identical Theta.  Increments the round counter t. */
 gist_status gist_aggregate(gist_ctx* ctx);
 
 /* Forward of the global model on the full graph (full-graph operator, R1/R2;

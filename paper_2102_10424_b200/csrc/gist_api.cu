@@ -182,7 +182,12 @@ struct gist_ctx {
   cudaEvent_t hstate_ev = nullptr;
   StepPlan<float> plan_f;
   StepPlan<bf16> plan_b;
-  float* Wrecv = nullptr;                      // world * slots_per_rank * S_max (world > 1)
+  float* Wrecv = nullptr;                      // world * slots_per_rank * S_max (world > 1, ALLGATHER)
+  // agg_mode P2P (f2): Theta (+ f3 moments) in one cudaMalloc region; peer_base[r] = rank r's
+  // region (opened from its IPC handle; peer_base[rank] = p2p_base); one-word barrier buffer
+  char* p2p_base = nullptr;
+  std::vector<char*> peer_base;
+  float* barrier_word = nullptr;
   int alloc_m = 0;
   void* sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
@@ -426,6 +431,9 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (cfg->optimizer != GIST_OPT_SGD && cfg->optimizer != GIST_OPT_ADAM) return GIST_E_ARG;
   if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
   if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
+  if (cfg->agg_mode != GIST_AGG_ALLGATHER && cfg->agg_mode != GIST_AGG_P2P) return GIST_E_ARG;
+  if (cfg->agg_mode == GIST_AGG_P2P && (cfg->arch == GIST_ARCH_GAT || cfg->world_size > kMaxPeers))
+    return GIST_E_UNSUPPORTED;  // R21 needs every copy of the attention rows; PeerDst holds 8 ranks
   if (cfg->clusters_per_batch < 1 || cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
     return GIST_E_ARG;
   for (int l = 0; l <= cfg->num_layers; ++l)
@@ -518,6 +526,9 @@ extern "C" void gist_destroy(gist_ctx* c) {
   free_slots(c);
   for (void* p : c->allocs) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
+  for (size_t r = 0; r < c->peer_base.size(); ++r)
+    if (c->peer_base[r] && c->peer_base[r] != c->p2p_base) cudaIpcCloseMemHandle(c->peer_base[r]);
+  if (c->p2p_base) cudaFree(c->p2p_base);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
@@ -562,6 +573,57 @@ extern "C" int64_t gist_stat(gist_ctx* c, int32_t which) {
 }
 
 // ============================================================ load graph ===
+// agg_mode P2P: Theta (and the f3 moments) in ONE cudaMalloc region (CUDA IPC
+// exports whole cudaMalloc allocations, not stream-ordered pool blocks), laid out identically on
+// every rank; the 64-byte IPC handles travel in one ncclAllGather and every rank opens its
+// peers' regions (NVLink peer access enabled lazily by the driver).  World 1: the only
+// "peer" is the local region, and gist_aggregate reduces to the ALLGATHER path's local scatter.
+static gist_status p2p_setup(gist_ctx* c) {
+  const int W = c->cfg.world_size, L = c->L;
+  const int parts = persistent_adam(c) ? 3 : 1;
+  std::vector<size_t> off(L);
+  size_t floats = 0;
+  for (int l = 0; l < L; ++l) {
+    off[l] = floats;
+    floats += (size_t)pad8(kphys(c, c->dims[l])) * pad8(c->dims[l + 1]);  // 32-byte aligned layers
+  }
+  const size_t bytes = floats * 4 * parts;
+  if (cudaMalloc(reinterpret_cast<void**>(&c->p2p_base), bytes) != cudaSuccess) {
+    cudaGetLastError();
+    c->p2p_base = nullptr;
+    return fail(c, GIST_E_OOM, "p2p: cudaMalloc of the Theta region failed");
+  }
+  float* f = reinterpret_cast<float*>(c->p2p_base);
+  if (parts == 3) c->theta_m.assign(L, nullptr), c->theta_v.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    c->theta[l] = f + off[l];
+    if (parts == 3) c->theta_m[l] = f + floats + off[l], c->theta_v[l] = f + 2 * floats + off[l];
+  }
+  TRY(dalloc_t(c, &c->barrier_word, 1));
+  CK(cudaMemsetAsync(c->barrier_word, 0, 4, c->stream));
+  c->peer_base.assign(W, nullptr);
+  c->peer_base[c->cfg.rank] = c->p2p_base;
+  if (W == 1) return GIST_OK;
+  cudaIpcMemHandle_t mine;
+  CK(cudaIpcGetMemHandle(&mine, c->p2p_base));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  char* hd = nullptr;
+  TRY(dalloc_t(c, &hd, (size_t)64 * (W + 1)));
+  CK(cudaMemcpyAsync(hd, &mine, 64, cudaMemcpyHostToDevice, c->stream));
+  NK(ncclAllGather(hd, hd + 64, 64, ncclChar, c->comm, c->stream));
+  std::vector<cudaIpcMemHandle_t> all(W);
+  CK(cudaMemcpyAsync(all.data(), hd + 64, (size_t)64 * W, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c, hd);
+  for (int r = 0; r < W; ++r) {
+    if (r == c->cfg.rank) continue;
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+    c->peer_base[r] = static_cast<char*>(p);
+  }
+  return GIST_OK;
+}
+
 extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                                        int64_t nnz, const float* X, const int32_t* labels, int32_t num_classes,
                                        const uint8_t* split, const int32_t* cluster_ids, int32_t num_clusters) {
@@ -737,12 +799,13 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   c->theta.assign(c->L, nullptr);
   c->th_K.assign(c->L, 0);
   c->th_N.assign(c->L, 0);
+  if (c->cfg.agg_mode == GIST_AGG_P2P) TRY(p2p_setup(c));
   for (int l = 0; l < c->L; ++l) {
     c->th_K[l] = kphys(c, c->dims[l]);
     c->th_N[l] = pad8(c->dims[l + 1]);
-    TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
+    if (!c->p2p_base) TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
     CK(cudaMemsetAsync(c->theta[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, s));
-    if (persistent_adam(c)) {  // f3: global moments, same physical layout as Theta
+    if (persistent_adam(c) && !c->p2p_base) {  // f3: global moments, same physical layout as Theta
       c->theta_m.resize(c->L, nullptr);
       c->theta_v.resize(c->L, nullptr);
       TRY(dalloc_t(c, &c->theta_m[l], (size_t)c->th_K[l] * c->th_N[l]));
@@ -847,7 +910,7 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     TRY(dalloc_t(c, &c->Wball, tot));
     CK(cudaMemsetAsync(c->Wball, 0, tot * 2, c->stream));
   }
-  if (W > 1) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
+  if (W > 1 && c->cfg.agg_mode == GIST_AGG_ALLGATHER) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
   if (!c->dstate) {
     TRY(dalloc_t(c, &c->dstate, 1));
     CK(cudaMallocHost(&c->hstate, sizeof(StepState)));
@@ -1883,6 +1946,35 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   std::vector<float*> wvec(c->theta.begin(), c->theta.end());
   std::vector<Part> parts = {{c->Wall, &wvec}};
   if (persistent_adam(c)) parts.push_back({c->Mall, &c->theta_m}), parts.push_back({c->Vall, &c->theta_v});
+  if (c->p2p_base) {  // agg_mode P2P (f2): owners store their blocks into every replica
+    // barrier 1: every rank has finished this round's reads of its replica (gist_partition's
+    // extraction) before any peer overwrites it
+    if (W > 1) NK(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+    for (const Part& pt : parts)
+      for (int i = c->cfg.rank; i < c->m; i += W) {
+        const int j = i / W;
+        const float* w = pt.local + (size_t)j * c->S_max;
+        for (int l = 0; l < c->L; ++l) {
+          const LayerShape& sh = c->shapes[i][l];
+          LayerMap mp;
+          mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = 0; mp.half = sh.half;
+          mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
+          mp.ldg = c->th_N[l];
+          PeerDst pd;
+          pd.n = W;
+          const size_t off = (size_t)(reinterpret_cast<char*>((*pt.global)[l]) - c->p2p_base);
+          for (int r = 0; r < W; ++r) pd.dst[r] = reinterpret_cast<float*>(c->peer_base[r] + off);
+          PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 4.0 * (2.0 + W), s, scatter_sub_peers(pd, mp, w + sh.off, s));
+        }
+      }
+    // barrier 2: every peer's stores into this replica have completed before anything reads it
+    if (W > 1) NK(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+    c->prof_now = false;
+    TRY(check_launch(c, "aggregate"));
+    c->round += 1;
+    c->state = S_PARAMS;
+    return GIST_OK;
+  }
   for (const Part& pt : parts) {
     const float* src = pt.local;
     if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink

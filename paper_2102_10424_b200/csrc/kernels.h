@@ -339,6 +339,13 @@ struct LayerMap {
 };
 void extract_sub(const float* theta, const LayerMap& m, float* w_sub, cudaStream_t s);
 void scatter_sub(float* theta, const LayerMap& m, const float* w_sub, cudaStream_t s);
+// agg_mode P2P (f2): one read of the block, one store per rank's replica of the layer
+constexpr int kMaxPeers = 8;
+struct PeerDst {
+  float* dst[kMaxPeers];
+  int n = 0;
+};
+void scatter_sub_peers(const PeerDst& d, const LayerMap& m, const float* w_sub, cudaStream_t s);
 void glorot_init(float* theta, int rows_logical, int cols, int sage, int d_l, int glob_half, int64_t ldg,
                  uint32_t layer, uint64_t seed, float scale, cudaStream_t s);
 

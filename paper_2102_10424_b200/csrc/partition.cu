@@ -119,6 +119,29 @@ void scatter_sub(float* theta, const LayerMap& m, const float* w_sub, cudaStream
   }
 }
 
+// subAgg over peer memory (agg_mode P2P): the owner reads its block once and
+// stores it into every rank's replica (d.dst[r] is rank r's copy of this layer of Theta, a
+// peer pointer opened from its CUDA IPC handle; d.dst[rank] is the local one).  Same element
+// placement as k_scatter; the system-scope fence orders the peer stores before this thread
+// retires, ahead of the NCCL barrier that follows the launch on the stream.
+__global__ void k_scatter_peers(const PeerDst d, const LayerMap m, const float* __restrict__ w, int p0) {
+  const int p = p0 + blockIdx.y;
+  const int64_t gr = glob_row(m, p);
+  if (gr < 0) return;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m.ncols; q += gridDim.x * blockDim.x) {
+    const float v = w[(int64_t)p * m.Np + q];
+    const int64_t o = gr * m.ldg + (m.cols ? m.cols[q] : q);
+    for (int r = 0; r < d.n; ++r) d.dst[r][o] = v;
+  }
+  __threadfence_system();
+}
+void scatter_sub_peers(const PeerDst& d, const LayerMap& m, const float* w_sub, cudaStream_t s) {
+  for (int p0 = 0; p0 < m.Kp; p0 += 65535) {
+    const int rows = m.Kp - p0 < 65535 ? m.Kp - p0 : 65535;
+    k_scatter_peers<<<grid_for(m, rows), 256, 0, s>>>(d, m, w_sub, p0);
+  }
+}
+
 // Glorot uniform (R11): u = (w0 >> 8) 2^-24, t = 2u - 1 (exact), W = fl32(t * scale).
 // Logical (r, c) of Theta_l (SAGE: r < d self rows, r >= d neighbour rows).
 __global__ void k_glorot(float* __restrict__ theta, int rows, int cols, int sage, int d_l, int glob_half,

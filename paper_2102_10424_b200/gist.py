@@ -34,6 +34,7 @@ PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregat
 
 
 GIST_OPT_STATE_RESET, GIST_OPT_STATE_PERSISTENT = 0, 1
+GIST_AGG_ALLGATHER, GIST_AGG_P2P = 0, 1
 
 
 class GistConfig(C.Structure):
@@ -43,7 +44,7 @@ class GistConfig(C.Structure):
         ("precision", C.c_int32), ("clusters_per_batch", C.c_int32), ("batch_seed", C.c_uint64),
         ("graph_residency", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("device", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
-        ("opt_state", C.c_int32),
+        ("opt_state", C.c_int32), ("agg_mode", C.c_int32),
     ]
 
 
@@ -111,7 +112,8 @@ class Gist:
     def __init__(self, arch: str, dims, optimizer: str = "adam", precision: str = "fp32",
                  clusters_per_batch: int = 1, batch_seed: int = 0, rank: int = 0, world_size: int = 1,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream: int | None = None,
-                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset"):
+                 beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset",
+                 agg_mode: str = "allgather"):
         L = lib()
         self.arch = arch
         self.dims = [int(d) for d in dims]
@@ -133,6 +135,7 @@ class Gist:
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         cfg.stream = stream
         cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
+        cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P}[agg_mode]
         self._cfg = cfg
         h = C.c_void_p()
         self._check(L.gist_create(C.byref(cfg), C.byref(h)), None)

@@ -58,7 +58,30 @@ def unpack(flat, shapes):
     return out
 
 
-def sharded_run(rank, world, opt_state="reset", arch="sage"):
+def p2p_exchange(rank, world, blocks_of, apply):
+    """agg_mode P2P as gist_aggregate runs it: barrier; each owner stores its
+    own slots i = rank, rank + W, ... (i // W = local index) into every rank's replica; barrier.
+    A peer store is a point-to-point send here (gloo has no peer memory); the oracle is FP64,
+    and the copy is bitwise either way (R9)."""
+    dist.barrier()
+    own = list(range(rank, M, world))
+    reqs = []
+    for i in own:
+        buf = torch.from_numpy(np.ascontiguousarray(blocks_of(i), dtype=np.float64))
+        apply(i, buf.numpy())                               # the local replica
+        reqs += [dist.isend(buf, dst=r, tag=i) for r in range(world) if r != rank]
+    for i in range(M):
+        if i in own:
+            continue
+        buf = torch.zeros(blocks_of(i).size, dtype=torch.float64)
+        dist.recv(buf, src=i % world, tag=i)                # owner = gist_slot_owner(i, W)
+        apply(i, buf.numpy())
+    for r in reqs:
+        r.wait()
+    dist.barrier()
+
+
+def sharded_run(rank, world, opt_state="reset", arch="sage", transport="allgather"):
     from paper_2102_10424_b200 import gist
     o = make(opt_state, arch)
     spr = gist.slots_per_rank(M, world)
@@ -78,6 +101,20 @@ def sharded_run(rank, world, opt_state="reset", arch="sage"):
         if opt_state == "persistent":
             tensors += [(k, [[st[k] for st in so] for so in o.opt]) for k in ("m", "v")]
         for name, blocks in tensors:
+            if transport == "p2p":
+                def blocks_of(i, blocks=blocks):
+                    return np.concatenate([b.ravel() for b in blocks[i]])
+
+                def apply(i, flat, name=name):
+                    got = unpack(flat, shapes[i])
+                    if name == "w":
+                        o.sub[i] = got
+                    else:
+                        for l in range(len(got)):
+                            o.opt[i][l][name] = got[l]
+                            o.opt[i][l]["t"] = o.t_global + ZETA
+                p2p_exchange(rank, world, blocks_of, apply)
+                continue
             send = torch.from_numpy(pack(blocks, mine, spr, smax))
             recv = [torch.zeros_like(send) for _ in range(world)]
             dist.all_gather(recv, send)
@@ -100,11 +137,11 @@ def sharded_run(rank, world, opt_state="reset", arch="sage"):
     return history
 
 
-def worker(rank, world, port, q, opt_state="reset", arch="sage"):
+def worker(rank, world, port, q, opt_state="reset", arch="sage", transport="allgather"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        hist = sharded_run(rank, world, opt_state, arch)
+        hist = sharded_run(rank, world, opt_state, arch, transport)
         q.put((rank, [[w.tobytes() for w in th] for th in hist]))
     finally:
         dist.destroy_process_group()
@@ -133,14 +170,16 @@ def test_layout_functions():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("opt_state,arch", [("reset", "sage"), ("persistent", "sage"), ("reset", "gat")])
-def test_world2_gloo_bit_identical_to_world1(opt_state, arch):
+@pytest.mark.parametrize("opt_state,arch,transport", [("reset", "sage", "allgather"), ("persistent", "sage", "allgather"),
+                                                      ("reset", "gat", "allgather"), ("reset", "sage", "p2p"),
+                                                      ("persistent", "sage", "p2p")])
+def test_world2_gloo_bit_identical_to_world1(opt_state, arch, transport):
     """(GAT, R21: the last layer's attention rows are the mean of all m copies, so every rank
-    needs every slot's copy -- the same all-gather delivers them.)"""
+    needs every slot's copy -- the same all-gather delivers them; agg_mode P2P refuses GAT.)"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q, opt_state, arch)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, q, opt_state, arch, transport)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
