@@ -1070,6 +1070,18 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     maxM = ops[i].M > maxM ? ops[i].M : maxM;
   }
   P->bn = maxN > 128 ? 256 : 128;  // persistent kernel: wide tiles amortise the epilogue
+  // A single-op launch (one slot per lockstep group: one sub-GCN per GPU at W = m) whose
+  // 256-wide tiles leave SMs idle takes 128-wide ones: single-slot C3 groups 2,806 -> 2,863
+  // steps/s; measured slower for 2-op (4,627 -> 4,564) and 8-op (8,46x -> 8,364) launches, so
+  // the rule stops at one op (profiles/r01p_*; GIST_BN_FEW=<max ops> overrides, 0 = off)
+  {
+    static const int few = [] { const char* e = std::getenv("GIST_BN_FEW"); return e ? atoi(e) : 1; }();
+    if (P->bn == 256 && n <= few) {
+      int64_t t256 = 0;
+      for (int i = 0; i < n; ++i) t256 += cdiv(ops[i].M, BM) * cdiv(ops[i].N, 256);
+      if (t256 < (int64_t)num_sms()) P->bn = 128;
+    }
+  }
   // CTA pairs for large, long-K GEMMs (>= 4 tiles per SM and K >= 2048: measured 82 -> 88% of
   // peak at width 4096); short-K GEMMs (the C3 step's dX, K = 512: 27 -> 41 us as pairs) and
   // the cluster-block aggregation stay on one CTA per tile
