@@ -18,8 +18,8 @@
  *  - Errors: every call returns a gist_status; a message is available from
  *    gist_last_error().  A CUDA or NCCL failure poisons the context: every
  *    later call returns the same sticky status (GIST_E_CUDA / GIST_E_NCCL).
- *  - State machine: CREATED -> load_graph -> GRAPH -> init_params/set_params
- *    -> PARAMS -> partition -> PARTITIONED -> subtrain* -> aggregate -> PARAMS.
+ *  - State machine: CREATED -> load_graph -> GRAPH -> init_params (or set_params of
+ *    every layer) -> PARAMS -> partition -> PARTITIONED -> subtrain* -> aggregate -> PARAMS.
  *    Out-of-order calls return GIST_E_STATE.
  *  - Multi-GPU: one process (context) per GPU.  Slot (sub-GCN) i lives on rank
  *    i mod world_size.  gist_aggregate and gist_eval are collectives: every rank
@@ -59,7 +59,7 @@ typedef enum {
 enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1, GIST_ARCH_GAT = 2 };
 enum { GIST_OPT_SGD = 0, GIST_OPT_ADAM = 1 };        /* subTrain = SGD step PAPER.md:168; Adam PAPER.md:660,680,690 */
 enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1 };     /* FP32 parity mode / BF16 tensor-core mode (R13) */
-enum { GIST_GRAPH_DEVICE = 0, GIST_GRAPH_HOST = 1 }; /* graph resident in HBM / in pinned host memory (streamed per step) */
+enum { GIST_GRAPH_DEVICE = 0 };                     /* the graph is resident in HBM (the only residency built) */
 /* Adam state across rounds: RESET = moments and step counter restart at every gist_partition
  * (R8; the default).  PERSISTENT = SURVEY.md §8 f3: global first / second moments
  * shaped like Theta are partitioned, extracted and aggregated with the weights (and
@@ -79,6 +79,20 @@ enum { GIST_OPT_STATE_RESET = 0, GIST_OPT_STATE_PERSISTENT = 1 };
  * of the attention rows, which needs every copy on every rank): GIST_E_UNSUPPORTED. */
 enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1 };
 
+/* Loopback transport (tests): W contexts of ONE process on one device stand in for W ranks.
+ * Every collective of gist_aggregate / gist_eval / gist_eval_parts (all-gather, sum all-reduce,
+ * barrier, the P2P replica-pointer exchange) is carried out by the host -- stream synchronise,
+ * rendezvous of the W calling threads, device-to-device copies -- instead of NCCL, so the
+ * library's W > 1 code paths (slot ownership i mod W, packed-buffer offsets, the unpack /
+ * scatter of the gathered buffers, peer stores, the row-split eval) run unchanged on one GPU.
+ * No kernel ever waits on another rank.  Each rank's context must be driven by its own host
+ * thread: a collective returns only once all W ranks have entered it.  Not a multi-GPU
+ * transport: across GPUs use NCCL (gist_config.nccl_unique_id).
+ *   gist_loopback_create: GIST_E_ARG if world_size < 1.  The group outlives its contexts. */
+typedef struct gist_loopback gist_loopback;
+gist_status gist_loopback_create(int32_t world_size, gist_loopback** out);
+void gist_loopback_destroy(gist_loopback* lb);
+
 typedef struct {
   int32_t arch;               /* GIST_ARCH_* */
   int32_t num_layers;         /* L >= 1 */
@@ -95,6 +109,7 @@ typedef struct {
   void* stream;               /* optional cudaStream_t to order work on; NULL = library-owned */
   int32_t opt_state;          /* GIST_OPT_STATE_* (default RESET) */
   int32_t agg_mode;           /* GIST_AGG_* (default ALLGATHER) */
+  gist_loopback* loopback;    /* tests: loopback group of world_size ranks replacing NCCL, or NULL */
 } gist_config;
 
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
@@ -105,7 +120,8 @@ void gist_config_default(gist_config* cfg);
 gist_status gist_nccl_unique_id(void* out128);
 
 /* Creates a context on cfg->device.  Errors: GIST_E_ARG (dims), GIST_E_UNSUPPORTED
- * (no CUDA device of compute capability 10.x), GIST_E_NCCL. */
+ * (no CUDA device of compute capability 10.x; a GAT layer wider than 2,048 output units;
+ * agg_mode P2P with GAT or more than 8 ranks), GIST_E_NCCL. */
 gist_status gist_create(const gist_config* cfg, gist_ctx** out);
 
 /* Loads graph G (n nodes, features X in R^{n x d_0}) and its Cluster
@@ -135,9 +151,10 @@ gist_status gist_partition(gist_ctx* ctx, uint64_t seed, int32_t m);
 
 /* subTrain: local_iters (zeta) steps for every local
  * slot, each on its own Cluster mini-batch (R7): batch build, forward (Eq. 2),
- * softmax-CE (R4), backward, Adam/SGD with learning rate lr.  Slots run
- * concurrently on separate streams.  mean_loss: NULL or float[m]; entries of
- * this rank's slots receive the mean loss over the local_iters steps, others 0. */
+ * softmax-CE (R4), backward, Adam/SGD with learning rate lr.  The local slots run
+ * in lockstep: every kernel of a step is one grouped launch over (up to 8) slots.
+ * mean_loss: NULL or float[m]; entries of this rank's slots receive the mean loss
+ * over the local_iters steps, others 0. */
 gist_status gist_subtrain(gist_ctx* ctx, int32_t local_iters, float lr, float* mean_loss);
 
 /* subAgg: every slot's block replaces its entries of the
@@ -149,7 +166,12 @@ gist_status gist_aggregate(gist_ctx* ctx);
 
 /* Forward of the global model on the full graph (full-graph operator, R1/R2;
  * no output scaling, R10); mean CE loss and accuracy over nodes with
- * split == split_code.  Either output may be NULL. */
+ * split == split_code.  Either output may be NULL.
+ * World > 1 (collective): GCN / GraphSAGE rows are split into W blocks of
+ * ceil(n / W) relabelled rows; each rank computes its block of every layer, one all-gather
+ * per hidden layer assembles the next layer's input, and one sum all-reduce combines the
+ * loss / accuracy counts.  GAT runs the whole forward on every rank.
+ * Errors: GIST_E_STATE (open round / no params), GIST_E_ARG (split code not in 0..3). */
 gist_status gist_eval(gist_ctx* ctx, int32_t split_code, float* loss, float* acc);
 
 /* Partition-wise evaluation of the global model ("for d_i > 4096
@@ -172,6 +194,14 @@ gist_status gist_eval_parts(gist_ctx* ctx, int32_t split_code, const int32_t* pa
                             int64_t max_rows, float* loss, float* acc, float* part_loss, float* part_acc);
 
 /* ---------------- inspection / parity hooks ---------------- */
+/* Per-node logits of the global model from exactly the forward that gist_eval (mode 0, the
+ * full graph) or gist_eval_parts (mode 1, every partition on its own induced subgraph, R20)
+ * runs.  out: host float[n * d_L], row = ORIGINAL node id.  part_ids / num_parts / max_rows
+ * as for gist_eval_parts (ignored for mode 0).  Collective like the evaluation it mirrors;
+ * every rank receives all rows.  Errors: GIST_E_STATE, GIST_E_ARG (mode, null out, ids). */
+gist_status gist_eval_logits(gist_ctx* ctx, int32_t mode, const int32_t* part_ids, int32_t num_parts,
+                             int64_t max_rows, float* out);
+
 /* Global Theta_l, logical row-major: rows = d_l (GCN), 2*d_l (SAGE: self rows then
  * neighbour rows) or d_l + 2 (GAT: W rows, then a_src, a_dst), cols = d_{l+1}.
  * out / in: float[rows*cols]. */
@@ -221,7 +251,8 @@ enum {
   GIST_PROF_BATCH = 0, GIST_PROF_SPMM = 1, GIST_PROF_GEMM = 2, GIST_PROF_LOSS = 3, GIST_PROF_OPTIM = 4,
   GIST_PROF_PARTITION = 5, GIST_PROF_AGGREGATE = 6,
   GIST_PROF_AGG_TC = 7, /* block-diagonal (intra-cluster) aggregation on tensor cores; work = FLOPs */
-  GIST_PROF_N = 8
+  GIST_PROF_COMM = 8,   /* subAgg collective (all-gather / barriers); work = bytes received per rank */
+  GIST_PROF_N = 9
 };
 gist_status gist_profile(gist_ctx* ctx, int32_t stride);
 gist_status gist_profile_get(gist_ctx* ctx, int32_t cls, double* ms, int64_t* launches, double* work);

@@ -72,68 +72,55 @@ __device__ __forceinline__ void load_row(const T* base, int64_t ld, int64_t r, i
   }
 }
 
-template <typename T, int NV>
+// Two dot products of one row (width w, any w; lane holds 4 consecutive columns of every
+// 128-column chunk, the chunks in order -- the summation order of the register-tile kernels)
+template <typename T>
+__device__ __forceinline__ void dot2(const T* row, int64_t w, const float* u1, const float* u2, int lane, float& p1,
+                                     float& p2) {
+  p1 = p2 = 0.f;
+  for (int64_t c = lane * 4; c < w; c += 128) {
+    float x[4];
+    ld4(row + c, x);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) p1 += x[q] * u1[c + q], p2 += x[q] * u2[c + q];
+  }
+  p1 = warp_sum(p1);
+  p2 = warp_sum(p2);
+}
+
+// s[v] = Z[v, :] . a_src, t[v] = Z[v, :] . a_dst (one warp per row)
+template <typename T>
 __global__ void __launch_bounds__(256) k_gat_scores(const __grid_constant__ GatGroup<T> Gp) {
   const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
-  float z[NV][4];
-  load_row<T, NV>(a.Z, a.ldz, v, a.w, lane, z);
-  float ps = 0.f, pt = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int64_t c = (int64_t)k * 128 + lane * 4;
-    if (c < a.w)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ps += z[k][q] * a.a_src[c + q], pt += z[k][q] * a.a_dst[c + q];
-  }
-  ps = warp_sum(ps);
-  pt = warp_sum(pt);
+  float ps, pt;
+  dot2(a.Z + v * a.ldz, a.w, a.a_src, a.a_dst, lane, ps, pt);
   if (lane == 0) a.s[v] = ps, a.t[v] = pt;
 }
 
 // wa[k] = W32[k, :] . a_src, wa[kw + k] = W32[k, :] . a_dst (fp32; one warp per row of W)
-template <typename T, int NV>
+template <typename T>
 __global__ void __launch_bounds__(256) k_gat_wa(const __grid_constant__ GatGroup<T> Gp) {
   const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (k >= a.kw) return;
-  float x[NV][4];
-  load_row<float, NV>(a.W32, a.ldw, k, a.w, lane, x);
-  float ps = 0.f, pt = 0.f;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int64_t c = (int64_t)j * 128 + lane * 4;
-    if (c < a.w)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ps += x[j][q] * a.a_src[c + q], pt += x[j][q] * a.a_dst[c + q];
-  }
-  ps = warp_sum(ps);
-  pt = warp_sum(pt);
+  float ps, pt;
+  dot2(a.W32 + k * a.ldw, a.w, a.a_src, a.a_dst, lane, ps, pt);
   if (lane == 0) a.wa[k] = ps, a.wa[a.kw + k] = pt;
 }
 
-// s[v] = H[v, :] . wa[0:kw], t[v] = H[v, :] . wa[kw:2kw]
-template <typename T, int NV>
+// s[v] = H[v, :] . wa[0:kw], t[v] = H[v, :] . wa[kw:2kw] (any input width kw, e.g. d_0 = 3,703)
+template <typename T>
 __global__ void __launch_bounds__(256) k_gat_scores_h(const __grid_constant__ GatGroup<T> Gp) {
   const GatLayer<T>& a = Gp.a[blockIdx.y];
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= a.rows) return;
-  float h[NV][4];
-  load_row<T, NV>(a.H, a.ldh, v, a.kw, lane, h);
-  float ps = 0.f, pt = 0.f;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int64_t c = (int64_t)j * 128 + lane * 4;
-    if (c < a.kw)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) ps += h[j][q] * a.wa[c + q], pt += h[j][q] * a.wa[a.kw + c + q];
-  }
-  ps = warp_sum(ps);
-  pt = warp_sum(pt);
+  float ps, pt;
+  dot2(a.H + v * a.ldh, a.kw, a.wa, a.wa + a.kw, lane, ps, pt);
   if (lane == 0) a.s[v] = ps, a.t[v] = pt;
 }
 
@@ -420,6 +407,9 @@ __global__ void __launch_bounds__(128) k_gat_da_sum(const __grid_constant__ GatG
 
 }  // namespace
 
+// the attention passes hold a row in registers: output widths up to kGatMaxWidth (gist_create
+// refuses wider GAT layers with GIST_E_UNSUPPORTED)
+static_assert(kGatMaxWidth == 16 * 128, "GAT_DISPATCH tops out at NV = 16 chunks of 128 columns");
 #define GAT_DISPATCH(KERNEL, W, ROWS)                                                            \
   do {                                                                                          \
     if ((ROWS) <= 0 || G.n <= 0) return;                                                        \
@@ -445,12 +435,13 @@ template <typename T>
 void gat_scores(const GatGroup<T>& G, cudaStream_t s) {
   int64_t w, rows, kw;
   group_max(G, w, rows, kw);
+  if (G.n <= 0) return;
   if (!G.a[0].H) {
-    GAT_DISPATCH(k_gat_scores, w, rows);
+    if (rows > 0) k_gat_scores<T><<<dim3((unsigned)cdiv(rows, 8), (unsigned)G.n), 256, 0, s>>>(G);
     return;
   }
-  GAT_DISPATCH(k_gat_wa, w, kw);
-  GAT_DISPATCH(k_gat_scores_h, kw, rows);
+  if (kw > 0) k_gat_wa<T><<<dim3((unsigned)cdiv(kw, 8), (unsigned)G.n), 256, 0, s>>>(G);
+  if (rows > 0) k_gat_scores_h<T><<<dim3((unsigned)cdiv(rows, 8), (unsigned)G.n), 256, 0, s>>>(G);
 }
 template <typename T>
 void gat_forward(const GatGroup<T>& G, cudaStream_t s) {

@@ -402,7 +402,7 @@ struct ProbBd {
   static constexpr int kMaxDesc = 3 * 64 + 4;
   static __device__ __forceinline__ void stage(const Group& G, int32_t* sdesc) {
     const int per = 3 * G.q + 4;
-    const int z = G.zfix >= 0 ? G.zfix : G.st->z;
+    const int z = G.st->z;
     for (int i = threadIdx.x; i < G.n * per; i += blockDim.x)
       sdesc[i] = G.s[i / per].desc[(size_t)z * per + (i % per)];
   }

@@ -16,6 +16,7 @@
 #include <nccl.h>
 
 #include "../../include/gist.h"
+#include "comm.h"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -23,6 +24,7 @@ using namespace gist;
 
 struct gist_ctx;
 static bool persistent_adam(const gist_ctx* c);
+static void drop_graphs(gist_ctx* c);
 
 bool gist::pdl_enabled() {
   static const bool on = [] { const char* e = std::getenv("GIST_PDL"); return !(e && e[0] == '0'); }();
@@ -113,11 +115,6 @@ struct gist_ctx {
   std::vector<int> dims;
   int L = 0, arch = 0, prec = 0;
   cudaStream_t stream = nullptr;
-  // GIST_STREAMS=2: the local slots run as two lockstep groups on two streams (fork / join
-  // per step) so one group's kernels fill the other's ramp-up / tail bubbles
-  int nstreams = 1;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   // dW stream (default; GIST_DW_STREAM=0 disables): the backward dW GEMMs (and, with one
   // lockstep group, the per-layer optimizer steps) run on a side stream, overlapping the rest
   // of the backward chain (dX -> aggregation); joined at the end of the step
@@ -126,18 +123,21 @@ struct gist_ctx {
   // run serialised so that the per-kernel event times of the live roofline are not inflated by
   // overlap (ncu's launch list is serialised too)
   cudaStream_t side_now = nullptr;
-  cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr, ev_dw_wread = nullptr;
-  // set per step: the optimizer runs per layer on the dW stream right after that layer's last
-  // reader of W (single lockstep group only), instead of one launch after the step
-  bool opt_per_layer = false;
-  // the next step's batch was built on the dW stream, overlapping this step's optimizer
+  cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr;
+  // this step's batches were built on the dW stream, overlapping the previous step's optimizer
   bool batch_prefetched = false;
-  bool agg0_prefetched = false;  // ... and its layer-0 aggregation
+  int cur_z = 0;  // host index of the step being enqueued (schedule bookkeeping / profiling only)
+  // CUDA graphs of one step, per variant [build * 2 + prefetch] (dropped at every plan rebuild)
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t nk = 0;  // kernels per replay
+  };
+  StepGraph graphs[4];
   bool own_stream = false;
   int state = S_CREATED;
   gist_status sticky = GIST_OK;
   std::string err;
-  ncclComm_t comm = nullptr;
+  Comm comm;  // NCCL communicator or loopback group (world > 1)
   cudaEvent_t fork_ev = nullptr;
   // graph (relabelled: clusters contiguous)
   int64_t n = 0, nnz = 0;
@@ -164,6 +164,7 @@ struct gist_ctx {
   std::vector<int64_t> th_K, th_N;
   // partition of the current round
   int m = 0;
+  std::vector<uint8_t> layer_set;              // set_params: layers written since load (PARAMS once all are)
   std::vector<int32_t*> units;                 // per dim (hidden dims only)
   std::vector<std::vector<int32_t>> offs;      // per dim, m+1
   std::vector<std::vector<LayerShape>> shapes;  // [slot][layer] for all m slots
@@ -179,6 +180,7 @@ struct gist_ctx {
   bool reassoc = false;                        // last SAGE layer re-associated (BF16, L >= 2)
   StepState* dstate = nullptr;                 // device step state (z, t, lr)
   StepState* hstate = nullptr;                 // pinned host staging for it
+  int32_t* bctr = nullptr;                     // per-group batch-build counters (BatchGroup::ctr), 2 per slot
   cudaEvent_t hstate_ev = nullptr;
   StepPlan<float> plan_f;
   StepPlan<bf16> plan_b;
@@ -222,6 +224,12 @@ gist_status fail(gist_ctx* c, gist_status s, const std::string& msg) {
     if (s == GIST_E_CUDA || s == GIST_E_NCCL) c->sticky = s;
   }
   return s;
+}
+
+// a collective's status: sticky on CUDA / NCCL failures (the message is already in c->err)
+gist_status coll(gist_ctx* c, gist_status st) {
+  if (st == GIST_E_CUDA || st == GIST_E_NCCL) c->sticky = st;
+  return st;
 }
 
 #define CK(x)                                                                              \
@@ -438,6 +446,9 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
     return GIST_E_ARG;
   for (int l = 0; l <= cfg->num_layers; ++l)
     if (cfg->dims[l] < 1) return GIST_E_SHAPE;
+  // GAT attention passes hold an output row in registers (gat.cu): layer outputs <= kGatMaxWidth
+  for (int l = 1; l <= cfg->num_layers && cfg->arch == GIST_ARCH_GAT; ++l)
+    if (pad8(cfg->dims[l]) > kGatMaxWidth) return GIST_E_UNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device || cfg->device < 0) {
     cudaGetLastError();
@@ -445,6 +456,8 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   }
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return GIST_E_UNSUPPORTED;
+  if (cfg->graph_residency != GIST_GRAPH_DEVICE) return GIST_E_UNSUPPORTED;
+  if (cfg->world_size > 1 && !cfg->nccl_unique_id && !cfg->loopback) return GIST_E_ARG;
   gist_ctx* c = new gist_ctx();
   c->cfg = *cfg;
   c->dims.assign(cfg->dims, cfg->dims + cfg->num_layers + 1);
@@ -452,51 +465,35 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   c->L = cfg->num_layers;
   c->arch = cfg->arch;
   c->prec = cfg->precision;
+  c->comm.rank = cfg->rank;
+  c->comm.world = cfg->world_size;
+  // every error below releases what was created so far through gist_destroy
+  auto bail = [&](gist_status st) {
+    gist_destroy(c);
+    return st;
+  };
   cudaSetDevice(cfg->device);
   if (cfg->stream) {
     c->stream = (cudaStream_t)cfg->stream;
   } else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete c;
-      return GIST_E_CUDA;
-    }
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(GIST_E_CUDA);
     c->own_stream = true;
   }
-  if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
-    delete c;
-    return GIST_E_CUDA;
-  }
-  if (const char* e = std::getenv("GIST_STREAMS")) c->nstreams = atoi(e) == 2 ? 2 : 1;
-  if (c->nstreams == 2 &&
-      (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
-       cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
-       cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess)) {
-    delete c;
-    return GIST_E_CUDA;
-  }
+  if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) return bail(GIST_E_CUDA);
   if (const char* e = std::getenv("GIST_DW_STREAM"); !(e && e[0] == '0')) {
     if (cudaStreamCreateWithFlags(&c->dws, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_dw_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_dw_join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_dw_wread, cudaEventDisableTiming) != cudaSuccess) {
-      delete c;
-      return GIST_E_CUDA;
-    }
-  }
-  if (cfg->graph_residency != GIST_GRAPH_DEVICE) {
-    delete c;
-    return GIST_E_UNSUPPORTED;
+        cudaEventCreateWithFlags(&c->ev_dw_join, cudaEventDisableTiming) != cudaSuccess)
+      return bail(GIST_E_CUDA);
   }
   if (cfg->world_size > 1) {
-    if (!cfg->nccl_unique_id) {
-      delete c;
-      return GIST_E_ARG;
-    }
-    ncclUniqueId id;
-    std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
-    if (ncclCommInitRank(&c->comm, cfg->world_size, id, cfg->rank) != ncclSuccess) {
-      delete c;
-      return GIST_E_NCCL;
+    if (cfg->loopback) {  // tests: W contexts of one process stand in for W ranks (comm.h)
+      if (loopback_join(cfg->loopback, cfg->rank, cfg->world_size) != GIST_OK) return bail(GIST_E_ARG);
+      c->comm.lb = cfg->loopback;
+    } else {
+      ncclUniqueId id;
+      std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+      if (ncclCommInitRank(&c->comm.nccl, cfg->world_size, id, cfg->rank) != ncclSuccess) return bail(GIST_E_NCCL);
     }
   }
   *out = c;
@@ -527,17 +524,15 @@ extern "C" void gist_destroy(gist_ctx* c) {
   for (void* p : c->allocs) cudaFreeAsync(p, c->stream);
   cudaStreamSynchronize(c->stream);
   for (size_t r = 0; r < c->peer_base.size(); ++r)
-    if (c->peer_base[r] && c->peer_base[r] != c->p2p_base) cudaIpcCloseMemHandle(c->peer_base[r]);
+    if (c->peer_base[r] && c->peer_base[r] != c->p2p_base && !c->comm.lb) cudaIpcCloseMemHandle(c->peer_base[r]);
   if (c->p2p_base) cudaFree(c->p2p_base);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm.nccl) ncclCommDestroy(c->comm.nccl);
+  if (c->comm.lb) loopback_leave(c->comm.lb, c->comm.rank);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
-  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
-  if (c->ev_join2) cudaEventDestroy(c->ev_join2);
-  if (c->side) cudaStreamDestroy(c->side);
+  drop_graphs(c);
   if (c->dws) cudaStreamDestroy(c->dws);
   if (c->ev_dw_fork) cudaEventDestroy(c->ev_dw_fork);
   if (c->ev_dw_join) cudaEventDestroy(c->ev_dw_join);
-  if (c->ev_dw_wread) cudaEventDestroy(c->ev_dw_wread);
   for (auto& r : c->prof_pending) c->ev_pool.push_back(r.a), c->ev_pool.push_back(r.b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->nnz_pin) cudaFreeHost(c->nnz_pin);
@@ -604,13 +599,20 @@ static gist_status p2p_setup(gist_ctx* c) {
   c->peer_base.assign(W, nullptr);
   c->peer_base[c->cfg.rank] = c->p2p_base;
   if (W == 1) return GIST_OK;
+  if (c->comm.lb) {  // loopback ranks share one process: the peers' regions are plain pointers
+    std::vector<void*> all;
+    gist_status st = comm_exchange_ptr(c->comm, c->p2p_base, all, &c->err);
+    if (st != GIST_OK) return fail(c, st, c->err);
+    for (int r = 0; r < W; ++r) c->peer_base[r] = static_cast<char*>(all[r]);
+    return GIST_OK;
+  }
   cudaIpcMemHandle_t mine;
   CK(cudaIpcGetMemHandle(&mine, c->p2p_base));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   char* hd = nullptr;
   TRY(dalloc_t(c, &hd, (size_t)64 * (W + 1)));
-  CK(cudaMemcpyAsync(hd, &mine, 64, cudaMemcpyHostToDevice, c->stream));
-  NK(ncclAllGather(hd, hd + 64, 64, ncclChar, c->comm, c->stream));
+  CK(cudaMemcpyAsync(hd + 64 * (1 + c->cfg.rank), &mine, 64, cudaMemcpyHostToDevice, c->stream));
+  TRY(coll(c, comm_allgather(c->comm, hd + 64 * (1 + c->cfg.rank), hd + 64, 64, c->stream, &c->err)));
   std::vector<cudaIpcMemHandle_t> all(W);
   CK(cudaMemcpyAsync(all.data(), hd + 64, (size_t)64 * W, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -834,6 +836,7 @@ extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
                    c->th_N[l], (uint32_t)l, seed, sc, c->stream));
   }
   TRY(check_launch(c, "init_params"));
+  c->layer_set.assign(c->L, 1);
   c->state = S_PARAMS;
   return GIST_OK;
 }
@@ -871,9 +874,11 @@ extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* 
   CK(cudaMemcpyAsync(c->theta[layer], buf.data(), K * N * 4, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->h2d += K * N * 4;
-  bool all = true;  // params become valid once every layer was set or init_params ran
-  c->state = S_PARAMS;
-  (void)all;
+  // the parameters become valid (PARAMS) once every layer was set since the graph load, or
+  // init_params ran: a partially set model cannot be trained
+  c->layer_set.resize(c->L, 0);
+  c->layer_set[layer] = 1;
+  if (std::all_of(c->layer_set.begin(), c->layer_set.end(), [](uint8_t v) { return v != 0; })) c->state = S_PARAMS;
   return GIST_OK;
 }
 
@@ -911,6 +916,8 @@ static gist_status alloc_slots(gist_ctx* c, int m) {
     CK(cudaMemsetAsync(c->Wball, 0, tot * 2, c->stream));
   }
   if (W > 1 && c->cfg.agg_mode == GIST_AGG_ALLGATHER) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
+  if (c->bctr) dfree(c, c->bctr);
+  TRY(dalloc_t(c, &c->bctr, 2 * (size_t)std::max(c->slots_per_rank, 1)));
   if (!c->dstate) {
     TRY(dalloc_t(c, &c->dstate, 1));
     CK(cudaMallocHost(&c->hstate, sizeof(StepState)));
@@ -1025,6 +1032,7 @@ static double spmm_bytes(const SpmmArgs<T, T>& a) {
 // Builds the launch plan of one subTrain step (every grouped launch's argument block).
 template <typename T>
 static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
+  drop_graphs(c);  // the captured steps hold the previous plan's argument blocks
   P.groups.clear();
   const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
   const bool sage = c->arch == GIST_ARCH_SAGE;
@@ -1036,7 +1044,6 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
   // L2-footprint / launch-count trade-off
   int gsz = kMaxGroup;
-  if (c->nstreams == 2) gsz = std::max(1, std::min(kMaxGroup, ((int)c->slots.size() + 1) / 2));
   if (const char* e = std::getenv("GIST_GROUP")) gsz = std::max(1, std::min(kMaxGroup, atoi(e)));
   for (int g0 = 0; g0 < (int)c->slots.size(); g0 += gsz) {
     typename StepPlan<T>::Group g;
@@ -1045,7 +1052,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
     g.batch.n = g.count;
     g.batch.q = q;
     g.batch.nb_max = nb;
-    g.batch.st = c->dstate;
+    g.batch.ctr = c->bctr + 2 * g0;
     g.fwd_spmm.assign(L, SpmmGroup<T, T>());
     g.bwd_spmm.assign(L, SpmmGroup<T, T>());
     g.fwd_tc.assign(L, GemmPlanTC());
@@ -1657,10 +1664,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       tc_l(g.ra_z, g.ra_gemm_fl / 6);
       continue;
     }
-    if (!(l == 0 && c->batch_prefetched && c->agg0_prefetched)) {
-      if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
-      spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
-    }
+    if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
+    spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
     launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
   }
   // ---- a4: softmax cross-entropy
@@ -1672,30 +1677,10 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     c->nk += 1;
   }
   // ---- a5/a6: backward.  With the dW stream, dW_l (it only feeds the optimizer) overlaps the
-  // rest of the backward chain, and with opt_per_layer layer l's optimizer step follows on that
-  // stream once the main stream's last reader of W_l (the dX / dH GEMM) is done.
+  // rest of the backward chain (dX -> aggregation), joined before the optimizer.
   auto fork = [&]() {
     CK(cudaEventRecord(c->ev_dw_fork, s));
     CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
-    return GIST_OK;
-  };
-  auto opt_layer = [&](int l) {
-    if (!c->opt_per_layer) return GIST_OK;
-    CK(cudaEventRecord(c->ev_dw_wread, s));
-    CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_wread, 0));
-    OptRanges R;
-    R.n = g.count;
-    for (int j = 0; j < g.count; ++j) {
-      const Slot& sl = c->slots[g.first + j];
-      const LayerShape& sh = c->shapes[sl.index][l];
-      R.off[j] = (int64_t)(sl.W - c->Wall) + sh.off;
-      R.len[j] = (int64_t)sh.Kp * sh.Np;
-      R.total += R.len[j];
-    }
-    const bool adam = c->cfg.optimizer == GIST_OPT_ADAM;
-    PL(GIST_PROF_OPTIM, (double)R.total * ((adam ? 28.0 : 12.0) + (c->Wball ? 2.0 : 0.0)), c->side_now,
-       opt_ranges_step(adam, c->Wall, c->Gall, c->Mall, c->Vall, R, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate,
-                       c->Wball, l == 0, c->side_now));
     return GIST_OK;
   };
   for (int l = L - 1; l >= 0; --l) {
@@ -1714,7 +1699,6 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
         tc_l(g.ra_dw, g.ra_gemm_fl / 3);
       }
       tc_l(g.ra_dh, g.ra_gemm_fl / 3);
-      TRY(opt_layer(l));
       continue;
     }
     if (c->side_now) {
@@ -1723,12 +1707,8 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     } else {
       launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
     }
-    if (l == 0) {
-      TRY(opt_layer(0));
-      break;
-    }
+    if (l == 0) break;
     launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
-    TRY(opt_layer(l));
     if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
     spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
   }
@@ -1739,40 +1719,18 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   return GIST_OK;
 }
 
-// a1 of step z for group g on stream bs with an explicit step index (the device step state
-// still points at the previous step while its optimizer runs on the main stream)
+// a1 of the next step for group g on stream bs: the build reads the batch index st->zb (the
+// device step state's z still points at the current step while its optimizer runs)
 template <typename T>
 static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs) {
-  BatchGroup B = g.batch;
-  B.zfix = z;
   double vol = 0.0;
   for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
   const int id = prof_begin(c, bs, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0);
-  batch_setup(B, c->cstart, c->rp, bs);
-  batch_build(B, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
+  batch_setup(g.batch, c->cstart, c->rp, bs);
+  batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
               c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, bs);
   prof_end(c, bs, id);
   c->nk += 2;
-  // layer-0 aggregation [X_b | N X_b] needs only the batch: opt-in GIST_AGG0_PREFETCH=1 runs it
-  // here too (C3: 8,214-8,231 vs 8,260-8,266 steps/s without: it competes with the HBM-bound
-  // optimizer instead of filling idle SMs)
-  static const bool agg0 = [] { const char* e = std::getenv("GIST_AGG0_PREFETCH"); return e && e[0] == '1'; }();
-  if (agg0 && c->arch != GIST_ARCH_GAT && !(g.reassoc && c->L == 1)) {
-    const bool bd = c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE;
-    if (bd) {
-      BdPlan P = g.fwd_bd[0];
-      P.G.zfix = z;
-      const int id2 = prof_begin(c, bs, GIST_PROF_AGG_TC, g.bd_fl[0]);
-      gemm_bd_launch(P, bs);
-      prof_end(c, bs, id2);
-      ++c->nk;
-    }
-    const int id3 = prof_begin(c, bs, GIST_PROF_SPMM, g.fwd_by[0], 4.0 * g.count, -1);
-    spmm_group<T, T>(g.fwd_spmm[0], bs);
-    prof_end(c, bs, id3);
-    ++c->nk;
-    c->agg0_prefetched = true;
-  }
   return GIST_OK;
 }
 
@@ -1848,6 +1806,73 @@ static gist_status schedule(gist_ctx* c, Slot& sl, int iters, bool* grew) {
   return GIST_OK;
 }
 
+// One subTrain step of every local slot (every lockstep group), the optimizer, and optionally
+// the next step's batch builds on the dW stream, overlapping the optimizer (`prefetch`; every
+// reader of this step's batch buffers precedes the fork).  `build`: this step builds its own
+// batches (else the previous step prefetched them).  Everything that changes from step to step
+// is read by the kernels from the device step state, so the enqueued sequence of a (build,
+// prefetch) variant is identical for every step: it is captured once as a CUDA graph and
+// replayed (step_graph).
+static gist_status enqueue_step(gist_ctx* c, bool build, bool prefetch) {
+  cudaStream_t s = c->stream;
+  const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
+  c->side_now = c->prof_now ? nullptr : c->dws;
+  c->batch_prefetched = !build;
+  for (size_t gi = 0; gi < ng; ++gi) {
+    if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], c->cur_z, s));
+    else TRY(run_group_step<float>(c, c->plan_f.groups[gi], c->cur_z, s));
+  }
+  if (prefetch) {
+    CK(cudaEventRecord(c->ev_dw_fork, s));
+    CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
+    for (size_t gi = 0; gi < ng; ++gi) {
+      if (c->prec == GIST_PREC_BF16) TRY(prefetch_batch<bf16>(c, c->plan_b.groups[gi], c->cur_z + 1, c->dws));
+      else TRY(prefetch_batch<float>(c, c->plan_f.groups[gi], c->cur_z + 1, c->dws));
+    }
+  }
+  TRY(run_optimizer(c));
+  if (prefetch) {
+    CK(cudaEventRecord(c->ev_dw_join, c->dws));
+    CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
+  }
+  return GIST_OK;
+}
+
+static void drop_graphs(gist_ctx* c) {
+  for (auto& g : c->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.nk = 0;
+  }
+}
+
+// the step of variant (build, prefetch) as a CUDA graph: captured on first use after every
+// plan (re)build, then one cudaGraphLaunch per step (the host enqueue of ~30 launches with
+// multi-kilobyte grouped argument blocks was as long as the step itself at one slot per GPU)
+static gist_status step_graph(gist_ctx* c, bool build, bool prefetch) {
+  gist_ctx::StepGraph& G = c->graphs[(build ? 2 : 0) + (prefetch ? 1 : 0)];
+  if (!G.exec) {
+    const int64_t nk0 = c->nk;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const gist_status st = enqueue_step(c, build, prefetch);
+    cudaGraph_t gr = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+    if (st != GIST_OK) {
+      if (gr) cudaGraphDestroy(gr);
+      return st;
+    }
+    CK(e);
+    const cudaError_t ei = cudaGraphInstantiate(&G.exec, gr, 0);
+    cudaGraphDestroy(gr);
+    CK(ei);
+    G.nk = c->nk - nk0;
+    c->nk = nk0;
+  }
+  CK(cudaGraphLaunch(G.exec, c->stream));
+  c->nk += G.nk;
+  return GIST_OK;
+}
+
 extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr, float* mean_loss) {
   PRE(c);
   if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "subtrain: call partition first");
@@ -1869,52 +1894,24 @@ extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr,
     CK(cudaMemsetAsync(sl.loss_acc, 0, 4, s));
   }
   *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0u};
+  if (!c->slots.empty()) CK(cudaMemsetAsync(c->bctr, 0, c->slots.size() * 2 * sizeof(int32_t), s));
   CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
   CK(cudaEventRecord(c->hstate_ev, s));
-  c->batch_prefetched = c->agg0_prefetched = false;
+  // GIST_BATCH_PREFETCH=0 / GIST_GRAPH=0: A/B switches (prefetch measured +1.4% on C3)
+  const char* e_pf = std::getenv("GIST_BATCH_PREFETCH");
+  const char* e_gr = std::getenv("GIST_GRAPH");
+  const bool prefetch_on = !(e_pf && e_pf[0] == '0'), graphs_on = !(e_gr && e_gr[0] == '0');
+  bool prefetched = false;  // step z's batches were built during step z-1's optimizer
   for (int z = 0; z < local_iters; ++z) {
     c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
-    const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
-    const bool two = c->nstreams == 2 && ng >= 2;
-    // per-layer optimizer on the dW stream (opt-in GIST_OPT_PER_LAYER=1: one lockstep group,
-    // GCN / GraphSAGE): measured 8,033 vs 8,078 steps/s for dW-only overlap on C3 -- four
-    // HBM-bound launches competing with the backward chain cost more than they hide
-    static const bool per_layer = [] { const char* e = std::getenv("GIST_OPT_PER_LAYER"); return e && e[0] == '1'; }();
-    c->side_now = c->prof_now ? nullptr : c->dws;
-    c->opt_per_layer = per_layer && c->side_now && ng == 1 && c->arch != GIST_ARCH_GAT;
-    if (two) {  // fork: the side stream sees the previous optimizer step / state advance
-      CK(cudaEventRecord(c->ev_fork2, s));
-      CK(cudaStreamWaitEvent(c->side, c->ev_fork2, 0));
-    }
-    for (size_t gi = 0; gi < ng; ++gi) {
-      cudaStream_t gs = (two && (gi & 1)) ? c->side : s;
-      if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], z, gs));
-      else TRY(run_group_step<float>(c, c->plan_f.groups[gi], z, gs));
-    }
-    if (two) {  // join before the optimizer (it updates every local slot at once)
-      CK(cudaEventRecord(c->ev_join2, c->side));
-      CK(cudaStreamWaitEvent(s, c->ev_join2, 0));
-    }
-    // prefetch: step z+1's batch build (it only needs the graph and the schedule) runs on the dW
-    // stream while the optimizer of step z runs here; every reader of the batch buffers of
-    // step z (the backward, dW included) is done by now.  One lockstep group only.
-    static const bool prefetch_on = [] { const char* e = std::getenv("GIST_BATCH_PREFETCH"); return !(e && e[0] == '0'); }();
     const bool next_prof = c->prof_stride > 0 && ((c->step + z + 1) % c->prof_stride) == 0;
-    const bool pf = prefetch_on && c->dws && ng == 1 && !two && z + 1 < local_iters && !c->prof_now && !next_prof;
-    c->agg0_prefetched = false;
-    if (pf) {
-      CK(cudaEventRecord(c->ev_dw_fork, s));
-      CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
-      if (c->prec == GIST_PREC_BF16) TRY(prefetch_batch<bf16>(c, c->plan_b.groups[0], z + 1, c->dws));
-      else TRY(prefetch_batch<float>(c, c->plan_f.groups[0], z + 1, c->dws));
-    }
-    if (!c->opt_per_layer) TRY(run_optimizer(c));
-    if (pf) {
-      CK(cudaEventRecord(c->ev_dw_join, c->dws));
-      CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
-    }
-    c->batch_prefetched = pf;
-    if (!pf) c->agg0_prefetched = false;
+    for (Slot& sl : c->slots) sl.last_nb = sl.nb_of_step[z];
+    c->cur_z = z;
+    // profiled steps run eagerly and serialised, and build their own batches
+    const bool pf = prefetch_on && c->dws && z + 1 < local_iters && !c->prof_now && !next_prof;
+    if (graphs_on && !c->prof_now) TRY(step_graph(c, !prefetched, pf));
+    else TRY(enqueue_step(c, !prefetched, pf));
+    prefetched = pf;
     c->prof_now = false;
   }
   c->adam_t += local_iters;
@@ -1949,7 +1946,7 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   if (c->p2p_base) {  // agg_mode P2P (f2): owners store their blocks into every replica
     // barrier 1: every rank has finished this round's reads of its replica (gist_partition's
     // extraction) before any peer overwrites it
-    if (W > 1) NK(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+    TRY(coll(c, comm_barrier(c->comm, c->barrier_word, s, &c->err)));
     for (const Part& pt : parts)
       for (int i = c->cfg.rank; i < c->m; i += W) {
         const int j = i / W;
@@ -1968,7 +1965,7 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
         }
       }
     // barrier 2: every peer's stores into this replica have completed before anything reads it
-    if (W > 1) NK(ncclAllReduce(c->barrier_word, c->barrier_word, 1, ncclFloat, ncclSum, c->comm, s));
+    TRY(coll(c, comm_barrier(c->comm, c->barrier_word, s, &c->err)));
     c->prof_now = false;
     TRY(check_launch(c, "aggregate"));
     c->round += 1;
@@ -1978,8 +1975,8 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   for (const Part& pt : parts) {
     const float* src = pt.local;
     if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
-      const int id = prof_begin(c, s, GIST_PROF_AGGREGATE, (double)W * c->slots_per_rank * c->S_max * 4.0);
-      NK(ncclAllGather(pt.local, c->Wrecv, (size_t)c->slots_per_rank * c->S_max, ncclFloat, c->comm, s));
+      const int id = prof_begin(c, s, GIST_PROF_COMM, (double)(W - 1) * c->slots_per_rank * c->S_max * 4.0);
+      TRY(coll(c, comm_allgather(c->comm, pt.local, c->Wrecv, (size_t)c->slots_per_rank * c->S_max * 4, s, &c->err)));
       prof_end(c, s, id);
       src = c->Wrecv;
     }
@@ -2067,23 +2064,38 @@ static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* ro
 }
 
 // ================================================================ eval ====
+// Full-graph forward of the global model (R1/R2 full-graph operator, R10 no scaling).  World > 1
+// (GCN / GraphSAGE): the relabelled rows are cut into W blocks of R = ceil(n / W); rank r
+// computes the SpMM and GEMM of block r of every layer and one all-gather per hidden layer
+// assembles the next layer's input on every rank (its SpMM gathers neighbours from every block);
+// the loss / accuracy sums of the blocks are combined with one sum all-reduce.
+// GAT runs the whole forward on every rank (its attention needs Z = H W of every neighbour row).
+// logits_host (optional): float[n x k] by ORIGINAL node id, assembled on every rank.
 template <typename T>
-static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
+static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float* logits_host) {
   cudaStream_t s = c->stream;
   const int64_t n = c->n;
   const bool sage = c->arch == GIST_ARCH_SAGE;
+  const bool gat = c->arch == GIST_ARCH_GAT;
+  const int W = gat ? 1 : c->cfg.world_size;
+  const int rank = gat ? 0 : c->cfg.rank;
+  const int64_t R = cdiv(n, W);
+  const int64_t r0 = std::min<int64_t>(n, (int64_t)rank * R);
+  const int64_t nr = std::min<int64_t>(n, r0 + R) - r0;  // rows of this rank's block
+  const int64_t npad = R * W;
+  const int64_t Nl = c->th_N[c->L - 1];
   int64_t maxK = 0;
   for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
   void *bufA = nullptr, *bufB = nullptr, *wtmp = nullptr;
   float* logits = nullptr;
   double* out3 = nullptr;
-  TRY(dalloc(c, &bufA, (size_t)n * maxK * sizeof(T)));
-  TRY(dalloc(c, &bufB, (size_t)n * maxK * sizeof(T)));
-  TRY(dalloc_t(c, &logits, (size_t)n * c->th_N[c->L - 1]));
+  TRY(dalloc(c, &bufA, (size_t)npad * maxK * sizeof(T)));
+  TRY(dalloc(c, &bufB, (size_t)npad * maxK * sizeof(T)));
+  TRY(dalloc_t(c, &logits, (size_t)npad * Nl));
   TRY(dalloc_t(c, &out3, 3));
   T* Cb = (T*)bufA;
   T* Hn = (T*)bufB;
-  if (c->arch == GIST_ARCH_GAT) {
+  if (gat) {
     std::vector<void*> wl(c->L, nullptr);
     int64_t maxN = 0;
     for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
@@ -2102,20 +2114,22 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
     dfree(c, Z);
     dfree(c, sc);
   }
-  for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {
+  for (int l = 0; l < c->L && !gat; ++l) {
     const int64_t K = c->th_K[l], N = c->th_N[l];
     const int64_t half = pad8(c->dims[l]);
     SpmmArgs<T, T> a;
-    a.row_beg = c->rp; a.row_end = c->rp + 1; a.col = c->col; a.rows = n; a.rowscale = c->full_scale;
+    a.row_beg = c->rp + r0; a.row_end = c->rp + r0 + 1; a.col = c->col; a.rows = nr;
+    a.row0 = r0; a.h_rows = n;
+    a.rowscale = c->full_scale + r0;
     const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
     if (sage) {
-      if (l == 0) { a.self_out = Cb; a.ld_self = K; }
+      if (l == 0) { a.self_out = Cb + r0 * K; a.ld_self = K; }
       a.H = l == 0 ? Hin : Cb; a.ldh = l == 0 ? half : K;
-      a.out = Cb + half; a.ldo = K; a.w = half;
+      a.out = Cb + r0 * K + half; a.ldo = K; a.w = half;
     } else {
-      a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
+      a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb + r0 * K; a.ldo = K; a.w = K;
     }
-    LK((spmm<T, T>(a, s)));
+    if (nr > 0) LK((spmm<T, T>(a, s)));
     const void* Wl = c->theta[l];
     if (sizeof(T) == 2) {
       if (wtmp) dfree(c, wtmp);
@@ -2124,17 +2138,34 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
       Wl = wtmp;
     }
     if (l + 1 < c->L) {
-      // next layer input: SAGE writes the left half of the next concat buffer (swap buffers)
-      // GCN: H_{l+1} -> Hn; SAGE: H_{l+1} -> left half of Hn, which becomes the next concat buffer
-      TRY(gemm_any(c, false, false, n, N, K, Cb, K, Wl, N, Hn, c->th_K[l + 1], false, true, s));
-      if (sage) std::swap(Cb, Hn);  // Hn (now holding H_{l+1} as left half) becomes the concat buffer
-    } else {
-      TRY(gemm_any(c, false, false, n, N, K, Cb, K, Wl, N, logits, N, true, false, s));
+      // next layer input: GCN H_{l+1} -> Hn; SAGE H_{l+1} -> left half of Hn, which becomes the
+      // next concat buffer (swap)
+      const int64_t Kn = c->th_K[l + 1];
+      if (nr > 0) TRY(gemm_any(c, false, false, nr, N, K, Cb + r0 * K, K, Wl, N, Hn + r0 * Kn, Kn, false, true, s));
+      if (sage) std::swap(Cb, Hn);
+      T* next = sage ? Cb : Hn;  // the buffer the next layer's SpMM gathers from
+      if (W > 1)
+        TRY(coll(c, comm_allgather(c->comm, next + (int64_t)rank * R * Kn, next, (size_t)R * Kn * sizeof(T), s,
+                                   &c->err)));
+    } else if (nr > 0) {
+      TRY(gemm_any(c, false, false, nr, N, K, Cb + r0 * K, K, Wl, N, logits + r0 * N, N, true, false, s));
     }
   }
-  LK(eval_rows(logits, c->th_N[c->L - 1], n, c->k, c->labels, c->split, code, out3, s));
+  CK(cudaMemsetAsync(out3, 0, 3 * sizeof(double), s));
+  if (nr > 0) LK(eval_rows(logits + r0 * Nl, Nl, nr, c->k, c->labels + r0, c->split + r0, code, out3, s));
+  if (W > 1) TRY(coll(c, comm_allreduce_sum(c->comm, out3, 3, true, s, &c->err)));
   double h[3];
   CK(cudaMemcpyAsync(h, out3, sizeof(h), cudaMemcpyDeviceToHost, s));
+  if (logits_host) {
+    if (W > 1)
+      TRY(coll(c, comm_allgather(c->comm, logits + (int64_t)rank * R * Nl, logits, (size_t)R * Nl * 4, s, &c->err)));
+    std::vector<float> lg((size_t)n * Nl);
+    CK(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int64_t g = 0; g < n; ++g)
+      std::memcpy(logits_host + (size_t)c->perm_h[g] * c->k, lg.data() + (size_t)g * Nl, (size_t)c->k * 4);
+    c->d2h += (int64_t)n * Nl * 4;
+  }
   CK(cudaStreamSynchronize(s));
   TRY(check_launch(c, "eval"));
   if (loss) *loss = h[2] > 0 ? (float)(h[0] / h[2]) : 0.f;
@@ -2150,9 +2181,9 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc) {
 extern "C" gist_status gist_eval(gist_ctx* c, int32_t split_code, float* loss, float* acc) {
   PRE(c);
   if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval: needs params and no open round");
-  if (split_code < 0 || split_code > 3) return GIST_E_ARG;
-  if (c->prec == GIST_PREC_BF16) return eval_t<bf16>(c, split_code, loss, acc);
-  return eval_t<float>(c, split_code, loss, acc);
+  if (split_code < 0 || split_code > 3) return fail(c, GIST_E_ARG, "eval: split code not in 0..3");
+  if (c->prec == GIST_PREC_BF16) return eval_t<bf16>(c, split_code, loss, acc, nullptr);
+  return eval_t<float>(c, split_code, loss, acc, nullptr);
 }
 
 // ==================================================== partition-wise eval (R20) ===
@@ -2164,7 +2195,7 @@ extern "C" gist_status gist_eval(gist_ctx* c, int32_t split_code, float* loss, f
 // partition p is evaluated by rank p mod W and the per-partition sums are all-reduced.
 template <typename T>
 static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t>& part, int np, int64_t max_rows,
-                                std::vector<double>& sums) {
+                                std::vector<double>& sums, float* logits_host) {
   cudaStream_t s = c->stream;
   const int64_t n = c->n;
   const bool sage = c->arch == GIST_ARCH_SAGE;
@@ -2303,6 +2334,13 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
       }
     }
     LK(eval_parts(logits, Nl, c->k, lbeg_d + f, k0, e - f, pnode_d, c->labels, c->split, code, out3 + 3 * f, s));
+    if (logits_host) {  // parity hook: chunk logits -> host rows of their nodes (internal ids)
+      std::vector<float> lg((size_t)rows * Nl);
+      CK(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < rows; ++i)
+        std::memcpy(logits_host + (size_t)pnode[k0 + i] * c->k, lg.data() + (size_t)i * Nl, (size_t)c->k * 4);
+    }
   }
   std::vector<double> loc(3 * (size_t)std::max(nlp, 1));
   CK(cudaMemcpyAsync(loc.data(), out3, loc.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -2315,10 +2353,19 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
     double* red = nullptr;
     TRY(dalloc_t(c, &red, sums.size()));
     CK(cudaMemcpyAsync(red, sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, s));
-    NK(ncclAllReduce(red, red, sums.size(), ncclDouble, ncclSum, c->comm, s));
+    TRY(coll(c, comm_allreduce_sum(c->comm, red, sums.size(), true, s, &c->err)));
     CK(cudaMemcpyAsync(sums.data(), red, sums.size() * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     dfree(c, red);
+    if (logits_host) {  // every node's row was written by exactly one rank, zeros elsewhere: exact sum
+      float* lr = nullptr;
+      TRY(dalloc_t(c, &lr, (size_t)n * c->k));
+      CK(cudaMemcpyAsync(lr, logits_host, (size_t)n * c->k * 4, cudaMemcpyHostToDevice, s));
+      TRY(coll(c, comm_allreduce_sum(c->comm, lr, (size_t)n * c->k, false, s, &c->err)));
+      CK(cudaMemcpyAsync(logits_host, lr, (size_t)n * c->k * 4, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      dfree(c, lr);
+    }
   }
   for (void* p : wl) if (p) dfree(c, p);
   for (void* p : {gX, gZ, (void*)gsc}) if (p) dfree(c, p);
@@ -2328,15 +2375,12 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
   return GIST_OK;
 }
 
-extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const int32_t* part_ids, int32_t num_parts,
-                                       int64_t max_rows, float* loss, float* acc, float* part_loss,
-                                       float* part_acc) {
-  PRE(c);
-  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_parts: needs params and no open round");
-  if (split_code < 0 || split_code > 3) return GIST_E_ARG;
+// partition of every internal node id from the caller's ids (original ids), or the training clusters
+static gist_status resolve_parts(gist_ctx* c, const int32_t* part_ids, int32_t num_parts, std::vector<int32_t>& part,
+                                 int* np) {
   const int64_t n = c->n;
-  std::vector<int32_t> part(n);
-  int np = num_parts;
+  part.assign(n, 0);
+  *np = num_parts;
   if (part_ids) {
     if (num_parts < 1) return fail(c, GIST_E_ARG, "eval_parts: num_parts < 1");
     for (int64_t g = 0; g < n; ++g) {
@@ -2345,14 +2389,26 @@ extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const in
       part[g] = p;
     }
   } else {  // the training clusters (contiguous internal id ranges after relabelling)
-    np = (int)c->cstart_h.size() - 1;
-    if (num_parts != 0 && num_parts != np) return fail(c, GIST_E_ARG, "eval_parts: num_parts != clusters");
-    for (int p = 0; p < np; ++p)
+    *np = (int)c->cstart_h.size() - 1;
+    if (num_parts != 0 && num_parts != *np) return fail(c, GIST_E_ARG, "eval_parts: num_parts != clusters");
+    for (int p = 0; p < *np; ++p)
       for (int64_t g = c->cstart_h[p]; g < c->cstart_h[p + 1]; ++g) part[g] = p;
   }
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const int32_t* part_ids, int32_t num_parts,
+                                       int64_t max_rows, float* loss, float* acc, float* part_loss,
+                                       float* part_acc) {
+  PRE(c);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_parts: needs params and no open round");
+  if (split_code < 0 || split_code > 3) return fail(c, GIST_E_ARG, "eval_parts: split code not in 0..3");
+  std::vector<int32_t> part;
+  int np = 0;
+  TRY(resolve_parts(c, part_ids, num_parts, part, &np));
   std::vector<double> sums;
-  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, split_code, part, np, max_rows, sums)
-                                : eval_parts_t<float>(c, split_code, part, np, max_rows, sums));
+  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, split_code, part, np, max_rows, sums, nullptr)
+                                : eval_parts_t<float>(c, split_code, part, np, max_rows, sums, nullptr));
   double ls = 0.0, as = 0.0;
   int cntp = 0;
   for (int p = 0; p < np; ++p) {
@@ -2365,6 +2421,26 @@ extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const in
   }
   if (loss) *loss = cntp ? (float)(ls / cntp) : 0.f;
   if (acc) *acc = cntp ? (float)(as / cntp) : 0.f;
+  return GIST_OK;
+}
+
+extern "C" gist_status gist_eval_logits(gist_ctx* c, int32_t mode, const int32_t* part_ids, int32_t num_parts,
+                                        int64_t max_rows, float* out) {
+  PRE(c);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_logits: needs params and no open round");
+  if (!out || (mode != 0 && mode != 1)) return fail(c, GIST_E_ARG, "eval_logits: mode not 0/1 or null output");
+  if (mode == 0)
+    return c->prec == GIST_PREC_BF16 ? eval_t<bf16>(c, 0, nullptr, nullptr, out) : eval_t<float>(c, 0, nullptr, nullptr, out);
+  std::vector<int32_t> part;
+  int np = 0;
+  TRY(resolve_parts(c, part_ids, num_parts, part, &np));
+  // internal-id rows, then the original-id order of the output
+  std::vector<float> li((size_t)c->n * c->k, 0.f);
+  std::vector<double> sums;
+  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, 0, part, np, max_rows, sums, li.data())
+                                : eval_parts_t<float>(c, 0, part, np, max_rows, sums, li.data()));
+  for (int64_t g = 0; g < c->n; ++g)
+    std::memcpy(out + (size_t)c->perm_h[g] * c->k, li.data() + (size_t)g * c->k, (size_t)c->k * 4);
   return GIST_OK;
 }
 

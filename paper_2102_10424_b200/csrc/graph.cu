@@ -162,7 +162,7 @@ __global__ void k_batch_setup(const __grid_constant__ BatchGroup G, const int64_
   pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
-  const int32_t* d = S.desc + (size_t)(G.zfix >= 0 ? G.zfix : G.st->z) * (3 * q + 4);
+  const int32_t* d = S.desc + (size_t)G.ctr[0] * (3 * q + 4);
   const int32_t* bcl = d;
   const int32_t* loff = d + q;
   const int32_t* voff = d + 2 * q + 1;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
   pdl_trigger();
   const BatchSlot& S = G.s[blockIdx.y];
   const int q = G.q;
-  const int32_t* d = S.desc + (size_t)(G.zfix >= 0 ? G.zfix : G.st->z) * (3 * q + 4);
+  const int32_t* d = S.desc + (size_t)G.ctr[0] * (3 * q + 4);
   const int nb = d[2 * q];
   const uint32_t tag = (uint32_t)d[3 * q + 3];
   if (SMAP) {
@@ -327,6 +327,13 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
     for (int k = 0; k < kBuildRows; ++k) a += s_cnt[k], b += s_tr[k];
     if (a) atomicAdd((unsigned long long*)&S.stats[0], (unsigned long long)a);
     if (b) atomicAdd((unsigned long long*)&S.stats[1], (unsigned long long)b);
+    // the last CTA of the launch (every CTA has read the batch index by now) advances it
+    __threadfence();
+    const unsigned total = gridDim.x * gridDim.y;
+    if (atomicAdd(reinterpret_cast<unsigned*>(G.ctr + 1), 1u) == total - 1) {
+      G.ctr[0] += 1;
+      G.ctr[1] = 0;
+    }
   }
 }
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,

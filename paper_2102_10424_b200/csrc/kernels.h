@@ -40,6 +40,10 @@ struct SpmmArgs {
   TI* self_out = nullptr;
   int64_t ld_self = 0;
   int64_t w = 0;  // padded width processed (multiple of 8)
+  // row-block launches (row-split eval): local row v is graph row v + row0 for the self term
+  // (H row, colscale); neighbours are graph ids.  h_rows = rows of H the gathers may reach
+  // (0: rows), for the 32-bit offset choice.
+  int64_t row0 = 0, h_rows = 0;
   // Cluster-slab staging (batch SpMMs only): rows of each batch cluster are a contiguous
   // local-id range loff[k]..loff[k+1] (from the step descriptor).  When set, one CTA stages
   // cluster k's rows of H (a column tile) in shared memory and serves intra-cluster
@@ -167,7 +171,6 @@ struct BdGroup {
   int64_t rows = 0;  // static batch rows (nb_max): dummy rows [n_b, rows) are zero-filled
   const StepState* st = nullptr;
   const int64_t* cstart = nullptr;
-  int zfix = -1;  // >= 0: descriptors of step zfix (prefetched layer-0 aggregation), not st->z
 };
 struct BdPlan {
   BdGroup G;
@@ -206,13 +209,13 @@ void part_fill(const int64_t* rp, const int32_t* col, const int32_t* pnode, cons
 void full_graph_scales(const int64_t* rp, int64_t n, int arch, float* scale, cudaStream_t s);
 
 // Device-resident step state: the kernels of one subTrain step read everything that
-// changes from step to step from here, so a step is a fixed launch sequence (CUDA-graph
-// capturable).  z = index of the current step in this call's descriptor array,
-// t = optimizer steps taken since the last partition, lr = learning rate of the call.
+// changes from step to step from here, so a step is a fixed launch sequence (captured once
+// as a CUDA graph and replayed).  z = index of the current step in this call's descriptor
+// array, t = optimizer steps taken since the last partition, lr = learning rate of the call.
 struct StepState {
   int32_t z, t;
   float lr;
-  uint32_t done;  // optimizer CTAs finished this step (the last one advances z, t and resets it)
+  uint32_t done;   // optimizer CTAs finished this step (the last one advances z, t and resets it)
 };
 // Per-step batch descriptor (host-built, R7), 3q+4 int32:
 //   [bcl(q) | loff(q+1) | voff(q+1) | qq | tag]
@@ -236,8 +239,10 @@ struct BatchSlot {
 struct BatchGroup {
   BatchSlot s[kMaxGroup];
   int n = 0, q = 0, nb_max = 0;
-  const StepState* st = nullptr;
-  int zfix = -1;  // >= 0: build the batch of step zfix (prefetch), not of the device step state's z
+  // per-group batch counter {index of the batch to build, finished build CTAs}: the build of
+  // step z+1 may run on a side stream while step z's optimizer advances the step state's z, so
+  // the builds keep their own index (zeroed per subTrain call; the last build CTA advances it)
+  int32_t* ctr = nullptr;
   // optional: copy the batch rows of the feature matrix X (bf16, ldx) into xdst[slot] (ldxd)
   const bf16* X = nullptr;
   int64_t ldx = 0, ldxd = 0;
@@ -406,6 +411,7 @@ template <typename T> void gat_scores(const GatGroup<T>& G, cudaStream_t s);
 template <typename T> void gat_forward(const GatGroup<T>& G, cudaStream_t s);
 template <typename T> void gat_backward(const GatGroup<T>& G, cudaStream_t s);
 constexpr int kGatDaChunks = 64;
+constexpr int kGatMaxWidth = 2048;  // widest GAT layer output (padded columns) the attention passes hold
 template <typename T>
 void gather_rows_t(const T* src, int64_t lds, const int32_t* idx, int64_t rows, int64_t w, T* dst, int64_t ldd,
                    cudaStream_t s);

@@ -73,9 +73,9 @@ __global__ void __launch_bounds__(256, PRED ? 3 : (J == 1 && sizeof(TI) == 2) ? 
 #pragma unroll
   for (int j = 0; j < J; ++j) act[j] = vbase + j * LPR < wv;
 
-  const Off hv = (Off)(a.h_index ? (int64_t)a.h_index[v] : v) * ldv;
+  const Off hv = (Off)(a.h_index ? (int64_t)a.h_index[v] : v + a.row0) * ldv;
   if (a.self || a.self_out) {
-    const float s = a.colscale ? a.colscale[v] : 1.f;
+    const float s = a.colscale ? a.colscale[v + a.row0] : 1.f;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (!act[j]) continue;
@@ -410,7 +410,8 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   bool wide = false, cs = G.a[0].colscale != nullptr;
   for (int i = 0; i < G.n; ++i) {
     const SpmmArgs<TI, TO>& a = G.a[i];
-    wide |= a.h_index != nullptr || a.rows * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
+    const int64_t hr = a.h_rows > a.rows + a.row0 ? a.h_rows : a.rows + a.row0;
+    wide |= a.h_index != nullptr || hr * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
   }
   if (!wide && cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, false>, grid, 256, 0, s, G, nchunks);
   else if (!wide) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, false>, grid, 256, 0, s, G, nchunks);
@@ -459,8 +460,9 @@ void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
   // GIST_FULL_SLAB=<columns> overrides (0 = one pass).
   int64_t slab = 0;
   const int64_t e = sizeof(TI);
-  if (!a.mbits && !a.desc && a.rows >= 65536) {
-    const int64_t fit = ((int64_t)128 << 20) / (a.rows * e);
+  const int64_t hr = a.h_rows > a.rows ? a.h_rows : a.rows;  // gathered rows of H
+  if (!a.mbits && !a.desc && hr >= 65536) {
+    const int64_t fit = ((int64_t)128 << 20) / (hr * e);
     slab = fit >= a.w ? 0 : std::max<int64_t>(128, (fit / 64) * 64);
   }
   if (const char* env = std::getenv("GIST_FULL_SLAB")) slab = atoll(env);

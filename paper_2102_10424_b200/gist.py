@@ -17,7 +17,7 @@ GIST_ARCH_GCN, GIST_ARCH_SAGE, GIST_ARCH_GAT = 0, 1, 2
 ARCHS = {"gcn": GIST_ARCH_GCN, "sage": GIST_ARCH_SAGE, "gat": GIST_ARCH_GAT}
 GIST_OPT_SGD, GIST_OPT_ADAM = 0, 1
 GIST_PREC_FP32, GIST_PREC_BF16 = 0, 1
-GIST_GRAPH_DEVICE, GIST_GRAPH_HOST = 0, 1
+GIST_GRAPH_DEVICE = 0
 TRACE_NODES, TRACE_ACT, TRACE_LOGITS, TRACE_GRAD, TRACE_LOSS = range(5)
 (STAT_ROUND, STAT_STEP, STAT_SELF_LOOPS_DROPPED, STAT_LAST_NNZ_B, STAT_LAST_NB, STAT_KERNELS,
  STAT_H2D_BYTES, STAT_D2H_BYTES, STAT_MAX_NB, STAT_BLOCK_AGG, STAT_BLOCK_DENSITY_PPM) = range(11)
@@ -29,8 +29,9 @@ EXPORTS = [
     "gist_get_partition", "gist_sub_shape", "gist_get_sub_params", "gist_get_trace", "gist_stat",
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
     "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
+    "gist_eval_logits", "gist_loopback_create", "gist_loopback_destroy",
 ]
-PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc"]
+PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc", "comm"]
 
 
 GIST_OPT_STATE_RESET, GIST_OPT_STATE_PERSISTENT = 0, 1
@@ -44,7 +45,7 @@ class GistConfig(C.Structure):
         ("precision", C.c_int32), ("clusters_per_batch", C.c_int32), ("batch_seed", C.c_uint64),
         ("graph_residency", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("device", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
-        ("opt_state", C.c_int32), ("agg_mode", C.c_int32),
+        ("opt_state", C.c_int32), ("agg_mode", C.c_int32), ("loopback", C.c_void_p),
     ]
 
 
@@ -89,6 +90,9 @@ def lib() -> C.CDLL:
         "gist_slot_owner": (i32, [i32, i32]),
         "gist_slots_per_rank": (i32, [i32, i32]),
         "gist_profile_get": (i32, [vp, i32, P(C.c_double), P(i64), P(C.c_double)]),
+        "gist_eval_logits": (i32, [vp, i32, vp, i32, i64, vp]),
+        "gist_loopback_create": (i32, [i32, P(vp)]),
+        "gist_loopback_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -113,7 +117,7 @@ class Gist:
                  clusters_per_batch: int = 1, batch_seed: int = 0, rank: int = 0, world_size: int = 1,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream: int | None = None,
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset",
-                 agg_mode: str = "allgather"):
+                 agg_mode: str = "allgather", loopback: "Loopback | None" = None):
         L = lib()
         self.arch = arch
         self.dims = [int(d) for d in dims]
@@ -136,6 +140,8 @@ class Gist:
         cfg.stream = stream
         cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
         cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P}[agg_mode]
+        self._lb = loopback  # keeps the group alive while this context exists
+        cfg.loopback = loopback.h if loopback is not None else None
         self._cfg = cfg
         h = C.c_void_p()
         self._check(L.gist_create(C.byref(cfg), C.byref(h)), None)
@@ -171,6 +177,7 @@ class Gist:
         self._check(lib().gist_load_graph(self.h, n, _ptr(rp), _ptr(ci), int(rp[-1]), _ptr(X), _ptr(lab),
                                           int(g["num_classes"]), _ptr(sp), _ptr(cl), int(g["num_clusters"])))
         self.num_clusters = int(g["num_clusters"])
+        self.num_nodes = n
 
     def init_params(self, seed: int):
         self._check(lib().gist_init_params(self.h, seed))
@@ -207,6 +214,17 @@ class Gist:
                                           num_parts if part_ids is not None else 0, max_rows,
                                           C.byref(loss), C.byref(acc), _ptr(lp), _ptr(ap)))
         return loss.value, acc.value, lp, ap
+
+    def eval_logits(self, mode: int = 0, part_ids=None, num_parts: int = 0, max_rows: int = 0) -> np.ndarray:
+        """Per-node logits [n x d_L] (original node ids) of the forward gist_eval (mode 0) or
+        gist_eval_parts (mode 1) runs."""
+        n = self.num_nodes
+        out = np.zeros((n, self.dims[-1]), dtype=np.float32)
+        if part_ids is not None:
+            part_ids = np.ascontiguousarray(part_ids, dtype=np.int32)
+        self._check(lib().gist_eval_logits(self.h, mode, _ptr(part_ids) if part_ids is not None else None,
+                                           int(num_parts) if part_ids is not None else 0, max_rows, _ptr(out)))
+        return out
 
     def param_shape(self, layer: int):
         d = self.dims[layer]
@@ -264,6 +282,30 @@ class Gist:
             self._check(lib().gist_profile_get(self.h, k, C.byref(ms), C.byref(n), C.byref(w)))
             out[name] = {"ms": ms.value, "launches": n.value, "work": w.value}
         return out
+
+
+class Loopback:
+    """Loopback transport group (gist_loopback_create): `world` contexts of this process, each
+    driven by its own thread, stand in for `world` ranks on one GPU (tests of the W > 1 paths)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        st = lib().gist_loopback_create(world, C.byref(h))
+        if st != 0:
+            raise GistError(f"gist_loopback_create: {lib().gist_status_str(st).decode()}")
+        self.h = h
+        self.world = world
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gist_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def slot_owner(slot: int, world: int) -> int:

@@ -20,6 +20,9 @@ CASES = [
     ("ragged", dict(n=700, nnz=6000, d0=29, classes=6, clusters=11), (29, 40, 24, 6), 3),
     ("wide", dict(n=900, nnz=16000, d0=130, classes=11, clusters=9), (130, 300, 11), 2),
     ("deep", dict(n=500, nnz=3000, d0=17, classes=5, clusters=10), (17, 64, 48, 33, 5), 2),
+    # input wider than the 2,048 columns one warp holds in registers (Citeseer-like d_0): the
+    # score dot products H (W a) loop over every 128-column chunk
+    ("wide-input", dict(n=300, nnz=2000, d0=2100, classes=6, clusters=6), (2100, 40, 6), 2),
 ]
 
 
@@ -176,3 +179,12 @@ def test_gat_c3g_full_size_one_step(precision):
         assert rel_err(gpu.trace(i, 1, 1).reshape(nb, -1), tr["tape"]["H"][1][p]) <= act_tol
         for l in range(len(dims) - 1):
             assert rel_err(gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape), tr["grads"][l]) <= grad_tol, (i, l)
+
+
+def test_gat_rejects_outputs_wider_than_registers():
+    """The attention passes hold an output row in registers (2,048 columns): wider GAT layers are
+    refused at create (GIST_E_UNSUPPORTED) instead of silently dropping columns."""
+    from paper_2102_10424_b200.gist import Gist, GistError
+    with pytest.raises(GistError, match="UNSUPPORTED"):
+        Gist("gat", (16, 2056, 4))
+    Gist("gat", (3000, 2048, 4)).close()   # wide input, widest supported output: accepted
