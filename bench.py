@@ -307,23 +307,25 @@ def oracle_extras(spec, g):
 
 def c1_side_by_side(G, seed=0):
     """C1 (Cora-shaped GCN, m = 2, 5 rounds x 10 local iterations) completely on both
-    the oracle and the CUDA path (FP32 parity mode), with their per-round losses and wall times."""
+    the oracle and the CUDA path (FP32 parity mode), with their per-round losses and wall times.
+    SGD (lr 0.1): under Adam the two trajectories separate by design after the first round (its
+    first step after every re-partition is -lr sign(g))."""
     import torch
     from oracle import gist_oracle as O
     spec = MODELS["C1"]
     g = generate(GRAPHS[spec.graph], seed=seed)
-    o = O.OracleGIST(arch=spec.arch, dims=list(spec.dims), optimizer="adam", clusters_per_batch=spec.q, batch_seed=1)
+    o = O.OracleGIST(arch=spec.arch, dims=list(spec.dims), optimizer="sgd", clusters_per_batch=spec.q, batch_seed=1)
     o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
                  g["cluster_ids"], g["num_clusters"])
     o.init_params(seed)
-    c = G.Gist(spec.arch, spec.dims, optimizer="adam", precision="fp32", clusters_per_batch=spec.q, batch_seed=1)
+    c = G.Gist(spec.arch, spec.dims, optimizer="sgd", precision="fp32", clusters_per_batch=spec.q, batch_seed=1)
     t0 = time.perf_counter()
     c.load_graph(g)
     c.init_params(seed)
     lg = []
     for t in range(spec.rounds):
         c.partition(seed=1000 + t, m=spec.m)
-        lg.append(c.subtrain(spec.zeta, 0.01))
+        lg.append(c.subtrain(spec.zeta, 0.1))
         c.aggregate()
     torch.cuda.synchronize()
     t_gpu = time.perf_counter() - t0
@@ -331,12 +333,13 @@ def c1_side_by_side(G, seed=0):
     lo = []
     for t in range(spec.rounds):
         o.partition(seed=1000 + t, m=spec.m)
-        lo.append(o.subtrain(spec.zeta, 0.01))
+        lo.append(o.subtrain(spec.zeta, 0.1))
         o.aggregate()
     t_or = time.perf_counter() - t0
     c.close()
     lg, lo = np.array(lg, dtype=np.float64), np.array(lo)
-    return {"rounds": spec.rounds, "zeta": spec.zeta, "m": spec.m, "gpu_s": t_gpu, "oracle_s": t_or,
+    return {"rounds": spec.rounds, "zeta": spec.zeta, "m": spec.m, "optimizer": "sgd", "lr": 0.1,
+            "gpu_s": t_gpu, "oracle_s": t_or,
             "max_rel_loss_diff": float(np.max(np.abs(lg - lo) / np.maximum(np.abs(lo), 1e-12))),
             "gpu_losses": lg.round(6).tolist(), "oracle_losses": lo.round(6).tolist()}
 

@@ -78,6 +78,13 @@ enum { GIST_OPT_STATE_RESET = 0, GIST_OPT_STATE_PERSISTENT = 1 };
  * second pass over the gathered bytes.  Not available for GAT (R21 averages the m copies
  * of the attention rows, which needs every copy on every rank): GIST_E_UNSUPPORTED. */
 enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1 };
+/* Output scaling of the evaluation forward (R10; the theory scales the global
+ * model's output by 1/m so that the expected sub-GCN output equals the global one).  NONE
+ * (default): Eq. (1) as written.  MEAN: every contraction over a partitioned input dimension
+ * (layers l >= 1, input dim d_l) is scaled by 1/m, m of the last gist_partition -- applied to
+ * the W rows of those layers (GAT: not to the attention vectors).  Evaluation only; training
+ * is unaffected. */
+enum { GIST_EVAL_SCALE_NONE = 0, GIST_EVAL_SCALE_MEAN = 1 };
 
 /* Loopback transport (tests): W contexts of ONE process on one device stand in for W ranks.
  * Every collective of gist_aggregate / gist_eval / gist_eval_parts (all-gather, sum all-reduce,
@@ -110,6 +117,7 @@ typedef struct {
   int32_t opt_state;          /* GIST_OPT_STATE_* (default RESET) */
   int32_t agg_mode;           /* GIST_AGG_* (default ALLGATHER) */
   gist_loopback* loopback;    /* tests: loopback group of world_size ranks replacing NCCL, or NULL */
+  int32_t eval_scale;         /* GIST_EVAL_SCALE_* (default NONE, R10) */
 } gist_config;
 
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
@@ -127,8 +135,9 @@ gist_status gist_create(const gist_config* cfg, gist_ctx** out);
 /* Loads graph G (n nodes, features X in R^{n x d_0}) and its Cluster
  * partition (METIS is an input here, not computed).
  *  row_ptr[n+1] (int64, non-decreasing, row_ptr[0] = 0, row_ptr[n] = nnz),
- *  col_idx[nnz] (int32 in [0,n), symmetric adjacency, no self loops -- self loops
- *     present in the input are dropped and counted, see gist_stat),
+ *  col_idx[nnz] (int32 in [0,n), strictly increasing within each row, symmetric adjacency:
+ *     every (u,v) has its (v,u); no self loops -- self loops present in the input are dropped
+ *     and counted, see gist_stat; violations are rejected on the device with GIST_E_ARG),
  *  X[n*d_0] fp32 row-major, labels[n] int32 in [0,num_classes), num_classes = d_L,
  *  split[n] uint8: 0 train, 1 val, 2 test, 3 none,
  *  cluster_ids[n] int32 in [0,num_clusters), every cluster non-empty.
@@ -293,6 +302,12 @@ gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_dev, int64_
 gist_status gist_gemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
                       const void* A_dev, int64_t lda, const void* B_dev, int64_t ldb,
                       void* C_dev, int64_t ldc, int32_t dtype, int32_t out_f32, int32_t relu, void* stream);
+/* The same GEMM launched `reps` times back to back from one plan (the tcgen05 tensor maps are
+ * encoded once): device timing of the kernel without per-call host work (tools/gemm_probe.py). */
+gist_status gist_gemm_reps(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
+                           const void* A_dev, int64_t lda, const void* B_dev, int64_t ldb,
+                           void* C_dev, int64_t ldc, int32_t dtype, int32_t out_f32, int32_t relu, void* stream,
+                           int32_t reps);
 
 #ifdef __cplusplus
 }

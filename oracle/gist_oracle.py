@@ -585,16 +585,33 @@ class OracleGIST:
         d = self.dims[L - 1]
         theta[L - 1][d:d + 2] = np.mean([sub[L - 1][-2:] for sub in subs], axis=0)
 
-    def eval(self, split_code: int):
-        """Forward of the global model on the full graph (R10: no output scaling)."""
+    def eval_theta(self, eval_scale: str = "none"):
+        """The weights the evaluation forward uses.  R10 (the theory scales the
+        global output by 1/m so that E[sub-GCN output] = global output): "none" (default) = Eq. (1)
+        as written; "mean" = every contraction over a partitioned input dimension -- the hidden
+        dims d_1..d_{L-1}, i.e. layers l >= 1 -- is scaled by 1/m (m of the last partition), done
+        by scaling those layers' W rows (GAT: the W rows, not the attention vectors)."""
+        if eval_scale == "none" or self.m <= 1:
+            return self.theta
+        out = [self.theta[0]]
+        for l in range(1, len(self.theta)):
+            w = self.theta[l].copy()
+            rows = self.dims[l] if self.arch == "gat" else w.shape[0]
+            w[:rows] /= self.m
+            out.append(w)
+        return out
+
+    def eval(self, split_code: int, eval_scale: str = "none"):
+        """Forward of the global model on the full graph (R10: no output scaling by default)."""
         op = self.operator(self.row_ptr, self.col_idx, self.n)
-        logits = forward(self.arch, self.theta, op, self.X)["logits"]
+        logits = forward(self.arch, self.eval_theta(eval_scale), op, self.X)["logits"]
         rows = self.split == split_code
         loss, _ = softmax_ce(logits, self.labels, rows)
         acc = float(np.mean(np.argmax(logits[rows], axis=1) == self.labels[rows])) if rows.any() else 0.0
         return loss, acc, logits
 
-    def eval_partitions(self, split_code: int, part_ids, num_parts: int, parts=None):
+    def eval_partitions(self, split_code: int, part_ids, num_parts: int, parts=None, logits_out=None,
+                        eval_scale: str = "none"):
         """Partition-wise evaluation (PAPER.md:696-697, Appendix "Training Ultra-Wide GCNs";
         reading R20): the graph is cut into `num_parts` partitions (part_ids[v] in
         [0, num_parts)); every partition is evaluated on its own induced subgraph with the
@@ -602,6 +619,8 @@ class OracleGIST:
         score measured on each partition is averaged over the partitions that hold at least
         one node with split == split_code.  Single-label F1 (micro) = accuracy.
         `parts`: evaluate only these partition ids (the means then cover only them).
+        `logits_out`: optional float array [n x d_L]; the rows of every evaluated partition's
+        nodes receive their logits (also for partitions without split_code nodes).
         Returns (mean loss, mean acc, per-partition loss, per-partition acc; NaN = no
         evaluated node)."""
         part = np.asarray(part_ids, dtype=np.int64)
@@ -611,11 +630,15 @@ class OracleGIST:
         for p in (range(num_parts) if parts is None else parts):
             nodes = np.nonzero(part == p)[0]              # ascending global id
             rows = self.split[nodes] == split_code
-            if not rows.any():
+            if not rows.any() and (logits_out is None or len(nodes) == 0):
                 continue
             rp, ci = induced_subgraph(self.row_ptr, self.col_idx, nodes)
             op = self.operator(rp, ci, len(nodes))
-            logits = forward(self.arch, self.theta, op, self.X[nodes])["logits"]
+            logits = forward(self.arch, self.eval_theta(eval_scale), op, self.X[nodes])["logits"]
+            if logits_out is not None:
+                logits_out[nodes] = logits
+            if not rows.any():
+                continue
             y = self.labels[nodes]
             loss_p[p], _ = softmax_ce(logits, y, rows)
             acc_p[p] = float(np.mean(np.argmax(logits[rows], axis=1) == y[rows]))

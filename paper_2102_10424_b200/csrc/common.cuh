@@ -2,6 +2,8 @@
 // Not shared with oracle/ (the oracle carries its own Philox; both are pinned to
 // the Random123 known-answer vectors).
 #pragma once
+#include <mutex>
+#include <unordered_map>
 #include <utility>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -102,6 +104,34 @@ __device__ __forceinline__ void st16(__nv_bfloat16* p, const float* v) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: set it once per
+// (kernel, device) -- a context on a second device must not launch without it.
+inline void ensure_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;  // kernel -> bitmask of devices
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lk(mu);
+  uint64_t& m = done[kern];
+  if (!(m & bit)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    m |= bit;
+  }
+}
+// SM count of the current device (cached per device)
+inline int device_sms() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& v = n[dev & 63];
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
 template <typename... P, typename... A>
 inline void launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
   cudaLaunchConfig_t cfg = {};

@@ -330,8 +330,6 @@ struct Tile {
   bool mma;    // false: zero-fill only (inert dummy rows of a batch)
   const CUtensorMap *ma, *mb;
   int a_row, b_col, b_k0, K;  // TMA coordinates
-  int a_k0 = 0;                // K offset of A (split-K chunk)
-  bool split = false;          // split-K chunk: the epilogue adds into the output (fp32 atomics)
   int64_t out_row0;
   int rows_valid, n0, N;
   int stream_a;  // evict_first hint on the A loads
@@ -344,24 +342,13 @@ struct ProbPlain {
   using Group = GemmGroupTC;
   static constexpr bool kTmaEpi = true;  // epilogue staging + TMA stores
   static __device__ __forceinline__ int ydim(const Group& G) { return G.tm; }
-  static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn * G.ksplit; }
+  static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
   static constexpr int kMaxDesc = 1;
   static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
   static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sd) {
-    const int ks = t % G.ksplit;  // the split-K chunks of one tile go to consecutive CTAs
-    t /= G.ksplit;
     const int per = G.tm * G.tn;
     const int z = t / per, r = t - z * per;
-    Tile T = decode_y(G, z, r / G.tn, r % G.tn, sd);
-    if (G.ksplit > 1) {
-      const int k0 = ks * G.kchunk;
-      T.split = true;
-      T.a_k0 = k0;
-      T.b_k0 = k0;
-      T.K = T.K - k0 < G.kchunk ? T.K - k0 : G.kchunk;
-      if (T.K <= 0) T.valid = T.mma = false;
-    }
-    return T;
+    return decode_y(G, z, r / G.tn, r % G.tn, sd);
   }
   // tile (slot z, 128-row tile y, n-tile nt)
   static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t*) {
@@ -475,7 +462,7 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
     // chunk j of row r at r*128 + ((j ^ (r & 7)) * 16), bank-conflict free) and written by
     // one cp.async.bulk.tensor per 32 x 128 B box, so stores are full lines instead of one
     // 16-byte piece of 32 different rows per instruction.
-    const bool tma = TMA_EPI && T.E.mc && !T.split && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
+    const bool tma = TMA_EPI && T.E.mc && (T.E.clip || lq * 32 + 32 <= T.rows_valid);
     constexpr int CPB = OUT_F32 ? 32 : 64;  // columns per 128-byte box row
 #pragma unroll 1
     for (int c = c0w; c < c0w + CW; c += 32) {
@@ -533,19 +520,6 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
             bits |= (T.n0 + c + i < T.N && sv > 0.f) ? (1u << i) : 0u;
           }
           T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
-        }
-      } else if (OUT_F32 && T.split) {  // split-K chunk: add into the zeroed fp32 output
-        if (live && T.n0 + c < T.N) {
-          float* dst = (float*)T.E.C + row * T.E.ldc + T.n0 + c;
-          if (T.n0 + c + 32 <= T.N && (((uintptr_t)dst & 15) == 0)) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              atomicAdd(reinterpret_cast<float4*>(dst + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (T.n0 + c + i < T.N) atomicAdd(dst + i, v[i]);
-          }
         }
       } else if (live && T.n0 + c < T.N) {
         epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
@@ -645,18 +619,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           if (T.stream_a) {  // last read of A for a while: evict first
             const uint64_t pol = policy_evict_first();
             if (!A_MN) {
-              tma_load_2d_hint(sa, T.ma, &full[s], T.a_k0 + k0, T.a_row, pol);
+              tma_load_2d_hint(sa, T.ma, &full[s], k0, T.a_row, pol);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, T.a_k0 + k0, pol);
+                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0, pol);
             }
           } else if (!A_MN) {
-            tma_load_2d(sa, T.ma, &full[s], T.a_k0 + k0, T.a_row);
+            tma_load_2d(sa, T.ma, &full[s], k0, T.a_row);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, T.a_k0 + k0);
+              tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0);
           }
           if (!B_MN) {
             tma_load_2d(sb, T.mb, &full[s], T.b_k0 + k0, T.b_col);
@@ -909,16 +883,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_cons
   }
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return device_sms(); }
 
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -952,14 +917,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool l2hint_enabled() {  // GIST_L2HINT=0: no L2 eviction-priority hints (A/B measurements)
-  static const bool on = [] { const char* e = std::getenv("GIST_L2HINT"); return !(e && e[0] == '0'); }();
-  return on;
-}
-bool tma_store_enabled() {  // GIST_TMA_STORE=0: direct epilogue stores (A/B measurements)
-  static const bool on = [] { const char* e = std::getenv("GIST_TMA_STORE"); return !(e && e[0] == '0'); }();
-  return on;
-}
+
 // Output store map: C [outer x inner] (ld elements), boxes of 32 rows x 128 bytes, SWIZZLE_128B.
 bool make_store_map(CUtensorMap* map, void* base, int64_t inner, int64_t outer, int64_t ld, bool f32) {
   EncodeFn enc = get_encode();
@@ -978,18 +936,9 @@ template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
 void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
   auto kern = k_gemm_persist<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
   constexpr int SMEM = Cfg<BN, ST>::SMEM_BASE + (Prob::kTmaEpi ? Cfg<BN, ST>::EPI_BYTES : 0) + 64;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
+  ensure_smem((const void*)kern, SMEM);
   const int grid = total < num_sms() ? total : num_sms();
   if (grid > 0) launch_pdl(kern, grid, kGemmThreads, SMEM, s, G);
-}
-
-bool pair_enabled() {  // GIST_2CTA=0: never use CTA pairs (A/B measurements)
-  static const bool on = [] { const char* e = std::getenv("GIST_2CTA"); return !(e && e[0] == '0'); }();
-  return on;
 }
 
 // CTA-pair launch: clusters of 2 (cudaLaunchAttributeClusterDimension) + PDL, grid = 2 x pairs
@@ -999,11 +948,7 @@ void launch_pair(const typename Prob::Group& G, int total2, cudaStream_t s) {
   constexpr int STAGE = BM * BK * 2 + (BN / 2) * BK * 2;
   constexpr int SMEM = ST * STAGE + (Prob::kTmaEpi ? kEpiWarps * 4096 : 0) + 1024 + 256 + 64;
   auto kern = k_gemm_pair<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
+  ensure_smem((const void*)kern, SMEM);
   const int pairs = total2 < num_sms() / 2 ? total2 : num_sms() / 2;
   if (pairs <= 0) return;
   cudaLaunchConfig_t cfg = {};
@@ -1073,10 +1018,9 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
   // A single-op launch (one slot per lockstep group: one sub-GCN per GPU at W = m) whose
   // 256-wide tiles leave SMs idle takes 128-wide ones: single-slot C3 groups 2,806 -> 2,863
   // steps/s; measured slower for 2-op (4,627 -> 4,564) and 8-op (8,46x -> 8,364) launches, so
-  // the rule stops at one op (profiles/r01p_*; GIST_BN_FEW=<max ops> overrides, 0 = off)
+  // the rule stops at one op (profiles/r01p_*)
   {
-    static const int few = [] { const char* e = std::getenv("GIST_BN_FEW"); return e ? atoi(e) : 1; }();
-    if (P->bn == 256 && n <= few) {
+    if (P->bn == 256 && n == 1) {
       int64_t t256 = 0;
       for (int i = 0; i < n; ++i) t256 += cdiv(ops[i].M, BM) * cdiv(ops[i].N, 256);
       if (t256 < (int64_t)num_sms()) P->bn = 128;
@@ -1093,7 +1037,7 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     }
     static const int64_t kmin_pair = [] { const char* e = std::getenv("GIST_PAIR_KMIN"); return e ? atoll(e) : 2048; }();
     static const int64_t tiles_pair = [] { const char* e = std::getenv("GIST_PAIR_TILES"); return e ? atoll(e) : 4; }();
-    P->pair = pair_enabled() && tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
+    P->pair = tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
   }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
@@ -1118,9 +1062,9 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     S.ldadd = o.ldadd;
     S.mbits_in = o.mbits_in;
     S.ldmbi = o.ldmbi;
-    S.keep_out = l2hint_enabled() ? o.keep_out : 0;
-    S.stream_a = l2hint_enabled() ? o.stream_a : 0;
-    S.tma_store = tma_store_enabled() && make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
+    S.keep_out = o.keep_out;
+    S.stream_a = o.stream_a;
+    S.tma_store = make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
     S.M = (int)o.M;
     S.N = (int)o.N;
     S.K = (int)o.K;
@@ -1129,48 +1073,11 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
   }
   P->G.tm = (int)cdiv(P->maxM, BM);
   P->G.tn = (int)cdiv(P->maxN, P->bn);
-  // split-K when the tile space leaves most SMs idle (few, long-K tiles: the step's dW GEMMs,
-  // K = batch rows): fp32 outputs without epilogue operands only.  Opt-in (GIST_SPLITK=1):
-  // measured slower -- C3 8,265 vs 8,386 steps/s, single-slot groups 2,025 vs 2,779 (the chunks
-  // of one tile add into the same addresses at the same time, and each short chunk pays the
-  // pipeline fill and a full-tile epilogue)
-  P->G.ksplit = 1;
-  P->G.kchunk = 0;
-  static const bool splitk = [] { const char* e = std::getenv("GIST_SPLITK"); return e && e[0] == '1'; }();
-  bool plain = splitk && !P->pair && o0.out_f32;
-  int64_t tiles = 0, kmax = 0;
-  for (int i = 0; i < n; ++i) {
-    const GemmOp& o = ops[i];
-    plain = plain && !o.relu && !o.mask && !o.rscale && !o.add && !o.mbits && !o.mbits_in;
-    tiles += cdiv(o.M, BM) * cdiv(o.N, P->bn);
-    kmax = o.K > kmax ? o.K : kmax;
-  }
-  if (plain) {
-    const int64_t nkb = cdiv(kmax, BK);
-    int64_t ks = (2 * (int64_t)num_sms()) / (tiles > 0 ? tiles : 1);
-    ks = ks < 8 ? ks : 8;
-    ks = ks < nkb / 4 ? ks : nkb / 4;
-    if (ks >= 2) {
-      P->G.ksplit = (int)ks;
-      P->G.kchunk = (int)(cdiv(nkb, ks) * BK);
-      for (int i = 0; i < n; ++i) P->G.s[i].tma_store = 0;
-    }
-  }
   return true;
-}
-
-// split-K outputs start at zero: one launch zeroes every op's M x N block (row stride ldc)
-__global__ void k_zero_ops(const __grid_constant__ GemmGroupTC G) {
-  const GemmSlotTC& S = G.s[blockIdx.y];
-  float* C = (float*)S.C;
-  const int64_t total = (int64_t)S.M * S.N;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
-    C[(i / S.N) * S.ldc + (i % S.N)] = 0.f;
 }
 
 void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
   if (P.G.n <= 0 || P.maxM <= 0 || P.maxN <= 0) return;
-  if (P.G.ksplit > 1) k_zero_ops<<<dim3(64, (unsigned)P.G.n), 256, 0, s>>>(P.G);
   if (P.bn == 256) dispatch_layout<256>(P, s);
   else dispatch_layout<128>(P, s);
 }
@@ -1201,17 +1108,16 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.global_rows = o.global_rows;
     S.N = (int)o.N;
     S.tma_store = 0;  // ProbBd::kTmaEpi == false
-    S.keep_out = l2hint_enabled() ? o.keep_out : 0;
+    S.keep_out = o.keep_out;
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;
   // single-slot launches: 128-wide tiles when 256-wide ones leave SMs idle (one slot per group:
   // block aggregation 35.6 -> 32.5 ms per profiled sample, 2,861 -> 2,867-2,873 steps/s,
-  // profiles/r01s_*; GIST_BD_FEW=<max ops> overrides, 0 = off); multi-slot launches unchanged
+  // profiles/r01s_*); multi-slot launches unchanged
   {
-    static const int few = [] { const char* e = std::getenv("GIST_BD_FEW"); return e ? atoi(e) : 1; }();
     const int64_t t256 = (int64_t)n * ((int64_t)q * cdiv(bs, BM) + cdiv(rows, BM)) * cdiv(P->maxN, 256);
-    if (P->bn == 256 && n <= few && t256 < (int64_t)num_sms()) P->bn = 128;
+    if (P->bn == 256 && n == 1 && t256 < (int64_t)num_sms()) P->bn = 128;
   }
   P->G.tn = (int)cdiv(P->maxN, P->bn);
   return true;
@@ -1224,13 +1130,13 @@ void gemm_bd_launch(const BdPlan& P, cudaStream_t s) {
 }
 
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda, const bf16* B,
-               int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s) {
+               int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s, int reps) {
   if (!get_encode()) return false;
   if (M == 0 || N == 0) return true;  // nothing to do (also the availability probe)
   GemmOp o{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, out_f32, relu, nullptr, 0, nullptr, 0};
   GemmPlanTC P;
   if (!gemm_bf16_prepare(&o, 1, &P)) return false;
-  gemm_bf16_launch(P, s);
+  for (int r = 0; r < reps; ++r) gemm_bf16_launch(P, s);  // one plan (tensor maps encoded once)
   return true;
 }
 

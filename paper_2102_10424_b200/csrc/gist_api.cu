@@ -440,6 +440,7 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
   if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
   if (cfg->agg_mode != GIST_AGG_ALLGATHER && cfg->agg_mode != GIST_AGG_P2P) return GIST_E_ARG;
+  if (cfg->eval_scale != GIST_EVAL_SCALE_NONE && cfg->eval_scale != GIST_EVAL_SCALE_MEAN) return GIST_E_ARG;
   if (cfg->agg_mode == GIST_AGG_P2P && (cfg->arch == GIST_ARCH_GAT || cfg->world_size > kMaxPeers))
     return GIST_E_UNSUPPORTED;  // R21 needs every copy of the attention rows; PeerDst holds 8 ranks
   if (cfg->clusters_per_batch < 1 || cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
@@ -704,18 +705,20 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
     int32_t* cid_o = nullptr;
     unsigned long long* cnt = nullptr;
     TRY(dalloc_t(c, &cid_o, n));
-    TRY(dalloc_t(c, &cnt, 3));
+    TRY(dalloc_t(c, &cnt, 5));
     CK(cudaMemcpyAsync(cid_o, cluster_ids, n * 4, cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(cnt, 0, 5 * sizeof(unsigned long long), s));
     LK(validate_edges(rp_o, col_o, cid_o, n, cnt, s));
-    unsigned long long h[3] = {0, 0, 0};
+    unsigned long long h[5] = {0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     dfree(c, cid_o);
     dfree(c, cnt);
-    if (h[0]) {
+    if (h[0] || h[3] || h[4]) {
       dfree(c, rp_o), dfree(c, col_o), dfree(c, perm_d), dfree(c, inv_d), dfree(c, deg_new);
-      return fail(c, GIST_E_ARG, "load_graph: col_idx out of range");
+      return fail(c, GIST_E_ARG, h[0] ? "load_graph: col_idx out of range"
+                                 : h[3] ? "load_graph: col_idx not strictly increasing within a row (unsorted or duplicate edges)"
+                                        : "load_graph: adjacency not symmetric (an edge (u,v) without (v,u))");
     }
     c->self_loops = (int64_t)h[1];
     c->nnz = nnz - c->self_loops;
@@ -1037,10 +1040,6 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
   const bool sage = c->arch == GIST_ARCH_SAGE;
   const bool tc = c->prec == GIST_PREC_BF16;
-  // GIST_SPMM_SLAB=1 enables the cluster-slab SpMM (measured slower than the L2 row gather
-  // on Reddit-shape batches: issue-bound, profiles/r01*_ncu_spmm_ct.txt); default off
-  const char* slab_env = std::getenv("GIST_SPMM_SLAB");
-  const int slab_max = (slab_env && slab_env[0] == '1') ? c->max_csize : 0;
   // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
   // L2-footprint / launch-count trade-off
   int gsz = kMaxGroup;
@@ -1272,7 +1271,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         // forward aggregation (a2)
         SpmmArgs<T, T>& a = g.fwd_spmm[l].a[j];
         a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-        a.desc = sl.desc_dev; a.st = c->dstate; a.q = q; a.max_cluster = slab_max;  // cluster slabs
+        a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
         if (sage) {
           a.rowscale = sl.scale;               // N = D^-1 A (R2)
           a.out = C + sh.half; a.ldo = sh.Kp;   // right half: N H
@@ -1327,7 +1326,7 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
           SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
           b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
-          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q; b.max_cluster = slab_max;
+          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
           b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
           if (tc) { b.mbits = sl.mb[l]; b.ld_mbits = c->mb_ld[l]; }  // ReLU mask of C_l / H_l as bits
           if (sage && bd) {  // dZ_{l-1} = (dC_self + A_blocks dC'_neigh + A_inter dC'_neigh) * 1[H_l > 0]
@@ -2031,27 +2030,68 @@ static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N,
   return GIST_OK;
 }
 
+// The weights of the evaluation forward: per layer the fp32 weights (Theta_l, or a copy with its W
+// rows scaled by 1/m for layers l >= 1 under eval_scale MEAN, R10) and their T-typed GEMM operand
+// (the same pointer in FP32 mode, a bf16 copy in BF16 mode).
+struct EvalWeights {
+  std::vector<float*> w32;
+  std::vector<void*> wT;
+  std::vector<void*> owned;
+};
+template <typename T>
+static gist_status eval_weights(gist_ctx* c, EvalWeights& ew) {
+  cudaStream_t s = c->stream;
+  ew.w32.assign(c->L, nullptr);
+  ew.wT.assign(c->L, nullptr);
+  const bool mean = c->cfg.eval_scale == GIST_EVAL_SCALE_MEAN && c->m > 1;
+  for (int l = 0; l < c->L; ++l) {
+    const int64_t n = c->th_K[l] * c->th_N[l];
+    ew.w32[l] = c->theta[l];
+    if (mean && l > 0) {  // hidden input dim d_l is partitioned: scale the W rows (not GAT's a rows)
+      const int64_t nw = (c->arch == GIST_ARCH_GAT ? pad8(c->dims[l]) : c->th_K[l]) * c->th_N[l];
+      float* w = nullptr;
+      TRY(dalloc_t(c, &w, (size_t)n));
+      ew.owned.push_back(w);
+      LK(scale_prefix_f32(c->theta[l], w, n, nw, 1.0f / (float)c->m, s));
+      ew.w32[l] = w;
+    }
+    if (sizeof(T) == 2) {
+      void* b = nullptr;
+      TRY(dalloc(c, &b, (size_t)n * 2));
+      ew.owned.push_back(b);
+      LK(f32_to_bf16(ew.w32[l], (bf16*)b, n, s));
+      ew.wT[l] = b;
+    } else {
+      ew.wT[l] = ew.w32[l];
+    }
+  }
+  return GIST_OK;
+}
+static void free_eval_weights(gist_ctx* c, EvalWeights& ew) {
+  for (void* p : ew.owned) dfree(c, p);
+  ew.owned.clear();
+}
+
 // GAT forward of the global model over `rows` rows of a CSR without self loops (R21): layer 0
 // reads X0 (ld pad8(d_0)); hidden outputs alternate between bufA / bufB; fp32 logits (ld th_N).
 template <typename T>
 static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* row_beg, const int64_t* row_end,
-                                    const int32_t* col, const T* X0, const std::vector<void*>& wl, T* bufA, T* bufB,
+                                    const int32_t* col, const T* X0, const EvalWeights& ew, T* bufA, T* bufB,
                                     T* Z, float* sc, float* logits, cudaStream_t s) {
   const T* Hin = X0;
   int64_t ldin = pad8(c->dims[0]);
   T* Hout = bufA;
   for (int l = 0; l < c->L; ++l) {
     const int64_t K = pad8(c->dims[l]), N = c->th_N[l];
-    const void* Wl = sizeof(T) == 2 ? wl[l] : (const void*)c->theta[l];
-    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, Wl, N, Z, N, sizeof(T) == 4, false, s));
+    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, ew.wT[l], N, Z, N, sizeof(T) == 4, false, s));
     GatGroup<T> G;
     G.n = 1;
     GatLayer<T>& a = G.a[0];
     a.row_beg = row_beg; a.row_end = row_end; a.col = col; a.rows = rows; a.w = N;
     a.Z = Z; a.ldz = N;
-    a.a_src = c->theta[l] + K * N; a.a_dst = a.a_src + N;
+    a.a_src = ew.w32[l] + K * N; a.a_dst = a.a_src + N;
     a.s = sc; a.t = sc + rows; a.lse = sc + 2 * rows;
-    a.H = Hin; a.ldh = ldin; a.kw = K; a.W32 = c->theta[l]; a.ldw = N; a.wa = sc + 3 * rows;
+    a.H = Hin; a.ldh = ldin; a.kw = K; a.W32 = ew.w32[l]; a.ldw = N; a.wa = sc + 3 * rows;
     if (l + 1 < c->L) { a.out = Hout; a.ldo = N; a.relu = 1; }
     else { a.out_f32 = logits; a.ldo = N; }
     LK(gat_scores<T>(G, s));
@@ -2086,9 +2126,11 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float*
   const int64_t Nl = c->th_N[c->L - 1];
   int64_t maxK = 0;
   for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
-  void *bufA = nullptr, *bufB = nullptr, *wtmp = nullptr;
+  void *bufA = nullptr, *bufB = nullptr;
   float* logits = nullptr;
   double* out3 = nullptr;
+  EvalWeights ew;
+  TRY(eval_weights<T>(c, ew));
   TRY(dalloc(c, &bufA, (size_t)npad * maxK * sizeof(T)));
   TRY(dalloc(c, &bufB, (size_t)npad * maxK * sizeof(T)));
   TRY(dalloc_t(c, &logits, (size_t)npad * Nl));
@@ -2096,21 +2138,14 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float*
   T* Cb = (T*)bufA;
   T* Hn = (T*)bufB;
   if (gat) {
-    std::vector<void*> wl(c->L, nullptr);
     int64_t maxN = 0;
     for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
     void* Z = nullptr;
     float* sc = nullptr;
     TRY(dalloc(c, &Z, (size_t)n * maxN * sizeof(T)));
     TRY(dalloc_t(c, &sc, (size_t)3 * std::max<int64_t>(n, 1) + 2 * maxK));
-    if (sizeof(T) == 2)
-      for (int l = 0; l < c->L; ++l) {
-        TRY(dalloc(c, &wl[l], (size_t)c->th_K[l] * c->th_N[l] * 2));
-        LK(f32_to_bf16(c->theta[l], (bf16*)wl[l], c->th_K[l] * c->th_N[l], s));
-      }
-    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, wl, Cb, Hn, (T*)Z, sc, logits, s));
+    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, ew, Cb, Hn, (T*)Z, sc, logits, s));
     CK(cudaStreamSynchronize(s));
-    for (void* p : wl) if (p) dfree(c, p);
     dfree(c, Z);
     dfree(c, sc);
   }
@@ -2130,13 +2165,7 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float*
       a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb + r0 * K; a.ldo = K; a.w = K;
     }
     if (nr > 0) LK((spmm<T, T>(a, s)));
-    const void* Wl = c->theta[l];
-    if (sizeof(T) == 2) {
-      if (wtmp) dfree(c, wtmp);
-      TRY(dalloc(c, &wtmp, (size_t)K * N * 2));
-      LK(f32_to_bf16(c->theta[l], (bf16*)wtmp, K * N, s));
-      Wl = wtmp;
-    }
+    const void* Wl = ew.wT[l];
     if (l + 1 < c->L) {
       // next layer input: GCN H_{l+1} -> Hn; SAGE H_{l+1} -> left half of Hn, which becomes the
       // next concat buffer (swap)
@@ -2174,7 +2203,7 @@ static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float*
   dfree(c, bufB);
   dfree(c, logits);
   dfree(c, out3);
-  if (wtmp) dfree(c, wtmp);
+  free_eval_weights(c, ew);
   return GIST_OK;
 }
 
@@ -2224,12 +2253,8 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
   int64_t maxK = 0;
   for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
   const int64_t Nl = c->th_N[c->L - 1];
-  std::vector<void*> wl(c->L, nullptr);
-  if (sizeof(T) == 2)
-    for (int l = 0; l < c->L; ++l) {
-      TRY(dalloc(c, &wl[l], (size_t)c->th_K[l] * c->th_N[l] * 2));
-      LK(f32_to_bf16(c->theta[l], (bf16*)wl[l], c->th_K[l] * c->th_N[l], s));
-    }
+  EvalWeights ew;
+  TRY(eval_weights<T>(c, ew));
   const int64_t row_bytes = 2 * maxK * (int64_t)sizeof(T) + Nl * 4;
   if (max_rows <= 0) {
     size_t fr = 0, tot = 0;
@@ -2307,7 +2332,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
     if (c->arch == GIST_ARCH_GAT) {  // X rows of the chunk gathered, then the GAT layers
       const int64_t d0p = pad8(c->dims[0]);
       LK(gather_rows_t<T>((const T*)c->X, d0p, pnode_d + k0, rows, d0p, (T*)gX, d0p, s));
-      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, wl, Cb, Hn, (T*)gZ, gsc, logits,
+      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, ew, Cb, Hn, (T*)gZ, gsc, logits,
                               s));
     }
     for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {
@@ -2325,7 +2350,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
         a.colscale = pscale + k0; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
       }
       LK((spmm<T, T>(a, s)));
-      const void* Wl = sizeof(T) == 2 ? wl[l] : (const void*)c->theta[l];
+      const void* Wl = ew.wT[l];
       if (l + 1 < c->L) {
         TRY(gemm_any(c, false, false, rows, N, K, Cb, K, Wl, N, Hn, c->th_K[l + 1], false, true, s));
         if (sage) std::swap(Cb, Hn);
@@ -2367,7 +2392,7 @@ static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t
       dfree(c, lr);
     }
   }
-  for (void* p : wl) if (p) dfree(c, p);
+  free_eval_weights(c, ew);
   for (void* p : {gX, gZ, (void*)gsc}) if (p) dfree(c, p);
   for (void* p : {(void*)pnode_d, (void*)pos_d, (void*)part_d, (void*)rb_d, (void*)pcol, (void*)deg, (void*)prp,
                   (void*)lbeg_d, (void*)pscale, (void*)out3, bufA, bufB, (void*)logits})
@@ -2595,10 +2620,6 @@ extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_
     SpmmArgs<bf16, bf16> a;
     a.row_beg = row_ptr_dev; a.row_end = row_ptr_dev + 1; a.col = col_dev; a.rows = rows; a.rowscale = rowscale_dev; a.colscale = colscale_dev;
     a.self = self; a.H = (const bf16*)H_dev; a.ldh = ld; a.out = (bf16*)out_dev; a.ldo = ld; a.w = pad8(w);
-    const char* few = std::getenv("GIST_SPMM_ENTRY_FEW");  // tools/kbench_inter.py: few-neighbour kernels
-    a.few_nnz = few && few[0] == '1';
-    const char* add = std::getenv("GIST_SPMM_ENTRY_ADD");  // tools/kbench_inter.py: in-place add (out += ...)
-    if (add && add[0] == '1') { a.add = (const bf16*)out_dev; a.ld_add = ld; }
     spmm<bf16, bf16>(a, s);
   } else {
     return GIST_E_ARG;
@@ -2609,13 +2630,21 @@ extern "C" gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_
 extern "C" gist_status gist_gemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K, const void* A_dev,
                                  int64_t lda, const void* B_dev, int64_t ldb, void* C_dev, int64_t ldc, int32_t dtype,
                                  int32_t out_f32, int32_t relu, void* stream) {
-  if (!A_dev || !B_dev || !C_dev || M < 0 || N < 0 || K < 0) return GIST_E_ARG;
+  return gist_gemm_reps(transA, transB, M, N, K, A_dev, lda, B_dev, ldb, C_dev, ldc, dtype, out_f32, relu, stream, 1);
+}
+
+extern "C" gist_status gist_gemm_reps(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
+                                      const void* A_dev, int64_t lda, const void* B_dev, int64_t ldb, void* C_dev,
+                                      int64_t ldc, int32_t dtype, int32_t out_f32, int32_t relu, void* stream,
+                                      int32_t reps) {
+  if (!A_dev || !B_dev || !C_dev || M < 0 || N < 0 || K < 0 || reps < 1) return GIST_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == 0) {
-    gemm_f32(transA, transB, M, N, K, (const float*)A_dev, lda, (const float*)B_dev, ldb, (float*)C_dev, ldc, relu, s);
+    for (int r = 0; r < reps; ++r)
+      gemm_f32(transA, transB, M, N, K, (const float*)A_dev, lda, (const float*)B_dev, ldb, (float*)C_dev, ldc, relu, s);
   } else if (dtype == 1) {
     if (!gemm_bf16(transA, transB, M, N, K, (const bf16*)A_dev, lda, (const bf16*)B_dev, ldb, C_dev, ldc, out_f32,
-                   relu, s))
+                   relu, s, reps))
       return GIST_E_UNSUPPORTED;
   } else {
     return GIST_E_ARG;

@@ -341,17 +341,13 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
                  const uint8_t* split, int skip_intra, int ob, cudaStream_t s) {
   if (G.nb_max <= 0) return;
   // two 512-thread CTAs per SM (launch bounds) shared by the slots; rows are dealt dynamically
-  const int per_slot = std::max(1, std::min((int)cdiv(G.nb_max, kBuildRows), 2 * 148 / std::max(G.n, 1)));
+  const int per_slot = std::max(1, std::min((int)cdiv(G.nb_max, kBuildRows), 2 * device_sms() / std::max(G.n, 1)));
   const dim3 grid((unsigned)per_slot, (unsigned)G.n);
   const size_t smem = (size_t)num_clusters * 4;
   const char* force = std::getenv("GIST_BATCH_GLOBAL_MAP");  // tests: exercise the global-map path
   if (smem <= 64 * 1024 && !(force && force[0] == '1')) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_batch_build<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      cudaFuncSetAttribute(k_batch_build<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
+    ensure_smem((const void*)k_batch_build<true, false>, 64 * 1024);
+    ensure_smem((const void*)k_batch_build<true, true>, 64 * 1024);
     if (ob > 0)
       launch_pdl(k_batch_build<true, true>, grid, kBuildRows * 32, smem, s, G, rp, col, ccol, cid, arch, labels,
                  split, skip_intra, cstart, num_clusters, ob);
@@ -380,8 +376,6 @@ void edge_codes(const int32_t* col, const int32_t* cid, const int64_t* cstart, i
 }
 int pack_bits(int num_clusters, int64_t max_csize) {
   if ((size_t)num_clusters * 4 > 64 * 1024 || std::getenv("GIST_BATCH_GLOBAL_MAP")) return 0;
-  const char* env = std::getenv("GIST_PACK_EDGES");
-  if (env && env[0] == '0') return 0;
   int ob = 1, cb = 1;
   while (((int64_t)1 << ob) < max_csize) ++ob;
   while ((1 << cb) < num_clusters) ++cb;
@@ -394,38 +388,50 @@ __global__ void k_edge_clusters(const int32_t* __restrict__ col, const int32_t* 
     ccol[e] = cid[col[e]];
 }
 // Edge checks of load_graph on the device (one warp per row, original ids): out[0] = edges with
-// col out of [0, n), out[1] = self loops, out[2] = non-loop edges inside a cluster.  Block-reduced
-// integer atomics: deterministic.
+// col out of [0, n), out[1] = self loops, out[2] = non-loop edges inside a cluster, out[3] = edges
+// not strictly after their predecessor in the row (unsorted or duplicate), out[4] = edges (v, u)
+// whose reverse (u, v) is missing (binary search in row u; the backward SpMM^T reuses the CSR of
+// the symmetric A).  Block-reduced integer atomics: deterministic.
+__device__ __forceinline__ bool row_has(const int64_t* rp, const int32_t* col, int64_t u, int32_t v) {
+  int64_t lo = rp[u], hi = rp[u + 1] - 1;
+  while (lo <= hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int32_t x = col[mid];
+    if (x == v) return true;
+    if (x < v) lo = mid + 1; else hi = mid - 1;
+  }
+  return false;
+}
 __global__ void __launch_bounds__(256) k_validate_edges(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                         const int32_t* __restrict__ cid, int64_t n,
                                                         unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long sb[3];
-  if (threadIdx.x < 3) sb[threadIdx.x] = 0;
+  constexpr int NC = 5;
+  __shared__ unsigned long long sb[NC];
+  if (threadIdx.x < NC) sb[threadIdx.x] = 0;
   __syncthreads();
   const int64_t v = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  unsigned long long bad = 0, self = 0, intra = 0;
+  unsigned long long c[NC] = {0, 0, 0, 0, 0};
   if (v < n) {
     const int32_t cv = cid[v];
     for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) {
       const int32_t u = col[e];
-      if (u < 0 || u >= n) { ++bad; continue; }
-      if (u == v) ++self;
-      else if (cid[u] == cv) ++intra;
+      if (e > rp[v] && col[e - 1] >= u) ++c[3];
+      if (u < 0 || u >= n) { ++c[0]; continue; }
+      if (u == v) { ++c[1]; continue; }
+      if (cid[u] == cv) ++c[2];
+      if (!row_has(rp, col, u, (int32_t)v)) ++c[4];
     }
   }
-  for (int o = 16; o; o >>= 1) {
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
-    self += __shfl_xor_sync(0xffffffffu, self, o);
-    intra += __shfl_xor_sync(0xffffffffu, intra, o);
-  }
-  if (lane == 0) {
-    if (bad) atomicAdd(&sb[0], bad);
-    if (self) atomicAdd(&sb[1], self);
-    if (intra) atomicAdd(&sb[2], intra);
-  }
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+    for (int o = 16; o; o >>= 1) c[k] += __shfl_xor_sync(0xffffffffu, c[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+      if (c[k]) atomicAdd(&sb[k], c[k]);
   __syncthreads();
-  if (threadIdx.x < 3 && sb[threadIdx.x]) atomicAdd(&out[threadIdx.x], sb[threadIdx.x]);
+  if (threadIdx.x < NC && sb[threadIdx.x]) atomicAdd(&out[threadIdx.x], sb[threadIdx.x]);
 }
 void validate_edges(const int64_t* rp, const int32_t* col, const int32_t* cid, int64_t n, unsigned long long* out,
                     cudaStream_t s) {

@@ -44,14 +44,10 @@ struct SpmmArgs {
   // (H row, colscale); neighbours are graph ids.  h_rows = rows of H the gathers may reach
   // (0: rows), for the 32-bit offset choice.
   int64_t row0 = 0, h_rows = 0;
-  // Cluster-slab staging (batch SpMMs only): rows of each batch cluster are a contiguous
-  // local-id range loff[k]..loff[k+1] (from the step descriptor).  When set, one CTA stages
-  // cluster k's rows of H (a column tile) in shared memory and serves intra-cluster
-  // neighbours from it.  max_cluster = largest cluster (rows), bounds the slab.
+  // batch SpMMs: the step descriptor (marks the launch as a mini-batch pass, not full-graph)
   const int32_t* desc = nullptr;
   const StepState* st = nullptr;
   int q = 0;
-  int max_cluster = 0;
   int few_nnz = 0;  // hint: rows have few neighbours (inter-cluster pass): favour occupancy
 };
 template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
@@ -122,9 +118,6 @@ struct alignas(64) GemmSlotTC {
 struct GemmGroupTC {
   GemmSlotTC s[kMaxGemmOps];
   int n = 0, tm = 0, tn = 0;  // slots, M tiles, N tiles (persistent tile space)
-  // split-K (fp32 outputs without epilogue operands, few tiles): every tile's K range is cut into
-  // ksplit chunks of kchunk (multiple of 64) reduced with fp32 atomics into a zeroed output
-  int ksplit = 1, kchunk = 0;
 };
 // Host-side plan of one grouped tcgen05 GEMM (tensor maps encoded once, launched many times).
 struct GemmPlanTC {
@@ -188,7 +181,8 @@ struct SgemmGroup {
 void gemm_f32_group(const SgemmGroup& g, cudaStream_t s);
 // returns false if the shape/alignment is not supported by the tensor-core path
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda,
-               const bf16* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s);
+               const bf16* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s,
+               int reps = 1);
 
 // --------------------------------------------------------------------------
 // Graph load (relabel nodes so clusters are contiguous) and Cluster mini-batch
@@ -260,7 +254,8 @@ int pack_bits(int num_clusters, int64_t max_csize);
 void edge_codes(const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t nnz, int ob, int32_t* code,
                 cudaStream_t s);
 void edge_clusters(const int32_t* col, const int32_t* cid, int64_t nnz, int32_t* ccol, cudaStream_t s);
-// out[3] (zeroed by the caller): edges with col outside [0, n), self loops, intra-cluster edges
+// out[5] (zeroed by the caller): edges with col outside [0, n), self loops, intra-cluster edges,
+// unsorted / duplicate edges within a row, edges without their reverse (asymmetric A)
 void validate_edges(const int64_t* rp, const int32_t* col, const int32_t* cid, int64_t n, unsigned long long* out,
                     cudaStream_t s);
 // Binary intra-cluster adjacency blocks: blocks[c][i][j] = 1 iff (cstart[c]+i, cstart[c]+j) is an
@@ -298,17 +293,6 @@ template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);
 void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
                StepState* st, bf16* Wb, cudaStream_t s);
 void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s);
-// per-layer optimizer step over one block per slot (offsets / lengths in floats, multiples of 4)
-struct OptRanges {
-  int64_t off[kMaxGroup];
-  int64_t len[kMaxGroup];
-  int n = 0;
-  int64_t total = 0;
-};
-void opt_ranges_step(bool adam, float* W, const float* G, float* M, float* V, const OptRanges& R, float b1, float b2,
-                     float eps, StepState* st, bf16* Wb, bool advance, cudaStream_t s);
-// (the optimizer kernels advance the step state themselves: their last CTA increments z, t)
-void step_advance(StepState* st, cudaStream_t s);
 // Re-associated last layer: Wcat[r][c2] = [W_top | W_bot] (half x 2Np, row-major) from the
 // bf16 shadow W = [W_top; W_bot] (2 half x Np), so dH = [dZ | Q] Wcat^T is one K = 2 Np GEMM.
 struct RelayoutGroup {
@@ -319,6 +303,8 @@ struct RelayoutGroup {
 };
 void relayout_last(const RelayoutGroup& G, cudaStream_t s);
 void f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s);
+// dst[i] = src[i] * (i < n_scaled ? s : 1) (eval_scale MEAN: the W rows of a layer, R10)
+void scale_prefix_f32(const float* src, float* dst, int64_t n, int64_t n_scaled, float s, cudaStream_t st);
 
 // --------------------------------------------------------------------------
 // subGCNs / subAgg / init (R5, R6, R9, R11).

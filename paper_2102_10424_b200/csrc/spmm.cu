@@ -204,183 +204,6 @@ __global__ void __launch_bounds__(256, PRED ? 3 : (J == 1 && sizeof(TI) == 2) ? 
   }
 }
 
-// Cluster-slab variant for mini-batch SpMMs (north_star: "shared-memory staging of feature
-// tiles").  CTA = (batch cluster k, column tile) of one slot.  The cluster's rows of H for the
-// tile (LPR*J 16-byte vectors per row) are staged in shared memory with coalesced 16-byte
-// loads; the cluster's rows are then aggregated by groups of LPR lanes, reading neighbours
-// inside the cluster (most edges of a Cluster batch) from shared memory
-// and the rest from global/L2.  Same arithmetic and order as k_spmm.
-template <typename TI, typename TO, int LPR, int J, bool CSCALE>
-__global__ void __launch_bounds__(512, 2)
-    k_spmm_ct(const __grid_constant__ SpmmGroup<TI, TO> G, int ntiles) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ uint4 slab[];
-  constexpr int V = Elem<TI>::kVec;
-  constexpr int TV = LPR * J;  // vectors per row in the tile
-  constexpr int UN = 4;        // neighbours in flight per group
-  const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];
-  const int k = blockIdx.x / ntiles, tile = blockIdx.x % ntiles;
-  const int q = a.q;
-  const int32_t* d = a.desc + (size_t)a.st->z * (3 * q + 4);
-  const int c0 = tile * TV;  // first vector column of the tile
-  const int64_t wv = a.w / V;
-  if (k == q) {  // inert dummy rows [n_b, rows): exact zeros (rowscale 0, no neighbours)
-    const int nb = d[2 * q];
-    const int64_t cnt = (a.rows - nb) * TV;
-    for (int64_t idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
-      const int64_t v = nb + idx / TV;
-      const int jv = (int)(idx % TV);
-      if (c0 + jv < wv) {
-        float z[V];
-#pragma unroll
-        for (int e = 0; e < V; ++e) z[e] = 0.f;
-        const int64_t c = (int64_t)(c0 + jv) * V;
-        if constexpr (sizeof(TO) == sizeof(TI)) {
-          st16(a.out + v * a.ldo + c, z);
-        } else {
-          constexpr int VO = Elem<TO>::kVec;
-#pragma unroll
-          for (int p2 = 0; p2 < V / VO; ++p2) st16(a.out + v * a.ldo + c + p2 * VO, z);
-        }
-      }
-    }
-    return;
-  }
-  if (k >= d[3 * q + 2]) return;  // fewer clusters in this batch
-  const int r0 = d[q + k], nrow = d[q + k + 1] - r0;
-  const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
-  const int64_t ldv = a.ldh / V;
-  // ---- stage the cluster slab [nrow x TV] (zero beyond the row width)
-  for (int idx = threadIdx.x; idx < nrow * TV; idx += blockDim.x) {
-    const int i = idx / TV, jv = idx - i * TV;
-    const int64_t src = a.h_index ? (int64_t)a.h_index[r0 + i] : (int64_t)(r0 + i);
-    slab[idx] = (c0 + jv < wv) ? __ldg(H4 + src * ldv + c0 + jv) : make_uint4(0, 0, 0, 0);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int gl = lane % LPR;
-  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane - gl));
-  const int ngroups = (blockDim.x >> 5) * (32 / LPR);
-  const int grp = (threadIdx.x >> 5) * (32 / LPR) + lane / LPR;
-  bool act[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) act[j] = c0 + gl + j * LPR < wv;
-  for (int i = grp; i < nrow; i += ngroups) {
-    const int64_t v = r0 + i;
-    float acc[J][V];
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-#pragma unroll
-      for (int e = 0; e < V; ++e) acc[j][e] = 0.f;
-    if (a.self || a.self_out) {
-      const float s = a.colscale ? a.colscale[v] : 1.f;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        if (!act[j]) continue;
-        const uint4 x = slab[i * TV + gl + j * LPR];
-        if (a.self_out)
-          *reinterpret_cast<uint4*>(a.self_out + v * a.ld_self + (int64_t)(c0 + gl + j * LPR) * V) = x;
-        if (a.self) {
-          float t[V];
-          unpack(x, t, TI());
-#pragma unroll
-          for (int e = 0; e < V; ++e) acc[j][e] = s * t[e];
-        }
-      }
-    }
-    const int64_t beg = a.row_beg[v], end = a.row_end[v];
-    for (int64_t base = beg; base < end; base += LPR) {
-      const int n = (end - base) < LPR ? (int)(end - base) : LPR;
-      int32_t uu = 0;
-      float su = 1.f;
-      if (gl < n) {
-        uu = a.col[base + gl];
-        if (CSCALE) su = a.colscale[uu];
-      }
-      for (int jj = 0; jj < n; jj += UN) {
-        uint4 x[UN][J];
-        float s[UN];
-#pragma unroll
-        for (int qq = 0; qq < UN; ++qq) {
-          const bool valid = jj + qq < n;
-          const int32_t u = __shfl_sync(gmask, uu, valid ? jj + qq : jj, LPR);
-          s[qq] = valid ? (CSCALE ? __shfl_sync(gmask, su, jj + qq, LPR) : 1.f) : 0.f;
-          const unsigned li = (unsigned)(u - r0);
-          if (li < (unsigned)nrow) {  // intra-cluster neighbour: shared memory
-#pragma unroll
-            for (int j = 0; j < J; ++j) x[qq][j] = slab[li * TV + gl + j * LPR];
-          } else {                    // other clusters of the batch: global / L2
-            const int64_t src = a.h_index ? (int64_t)a.h_index[u] : (int64_t)u;
-#pragma unroll
-            for (int j = 0; j < J; ++j)
-              x[qq][j] = act[j] ? __ldg(H4 + src * ldv + c0 + gl + j * LPR) : make_uint4(0, 0, 0, 0);
-          }
-        }
-#pragma unroll
-        for (int qq = 0; qq < UN; ++qq) {
-          if (jj + qq >= n) break;  // fixed summation order: neighbours in CSR order
-#pragma unroll
-          for (int j = 0; j < J; ++j) {
-            float t[V];
-            unpack(x[qq][j], t, TI());
-#pragma unroll
-            for (int e = 0; e < V; ++e) acc[j][e] = CSCALE ? fmaf(s[qq], t[e], acc[j][e]) : acc[j][e] + t[e];
-          }
-        }
-      }
-    }
-    const float rs = a.rowscale ? a.rowscale[v] : 1.f;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      if (!act[j]) continue;
-      const int64_t c = (int64_t)(c0 + gl + j * LPR) * V;
-      float o[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) o[e] = acc[j][e] * rs;
-      if (a.add) {
-        float t[V];
-        unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] += t[e];
-      }
-      if (a.mask) {
-        float t[V];
-        unpack(*reinterpret_cast<const uint4*>(a.mask + v * a.ld_mask + c), t, TI());
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = t[e] > 0.f ? o[e] : 0.f;  // ReLU'(0) = 0 (R3)
-      }
-      if (a.relu) {
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = fmaxf(o[e], 0.f);
-      }
-      if constexpr (sizeof(TO) == sizeof(TI)) {
-        st16(a.out + v * a.ldo + c, o);
-      } else {
-        constexpr int VO = Elem<TO>::kVec;
-#pragma unroll
-        for (int p2 = 0; p2 < V / VO; ++p2) st16(a.out + v * a.ldo + c + p2 * VO, o + p2 * VO);
-      }
-    }
-  }
-}
-
-template <typename TI, typename TO, int LPR, int J>
-void launch_ct(const SpmmGroup<TI, TO>& G, int64_t w, int maxc, cudaStream_t s) {
-  constexpr int TV = LPR * J;
-  const int ntiles = (int)cdiv(w, TV * Elem<TI>::kVec);
-  const size_t smem = (size_t)maxc * TV * 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_spmm_ct<TI, TO, LPR, J, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_spmm_ct<TI, TO, LPR, J, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  const dim3 grid((unsigned)((G.a[0].q + 1) * ntiles), (unsigned)G.n);  // + dummy-row CTA per tile
-  if (G.a[0].colscale) launch_pdl(k_spmm_ct<TI, TO, LPR, J, true>, grid, 512, smem, s, G, ntiles);
-  else launch_pdl(k_spmm_ct<TI, TO, LPR, J, false>, grid, 512, smem, s, G, ntiles);
-}
-
 template <typename TI, typename TO, int LPR, int J>
 void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s) {
   constexpr int CW = LPR * J * Elem<TI>::kVec;
@@ -431,15 +254,6 @@ void spmm_group(const SpmmGroup<TI, TO>& G, cudaStream_t s) {
   if (G.n <= 0 || rows <= 0 || w <= 0) return;
   constexpr int V = Elem<TI>::kVec;
   const int64_t vecs = cdiv(w, V);  // 16-byte vectors per row (widest slot)
-  // cluster-slab path: the slab (largest cluster x tile) must fit 2 CTAs per SM
-  const int maxc = G.a[0].max_cluster;
-  if (G.a[0].desc && maxc > 0) {
-    constexpr int64_t budget = 100 * 1024;
-    if (vecs <= 8 && (int64_t)maxc * 8 * 16 <= budget) return launch_ct<TI, TO, 8, 1>(G, w, maxc, s);
-    if (vecs <= 16 && (int64_t)maxc * 16 * 16 <= budget) return launch_ct<TI, TO, 16, 1>(G, w, maxc, s);
-    if ((int64_t)maxc * 32 * 16 <= budget) return launch_ct<TI, TO, 32, 1>(G, w, maxc, s);
-    if ((int64_t)maxc * 16 * 16 <= budget) return launch_ct<TI, TO, 16, 1>(G, w, maxc, s);
-  }
   if (vecs <= 4) launch<TI, TO, 4, 1>(G, rows, w, s);
   else if (vecs <= 8) launch<TI, TO, 8, 1>(G, rows, w, s);
   else if (vecs <= 16) launch<TI, TO, 16, 1>(G, rows, w, s);
@@ -457,7 +271,6 @@ void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
   // 21.4 -> 16.9 ms, width 4096 160 -> 137 ms with 256-column slabs (64 columns: slower, the
   // 128-byte row pieces and 8 CSR passes cost more than the L2 hits save; 384 / 512 columns:
   // 211 / 172 ms at width 4096; evict-first loads of the CSR stream: no change).
-  // GIST_FULL_SLAB=<columns> overrides (0 = one pass).
   int64_t slab = 0;
   const int64_t e = sizeof(TI);
   const int64_t hr = a.h_rows > a.rows ? a.h_rows : a.rows;  // gathered rows of H
@@ -465,7 +278,6 @@ void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s) {
     const int64_t fit = ((int64_t)128 << 20) / (hr * e);
     slab = fit >= a.w ? 0 : std::max<int64_t>(128, (fit / 64) * 64);
   }
-  if (const char* env = std::getenv("GIST_FULL_SLAB")) slab = atoll(env);
   if (slab <= 0 || slab >= a.w) {
     SpmmGroup<TI, TO> G;
     G.a[0] = a;

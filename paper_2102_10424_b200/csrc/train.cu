@@ -146,83 +146,6 @@ void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1
   launch_pdl(k_adam, (unsigned)(blocks > 0 ? blocks : 1), 256, 0, s, W, G, M, V, n, b1, b2, eps, st, Wb);
 }
 
-// Per-layer optimizer launch (the dW side stream): the same update over up to kMaxGroup
-// ranges (one per slot: that layer's block of the packed slot buffer); only the launch with
-// `advance` set (the last layer of the step) advances the step state.
-__device__ __forceinline__ int64_t range_index(const OptRanges& R, int64_t i4) {
-  int64_t i = i4 * 4;
-#pragma unroll 1
-  for (int k = 0; k < R.n; ++k) {
-    if (i < R.len[k]) return R.off[k] + i;
-    i -= R.len[k];
-  }
-  return -1;
-}
-__global__ void k_adam_r(float* __restrict__ W, const float* __restrict__ G, float* __restrict__ M,
-                         float* __restrict__ V, const __grid_constant__ OptRanges R, float b1, float b2, float eps,
-                         StepState* st, bf16* __restrict__ Wb, int advance) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ float s_step, s_bc2;
-  if (threadIdx.x == 0) {
-    const double t = (double)(st->t + 1);
-    s_step = st->lr / (float)(1.0 - pow((double)b1, t));
-    s_bc2 = sqrtf((float)(1.0 - pow((double)b2, t)));
-  }
-  __syncthreads();
-  const float step = s_step, bc2_sqrt = s_bc2;
-  const int64_t n4 = R.total >> 2;
-  for (int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = range_index(R, i4);
-    const int64_t i = e >> 2;
-    float4 w = reinterpret_cast<float4*>(W)[i];
-    const float4 g = reinterpret_cast<const float4*>(G)[i];
-    float4 m = reinterpret_cast<float4*>(M)[i];
-    float4 v = reinterpret_cast<float4*>(V)[i];
-    float* wp = &w.x; const float* gp = &g.x; float* mp = &m.x; float* vp = &v.x;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      mp[j] = b1 * mp[j] + (1.f - b1) * gp[j];
-      vp[j] = b2 * vp[j] + (1.f - b2) * gp[j] * gp[j];
-      const float denom = sqrtf(vp[j]) / bc2_sqrt + eps;
-      wp[j] = wp[j] - step * (mp[j] / denom);
-    }
-    reinterpret_cast<float4*>(W)[i] = w;
-    reinterpret_cast<float4*>(M)[i] = m;
-    reinterpret_cast<float4*>(V)[i] = v;
-    if (Wb) {
-      reinterpret_cast<__nv_bfloat162*>(Wb)[2 * i] = __floats2bfloat162_rn(w.x, w.y);
-      reinterpret_cast<__nv_bfloat162*>(Wb)[2 * i + 1] = __floats2bfloat162_rn(w.z, w.w);
-    }
-  }
-  if (advance) advance_if_last(st);
-}
-__global__ void k_sgd_r(float* __restrict__ W, const float* __restrict__ G, const __grid_constant__ OptRanges R,
-                        StepState* st, bf16* __restrict__ Wb, int advance) {
-  pdl_wait();
-  pdl_trigger();
-  const float lr = st->lr;
-  const int64_t n4 = R.total >> 2;
-  for (int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i4 < n4; i4 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = range_index(R, i4);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float w = W[e + j] - lr * G[e + j];
-      W[e + j] = w;
-      if (Wb) Wb[e + j] = __float2bfloat16_rn(w);
-    }
-  }
-  if (advance) advance_if_last(st);
-}
-void opt_ranges_step(bool adam, float* W, const float* G, float* M, float* V, const OptRanges& R, float b1, float b2,
-                     float eps, StepState* st, bf16* Wb, bool advance, cudaStream_t s) {
-  if (R.total <= 0) return;
-  const int64_t b = cdiv(R.total >> 2, 256);
-  const unsigned blocks = (unsigned)(b < 148 * 8 ? (b > 0 ? b : 1) : 148 * 8);
-  if (adam) launch_pdl(k_adam_r, blocks, 256, 0, s, W, G, M, V, R, b1, b2, eps, st, Wb, (int)advance);
-  else launch_pdl(k_sgd_r, blocks, 256, 0, s, W, G, R, st, Wb, (int)advance);
-}
-
 __global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_t n, StepState* st,
                       bf16* __restrict__ Wb) {
   pdl_wait();
@@ -241,13 +164,6 @@ void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cuda
   launch_pdl(k_sgd, (unsigned)blocks, 256, 0, s, W, G, n, st, Wb);
 }
 
-__global__ void k_step_advance(StepState* st) {
-  pdl_wait();
-  pdl_trigger();
-  st->z += 1;
-  st->t += 1;
-}
-void step_advance(StepState* st, cudaStream_t s) { launch_pdl(k_step_advance, 1, 1, 0, s, st); }
 
 __global__ void k_relayout_last(const __grid_constant__ RelayoutGroup G) {
   pdl_wait();
@@ -273,6 +189,16 @@ void f32_to_bf16(const float* src, bf16* dst, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
   k_f32_to_bf16<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n);
+}
+
+__global__ void k_scale_prefix(const float* __restrict__ src, float* __restrict__ dst, int64_t n, int64_t ns, float s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = i < ns ? src[i] * s : src[i];
+}
+void scale_prefix_f32(const float* src, float* dst, int64_t n, int64_t n_scaled, float s, cudaStream_t st) {
+  if (n <= 0) return;
+  const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
+  k_scale_prefix<<<(unsigned)blocks, 256, 0, st>>>(src, dst, n, n_scaled, s);
 }
 
 // Evaluation: out3 = {sum CE over rows with split==code, #correct (argmax, ties -> lowest index), #rows}

@@ -29,7 +29,7 @@ EXPORTS = [
     "gist_get_partition", "gist_sub_shape", "gist_get_sub_params", "gist_get_trace", "gist_stat",
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
     "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
-    "gist_eval_logits", "gist_loopback_create", "gist_loopback_destroy",
+    "gist_eval_logits", "gist_loopback_create", "gist_loopback_destroy", "gist_gemm_reps",
 ]
 PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc", "comm"]
 
@@ -45,7 +45,7 @@ class GistConfig(C.Structure):
         ("precision", C.c_int32), ("clusters_per_batch", C.c_int32), ("batch_seed", C.c_uint64),
         ("graph_residency", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("device", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
-        ("opt_state", C.c_int32), ("agg_mode", C.c_int32), ("loopback", C.c_void_p),
+        ("opt_state", C.c_int32), ("agg_mode", C.c_int32), ("loopback", C.c_void_p), ("eval_scale", C.c_int32),
     ]
 
 
@@ -85,6 +85,7 @@ def lib() -> C.CDLL:
         "gist_destroy": (None, [vp]),
         "gist_spmm": (i32, [vp, vp, i64, vp, vp, i32, vp, vp, i64, i64, i32, vp]),
         "gist_gemm": (i32, [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, vp]),
+        "gist_gemm_reps": (i32, [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, vp, i32]),
         "gist_profile": (i32, [vp, i32]),
         "gist_nccl_unique_id": (i32, [vp]),
         "gist_slot_owner": (i32, [i32, i32]),
@@ -117,7 +118,7 @@ class Gist:
                  clusters_per_batch: int = 1, batch_seed: int = 0, rank: int = 0, world_size: int = 1,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream: int | None = None,
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset",
-                 agg_mode: str = "allgather", loopback: "Loopback | None" = None):
+                 agg_mode: str = "allgather", loopback: "Loopback | None" = None, eval_scale: str = "none"):
         L = lib()
         self.arch = arch
         self.dims = [int(d) for d in dims]
@@ -140,6 +141,7 @@ class Gist:
         cfg.stream = stream
         cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
         cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P}[agg_mode]
+        cfg.eval_scale = {"none": 0, "mean": 1}[eval_scale]
         self._lb = loopback  # keeps the group alive while this context exists
         cfg.loopback = loopback.h if loopback is not None else None
         self._cfg = cfg
@@ -338,8 +340,9 @@ def spmm(row_ptr_dev: int, col_dev: int, rows: int, rowscale_dev: int | None, co
 
 
 def gemm(transA: bool, transB: bool, M: int, N: int, K: int, A_dev: int, lda: int, B_dev: int, ldb: int,
-         C_dev: int, ldc: int, dtype: int, out_f32: bool = True, relu: bool = False, stream: int | None = None):
-    st = lib().gist_gemm(int(transA), int(transB), M, N, K, A_dev, lda, B_dev, ldb, C_dev, ldc, dtype,
-                         int(out_f32), int(relu), stream)
+         C_dev: int, ldc: int, dtype: int, out_f32: bool = True, relu: bool = False, stream: int | None = None,
+         reps: int = 1):
+    st = lib().gist_gemm_reps(int(transA), int(transB), M, N, K, A_dev, lda, B_dev, ldb, C_dev, ldc, dtype,
+                              int(out_f32), int(relu), stream, reps)
     if st != 0:
         raise GistError(f"gist_gemm: {lib().gist_status_str(st).decode()}")

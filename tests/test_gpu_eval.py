@@ -112,13 +112,19 @@ def test_eval_parts_c3_full_size_sampled(c3, precision):
     gpu = Gist(spec.arch, list(spec.dims), precision=precision, clusters_per_batch=spec.q)
     gpu.load_graph(g)
     gpu.init_params(11)
+    from tests.gpu_helpers import rel_err
     lg, ag, lpg, apg = gpu.eval_parts(2, part, 5000)
     sample = np.random.default_rng(0).choice(5000, 12, replace=False)
-    _, _, lpo, apo = ora.eval_partitions(2, part, 5000, parts=sample)
+    lref = np.zeros((len(g["labels"]), g["num_classes"]))
+    _, _, lpo, apo = ora.eval_partitions(2, part, 5000, parts=sample, logits_out=lref)
     ok = ~np.isnan(apo[sample])
     assert ok.sum() >= 8
     s = sample[ok]
     t = TOL[precision]
+    # per node: the logits of every node of the sampled partitions
+    lgot = gpu.eval_logits(1, part, 5000)
+    nodes = np.nonzero(np.isin(part, sample))[0]
+    assert rel_err(lgot[nodes], lref[nodes]) <= t
     assert np.max(np.abs(lpg[s] - lpo[s])) <= t * max(1.0, np.max(np.abs(lpo[s])))
     if precision == "fp32":
         assert np.array_equal(apg[s], apo[s].astype(np.float32))
@@ -139,13 +145,104 @@ def test_full_graph_eval_c2_full_size(precision):
     dims = list(spec.dims)
     gpu, ora = make_pair(g, spec.arch, dims, precision=precision, q=spec.q)
     t = TOL[precision]
+    from tests.gpu_helpers import rel_err
     for code in (1, 2):
         lg, ag = gpu.eval(code)
-        lo, ao, _ = ora.eval(code)
+        lo, ao, lref = ora.eval(code)
         assert abs(lg - lo) <= t * max(1.0, abs(lo)), (code, lg, lo)
+        if code == 1:   # per node, every one of the 169,343 rows
+            assert rel_err(gpu.eval_logits(0), lref) <= t
         assert abs(ag - ao) <= (1e-5 if precision == "fp32" else 5e-3), (code, ag, ao)
     # partition-wise over the training clusters, checked on every partition
     lg, ag, lpg, apg = gpu.eval_parts(2)
     lo, ao, lpo, apo = ora.eval_partitions(2, g["cluster_ids"], g["num_clusters"])
     ok = ~np.isnan(apo)
     assert np.max(np.abs(lpg[ok] - lpo[ok])) <= t * max(1.0, np.max(np.abs(lpo[ok])))
+
+
+# ---------------------------------------------------------------- per-node eval logits
+# gist_eval_logits returns the logits of exactly the forward gist_eval (mode 0) / gist_eval_parts
+# (mode 1) run, so the evaluation is checked element by element, not only through its means.
+def _trained_pair(arch, precision, dims=(29, 40, 24, 6), optimizer="adam"):
+    g = generate(tiny_spec(n=700, nnz=6000, d0=dims[0], classes=dims[-1], clusters=11), seed=2)
+    gpu, ora = make_pair(g, arch, dims, precision=precision, q=3, optimizer=optimizer)
+    gpu.partition(seed=3, m=2)
+    ora.partition(seed=3, m=2)
+    gpu.subtrain(2, lr=0.01)
+    ora.subtrain(2, lr=0.01)
+    gpu.aggregate()
+    ora.aggregate()
+    # the trained weights may differ slightly between the two (Adam sign steps):
+    # evaluate both at the GPU's global weights, so the eval forward alone is compared
+    ora.set_params([gpu.get_params(l).astype(np.float64) for l in range(len(dims) - 1)])
+    return g, gpu, ora
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage", "gat"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_eval_logits_full_graph_per_node(arch, precision):
+    from tests.gpu_helpers import rel_err
+    g, gpu, ora = _trained_pair(arch, precision)
+    got = gpu.eval_logits(0)
+    _, _, ref = ora.eval(2)
+    assert got.shape == ref.shape
+    assert rel_err(got, ref) <= TOL[precision], rel_err(got, ref)
+    # the loss / accuracy of gist_eval are those of these logits
+    lg, ag = gpu.eval(2)
+    rows = g["split"] == 2
+    z = got[rows].astype(np.float64)
+    ce = np.log(np.exp(z - z.max(1, keepdims=True)).sum(1)) + z.max(1) - z[np.arange(len(z)), g["labels"][rows]]
+    assert lg == pytest.approx(ce.mean(), rel=1e-5)
+    assert ag == pytest.approx(np.mean(np.argmax(got[rows], 1) == g["labels"][rows]), abs=1e-6)
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage", "gat"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_eval_logits_partitions_per_node(arch, precision):
+    from tests.gpu_helpers import rel_err
+    g, gpu, ora = _trained_pair(arch, precision)
+    n = len(g["labels"])
+    rng = np.random.default_rng(1)
+    part = (rng.integers(0, 22, n) + (rng.random(n) < 0.3) * (np.arange(n) % 3)) % 22
+    part[part >= 5] += 1                        # partition 5 empty
+    got = gpu.eval_logits(1, part, 23, max_rows=37)
+    ref = np.zeros((n, g["num_classes"]))
+    ora.eval_partitions(0, part, 23, logits_out=ref)
+    assert rel_err(got, ref) <= TOL[precision], rel_err(got, ref)
+    # per partition too: a wrong row inside one small partition cannot hide in the max
+    for p in range(23):
+        idx = np.nonzero(part == p)[0]
+        if len(idx):
+            assert rel_err(got[idx], ref[idx]) <= TOL[precision], p
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage", "gat"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_eval_scale_mean(arch, precision):
+    """R10 "mean": contractions over the partitioned hidden input dims scaled by
+    1/m in the evaluation forward -- per-node logits of the full-graph and the partition-wise
+    evaluation against the oracle's scaled forward (m = 3 of the last partition)."""
+    from paper_2102_10424_b200.gist import Gist
+    from tests.gpu_helpers import rel_err
+    g = generate(tiny_spec(n=600, nnz=5000, d0=21, classes=5, clusters=9), seed=3)
+    dims = (21, 36, 30, 5)
+    gpu = Gist(arch, dims, optimizer="sgd", precision=precision, clusters_per_batch=3, batch_seed=2,
+               eval_scale="mean")
+    gpu.load_graph(g)
+    gpu.init_params(5)
+    ora = O.OracleGIST(arch=arch, dims=list(dims), optimizer="sgd", clusters_per_batch=3, batch_seed=2)
+    ora.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], g["num_classes"], g["split"],
+                   g["cluster_ids"], g["num_clusters"])
+    gpu.partition(seed=4, m=3)
+    gpu.subtrain(2, lr=0.05)
+    gpu.aggregate()
+    ora.set_params([gpu.get_params(l).astype(np.float64) for l in range(len(dims) - 1)])
+    ora.m = 3
+    _, _, ref = ora.eval(2, eval_scale="mean")
+    _, _, unscaled = ora.eval(2)
+    assert rel_err(ref, unscaled) > 0.5                 # the scaling is visible
+    assert rel_err(gpu.eval_logits(0), ref) <= TOL[precision]
+    part = (np.arange(len(g["labels"])) * 5) % 7
+    pref = np.zeros_like(ref)
+    ora.eval_partitions(2, part, 7, logits_out=pref, eval_scale="mean")
+    assert rel_err(gpu.eval_logits(1, part, 7), pref) <= TOL[precision]

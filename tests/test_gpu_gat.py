@@ -8,14 +8,18 @@ import pytest
 
 from oracle import gist_oracle as O
 from synth.planted import GRAPHS, generate, tiny_spec
+from tests import bf16_twin
 from tests.gpu_helpers import align, make_pair, rel_err
 
 pytestmark = pytest.mark.gpu
 
-# BF16 gradients: 5e-2 (R21): the attention backward subtracts S_i = sum_j alpha_ij
-# dalpha_ij from every dalpha_ij, which amplifies the bf16 rounding of the GEMM operands
-# (H, W, dZ; u = 2^-8) by the cancellation; measured max 2.9e-2 on these cases
-TOL = {"fp32": (1e-4, 1e-3), "bf16": (2e-2, 5e-2)}
+# FP32: activations 1e-4, gradients 1e-3 against the FP64 oracle.  BF16: 2e-2 for both, with
+# the gradients gated against the bf16-operand twin (tests/bf16_twin.py: the FP64 GAT step with
+# bf16 rounding exactly where the CUDA path stores bf16), because against the FP64 oracle the
+# GAT gradient itself moves by up to 4e-2 once its forward operands are bf16 -- for any bf16
+# implementation (the floor is pinned on the CPU in tests/test_bf16_twin.py).
+# Against the FP64 oracle the GPU must then be no worse than that floor.
+TOL = {"fp32": (1e-4, 1e-3), "bf16": (2e-2, 2e-2)}
 CASES = [
     ("ragged", dict(n=700, nnz=6000, d0=29, classes=6, clusters=11), (29, 40, 24, 6), 3),
     ("wide", dict(n=900, nnz=16000, d0=130, classes=11, clusters=9), (130, 300, 11), 2),
@@ -64,6 +68,7 @@ def test_gat_one_step(name, kw, dims, q, precision):
     ora.partition(seed=99, m=m)
     gpu.subtrain(1, lr=0.01)
     for i in range(m):
+        w0 = [w.copy() for w in ora.sub[i]]   # the step's weights (train_step updates ora.sub)
         ora.train_step(i, 0, 0.01)
         tr = ora.last_trace[i]
         nodes = gpu.trace(i, 0)
@@ -72,12 +77,18 @@ def test_gat_one_step(name, kw, dims, q, precision):
         assert rel_err(gpu.trace(i, 2).reshape(nb, -1), tr["tape"]["logits"][p]) <= act_tol
         for l in range(1, len(dims) - 1):
             assert rel_err(gpu.trace(i, 1, l).reshape(nb, -1), tr["tape"]["H"][l][p]) <= act_tol, (l,)
+        if precision == "bf16":
+            S = ora.operator(*O.induced_subgraph(ora.row_ptr, ora.col_idx, tr["nodes"]), len(tr["nodes"]))
+            _, _, _, twin = bf16_twin.gat_step(w0, S, ora.X[tr["nodes"]], ora.labels[tr["nodes"]],
+                                               ora.split[tr["nodes"]] == 0)
         for l in range(len(dims) - 1):
-            gg = gpu.trace(i, 3, l).reshape(ora.sub[i][l].shape)
-            assert rel_err(gg, tr["grads"][l]) <= grad_tol, (i, l)
-            if precision == "fp32":   # (bf16: the attention rows are covered by the matrix gate above;
-                # their own entries are small differences of rounded products, R21)
-                assert rel_err(gg[-2:], tr["grads"][l][-2:]) <= grad_tol, ("attention rows", i, l)
+            gg = gpu.trace(i, 3, l).reshape(w0[l].shape)
+            ref = tr["grads"][l] if precision == "fp32" else twin[l]
+            assert rel_err(gg, ref) <= grad_tol, (i, l, rel_err(gg, ref))
+            assert rel_err(gg[-2:], ref[-2:]) <= grad_tol, ("attention rows", i, l, rel_err(gg[-2:], ref[-2:]))
+            if precision == "bf16":   # no worse than the bf16 floor against the FP64 oracle
+                floor = rel_err(twin[l], tr["grads"][l])
+                assert rel_err(gg, tr["grads"][l]) <= max(grad_tol, 1.25 * floor), (i, l, floor)
         assert abs(gpu.trace(i, 4)[0] - tr["loss"]) <= act_tol * max(1.0, tr["loss"])
 
 
@@ -133,6 +144,40 @@ def test_gat_adam_one_round():
         got = gpu.get_params(l)
         assert rel_err(got[:-1], ora.theta[l][:-1]) <= 1e-3, l
         assert np.max(np.abs(got[-1] - w0[l][-1])) <= zeta * lr * 1.001
+
+
+def test_gat_adam_a_dst_rows_entrywise():
+    """The a_dst rows under Adam, entry by entry (one step, m = 3).  Where the oracle's d a_dst is
+    non-zero the GPU gradient matches it (1e-3) and so does the Adam step (the same sign decides
+    it); where it is zero in exact arithmetic (every edge of the rows feeding it takes the same
+    LeakyReLU branch, so t_i cancels in the row softmax) the GPU gradient is rounding-level too
+    and the step stays within Adam's first-step bound lr."""
+    kw, dims, q = CASES[0][1], CASES[0][2], CASES[0][3]
+    g = graph(kw, seed=1)
+    gpu, ora = make_pair(g, "gat", dims, optimizer="adam", q=q)
+    lr, m = 0.01, 3
+    gpu.partition(seed=11, m=m)
+    ora.partition(seed=11, m=m)
+    before = [[gpu.get_sub_params(i, l)[-1].copy() for l in range(len(dims) - 1)] for i in range(m)]
+    gpu.subtrain(1, lr=lr)
+    nsig = 0
+    for i in range(m):
+        ora.train_step(i, 0, lr)
+        tr = ora.last_trace[i]
+        for l in range(len(dims) - 1):
+            go = tr["grads"][l]
+            scale = np.max(np.abs(go))
+            gg = gpu.trace(i, 3, l).reshape(go.shape)
+            sig = np.abs(go[-1]) > 1e-6 * scale
+            nsig += int(sig.sum())
+            assert np.max(np.abs(gg[-1][~sig]), initial=0.0) <= 1e-5 * scale, (i, l)
+            if sig.any():
+                assert rel_err(gg[-1][sig], go[-1][sig]) <= 1e-3, (i, l)
+            wg = gpu.get_sub_params(i, l)[-1]
+            if sig.any():
+                assert rel_err(wg[sig], ora.sub[i][l][-1][sig]) <= 1e-3, (i, l)
+            assert np.max(np.abs(wg[~sig] - before[i][l][~sig]), initial=0.0) <= lr * 1.001, (i, l)
+    assert nsig > 0
 
 
 def test_gat_bf16_loss_curve_10_rounds():

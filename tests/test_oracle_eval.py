@@ -142,3 +142,30 @@ def test_one_partition_is_full_graph_eval():
     l_full, a_full, _ = o.eval(0)
     l, a, lp, ap = o.eval_partitions(0, np.zeros(200, np.int64), 1)
     assert l == pytest.approx(l_full, rel=1e-12) and a == a_full and lp[0] == l and ap[0] == a
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage"])
+@pytest.mark.parametrize("L", [2, 3])
+def test_eval_scale_mean_closed_form(arch, L):
+    """R10 "mean" (the theory's 1/m output scaling): every contraction over a
+    partitioned (hidden) input dimension is scaled by 1/m.  ReLU is positively homogeneous, so
+    for GCN / GraphSAGE the scaled logits are the unscaled ones times m^-(L-1) exactly (each of
+    the L-1 layers after the first contributes one factor); m = 1 and "none" change nothing."""
+    g = generate(tiny_spec(n=150, nnz=900, d0=6, classes=3, clusters=3), seed=2)
+    dims = [6] + [8] * (L - 1) + [3]
+    o = O.OracleGIST(arch=arch, dims=dims)
+    o.load_graph(g["row_ptr"], g["col_idx"], g["X"], g["labels"], 3, g["split"], g["cluster_ids"], 3)
+    o.init_params(4)
+    _, _, base = o.eval(0)
+    o.partition(seed=1, m=4)
+    o.aggregate()                        # no training: Theta unchanged, m = 4 recorded
+    _, _, none = o.eval(0, eval_scale="none")
+    _, _, mean = o.eval(0, eval_scale="mean")
+    assert np.array_equal(none, base)
+    np.testing.assert_allclose(mean, base / 4.0 ** (L - 1), rtol=1e-12, atol=1e-14)
+    ref = np.zeros_like(base)
+    o.eval_partitions(0, np.zeros(150, np.int64), 1, logits_out=ref, eval_scale="mean")
+    np.testing.assert_allclose(ref, mean, rtol=1e-12, atol=1e-14)
+    o.partition(seed=2, m=1)
+    o.aggregate()
+    assert np.array_equal(o.eval(0, eval_scale="mean")[2], base)
