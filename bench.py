@@ -352,7 +352,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gist", choices=["gist", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(MODELS))
-    ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16"])
+    ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16", "tf32"])
     ap.add_argument("--zeta", type=int, default=0, help="local iterations per round (0 = paper's zeta, capped)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--agg", default="allgather", choices=["allgather", "p2p"],
@@ -530,6 +530,9 @@ def main():
             if args.precision == "bf16":
                 roof = {"bound": "tensor", "peak": pk["bf16_sustained"] or pk["bf16"], "unit": "TFLOP/s",
                         "peak_src": f"{pk['src']} bf16 sustained"}
+            elif args.precision == "tf32":   # a contraction takes its own dtype's peak: bf16 x 1/2 (nominal ratio)
+                roof = {"bound": "tensor", "peak": 0.5 * (pk["bf16_sustained"] or pk["bf16"]), "unit": "TFLOP/s",
+                        "peak_src": f"{pk['src']} bf16 sustained x nominal tf32/bf16 ratio 1.13/2.25"}
             else:
                 # FP32 SIMT: 148 SMs x 128 FP32 lanes x 2 flop x max SM clock
                 roof = {"bound": "alu", "peak": 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12, "unit": "TFLOP/s",
@@ -552,7 +555,8 @@ def main():
     line = {
         "metric": metric_for(spec), "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32", "bf16": "bf16"}[args.precision],
+        "data": "synthetic",
         "config": {"workload": spec.name, "graph": f"{spec.graph}-shaped planted-cluster synthetic "
                    f"(n={g['n']}, nnz={int(g['row_ptr'][-1])})", "arch": spec.arch, "dims": list(spec.dims),
                    "m": spec.m, "q": spec.q, "zeta": zeta, "step": "one GIST round (partition + zeta subTrain "
@@ -580,23 +584,28 @@ def main():
             d["predicted_speedup_vs_1gpu"] = d["predicted_box_steps_s"] / value
         if spec.graph == "reddit":
             line["kernel_targets"] = kernel_targets(G, g, pk)
-        if args.precision == "bf16":   # the paper's precision (PyTorch default FP32, R13): FP32 parity mode
-            z32 = min(zeta, 100)
-            c32 = make("fp32")
-            c32.load_graph(g)
-            c32.init_params(args.seed)
-            st32 = torch.cuda.ExternalStream(c32.stream())
-            one_round(c32, 0, z=z32)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st32)
-            for t in range(2):
-                one_round(c32, 1 + t, z=z32)
-            e1.record(st32)
-            torch.cuda.synchronize()
-            line["fp32"] = {"value": 2 * z32 * spec.m / (e0.elapsed_time(e1) / 1e3), "unit": "steps/s",
-                            "zeta": z32, "rounds": 2, "note": "FP32 parity mode (FP32 storage, SIMT FFMA GEMMs)"}
-            c32.close()
+        if args.precision == "bf16":
+            # the paper's precision (PyTorch's FP32 default, R13): FP32 parity mode (SIMT GEMMs) and
+            # TF32 mode (FP32 storage, tcgen05 kind::tf32 GEMMs), same workload, zeta capped at 100
+            notes = {"fp32": "FP32 parity mode (FP32 storage, SIMT FFMA GEMMs)",
+                     "tf32": "TF32 mode (FP32 storage, tcgen05 kind::tf32 GEMMs, fp32 accumulation)"}
+            for prec, note in notes.items():
+                z32 = min(zeta, 100)
+                c32 = make(prec)
+                c32.load_graph(g)
+                c32.init_params(args.seed)
+                st32 = torch.cuda.ExternalStream(c32.stream())
+                one_round(c32, 0, z=z32)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st32)
+                for t in range(2):
+                    one_round(c32, 1 + t, z=z32)
+                e1.record(st32)
+                torch.cuda.synchronize()
+                line[prec] = {"value": 2 * z32 * spec.m / (e0.elapsed_time(e1) / 1e3), "unit": "steps/s",
+                              "zeta": z32, "rounds": 2, "note": note}
+                c32.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, n, dt, cores = oracle_steps_per_s(spec, g, seconds=args.cpu_seconds, max_steps=64)
         line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",

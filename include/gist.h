@@ -58,7 +58,11 @@ typedef enum {
  * head, Theta_l = [W; a_src^T; a_dst^T] with logical rows d_l + 2, self loops added, ReLU hidden) */
 enum { GIST_ARCH_GCN = 0, GIST_ARCH_SAGE = 1, GIST_ARCH_GAT = 2 };
 enum { GIST_OPT_SGD = 0, GIST_OPT_ADAM = 1 };        /* subTrain = SGD step PAPER.md:168; Adam PAPER.md:660,680,690 */
-enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1 };     /* FP32 parity mode / BF16 tensor-core mode (R13) */
+/* R13 precision modes: FP32 parity (FP32 storage, FP32 SIMT GEMMs); BF16 (bf16 activations and GEMM
+ * operands on tcgen05, fp32 accumulation, fp32 master weights / gradients / optimizer state);
+ * TF32 (FP32 storage everywhere, the GEMMs on tcgen05 kind::tf32: operands rounded to tf32 by the
+ * tensor core, fp32 accumulation -- PyTorch's allow_tf32 matmul precision). */
+enum { GIST_PREC_FP32 = 0, GIST_PREC_BF16 = 1, GIST_PREC_TF32 = 2 };
 enum { GIST_GRAPH_DEVICE = 0 };                     /* the graph is resident in HBM (the only residency built) */
 /* Adam state across rounds: RESET = moments and step counter restart at every gist_partition
  * (R8; the default).  PERSISTENT = SURVEY.md §8 f3: global first / second moments
@@ -297,8 +301,8 @@ gist_status gist_spmm(const int64_t* row_ptr_dev, const int32_t* col_dev, int64_
 
 /* C[M x N] = op(A) op(B) (row-major, leading dims lda/ldb/ldc), fp32 or bf16 in,
  * fp32 or bf16 out, fp32 accumulation; trans flags per operand.  dtype 0 = fp32
- * SIMT path, 1 = bf16 tcgen05 path (out fp32 when out_f32 != 0).  relu != 0 applies
- * max(.,0) in the epilogue. */
+ * SIMT path, 1 = bf16 tcgen05 path (out fp32 when out_f32 != 0), 2 = tf32 tcgen05 path
+ * (fp32 in and out).  relu != 0 applies max(.,0) in the epilogue. */
 gist_status gist_gemm(int32_t transA, int32_t transB, int64_t M, int64_t N, int64_t K,
                       const void* A_dev, int64_t lda, const void* B_dev, int64_t ldb,
                       void* C_dev, int64_t ldc, int32_t dtype, int32_t out_f32, int32_t relu, void* stream);

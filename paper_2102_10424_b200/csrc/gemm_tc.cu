@@ -27,7 +27,7 @@ constexpr int BM = 128;
 // epilogue warps: two per TMEM lane quarter, each owning half of the tile's columns
 constexpr int kEpiWarps = 8;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
-constexpr int BK = 64;  // 64 bf16 = 128 bytes: one SWIZZLE_128B row
+constexpr int BK = 64;  // 64 bf16 = 128 bytes: one SWIZZLE_128B row (TF32: 32 fp32, the same 128 bytes)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -158,14 +158,16 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-// UMMA shared-memory descriptor: start, LBO, SBO in 16-byte units; version 1 (sm_100); SWIZZLE_128B.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor: start, LBO, SBO in 16-byte units; version 1 (sm_100); layout type
+// SWIZZLE_128B (2) or, for MN-major 32-bit (tf32) operands, SWIZZLE_128B_BASE32B (1): the only
+// shared-memory layout UMMA accepts for MN-major tf32 (32-byte swizzle atoms, 4-row K groups).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -175,6 +177,18 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// TF32 mode (R13): fp32 operands read as tf32 by the tensor cores, fp32 accumulation; K = 8 per MMA
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
@@ -559,9 +573,18 @@ __device__ __forceinline__ void zero_fill_tile(const Tile& T, int et) {
 // splitting the columns (TMEM -> registers ->
 // global), releasing the accumulator to the MMA warp, so the epilogue of tile i overlaps the
 // main loop of tile i+1 and the CTA set-up (barriers, TMEM allocation) is paid once per SM.
-template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+// TF: TF32 mode -- operands are fp32 (4 bytes): a 128-byte swizzle row holds BKE = 32 K elements,
+// an MN-major TMA box is 32 elements wide (4 per 128-row tile, 4 KB apart), one MMA covers K = 8
+// (+32 bytes K-major, +1 KB MN-major).  The ring, its byte counts and the epilogue are unchanged.
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob, bool TF = false>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_constant__ typename Prob::Group G) {
   using CF = Cfg<BN, ST>;
+  constexpr int BKE = TF ? 32 : BK;            // K elements per k-block (128 bytes)
+  constexpr int MNB = TF ? 32 : 64;            // MN elements per MN-major box (128 bytes)
+  constexpr uint32_t BOXB = (uint32_t)MNB * BKE * (TF ? 4 : 2);  // bytes per MN-major box
+  constexpr uint32_t KSTEP_MN = TF ? 1024u : 2048u;            // MN-major descriptor advance per MMA
+  // MN-major tf32: SWIZZLE_128B_BASE32B (layout 1, K groups of 4 rows = 512 B); bf16: SWIZZLE_128B
+  constexpr uint32_t MN_LAYOUT = TF ? 1u : 2u, MN_SBO = TF ? 512u : 1024u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int EPI = Prob::kTmaEpi ? CF::EPI_BYTES : 0;
@@ -607,7 +630,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const Tile T = Prob::decode(G, t, sdesc);
         if (!T.mma) continue;
-        const int nk = (T.K + BK - 1) / BK;
+        const int nk = (T.K + BKE - 1) / BKE;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % CF::STAGES;
           const uint32_t ph = (it / CF::STAGES) & 1u;
@@ -615,36 +638,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           uint8_t* sa = smem + s * CF::STAGE_BYTES;
           uint8_t* sb = sa + CF::A_BYTES;
           mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
-          const int k0 = kb * BK;
+          const int k0 = kb * BKE;
           if (T.stream_a) {  // last read of A for a while: evict first
             const uint64_t pol = policy_evict_first();
             if (!A_MN) {
               tma_load_2d_hint(sa, T.ma, &full[s], k0, T.a_row, pol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d_hint(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0, pol);
+              for (int j = 0; j < BM / MNB; ++j)
+                tma_load_2d_hint(sa + j * BOXB, T.ma, &full[s], T.a_row + MNB * j, k0, pol);
             }
           } else if (!A_MN) {
             tma_load_2d(sa, T.ma, &full[s], k0, T.a_row);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(sa + j * 8192, T.ma, &full[s], T.a_row + 64 * j, k0);
+            for (int j = 0; j < BM / MNB; ++j)
+              tma_load_2d(sa + j * BOXB, T.ma, &full[s], T.a_row + MNB * j, k0);
           }
           if (!B_MN) {
             tma_load_2d(sb, T.mb, &full[s], T.b_k0 + k0, T.b_col);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * 8192, T.mb, &full[s], T.b_col + 64 * j, T.b_k0 + k0);
+            for (int j = 0; j < BN / MNB; ++j)
+              tma_load_2d(sb + j * BOXB, T.mb, &full[s], T.b_col + MNB * j, T.b_k0 + k0);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
+      // c_format F32 (bit 4); a/b format BF16 = 1 or TF32 = 2 (bits 7-9, 10-12); majorness; N >> 3; M >> 4
+      constexpr uint32_t fmt = TF ? 2u : 1u;
+      constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((A_MN ? 1u : 0u) << 15) |
                                  ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       uint32_t it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -654,7 +679,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
         mbar_wait(&acce[b], aph ^ 1u);  // the epilogue has drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem + b * BN;
-        const int nk = (T.K + BK - 1) / BK;
+        const int nk = (T.K + BKE - 1) / BKE;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % CF::STAGES;
           const uint32_t ph = (it / CF::STAGES) & 1u;
@@ -663,11 +688,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
           const uint32_t sb = sa + CF::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 bytes per K16 inside the swizzled row; MN-major: +16 K-rows = 2048 bytes
-            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024) : make_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024) : make_desc(sb + k * 32, 16, 1024);
-            umma_bf16(dacc, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < 4; ++k) {
+            // K-major: +32 bytes per MMA (K16 bf16 / K8 tf32) inside the swizzled row; MN-major:
+            // +16 (bf16) / +8 (tf32) K-rows of 128 bytes; LBO = one MN box
+            const uint64_t ad = A_MN ? make_desc(sa + k * KSTEP_MN, BOXB, MN_SBO, MN_LAYOUT) : make_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * KSTEP_MN, BOXB, MN_SBO, MN_LAYOUT) : make_desc(sb + k * 32, 16, 1024);
+            if constexpr (TF) umma_tf32(dacc, ad, bd, idesc, (kb | k) != 0);
+            else umma_bf16(dacc, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
@@ -903,17 +930,19 @@ EncodeFn get_encode() {
   return fn;
 }
 
-// 2D bf16 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride ld elements
+// 2D bf16 (or fp32: TF32 mode) tensor map: inner dim `inner` (contiguous), outer dim `outer`, row
+// stride ld elements
 bool make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner,
-              int box_outer) {
+              int box_outer, bool f32 = false, bool mn32 = false) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (f32 ? 4 : 2))};
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  return enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             mn32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -932,9 +961,9 @@ bool make_store_map(CUtensorMap* map, void* base, int64_t inner, int64_t outer, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob>
+template <int BN, int ST, bool A_MN, bool B_MN, bool OUT_F32, class Prob, bool TF = false>
 void launch_persist(const typename Prob::Group& G, int total, cudaStream_t s) {
-  auto kern = k_gemm_persist<BN, ST, A_MN, B_MN, OUT_F32, Prob>;
+  auto kern = k_gemm_persist<BN, ST, A_MN, B_MN, OUT_F32, Prob, TF>;
   constexpr int SMEM = Cfg<BN, ST>::SMEM_BASE + (Prob::kTmaEpi ? Cfg<BN, ST>::EPI_BYTES : 0) + 64;
   ensure_smem((const void*)kern, SMEM);
   const int grid = total < num_sms() ? total : num_sms();
@@ -970,6 +999,11 @@ void launch_pair(const typename Prob::Group& G, int total2, cudaStream_t s) {
 
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
+  if (P.tf32) {  // TF32 mode: fp32 in, fp32 out, one CTA per tile
+    constexpr int ST = BN == 256 ? 4 : 6;
+    launch_persist<BN, ST, A_MN, B_MN, true, ProbPlain<BN>, true>(P.G, P.G.n * P.G.tm * P.G.tn, s);
+    return;
+  }
   if (P.pair) {
     const int total2 = P.G.n * ((P.G.tm + 1) / 2) * P.G.tn;
     if (P.out_f32) launch_pair<BN, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total2, s);
@@ -1000,9 +1034,14 @@ void launch_bd(const BdPlan& P, cudaStream_t s) {
 
 }  // namespace
 
-bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
+bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) { return gemm_tc_prepare(ops, n, P, false); }
+
+bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
   if (!get_encode() || n < 1 || n > kMaxGemmOps) return false;
   const GemmOp& o0 = ops[0];
+  P->tf32 = tf32;
+  if (tf32 && (!o0.out_f32 || o0.mask)) return false;  // TF32 mode: fp32 outputs, no bf16 epilogue operands
+  const int ebox = tf32 ? 32 : 64;  // elements per 128-byte TMA box row
   P->a_mn = o0.transA;     // A stored K x M
   P->b_mn = !o0.transB;    // B stored K x N
   P->out_f32 = o0.out_f32;
@@ -1037,17 +1076,19 @@ bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* P) {
     }
     static const int64_t kmin_pair = [] { const char* e = std::getenv("GIST_PAIR_KMIN"); return e ? atoll(e) : 2048; }();
     static const int64_t tiles_pair = [] { const char* e = std::getenv("GIST_PAIR_TILES"); return e ? atoll(e) : 4; }();
-    P->pair = tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
+    P->pair = !tf32 && tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
   }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
     const GemmOp& o = ops[i];
     if (o.transA != o0.transA || o.transB != o0.transB || o.out_f32 != o0.out_f32) return false;
     if (o.K <= 0 || ((uintptr_t)o.A & 15) || ((uintptr_t)o.B & 15) || (o.lda % 8) || (o.ldb % 8)) return false;
+    if (tf32 && (o.mbits || o.add || o.mbits_in || o.rscale)) return false;
     GemmSlotTC& S = P->G.s[i];
-    bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, 64, 64) : make_map(&S.ma, o.A, o.K, o.M, o.lda, 64, BM);
-    ok = ok && (P->b_mn ? make_map(&S.mb, o.B, o.N, o.K, o.ldb, 64, 64)
-                        : make_map(&S.mb, o.B, o.K, o.N, o.ldb, 64, P->pair ? P->bn / 2 : P->bn));
+    bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, ebox, ebox, tf32, tf32)
+                      : make_map(&S.ma, o.A, o.K, o.M, o.lda, ebox, BM, tf32);
+    ok = ok && (P->b_mn ? make_map(&S.mb, o.B, o.N, o.K, o.ldb, ebox, ebox, tf32, tf32)
+                        : make_map(&S.mb, o.B, o.K, o.N, o.ldb, ebox, P->pair ? P->bn / 2 : P->bn, tf32));
     if (!ok) return false;
     S.C = o.C;
     S.ldc = o.ldc;
@@ -1109,6 +1150,7 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.N = (int)o.N;
     S.tma_store = 0;  // ProbBd::kTmaEpi == false
     S.keep_out = o.keep_out;
+
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;
@@ -1137,6 +1179,17 @@ bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const 
   GemmPlanTC P;
   if (!gemm_bf16_prepare(&o, 1, &P)) return false;
   for (int r = 0; r < reps; ++r) gemm_bf16_launch(P, s);  // one plan (tensor maps encoded once)
+  return true;
+}
+
+bool gemm_tf32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+               int64_t ldb, float* C, int64_t ldc, bool relu, cudaStream_t s, int reps) {
+  if (!get_encode()) return false;
+  if (M == 0 || N == 0) return true;
+  GemmOp o{transA, transB, M, N, K, A, lda, B, ldb, C, ldc, true, relu, nullptr, 0, nullptr, 0};
+  GemmPlanTC P;
+  if (!gemm_tc_prepare(&o, 1, &P, true)) return false;
+  for (int r = 0; r < reps; ++r) gemm_bf16_launch(P, s);
   return true;
 }
 

@@ -437,7 +437,8 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   *out = nullptr;
   if (cfg->arch != GIST_ARCH_GCN && cfg->arch != GIST_ARCH_SAGE && cfg->arch != GIST_ARCH_GAT) return GIST_E_ARG;
   if (cfg->optimizer != GIST_OPT_SGD && cfg->optimizer != GIST_OPT_ADAM) return GIST_E_ARG;
-  if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16) return GIST_E_ARG;
+  if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16 && cfg->precision != GIST_PREC_TF32)
+    return GIST_E_ARG;
   if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
   if (cfg->agg_mode != GIST_AGG_ALLGATHER && cfg->agg_mode != GIST_AGG_P2P) return GIST_E_ARG;
   if (cfg->eval_scale != GIST_EVAL_SCALE_NONE && cfg->eval_scale != GIST_EVAL_SCALE_MEAN) return GIST_E_ARG;
@@ -1039,7 +1040,8 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   P.groups.clear();
   const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
   const bool sage = c->arch == GIST_ARCH_SAGE;
-  const bool tc = c->prec == GIST_PREC_BF16;
+  const bool tc = c->prec == GIST_PREC_BF16;  // BF16 tensor-core mode (bf16 operands and its fused features)
+  const bool tf = c->prec == GIST_PREC_TF32;  // TF32 mode: FP32 storage, step GEMMs on tcgen05 kind::tf32
   // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
   // L2-footprint / launch-count trade-off
   int gsz = kMaxGroup;
@@ -1108,9 +1110,10 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           g.dw_fl[l] += 2.0 * nb * sh.Np * sh.half;
           if (l > 0) g.dx_fl[l] += 2.0 * nb * sh.Np * sh.half;
         }
-        if (tc) {
-          if (!gemm_bf16_prepare(fw.data(), g.count, &g.fwd_tc[l]) || !gemm_bf16_prepare(dw.data(), g.count, &g.dw_tc[l]) ||
-              (l > 0 && !gemm_bf16_prepare(dx.data(), g.count, &g.dx_tc[l])))
+        if (tc || tf) {
+          if (!gemm_tc_prepare(fw.data(), g.count, &g.fwd_tc[l], tf) ||
+              !gemm_tc_prepare(dw.data(), g.count, &g.dw_tc[l], tf) ||
+              (l > 0 && !gemm_tc_prepare(dx.data(), g.count, &g.dx_tc[l], tf)))
             return fail(c, GIST_E_UNSUPPORTED, "GAT: tcgen05 GEMM plan failed");
         } else {
           for (int j = 0; j < g.count; ++j) {
@@ -1360,10 +1363,13 @@ static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
                                        &g.bwd_bd[l])))
           return fail(c, GIST_E_UNSUPPORTED, "block-diagonal aggregation plan failed");
       }
-      if (tc) {
-        if (!gemm_bf16_prepare(fw.data(), g.count, &g.fwd_tc[l]) ||
-            !gemm_bf16_prepare(dw.data(), g.count, &g.dw_tc[l]) ||
-            (l > 0 && !gemm_bf16_prepare(dx.data(), g.count, &g.dx_tc[l])))
+      if (tc || tf) {
+        if (tf)  // TF32 mode: every output of the step GEMMs is fp32 (the mode's element type)
+          for (auto* v : {&fw, &dw, &dx})
+            for (GemmOp& o : *v) o.out_f32 = true;
+        if (!gemm_tc_prepare(fw.data(), g.count, &g.fwd_tc[l], tf) ||
+            !gemm_tc_prepare(dw.data(), g.count, &g.dw_tc[l], tf) ||
+            (l > 0 && !gemm_tc_prepare(dx.data(), g.count, &g.dx_tc[l], tf)))
           return fail(c, GIST_E_UNSUPPORTED, "tcgen05 GEMM plan failed (alignment / driver entry point)");
       } else {
         for (int j = 0; j < g.count; ++j) {
@@ -1501,8 +1507,8 @@ extern "C" gist_status gist_get_partition(gist_ctx* c, int32_t dim, int32_t* uni
 template <typename T>
 static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp, double flops, cudaStream_t s) {
   const int id = prof_begin(c, s, GIST_PROF_GEMM, flops);
-  if (c->prec == GIST_PREC_BF16) gemm_bf16_launch(tcp, s);
-  else gemm_f32_group(fp, s);
+  if (c->prec == GIST_PREC_FP32) gemm_f32_group(fp, s);
+  else gemm_bf16_launch(tcp, s);  // BF16 or TF32 tcgen05 plan
   prof_end(c, s, id);
   ++c->nk;
 }
@@ -2023,6 +2029,9 @@ static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N,
                             cudaStream_t s) {
   if (c->prec == GIST_PREC_FP32) {
     gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s);
+  } else if (c->prec == GIST_PREC_TF32) {
+    if (!gemm_tf32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s))
+      return fail(c, GIST_E_UNSUPPORTED, "tf32 tensor-core GEMM unavailable for this shape");
   } else if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s)) {
     return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
   }
@@ -2644,6 +2653,10 @@ extern "C" gist_status gist_gemm_reps(int32_t transA, int32_t transB, int64_t M,
       gemm_f32(transA, transB, M, N, K, (const float*)A_dev, lda, (const float*)B_dev, ldb, (float*)C_dev, ldc, relu, s);
   } else if (dtype == 1) {
     if (!gemm_bf16(transA, transB, M, N, K, (const bf16*)A_dev, lda, (const bf16*)B_dev, ldb, C_dev, ldc, out_f32,
+                   relu, s, reps))
+      return GIST_E_UNSUPPORTED;
+  } else if (dtype == 2) {  // TF32 tensor cores: fp32 in, fp32 out
+    if (!gemm_tf32(transA, transB, M, N, K, (const float*)A_dev, lda, (const float*)B_dev, ldb, (float*)C_dev, ldc,
                    relu, s, reps))
       return GIST_E_UNSUPPORTED;
   } else {

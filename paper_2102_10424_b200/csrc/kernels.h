@@ -124,10 +124,13 @@ struct GemmPlanTC {
   GemmGroupTC G;
   bool a_mn = false, b_mn = false, out_f32 = false, relu = false, mask = false;
   bool pair = false;  // CTA-pair (cta_group::2) kernel
+  bool tf32 = false;  // TF32 mode: fp32 operands (kind::tf32), fp32 outputs
   int bn = 128;
   int64_t maxM = 0, maxN = 0;
 };
 bool gemm_bf16_prepare(const GemmOp* ops, int n, GemmPlanTC* plan);
+// tf32 = true: TF32 mode (R13) -- fp32 operands read as tf32, fp32 outputs, relu only
+bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* plan, bool tf32);
 void gemm_bf16_launch(const GemmPlanTC& plan, cudaStream_t s);
 
 // Block-diagonal cluster aggregation on tcgen05 (SAGE, Cluster mini-batches):
@@ -183,6 +186,8 @@ void gemm_f32_group(const SgemmGroup& g, cudaStream_t s);
 bool gemm_bf16(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const bf16* A, int64_t lda,
                const bf16* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu, cudaStream_t s,
                int reps = 1);
+bool gemm_tf32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, bool relu, cudaStream_t s, int reps = 1);
 
 // --------------------------------------------------------------------------
 // Graph load (relabel nodes so clusters are contiguous) and Cluster mini-batch

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libgist.so")
 GIST_ARCH_GCN, GIST_ARCH_SAGE, GIST_ARCH_GAT = 0, 1, 2
 ARCHS = {"gcn": GIST_ARCH_GCN, "sage": GIST_ARCH_SAGE, "gat": GIST_ARCH_GAT}
 GIST_OPT_SGD, GIST_OPT_ADAM = 0, 1
-GIST_PREC_FP32, GIST_PREC_BF16 = 0, 1
+GIST_PREC_FP32, GIST_PREC_BF16, GIST_PREC_TF32 = 0, 1, 2
 GIST_GRAPH_DEVICE = 0
 TRACE_NODES, TRACE_ACT, TRACE_LOGITS, TRACE_GRAD, TRACE_LOSS = range(5)
 (STAT_ROUND, STAT_STEP, STAT_SELF_LOOPS_DROPPED, STAT_LAST_NNZ_B, STAT_LAST_NB, STAT_KERNELS,
@@ -130,7 +130,7 @@ class Gist:
         cfg.dims = self._dims
         cfg.optimizer = GIST_OPT_ADAM if optimizer == "adam" else GIST_OPT_SGD
         cfg.beta1, cfg.beta2, cfg.eps = beta1, beta2, eps
-        cfg.precision = GIST_PREC_BF16 if precision == "bf16" else GIST_PREC_FP32
+        cfg.precision = {"fp32": GIST_PREC_FP32, "bf16": GIST_PREC_BF16, "tf32": GIST_PREC_TF32}[precision]
         cfg.clusters_per_batch = clusters_per_batch
         cfg.batch_seed = batch_seed
         cfg.rank, cfg.world_size, cfg.device = rank, world_size, device
