@@ -224,7 +224,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN, int ST = (BN == 256 ? 4 : 6)>
+template <int BN, int ST = (BN == 256 ? 4 : (BN == 64 ? 8 : 6))>
 struct Cfg {
   static constexpr int STAGES = ST;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
@@ -1000,17 +1000,17 @@ void launch_pair(const typename Prob::Group& G, int total2, cudaStream_t s) {
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmPlanTC& P, cudaStream_t s) {
   if (P.tf32) {  // TF32 mode: fp32 in, fp32 out, one CTA per tile
-    constexpr int ST = BN == 256 ? 4 : 6;
+    constexpr int ST = BN == 256 ? 4 : (BN == 64 ? 8 : 6);
     launch_persist<BN, ST, A_MN, B_MN, true, ProbPlain<BN>, true>(P.G, P.G.n * P.G.tm * P.G.tn, s);
     return;
   }
-  if (P.pair) {
+  if constexpr (BN >= 128) if (P.pair) {
     const int total2 = P.G.n * ((P.G.tm + 1) / 2) * P.G.tn;
     if (P.out_f32) launch_pair<BN, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total2, s);
     else launch_pair<BN, A_MN, B_MN, false, ProbPlain<BN>>(P.G, total2, s);
     return;
   }
-  constexpr int ST = BN == 256 ? 4 : 6;
+  constexpr int ST = BN == 256 ? 4 : (BN == 64 ? 8 : 6);
   const int total = P.G.n * P.G.tm * P.G.tn;
   if (P.out_f32) launch_persist<BN, ST, A_MN, B_MN, true, ProbPlain<BN>>(P.G, total, s);
   else launch_persist<BN, ST, A_MN, B_MN, false, ProbPlain<BN>>(P.G, total, s);
@@ -1064,6 +1064,10 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
       for (int i = 0; i < n; ++i) t256 += cdiv(ops[i].M, BM) * cdiv(ops[i].N, 256);
       if (t256 < (int64_t)num_sms()) P->bn = 128;
     }
+    // ... and 64-wide ones when even 128-wide tiles fill less than half of the SMs (a single
+    // sub-GCN's dW GEMMs: 1,024 x 512 outputs = 32 tiles of 128 x 128 for a K = 3,106 reduction).
+    // Per-element K order is independent of the tile width: the same bits for any choice.
+    if (P->bn == 128 && n == 1 && cdiv(ops[0].M, BM) * cdiv(ops[0].N, 128) < (int64_t)num_sms() / 2) P->bn = 64;
   }
   // CTA pairs for large, long-K GEMMs (>= 4 tiles per SM and K >= 2048: measured 82 -> 88% of
   // peak at width 4096); short-K GEMMs (the C3 step's dX, K = 512: 27 -> 41 us as pairs) and
@@ -1076,7 +1080,7 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
     }
     static const int64_t kmin_pair = [] { const char* e = std::getenv("GIST_PAIR_KMIN"); return e ? atoll(e) : 2048; }();
     static const int64_t tiles_pair = [] { const char* e = std::getenv("GIST_PAIR_TILES"); return e ? atoll(e) : 4; }();
-    P->pair = !tf32 && tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
+    P->pair = !tf32 && P->bn >= 128 && tiles >= tiles_pair * (int64_t)num_sms() && kmin >= kmin_pair;
   }
   P->G.n = n;
   for (int i = 0; i < n; ++i) {
@@ -1105,7 +1109,8 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
     S.ldmbi = o.ldmbi;
     S.keep_out = o.keep_out;
     S.stream_a = o.stream_a;
-    S.tma_store = make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
+    // 64-wide bf16 tiles: an epilogue warp owns 32 columns, half of a 128-byte store box -> direct stores
+    S.tma_store = !(P->bn == 64 && !o.out_f32) && make_store_map(&S.mc, o.C, o.N, o.M, o.ldc, o.out_f32) ? 1 : 0;
     S.M = (int)o.M;
     S.N = (int)o.N;
     S.K = (int)o.K;
@@ -1120,6 +1125,7 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
 void gemm_bf16_launch(const GemmPlanTC& P, cudaStream_t s) {
   if (P.G.n <= 0 || P.maxM <= 0 || P.maxN <= 0) return;
   if (P.bn == 256) dispatch_layout<256>(P, s);
+  else if (P.bn == 64) dispatch_layout<64>(P, s);
   else dispatch_layout<128>(P, s);
 }
 

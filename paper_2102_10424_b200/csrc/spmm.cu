@@ -39,7 +39,7 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
 }
 
 template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE, bool PRED = false>
-__global__ void __launch_bounds__(256, PRED ? 3 : (J == 1 && sizeof(TI) == 2) ? 4
+__global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && sizeof(TI) == 2) ? 4
                                            : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
   pdl_wait();
@@ -215,6 +215,16 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     const bool wide = G.a[0].h_index != nullptr;
     if (wide) launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, true, true>, grid, 256, 0, s, G, nchunks);
     else launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, false, true>, grid, 256, 0, s, G, nchunks);
+    return;
+  }
+  if (G.a[0].few_nnz && J <= 3 && !G.a[0].colscale && rows * G.n <= 16384) {
+    // few neighbours per row and a small launch (one sub-GCN per GPU: ~3,100 rows, a third of the
+    // warp slots): the GPU has warps to spare, so each row keeps several gathers in flight (its
+    // degree tail sets the launch length)
+    constexpr int UF = J == 1 ? 8 : (J == 2 ? 4 : 2);
+    const bool wide = G.a[0].h_index != nullptr;
+    if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, true, true>, grid, 256, 0, s, G, nchunks);
+    else launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, false, true>, grid, 256, 0, s, G, nchunks);
     return;
   }
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
