@@ -355,8 +355,9 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["fp32", "bf16", "tf32"])
     ap.add_argument("--zeta", type=int, default=0, help="local iterations per round (0 = paper's zeta, capped)")
     ap.add_argument("--lr", type=float, default=0.01)
-    ap.add_argument("--agg", default="allgather", choices=["allgather", "p2p"],
-                    help="subAgg transport (gist_config.agg_mode; p2p = SURVEY §8 f2 peer stores)")
+    ap.add_argument("--agg", default="allgather", choices=["allgather", "p2p", "symm"],
+                    help="subAgg transport (gist_config.agg_mode; p2p / symm = SURVEY §8 f2 peer stores over CUDA IPC /"
+                         " the NCCL device API)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--profile-stride", type=int, default=32,
                     help="every N-th step of the extra profiled round is timed per kernel class (0: no profile)")

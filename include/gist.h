@@ -81,7 +81,14 @@ enum { GIST_OPT_STATE_RESET = 0, GIST_OPT_STATE_PERSISTENT = 1 };
  * write; no rank reads it before every peer's stores completed).  No receive buffer, no
  * second pass over the gathered bytes.  Not available for GAT (R21 averages the m copies
  * of the attention rows, which needs every copy on every rank): GIST_E_UNSUPPORTED. */
-enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1 };
+/* SYMM (SURVEY.md §8 f2 with the NCCL device API): Theta (+ f3 moments) in an ncclMemAlloc region
+ * registered as an NCCL symmetric window (ncclCommWindowRegister, NCCL_WIN_COLL_SYMMETRIC) with a
+ * device communicator (ncclDevCommCreate; NVLS multicast requested at W > 1).  gist_aggregate has
+ * each owner's kernel store its slots' blocks into every LSA peer's replica through
+ * ncclGetLsaPointer -- or, with multicast, one multimem.st per element that NVSwitch delivers to
+ * every replica -- between the same two barriers as P2P.  World 1 uses a one-rank communicator.
+ * Not available with the loopback transport or for GAT (GIST_E_UNSUPPORTED). */
+enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1, GIST_AGG_SYMM = 2 };
 /* Output scaling of the evaluation forward (R10; the theory scales the global
  * model's output by 1/m so that the expected sub-GCN output equals the global one).  NONE
  * (default): Eq. (1) as written.  MEAN: every contraction over a partitioned input dimension

@@ -14,6 +14,7 @@
 
 #include <cub/cub.cuh>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include "../../include/gist.h"
 #include "comm.h"
@@ -188,6 +189,11 @@ struct gist_ctx {
   // agg_mode P2P (f2): Theta (+ f3 moments) in one cudaMalloc region; peer_base[r] = rank r's
   // region (opened from its IPC handle; peer_base[rank] = p2p_base); one-word barrier buffer
   char* p2p_base = nullptr;
+  // agg_mode SYMM (f2): the same region from ncclMemAlloc, registered as an NCCL symmetric window,
+  // with a device communicator (LSA team; NVLS multicast when available) for the device-API stores
+  ncclWindow_t win = nullptr;
+  ncclDevComm* devcomm = nullptr;  // host copy, passed by value to the scatter kernel
+  bool symm_mm = false;             // the device communicator has an NVLS multimem object
   std::vector<char*> peer_base;
   float* barrier_word = nullptr;
   int alloc_m = 0;
@@ -440,7 +446,11 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   if (cfg->precision != GIST_PREC_FP32 && cfg->precision != GIST_PREC_BF16 && cfg->precision != GIST_PREC_TF32)
     return GIST_E_ARG;
   if (cfg->opt_state != GIST_OPT_STATE_RESET && cfg->opt_state != GIST_OPT_STATE_PERSISTENT) return GIST_E_ARG;
-  if (cfg->agg_mode != GIST_AGG_ALLGATHER && cfg->agg_mode != GIST_AGG_P2P) return GIST_E_ARG;
+  if (cfg->agg_mode != GIST_AGG_ALLGATHER && cfg->agg_mode != GIST_AGG_P2P && cfg->agg_mode != GIST_AGG_SYMM)
+    return GIST_E_ARG;
+  // SYMM: NCCL symmetric windows need an NCCL communicator (not the loopback test transport); R21's
+  // mean of the GAT attention rows needs every copy on every rank
+  if (cfg->agg_mode == GIST_AGG_SYMM && (cfg->loopback || cfg->arch == GIST_ARCH_GAT)) return GIST_E_UNSUPPORTED;
   if (cfg->eval_scale != GIST_EVAL_SCALE_NONE && cfg->eval_scale != GIST_EVAL_SCALE_MEAN) return GIST_E_ARG;
   if (cfg->agg_mode == GIST_AGG_P2P && (cfg->arch == GIST_ARCH_GAT || cfg->world_size > kMaxPeers))
     return GIST_E_UNSUPPORTED;  // R21 needs every copy of the attention rows; PeerDst holds 8 ranks
@@ -488,6 +498,11 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_dw_join, cudaEventDisableTiming) != cudaSuccess)
       return bail(GIST_E_CUDA);
   }
+  if (cfg->world_size == 1 && cfg->agg_mode == GIST_AGG_SYMM) {  // a one-rank communicator owns the window
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess || ncclCommInitRank(&c->comm.nccl, 1, id, 0) != ncclSuccess)
+      return bail(GIST_E_NCCL);
+  }
   if (cfg->world_size > 1) {
     if (cfg->loopback) {  // tests: W contexts of one process stand in for W ranks (comm.h)
       if (loopback_join(cfg->loopback, cfg->rank, cfg->world_size) != GIST_OK) return bail(GIST_E_ARG);
@@ -527,7 +542,15 @@ extern "C" void gist_destroy(gist_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (size_t r = 0; r < c->peer_base.size(); ++r)
     if (c->peer_base[r] && c->peer_base[r] != c->p2p_base && !c->comm.lb) cudaIpcCloseMemHandle(c->peer_base[r]);
-  if (c->p2p_base) cudaFree(c->p2p_base);
+  if (c->devcomm) {
+    ncclDevCommDestroy(c->comm.nccl, c->devcomm);
+    delete c->devcomm;
+  }
+  if (c->win) ncclCommWindowDeregister(c->comm.nccl, c->win);
+  if (c->p2p_base) {
+    if (c->cfg.agg_mode == GIST_AGG_SYMM) ncclMemFree(c->p2p_base);
+    else cudaFree(c->p2p_base);
+  }
   if (c->comm.nccl) ncclCommDestroy(c->comm.nccl);
   if (c->comm.lb) loopback_leave(c->comm.lb, c->comm.rank);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
@@ -584,8 +607,24 @@ static gist_status p2p_setup(gist_ctx* c) {
     off[l] = floats;
     floats += (size_t)pad8(kphys(c, c->dims[l])) * pad8(c->dims[l + 1]);  // 32-byte aligned layers
   }
-  const size_t bytes = floats * 4 * parts;
-  if (cudaMalloc(reinterpret_cast<void**>(&c->p2p_base), bytes) != cudaSuccess) {
+  const bool symm = c->cfg.agg_mode == GIST_AGG_SYMM;
+  const size_t bytes = symm ? cdiv(floats * 4 * parts, NCCL_WIN_REQUIRED_ALIGNMENT) * NCCL_WIN_REQUIRED_ALIGNMENT
+                            : floats * 4 * parts;
+  if (symm) {
+    // SYMM: ncclMemAlloc + a collective window registration (identical offsets on every rank) and a
+    // device communicator; NVLS multicast is requested at W > 1 and dropped if unavailable
+    NK(ncclMemAlloc(reinterpret_cast<void**>(&c->p2p_base), bytes));
+    NK(ncclCommWindowRegister(c->comm.nccl, c->p2p_base, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC));
+    c->devcomm = new ncclDevComm();
+    ncclDevCommRequirements req;
+    std::memset(&req, 0, sizeof(req));
+    req.lsaMultimem = W > 1;
+    if (ncclDevCommCreate(c->comm.nccl, &req, c->devcomm) != ncclSuccess) {
+      req.lsaMultimem = false;
+      NK(ncclDevCommCreate(c->comm.nccl, &req, c->devcomm));
+    }
+    c->symm_mm = req.lsaMultimem;
+  } else if (cudaMalloc(reinterpret_cast<void**>(&c->p2p_base), bytes) != cudaSuccess) {
     cudaGetLastError();
     c->p2p_base = nullptr;
     return fail(c, GIST_E_OOM, "p2p: cudaMalloc of the Theta region failed");
@@ -600,7 +639,7 @@ static gist_status p2p_setup(gist_ctx* c) {
   CK(cudaMemsetAsync(c->barrier_word, 0, 4, c->stream));
   c->peer_base.assign(W, nullptr);
   c->peer_base[c->cfg.rank] = c->p2p_base;
-  if (W == 1) return GIST_OK;
+  if (W == 1 || symm) return GIST_OK;  // SYMM: the device API maps the peers
   if (c->comm.lb) {  // loopback ranks share one process: the peers' regions are plain pointers
     std::vector<void*> all;
     gist_status st = comm_exchange_ptr(c->comm, c->p2p_base, all, &c->err);
@@ -805,7 +844,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   c->theta.assign(c->L, nullptr);
   c->th_K.assign(c->L, 0);
   c->th_N.assign(c->L, 0);
-  if (c->cfg.agg_mode == GIST_AGG_P2P) TRY(p2p_setup(c));
+  if (c->cfg.agg_mode == GIST_AGG_P2P || c->cfg.agg_mode == GIST_AGG_SYMM) TRY(p2p_setup(c));
   for (int l = 0; l < c->L; ++l) {
     c->th_K[l] = kphys(c, c->dims[l]);
     c->th_N[l] = pad8(c->dims[l + 1]);
@@ -1962,9 +2001,14 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
           mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = 0; mp.half = sh.half;
           mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
           mp.ldg = c->th_N[l];
+          const size_t off = (size_t)(reinterpret_cast<char*>((*pt.global)[l]) - c->p2p_base);
+          if (c->cfg.agg_mode == GIST_AGG_SYMM) {  // NCCL device API: LSA peer pointers / NVLS multimem
+            PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 4.0 * (2.0 + W), s,
+               scatter_sub_symm(*c->devcomm, c->win, off, mp, w + sh.off, c->symm_mm, s));
+            continue;
+          }
           PeerDst pd;
           pd.n = W;
-          const size_t off = (size_t)(reinterpret_cast<char*>((*pt.global)[l]) - c->p2p_base);
           for (int r = 0; r < W; ++r) pd.dst[r] = reinterpret_cast<float*>(c->peer_base[r] + off);
           PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 4.0 * (2.0 + W), s, scatter_sub_peers(pd, mp, w + sh.off, s));
         }

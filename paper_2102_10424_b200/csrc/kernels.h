@@ -342,6 +342,15 @@ struct PeerDst {
   int n = 0;
 };
 void scatter_sub_peers(const PeerDst& d, const LayerMap& m, const float* w_sub, cudaStream_t s);
+}  // namespace gist
+#include <nccl.h>
+#include <nccl_device/core.h>
+namespace gist {
+// agg_mode SYMM (f2): stores through the NCCL device API into every LSA peer's replica (or one
+// multimem.st per element when the window has an NVLS multicast object); `base` = byte offset of
+// the layer inside the registered window
+void scatter_sub_symm(const ncclDevComm& dc, ncclWindow_t win, size_t base, const LayerMap& m, const float* w_sub,
+                      bool multimem, cudaStream_t s);
 void glorot_init(float* theta, int rows_logical, int cols, int sage, int d_l, int glob_half, int64_t ldg,
                  uint32_t layer, uint64_t seed, float scale, cudaStream_t s);
 

@@ -6,6 +6,8 @@
 // key with the unit index as value), block i = pi[b_i, b_{i+1}) where the first
 // d mod m blocks hold ceil(d/m) units, each block re-sorted ascending.
 #include <cub/cub.cuh>
+#include <nccl.h>
+#include <nccl_device.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -139,6 +141,36 @@ void scatter_sub_peers(const PeerDst& d, const LayerMap& m, const float* w_sub, 
   for (int p0 = 0; p0 < m.Kp; p0 += 65535) {
     const int rows = m.Kp - p0 < 65535 ? m.Kp - p0 : 65535;
     k_scatter_peers<<<grid_for(m, rows), 256, 0, s>>>(d, m, w_sub, p0);
+  }
+}
+
+// subAgg through an NCCL symmetric window (agg_mode SYMM): Theta lives in an
+// ncclMemAlloc region registered as a symmetric window; the owner of a slot reads each element of its
+// block once and stores it into every LSA peer's replica through the device API (ncclGetLsaPointer:
+// peer replicas mapped into this process by NCCL), or -- when the communicator has an NVLS
+// multicast object (lsaMultimem) -- with one multimem.st that the NVSwitch fans out to every replica.
+__global__ void k_scatter_symm(const ncclDevComm dc, ncclWindow_t win, size_t base, const LayerMap m,
+                               const float* __restrict__ w, int p0, int mm) {
+  const int p = p0 + blockIdx.y;
+  const int64_t gr = glob_row(m, p);
+  if (gr < 0) return;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m.ncols; q += gridDim.x * blockDim.x) {
+    const float v = w[(int64_t)p * m.Np + q];
+    const size_t off = base + (size_t)(gr * m.ldg + (m.cols ? m.cols[q] : q)) * sizeof(float);
+    if (mm) {
+      float* mp = static_cast<float*>(ncclGetLsaMultimemPointer(win, off, dc));
+      asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mp), "f"(v) : "memory");
+    } else {
+      for (int r = 0; r < dc.lsaSize; ++r) *static_cast<float*>(ncclGetLsaPointer(win, off, r)) = v;
+    }
+  }
+  __threadfence_system();
+}
+void scatter_sub_symm(const ncclDevComm& dc, ncclWindow_t win, size_t base, const LayerMap& m, const float* w_sub,
+                      bool multimem, cudaStream_t s) {
+  for (int p0 = 0; p0 < m.Kp; p0 += 65535) {
+    const int rows = m.Kp - p0 < 65535 ? m.Kp - p0 : 65535;
+    k_scatter_symm<<<grid_for(m, rows), 256, 0, s>>>(dc, win, base, m, w_sub, p0, multimem ? 1 : 0);
   }
 }
 

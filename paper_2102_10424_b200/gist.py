@@ -35,7 +35,7 @@ PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregat
 
 
 GIST_OPT_STATE_RESET, GIST_OPT_STATE_PERSISTENT = 0, 1
-GIST_AGG_ALLGATHER, GIST_AGG_P2P = 0, 1
+GIST_AGG_ALLGATHER, GIST_AGG_P2P, GIST_AGG_SYMM = 0, 1, 2
 
 
 class GistConfig(C.Structure):
@@ -140,7 +140,7 @@ class Gist:
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         cfg.stream = stream
         cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
-        cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P}[agg_mode]
+        cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P, "symm": GIST_AGG_SYMM}[agg_mode]
         cfg.eval_scale = {"none": 0, "mean": 1}[eval_scale]
         self._lb = loopback  # keeps the group alive while this context exists
         cfg.loopback = loopback.h if loopback is not None else None

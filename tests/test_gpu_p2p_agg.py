@@ -58,3 +58,32 @@ def test_p2p_rejects_gat():
     from paper_2102_10424_b200.gist import Gist, GistError
     with pytest.raises(GistError, match="UNSUPPORTED"):
         Gist("gat", (16, 8, 4), agg_mode="p2p")
+
+
+@pytest.mark.parametrize("case,m,precision,opt_state", [
+    (1, 2, "fp32", "reset"),
+    (0, 3, "fp32", "persistent"),
+    (3, 4, "bf16", "reset"),
+])
+def test_symm_window_aggregate_bit_identical_to_allgather(case, m, precision, opt_state):
+    """agg_mode SYMM (SURVEY §8 f2 with the NCCL device API): Theta in an ncclMemAlloc region
+    registered as a symmetric window, a device communicator, and the owners' stores through
+    ncclGetLsaPointer.  World 1 (one-rank communicator): bit-identical Theta to the all-gather."""
+    _, kw, arch, dims, q = CASES[case]
+    g = generate(tiny_spec(**kw), seed=4)
+    ref, lref = _run(arch, dims, m, q, g, "allgather", precision, opt_state)
+    got, lgot = _run(arch, dims, m, q, g, "symm", precision, opt_state)
+    for t in range(len(ref)):
+        np.testing.assert_array_equal(np.asarray(lgot[t]), np.asarray(lref[t]), err_msg=f"round {t} losses")
+        for l in range(len(ref[t])):
+            np.testing.assert_array_equal(got[t][l], ref[t][l], err_msg=f"round {t} layer {l}")
+
+
+def test_symm_refusals():
+    from paper_2102_10424_b200.gist import Gist, GistError, Loopback
+    with pytest.raises(GistError, match="UNSUPPORTED"):
+        Gist("gat", (16, 8, 4), agg_mode="symm")
+    lb = Loopback(2)
+    with pytest.raises(GistError, match="UNSUPPORTED"):
+        Gist("gcn", (16, 8, 4), agg_mode="symm", rank=0, world_size=2, loopback=lb)
+    lb.close()
