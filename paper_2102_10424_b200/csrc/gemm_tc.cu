@@ -1053,7 +1053,9 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
     maxN = ops[i].N > maxN ? ops[i].N : maxN;
     maxM = ops[i].M > maxM ? ops[i].M : maxM;
   }
-  P->bn = maxN > 128 ? 256 : 128;  // persistent kernel: wide tiles amortise the epilogue
+  // persistent kernel: wide tiles amortise the epilogue; class-width outputs (the re-associated
+  // last layer, N = 48) take 64-wide tiles instead of wasting 5/8 of a 128-wide MMA
+  P->bn = maxN > 128 ? 256 : (maxN > 64 ? 128 : 64);
   // A single-op launch (one slot per lockstep group: one sub-GCN per GPU at W = m) whose
   // 256-wide tiles leave SMs idle takes 128-wide ones: single-slot C3 groups 2,806 -> 2,863
   // steps/s; measured slower for 2-op (4,627 -> 4,564) and 8-op (8,46x -> 8,364) launches, so
