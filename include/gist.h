@@ -228,6 +228,16 @@ gist_status gist_eval_logits(gist_ctx* ctx, int32_t mode, const int32_t* part_id
 gist_status gist_get_params(gist_ctx* ctx, int32_t layer, float* out);
 gist_status gist_set_params(gist_ctx* ctx, int32_t layer, const float* in);
 
+/* Model checkpoint file (SPEC.md "External Interfaces"): little-endian binary -- magic "GIST",
+ * version u32 (= 1), arch u8 (GIST_ARCH_*), L u32, dims u32[L+1], then every global Theta_l in
+ * the logical row-major layout of gist_get_params as f32.  Deterministic bytes for a given model.
+ * save: needs parameters and no open round (GIST_E_STATE); I/O failure GIST_E_ARG.
+ * load: after gist_load_graph and outside a round; the header must match this context's arch and
+ * dims (GIST_E_SHAPE), else GIST_E_ARG for a malformed / short file; the context then holds those
+ * parameters (PARAMS, like gist_set_params of every layer). */
+gist_status gist_save_checkpoint(gist_ctx* ctx, const char* path);
+gist_status gist_load_checkpoint(gist_ctx* ctx, const char* path);
+
 /* Partition of dim `dim` for the current round: units[d_dim] = blocks D^(0..m-1)
  * concatenated (each ascending), offs[m+1] block offsets.  Valid after partition. */
 gist_status gist_get_partition(gist_ctx* ctx, int32_t dim, int32_t* units, int32_t* offs);

@@ -1,399 +1,18 @@
-// gist_api.cu -- the C ABI (include/gist.h): context, state machine, the GIST
-// round structure of Algorithm 1 and the subTrain step
-// orchestration.  Every arithmetic step runs in the kernels of kernels.h; this
-// file only sequences launches, owns device memory and streams, and computes
-// the (tiny, integer) per-step batch schedule on the host (R7).
-#include <algorithm>
-#include <mutex>
-#include <cstdlib>
-#include <cmath>
-#include <cstring>
-#include <numeric>
-#include <string>
-#include <vector>
-
-#include <cub/cub.cuh>
-#include <nccl.h>
-#include <nccl_device.h>
-
-#include "../../include/gist.h"
-#include "comm.h"
-#include "common.cuh"
-#include "kernels.h"
+// gist_api.cu -- the C ABI (include/gist.h): context lifecycle, graph load, parameters,
+// inspection hooks, live profiling and the kernel-level entry points.  The GIST round lives in
+// round.cu (subGCNs / subAgg), plan.cu + step.cu (subTrain) and eval.cu (evaluation); every
+// arithmetic step runs in the kernels of kernels.h.
+#include "ctx.h"
 
 using namespace gist;
-
-struct gist_ctx;
-static bool persistent_adam(const gist_ctx* c);
-static void drop_graphs(gist_ctx* c);
+using namespace gist_impl;
 
 bool gist::pdl_enabled() {
   static const bool on = [] { const char* e = std::getenv("GIST_PDL"); return !(e && e[0] == '0'); }();
   return on;
 }
 
-namespace {
-
-enum State { S_CREATED = 0, S_GRAPH = 1, S_PARAMS = 2, S_PARTITIONED = 3 };
-
-struct LayerShape {
-  int nrows = 0, ncols = 0;  // logical rows (self block for SAGE) / cols of the sub block
-  int Kp = 0, Np = 0;        // physical (padded) shape
-  int half = 0;              // SAGE: physical offset of neighbour rows
-  int64_t off = 0;           // float offset in the packed slot buffer
-  int32_t* rows = nullptr;   // device unit list (nullptr = identity)
-  int32_t* cols = nullptr;
-};
-
-struct Slot {
-  int index = 0;  // global slot id i
-  // views into the rank's contiguous [slots_per_rank x S_max] buffers (Wall / Gall / Mall / Vall / Wball)
-  float *W = nullptr, *G = nullptr, *M = nullptr, *V = nullptr;
-  bf16* Wb = nullptr;
-  // batch schedule (device + pinned host mirror), capacity `cap` steps
-  int cap = 0;
-  int32_t *desc_dev = nullptr, *desc_host = nullptr;
-  std::vector<int> nb_of_step, q_of_step;
-  std::vector<int64_t> vol_of_step;
-  int cached_epoch = -1;
-  std::vector<int32_t> epoch_perm;
-  // batch buffers (nb_max rows)
-  int32_t *b_nodes = nullptr, *lab_b = nullptr, *b_col = nullptr;
-  uint64_t* map64 = nullptr;  // cluster -> (step tag, local-id delta)
-  uint8_t* train_b = nullptr;
-  float* scale = nullptr;
-  int64_t *b_beg = nullptr, *b_end = nullptr, *stats = nullptr;
-  // activations (element type T of the precision mode)
-  std::vector<void*> C, H, dZ;
-  std::vector<uint32_t*> mb;  // BF16: bit-packed ReLU masks of C_l / H_l (l >= 1), words [nb_max x mb_ld[l]]
-  void* dC = nullptr;
-  float* logits = nullptr;
-  float *row_loss = nullptr, *step_loss = nullptr, *loss_acc = nullptr;
-  uint32_t* ce_done = nullptr;  // softmax-CE last-CTA counter
-  // re-associated last layer (BF16 GraphSAGE): P = H W_bot, AGG = N P, DQ = [dZ | Q = N^T dZ],
-  // DZs = dZ / deg (block-diagonal path)
-  void *rP = nullptr, *rAGG = nullptr, *rDQ = nullptr, *rDZs = nullptr;
-  void* rWc = nullptr;  // [W_top | W_bot] of the last layer, half x 2Np bf16 (refreshed every step)
-  // GAT (R21): Z_l = H_l W_l per layer, per-row scalars [s | t | lse | S | dt | ds] (6 x nb_max),
-  // and the backward operand G (dlogits, then dH_l of each layer)
-  std::vector<void*> gZ;
-  std::vector<float*> gsc;
-  void* gG = nullptr;
-  int last_nb = 0;
-};
-
-// Launch plan of one subTrain step for a group of <= kMaxGroup local slots run in lockstep:
-// argument blocks of every grouped launch, built once per partition (TMA descriptors encoded once).
-template <typename T>
-struct StepPlan {
-  struct Group {
-    int first = 0, count = 0;
-    BatchGroup batch;
-    std::vector<SpmmGroup<T, T>> fwd_spmm, bwd_spmm;  // per layer (bwd index l produces dZ_{l-1})
-    std::vector<GemmPlanTC> fwd_tc, dw_tc, dx_tc;     // BF16 mode
-    std::vector<SgemmGroup> fwd_f, dw_f, dx_f;        // FP32 mode
-    std::vector<double> fwd_fl, dw_fl, dx_fl;         // algorithmic FLOPs (profiling)
-    std::vector<double> fwd_by, bwd_by;               // SpMM compulsory bytes excl. nnz part (profiling)
-    std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
-    std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
-    CeGroup<T> ce;
-    // re-associated last layer: Z = H W_top + N (H W_bot); backward via Q = N^T dZ
-    bool reassoc = false;
-    GemmPlanTC ra_p, ra_z, ra_dw, ra_dh;
-    RelayoutGroup ra_wc;
-    BdPlan ra_fbd, ra_bbd;
-    SpmmGroup<T, T> ra_fsp, ra_bsp;
-    SpmmGroup<T, float> ra_fsp_f;  // GCN: logits = A_hat P straight into the fp32 logits
-    double ra_gemm_fl = 0.0, ra_bd_fl = 0.0, ra_fby = 0.0, ra_bby = 0.0;
-  };
-  std::vector<Group> groups;
-};
-
-}  // namespace
-
-struct gist_ctx {
-  gist_config cfg{};
-  std::vector<int> dims;
-  int L = 0, arch = 0, prec = 0;
-  cudaStream_t stream = nullptr;
-  // dW stream (default; GIST_DW_STREAM=0 disables): the backward dW GEMMs (and, with one
-  // lockstep group, the per-layer optimizer steps) run on a side stream, overlapping the rest
-  // of the backward chain (dX -> aggregation); joined at the end of the step
-  cudaStream_t dws = nullptr;
-  // the side stream for this step: dws, except in profiled steps (every prof_stride-th), which
-  // run serialised so that the per-kernel event times of the live roofline are not inflated by
-  // overlap (ncu's launch list is serialised too)
-  cudaStream_t side_now = nullptr;
-  cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr;
-  // this step's batches were built on the dW stream, overlapping the previous step's optimizer
-  bool batch_prefetched = false;
-  int cur_z = 0;  // host index of the step being enqueued (schedule bookkeeping / profiling only)
-  // CUDA graphs of one step, per variant [build * 2 + prefetch] (dropped at every plan rebuild)
-  struct StepGraph {
-    cudaGraphExec_t exec = nullptr;
-    int64_t nk = 0;  // kernels per replay
-  };
-  StepGraph graphs[4];
-  bool own_stream = false;
-  int state = S_CREATED;
-  gist_status sticky = GIST_OK;
-  std::string err;
-  Comm comm;  // NCCL communicator or loopback group (world > 1)
-  cudaEvent_t fork_ev = nullptr;
-  // graph (relabelled: clusters contiguous)
-  int64_t n = 0, nnz = 0;
-  int c = 0, k = 0;
-  int64_t self_loops = 0;
-  int64_t *rp = nullptr, *cstart = nullptr;
-  int32_t *col = nullptr, *cid = nullptr, *labels = nullptr;
-  int32_t* ccol = nullptr;  // cluster of every edge's neighbour (batch build), or packed codes (pack_ob > 0)
-  int pack_ob = 0;          // offset bits of the packed edge codes (0: plain cluster ids)
-  uint8_t* split = nullptr;
-  void* X = nullptr;  // n x pad8(d0), T
-  float* full_scale = nullptr;
-  std::vector<int32_t> perm_h;  // new id -> original id
-  std::vector<int64_t> cstart_h, cvol_h;  // cluster offsets (new ids) / cluster volumes (sum of degrees)
-  int nb_max = 0, max_csize = 0;
-  int64_t nnzb_max = 0;
-  // block-diagonal tensor-core aggregation (SAGE, BF16): binary intra-cluster blocks
-  bf16* blocks = nullptr;
-  int bs = 0;
-  bool bd = false;
-  double block_density = 0.0;
-  // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
-  std::vector<float*> theta;
-  std::vector<int64_t> th_K, th_N;
-  // partition of the current round
-  int m = 0;
-  std::vector<uint8_t> layer_set;              // set_params: layers written since load (PARAMS once all are)
-  std::vector<int32_t*> units;                 // per dim (hidden dims only)
-  std::vector<std::vector<int32_t>> offs;      // per dim, m+1
-  std::vector<std::vector<LayerShape>> shapes;  // [slot][layer] for all m slots
-  int64_t S_max = 0;                           // floats per packed slot buffer
-  int slots_per_rank = 0;
-  std::vector<Slot> slots;                     // local slots
-  float* Wall = nullptr;                       // slots_per_rank * S_max (local slot weights, contiguous)
-  float *Gall = nullptr, *Mall = nullptr, *Vall = nullptr;  // same packing: gradients, Adam moments
-  std::vector<float*> theta_m, theta_v;  // GIST_OPT_STATE_PERSISTENT: global Adam moments (Theta layout)
-  bf16* Wball = nullptr;                       // bf16 shadow of Wall (BF16 mode)
-  int nb_max_rows = 0;                         // static row count of every batch launch
-  std::vector<int64_t> mb_ld;                  // words per row of Slot::mb[l]
-  bool reassoc = false;                        // last SAGE layer re-associated (BF16, L >= 2)
-  StepState* dstate = nullptr;                 // device step state (z, t, lr)
-  StepState* hstate = nullptr;                 // pinned host staging for it
-  int32_t* bctr = nullptr;                     // per-group batch-build counters (BatchGroup::ctr), 2 per slot
-  cudaEvent_t hstate_ev = nullptr;
-  StepPlan<float> plan_f;
-  StepPlan<bf16> plan_b;
-  float* Wrecv = nullptr;                      // world * slots_per_rank * S_max (world > 1, ALLGATHER)
-  // agg_mode P2P (f2): Theta (+ f3 moments) in one cudaMalloc region; peer_base[r] = rank r's
-  // region (opened from its IPC handle; peer_base[rank] = p2p_base); one-word barrier buffer
-  char* p2p_base = nullptr;
-  // agg_mode SYMM (f2): the same region from ncclMemAlloc, registered as an NCCL symmetric window,
-  // with a device communicator (LSA team; NVLS multicast when available) for the device-API stores
-  ncclWindow_t win = nullptr;
-  ncclDevComm* devcomm = nullptr;  // host copy, passed by value to the scatter kernel
-  bool symm_mm = false;             // the device communicator has an NVLS multimem object
-  std::vector<char*> peer_base;
-  float* barrier_word = nullptr;
-  int alloc_m = 0;
-  void* sort_tmp = nullptr;
-  size_t sort_tmp_bytes = 0;
-  uint64_t *keys_a = nullptr, *keys_b = nullptr;
-  int32_t *idx_a = nullptr, *idx_b = nullptr, *blk = nullptr, *offs_dev = nullptr;
-  int64_t round = 0, step = 0, adam_t = 0;
-  int64_t nk = 0, h2d = 0, d2h = 0;
-  std::vector<void*> allocs;
-  // live profiling (gist_profile): event pairs around launches of sampled steps
-  struct ProfRec {
-    int cls;
-    double work, per_nnz;
-    int nnz_slot;  // index into nnz_pin (-1: none)
-    cudaEvent_t a, b;
-  };
-  int prof_stride = 0;
-  bool prof_now = false;
-  std::vector<ProfRec> prof_pending;
-  std::vector<cudaEvent_t> ev_pool;
-  int64_t* nnz_pin = nullptr;
-  int nnz_pin_cap = 0, nnz_pin_used = 0;
-  double prof_ms[GIST_PROF_N] = {0}, prof_work[GIST_PROF_N] = {0};
-  int64_t prof_n[GIST_PROF_N] = {0};
-};
-
-// ============================================================== helpers ====
-namespace {
-
-gist_status fail(gist_ctx* c, gist_status s, const std::string& msg) {
-  if (c) {
-    c->err = msg;
-    if (s == GIST_E_CUDA || s == GIST_E_NCCL) c->sticky = s;
-  }
-  return s;
-}
-
-// a collective's status: sticky on CUDA / NCCL failures (the message is already in c->err)
-gist_status coll(gist_ctx* c, gist_status st) {
-  if (st == GIST_E_CUDA || st == GIST_E_NCCL) c->sticky = st;
-  return st;
-}
-
-#define CK(x)                                                                              \
-  do {                                                                                     \
-    cudaError_t e_ = (x);                                                                  \
-    if (e_ != cudaSuccess)                                                                 \
-      return fail(c, e_ == cudaErrorMemoryAllocation ? GIST_E_OOM : GIST_E_CUDA,           \
-                  std::string(#x) + ": " + cudaGetErrorString(e_));                        \
-  } while (0)
-#define NK(x)                                                                              \
-  do {                                                                                     \
-    ncclResult_t r_ = (x);                                                                 \
-    if (r_ != ncclSuccess) return fail(c, GIST_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
-#define TRY(x)                        \
-  do {                                \
-    gist_status s_ = (x);             \
-    if (s_ != GIST_OK) return s_;     \
-  } while (0)
-#define PRE(c)                                                        \
-  do {                                                                \
-    if (!(c)) return GIST_E_ARG;                                      \
-    if ((c)->sticky != GIST_OK) return (c)->sticky;                   \
-    cudaSetDevice((c)->cfg.device);                                   \
-  } while (0)
-// profiled launch: PL(class, algorithmic work, stream, launch-expression)
-#define PL(cls, work, st, expr)                     \
-  do {                                              \
-    int id_ = prof_begin(c, (st), (cls), (work));   \
-    expr;                                           \
-    prof_end(c, (st), id_);                         \
-    ++c->nk;                                        \
-  } while (0)
-// launch bookkeeping: every kernel launch of the library goes through LK or PL
-#define LK(expr)  \
-  do {            \
-    expr;         \
-    ++c->nk;      \
-  } while (0)
-
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync on the context
-// stream), which keeps up to 16 GB reserved after frees: a second context in the same process
-// (e.g. bench.py's e2e run after its device-timed run) reuses it instead of paying cudaMalloc /
-// page mapping again.  Allocation happens at load / partition time only, never in the step.
-static void configure_pool() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = 16ull << 30;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-  });
-}
-gist_status dalloc(gist_ctx* c, void** p, size_t bytes) {
-  *p = nullptr;
-  if (bytes == 0) bytes = 16;
-  configure_pool();
-  cudaError_t e = cudaMallocAsync(p, bytes, c->stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(c, GIST_E_OOM, "cudaMalloc(" + std::to_string(bytes) + " bytes) failed: " + cudaGetErrorString(e));
-  }
-  c->allocs.push_back(*p);
-  return GIST_OK;
-}
-template <typename P>
-gist_status dalloc_t(gist_ctx* c, P** p, size_t count) {
-  return dalloc(c, reinterpret_cast<void**>(p), count * sizeof(P));
-}
-void dfree(gist_ctx* c, void* p) {
-  if (!p) return;
-  auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
-  if (it != c->allocs.end()) c->allocs.erase(it);
-  cudaFreeAsync(p, c->stream);
-}
-
-gist_status check_launch(gist_ctx* c, const char* where) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(c, GIST_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
-  return GIST_OK;
-}
-
-size_t esize(const gist_ctx* c) { return c->prec == GIST_PREC_BF16 ? 2 : 4; }
-
-cudaEvent_t pool_event(gist_ctx* c) {
-  if (!c->ev_pool.empty()) {
-    cudaEvent_t e = c->ev_pool.back();
-    c->ev_pool.pop_back();
-    return e;
-  }
-  cudaEvent_t e;
-  cudaEventCreate(&e);
-  return e;
-}
-// opens a profiled launch on stream s (only while c->prof_now)
-int prof_begin(gist_ctx* c, cudaStream_t s, int cls, double work, double per_nnz = 0.0, int nnz_slot = -1) {
-  if (!c->prof_now) return -1;
-  gist_ctx::ProfRec r{cls, work, per_nnz, nnz_slot, pool_event(c), pool_event(c)};
-  cudaEventRecord(r.a, s);
-  c->prof_pending.push_back(r);
-  return (int)c->prof_pending.size() - 1;
-}
-void prof_end(gist_ctx* c, cudaStream_t s, int id) {
-  if (id >= 0) cudaEventRecord(c->prof_pending[id].b, s);
-}
-// synchronises and folds pending records into the per-class totals
-void prof_flush(gist_ctx* c) {
-  if (c->prof_pending.empty()) return;
-  cudaDeviceSynchronize();
-  for (auto& r : c->prof_pending) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, r.a, r.b);
-    double w = r.work;
-    if (r.nnz_slot >= 0) w += r.per_nnz * (double)c->nnz_pin[r.nnz_slot];
-    c->prof_ms[r.cls] += ms;
-    c->prof_work[r.cls] += w;
-    c->prof_n[r.cls] += 1;
-    c->ev_pool.push_back(r.a);
-    c->ev_pool.push_back(r.b);
-  }
-  c->prof_pending.clear();
-  c->nnz_pin_used = 0;
-}
-
-int hidden_block_max(const gist_ctx* c, int l, int m) {
-  return (c->dims[l] + m - 1) / m;  // ceil: the largest balanced block (R5)
-}
-
-// logical shape of the sub-weight of slot i, layer l (R6)
-void sub_logical(const gist_ctx* c, int i, int l, int* nrows, int* ncols) {
-  auto bsize = [&](int dim) {
-    if (dim == 0 || dim == c->L) return c->dims[dim];
-    return c->offs[dim][i + 1] - c->offs[dim][i];
-  };
-  *nrows = bsize(l);
-  *ncols = bsize(l + 1);
-}
-
-// Host side of R7: cluster permutation of slot i in epoch e; batch p = perm[pq : (p+1)q)
-void epoch_perm(const gist_ctx* c, int slot, int64_t e, std::vector<int32_t>& out) {
-  std::vector<std::pair<uint64_t, int32_t>> kv(c->c);
-  for (int j = 0; j < c->c; ++j)
-    kv[j] = {philox_key64((uint32_t)j, (uint32_t)e, (uint32_t)slot, PURPOSE_BATCH, c->cfg.batch_seed), j};
-  std::sort(kv.begin(), kv.end());
-  out.resize(c->c);
-  for (int j = 0; j < c->c; ++j) out[j] = kv[j].second;
-}
-
-}  // namespace
-
 // ============================================================ lifecycle ====
-static bool persistent_adam(const gist_ctx* c) {
-  return c->cfg.optimizer == GIST_OPT_ADAM && c->cfg.opt_state == GIST_OPT_STATE_PERSISTENT;
-}
 
 extern "C" void gist_config_default(gist_config* cfg) {
   std::memset(cfg, 0, sizeof(*cfg));
@@ -517,21 +136,6 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   return GIST_OK;
 }
 
-// Logical rows of Theta_l for input width d (GCN d, GraphSAGE 2d (R2), GAT d + 2 (R21)) and the
-// physical rows (second block at pad8(d): SAGE neighbour rows, GAT the two attention rows)
-static int wrows(const gist_ctx* c, int d) {
-  return c->arch == GIST_ARCH_SAGE ? 2 * d : (c->arch == GIST_ARCH_GAT ? d + 2 : d);
-}
-static int64_t kphys(const gist_ctx* c, int64_t d) {
-  return c->arch == GIST_ARCH_SAGE ? 2 * pad8(d) : (c->arch == GIST_ARCH_GAT ? pad8(d) + 8 : pad8(d));
-}
-static bool two_blocks(const gist_ctx* c) { return c->arch != GIST_ARCH_GCN; }
-
-static void free_slots(gist_ctx* c) {
-  for (auto& s : c->slots)
-    if (s.desc_host) cudaFreeHost(s.desc_host);
-  c->slots.clear();
-}
 
 extern "C" void gist_destroy(gist_ctx* c) {
   if (!c) return;
@@ -671,6 +275,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
                                        int64_t nnz, const float* X, const int32_t* labels, int32_t num_classes,
                                        const uint8_t* split, const int32_t* cluster_ids, int32_t num_clusters) {
   PRE(c);
+  Range nvtx_range("gist_load_graph");
   if (c->state != S_CREATED) return fail(c, GIST_E_STATE, "load_graph: graph already loaded");
   if (n < 1 || n > INT32_MAX - 1 || !row_ptr || (!col_idx && nnz > 0) || !X || !labels || !split || !cluster_ids)
     return fail(c, GIST_E_ARG, "load_graph: null pointer or bad n");
@@ -864,6 +469,7 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
 // ============================================================= params =====
 extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
   PRE(c);
+  Range nvtx_range("gist_init_params");
   if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "init_params: bad state");
   for (int l = 0; l < (int)c->theta_m.size(); ++l) {  // f3: moments restart with the parameters
     CK(cudaMemsetAsync(c->theta_m[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, c->stream));
@@ -925,1600 +531,75 @@ extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* 
   return GIST_OK;
 }
 
-// ============================================================ partition ===
-static gist_status alloc_slots(gist_ctx* c, int m) {
-  free_slots(c);
-  for (void* p : {(void*)c->Wall, (void*)c->Gall, (void*)c->Mall, (void*)c->Vall, (void*)c->Wball, (void*)c->Wrecv})
-    dfree(c, p);
-  c->Wall = c->Gall = c->Mall = c->Vall = c->Wrecv = nullptr;
-  c->Wball = nullptr;
-  const int W = c->cfg.world_size, r = c->cfg.rank;
-  c->slots_per_rank = gist_slots_per_rank(m, W);
-  // largest packed slot (every hidden block at ceil(d/m))
-  int64_t smax = 0;
-  std::vector<int> maxK(c->L), maxN(c->L);
-  for (int l = 0; l < c->L; ++l) {
-    const int nr = (l == 0) ? c->dims[0] : hidden_block_max(c, l, m);
-    const int nc = (l + 1 == c->L) ? c->dims[c->L] : hidden_block_max(c, l + 1, m);
-    maxK[l] = (int)kphys(c, nr);
-    maxN[l] = (int)pad8(nc);
-    smax += (int64_t)maxK[l] * maxN[l];
-  }
-  c->S_max = smax;
-  const size_t tot = (size_t)c->slots_per_rank * smax;
-  TRY(dalloc_t(c, &c->Wall, tot));
-  TRY(dalloc_t(c, &c->Gall, tot));
-  CK(cudaMemsetAsync(c->Wall, 0, tot * 4, c->stream));
-  CK(cudaMemsetAsync(c->Gall, 0, tot * 4, c->stream));
-  if (c->cfg.optimizer == GIST_OPT_ADAM) {
-    TRY(dalloc_t(c, &c->Mall, tot));
-    TRY(dalloc_t(c, &c->Vall, tot));
-  }
-  if (c->prec == GIST_PREC_BF16) {
-    TRY(dalloc_t(c, &c->Wball, tot));
-    CK(cudaMemsetAsync(c->Wball, 0, tot * 2, c->stream));
-  }
-  if (W > 1 && c->cfg.agg_mode == GIST_AGG_ALLGATHER) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
-  if (c->bctr) dfree(c, c->bctr);
-  TRY(dalloc_t(c, &c->bctr, 2 * (size_t)std::max(c->slots_per_rank, 1)));
-  if (!c->dstate) {
-    TRY(dalloc_t(c, &c->dstate, 1));
-    CK(cudaMallocHost(&c->hstate, sizeof(StepState)));
-    CK(cudaEventCreateWithFlags(&c->hstate_ev, cudaEventDisableTiming));
-  }
-  const int nbm = std::max(c->nb_max, 1);
-  c->nb_max_rows = nbm;
-  const size_t E = esize(c);
-  int maxKall = 0;
-  for (int l = 0; l < c->L; ++l) maxKall = std::max(maxKall, maxK[l]);
-  for (int i = r, j = 0; i < m; i += W, ++j) {
-    c->slots.emplace_back();
-    Slot& s = c->slots.back();
-    s.index = i;
-    s.W = c->Wall + (size_t)j * smax;
-    s.G = c->Gall + (size_t)j * smax;
-    if (c->Mall) s.M = c->Mall + (size_t)j * smax, s.V = c->Vall + (size_t)j * smax;
-    if (c->Wball) s.Wb = c->Wball + (size_t)j * smax;
-    TRY(dalloc_t(c, &s.b_nodes, nbm));
-    TRY(dalloc_t(c, &s.lab_b, nbm));
-    TRY(dalloc_t(c, &s.train_b, nbm));
-    TRY(dalloc_t(c, &s.scale, nbm));
-    TRY(dalloc_t(c, &s.b_beg, nbm));
-    TRY(dalloc_t(c, &s.b_end, nbm));
-    TRY(dalloc_t(c, &s.stats, 4));  // [0] nnz_b, [1] train rows, [2] batch-build row counter
-    TRY(dalloc_t(c, &s.b_col, std::max<int64_t>(c->nnzb_max, 1)));
-    TRY(dalloc_t(c, &s.map64, c->c));
-    CK(cudaMemsetAsync(s.map64, 0, (size_t)c->c * 8, c->stream));  // tag 0 = never in a batch
-    s.C.assign(c->L, nullptr);
-    s.H.assign(c->L, nullptr);
-    s.dZ.assign(c->L, nullptr);
-    s.mb.assign(c->L, nullptr);
-    c->mb_ld.assign(c->L, 0);
-    for (int l = 1; l < c->L && c->prec == GIST_PREC_BF16; ++l) {
-      c->mb_ld[l] = cdiv(maxK[l], 32);
-      TRY(dalloc_t(c, &s.mb[l], (size_t)nbm * c->mb_ld[l]));
-      CK(cudaMemsetAsync(s.mb[l], 0, (size_t)nbm * c->mb_ld[l] * 4, c->stream));
-    }
-    for (int l = 0; l < c->L; ++l) {  // zero-initialised: padding columns must read as 0
-      TRY(dalloc(c, &s.C[l], (size_t)nbm * maxK[l] * E));
-      CK(cudaMemsetAsync(s.C[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
-      if (c->arch == GIST_ARCH_GCN && l > 0) {
-        TRY(dalloc(c, &s.H[l], (size_t)nbm * maxK[l] * E));
-        CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * maxK[l] * E, c->stream));
-      }
-      if (c->arch == GIST_ARCH_GAT) {  // H_l (layer 0: the gathered X_b rows), Z_l, scalars
-        const size_t kw = (size_t)(maxK[l] - 8);  // pad8 of the widest input slice
-        TRY(dalloc(c, &s.H[l], (size_t)nbm * kw * E));
-        CK(cudaMemsetAsync(s.H[l], 0, (size_t)nbm * kw * E, c->stream));
-        s.gZ.resize(c->L, nullptr);
-        s.gsc.resize(c->L, nullptr);
-        TRY(dalloc(c, &s.gZ[l], (size_t)nbm * maxN[l] * E));
-        CK(cudaMemsetAsync(s.gZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
-        TRY(dalloc_t(c, &s.gsc[l], (size_t)6 * nbm + 2 * kw + (size_t)2 * kGatDaChunks * maxN[l]));
-      }
-      TRY(dalloc(c, &s.dZ[l], (size_t)nbm * maxN[l] * E));
-      CK(cudaMemsetAsync(s.dZ[l], 0, (size_t)nbm * maxN[l] * E, c->stream));
-    }
-    // (only where it pays: the last layer's input slice is >= 256 wide; measured neutral to
-    // slightly negative on the Cora-shaped C1 with a 128-wide slice)
-    // GIST_REASSOC=1 / 0 forces it on / off (tests exercise both on small shapes)
-    const int last_in = c->arch == GIST_ARCH_SAGE ? maxK[c->L - 1] / 2 : maxK[c->L - 1];
-    c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && last_in >= 256;
-    if (const char* e = std::getenv("GIST_REASSOC")) c->reassoc = c->prec == GIST_PREC_BF16 && c->L >= 2 && e[0] == '1';
-    if (c->arch == GIST_ARCH_GAT) c->reassoc = false;
-    if (c->reassoc) {
-      const size_t npl = (size_t)maxN[c->L - 1];
-      TRY(dalloc(c, &s.rP, (size_t)nbm * npl * E));
-      TRY(dalloc(c, &s.rAGG, (size_t)nbm * npl * E));
-      TRY(dalloc(c, &s.rDQ, (size_t)nbm * 2 * npl * E));
-      TRY(dalloc(c, &s.rDZs, (size_t)nbm * 2 * npl * E));
-      TRY(dalloc(c, &s.rWc, (size_t)maxK[c->L - 1] * npl * E));
-      CK(cudaMemsetAsync(s.rP, 0, (size_t)nbm * npl * E, c->stream));
-      CK(cudaMemsetAsync(s.rAGG, 0, (size_t)nbm * npl * E, c->stream));
-      CK(cudaMemsetAsync(s.rDQ, 0, (size_t)nbm * 2 * npl * E, c->stream));
-      CK(cudaMemsetAsync(s.rDZs, 0, (size_t)nbm * 2 * npl * E, c->stream));
-    }
-    if (c->arch == GIST_ARCH_GAT) {
-      int gw = 0;
-      for (int l = 0; l < c->L; ++l) gw = std::max(gw, maxN[l]);
-      TRY(dalloc(c, &s.gG, (size_t)nbm * gw * E));  // dlogits, then dH of each layer
-      CK(cudaMemsetAsync(s.gG, 0, (size_t)nbm * gw * E, c->stream));
-    }
-    TRY(dalloc(c, &s.dC, (size_t)nbm * maxKall * E));
-    CK(cudaMemsetAsync(s.dC, 0, (size_t)nbm * maxKall * E, c->stream));
-    TRY(dalloc_t(c, &s.logits, (size_t)nbm * maxN[c->L - 1]));
-    CK(cudaMemsetAsync(s.logits, 0, (size_t)nbm * maxN[c->L - 1] * 4, c->stream));
-    TRY(dalloc_t(c, &s.row_loss, nbm));
-    TRY(dalloc_t(c, &s.ce_done, 1));
-    CK(cudaMemsetAsync(s.ce_done, 0, 4, c->stream));
-    TRY(dalloc_t(c, &s.step_loss, 1));
-    TRY(dalloc_t(c, &s.loss_acc, 1));
-  }
-  c->alloc_m = m;
-  return GIST_OK;
-}
-
-// compulsory bytes of one SpMM launch excluding the nnz-proportional part
-template <typename T>
-static double spmm_bytes(const SpmmArgs<T, T>& a) {
-  const double rw = (double)a.rows * (double)a.w * sizeof(T);
-  double b = (double)a.rows * 16 + rw /*H*/ + rw /*out*/;
-  if (a.add) b += rw;
-  if (a.mask) b += rw;
-  if (a.self_out) b += rw;
-  if (a.rowscale) b += a.rows * 4.0;
-  if (a.colscale) b += a.rows * 4.0;
-  if (a.h_index) b += a.rows * 4.0;
-  return b;
-}
-
-// Builds the launch plan of one subTrain step (every grouped launch's argument block).
-template <typename T>
-static gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
-  drop_graphs(c);  // the captured steps hold the previous plan's argument blocks
-  P.groups.clear();
-  const int L = c->L, nb = c->nb_max_rows, q = c->cfg.clusters_per_batch;
-  const bool sage = c->arch == GIST_ARCH_SAGE;
-  const bool tc = c->prec == GIST_PREC_BF16;  // BF16 tensor-core mode (bf16 operands and its fused features)
-  const bool tf = c->prec == GIST_PREC_TF32;  // TF32 mode: FP32 storage, step GEMMs on tcgen05 kind::tf32
-  // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
-  // L2-footprint / launch-count trade-off
-  int gsz = kMaxGroup;
-  if (const char* e = std::getenv("GIST_GROUP")) gsz = std::max(1, std::min(kMaxGroup, atoi(e)));
-  for (int g0 = 0; g0 < (int)c->slots.size(); g0 += gsz) {
-    typename StepPlan<T>::Group g;
-    g.first = g0;
-    g.count = std::min<int>(gsz, (int)c->slots.size() - g0);
-    g.batch.n = g.count;
-    g.batch.q = q;
-    g.batch.nb_max = nb;
-    g.batch.ctr = c->bctr + 2 * g0;
-    g.fwd_spmm.assign(L, SpmmGroup<T, T>());
-    g.bwd_spmm.assign(L, SpmmGroup<T, T>());
-    g.fwd_tc.assign(L, GemmPlanTC());
-    g.dw_tc.assign(L, GemmPlanTC());
-    g.dx_tc.assign(L, GemmPlanTC());
-    g.fwd_f.assign(L, SgemmGroup());
-    g.dw_f.assign(L, SgemmGroup());
-    g.dx_f.assign(L, SgemmGroup());
-    g.fwd_fl.assign(L, 0.0);
-    g.dw_fl.assign(L, 0.0);
-    g.dx_fl.assign(L, 0.0);
-    g.fwd_by.assign(L, 0.0);
-    g.bwd_by.assign(L, 0.0);
-    g.fwd_bd.assign(L, BdPlan());
-    g.bwd_bd.assign(L, BdPlan());
-    g.bd_fl.assign(L, 0.0);
-    const bool bd = c->bd && tc && sage;
-    if (bd) {  // the batch build copies the layer-0 self half [X_b | .] (no self_out in the sparse pass)
-      g.batch.X = (const bf16*)c->X;
-      g.batch.ldx = pad8(c->dims[0]);
-      g.batch.ldxd = c->shapes[c->slots[g0].index][0].Kp;
-    }
-    g.ce.n = g.count;
-    g.ce.rows = nb;
-    g.ce.k = c->k;
-    g.ce.ld = c->shapes[c->slots[g0].index][L - 1].Np;
-    g.reassoc = c->reassoc && tc && L >= 2;
-    if (c->arch == GIST_ARCH_GAT) {  // R21: batch build and loss are grouped; the layers run per slot
-      for (int j = 0; j < g.count; ++j) {
-        Slot& sl = c->slots[g0 + j];
-        BatchSlot& b = g.batch.s[j];
-        b.desc = sl.desc_dev; b.map64 = sl.map64; b.b_nodes = sl.b_nodes; b.b_beg = sl.b_beg; b.b_end = sl.b_end;
-        b.b_col = sl.b_col; b.scale = sl.scale; b.lab_b = sl.lab_b; b.train_b = sl.train_b; b.stats = sl.stats;
-        CeSlot<T>& e = g.ce.s[j];
-        e.logits = sl.logits; e.dlog = (T*)sl.gG; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
-        e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
-        e.done = sl.ce_done;
-      }
-      // the GEMMs of every layer are grouped over the slots: Z = H W, dW = H^T dZ, dH = dZ W^T
-      for (int l = 0; l < L; ++l) {
-        std::vector<GemmOp> fw, dw, dx;
-        for (int j = 0; j < g.count; ++j) {
-          Slot& sl = c->slots[g0 + j];
-          const LayerShape& sh = c->shapes[sl.index][l];
-          const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
-          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.half, sl.H[l], sh.half, Wl, sh.Np, sl.gZ[l], sh.Np, !tc,
-                              false, nullptr, 0, nullptr, 0});
-          dw.push_back(GemmOp{true, false, sh.half, sh.Np, nb, sl.H[l], sh.half, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np,
-                              true, false, nullptr, 0, nullptr, 0});
-          if (l > 0)
-            dx.push_back(GemmOp{false, true, nb, sh.half, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.gG, sh.half, !tc, false,
-                                nullptr, 0, nullptr, 0});
-          g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.half;
-          g.dw_fl[l] += 2.0 * nb * sh.Np * sh.half;
-          if (l > 0) g.dx_fl[l] += 2.0 * nb * sh.Np * sh.half;
-        }
-        if (tc || tf) {
-          if (!gemm_tc_prepare(fw.data(), g.count, &g.fwd_tc[l], tf) ||
-              !gemm_tc_prepare(dw.data(), g.count, &g.dw_tc[l], tf) ||
-              (l > 0 && !gemm_tc_prepare(dx.data(), g.count, &g.dx_tc[l], tf)))
-            return fail(c, GIST_E_UNSUPPORTED, "GAT: tcgen05 GEMM plan failed");
-        } else {
-          for (int j = 0; j < g.count; ++j) {
-            g.fwd_f[l].op[j] = fw[j];
-            g.dw_f[l].op[j] = dw[j];
-            if (l > 0) g.dx_f[l].op[j] = dx[j];
-          }
-          g.fwd_f[l].n = g.dw_f[l].n = g.count;
-          g.dx_f[l].n = l > 0 ? g.count : 0;
-        }
-      }
-      P.groups.push_back(g);
-      continue;
-    }
-    for (int l = 0; l < L; ++l) {
-      std::vector<GemmOp> fw, dw, dx;
-      std::vector<BdOp> bfw, bbw;
-      if (g.reassoc && l == L - 1 && !sage) {
-        // Re-associated last GCN layer (Eq. (1): Z = A_hat (H W), width Np instead of
-        // the hidden width; A_hat symmetric): forward P = H W, logits = A_hat P; backward
-        // Q = A_hat dZ, dW = H^T Q, dH = Q W^T * ReLU'(H).
-        std::vector<GemmOp> op_p, op_w, op_h;
-        for (int j = 0; j < g.count; ++j) {
-          Slot& sl = c->slots[g0 + j];
-          const auto& shp = c->shapes[sl.index];
-          const LayerShape& sh = shp[l];
-          const int64_t Np = sh.Np, Kp = sh.Kp;
-          const bf16* Wl = sl.Wb + sh.off;
-          const bf16* H = (const bf16*)sl.H[l];
-          bf16 *P = (bf16*)sl.rP, *DQ = (bf16*)sl.rDQ;
-          op_p.push_back(GemmOp{false, false, nb, Np, Kp, H, Kp, Wl, Np, P, Np, false, false, nullptr, 0, nullptr, 0,
-                                nullptr, 0, /*keep_out*/ 1, 0});
-          SpmmArgs<T, float>& a = g.ra_fsp_f.a[j];
-          a = SpmmArgs<T, float>();
-          a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-          a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
-          a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;
-          a.H = (const T*)P; a.ldh = Np; a.w = Np; a.out = sl.logits; a.ldo = Np;
-          SpmmArgs<T, T>& b = g.ra_bsp.a[j];
-          b = SpmmArgs<T, T>();
-          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
-          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
-          b.rowscale = sl.scale; b.colscale = sl.scale; b.self = 1;
-          b.H = (const T*)DQ; b.ldh = 2 * Np; b.w = Np; b.out = (T*)(DQ + Np); b.ldo = 2 * Np;
-          g.ra_fby += (double)nb * Np * 6.0 + nb * 16.0;
-          g.ra_bby += spmm_bytes(b);
-          op_w.push_back(GemmOp{true, false, Kp, Np, nb, H, Kp, DQ + Np, 2 * Np, sl.G + sh.off, Np, true, false, nullptr,
-                                0, nullptr, 0, nullptr, 0, 0, /*stream_a*/ 1});
-          GemmOp h{false, true, nb, Kp, Np, DQ + Np, 2 * Np, Wl, Np, sl.dZ[l - 1], shp[l - 1].Np, false, false, nullptr,
-                   0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
-          h.mbits_in = sl.mb[l]; h.ldmbi = c->mb_ld[l];
-          op_h.push_back(h);
-          g.ra_gemm_fl += 2.0 * nb * Np * Kp * 3;
-        }
-        g.ra_fsp_f.n = g.ra_bsp.n = g.count;
-        if (!gemm_bf16_prepare(op_p.data(), g.count, &g.ra_p) || !gemm_bf16_prepare(op_w.data(), g.count, &g.ra_dw) ||
-            !gemm_bf16_prepare(op_h.data(), g.count, &g.ra_dh))
-          return fail(c, GIST_E_UNSUPPORTED, "re-associated GCN layer: tcgen05 GEMM plan failed");
-        g.ce.ld_dlog = 2 * (int64_t)c->shapes[c->slots[g0].index][l].Np;
-        for (int j = 0; j < g.count; ++j) g.ce.s[j].dlog = (T*)c->slots[g0 + j].rDQ;
-        continue;
-      }
-      if (g.reassoc && l == L - 1) {
-        // Re-associated last GraphSAGE layer (exact algebra of Eq. (2), with the
-        // class width far below the hidden width): Z = H W_top + N (H W_bot), so the
-        // aggregation runs at the class width Np instead of the hidden width; backward:
-        // Q = N^T dZ (width Np), dW_top = H^T dZ, dW_bot = H^T Q, dH = dZ W_top^T + Q W_bot^T.
-        std::vector<GemmOp> op_p, op_z, op_w, op_hb;
-        std::vector<BdOp> fb, bb;
-        for (int j = 0; j < g.count; ++j) {
-          Slot& sl = c->slots[g0 + j];
-          const auto& shp = c->shapes[sl.index];
-          const LayerShape& sh = shp[l];
-          const int64_t Np = sh.Np, half = sh.half, Kp = sh.Kp;
-          const bf16* Wl = sl.Wb + sh.off;  // [W_top; W_bot], Kp x Np
-          const bf16* H = (const bf16*)sl.C[l];  // left half of C_l (written by GEMM l-1)
-          bf16 *P = (bf16*)sl.rP, *AGG = (bf16*)sl.rAGG, *DQ = (bf16*)sl.rDQ, *DZs = (bf16*)sl.rDZs;
-          op_p.push_back(GemmOp{false, false, nb, Np, half, H, Kp, Wl + half * Np, Np, P, Np, false, false, nullptr, 0,
-                                nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0});
-          GemmOp z{false, false, nb, Np, half, H, Kp, Wl, Np, sl.logits, Np, true, false, nullptr, 0, nullptr, 0};
-          z.add = AGG; z.ldadd = Np;
-          op_z.push_back(z);
-          // forward aggregation of P
-          SpmmArgs<T, T>& a = g.ra_fsp.a[j];
-          a = SpmmArgs<T, T>();
-          a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-          a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
-          a.rowscale = sl.scale; a.H = (const T*)P; a.ldh = Np; a.w = Np; a.out = (T*)AGG; a.ldo = Np;
-          if (bd) {
-            fb.push_back(BdOp{P, Np, (int64_t)nb, Np, (void*)AGG, Np, nullptr, 0, sl.scale, sl.desc_dev, 0, 1});
-            a.add = (const T*)AGG; a.ld_add = Np; a.few_nnz = 1;
-          }
-          g.ra_fby += spmm_bytes(a);
-          // backward: Q = N^T dZ into DQ[:, Np:2Np) (dZ in DQ[:, 0:Np) from the loss kernel)
-          SpmmArgs<T, T>& b = g.ra_bsp.a[j];
-          b = SpmmArgs<T, T>();
-          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
-          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
-          b.w = Np; b.out = (T*)(DQ + Np); b.ldo = 2 * Np;
-          if (bd) {  // N^T = A diag(1/deg): aggregate DZs = dZ / deg (written by the loss kernel)
-            bb.push_back(BdOp{DZs, 2 * Np, (int64_t)nb, Np, (void*)(DQ + Np), 2 * Np, nullptr, 0, nullptr, sl.desc_dev, 0, 1});
-            b.H = (const T*)DZs; b.ldh = 2 * Np;
-            b.add = (const T*)(DQ + Np); b.ld_add = 2 * Np; b.few_nnz = 1;
-          } else {
-            b.colscale = sl.scale; b.H = (const T*)DQ; b.ldh = 2 * Np;
-          }
-          g.ra_bby += spmm_bytes(b);
-          op_w.push_back(GemmOp{true, false, half, Np, nb, H, Kp, DQ, 2 * Np, sl.G + sh.off, Np, true, false, nullptr, 0,
-                                nullptr, 0, nullptr, 0, 0, /*stream_a*/ 1});
-          op_w.push_back(GemmOp{true, false, half, Np, nb, H, Kp, DQ + Np, 2 * Np, sl.G + sh.off + half * Np, Np, true,
-                                false, nullptr, 0, nullptr, 0, nullptr, 0, 0, 1});
-          // dH = [dZ | Q] [W_top | W_bot]^T (one K = 2 Np GEMM), masked by ReLU'(H) -> dZ_{l-1}
-          GemmOp hb{false, true, nb, half, 2 * Np, DQ, 2 * Np, (const bf16*)sl.rWc, 2 * Np, sl.dZ[l - 1],
-                    shp[l - 1].Np, false, false, nullptr, 0, nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0};
-          hb.mbits_in = sl.mb[l]; hb.ldmbi = c->mb_ld[l];
-          op_hb.push_back(hb);
-          g.ra_wc.src[j] = Wl;
-          g.ra_wc.dst[j] = (bf16*)sl.rWc;
-          g.ra_wc.half[j] = (int)half;
-          g.ra_wc.Np = (int)Np;
-          g.ra_wc.max_half = std::max<int>(g.ra_wc.max_half, (int)half);
-          g.ra_gemm_fl += 2.0 * nb * Np * half * 6;
-          if (bd) g.ra_bd_fl += 2.0 * q * c->bs * c->bs * Np;
-        }
-        g.ra_fsp.n = g.ra_bsp.n = g.count;
-        g.ra_wc.n = g.count;
-        if (bd && (!gemm_bd_prepare(c->blocks, c->c, c->bs, fb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_fbd) ||
-                   !gemm_bd_prepare(c->blocks, c->c, c->bs, bb.data(), g.count, q, nb, c->cstart, c->dstate, &g.ra_bbd)))
-          return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: block-diagonal plan failed");
-        if (!gemm_bf16_prepare(op_p.data(), g.count, &g.ra_p) || !gemm_bf16_prepare(op_z.data(), g.count, &g.ra_z) ||
-            !gemm_bf16_prepare(op_w.data(), 2 * g.count, &g.ra_dw) ||
-            !gemm_bf16_prepare(op_hb.data(), g.count, &g.ra_dh))
-          return fail(c, GIST_E_UNSUPPORTED, "re-associated layer: tcgen05 GEMM plan failed");
-        // the loss kernel writes dZ into DQ[:, 0:Np) (and dZ / deg for the block-diagonal path)
-        g.ce.ld_dlog = 2 * (int64_t)c->shapes[c->slots[g0].index][l].Np;
-        for (int j = 0; j < g.count; ++j) {
-          Slot& sl = c->slots[g0 + j];
-          g.ce.s[j].dlog = (T*)sl.rDQ;
-          g.ce.s[j].dlog_s = bd ? (T*)sl.rDZs : nullptr;
-          g.ce.s[j].scale_s = sl.scale;
-        }
-        continue;
-      }
-      for (int j = 0; j < g.count; ++j) {
-        Slot& sl = c->slots[g0 + j];
-        const auto& shp = c->shapes[sl.index];
-        const LayerShape& sh = shp[l];
-        if (l == 0) {
-          BatchSlot& b = g.batch.s[j];
-          b.desc = sl.desc_dev; b.map64 = sl.map64; b.b_nodes = sl.b_nodes; b.b_beg = sl.b_beg; b.b_end = sl.b_end;
-          b.b_col = sl.b_col; b.scale = sl.scale; b.lab_b = sl.lab_b; b.train_b = sl.train_b; b.stats = sl.stats;
-          CeSlot<T>& e = g.ce.s[j];
-          e.logits = sl.logits; e.dlog = (T*)sl.dZ[L - 1]; e.row_loss = sl.row_loss; e.lab = sl.lab_b;
-          e.train = sl.train_b; e.stats = sl.stats; e.step_loss = sl.step_loss; e.loss_acc = sl.loss_acc;
-          e.done = sl.ce_done;
-        }
-        T* C = (T*)sl.C[l];
-        // forward aggregation (a2)
-        SpmmArgs<T, T>& a = g.fwd_spmm[l].a[j];
-        a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb;
-        a.desc = sl.desc_dev; a.st = c->dstate; a.q = q;
-        if (sage) {
-          a.rowscale = sl.scale;               // N = D^-1 A (R2)
-          a.out = C + sh.half; a.ldo = sh.Kp;   // right half: N H
-          a.w = sh.half;
-          if (l == 0) {
-            a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]);
-            a.self_out = C; a.ld_self = sh.Kp;  // left half: gathered X rows
-          } else {
-            a.H = C; a.ldh = sh.Kp;             // left half written by the previous GEMM epilogue
-          }
-        } else {
-          a.rowscale = sl.scale; a.colscale = sl.scale; a.self = 1;  // D~^-1/2 (A+I) D~^-1/2 (R1)
-          a.out = C; a.ldo = sh.Kp; a.w = sh.Kp;
-          if (l == 0) { a.h_index = sl.b_nodes; a.H = (const T*)c->X; a.ldh = pad8(c->dims[0]); }
-          else { a.H = (const T*)sl.H[l]; a.ldh = sh.Kp; }
-        }
-        if (bd) {  // intra-cluster part on tensor cores, then the sparse kernel adds the rest in place.
-          // Layer 0 reads the batch-local X_b rows the batch build copied into the left half
-          // (L2-resident) rather than gathering rows of the global X from HBM.
-          bfw.push_back(BdOp{(const bf16*)C, sh.Kp, (int64_t)nb, sh.half, (void*)(C + sh.half), sh.Kp, nullptr, 0,
-                             sl.scale, sl.desc_dev, 0, /*keep_out*/ 1});
-          a.add = C + sh.half; a.ld_add = sh.Kp;
-          a.few_nnz = 1;
-          if (l == 0) {
-            a.self_out = nullptr; a.h_index = nullptr; a.H = C; a.ldh = sh.Kp;
-            g.batch.xdst[j] = (bf16*)C;
-          }
-          g.bd_fl[l] += 2.0 * q * c->bs * c->bs * sh.half;
-        }
-        g.fwd_by[l] += spmm_bytes(a);
-        // forward contraction (a3)
-        const void* Wl = tc ? (const void*)(sl.Wb + sh.off) : (const void*)(sl.W + sh.off);
-        if (l + 1 < L) {
-          void* out = sage ? sl.C[l + 1] : sl.H[l + 1];
-          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, out, shp[l + 1].Kp, false, true,
-                              nullptr, 0, nullptr, 0, tc ? sl.mb[l + 1] : nullptr, tc ? c->mb_ld[l + 1] : 0,
-                              /*keep_out: read by the next aggregation + GEMM*/ 1, /*stream_a*/ 1});
-        } else {
-          fw.push_back(GemmOp{false, false, nb, sh.Np, sh.Kp, C, sh.Kp, Wl, sh.Np, sl.logits, sh.Np, true, false,
-                              nullptr, 0, nullptr, 0});
-        }
-        g.fwd_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
-        // backward: dW_l = C_l^T dZ_l (fp32 into the packed gradient buffer)
-        dw.push_back(GemmOp{true, false, sh.Kp, sh.Np, nb, C, sh.Kp, sl.dZ[l], sh.Np, sl.G + sh.off, sh.Np, true, false,
-                            nullptr, 0, nullptr, 0, nullptr, 0, 0, /*stream_a: C_l's last read*/ 1});
-        g.dw_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
-        if (l > 0) {
-          // dC_l = dZ_l W_l^T
-          // (bd: the epilogue pre-scales the neighbour half by 1/deg of the row: N^T = A diag(1/deg))
-          dx.push_back(GemmOp{false, true, nb, sh.Kp, sh.Np, sl.dZ[l], sh.Np, Wl, sh.Np, sl.dC, sh.Kp, false, false,
-                              nullptr, 0, bd ? sl.scale : nullptr, sh.half, nullptr, 0, /*keep_out*/ 1, 0});
-          g.dx_fl[l] += 2.0 * nb * sh.Np * sh.Kp;
-          SpmmArgs<T, T>& b = g.bwd_spmm[l].a[j];
-          b.row_beg = sl.b_beg; b.row_end = sl.b_end; b.col = sl.b_col; b.rows = nb;
-          b.desc = sl.desc_dev; b.st = c->dstate; b.q = q;
-          b.out = (T*)sl.dZ[l - 1]; b.ldo = shp[l - 1].Np;
-          if (tc) { b.mbits = sl.mb[l]; b.ld_mbits = c->mb_ld[l]; }  // ReLU mask of C_l / H_l as bits
-          if (sage && bd) {  // dZ_{l-1} = (dC_self + A_blocks dC'_neigh + A_inter dC'_neigh) * 1[H_l > 0]
-            bbw.push_back(BdOp{(const bf16*)sl.dC + sh.half, sh.Kp, (int64_t)nb, sh.half, sl.dZ[l - 1],
-                               shp[l - 1].Np, (const bf16*)sl.dC, sh.Kp, nullptr, sl.desc_dev, 0, /*keep_out*/ 1});
-            b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
-            b.add = (const T*)sl.dZ[l - 1]; b.ld_add = shp[l - 1].Np;
-            b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
-            b.w = sh.half;
-            b.few_nnz = 1;
-          } else if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
-            b.colscale = sl.scale; b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
-            b.add = (const T*)sl.dC; b.ld_add = sh.Kp;
-            b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
-            b.w = sh.half;
-          } else {     // dZ_{l-1} = (A_hat^T dC) * 1[H_l > 0]
-            b.rowscale = sl.scale; b.colscale = sl.scale; b.self = 1;
-            b.H = (const T*)sl.dC; b.ldh = sh.Kp;
-            b.mask = (const T*)sl.H[l]; b.ld_mask = sh.Kp;
-            b.w = sh.Kp;
-          }
-          g.bwd_by[l] += spmm_bytes(b);
-        }
-      }
-      g.fwd_spmm[l].n = g.count;
-      g.bwd_spmm[l].n = l > 0 ? g.count : 0;
-      if (bd) {
-        if (!gemm_bd_prepare(c->blocks, c->c, c->bs, bfw.data(), g.count, q, nb, c->cstart, c->dstate,
-                             &g.fwd_bd[l]) ||
-            (l > 0 && !gemm_bd_prepare(c->blocks, c->c, c->bs, bbw.data(), g.count, q, nb, c->cstart, c->dstate,
-                                       &g.bwd_bd[l])))
-          return fail(c, GIST_E_UNSUPPORTED, "block-diagonal aggregation plan failed");
-      }
-      if (tc || tf) {
-        if (tf)  // TF32 mode: every output of the step GEMMs is fp32 (the mode's element type)
-          for (auto* v : {&fw, &dw, &dx})
-            for (GemmOp& o : *v) o.out_f32 = true;
-        if (!gemm_tc_prepare(fw.data(), g.count, &g.fwd_tc[l], tf) ||
-            !gemm_tc_prepare(dw.data(), g.count, &g.dw_tc[l], tf) ||
-            (l > 0 && !gemm_tc_prepare(dx.data(), g.count, &g.dx_tc[l], tf)))
-          return fail(c, GIST_E_UNSUPPORTED, "tcgen05 GEMM plan failed (alignment / driver entry point)");
-      } else {
-        for (int j = 0; j < g.count; ++j) {
-          g.fwd_f[l].op[j] = fw[j];
-          g.dw_f[l].op[j] = dw[j];
-          if (l > 0) g.dx_f[l].op[j] = dx[j];
-        }
-        g.fwd_f[l].n = g.dw_f[l].n = g.count;
-        g.dx_f[l].n = l > 0 ? g.count : 0;
-      }
-    }
-    P.groups.push_back(g);
-  }
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
+// ============================================================ checkpoint ===
+// SPEC.md "External Interfaces": "GIST", version u32, arch u8, L u32, dims u32[L+1], then the
+// weights row-major f32 (logical layout, layer by layer).  Little-endian hosts only (x86 / ARM).
+extern "C" gist_status gist_save_checkpoint(gist_ctx* c, const char* path) {
   PRE(c);
-  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "partition: needs params and no open round");
-  if (m < 1) return fail(c, GIST_E_ARG, "partition: m < 1");
-  if (c->arch == GIST_ARCH_GAT && m > kMaxMean) return fail(c, GIST_E_ARG, "partition: GAT supports m <= 128");
-  for (int l = 1; l < c->L; ++l)
-    if (m > c->dims[l]) return fail(c, GIST_E_ARG, "partition: m exceeds hidden dim " + std::to_string(l));
-  cudaStream_t s = c->stream;
-  if (m != c->alloc_m) TRY(alloc_slots(c, m));
-  c->prof_now = c->prof_stride > 0;
-  c->m = m;
-  // subGCNs keys / sort / blocks for every hidden dim (R5)
-  int dmax = 0;
-  for (int l = 1; l < c->L; ++l) dmax = std::max(dmax, c->dims[l]);
-  if (c->units.empty()) {
-    c->units.assign(c->L + 1, nullptr);
-    for (int l = 1; l < c->L; ++l) TRY(dalloc_t(c, &c->units[l], c->dims[l]));
-    if (dmax > 0) {
-      TRY(dalloc_t(c, &c->keys_a, dmax));
-      TRY(dalloc_t(c, &c->keys_b, dmax));
-      TRY(dalloc_t(c, &c->idx_a, dmax));
-      TRY(dalloc_t(c, &c->idx_b, dmax));
-      TRY(dalloc_t(c, &c->blk, dmax));
-      c->sort_tmp_bytes = partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, dmax, nullptr, 0, s);
-      TRY(dalloc(c, &c->sort_tmp, c->sort_tmp_bytes));
-    }
-  }
-  if (c->offs_dev) dfree(c, c->offs_dev);
-  TRY(dalloc_t(c, &c->offs_dev, (size_t)(m + 1) * (c->L + 1)));
-  c->offs.assign(c->L + 1, std::vector<int32_t>());
-  std::vector<int32_t> offs_all((size_t)(m + 1) * (c->L + 1), 0);
+  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "save_checkpoint: needs parameters and no open round");
+  if (!path) return fail(c, GIST_E_ARG, "save_checkpoint: null path");
+  std::string buf("GIST", 4);
+  auto put = [&](const void* p, size_t n) { buf.append(static_cast<const char*>(p), n); };
+  const uint32_t version = 1, L = (uint32_t)c->L;
+  const uint8_t arch = (uint8_t)c->arch;
+  put(&version, 4);
+  put(&arch, 1);
+  put(&L, 4);
   for (int l = 0; l <= c->L; ++l) {
-    const int d = c->dims[l];
-    std::vector<int32_t>& o = c->offs[l];
-    o.assign(m + 1, 0);
-    if (l == 0 || l == c->L) {
-      for (int i = 0; i <= m; ++i) o[i] = 0;  // unused: identity
-      continue;
-    }
-    const int base = d / m, extra = d % m;
-    for (int i = 0; i < m; ++i) o[i + 1] = o[i] + base + (i < extra ? 1 : 0);
-    std::copy(o.begin(), o.end(), offs_all.begin() + (size_t)l * (m + 1));
+    const uint32_t d = (uint32_t)c->dims[l];
+    put(&d, 4);
   }
-  CK(cudaMemcpyAsync(c->offs_dev, offs_all.data(), offs_all.size() * 4, cudaMemcpyHostToDevice, s));
-  for (int l = 1; l < c->L; ++l) {
-    const int d = c->dims[l];
-    PL(GIST_PROF_PARTITION, d * 12.0, s, partition_keys(d, (uint32_t)c->round, (uint32_t)l, seed, c->keys_a, c->idx_a, s));
-    PL(GIST_PROF_PARTITION, d * 24.0, s,
-       partition_sort(c->keys_a, c->keys_b, c->idx_a, c->idx_b, d, c->sort_tmp, c->sort_tmp_bytes, s));
-    PL(GIST_PROF_PARTITION, d * 8.0, s, partition_assign(c->idx_b, d, m, c->blk, s));
-    PL(GIST_PROF_PARTITION, d * 4.0 * (m + 1), s,
-       partition_compact(c->blk, d, m, c->offs_dev + (size_t)l * (m + 1), c->units[l], s));
-  }
-  // shapes of every slot (all ranks know the full partition)
-  c->shapes.assign(m, std::vector<LayerShape>(c->L));
-  for (int i = 0; i < m; ++i) {
-    int64_t off = 0;
-    for (int l = 0; l < c->L; ++l) {
-      LayerShape& sh = c->shapes[i][l];
-      sub_logical(c, i, l, &sh.nrows, &sh.ncols);
-      sh.half = (int)pad8(sh.nrows);
-      sh.Kp = (int)kphys(c, sh.nrows);
-      sh.Np = (int)pad8(sh.ncols);
-      sh.off = off;
-      off += (int64_t)sh.Kp * sh.Np;
-      sh.rows = (l == 0) ? nullptr : c->units[l] + c->offs[l][i];
-      sh.cols = (l + 1 == c->L) ? nullptr : c->units[l + 1] + c->offs[l + 1][i];
-    }
-  }
-  // extract Theta^(i) for local slots (R6), reset optimizer state (R8)
-  for (Slot& sl : c->slots) {
-    const auto& shp = c->shapes[sl.index];
-    for (int l = 0; l < c->L; ++l) {
-      const LayerShape& sh = shp[l];
-      LayerMap mp;
-      mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = c->arch == GIST_ARCH_GAT; mp.half = sh.half;
-      mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
-      mp.ldg = c->th_N[l];
-      PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta[l], mp, sl.W + sh.off, s));
-      if (persistent_adam(c)) {  // f3: slice the global moments exactly like the weights
-        PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta_m[l], mp, sl.M + sh.off, s));
-        PL(GIST_PROF_PARTITION, (double)sh.Kp * sh.Np * 12.0, s, extract_sub(c->theta_v[l], mp, sl.V + sh.off, s));
-      }
-    }
-  }
-  const int64_t tot_local = (int64_t)c->slots.size() * c->S_max;
-  if (c->Mall && tot_local > 0 && !persistent_adam(c)) {  // R8: reset per round
-    CK(cudaMemsetAsync(c->Mall, 0, (size_t)tot_local * 4, s));
-    CK(cudaMemsetAsync(c->Vall, 0, (size_t)tot_local * 4, s));
-  }
-  if (c->Wball && tot_local > 0) LK(f32_to_bf16(c->Wall, c->Wball, tot_local, s));
-  if (c->prec == GIST_PREC_BF16) TRY(build_plan<bf16>(c, c->plan_b));
-  else TRY(build_plan<float>(c, c->plan_f));
-  c->prof_now = false;
-  TRY(check_launch(c, "partition"));
-  if (!persistent_adam(c)) c->adam_t = 0;  // R8 (f3: the counter carries over)
-  c->state = S_PARTITIONED;
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_get_partition(gist_ctx* c, int32_t dim, int32_t* units, int32_t* offs) {
-  PRE(c);
-  if (c->m == 0 || c->offs.empty()) return fail(c, GIST_E_STATE, "get_partition: no partition yet");
-  if (dim < 0 || dim > c->L || !units || !offs) return GIST_E_ARG;
-  const int d = c->dims[dim];
-  if (dim == 0 || dim == c->L) {
-    for (int r = 0; r < d; ++r) units[r] = r;
-    for (int i = 0; i <= c->m; ++i) offs[i] = 0;
-    offs[c->m] = d;
-    return GIST_OK;
-  }
-  CK(cudaMemcpyAsync(units, c->units[dim], (size_t)d * 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  std::copy(c->offs[dim].begin(), c->offs[dim].end(), offs);
-  return GIST_OK;
-}
-
-// ============================================================== step ======
-template <typename T>
-static void launch_gemm(gist_ctx* c, const GemmPlanTC& tcp, const SgemmGroup& fp, double flops, cudaStream_t s) {
-  const int id = prof_begin(c, s, GIST_PROF_GEMM, flops);
-  if (c->prec == GIST_PREC_FP32) gemm_f32_group(fp, s);
-  else gemm_bf16_launch(tcp, s);  // BF16 or TF32 tcgen05 plan
-  prof_end(c, s, id);
-  ++c->nk;
-}
-
-// One GAT subTrain step (R21) of every slot of group g after the grouped batch build: per slot
-// and layer Z = H W (GEMM), attention scores and aggregation; the grouped softmax-CE; then per
-// slot and layer the two attention backward passes, dW = H^T dZ (plus the attention rows) and
-// dH = dZ W^T.  Dummy batch rows (v >= n_b) carry no neighbours and a zero loss gradient.
-template <typename T>
-static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int nnz_slot, cudaStream_t s) {
-  const int L = c->L;
-  const int64_t nb = c->nb_max_rows;
-  auto layer_args = [&](Slot& sl, int l) {
-    const LayerShape& sh = c->shapes[sl.index][l];
-    GatLayer<T> a;
-    a.row_beg = sl.b_beg; a.row_end = sl.b_end; a.col = sl.b_col; a.rows = nb; a.w = sh.Np;
-    a.Z = (const T*)sl.gZ[l]; a.ldz = sh.Np;
-    a.a_src = sl.W + sh.off + (int64_t)sh.half * sh.Np;
-    a.a_dst = a.a_src + sh.Np;
-    float* sc = sl.gsc[l];
-    a.s = sc; a.t = sc + nb; a.lse = sc + 2 * nb; a.Srow = sc + 3 * nb; a.dt = sc + 4 * nb; a.ds = sc + 5 * nb;
-    return a;
-  };
-  const int64_t d0p = pad8(c->dims[0]);
-  for (int j = 0; j < g.count; ++j) {  // layer-0 input: the batch rows of X
-    Slot& sl = c->slots[g.first + j];
-    LK(gather_rows_t<T>((const T*)c->X, d0p, sl.b_nodes, nb, d0p, (T*)sl.H[0], d0p, s));
-  }
-  for (int l = 0; l < L; ++l) {  // ---- a2/a3: forward
-    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);  // Z = H W (grouped)
-    // compulsory bytes: Z read once, H (scores) and the output written once, per-row scalars,
-    // 4 B per edge of the batch CSR (the gathered Z rows are served from L2, as for k_spmm)
-    double by = 0.0;
-    GatGroup<T> G;
-    G.n = g.count;
-    for (int j = 0; j < g.count; ++j) {
-      Slot& sl = c->slots[g.first + j];
-      const auto& shp = c->shapes[sl.index];
-      const LayerShape& sh = shp[l];
-      by += (double)nb * (sh.Np * 2.0 * sizeof(T) + sh.half * sizeof(T) + 32.0);
-      GatLayer<T>& a = G.a[j];
-      a = layer_args(sl, l);
-      a.H = (const T*)sl.H[l]; a.ldh = sh.half; a.kw = sh.half;  // scores = H (W a), fp32 W a
-      a.W32 = sl.W + sh.off; a.ldw = sh.Np; a.wa = sl.gsc[l] + 6 * nb;
-      if (l + 1 < L) { a.out = (T*)sl.H[l + 1]; a.ldo = shp[l + 1].half; a.relu = 1; }
-      else { a.out_f32 = sl.logits; a.ldo = sh.Np; }
-    }
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 4.0 * g.count, nnz_slot);
-    LK(gat_scores<T>(G, s));
-    LK(gat_forward<T>(G, s));
-    ++c->nk;
-    prof_end(c, s, id);
-  }
-  {  // ---- a4: softmax cross-entropy (grouped), dlogits into gG
-    const int id = prof_begin(c, s, GIST_PROF_LOSS, (double)g.count * nb * (g.ce.ld * (4.0 + sizeof(T)) + 17.0));
-    softmax_ce<T>(g.ce, s);
-    prof_end(c, s, id);
-    ++c->nk;
-  }
-  for (int l = L - 1; l >= 0; --l) {  // ---- a5/a6: backward
-    double by = 0.0;  // Z, G (+ mask), dZ once; scalars; two passes over the batch CSR
-    GatGroup<T> G;
-    G.n = g.count;
-    for (int j = 0; j < g.count; ++j) {
-      Slot& sl = c->slots[g.first + j];
-      const auto& shp = c->shapes[sl.index];
-      const LayerShape& sh = shp[l];
-      by += (double)nb * (sh.Np * 4.0 * sizeof(T) + 48.0);
-      GatLayer<T>& a = G.a[j];
-      a = layer_args(sl, l);
-      a.G = (const T*)sl.gG; a.ldg = sh.Np;  // dlogits (last layer) or dH_{l+1} (width Np_l)
-      if (l + 1 < L) { a.mask = (const T*)sl.H[l + 1]; a.ldm = shp[l + 1].half; }
-      a.dZ = (T*)sl.dZ[l]; a.ldd = sh.Np;
-      a.da_src = sl.G + sh.off + (int64_t)sh.half * sh.Np;
-      a.da_dst = a.da_src + sh.Np;
-      a.da_part = sl.gsc[l] + 6 * nb + 2 * sh.half;
-    }
-    const int id = prof_begin(c, s, GIST_PROF_SPMM, by, 8.0 * g.count, nnz_slot);
-    LK(gat_backward<T>(G, s));
-    c->nk += 3;
-    prof_end(c, s, id);
-    if (c->side_now) {  // dW_l only feeds the optimizer: overlap it with the rest of the backward chain
-      CK(cudaEventRecord(c->ev_dw_fork, s));
-      CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
-    }
-    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->side_now ? c->side_now : s);  // dW = H^T dZ (rows [0, half))
-    if (l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);          // dH = dZ W^T -> gG
-  }
-  if (c->side_now) {
-    CK(cudaEventRecord(c->ev_dw_join, c->side_now));
-    CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
-  }
-  return GIST_OK;
-}
-
-// One subTrain step of every slot of group g, in lockstep: every
-// kernel below is one launch over all slots of the group.
-template <typename T>
-static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t s) {
-  const int L = c->L;
-  for (int j = 0; j < g.count; ++j) c->slots[g.first + j].last_nb = c->slots[g.first + j].nb_of_step[z];
-  int nnz_slot = -1;
-  if (c->prof_now && c->nnz_pin_used < c->nnz_pin_cap) nnz_slot = c->nnz_pin_used++;
-  // ---- a1: Cluster mini-batch build (unless prefetched during the previous step's optimizer)
-  if (!c->batch_prefetched) {
-    double vol = 0.0;
-    for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
-    int id = -1;
-    if (c->prof_now)
-      id = prof_begin(c, s, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0, 4.0,
-                      nnz_slot);
-    batch_setup(g.batch, c->cstart, c->rp, s);
-    batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
-                c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, s);
-    prof_end(c, s, id);
-    c->nk += 2;
-  }
-  if (nnz_slot >= 0)  // nnz of the group's first slot; the profile scales it by the group size
-    CK(cudaMemcpyAsync(c->nnz_pin + nnz_slot, c->slots[g.first].stats, 8, cudaMemcpyDeviceToHost, s));
-  if (c->arch == GIST_ARCH_GAT) return gat_group_step<T>(c, g, nnz_slot, s);
-  const double per_nnz = 4.0 * g.count;
-  auto spmm_l = [&](const SpmmGroup<T, T>& G, double bytes) {
-    int id = -1;
-    if (c->prof_now) id = prof_begin(c, s, GIST_PROF_SPMM, bytes, per_nnz, nnz_slot);
-    spmm_group<T, T>(G, s);
-    prof_end(c, s, id);
-    ++c->nk;
-  };
-  auto bd_l = [&](const BdPlan& P, double flops) {
-    const int id = prof_begin(c, s, GIST_PROF_AGG_TC, flops);
-    gemm_bd_launch(P, s);
-    prof_end(c, s, id);
-    ++c->nk;
-  };
-  const bool bd = c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE;
-  auto tc_l = [&](const GemmPlanTC& P, double fl) {  // one tcgen05 GEMM launch (BF16 plans only)
-    const int id = prof_begin(c, s, GIST_PROF_GEMM, fl);
-    gemm_bf16_launch(P, s);
-    prof_end(c, s, id);
-    ++c->nk;
-  };
-  // ---- a2/a3: forward
-  for (int l = 0; l < L; ++l) {
-    if (g.reassoc && l == L - 1 && c->arch != GIST_ARCH_SAGE) {  // GCN: logits = A_hat (H W)
-      tc_l(g.ra_p, g.ra_gemm_fl / 3);
-      const int id = prof_begin(c, s, GIST_PROF_SPMM, g.ra_fby, per_nnz, nnz_slot);
-      spmm_group<T, float>(g.ra_fsp_f, s);
-      prof_end(c, s, id);
-      ++c->nk;
-      continue;
-    }
-    if (g.reassoc && l == L - 1) {  // Z = H W_top + N (H W_bot)
-      LK(relayout_last(g.ra_wc, s));  // [W_top | W_bot] of this step's weights, for dH below
-      ++c->nk;
-      tc_l(g.ra_p, g.ra_gemm_fl / 6);
-      if (bd) bd_l(g.ra_fbd, g.ra_bd_fl / 2);
-      spmm_l(g.ra_fsp, g.ra_fby);
-      tc_l(g.ra_z, g.ra_gemm_fl / 6);
-      continue;
-    }
-    if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
-    spmm_l(g.fwd_spmm[l], g.fwd_by[l]);
-    launch_gemm<T>(c, g.fwd_tc[l], g.fwd_f[l], g.fwd_fl[l], s);
-  }
-  // ---- a4: softmax cross-entropy
-  {
-    const double bytes = (double)g.count * c->nb_max_rows * (g.ce.ld * (4.0 + sizeof(T)) + 17.0);
-    const int id = prof_begin(c, s, GIST_PROF_LOSS, bytes);
-    softmax_ce<T>(g.ce, s);  // (its last CTA per slot also reduces the step loss)
-    prof_end(c, s, id);
-    c->nk += 1;
-  }
-  // ---- a5/a6: backward.  With the dW stream, dW_l (it only feeds the optimizer) overlaps the
-  // rest of the backward chain (dX -> aggregation), joined before the optimizer.
-  auto fork = [&]() {
-    CK(cudaEventRecord(c->ev_dw_fork, s));
-    CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
-    return GIST_OK;
-  };
-  for (int l = L - 1; l >= 0; --l) {
-    if (g.reassoc && l == L - 1) {
-      // GCN: Q = A_hat dZ; dW = H^T Q; dH = Q W^T.  SAGE: Q = N^T dZ; dW = [H^T dZ; H^T Q];
-      // dZ_{l-1} = (dZ W_top^T + Q W_bot^T) * ReLU'
-      if (bd && c->arch == GIST_ARCH_SAGE) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
-      spmm_l(g.ra_bsp, g.ra_bby);
-      if (c->side_now) {
-        TRY(fork());
-        const int id = prof_begin(c, c->side_now, GIST_PROF_GEMM, g.ra_gemm_fl / 3);
-        gemm_bf16_launch(g.ra_dw, c->side_now);
-        prof_end(c, c->side_now, id);
-        ++c->nk;
-      } else {
-        tc_l(g.ra_dw, g.ra_gemm_fl / 3);
-      }
-      tc_l(g.ra_dh, g.ra_gemm_fl / 3);
-      continue;
-    }
-    if (c->side_now) {
-      TRY(fork());
-      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->side_now);
-    } else {
-      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
-    }
-    if (l == 0) break;
-    launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
-    if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
-    spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
-  }
-  if (c->side_now) {  // join: the optimizer (or the next step) reads every gradient / weight
-    CK(cudaEventRecord(c->ev_dw_join, c->side_now));
-    CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
-  }
-  return GIST_OK;
-}
-
-// a1 of the next step for group g on stream bs: the build reads the batch index st->zb (the
-// device step state's z still points at the current step while its optimizer runs)
-template <typename T>
-static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs) {
-  double vol = 0.0;
-  for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
-  const int id = prof_begin(c, bs, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0);
-  batch_setup(g.batch, c->cstart, c->rp, bs);
-  batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
-              c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, bs);
-  prof_end(c, bs, id);
-  c->nk += 2;
-  return GIST_OK;
-}
-
-// a7 over every local slot at once (the packed buffers are contiguous), then advance the step state
-static gist_status run_optimizer(gist_ctx* c) {
-  cudaStream_t s = c->stream;
-  const int64_t n = (int64_t)c->slots.size() * c->S_max;
-  if (c->cfg.optimizer == GIST_OPT_ADAM)
-    PL(GIST_PROF_OPTIM, (double)n * (28.0 + (c->Wball ? 2.0 : 0.0)), s,
-       adam_step(c->Wall, c->Gall, c->Mall, c->Vall, n, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate, c->Wball,
-                 s));
-  else
-    PL(GIST_PROF_OPTIM, (double)n * (12.0 + (c->Wball ? 2.0 : 0.0)), s,
-       sgd_step(c->Wall, c->Gall, n, c->dstate, c->Wball, s));
-  ++c->nk;  // (no step_advance launch: the optimizer's last CTA advances the step state)
-  return GIST_OK;
-}
-
-// host side of R7 for a whole subtrain call: cluster lists, offsets, n_b, tags per step
-static gist_status schedule(gist_ctx* c, Slot& sl, int iters, bool* grew) {
-  const int q = c->cfg.clusters_per_batch;
-  const int per = 3 * q + 4;
-  if (iters > sl.cap || !sl.desc_dev) {
-    *grew = true;
-    CK(cudaStreamSynchronize(c->stream));  // previous uploads / readers of the old buffers are done
-    if (sl.desc_host) {
-      cudaFreeHost(sl.desc_host);
-      dfree(c, sl.desc_dev);
-    }
-    sl.cap = std::max(iters, 64);
-    CK(cudaMallocHost(&sl.desc_host, (size_t)sl.cap * per * 4));
-    TRY(dalloc_t(c, &sl.desc_dev, (size_t)sl.cap * per));
-  }
-  sl.nb_of_step.assign(iters, 0);
-  sl.q_of_step.assign(iters, 0);
-  sl.vol_of_step.assign(iters, 0);
-  const int64_t B = (c->c + q - 1) / q;
-  for (int z = 0; z < iters; ++z) {
-    const int64_t st = c->step + z;
-    const int64_t e = st / B, p = st % B;
-    if (sl.cached_epoch != e) {
-      epoch_perm(c, sl.index, e, sl.epoch_perm);
-      sl.cached_epoch = (int)e;
-    }
-    int32_t* d = sl.desc_host + (size_t)z * per;
-    const int64_t lo = p * q, hi = std::min<int64_t>((p + 1) * q, c->c);
-    const int qq = (int)(hi - lo);
-    int32_t off = 0;
-    int64_t voff = 0;
-    int32_t* dv = d + 2 * q + 1;
-    for (int k = 0; k < q; ++k) {
-      if (k < qq) {
-        const int32_t cl = sl.epoch_perm[lo + k];
-        d[k] = cl;
-        d[q + k] = off;
-        dv[k] = (int32_t)voff;
-        off += (int32_t)(c->cstart_h[cl + 1] - c->cstart_h[cl]);
-        voff += c->cvol_h[cl];
-      } else {  // last batch of an epoch may hold fewer clusters
-        d[k] = d[qq - 1];
-        d[q + k] = off;
-        dv[k] = (int32_t)voff;
-      }
-    }
-    d[2 * q] = off;
-    dv[q] = (int32_t)voff;
-    d[3 * q + 2] = qq;
-    d[3 * q + 3] = (int32_t)(uint32_t)(c->step + z + 1);  // unique tag per step (0 = never)
-    sl.nb_of_step[z] = off;
-    sl.q_of_step[z] = qq;
-    sl.vol_of_step[z] = voff;
-  }
-  return GIST_OK;
-}
-
-// One subTrain step of every local slot (every lockstep group), the optimizer, and optionally
-// the next step's batch builds on the dW stream, overlapping the optimizer (`prefetch`; every
-// reader of this step's batch buffers precedes the fork).  `build`: this step builds its own
-// batches (else the previous step prefetched them).  Everything that changes from step to step
-// is read by the kernels from the device step state, so the enqueued sequence of a (build,
-// prefetch) variant is identical for every step: it is captured once as a CUDA graph and
-// replayed (step_graph).
-static gist_status enqueue_step(gist_ctx* c, bool build, bool prefetch) {
-  cudaStream_t s = c->stream;
-  const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
-  c->side_now = c->prof_now ? nullptr : c->dws;
-  c->batch_prefetched = !build;
-  for (size_t gi = 0; gi < ng; ++gi) {
-    if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], c->cur_z, s));
-    else TRY(run_group_step<float>(c, c->plan_f.groups[gi], c->cur_z, s));
-  }
-  if (prefetch) {
-    CK(cudaEventRecord(c->ev_dw_fork, s));
-    CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));
-    for (size_t gi = 0; gi < ng; ++gi) {
-      if (c->prec == GIST_PREC_BF16) TRY(prefetch_batch<bf16>(c, c->plan_b.groups[gi], c->cur_z + 1, c->dws));
-      else TRY(prefetch_batch<float>(c, c->plan_f.groups[gi], c->cur_z + 1, c->dws));
-    }
-  }
-  TRY(run_optimizer(c));
-  if (prefetch) {
-    CK(cudaEventRecord(c->ev_dw_join, c->dws));
-    CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
-  }
-  return GIST_OK;
-}
-
-static void drop_graphs(gist_ctx* c) {
-  for (auto& g : c->graphs) {
-    if (g.exec) cudaGraphExecDestroy(g.exec);
-    g.exec = nullptr;
-    g.nk = 0;
-  }
-}
-
-// the step of variant (build, prefetch) as a CUDA graph: captured on first use after every
-// plan (re)build, then one cudaGraphLaunch per step (the host enqueue of ~30 launches with
-// multi-kilobyte grouped argument blocks was as long as the step itself at one slot per GPU)
-static gist_status step_graph(gist_ctx* c, bool build, bool prefetch) {
-  gist_ctx::StepGraph& G = c->graphs[(build ? 2 : 0) + (prefetch ? 1 : 0)];
-  if (!G.exec) {
-    const int64_t nk0 = c->nk;
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    const gist_status st = enqueue_step(c, build, prefetch);
-    cudaGraph_t gr = nullptr;
-    const cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
-    if (st != GIST_OK) {
-      if (gr) cudaGraphDestroy(gr);
-      return st;
-    }
-    CK(e);
-    const cudaError_t ei = cudaGraphInstantiate(&G.exec, gr, 0);
-    cudaGraphDestroy(gr);
-    CK(ei);
-    G.nk = c->nk - nk0;
-    c->nk = nk0;
-  }
-  CK(cudaGraphLaunch(G.exec, c->stream));
-  c->nk += G.nk;
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_subtrain(gist_ctx* c, int32_t local_iters, float lr, float* mean_loss) {
-  PRE(c);
-  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "subtrain: call partition first");
-  if (local_iters < 0) return fail(c, GIST_E_ARG, "subtrain: local_iters < 0");
-  cudaStream_t s = c->stream;
-  // host schedule for every local slot; the previous call's uploads must have left the pinned buffers
-  CK(cudaEventSynchronize(c->hstate_ev));
-  const int per = 3 * c->cfg.clusters_per_batch + 4;
-  bool grew = false;
-  for (Slot& sl : c->slots) TRY(schedule(c, sl, local_iters, &grew));
-  if (grew) {  // descriptor buffers moved: the step plan holds their addresses
-    if (c->prec == GIST_PREC_BF16) TRY(build_plan<bf16>(c, c->plan_b));
-    else TRY(build_plan<float>(c, c->plan_f));
-  }
-  for (Slot& sl : c->slots) {
-    if (local_iters > 0)
-      CK(cudaMemcpyAsync(sl.desc_dev, sl.desc_host, (size_t)local_iters * per * 4, cudaMemcpyHostToDevice, s));
-    c->h2d += (int64_t)local_iters * per * 4;
-    CK(cudaMemsetAsync(sl.loss_acc, 0, 4, s));
-  }
-  *c->hstate = StepState{0, (int32_t)c->adam_t, lr, 0u};
-  if (!c->slots.empty()) CK(cudaMemsetAsync(c->bctr, 0, c->slots.size() * 2 * sizeof(int32_t), s));
-  CK(cudaMemcpyAsync(c->dstate, c->hstate, sizeof(StepState), cudaMemcpyHostToDevice, s));
-  CK(cudaEventRecord(c->hstate_ev, s));
-  // GIST_BATCH_PREFETCH=0 / GIST_GRAPH=0: A/B switches (prefetch measured +1.4% on C3)
-  const char* e_pf = std::getenv("GIST_BATCH_PREFETCH");
-  const char* e_gr = std::getenv("GIST_GRAPH");
-  const bool prefetch_on = !(e_pf && e_pf[0] == '0'), graphs_on = !(e_gr && e_gr[0] == '0');
-  bool prefetched = false;  // step z's batches were built during step z-1's optimizer
-  for (int z = 0; z < local_iters; ++z) {
-    c->prof_now = c->prof_stride > 0 && ((c->step + z) % c->prof_stride) == 0;
-    const bool next_prof = c->prof_stride > 0 && ((c->step + z + 1) % c->prof_stride) == 0;
-    for (Slot& sl : c->slots) sl.last_nb = sl.nb_of_step[z];
-    c->cur_z = z;
-    // profiled steps run eagerly and serialised, and build their own batches
-    const bool pf = prefetch_on && c->dws && z + 1 < local_iters && !c->prof_now && !next_prof;
-    if (graphs_on && !c->prof_now) TRY(step_graph(c, !prefetched, pf));
-    else TRY(enqueue_step(c, !prefetched, pf));
-    prefetched = pf;
-    c->prof_now = false;
-  }
-  c->adam_t += local_iters;
-  c->step += local_iters;
-  TRY(check_launch(c, "subtrain"));
-  if (c->prof_stride > 0) prof_flush(c);
-  if (mean_loss) {
-    std::fill(mean_loss, mean_loss + c->m, 0.f);
-    CK(cudaStreamSynchronize(s));
-    for (Slot& sl : c->slots) {
-      float v = 0.f;
-      CK(cudaMemcpy(&v, sl.loss_acc, 4, cudaMemcpyDeviceToHost));
-      mean_loss[sl.index] = local_iters > 0 ? v / (float)local_iters : 0.f;
-      c->d2h += 4;
-    }
-  }
-  return GIST_OK;
-}
-
-// ============================================================ aggregate ===
-extern "C" gist_status gist_aggregate(gist_ctx* c) {
-  PRE(c);
-  if (c->state != S_PARTITIONED) return fail(c, GIST_E_STATE, "aggregate: no open round");
-  cudaStream_t s = c->stream;
-  const int W = c->cfg.world_size;
-  c->prof_now = c->prof_stride > 0;
-  // the weights, and with persistent Adam state (f3) the two moments, travel the same way
-  struct Part { float* local; std::vector<float*>* global; };
-  std::vector<float*> wvec(c->theta.begin(), c->theta.end());
-  std::vector<Part> parts = {{c->Wall, &wvec}};
-  if (persistent_adam(c)) parts.push_back({c->Mall, &c->theta_m}), parts.push_back({c->Vall, &c->theta_v});
-  if (c->p2p_base) {  // agg_mode P2P (f2): owners store their blocks into every replica
-    // barrier 1: every rank has finished this round's reads of its replica (gist_partition's
-    // extraction) before any peer overwrites it
-    TRY(coll(c, comm_barrier(c->comm, c->barrier_word, s, &c->err)));
-    for (const Part& pt : parts)
-      for (int i = c->cfg.rank; i < c->m; i += W) {
-        const int j = i / W;
-        const float* w = pt.local + (size_t)j * c->S_max;
-        for (int l = 0; l < c->L; ++l) {
-          const LayerShape& sh = c->shapes[i][l];
-          LayerMap mp;
-          mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = 0; mp.half = sh.half;
-          mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
-          mp.ldg = c->th_N[l];
-          const size_t off = (size_t)(reinterpret_cast<char*>((*pt.global)[l]) - c->p2p_base);
-          if (c->cfg.agg_mode == GIST_AGG_SYMM) {  // NCCL device API: LSA peer pointers / NVLS multimem
-            PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 4.0 * (2.0 + W), s,
-               scatter_sub_symm(*c->devcomm, c->win, off, mp, w + sh.off, c->symm_mm, s));
-            continue;
-          }
-          PeerDst pd;
-          pd.n = W;
-          for (int r = 0; r < W; ++r) pd.dst[r] = reinterpret_cast<float*>(c->peer_base[r] + off);
-          PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 4.0 * (2.0 + W), s, scatter_sub_peers(pd, mp, w + sh.off, s));
-        }
-      }
-    // barrier 2: every peer's stores into this replica have completed before anything reads it
-    TRY(coll(c, comm_barrier(c->comm, c->barrier_word, s, &c->err)));
-    c->prof_now = false;
-    TRY(check_launch(c, "aggregate"));
-    c->round += 1;
-    c->state = S_PARAMS;
-    return GIST_OK;
-  }
-  for (const Part& pt : parts) {
-    const float* src = pt.local;
-    if (W > 1) {  // subAgg exchange: one all-gather of the packed slot buffers over NVLink
-      const int id = prof_begin(c, s, GIST_PROF_COMM, (double)(W - 1) * c->slots_per_rank * c->S_max * 4.0);
-      TRY(coll(c, comm_allgather(c->comm, pt.local, c->Wrecv, (size_t)c->slots_per_rank * c->S_max * 4, s, &c->err)));
-      prof_end(c, s, id);
-      src = c->Wrecv;
-    }
-    for (int i = 0; i < c->m; ++i) {
-      const int rank = gist_slot_owner(i, W), j = i / W;
-      const float* w = src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
-      if (W == 1) w = pt.local + (size_t)j * c->S_max;
-      for (int l = 0; l < c->L; ++l) {
-        const LayerShape& sh = c->shapes[i][l];
-        LayerMap mp;
-        mp.rows = sh.rows; mp.nrows = sh.nrows; mp.sage = c->arch == GIST_ARCH_SAGE; mp.gat = c->arch == GIST_ARCH_GAT; mp.half = sh.half;
-        mp.glob_half = (int)pad8(c->dims[l]); mp.cols = sh.cols; mp.ncols = sh.ncols; mp.Kp = sh.Kp; mp.Np = sh.Np;
-        mp.ldg = c->th_N[l];
-        PL(GIST_PROF_AGGREGATE, (double)sh.Kp * sh.Np * 12.0, s, scatter_sub((*pt.global)[l], mp, w + sh.off, s));
-      }
-    }
-    if (c->arch == GIST_ARCH_GAT) {  // R21: the last layer's attention rows = mean of the m copies
-      const int l = c->L - 1;
-      MeanRows mr;
-      mr.n = c->m;
-      mr.cols = c->dims[c->L];
-      mr.ld_dst = c->th_N[l];
-      for (int i = 0; i < c->m; ++i) {
-        const int rank = gist_slot_owner(i, W), j = i / W;
-        const float* w = W == 1 ? pt.local + (size_t)j * c->S_max
-                                : src + ((size_t)rank * c->slots_per_rank + j) * c->S_max;
-        const LayerShape& sh = c->shapes[i][l];
-        mr.src[i] = w + sh.off + (int64_t)sh.half * sh.Np;
-        mr.ld_src[i] = sh.Np;
-      }
-      PL(GIST_PROF_AGGREGATE, 2.0 * c->m * mr.cols * 4.0, s,
-         mean_rows((*pt.global)[l] + pad8(c->dims[l]) * c->th_N[l], mr, 2, s));
-    }
-  }
-  c->prof_now = false;
-  TRY(check_launch(c, "aggregate"));
-  c->round += 1;
-  c->state = S_PARAMS;
-  return GIST_OK;
-}
-
-// single GEMM (eval path): FP32 SIMT or BF16 tcgen05
-static gist_status gemm_any(gist_ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
-                            const void* B, int64_t ldb, void* C, int64_t ldc, bool out_f32, bool relu,
-                            cudaStream_t s) {
-  if (c->prec == GIST_PREC_FP32) {
-    gemm_f32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s);
-  } else if (c->prec == GIST_PREC_TF32) {
-    if (!gemm_tf32(ta, tb, M, N, K, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, relu, s))
-      return fail(c, GIST_E_UNSUPPORTED, "tf32 tensor-core GEMM unavailable for this shape");
-  } else if (!gemm_bf16(ta, tb, M, N, K, (const bf16*)A, lda, (const bf16*)B, ldb, C, ldc, out_f32, relu, s)) {
-    return fail(c, GIST_E_UNSUPPORTED, "bf16 tensor-core GEMM unavailable for this shape");
-  }
-  ++c->nk;
-  return GIST_OK;
-}
-
-// The weights of the evaluation forward: per layer the fp32 weights (Theta_l, or a copy with its W
-// rows scaled by 1/m for layers l >= 1 under eval_scale MEAN, R10) and their T-typed GEMM operand
-// (the same pointer in FP32 mode, a bf16 copy in BF16 mode).
-struct EvalWeights {
-  std::vector<float*> w32;
-  std::vector<void*> wT;
-  std::vector<void*> owned;
-};
-template <typename T>
-static gist_status eval_weights(gist_ctx* c, EvalWeights& ew) {
-  cudaStream_t s = c->stream;
-  ew.w32.assign(c->L, nullptr);
-  ew.wT.assign(c->L, nullptr);
-  const bool mean = c->cfg.eval_scale == GIST_EVAL_SCALE_MEAN && c->m > 1;
   for (int l = 0; l < c->L; ++l) {
-    const int64_t n = c->th_K[l] * c->th_N[l];
-    ew.w32[l] = c->theta[l];
-    if (mean && l > 0) {  // hidden input dim d_l is partitioned: scale the W rows (not GAT's a rows)
-      const int64_t nw = (c->arch == GIST_ARCH_GAT ? pad8(c->dims[l]) : c->th_K[l]) * c->th_N[l];
-      float* w = nullptr;
-      TRY(dalloc_t(c, &w, (size_t)n));
-      ew.owned.push_back(w);
-      LK(scale_prefix_f32(c->theta[l], w, n, nw, 1.0f / (float)c->m, s));
-      ew.w32[l] = w;
-    }
-    if (sizeof(T) == 2) {
-      void* b = nullptr;
-      TRY(dalloc(c, &b, (size_t)n * 2));
-      ew.owned.push_back(b);
-      LK(f32_to_bf16(ew.w32[l], (bf16*)b, n, s));
-      ew.wT[l] = b;
-    } else {
-      ew.wT[l] = ew.w32[l];
-    }
+    std::vector<float> w((size_t)wrows(c, c->dims[l]) * c->dims[l + 1]);
+    TRY(gist_get_params(c, l, w.data()));
+    put(w.data(), w.size() * 4);
   }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(c, GIST_E_ARG, std::string("save_checkpoint: cannot open ") + path);
+  const size_t wr = std::fwrite(buf.data(), 1, buf.size(), f);
+  const int cl = std::fclose(f);
+  if (wr != buf.size() || cl != 0) return fail(c, GIST_E_ARG, "save_checkpoint: short write");
   return GIST_OK;
 }
-static void free_eval_weights(gist_ctx* c, EvalWeights& ew) {
-  for (void* p : ew.owned) dfree(c, p);
-  ew.owned.clear();
-}
 
-// GAT forward of the global model over `rows` rows of a CSR without self loops (R21): layer 0
-// reads X0 (ld pad8(d_0)); hidden outputs alternate between bufA / bufB; fp32 logits (ld th_N).
-template <typename T>
-static gist_status gat_forward_rows(gist_ctx* c, int64_t rows, const int64_t* row_beg, const int64_t* row_end,
-                                    const int32_t* col, const T* X0, const EvalWeights& ew, T* bufA, T* bufB,
-                                    T* Z, float* sc, float* logits, cudaStream_t s) {
-  const T* Hin = X0;
-  int64_t ldin = pad8(c->dims[0]);
-  T* Hout = bufA;
+extern "C" gist_status gist_load_checkpoint(gist_ctx* c, const char* path) {
+  PRE(c);
+  if (c->state == S_CREATED || c->state == S_PARTITIONED)
+    return fail(c, GIST_E_STATE, "load_checkpoint: needs a graph and no open round");
+  if (!path) return fail(c, GIST_E_ARG, "load_checkpoint: null path");
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(c, GIST_E_ARG, std::string("load_checkpoint: cannot open ") + path);
+  std::string buf;
+  char tmp[1 << 16];
+  size_t got;
+  while ((got = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.append(tmp, got);
+  std::fclose(f);
+  size_t pos = 0;
+  auto take = [&](void* p, size_t n) {
+    if (pos + n > buf.size()) return false;
+    std::memcpy(p, buf.data() + pos, n);
+    pos += n;
+    return true;
+  };
+  char magic[4];
+  uint32_t version = 0, L = 0;
+  uint8_t arch = 0;
+  if (!take(magic, 4) || std::memcmp(magic, "GIST", 4) != 0 || !take(&version, 4) || version != 1 ||
+      !take(&arch, 1) || !take(&L, 4))
+    return fail(c, GIST_E_ARG, "load_checkpoint: not a GIST checkpoint (magic / version)");
+  if ((int)arch != c->arch || (int)L != c->L) return fail(c, GIST_E_SHAPE, "load_checkpoint: arch or depth differs");
+  for (int l = 0; l <= c->L; ++l) {
+    uint32_t d = 0;
+    if (!take(&d, 4)) return fail(c, GIST_E_ARG, "load_checkpoint: truncated header");
+    if ((int)d != c->dims[l]) return fail(c, GIST_E_SHAPE, "load_checkpoint: dims differ");
+  }
+  std::vector<std::vector<float>> w(c->L);
   for (int l = 0; l < c->L; ++l) {
-    const int64_t K = pad8(c->dims[l]), N = c->th_N[l];
-    TRY(gemm_any(c, false, false, rows, N, K, Hin, ldin, ew.wT[l], N, Z, N, sizeof(T) == 4, false, s));
-    GatGroup<T> G;
-    G.n = 1;
-    GatLayer<T>& a = G.a[0];
-    a.row_beg = row_beg; a.row_end = row_end; a.col = col; a.rows = rows; a.w = N;
-    a.Z = Z; a.ldz = N;
-    a.a_src = ew.w32[l] + K * N; a.a_dst = a.a_src + N;
-    a.s = sc; a.t = sc + rows; a.lse = sc + 2 * rows;
-    a.H = Hin; a.ldh = ldin; a.kw = K; a.W32 = ew.w32[l]; a.ldw = N; a.wa = sc + 3 * rows;
-    if (l + 1 < c->L) { a.out = Hout; a.ldo = N; a.relu = 1; }
-    else { a.out_f32 = logits; a.ldo = N; }
-    LK(gat_scores<T>(G, s));
-    LK(gat_forward<T>(G, s));
-    Hin = Hout;
-    ldin = N;
-    Hout = Hout == bufA ? bufB : bufA;
+    w[l].resize((size_t)wrows(c, c->dims[l]) * c->dims[l + 1]);
+    if (!take(w[l].data(), w[l].size() * 4)) return fail(c, GIST_E_ARG, "load_checkpoint: truncated weights");
   }
-  return GIST_OK;
-}
-
-// ================================================================ eval ====
-// Full-graph forward of the global model (R1/R2 full-graph operator, R10 no scaling).  World > 1
-// (GCN / GraphSAGE): the relabelled rows are cut into W blocks of R = ceil(n / W); rank r
-// computes the SpMM and GEMM of block r of every layer and one all-gather per hidden layer
-// assembles the next layer's input on every rank (its SpMM gathers neighbours from every block);
-// the loss / accuracy sums of the blocks are combined with one sum all-reduce.
-// GAT runs the whole forward on every rank (its attention needs Z = H W of every neighbour row).
-// logits_host (optional): float[n x k] by ORIGINAL node id, assembled on every rank.
-template <typename T>
-static gist_status eval_t(gist_ctx* c, int code, float* loss, float* acc, float* logits_host) {
-  cudaStream_t s = c->stream;
-  const int64_t n = c->n;
-  const bool sage = c->arch == GIST_ARCH_SAGE;
-  const bool gat = c->arch == GIST_ARCH_GAT;
-  const int W = gat ? 1 : c->cfg.world_size;
-  const int rank = gat ? 0 : c->cfg.rank;
-  const int64_t R = cdiv(n, W);
-  const int64_t r0 = std::min<int64_t>(n, (int64_t)rank * R);
-  const int64_t nr = std::min<int64_t>(n, r0 + R) - r0;  // rows of this rank's block
-  const int64_t npad = R * W;
-  const int64_t Nl = c->th_N[c->L - 1];
-  int64_t maxK = 0;
-  for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
-  void *bufA = nullptr, *bufB = nullptr;
-  float* logits = nullptr;
-  double* out3 = nullptr;
-  EvalWeights ew;
-  TRY(eval_weights<T>(c, ew));
-  TRY(dalloc(c, &bufA, (size_t)npad * maxK * sizeof(T)));
-  TRY(dalloc(c, &bufB, (size_t)npad * maxK * sizeof(T)));
-  TRY(dalloc_t(c, &logits, (size_t)npad * Nl));
-  TRY(dalloc_t(c, &out3, 3));
-  T* Cb = (T*)bufA;
-  T* Hn = (T*)bufB;
-  if (gat) {
-    int64_t maxN = 0;
-    for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
-    void* Z = nullptr;
-    float* sc = nullptr;
-    TRY(dalloc(c, &Z, (size_t)n * maxN * sizeof(T)));
-    TRY(dalloc_t(c, &sc, (size_t)3 * std::max<int64_t>(n, 1) + 2 * maxK));
-    TRY(gat_forward_rows<T>(c, n, c->rp, c->rp + 1, c->col, (const T*)c->X, ew, Cb, Hn, (T*)Z, sc, logits, s));
-    CK(cudaStreamSynchronize(s));
-    dfree(c, Z);
-    dfree(c, sc);
-  }
-  for (int l = 0; l < c->L && !gat; ++l) {
-    const int64_t K = c->th_K[l], N = c->th_N[l];
-    const int64_t half = pad8(c->dims[l]);
-    SpmmArgs<T, T> a;
-    a.row_beg = c->rp + r0; a.row_end = c->rp + r0 + 1; a.col = c->col; a.rows = nr;
-    a.row0 = r0; a.h_rows = n;
-    a.rowscale = c->full_scale + r0;
-    const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
-    if (sage) {
-      if (l == 0) { a.self_out = Cb + r0 * K; a.ld_self = K; }
-      a.H = l == 0 ? Hin : Cb; a.ldh = l == 0 ? half : K;
-      a.out = Cb + r0 * K + half; a.ldo = K; a.w = half;
-    } else {
-      a.colscale = c->full_scale; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb + r0 * K; a.ldo = K; a.w = K;
-    }
-    if (nr > 0) LK((spmm<T, T>(a, s)));
-    const void* Wl = ew.wT[l];
-    if (l + 1 < c->L) {
-      // next layer input: GCN H_{l+1} -> Hn; SAGE H_{l+1} -> left half of Hn, which becomes the
-      // next concat buffer (swap)
-      const int64_t Kn = c->th_K[l + 1];
-      if (nr > 0) TRY(gemm_any(c, false, false, nr, N, K, Cb + r0 * K, K, Wl, N, Hn + r0 * Kn, Kn, false, true, s));
-      if (sage) std::swap(Cb, Hn);
-      T* next = sage ? Cb : Hn;  // the buffer the next layer's SpMM gathers from
-      if (W > 1)
-        TRY(coll(c, comm_allgather(c->comm, next + (int64_t)rank * R * Kn, next, (size_t)R * Kn * sizeof(T), s,
-                                   &c->err)));
-    } else if (nr > 0) {
-      TRY(gemm_any(c, false, false, nr, N, K, Cb + r0 * K, K, Wl, N, logits + r0 * N, N, true, false, s));
-    }
-  }
-  CK(cudaMemsetAsync(out3, 0, 3 * sizeof(double), s));
-  if (nr > 0) LK(eval_rows(logits + r0 * Nl, Nl, nr, c->k, c->labels + r0, c->split + r0, code, out3, s));
-  if (W > 1) TRY(coll(c, comm_allreduce_sum(c->comm, out3, 3, true, s, &c->err)));
-  double h[3];
-  CK(cudaMemcpyAsync(h, out3, sizeof(h), cudaMemcpyDeviceToHost, s));
-  if (logits_host) {
-    if (W > 1)
-      TRY(coll(c, comm_allgather(c->comm, logits + (int64_t)rank * R * Nl, logits, (size_t)R * Nl * 4, s, &c->err)));
-    std::vector<float> lg((size_t)n * Nl);
-    CK(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int64_t g = 0; g < n; ++g)
-      std::memcpy(logits_host + (size_t)c->perm_h[g] * c->k, lg.data() + (size_t)g * Nl, (size_t)c->k * 4);
-    c->d2h += (int64_t)n * Nl * 4;
-  }
-  CK(cudaStreamSynchronize(s));
-  TRY(check_launch(c, "eval"));
-  if (loss) *loss = h[2] > 0 ? (float)(h[0] / h[2]) : 0.f;
-  if (acc) *acc = h[2] > 0 ? (float)(h[1] / h[2]) : 0.f;
-  dfree(c, bufA);
-  dfree(c, bufB);
-  dfree(c, logits);
-  dfree(c, out3);
-  free_eval_weights(c, ew);
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_eval(gist_ctx* c, int32_t split_code, float* loss, float* acc) {
-  PRE(c);
-  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval: needs params and no open round");
-  if (split_code < 0 || split_code > 3) return fail(c, GIST_E_ARG, "eval: split code not in 0..3");
-  if (c->prec == GIST_PREC_BF16) return eval_t<bf16>(c, split_code, loss, acc, nullptr);
-  return eval_t<float>(c, split_code, loss, acc, nullptr);
-}
-
-// ==================================================== partition-wise eval (R20) ===
-// for wide models the global model is evaluated partition by partition.
-// Every partition is a closed subgraph (cut edges dropped), so the local partitions of this
-// rank are laid out contiguously (partition order) and processed in row chunks of whole
-// partitions: per layer one SpMM over the chunk's partition-induced CSR (layer 0 reads X
-// through a row index, no copy) and one GEMM, all buffers chunk-sized.  World > 1:
-// partition p is evaluated by rank p mod W and the per-partition sums are all-reduced.
-template <typename T>
-static gist_status eval_parts_t(gist_ctx* c, int code, const std::vector<int32_t>& part, int np, int64_t max_rows,
-                                std::vector<double>& sums, float* logits_host) {
-  cudaStream_t s = c->stream;
-  const int64_t n = c->n;
-  const bool sage = c->arch == GIST_ARCH_SAGE;
-  const int W = c->cfg.world_size, rank = c->cfg.rank;
-  // local partitions (p mod W == rank) in partition order, nodes ascending (internal ids)
-  std::vector<int64_t> cnt(np + 1, 0);
-  for (int64_t g = 0; g < n; ++g) ++cnt[part[g] + 1];
-  std::vector<int32_t> lparts;
-  for (int p = rank; p < np; p += W) lparts.push_back(p);
-  const int nlp = (int)lparts.size();
-  std::vector<int64_t> lbeg(nlp + 1, 0);
-  std::vector<int64_t> fill(np, -1);
-  for (int j = 0; j < nlp; ++j) {
-    fill[lparts[j]] = lbeg[j];
-    lbeg[j + 1] = lbeg[j] + cnt[lparts[j] + 1];
-  }
-  const int64_t nl = lbeg[nlp];
-  std::vector<int32_t> pnode(std::max<int64_t>(nl, 1)), pos(n, -1), rowbase(std::max<int64_t>(nl, 1));
-  for (int64_t g = 0; g < n; ++g) {
-    const int p = part[g];
-    if (fill[p] < 0) continue;
-    pos[g] = (int32_t)fill[p];
-    pnode[fill[p]++] = (int32_t)g;
-  }
-  // buffers and chunking
-  int64_t maxK = 0;
-  for (int l = 0; l < c->L; ++l) maxK = std::max(maxK, c->th_K[l]);
-  const int64_t Nl = c->th_N[c->L - 1];
-  EvalWeights ew;
-  TRY(eval_weights<T>(c, ew));
-  const int64_t row_bytes = 2 * maxK * (int64_t)sizeof(T) + Nl * 4;
-  if (max_rows <= 0) {
-    size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot));
-    max_rows = std::max<int64_t>(1, (int64_t)(fr / 2) / row_bytes);
-  }
-  std::vector<int> chunk_first{0};  // chunk j = local partitions chunk_first[j] .. chunk_first[j+1]
-  for (int j = 0; j < nlp; ++j) {
-    const int f = chunk_first.back();
-    if (j > f && lbeg[j + 1] - lbeg[f] > max_rows) chunk_first.push_back(j);
-  }
-  chunk_first.push_back(nlp);
-  int64_t max_chunk = 0;
-  for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
-    const int64_t k0 = lbeg[chunk_first[j]], k1 = lbeg[chunk_first[j + 1]];
-    max_chunk = std::max(max_chunk, k1 - k0);
-    for (int64_t r = k0; r < k1; ++r) rowbase[r] = (int32_t)k0;
-  }
-  // partition-induced CSR (device)
-  int32_t *pnode_d = nullptr, *pos_d = nullptr, *part_d = nullptr, *rb_d = nullptr, *pcol = nullptr;
-  int64_t *deg = nullptr, *prp = nullptr, *lbeg_d = nullptr;
-  float* pscale = nullptr;
-  double* out3 = nullptr;
-  TRY(dalloc_t(c, &pnode_d, std::max<int64_t>(nl, 1)));
-  TRY(dalloc_t(c, &pos_d, n));
-  TRY(dalloc_t(c, &part_d, n));
-  TRY(dalloc_t(c, &rb_d, std::max<int64_t>(nl, 1)));
-  TRY(dalloc_t(c, &deg, nl + 1));
-  TRY(dalloc_t(c, &prp, nl + 1));
-  TRY(dalloc_t(c, &lbeg_d, nlp + 1));
-  TRY(dalloc_t(c, &pscale, std::max<int64_t>(nl, 1)));
-  TRY(dalloc_t(c, &out3, 3 * (size_t)std::max(nlp, 1)));
-  CK(cudaMemcpyAsync(pnode_d, pnode.data(), nl * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(pos_d, pos.data(), n * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(part_d, part.data(), n * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(rb_d, rowbase.data(), nl * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(lbeg_d, lbeg.data(), (nlp + 1) * 8, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(deg, 0, (nl + 1) * 8, s));
-  LK(part_count(c->rp, c->col, pnode_d, part_d, nl, deg, s));
-  {
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, prp, nl + 1, s);
-    void* tmp = nullptr;
-    TRY(dalloc(c, &tmp, tb));
-    cub::DeviceScan::ExclusiveSum(tmp, tb, deg, prp, nl + 1, s);
-    ++c->nk;
-    CK(cudaStreamSynchronize(s));
-    dfree(c, tmp);
-  }
-  int64_t pnnz = 0;
-  CK(cudaMemcpy(&pnnz, prp + nl, 8, cudaMemcpyDeviceToHost));
-  TRY(dalloc_t(c, &pcol, std::max<int64_t>(pnnz, 1)));
-  LK(part_fill(c->rp, c->col, pnode_d, pos_d, part_d, rb_d, prp, nl, pcol, s));
-  LK(full_graph_scales(prp, nl, c->arch, pscale, s));
-  void *bufA = nullptr, *bufB = nullptr;
-  float* logits = nullptr;
-  TRY(dalloc(c, &bufA, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
-  TRY(dalloc(c, &bufB, (size_t)std::max<int64_t>(max_chunk, 1) * maxK * sizeof(T)));
-  TRY(dalloc_t(c, &logits, (size_t)std::max<int64_t>(max_chunk, 1) * Nl));
-  void *gX = nullptr, *gZ = nullptr;
-  float* gsc = nullptr;
-  if (c->arch == GIST_ARCH_GAT) {
-    int64_t maxN = 0;
-    for (int l = 0; l < c->L; ++l) maxN = std::max(maxN, c->th_N[l]);
-    TRY(dalloc(c, &gX, (size_t)std::max<int64_t>(max_chunk, 1) * pad8(c->dims[0]) * sizeof(T)));
-    TRY(dalloc(c, &gZ, (size_t)std::max<int64_t>(max_chunk, 1) * maxN * sizeof(T)));
-    TRY(dalloc_t(c, &gsc, (size_t)3 * std::max<int64_t>(max_chunk, 1) + 2 * maxK));
-  }
-  for (size_t j = 0; j + 1 < chunk_first.size(); ++j) {
-    const int f = chunk_first[j], e = chunk_first[j + 1];
-    const int64_t k0 = lbeg[f], rows = lbeg[e] - k0;
-    if (rows == 0) continue;
-    T* Cb = (T*)bufA;
-    T* Hn = (T*)bufB;
-    if (c->arch == GIST_ARCH_GAT) {  // X rows of the chunk gathered, then the GAT layers
-      const int64_t d0p = pad8(c->dims[0]);
-      LK(gather_rows_t<T>((const T*)c->X, d0p, pnode_d + k0, rows, d0p, (T*)gX, d0p, s));
-      TRY(gat_forward_rows<T>(c, rows, prp + k0, prp + k0 + 1, pcol, (const T*)gX, ew, Cb, Hn, (T*)gZ, gsc, logits,
-                              s));
-    }
-    for (int l = 0; l < c->L && c->arch != GIST_ARCH_GAT; ++l) {
-      const int64_t K = c->th_K[l], N = c->th_N[l];
-      const int64_t half = pad8(c->dims[l]);
-      SpmmArgs<T, T> a;
-      a.row_beg = prp + k0; a.row_end = prp + k0 + 1; a.col = pcol; a.rows = rows; a.rowscale = pscale + k0;
-      const T* Hin = l == 0 ? (const T*)c->X : (const T*)Hn;
-      if (l == 0) a.h_index = pnode_d + k0;  // chunk row -> internal node id (rows of X)
-      if (sage) {
-        if (l == 0) { a.self_out = Cb; a.ld_self = K; }
-        a.H = l == 0 ? Hin : Cb; a.ldh = l == 0 ? half : K;
-        a.out = Cb + half; a.ldo = K; a.w = half;
-      } else {
-        a.colscale = pscale + k0; a.self = 1; a.H = Hin; a.ldh = half; a.out = Cb; a.ldo = K; a.w = K;
-      }
-      LK((spmm<T, T>(a, s)));
-      const void* Wl = ew.wT[l];
-      if (l + 1 < c->L) {
-        TRY(gemm_any(c, false, false, rows, N, K, Cb, K, Wl, N, Hn, c->th_K[l + 1], false, true, s));
-        if (sage) std::swap(Cb, Hn);
-      } else {
-        TRY(gemm_any(c, false, false, rows, N, K, Cb, K, Wl, N, logits, N, true, false, s));
-      }
-    }
-    LK(eval_parts(logits, Nl, c->k, lbeg_d + f, k0, e - f, pnode_d, c->labels, c->split, code, out3 + 3 * f, s));
-    if (logits_host) {  // parity hook: chunk logits -> host rows of their nodes (internal ids)
-      std::vector<float> lg((size_t)rows * Nl);
-      CK(cudaMemcpyAsync(lg.data(), logits, lg.size() * 4, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      for (int64_t i = 0; i < rows; ++i)
-        std::memcpy(logits_host + (size_t)pnode[k0 + i] * c->k, lg.data() + (size_t)i * Nl, (size_t)c->k * 4);
-    }
-  }
-  std::vector<double> loc(3 * (size_t)std::max(nlp, 1));
-  CK(cudaMemcpyAsync(loc.data(), out3, loc.size() * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  TRY(check_launch(c, "eval_parts"));
-  sums.assign(3 * (size_t)np, 0.0);
-  for (int j = 0; j < nlp; ++j)
-    for (int q = 0; q < 3; ++q) sums[3 * (size_t)lparts[j] + q] = loc[3 * (size_t)j + q];
-  if (W > 1) {  // every partition was evaluated by exactly one rank: a sum-all-reduce assembles them
-    double* red = nullptr;
-    TRY(dalloc_t(c, &red, sums.size()));
-    CK(cudaMemcpyAsync(red, sums.data(), sums.size() * 8, cudaMemcpyHostToDevice, s));
-    TRY(coll(c, comm_allreduce_sum(c->comm, red, sums.size(), true, s, &c->err)));
-    CK(cudaMemcpyAsync(sums.data(), red, sums.size() * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    dfree(c, red);
-    if (logits_host) {  // every node's row was written by exactly one rank, zeros elsewhere: exact sum
-      float* lr = nullptr;
-      TRY(dalloc_t(c, &lr, (size_t)n * c->k));
-      CK(cudaMemcpyAsync(lr, logits_host, (size_t)n * c->k * 4, cudaMemcpyHostToDevice, s));
-      TRY(coll(c, comm_allreduce_sum(c->comm, lr, (size_t)n * c->k, false, s, &c->err)));
-      CK(cudaMemcpyAsync(logits_host, lr, (size_t)n * c->k * 4, cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      dfree(c, lr);
-    }
-  }
-  free_eval_weights(c, ew);
-  for (void* p : {gX, gZ, (void*)gsc}) if (p) dfree(c, p);
-  for (void* p : {(void*)pnode_d, (void*)pos_d, (void*)part_d, (void*)rb_d, (void*)pcol, (void*)deg, (void*)prp,
-                  (void*)lbeg_d, (void*)pscale, (void*)out3, bufA, bufB, (void*)logits})
-    dfree(c, p);
-  return GIST_OK;
-}
-
-// partition of every internal node id from the caller's ids (original ids), or the training clusters
-static gist_status resolve_parts(gist_ctx* c, const int32_t* part_ids, int32_t num_parts, std::vector<int32_t>& part,
-                                 int* np) {
-  const int64_t n = c->n;
-  part.assign(n, 0);
-  *np = num_parts;
-  if (part_ids) {
-    if (num_parts < 1) return fail(c, GIST_E_ARG, "eval_parts: num_parts < 1");
-    for (int64_t g = 0; g < n; ++g) {
-      const int32_t p = part_ids[c->perm_h[g]];
-      if (p < 0 || p >= num_parts) return fail(c, GIST_E_ARG, "eval_parts: partition id out of range");
-      part[g] = p;
-    }
-  } else {  // the training clusters (contiguous internal id ranges after relabelling)
-    *np = (int)c->cstart_h.size() - 1;
-    if (num_parts != 0 && num_parts != *np) return fail(c, GIST_E_ARG, "eval_parts: num_parts != clusters");
-    for (int p = 0; p < *np; ++p)
-      for (int64_t g = c->cstart_h[p]; g < c->cstart_h[p + 1]; ++g) part[g] = p;
-  }
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_eval_parts(gist_ctx* c, int32_t split_code, const int32_t* part_ids, int32_t num_parts,
-                                       int64_t max_rows, float* loss, float* acc, float* part_loss,
-                                       float* part_acc) {
-  PRE(c);
-  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_parts: needs params and no open round");
-  if (split_code < 0 || split_code > 3) return fail(c, GIST_E_ARG, "eval_parts: split code not in 0..3");
-  std::vector<int32_t> part;
-  int np = 0;
-  TRY(resolve_parts(c, part_ids, num_parts, part, &np));
-  std::vector<double> sums;
-  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, split_code, part, np, max_rows, sums, nullptr)
-                                : eval_parts_t<float>(c, split_code, part, np, max_rows, sums, nullptr));
-  double ls = 0.0, as = 0.0;
-  int cntp = 0;
-  for (int p = 0; p < np; ++p) {
-    const double k = sums[3 * (size_t)p + 2];
-    const float lp = k > 0 ? (float)(sums[3 * (size_t)p] / k) : NAN;
-    const float ap = k > 0 ? (float)(sums[3 * (size_t)p + 1] / k) : NAN;
-    if (part_loss) part_loss[p] = lp;
-    if (part_acc) part_acc[p] = ap;
-    if (k > 0) ls += sums[3 * (size_t)p] / k, as += sums[3 * (size_t)p + 1] / k, ++cntp;
-  }
-  if (loss) *loss = cntp ? (float)(ls / cntp) : 0.f;
-  if (acc) *acc = cntp ? (float)(as / cntp) : 0.f;
-  return GIST_OK;
-}
-
-extern "C" gist_status gist_eval_logits(gist_ctx* c, int32_t mode, const int32_t* part_ids, int32_t num_parts,
-                                        int64_t max_rows, float* out) {
-  PRE(c);
-  if (c->state != S_PARAMS) return fail(c, GIST_E_STATE, "eval_logits: needs params and no open round");
-  if (!out || (mode != 0 && mode != 1)) return fail(c, GIST_E_ARG, "eval_logits: mode not 0/1 or null output");
-  if (mode == 0)
-    return c->prec == GIST_PREC_BF16 ? eval_t<bf16>(c, 0, nullptr, nullptr, out) : eval_t<float>(c, 0, nullptr, nullptr, out);
-  std::vector<int32_t> part;
-  int np = 0;
-  TRY(resolve_parts(c, part_ids, num_parts, part, &np));
-  // internal-id rows, then the original-id order of the output
-  std::vector<float> li((size_t)c->n * c->k, 0.f);
-  std::vector<double> sums;
-  TRY(c->prec == GIST_PREC_BF16 ? eval_parts_t<bf16>(c, 0, part, np, max_rows, sums, li.data())
-                                : eval_parts_t<float>(c, 0, part, np, max_rows, sums, li.data()));
-  for (int64_t g = 0; g < c->n; ++g)
-    std::memcpy(out + (size_t)c->perm_h[g] * c->k, li.data() + (size_t)g * c->k, (size_t)c->k * 4);
+  if (pos != buf.size()) return fail(c, GIST_E_ARG, "load_checkpoint: trailing bytes");
+  for (int l = 0; l < c->L; ++l) TRY(gist_set_params(c, l, w[l].data()));
   return GIST_OK;
 }
 

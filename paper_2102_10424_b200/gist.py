@@ -30,6 +30,7 @@ EXPORTS = [
     "gist_stream", "gist_last_error", "gist_status_str", "gist_destroy", "gist_spmm", "gist_gemm",
     "gist_profile", "gist_profile_get", "gist_nccl_unique_id", "gist_slot_owner", "gist_slots_per_rank",
     "gist_eval_logits", "gist_loopback_create", "gist_loopback_destroy", "gist_gemm_reps",
+    "gist_save_checkpoint", "gist_load_checkpoint",
 ]
 PROF_CLASSES = ["batch", "spmm", "gemm", "loss", "optim", "partition", "aggregate", "agg_tc", "comm"]
 
@@ -94,6 +95,8 @@ def lib() -> C.CDLL:
         "gist_eval_logits": (i32, [vp, i32, vp, i32, i64, vp]),
         "gist_loopback_create": (i32, [i32, P(vp)]),
         "gist_loopback_destroy": (None, [vp]),
+        "gist_save_checkpoint": (i32, [vp, C.c_char_p]),
+        "gist_load_checkpoint": (i32, [vp, C.c_char_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -227,6 +230,12 @@ class Gist:
         self._check(lib().gist_eval_logits(self.h, mode, _ptr(part_ids) if part_ids is not None else None,
                                            int(num_parts) if part_ids is not None else 0, max_rows, _ptr(out)))
         return out
+
+    def save_checkpoint(self, path: str):
+        self._check(lib().gist_save_checkpoint(self.h, os.fsencode(path)))
+
+    def load_checkpoint(self, path: str):
+        self._check(lib().gist_load_checkpoint(self.h, os.fsencode(path)))
 
     def param_shape(self, layer: int):
         d = self.dims[layer]
