@@ -38,60 +38,15 @@ __device__ __forceinline__ void unpack(const uint4& x, float* v, bf16) {
   }
 }
 
-template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE, bool PRED = false>
-__global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && sizeof(TI) == 2) ? 4
-                                           : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
-    k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks) {
-  pdl_wait();
-  pdl_trigger();
-  const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
-  constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
-  constexpr int GPW = 32 / LPR;      // groups per warp
-  using Off = typename std::conditional<WIDE, int64_t, uint32_t>::type;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane % LPR;         // lane inside the group
-  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane - gl));
-  const int64_t gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LPR;
-  const int64_t v = gid / nchunks;
-  const int chunk = (int)(gid - v * nchunks);
-  if (v >= a.rows) return;           // whole group exits together
-  // inert dummy rows of a batch launch (v >= n_b, marked row_beg < 0 by the batch build):
-  // exact zeros, never a stale `add`
-  const int64_t beg = a.row_beg[v], end = a.row_end[v];
-  const bool dummy = beg < 0;
-  const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
-  const Off ldv = (Off)(a.ldh / V);  // row stride in 16-byte vectors
-  const int64_t wv = a.w / V;        // width in vectors
-  const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
-
-  float acc[J][V];
-#pragma unroll
-  for (int j = 0; j < J; ++j)
-#pragma unroll
-    for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
-  bool act[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) act[j] = vbase + j * LPR < wv;
-
-  const Off hv = (Off)(a.h_index ? (int64_t)a.h_index[v] : v + a.row0) * ldv;
-  if (a.self || a.self_out) {
-    const float s = a.colscale ? a.colscale[v + a.row0] : 1.f;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      if (!act[j]) continue;
-      const uint4 x = H4[hv + vbase + j * LPR];
-      if (a.self_out) *reinterpret_cast<uint4*>(a.self_out + v * a.ld_self + (int64_t)(vbase + j * LPR) * V) = x;
-      if (a.self) {
-        float t[V];
-        unpack(x, t, TI());
-#pragma unroll
-        for (int i = 0; i < V; ++i) acc[j][i] = s * t[i];
-      }
-    }
-  }
-
-  for (int64_t base = beg; base < end; base += LPR) {
-    const int n = (end - base) < LPR ? (int)(end - base) : LPR;
+// Sum of the neighbour rows col[b .. e) of one (row, column chunk) unit into acc, in edge order
+// (UNROLL gathers per round; PRED: every round predicated, no serial tail -- same order).
+template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool PRED, typename Off>
+__device__ __forceinline__ void gather_range(const SpmmArgs<TI, TO>& a, int64_t b, int64_t e, const uint4* H4, Off ldv,
+                                             int vbase, const bool (&act)[J], unsigned gmask, int gl,
+                                             float (&acc)[J][Elem<TI>::kVec]) {
+  constexpr int V = Elem<TI>::kVec;
+  for (int64_t base = b; base < e; base += LPR) {
+    const int n = (e - base) < LPR ? (int)(e - base) : LPR;
     Off ou = 0;
     float su = 1.f;
     if (gl < n) {
@@ -161,60 +116,193 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
       }
     }
   }
-  const float rs = a.rowscale ? a.rowscale[v] : 1.f;
+}
+
+// Heavy rows (split_min > 0: a unit whose row has more than split_min neighbours): the row's
+// dependency chain would set the launch length (the degree tail of a batch: ~1% of the rows hold
+// 5-20x the mean neighbour count), so after the light rows the whole CTA takes each heavy unit
+// of its range in turn -- group g sums the g-th contiguous slice of the edge list, the slices
+// meet in shared memory and the unit's own group adds them in slice order.  The split depends
+// only on the row's degree, so the result is deterministic and independent of the launch shape
+// (grouped or single-slot, any world size).  Dynamic shared memory: 256 * J * V floats.
+template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE, bool PRED = false>
+__global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && sizeof(TI) == 2) ? 4
+                                           : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
+    k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks, int split_min) {
+  pdl_wait();
+  pdl_trigger();
+  const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
+  constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
+  constexpr int GPW = 32 / LPR;      // groups per warp
+  constexpr int NG = 8 * GPW;        // groups per CTA (256 threads)
+  using Off = typename std::conditional<WIDE, int64_t, uint32_t>::type;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % LPR;         // lane inside the group
+  const int grp = (threadIdx.x >> 5) * GPW + lane / LPR;  // group inside the CTA
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane - gl));
+  const int64_t gid = (int64_t)blockIdx.x * NG + grp;
+  const uint4* __restrict__ H4 = reinterpret_cast<const uint4*>(a.H);
+  const Off ldv = (Off)(a.ldh / V);  // row stride in 16-byte vectors
+  const int64_t wv = a.w / V;        // width in vectors
+
+  // self term (and the copy of the row into self_out) of unit (v, vbase)
+  auto self_term = [&](int64_t v, int vbase, const bool(&act)[J], float(&acc)[J][V]) {
+    if (!(a.self || a.self_out)) return;
+    const Off hv = (Off)(a.h_index ? (int64_t)a.h_index[v] : v + a.row0) * ldv;
+    const float s = a.colscale ? a.colscale[v + a.row0] : 1.f;
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-    if (!act[j]) continue;
-    const int64_t c = (int64_t)(vbase + j * LPR) * V;
-    float o[V];
+    for (int j = 0; j < J; ++j) {
+      if (!act[j]) continue;
+      const uint4 x = H4[hv + vbase + j * LPR];
+      if (a.self_out) *reinterpret_cast<uint4*>(a.self_out + v * a.ld_self + (int64_t)(vbase + j * LPR) * V) = x;
+      if (a.self) {
+        float t[V];
+        unpack(x, t, TI());
 #pragma unroll
-    for (int i = 0; i < V; ++i) o[i] = acc[j][i] * rs;
-    if (dummy) {
-#pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = 0.f;
-    } else {
-    if (a.add) {
-      float t[V];
-      unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
-#pragma unroll
-      for (int i = 0; i < V; ++i) o[i] += t[i];
+        for (int i = 0; i < V; ++i) acc[j][i] = s * t[i];
+      }
     }
-    if (a.mbits) {  // bit-packed ReLU mask: 4 bytes per 32 columns instead of 2-4 bytes per column
-      const uint32_t wd = a.mbits[v * a.ld_mbits + (c >> 5)] >> (c & 31);
+  };
+  // row scale, residual add, ReLU mask / ReLU and the store of unit (v, vbase)
+  auto epilogue = [&](int64_t v, int vbase, const bool(&act)[J], float(&acc)[J][V], bool dummy) {
+    const float rs = a.rowscale ? a.rowscale[v] : 1.f;
 #pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = (wd >> i) & 1u ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
-    } else if (a.mask) {
-      float t[V];
-      unpack(*reinterpret_cast<const uint4*>(a.mask + v * a.ld_mask + c), t, TI());
+    for (int j = 0; j < J; ++j) {
+      if (!act[j]) continue;
+      const int64_t c = (int64_t)(vbase + j * LPR) * V;
+      float o[V];
 #pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = t[i] > 0.f ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
-    }
-    if (a.relu) {
+      for (int i = 0; i < V; ++i) o[i] = acc[j][i] * rs;
+      if (dummy) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) o[i] = fmaxf(o[i], 0.f);
-    }
-    }
-    if constexpr (sizeof(TO) == sizeof(TI)) {
-      st16(a.out + v * a.ldo + c, o);
-    } else {
-      constexpr int VO = Elem<TO>::kVec;
+        for (int i = 0; i < V; ++i) o[i] = 0.f;
+      } else {
+        if (a.add) {
+          float t[V];
+          unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
 #pragma unroll
-      for (int p = 0; p < V / VO; ++p) st16(a.out + v * a.ldo + c + p * VO, o + p * VO);
+          for (int i = 0; i < V; ++i) o[i] += t[i];
+        }
+        if (a.mbits) {  // bit-packed ReLU mask: 4 bytes per 32 columns instead of 2-4 bytes per column
+          const uint32_t wd = a.mbits[v * a.ld_mbits + (c >> 5)] >> (c & 31);
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = (wd >> i) & 1u ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
+        } else if (a.mask) {
+          float t[V];
+          unpack(*reinterpret_cast<const uint4*>(a.mask + v * a.ld_mask + c), t, TI());
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = t[i] > 0.f ? o[i] : 0.f;  // ReLU'(0) = 0 (R3)
+        }
+        if (a.relu) {
+#pragma unroll
+          for (int i = 0; i < V; ++i) o[i] = fmaxf(o[i], 0.f);
+        }
+      }
+      if constexpr (sizeof(TO) == sizeof(TI)) {
+        st16(a.out + v * a.ldo + c, o);
+      } else {
+        constexpr int VO = Elem<TO>::kVec;
+#pragma unroll
+        for (int p = 0; p < V / VO; ++p) st16(a.out + v * a.ldo + c + p * VO, o + p * VO);
+      }
     }
+  };
+
+  const int64_t v = gid / nchunks;
+  const int chunk = (int)(gid - v * nchunks);
+  const bool valid = v < a.rows;
+  int64_t beg = 0, end = 0;
+  if (valid) {
+    beg = a.row_beg[v];
+    end = a.row_end[v];
+  }
+  // inert dummy rows of a batch launch (v >= n_b, marked row_beg < 0 by the batch build):
+  // exact zeros, never a stale `add`
+  const bool dummy = beg < 0;
+  const bool heavy = split_min > 0 && valid && !dummy && end - beg > split_min;
+  if (valid && !heavy) {
+    const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
+    bool act[J];
+    float acc[J][V];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      act[j] = vbase + j * LPR < wv;
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+    }
+    self_term(v, vbase, act, acc);
+    gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, beg, end, H4, ldv, vbase, act, gmask, gl, acc);
+    epilogue(v, vbase, act, acc, dummy);
+  }
+  if (split_min <= 0) return;  // uniform over the launch
+  __shared__ uint8_t hflag[NG];
+  if (gl == 0) hflag[grp] = heavy;
+  if (!__syncthreads_or(heavy)) return;
+  extern __shared__ float4 spart[];  // [NG][LPR * J] vectors of V floats (V / 4 float4 each)
+  for (int h = 0; h < NG; ++h) {
+    if (!hflag[h]) continue;  // uniform over the CTA
+    const int64_t gh = (int64_t)blockIdx.x * NG + h;
+    const int64_t vh = gh / nchunks;
+    const int ch = (int)(gh - vh * nchunks);
+    const int64_t bh = a.row_beg[vh], n = a.row_end[vh] - bh;
+    const int64_t per = (n + NG - 1) / NG;
+    const int64_t b0 = bh + (grp * per < n ? grp * per : n);
+    const int64_t b1 = bh + ((grp + 1) * per < n ? (grp + 1) * per : n);
+    const int vbase = ch * LPR * J + gl;
+    bool act[J];
+    float acc[J][V];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      act[j] = vbase + j * LPR < wv;
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+    }
+    if (grp == 0) self_term(vh, vbase, act, acc);
+    gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, b0, b1, H4, ldv, vbase, act, gmask, gl, acc);
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+#pragma unroll
+      for (int i = 0; i < V; i += 4)
+        spart[((int64_t)grp * LPR * J + j * LPR + gl) * (V / 4) + i / 4] =
+            make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+    __syncthreads();
+    if (grp == h) {
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+      for (int g = 0; g < NG; ++g)  // slice order
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+#pragma unroll
+          for (int i = 0; i < V; i += 4) {
+            const float4 p = spart[((int64_t)g * LPR * J + j * LPR + gl) * (V / 4) + i / 4];
+            acc[j][i] += p.x; acc[j][i + 1] += p.y; acc[j][i + 2] += p.z; acc[j][i + 3] += p.w;
+          }
+      epilogue(vh, vbase, act, acc, false);
+    }
+    __syncthreads();
   }
 }
 
 template <typename TI, typename TO, int LPR, int J>
 void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s) {
   constexpr int CW = LPR * J * Elem<TI>::kVec;
+  // heavy-row split for mini-batch passes (see k_spmm); the threshold depends only on the pass
+  // kind, never on the launch shape
+  // (GIST_SPMM_SPLIT=0: no split -- the A/B and test switch that pins the split against the
+  // unsplit row sums)
+  const char* e_split = std::getenv("GIST_SPMM_SPLIT");
+  const int split_min = e_split && e_split[0] == '0' ? 0 : (G.a[0].desc ? (G.a[0].few_nnz ? 32 : 128) : 0);
+  const size_t sm = split_min > 0 ? (size_t)256 * J * Elem<TI>::kVec * sizeof(float) : 0;
   const int nchunks = (int)cdiv(w, CW);
   const int64_t groups = rows * nchunks;
   const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
   if (G.a[0].few_nnz && J == 1 && !G.a[0].colscale) {  // few neighbours, narrow rows: the row's
     // dependency chain dominates (not bytes), so every round keeps 8 gathers in flight
     const bool wide = G.a[0].h_index != nullptr;
-    if (wide) launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, true, true>, grid, 256, 0, s, G, nchunks);
-    else launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, false, true>, grid, 256, 0, s, G, nchunks);
+    if (wide) launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, true, true>, grid, 256, sm, s, G, nchunks, split_min);
+    else launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, false, true>, grid, 256, sm, s, G, nchunks, split_min);
     return;
   }
   if (G.a[0].few_nnz && J <= 3 && !G.a[0].colscale && rows * G.n <= 16384) {
@@ -223,18 +311,18 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     // degree tail sets the launch length)
     constexpr int UF = J == 1 ? 8 : (J == 2 ? 4 : 2);
     const bool wide = G.a[0].h_index != nullptr;
-    if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, true, true>, grid, 256, 0, s, G, nchunks);
-    else launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, false, true>, grid, 256, 0, s, G, nchunks);
+    if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, true, true>, grid, 256, sm, s, G, nchunks, split_min);
+    else launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, false, true>, grid, 256, sm, s, G, nchunks, split_min);
     return;
   }
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
     const bool wide = G.a[0].h_index != nullptr;
     if (G.a[0].colscale) {
-      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, true>, grid, 256, 0, s, G, nchunks);
-      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, false>, grid, 256, 0, s, G, nchunks);
+      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, true>, grid, 256, sm, s, G, nchunks, split_min);
+      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, false>, grid, 256, sm, s, G, nchunks, split_min);
     } else {
-      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, true>, grid, 256, 0, s, G, nchunks);
-      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, false>, grid, 256, 0, s, G, nchunks);
+      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, true>, grid, 256, sm, s, G, nchunks, split_min);
+      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, false>, grid, 256, sm, s, G, nchunks, split_min);
     }
     return;
   }
@@ -246,10 +334,10 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     const int64_t hr = a.h_rows > a.rows + a.row0 ? a.h_rows : a.rows + a.row0;
     wide |= a.h_index != nullptr || hr * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
   }
-  if (!wide && cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, false>, grid, 256, 0, s, G, nchunks);
-  else if (!wide) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, false>, grid, 256, 0, s, G, nchunks);
-  else if (cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, true>, grid, 256, 0, s, G, nchunks);
-  else launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, true>, grid, 256, 0, s, G, nchunks);
+  if (!wide && cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, false>, grid, 256, sm, s, G, nchunks, split_min);
+  else if (!wide) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, false>, grid, 256, sm, s, G, nchunks, split_min);
+  else if (cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, true>, grid, 256, sm, s, G, nchunks, split_min);
+  else launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, true>, grid, 256, sm, s, G, nchunks, split_min);
 }
 
 }  // namespace
