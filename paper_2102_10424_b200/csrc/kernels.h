@@ -49,6 +49,9 @@ struct SpmmArgs {
   const StepState* st = nullptr;
   int q = 0;
   int few_nnz = 0;  // hint: rows have few neighbours (inter-cluster pass): favour occupancy
+  // every operand except `add` was written two or more launches back (the inter-cluster pass
+  // after its block-diagonal pass): gather before waiting on the predecessor (k_spmm)
+  int early = 0;
 };
 template <typename TI, typename TO> void spmm(const SpmmArgs<TI, TO>& a, cudaStream_t s);
 

@@ -192,7 +192,7 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           a.rowscale = sl.scale; a.H = (const T*)P; a.ldh = Np; a.w = Np; a.out = (T*)AGG; a.ldo = Np;
           if (bd) {
             fb.push_back(BdOp{P, Np, (int64_t)nb, Np, (void*)AGG, Np, nullptr, 0, sl.scale, sl.desc_dev, 0, 1});
-            a.add = (const T*)AGG; a.ld_add = Np; a.few_nnz = 1;
+            a.add = (const T*)AGG; a.ld_add = Np; a.few_nnz = 1; a.early = 1;
           }
           g.ra_fby += spmm_bytes(a);
           // backward: Q = N^T dZ into DQ[:, Np:2Np) (dZ in DQ[:, 0:Np) from the loss kernel)
@@ -204,7 +204,7 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           if (bd) {  // N^T = A diag(1/deg): aggregate DZs = dZ / deg (written by the loss kernel)
             bb.push_back(BdOp{DZs, 2 * Np, (int64_t)nb, Np, (void*)(DQ + Np), 2 * Np, nullptr, 0, nullptr, sl.desc_dev, 0, 1});
             b.H = (const T*)DZs; b.ldh = 2 * Np;
-            b.add = (const T*)(DQ + Np); b.ld_add = 2 * Np; b.few_nnz = 1;
+            b.add = (const T*)(DQ + Np); b.ld_add = 2 * Np; b.few_nnz = 1; b.early = 1;
           } else {
             b.colscale = sl.scale; b.H = (const T*)DQ; b.ldh = 2 * Np;
           }
@@ -286,6 +286,7 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
                              sl.scale, sl.desc_dev, 0, /*keep_out*/ 1});
           a.add = C + sh.half; a.ld_add = sh.Kp;
           a.few_nnz = 1;
+          a.early = 1;
           if (l == 0) {
             a.self_out = nullptr; a.h_index = nullptr; a.H = C; a.ldh = sh.Kp;
             g.batch.xdst[j] = (bf16*)C;
@@ -328,6 +329,7 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
             b.mask = (const T*)sl.C[l]; b.ld_mask = sh.Kp;
             b.w = sh.half;
             b.few_nnz = 1;
+            b.early = 1;
           } else if (sage) {  // dZ_{l-1} = (dC_self + N^T dC_neigh) * 1[H_l > 0]
             b.colscale = sl.scale; b.H = (const T*)sl.dC + sh.half; b.ldh = sh.Kp;
             b.add = (const T*)sl.dC; b.ld_add = sh.Kp;

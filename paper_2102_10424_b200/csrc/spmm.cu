@@ -124,14 +124,20 @@ __device__ __forceinline__ void gather_range(const SpmmArgs<TI, TO>& a, int64_t 
 // of its range in turn -- group g sums the g-th contiguous slice of the edge list, the slices
 // meet in shared memory and the unit's own group adds them in slice order.  The split depends
 // only on the row's degree, so the result is deterministic and independent of the launch shape
-// (grouped or single-slot, any world size).  Dynamic shared memory: 256 * J * V floats.
+// (grouped or single-slot, any world size).  Dynamic shared memory: 2 * 256 * J * V floats.
 template <typename TI, typename TO, int LPR, int J, int UNROLL, bool CSCALE, bool WIDE, bool PRED = false>
 __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && sizeof(TI) == 2) ? 4
                                            : UNROLL == 1 ? (J <= 2 ? 4 : 3) : (J <= 2 ? 3 : 2))
     k_spmm(const __grid_constant__ SpmmGroup<TI, TO> G, int nchunks, int split_min) {
-  pdl_wait();
-  pdl_trigger();
   const SpmmArgs<TI, TO>& a = G.a[blockIdx.y];  // one sub-GCN slot per grid row
+  // early: every gathered operand was written at least two launches back (the launch before this
+  // one, the block-diagonal pass, only produces `add`), so the whole gather phase runs before
+  // griddepcontrol.wait, overlapping the predecessor; only the epilogue waits for it
+  const bool early = a.early && !a.self_out;
+  if (!early) {
+    pdl_wait();
+    pdl_trigger();
+  }
   constexpr int V = Elem<TI>::kVec;  // elements per 16-byte vector of TI
   constexpr int GPW = 32 / LPR;      // groups per warp
   constexpr int NG = 8 * GPW;        // groups per CTA (256 threads)
@@ -220,69 +226,87 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
   // exact zeros, never a stale `add`
   const bool dummy = beg < 0;
   const bool heavy = split_min > 0 && valid && !dummy && end - beg > split_min;
+  const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
+  bool act[J];
+  float acc[J][V];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    act[j] = vbase + j * LPR < wv;
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
+  }
   if (valid && !heavy) {
-    const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
-    bool act[J];
-    float acc[J][V];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      act[j] = vbase + j * LPR < wv;
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
-    }
     self_term(v, vbase, act, acc);
     gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, beg, end, H4, ldv, vbase, act, gmask, gl, acc);
-    epilogue(v, vbase, act, acc, dummy);
   }
-  if (split_min <= 0) return;  // uniform over the launch
-  __shared__ uint8_t hflag[NG];
-  if (gl == 0) hflag[grp] = heavy;
-  if (!__syncthreads_or(heavy)) return;
-  extern __shared__ float4 spart[];  // [NG][LPR * J] vectors of V floats (V / 4 float4 each)
-  for (int h = 0; h < NG; ++h) {
-    if (!hflag[h]) continue;  // uniform over the CTA
-    const int64_t gh = (int64_t)blockIdx.x * NG + h;
-    const int64_t vh = gh / nchunks;
-    const int ch = (int)(gh - vh * nchunks);
-    const int64_t bh = a.row_beg[vh], n = a.row_end[vh] - bh;
-    const int64_t per = (n + NG - 1) / NG;
-    const int64_t b0 = bh + (grp * per < n ? grp * per : n);
-    const int64_t b1 = bh + ((grp + 1) * per < n ? (grp + 1) * per : n);
-    const int vbase = ch * LPR * J + gl;
-    bool act[J];
-    float acc[J][V];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      act[j] = vbase + j * LPR < wv;
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
-    }
-    if (grp == 0) self_term(vh, vbase, act, acc);
-    gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, b0, b1, H4, ldv, vbase, act, gmask, gl, acc);
-#pragma unroll
-    for (int j = 0; j < J; ++j)
-#pragma unroll
-      for (int i = 0; i < V; i += 4)
-        spart[((int64_t)grp * LPR * J + j * LPR + gl) * (V / 4) + i / 4] =
-            make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
-    __syncthreads();
-    if (grp == h) {
+  if (split_min > 0) {  // uniform over the launch
+    __shared__ uint8_t hflag[NG];
+    if (gl == 0) hflag[grp] = heavy;
+    if (__syncthreads_or(heavy)) {
+      // [NG][LPR * J] vectors of V floats (V / 4 float4 each): the slices' partial sums, then
+      // every group's own sum parked while the heavy units run (keeps it out of registers)
+      extern __shared__ float4 spart[];
+      float4* sacc = spart + (size_t)NG * LPR * J * (V / 4);
+      auto slot = [&](float4* buf, int g, int j, int i) -> float4& {
+        return buf[((int64_t)g * LPR * J + j * LPR + gl) * (V / 4) + i / 4];
+      };
 #pragma unroll
       for (int j = 0; j < J; ++j)
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
-      for (int g = 0; g < NG; ++g)  // slice order
+        for (int i = 0; i < V; i += 4) slot(sacc, grp, j, i) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
+      for (int h = 0; h < NG; ++h) {
+        if (!hflag[h]) continue;  // uniform over the CTA
+        const int64_t gh = (int64_t)blockIdx.x * NG + h;
+        const int64_t vh = gh / nchunks;
+        const int ch = (int)(gh - vh * nchunks);
+        const int64_t bh = a.row_beg[vh], n = a.row_end[vh] - bh;
+        const int64_t per = (n + NG - 1) / NG;
+        const int64_t b0 = bh + (grp * per < n ? grp * per : n);
+        const int64_t b1 = bh + ((grp + 1) * per < n ? (grp + 1) * per : n);
+        const int vb = ch * LPR * J + gl;
+        bool ah[J];
+        float p[J][V];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          ah[j] = vb + j * LPR < wv;
+#pragma unroll
+          for (int i = 0; i < V; ++i) p[j][i] = 0.f;
+        }
+        if (grp == 0) self_term(vh, vb, ah, p);
+        gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, b0, b1, H4, ldv, vb, ah, gmask, gl, p);
 #pragma unroll
         for (int j = 0; j < J; ++j)
 #pragma unroll
-          for (int i = 0; i < V; i += 4) {
-            const float4 p = spart[((int64_t)g * LPR * J + j * LPR + gl) * (V / 4) + i / 4];
-            acc[j][i] += p.x; acc[j][i + 1] += p.y; acc[j][i + 2] += p.z; acc[j][i + 3] += p.w;
-          }
-      epilogue(vh, vbase, act, acc, false);
+          for (int i = 0; i < V; i += 4) slot(spart, grp, j, i) = make_float4(p[j][i], p[j][i + 1], p[j][i + 2], p[j][i + 3]);
+        __syncthreads();
+        if (grp == h)  // the unit's own group: the slices in slice order (its own sum was zero)
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+#pragma unroll
+            for (int i = 0; i < V; i += 4) {
+              float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int g = 0; g < NG; ++g) {
+                const float4 q = slot(spart, g, j, i);
+                t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+              }
+              slot(sacc, grp, j, i) = t;
+            }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int i = 0; i < V; i += 4) {
+          const float4 q = slot(sacc, grp, j, i);
+          acc[j][i] = q.x; acc[j][i + 1] = q.y; acc[j][i + 2] = q.z; acc[j][i + 3] = q.w;
+        }
     }
-    __syncthreads();
   }
+  if (early) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (valid) epilogue(v, vbase, act, acc, dummy);
 }
 
 template <typename TI, typename TO, int LPR, int J>
@@ -294,15 +318,19 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
   // unsplit row sums)
   const char* e_split = std::getenv("GIST_SPMM_SPLIT");
   const int split_min = e_split && e_split[0] == '0' ? 0 : (G.a[0].desc ? (G.a[0].few_nnz ? 32 : 128) : 0);
-  const size_t sm = split_min > 0 ? (size_t)256 * J * Elem<TI>::kVec * sizeof(float) : 0;
+  const size_t sm = split_min > 0 ? (size_t)2 * 256 * J * Elem<TI>::kVec * sizeof(float) : 0;
   const int nchunks = (int)cdiv(w, CW);
   const int64_t groups = rows * nchunks;
   const dim3 grid((unsigned)cdiv(groups, 8 * (32 / LPR)), (unsigned)G.n);
+  auto go = [&](auto kern) {
+    if (sm > 0) ensure_smem((const void*)kern, (int)sm);  // (static smem counts against 48 KB too)
+    launch_pdl(kern, grid, 256, sm, s, G, nchunks, split_min);
+  };
   if (G.a[0].few_nnz && J == 1 && !G.a[0].colscale) {  // few neighbours, narrow rows: the row's
     // dependency chain dominates (not bytes), so every round keeps 8 gathers in flight
     const bool wide = G.a[0].h_index != nullptr;
-    if (wide) launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, true, true>, grid, 256, sm, s, G, nchunks, split_min);
-    else launch_pdl(k_spmm<TI, TO, LPR, 1, 8, false, false, true>, grid, 256, sm, s, G, nchunks, split_min);
+    if (wide) go(k_spmm<TI, TO, LPR, 1, 8, false, true, true>);
+    else go(k_spmm<TI, TO, LPR, 1, 8, false, false, true>);
     return;
   }
   if (G.a[0].few_nnz && J <= 3 && !G.a[0].colscale && rows * G.n <= 16384) {
@@ -311,18 +339,18 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     // degree tail sets the launch length)
     constexpr int UF = J == 1 ? 8 : (J == 2 ? 4 : 2);
     const bool wide = G.a[0].h_index != nullptr;
-    if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, true, true>, grid, 256, sm, s, G, nchunks, split_min);
-    else launch_pdl(k_spmm<TI, TO, LPR, J, UF, false, false, true>, grid, 256, sm, s, G, nchunks, split_min);
+    if (wide) go(k_spmm<TI, TO, LPR, J, UF, false, true, true>);
+    else go(k_spmm<TI, TO, LPR, J, UF, false, false, true>);
     return;
   }
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads
     const bool wide = G.a[0].h_index != nullptr;
     if (G.a[0].colscale) {
-      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, true>, grid, 256, sm, s, G, nchunks, split_min);
-      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, true, false>, grid, 256, sm, s, G, nchunks, split_min);
+      if (wide) go(k_spmm<TI, TO, LPR, J, 1, true, true>);
+      else go(k_spmm<TI, TO, LPR, J, 1, true, false>);
     } else {
-      if (wide) launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, true>, grid, 256, sm, s, G, nchunks, split_min);
-      else launch_pdl(k_spmm<TI, TO, LPR, J, 1, false, false>, grid, 256, sm, s, G, nchunks, split_min);
+      if (wide) go(k_spmm<TI, TO, LPR, J, 1, false, true>);
+      else go(k_spmm<TI, TO, LPR, J, 1, false, false>);
     }
     return;
   }
@@ -334,10 +362,10 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     const int64_t hr = a.h_rows > a.rows + a.row0 ? a.h_rows : a.rows + a.row0;
     wide |= a.h_index != nullptr || hr * (a.ldh / Elem<TI>::kVec) >= ((int64_t)1 << 31);
   }
-  if (!wide && cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, false>, grid, 256, sm, s, G, nchunks, split_min);
-  else if (!wide) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, false>, grid, 256, sm, s, G, nchunks, split_min);
-  else if (cs) launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, true, true>, grid, 256, sm, s, G, nchunks, split_min);
-  else launch_pdl(k_spmm<TI, TO, LPR, J, UNROLL, false, true>, grid, 256, sm, s, G, nchunks, split_min);
+  if (!wide && cs) go(k_spmm<TI, TO, LPR, J, UNROLL, true, false>);
+  else if (!wide) go(k_spmm<TI, TO, LPR, J, UNROLL, false, false>);
+  else if (cs) go(k_spmm<TI, TO, LPR, J, UNROLL, true, true>);
+  else go(k_spmm<TI, TO, LPR, J, UNROLL, false, true>);
 }
 
 }  // namespace

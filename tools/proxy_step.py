@@ -38,9 +38,17 @@ for t in range(rounds + 1):
     if t:
         ts.append(e0.elapsed_time(e1))
 ms = sorted(ts)[len(ts) // 2]
+prof = None
+if os.environ.get("PROXY_PROF"):  # one more call with every step serialised and event-timed
+    c.profile(1)
+    c.subtrain(zeta, 0.01, want_loss=False)
+    torch.cuda.synchronize()
+    prof = {k: {"us_per_step": round(1e3 * v["ms"] / zeta, 2), "launches_per_step": v["launches"] / zeta}
+            for k, v in c.profile_get().items() if v["launches"]}
+    c.profile(0)
 slots = len([i for i in range(spec.m) if i % W == 0])
 print(json.dumps({"W": W, "slots": slots, "zeta": zeta, "us_per_step": 1e3 * ms / zeta,
-                  "per_gpu_steps_s": slots * zeta / (ms / 1e3), "env": {k: v for k, v in os.environ.items()
+                  "per_gpu_steps_s": slots * zeta / (ms / 1e3), "profile": prof, "env": {k: v for k, v in os.environ.items()
                                                                         if k.startswith("GIST_")}}), flush=True)
 c.close()
 lb.close()
