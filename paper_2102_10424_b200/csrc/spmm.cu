@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
     }
   };
   // row scale, residual add, ReLU mask / ReLU and the store of unit (v, vbase)
-  auto epilogue = [&](int64_t v, int vbase, const bool(&act)[J], float(&acc)[J][V], bool dummy) {
+  auto epilogue = [&](int64_t v, int vbase, const bool(&act)[J], float(&acc)[J][V], bool dummy, const uint4* addv) {
     const float rs = a.rowscale ? a.rowscale[v] : 1.f;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
       } else {
         if (a.add) {
           float t[V];
-          unpack(*reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
+          unpack(addv ? addv[j] : *reinterpret_cast<const uint4*>(a.add + v * a.ld_add + c), t, TI());
 #pragma unroll
           for (int i = 0; i < V; ++i) o[i] += t[i];
         }
@@ -226,6 +226,14 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
   // exact zeros, never a stale `add`
   const bool dummy = beg < 0;
   const bool heavy = split_min > 0 && valid && !dummy && end - beg > split_min;
+  // whether the CTA holds a heavy unit, decided up front: CTAs without one (most) never meet
+  // at a barrier after their gathers, so a warp does not idle behind the CTA's slowest row
+  __shared__ uint8_t hflag[NG];
+  bool any_heavy = false;
+  if (split_min > 0) {  // uniform over the launch
+    if (gl == 0) hflag[grp] = heavy;
+    any_heavy = __syncthreads_or(heavy);
+  }
   const int vbase = chunk * LPR * J + gl;  // this lane's first vector column
   bool act[J];
   float acc[J][V];
@@ -235,14 +243,21 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[j][i] = 0.f;
   }
+  // the residual row is loaded ahead of the gathers (its latency overlaps them) unless it is
+  // the predecessor's output (early)
+  uint4 addv[J];
+  const bool pre_add = !early && valid && !heavy && !dummy && a.add;
+  if (pre_add) {
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (act[j]) addv[j] = *reinterpret_cast<const uint4*>(a.add + v * a.ld_add + (int64_t)(vbase + j * LPR) * V);
+  }
   if (valid && !heavy) {
     self_term(v, vbase, act, acc);
     gather_range<TI, TO, LPR, J, UNROLL, CSCALE, PRED, Off>(a, beg, end, H4, ldv, vbase, act, gmask, gl, acc);
   }
-  if (split_min > 0) {  // uniform over the launch
-    __shared__ uint8_t hflag[NG];
-    if (gl == 0) hflag[grp] = heavy;
-    if (__syncthreads_or(heavy)) {
+  {
+    if (any_heavy) {  // uniform over the CTA
       // [NG][LPR * J] vectors of V floats (V / 4 float4 each): the slices' partial sums, then
       // every group's own sum parked while the heavy units run (keeps it out of registers)
       extern __shared__ float4 spart[];
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(256, PRED ? (J == 1 ? 3 : 2) : (J == 1 && size
     pdl_wait();
     pdl_trigger();
   }
-  if (valid) epilogue(v, vbase, act, acc, dummy);
+  if (valid) epilogue(v, vbase, act, acc, dummy, pre_add ? addv : nullptr);
 }
 
 template <typename TI, typename TO, int LPR, int J>
@@ -331,16 +346,6 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     const bool wide = G.a[0].h_index != nullptr;
     if (wide) go(k_spmm<TI, TO, LPR, 1, 8, false, true, true>);
     else go(k_spmm<TI, TO, LPR, 1, 8, false, false, true>);
-    return;
-  }
-  if (G.a[0].few_nnz && J <= 3 && !G.a[0].colscale && rows * G.n <= 16384) {
-    // few neighbours per row and a small launch (one sub-GCN per GPU: ~3,100 rows, a third of the
-    // warp slots): the GPU has warps to spare, so each row keeps several gathers in flight (its
-    // degree tail sets the launch length)
-    constexpr int UF = J == 1 ? 8 : (J == 2 ? 4 : 2);
-    const bool wide = G.a[0].h_index != nullptr;
-    if (wide) go(k_spmm<TI, TO, LPR, J, UF, false, true, true>);
-    else go(k_spmm<TI, TO, LPR, J, UF, false, false, true>);
     return;
   }
   if (G.a[0].few_nnz && J <= 3) {  // few neighbours per row: occupancy over in-flight loads

@@ -101,3 +101,4 @@ def test_heavy_rows_bit_identical_across_world_sizes(precision):
         for t in range(len(ref["hist"])):
             for l in range(len(dims) - 1):
                 np.testing.assert_array_equal(got[r]["hist"][t][l], ref["hist"][t][l])
+
