@@ -86,6 +86,19 @@ __device__ __forceinline__ void st16_hint(bf16* p, const float* v, uint64_t pol)
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
+// GIST_GEMM_TRACE (debug builds only, tools/gemm_trace.py): %globaltimer at the phases of
+// each CTA's first tile -- entry, after the PDL wait, first TMA issue, first stage landed,
+// last MMA of the tile issued, accumulator ready in the epilogue, epilogue done, exit.
+#ifdef GIST_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[1024][16];
+__device__ __forceinline__ void gtrace(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 1024) g_gemm_trace[blockIdx.x][k] = t;
+}
+#else
+__device__ __forceinline__ void gtrace(int) {}
+#endif
 // TMA store of one staged box (shared -> global; out-of-bounds rows/columns are clipped)
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
@@ -265,7 +278,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // `pre`: the chunk's 16 `add` values (two 16-byte vectors) loaded ahead of time, or nullptr.
 template <bool OUT_F32, bool STORE = true>
 __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, int col, int N, float* v,
-                                          const uint4* pre) {
+                                          const uint4* pre, const uint32_t* mw_pre = nullptr) {
   const bool full16 = col + 16 <= N;
   if (E.rscale) {  // per-row scale of the columns >= rs_from (sc = rscale[row], loaded once per tile)
 #pragma unroll
@@ -297,7 +310,7 @@ __device__ __forceinline__ void epi_chunk(const Epi& E, float sc, int64_t row, i
     for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.f);
   }
   if (E.mbits_in) {  // ReLU'(0) = 0 of the layer below (R3), bit-packed (col % 16 == 0 here)
-    const uint32_t wd = E.mbits_in[row * E.ldmbi + (col >> 5)] >> (col & 31);
+    const uint32_t wd = (mw_pre ? *mw_pre : E.mbits_in[row * E.ldmbi + (col >> 5)]) >> (col & 31);
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (!((wd >> i) & 1u)) v[i] = 0.f;
@@ -350,6 +363,43 @@ struct Tile {
   Epi E;
 };
 
+// The scalar fields of a slot (everything after its tensor maps), copied from the kernel
+// parameters into shared memory before the PDL wait: a tile decode then reads shared memory
+// instead of the parameter bank, whose per-slot fields (dynamically indexed) miss the constant
+// cache -- ~0.5 us of serial misses in the producer's first decode and again in the epilogue.
+// (compact: 16 of them fit next to the largest ring + staging configuration)
+struct SlotTailTC {
+  void* C;
+  const void* mask;
+  const float* rscale;
+  uint32_t* mbits;
+  const bf16* add;
+  const uint32_t* mbits_in;
+  int32_t ldc, ldm, ldmb, ldadd, ldmbi;
+  int32_t M, N, K, rs_from;
+  uint8_t relu, tma_store, keep_out, stream_a;
+};
+static_assert(sizeof(SlotTailTC) == 88, "compact tail");
+struct BdTail {
+  void* C;
+  const bf16* add;
+  const float* rscale;
+  const int32_t* desc;
+  int64_t ldc, ldadd;
+  int N, global_rows, tma_store, keep_out;
+};
+static_assert(offsetof(BdSlot, C) == 2 * sizeof(CUtensorMap), "BdSlot tail");
+static_assert(offsetof(BdSlot, keep_out) - offsetof(BdSlot, C) == offsetof(BdTail, keep_out), "tail");
+template <class Tail, class Slot>
+__device__ __forceinline__ void copy_tails(const Slot* slots, int n, Tail* dst, size_t off) {
+  static_assert(sizeof(Tail) % 8 == 0, "tail words");
+  constexpr int W = (int)(sizeof(Tail) / 8);
+  for (int i = threadIdx.x; i < n * W; i += blockDim.x) {
+    const int z = i / W, w = i - z * W;
+    reinterpret_cast<uint64_t*>(dst + z)[w] = reinterpret_cast<const uint64_t*>(reinterpret_cast<const char*>(slots + z) + off)[w];
+  }
+}
+
 // Plain grouped GEMM: tiles (slot, m-tile, n-tile), n fastest.
 template <int BN>
 struct ProbPlain {
@@ -357,21 +407,43 @@ struct ProbPlain {
   static constexpr bool kTmaEpi = true;  // epilogue staging + TMA stores
   static __device__ __forceinline__ int ydim(const Group& G) { return G.tm; }
   static __device__ __forceinline__ int count(const Group& G) { return G.n * G.tm * G.tn; }
-  static constexpr int kMaxDesc = 1;
+  // shared scratch (int32 words): the slots' scalar tails
+  static constexpr int kTailWords = (int)(kMaxGemmOps * sizeof(SlotTailTC) / 4);
+  static constexpr int kScratchWords = kTailWords;
+  static __device__ __forceinline__ void stage_tail(const Group& G, int32_t* sd) {
+    if ((int)threadIdx.x < G.n) {  // one slot per thread (leading dimensions < 2^31 elements)
+      const GemmSlotTC& S = G.s[threadIdx.x];
+      SlotTailTC& t = reinterpret_cast<SlotTailTC*>(sd)[threadIdx.x];
+      t.C = S.C; t.mask = S.mask; t.rscale = S.rscale; t.mbits = S.mbits; t.add = S.add; t.mbits_in = S.mbits_in;
+      t.ldc = (int32_t)S.ldc; t.ldm = (int32_t)S.ldm; t.ldmb = (int32_t)S.ldmb; t.ldadd = (int32_t)S.ldadd;
+      t.ldmbi = (int32_t)S.ldmbi;
+      t.M = S.M; t.N = S.N; t.K = S.K; t.rs_from = S.rs_from;
+      t.relu = (uint8_t)S.relu; t.tma_store = (uint8_t)S.tma_store; t.keep_out = (uint8_t)S.keep_out;
+      t.stream_a = (uint8_t)S.stream_a;
+    }
+  }
   static __device__ __forceinline__ void stage(const Group&, int32_t*) {}
+  // the tensor maps of this CTA's first tile, fetched while the predecessor drains
+  static __device__ __forceinline__ void prefetch(const Group& G, int t) {
+    if (t >= count(G)) return;
+    const GemmSlotTC& S = G.s[t / (G.tm * G.tn)];
+    prefetch_map(&S.ma);
+    prefetch_map(&S.mb);
+    if (S.tma_store) prefetch_map(&S.mc);
+  }
   static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sd) {
     const int per = G.tm * G.tn;
     const int z = t / per, r = t - z * per;
     return decode_y(G, z, r / G.tn, r % G.tn, sd);
   }
   // tile (slot z, 128-row tile y, n-tile nt)
-  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t*) {
+  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t* sd) {
     Tile T;
-    const GemmSlotTC& S = G.s[z];
+    const SlotTailTC& S = reinterpret_cast<const SlotTailTC*>(sd)[z];
     const int m0 = y * BM, n0 = nt * BN;
     T.valid = T.mma = m0 < S.M && n0 < S.N;
-    T.ma = &S.ma;
-    T.mb = &S.mb;
+    T.ma = &G.s[z].ma;
+    T.mb = &G.s[z].mb;
     T.a_row = m0;
     T.b_col = n0;
     T.b_k0 = 0;
@@ -381,7 +453,7 @@ struct ProbPlain {
     T.n0 = n0;
     T.N = S.N;
     T.E = Epi{S.C, S.ldc, S.relu, (const bf16*)S.mask, S.ldm, S.rscale, S.rs_from, S.add, S.ldadd, S.mbits, S.ldmb,
-                 S.tma_store ? &S.mc : nullptr, 1, S.keep_out, S.mbits_in, S.ldmbi};
+                 S.tma_store ? &G.s[z].mc : nullptr, 1, S.keep_out, S.mbits_in, S.ldmbi};
     T.stream_a = S.stream_a;
     return T;
   }
@@ -391,38 +463,49 @@ struct ProbPlain {
 template <int BN>
 struct ProbBd {
   using Group = BdGroup;
-  // direct stores: its tiles end at cluster boundaries (most warps would fall back anyway)
-  // and the 4-stage ring + descriptor staging leave no room for the staging buffers
-  static constexpr bool kTmaEpi = false;
+  // TMA-staged stores for every 32-row lane quarter inside its cluster (a tile's last quarter
+  // may cross the cluster end: direct stores there, E.clip = 0); a 3-stage ring leaves room
+  static constexpr bool kTmaEpi = true;
   static __device__ __forceinline__ int mt_per(const Group& G) { return (G.bs + BM - 1) / BM; }
   static __device__ __forceinline__ int ydim(const Group& G) {
     return G.q * mt_per(G) + (int)((G.rows + BM - 1) / BM);
   }
   static __device__ __forceinline__ int count(const Group& G) { return G.n * ydim(G) * G.tn; }
-  // this step's descriptors of every slot, staged in shared memory once per CTA
+  // shared scratch: the slots' scalar tails, then this step's descriptors of every slot
   static constexpr int kMaxDesc = 3 * 64 + 4;
-  static __device__ __forceinline__ void stage(const Group& G, int32_t* sdesc) {
+  static constexpr int kTailWords = (int)(kMaxGroup * sizeof(BdTail) / 4);
+  static constexpr int kScratchWords = kTailWords + kMaxDesc * kMaxGroup;
+  static __device__ __forceinline__ void stage_tail(const Group& G, int32_t* sd) {
+    copy_tails(G.s, G.n, reinterpret_cast<BdTail*>(sd), offsetof(BdSlot, C));
+  }
+  static __device__ __forceinline__ void prefetch(const Group& G, int) {
+    prefetch_map(&G.ma);
+    prefetch_map(&G.s[0].mb);
+  }
+  static __device__ __forceinline__ void stage(const Group& G, int32_t* sd) {
     const int per = 3 * G.q + 4;
     const int z = G.st->z;
+    const BdTail* tl = reinterpret_cast<const BdTail*>(sd);
+    int32_t* sdesc = sd + kTailWords;
     for (int i = threadIdx.x; i < G.n * per; i += blockDim.x)
-      sdesc[i] = G.s[i / per].desc[(size_t)z * per + (i % per)];
+      sdesc[i] = tl[i / per].desc[(size_t)z * per + (i % per)];
   }
   static __device__ __forceinline__ Tile decode(const Group& G, int t, const int32_t* sdesc) {
     const int per = ydim(G) * G.tn;
     const int z = t / per, r = t - z * per;
     return decode_y(G, z, r / G.tn, r % G.tn, sdesc);
   }
-  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t* sdesc) {
+  static __device__ __forceinline__ Tile decode_y(const Group& G, int z, int y, int nt, const int32_t* sd) {
     Tile T;
     const int n0 = nt * BN;
-    const BdSlot& S = G.s[z];
+    const BdTail& S = reinterpret_cast<const BdTail*>(sd)[z];
     const int q = G.q, mp = mt_per(G);
-    const int32_t* d = sdesc + z * (3 * q + 4);
+    const int32_t* d = sd + kTailWords + z * (3 * q + 4);
     T.ma = &G.ma;
-    T.mb = &S.mb;
+    T.mb = &G.s[z].mb;
     T.n0 = n0;
     T.N = S.N;
-    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &S.mc : nullptr, 0,
+    T.E = Epi{S.C, S.ldc, 0, nullptr, 0, S.rscale, 0, S.add, S.ldadd, nullptr, 0, S.tma_store ? &G.s[z].mc : nullptr, 0,
               S.keep_out, nullptr, 0};
     T.stream_a = 0;
     T.b_col = n0;
@@ -466,10 +549,19 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
     const bool avec = arow && live && ((((uintptr_t)arow) & 15) == 0) && ((T.E.ldadd & 7) == 0);
     uint4 cur[4], nxt[4];
     bool cur_ok = avec && c0w + 32 <= T.N - T.n0;
+    // the ReLU-mask words of this warp's columns, also ahead of the wait (one per 32 columns)
+    constexpr int MW = CW / 32;
+    uint32_t mw[MW];
+    const bool mpre = T.E.mbits_in && live;
+    if (mpre)
+#pragma unroll
+      for (int i = 0; i < MW; ++i)
+        mw[i] = T.n0 + c0w + 32 * i < T.N ? T.E.mbits_in[row * T.E.ldmbi + ((T.n0 + c0w) >> 5) + i] : 0u;
     if (cur_ok)
 #pragma unroll
       for (int i = 0; i < 4; ++i) cur[i] = __ldg(reinterpret_cast<const uint4*>(arow + c0w) + i);
     mbar_wait(accf_b, aph);
+    if (lq == 2 && c0w == 0 && lane == 0) gtrace(5);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t trow = tmem_acc + ((uint32_t)(lq * 32) << 16);
     // TMA-store path: this warp's 32 rows are staged (128-byte rows, SWIZZLE_128B: 16-byte
@@ -489,6 +581,8 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
         for (int i = 0; i < 4; ++i) nxt[i] = __ldg(reinterpret_cast<const uint4*>(arow + c + 32) + i);
       float v[32];
       tmem_ld32(trow + c, v);
+      const bool trc = lq == 2 && c0w == 0 && lane == 0 && c == 0;
+      if (trc) gtrace(8);
       if (tma) {
         const int cb = c % CPB;  // column of this piece inside its box
         uint8_t* buf = stg;
@@ -497,8 +591,9 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
           __syncwarp();
         }
         if (live && T.n0 + c < T.N) {
-          epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
-          if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+          epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr, mpre ? mw : nullptr);
+          if (T.n0 + c + 16 < T.N)
+            epi_chunk<OUT_F32, false>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr, mpre ? mw : nullptr);
         }
         uint8_t* rbase = buf + lane * 128;
         if (OUT_F32) {
@@ -518,12 +613,14 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
           }
         }
         if (cb + 32 == CPB || c + 32 == c0w + CW || T.n0 + c + 32 >= T.N) {  // box complete: store it
+          if (lq == 2 && c0w == 0 && lane == 0) gtrace(9);
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
             if (T.E.keep) tma_store_2d_hint(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32), policy_evict_last());
             else tma_store_2d(T.E.mc, buf, T.n0 + c - cb, (int)(T.out_row0 + lq * 32));
             bulk_commit();
+            if (lq == 2 && c0w == 0) gtrace(10);
           }
         }
         if (live && T.n0 + c < T.N && T.E.mbits) {
@@ -536,8 +633,9 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
           T.E.mbits[row * T.E.ldmb + ((T.n0 + c) >> 5)] = bits;
         }
       } else if (live && T.n0 + c < T.N) {
-        epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr);
-        if (T.n0 + c + 16 < T.N) epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr);
+        epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c, T.N, v, cur_ok ? cur : nullptr, mpre ? mw : nullptr);
+        if (T.n0 + c + 16 < T.N)
+          epi_chunk<OUT_F32>(T.E, sc, row, T.n0 + c + 16, T.N, v + 16, cur_ok ? cur + 2 : nullptr, mpre ? mw : nullptr);
         if (T.E.mbits) {  // sign bits of the values as stored (bf16-rounded on the bf16 path)
           uint32_t bits = 0;
 #pragma unroll
@@ -551,6 +649,8 @@ __device__ __forceinline__ void epi_tile(const Tile& T, uint32_t tmem_acc, uint6
 #pragma unroll
       for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       cur_ok = nxt_ok;
+#pragma unroll
+      for (int i = 0; i + 1 < MW; ++i) mw[i] = mw[i + 1];
     }
 }
 
@@ -595,9 +695,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
   uint32_t* tmem_slot = (uint32_t*)(acce + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
-  __shared__ int32_t sdesc[Prob::kMaxDesc * kMaxGroup];
+  __shared__ __align__(16) int32_t sdesc[Prob::kScratchWords];
 
   if (threadIdx.x == 0) {
+    gtrace(0);
     for (int s = 0; s < CF::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -613,8 +714,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
                  "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // prologue above (barriers, TMEM) overlaps the predecessor kernel's tail under PDL;
-  // everything below may read what it wrote
+  if (warp == 0 && lane == 0) Prob::prefetch(G, blockIdx.x);
+  Prob::stage_tail(G, sdesc);
+  __syncthreads();  // the tails are read by other threads from here on (ProbBd::stage, decode)
+  if (threadIdx.x == 0) gtrace(12);
+  // prologue above (barriers, TMEM, tensor-map prefetch) overlaps the predecessor kernel's
+  // tail under PDL; everything below may read what it wrote
   pdl_wait();
   pdl_trigger();
   Prob::stage(G, sdesc);
@@ -623,6 +728,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   const int total = Prob::count(G);
+  if (threadIdx.x == 0) gtrace(1);
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
@@ -638,6 +744,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           uint8_t* sa = smem + s * CF::STAGE_BYTES;
           uint8_t* sb = sa + CF::A_BYTES;
           mbar_arrive_expect_tx(&full[s], CF::STAGE_BYTES);
+          if (it == 0) gtrace(2);
           const int k0 = kb * BKE;
           if (T.stream_a) {  // last read of A for a while: evict first
             const uint64_t pol = policy_evict_first();
@@ -684,6 +791,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           const int s = it % CF::STAGES;
           const uint32_t ph = (it / CF::STAGES) & 1u;
           mbar_wait(&full[s], ph);
+          if (it == 0) gtrace(3);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(smem + s * CF::STAGE_BYTES);
           const uint32_t sb = sa + CF::A_BYTES;
@@ -699,6 +807,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
           umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
         umma_commit(&accf[b]);  // accumulator b complete
+        if (tc == 0) gtrace(4);
         ++tc;
       }
     }
@@ -719,16 +828,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_persist(const __grid_c
       }
       const uint32_t b = tc & 1u, aph = (tc >> 1) & 1u;
       epi_tile<BN, OUT_F32, Prob::kTmaEpi>(T, tmem + b * BN, &accf[b], aph, lq, lane, c0w, stg);
+      if (tc == 0 && ew == 0 && lane == 0) gtrace(6);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[b]);
       ++tc;
     }
-    if (lane == 0) bulk_wait_all();  // every TMA store has landed before the grid completes
+    if (lane == 0) bulk_wait_read0();  // the staging buffers are read before the CTA exits
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) gtrace(7);
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
@@ -760,7 +871,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_cons
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
-  __shared__ int32_t sdesc[Prob::kMaxDesc * kMaxGroup];
+  __shared__ __align__(16) int32_t sdesc[Prob::kScratchWords];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -779,6 +890,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_cons
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrival
+  Prob::stage_tail(G, sdesc);
+  __syncthreads();
   pdl_wait();
   pdl_trigger();
   Prob::stage(G, sdesc);
@@ -898,7 +1011,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_cons
       if (lane == 0) mbar_arrive_leader(&acce[b]);
       ++tc;
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_read0();
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1029,7 +1142,7 @@ void launch_bd(const BdPlan& P, cudaStream_t s) {
   const int mt_per = (P.G.bs + BM - 1) / BM;
   const int yd = P.G.q * mt_per + (int)cdiv(P.G.rows, BM);
   const int total = P.G.n * yd * P.G.tn;
-  launch_persist<BN, 4, false, true, false, ProbBd<BN>>(P.G, total, s);
+  launch_persist<BN, 3, false, true, false, ProbBd<BN>>(P.G, total, s);
 }
 
 }  // namespace
@@ -1090,6 +1203,9 @@ bool gemm_tc_prepare(const GemmOp* ops, int n, GemmPlanTC* P, bool tf32) {
     if (o.transA != o0.transA || o.transB != o0.transB || o.out_f32 != o0.out_f32) return false;
     if (o.K <= 0 || ((uintptr_t)o.A & 15) || ((uintptr_t)o.B & 15) || (o.lda % 8) || (o.ldb % 8)) return false;
     if (tf32 && (o.mbits || o.add || o.mbits_in || o.rscale)) return false;
+    // the kernel keeps the epilogue's leading dimensions as 32-bit (SlotTailTC)
+    const int64_t lim = INT32_MAX;
+    if (o.ldc > lim || o.ldm > lim || o.ldmb > lim || o.ldadd > lim || o.ldmbi > lim) return false;
     GemmSlotTC& S = P->G.s[i];
     bool ok = P->a_mn ? make_map(&S.ma, o.A, o.M, o.K, o.lda, ebox, ebox, tf32, tf32)
                       : make_map(&S.ma, o.A, o.K, o.M, o.lda, ebox, BM, tf32);
@@ -1156,7 +1272,7 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     S.desc = o.desc;
     S.global_rows = o.global_rows;
     S.N = (int)o.N;
-    S.tma_store = 0;  // ProbBd::kTmaEpi == false
+    S.tma_store = make_store_map(&S.mc, o.C, o.N, rows, o.ldc, false) ? 1 : 0;
     S.keep_out = o.keep_out;
 
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
@@ -1202,3 +1318,10 @@ bool gemm_tf32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const 
 }
 
 }  // namespace gist
+
+#ifdef GIST_GEMM_TRACE
+extern "C" int gist_debug_gemm_trace(unsigned long long* out, int n) {
+  if (n > 1024) n = 1024;
+  return cudaMemcpyFromSymbol(out, gist::g_gemm_trace, (size_t)n * 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -19,13 +19,17 @@ from paper_2102_10424_b200 import gist  # noqa: E402
 REPS = 20
 label = sys.argv[1] if len(sys.argv) > 1 else "default"
 NB = 3106
+ONLY = os.environ.get("PROBE_ONLY")
 SHAPES = {  # name: (transA, transB, M, N, K) -- single slot and 8-slot stacks
     "fwd1": (0, 0, NB, 512, 1024), "dX1": (0, 1, NB, 1024, 512), "dW1": (1, 0, 1024, 512, NB),
     "fwd8": (0, 0, 8 * NB, 512, 1024), "dX8": (0, 1, 8 * NB, 1024, 512), "dW8": (1, 0, 8 * 1024, 512, NB),
     "w4096": (0, 0, NB, 4096, 8192),
+    "radh8": (0, 1, 8 * NB, 512, 96), "radh1": (0, 1, NB, 512, 96), "out8": (0, 0, 8 * NB, 512, 64),
 }
 dev = "cuda"
 for name, (ta, tb, M, N, K) in SHAPES.items():
+    if ONLY and name not in ONLY.split(","):
+        continue
     A = torch.randn((K, M) if ta else (M, K), device=dev).to(torch.bfloat16)
     B = torch.randn((N, K) if tb else (K, N), device=dev).to(torch.bfloat16)
     C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
