@@ -96,6 +96,18 @@ enum { GIST_AGG_ALLGATHER = 0, GIST_AGG_P2P = 1, GIST_AGG_SYMM = 2 };
  * the W rows of those layers (GAT: not to the attention vectors).  Evaluation only; training
  * is unaffected. */
 enum { GIST_EVAL_SCALE_NONE = 0, GIST_EVAL_SCALE_MEAN = 1 };
+/* Storage of the global model across ranks (SURVEY.md §8(e) alternatives, §8 f2 "variant for C5:
+ * owner-sharded Theta with all-to-all re-partition and aggregate"; it takes the place of the
+ * paper's parameter server).  REPLICATED (default): every rank holds all of
+ * Theta.  SHARDED: rank r holds physical rows [K_l r / W, K_l (r+1) / W) of every Theta_l (and of
+ * the f3 moments), ~1/W of the memory; gist_partition sends every owned row of every sub-model
+ * to the sub-model's rank and gist_aggregate sends the updated rows back to their owners, both as
+ * one grouped point-to-point exchange (ncclSend / ncclRecv) of (W-1)/W of the sub-model bytes --
+ * the same values land in the same places, so Theta stays bit-identical to REPLICATED.
+ * gist_get_params, gist_save_checkpoint and gist_eval* become collectives (every rank calls
+ * them: the rows are gathered for the call); gist_set_params / gist_load_checkpoint and
+ * gist_init_params write the local rows only.  Only with agg_mode ALLGATHER. */
+enum { GIST_THETA_REPLICATED = 0, GIST_THETA_SHARDED = 1 };
 
 /* Loopback transport (tests): W contexts of ONE process on one device stand in for W ranks.
  * Every collective of gist_aggregate / gist_eval / gist_eval_parts (all-gather, sum all-reduce,
@@ -129,6 +141,7 @@ typedef struct {
   int32_t agg_mode;           /* GIST_AGG_* (default ALLGATHER) */
   gist_loopback* loopback;    /* tests: loopback group of world_size ranks replacing NCCL, or NULL */
   int32_t eval_scale;         /* GIST_EVAL_SCALE_* (default NONE, R10) */
+  int32_t theta_mode;         /* GIST_THETA_* (default REPLICATED) */
 } gist_config;
 
 /* Fills *cfg with defaults (GCN, Adam .9/.999/1e-8, FP32, q=1, world 1, device 0). */
@@ -266,7 +279,8 @@ enum {
   GIST_STAT_ROUND = 0, GIST_STAT_STEP = 1, GIST_STAT_SELF_LOOPS_DROPPED = 2, GIST_STAT_LAST_NNZ_B = 3,
   GIST_STAT_LAST_NB = 4, GIST_STAT_KERNELS = 5, GIST_STAT_H2D_BYTES = 6, GIST_STAT_D2H_BYTES = 7,
   GIST_STAT_MAX_NB = 8, GIST_STAT_BLOCK_AGG = 9 /* 1 if block-diagonal tensor-core aggregation is on */,
-  GIST_STAT_BLOCK_DENSITY_PPM = 10 /* intra-cluster block density x 1e6 */
+  GIST_STAT_BLOCK_DENSITY_PPM = 10 /* intra-cluster block density x 1e6 */,
+  GIST_STAT_THETA_BYTES = 11 /* device bytes of this rank's global model storage (Theta + f3 moments) */
 };
 int64_t gist_stat(gist_ctx* ctx, int32_t which);
 

@@ -13,6 +13,8 @@ struct gist_loopback {
   uint64_t gen = 0;
   std::vector<const void*> ptr;  // per rank: the buffer published for the current collective
   std::vector<int> joined;
+  // comm_alltoallv: per source rank, per destination rank, its sends in order
+  std::vector<std::vector<std::vector<std::pair<const void*, size_t>>>> a2a;
 };
 
 extern "C" gist_status gist_loopback_create(int32_t world_size, gist_loopback** out) {
@@ -153,6 +155,64 @@ gist_status comm_barrier(const Comm& c, float* word_dev, cudaStream_t s, std::st
   }
   CKC(cudaStreamSynchronize(s), "loopback barrier: sync");
   lb_barrier(c.lb);
+  return GIST_OK;
+}
+
+gist_status comm_alltoallv(const Comm& c, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                           cudaStream_t s, std::string* err) {
+  if (c.nccl) {
+    ncclResult_t r = ncclGroupStart();
+    for (const Xfer& x : sends)
+      if (r == ncclSuccess && x.bytes) r = ncclSend(x.ptr, x.bytes, ncclChar, x.peer, c.nccl, s);
+    for (const Xfer& x : recvs)
+      if (r == ncclSuccess && x.bytes) r = ncclRecv(x.ptr, x.bytes, ncclChar, x.peer, c.nccl, s);
+    const ncclResult_t e = ncclGroupEnd();
+    if (r == ncclSuccess) r = e;
+    return r == ncclSuccess ? GIST_OK : nccl_fail(r, "ncclSend/ncclRecv (all-to-all)", err);
+  }
+  if (c.world == 1) {  // only self transfers
+    size_t k = 0;
+    for (const Xfer& x : recvs) {
+      if (k >= sends.size() || sends[k].bytes != x.bytes) {
+        if (err) *err = "alltoallv: unmatched self transfer";
+        return GIST_E_ARG;
+      }
+      if (x.bytes && x.ptr != sends[k].ptr)
+        CKC(cudaMemcpyAsync(x.ptr, sends[k].ptr, x.bytes, cudaMemcpyDeviceToDevice, s), "alltoallv self copy");
+      ++k;
+    }
+    return GIST_OK;
+  }
+  gist_loopback* lb = c.lb;
+  CKC(cudaStreamSynchronize(s), "loopback alltoallv: sync");  // this rank's send buffers are final
+  {
+    std::lock_guard<std::mutex> lk(lb->mu);
+    if (lb->a2a.size() != (size_t)c.world) lb->a2a.assign(c.world, {});
+    auto& mine = lb->a2a[c.rank];
+    mine.assign(c.world, {});
+    for (const Xfer& x : sends) mine[x.peer].push_back({x.ptr, x.bytes});
+  }
+  lb_barrier(lb);
+  std::vector<size_t> next(c.world, 0);
+  bool match = true;
+  cudaError_t ce = cudaSuccess;
+  for (const Xfer& x : recvs) {
+    const auto& from = lb->a2a[x.peer][c.rank];
+    const size_t k = next[x.peer]++;
+    if (k >= from.size() || from[k].second != x.bytes) {
+      match = false;
+      continue;
+    }
+    if (x.bytes && ce == cudaSuccess) ce = cudaMemcpyAsync(x.ptr, from[k].first, x.bytes, cudaMemcpyDeviceToDevice, s);
+  }
+  const cudaError_t ce2 = cudaStreamSynchronize(s);
+  lb_barrier(lb);  // no rank reuses its send buffers before every peer has copied them
+  if (ce != cudaSuccess) return cuda_fail(ce, "loopback alltoallv: copy", err);
+  if (ce2 != cudaSuccess) return cuda_fail(ce2, "loopback alltoallv: sync", err);
+  if (!match) {
+    if (err) *err = "alltoallv: send / recv lists do not match";
+    return GIST_E_ARG;
+  }
   return GIST_OK;
 }
 

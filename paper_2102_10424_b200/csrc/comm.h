@@ -32,6 +32,17 @@ gist_status comm_allreduce_sum(const Comm& c, void* buf, size_t count, bool f64,
 // every rank's stream work issued before the call has completed before any rank's work after it
 // (NCCL: a one-word all-reduce on `word_dev`, which orders the streams device-side)
 gist_status comm_barrier(const Comm& c, float* word_dev, cudaStream_t s, std::string* err);
+// point-to-point exchange of variable-size pieces (the owner-sharded Theta's re-partition and
+// subAgg): `sends` / `recvs` list (peer, device pointer, bytes); the k-th send of rank a to rank b
+// is matched with the k-th recv of rank b from rank a (both sides enumerate in the same order).
+// NCCL: one grouped ncclSend / ncclRecv; loopback: device-to-device copies by the receiver.
+struct Xfer {
+  int peer;
+  void* ptr;
+  size_t bytes;
+};
+gist_status comm_alltoallv(const Comm& c, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                           cudaStream_t s, std::string* err);
 // loopback only: every rank's pointer (the P2P subAgg replica regions of one process)
 gist_status comm_exchange_ptr(const Comm& c, void* mine, std::vector<void*>& all, std::string* err);
 // loopback: attach / validate a context's rank

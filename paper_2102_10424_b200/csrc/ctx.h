@@ -160,6 +160,13 @@ struct gist_ctx {
   // global parameters, physical layout (R6): SAGE rows [0,d) self, [pad8(d), pad8(d)+d) neighbour
   std::vector<float*> theta;
   std::vector<int64_t> th_K, th_N;
+  // owner-sharded Theta (GIST_THETA_SHARDED): this rank's physical rows [sh_lo, sh_hi) of every
+  // layer (replicated: [0, th_K)); xscr = every slot's packed sub-model (m x S_max), of which
+  // this rank fills / reads only the rows it owns (the send / receive side of the exchanges);
+  // units_h = host copy of the round's hidden-dim partition (the exchange runs are planned on it)
+  std::vector<int64_t> sh_lo, sh_hi;
+  float* xscr = nullptr;
+  std::vector<std::vector<int32_t>> units_h;
   // partition of the current round
   int m = 0;
   std::vector<uint8_t> layer_set;              // set_params: layers written since load (PARAMS once all are)
@@ -408,6 +415,10 @@ inline int64_t kphys(const gist_ctx* c, int64_t d) {
   return c->arch == GIST_ARCH_SAGE ? 2 * pad8(d) : (c->arch == GIST_ARCH_GAT ? pad8(d) + 8 : pad8(d));
 }
 inline bool two_blocks(const gist_ctx* c) { return c->arch != GIST_ARCH_GCN; }
+inline bool sharded(const gist_ctx* c) { return c->cfg.theta_mode == GIST_THETA_SHARDED; }
+// physical rows of Theta_l owned by rank r (contiguous, balanced)
+inline int64_t shard_lo(const gist_ctx* c, int l, int r) { return c->th_K[l] * r / c->cfg.world_size; }
+inline int64_t rows_here(const gist_ctx* c, int l) { return c->sh_hi[l] - c->sh_lo[l]; }
 inline void free_slots(gist_ctx* c) {
   for (auto& s : c->slots)
     if (s.desc_host) cudaFreeHost(s.desc_host);
@@ -415,6 +426,10 @@ inline void free_slots(gist_ctx* c) {
 }
 // cross-file entry points
 gist_status alloc_slots(gist_ctx* c, int m);
+// shard.cu: the owner-sharded model's exchanges (collectives over the group)
+gist_status shard_extract(gist_ctx* c);     // gist_partition: owners' rows -> every slot's rank
+gist_status shard_aggregate(gist_ctx* c);   // gist_aggregate: slots' rows -> their owners
+gist_status shard_gather_layer(gist_ctx* c, const float* shard, int l, float* full, cudaStream_t s);
 template <typename T> gist_status build_plan(gist_ctx* c, StepPlan<T>& P);
 void drop_graphs(gist_ctx* c);
 }  // namespace gist_impl

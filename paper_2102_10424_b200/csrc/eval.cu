@@ -38,13 +38,21 @@ static gist_status eval_weights(gist_ctx* c, EvalWeights& ew) {
   const bool mean = c->cfg.eval_scale == GIST_EVAL_SCALE_MEAN && c->m > 1;
   for (int l = 0; l < c->L; ++l) {
     const int64_t n = c->th_K[l] * c->th_N[l];
-    ew.w32[l] = c->theta[l];
+    float* src = c->theta[l];
+    if (sharded(c)) {  // owner-sharded Theta: the layer's rows from every rank (collective)
+      float* full = nullptr;
+      TRY(dalloc_t(c, &full, (size_t)n));
+      ew.owned.push_back(full);
+      TRY(shard_gather_layer(c, c->theta[l], l, full, s));
+      src = full;
+    }
+    ew.w32[l] = src;
     if (mean && l > 0) {  // hidden input dim d_l is partitioned: scale the W rows (not GAT's a rows)
       const int64_t nw = (c->arch == GIST_ARCH_GAT ? pad8(c->dims[l]) : c->th_K[l]) * c->th_N[l];
       float* w = nullptr;
       TRY(dalloc_t(c, &w, (size_t)n));
       ew.owned.push_back(w);
-      LK(scale_prefix_f32(c->theta[l], w, n, nw, 1.0f / (float)c->m, s));
+      LK(scale_prefix_f32(src, w, n, nw, 1.0f / (float)c->m, s));
       ew.w32[l] = w;
     }
     if (sizeof(T) == 2) {

@@ -71,6 +71,9 @@ extern "C" gist_status gist_create(const gist_config* cfg, gist_ctx** out) {
   // mean of the GAT attention rows needs every copy on every rank
   if (cfg->agg_mode == GIST_AGG_SYMM && (cfg->loopback || cfg->arch == GIST_ARCH_GAT)) return GIST_E_UNSUPPORTED;
   if (cfg->eval_scale != GIST_EVAL_SCALE_NONE && cfg->eval_scale != GIST_EVAL_SCALE_MEAN) return GIST_E_ARG;
+  if (cfg->theta_mode != GIST_THETA_REPLICATED && cfg->theta_mode != GIST_THETA_SHARDED) return GIST_E_ARG;
+  // the owner-sharded model moves rows point to point; the peer-store subAgg modes write replicas
+  if (cfg->theta_mode == GIST_THETA_SHARDED && cfg->agg_mode != GIST_AGG_ALLGATHER) return GIST_E_UNSUPPORTED;
   if (cfg->agg_mode == GIST_AGG_P2P && (cfg->arch == GIST_ARCH_GAT || cfg->world_size > kMaxPeers))
     return GIST_E_UNSUPPORTED;  // R21 needs every copy of the attention rows; PeerDst holds 8 ranks
   if (cfg->clusters_per_batch < 1 || cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
@@ -192,6 +195,11 @@ extern "C" int64_t gist_stat(gist_ctx* c, int32_t which) {
     case GIST_STAT_MAX_NB: return c->nb_max;
     case GIST_STAT_BLOCK_AGG: return c->bd ? 1 : 0;
     case GIST_STAT_BLOCK_DENSITY_PPM: return (int64_t)(c->block_density * 1e6);
+    case GIST_STAT_THETA_BYTES: {
+      int64_t b = 0;
+      for (int l = 0; l < (int)c->sh_lo.size(); ++l) b += rows_here(c, l) * c->th_N[l] * 4;
+      return persistent_adam(c) ? 3 * b : b;
+    }
   }
   return -1;
 }
@@ -450,16 +458,29 @@ extern "C" gist_status gist_load_graph(gist_ctx* c, int64_t n, const int64_t* ro
   c->th_K.assign(c->L, 0);
   c->th_N.assign(c->L, 0);
   if (c->cfg.agg_mode == GIST_AGG_P2P || c->cfg.agg_mode == GIST_AGG_SYMM) TRY(p2p_setup(c));
+  c->sh_lo.assign(c->L, 0);
+  c->sh_hi.assign(c->L, 0);
   for (int l = 0; l < c->L; ++l) {
     c->th_K[l] = kphys(c, c->dims[l]);
     c->th_N[l] = pad8(c->dims[l + 1]);
-    if (!c->p2p_base) TRY(dalloc_t(c, &c->theta[l], (size_t)c->th_K[l] * c->th_N[l]));
-    CK(cudaMemsetAsync(c->theta[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, s));
+    c->sh_hi[l] = c->th_K[l];
+    if (sharded(c)) {  // this rank's physical rows of Theta_l
+      c->sh_lo[l] = shard_lo(c, l, c->cfg.rank);
+      c->sh_hi[l] = shard_lo(c, l, c->cfg.rank + 1);
+      if (c->arch == GIST_ARCH_GAT && l + 1 == c->L) {  // R21 mean: both attention rows on one rank
+        for (int r = 1; r < c->cfg.world_size; ++r)
+          if (shard_lo(c, l, r) == pad8(c->dims[l]) + 1)
+            return fail(c, GIST_E_UNSUPPORTED, "sharded GAT: a shard boundary splits the attention rows");
+      }
+    }
+    const size_t n = (size_t)rows_here(c, l) * c->th_N[l];
+    if (!c->p2p_base) TRY(dalloc_t(c, &c->theta[l], std::max<size_t>(n, 1)));
+    CK(cudaMemsetAsync(c->theta[l], 0, n * 4, s));
     if (persistent_adam(c) && !c->p2p_base) {  // f3: global moments, same physical layout as Theta
       c->theta_m.resize(c->L, nullptr);
       c->theta_v.resize(c->L, nullptr);
-      TRY(dalloc_t(c, &c->theta_m[l], (size_t)c->th_K[l] * c->th_N[l]));
-      TRY(dalloc_t(c, &c->theta_v[l], (size_t)c->th_K[l] * c->th_N[l]));
+      TRY(dalloc_t(c, &c->theta_m[l], std::max<size_t>(n, 1)));
+      TRY(dalloc_t(c, &c->theta_v[l], std::max<size_t>(n, 1)));
     }
   }
   c->state = S_GRAPH;
@@ -472,8 +493,8 @@ extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
   Range nvtx_range("gist_init_params");
   if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "init_params: bad state");
   for (int l = 0; l < (int)c->theta_m.size(); ++l) {  // f3: moments restart with the parameters
-    CK(cudaMemsetAsync(c->theta_m[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, c->stream));
-    CK(cudaMemsetAsync(c->theta_v[l], 0, (size_t)c->th_K[l] * c->th_N[l] * 4, c->stream));
+    CK(cudaMemsetAsync(c->theta_m[l], 0, (size_t)rows_here(c, l) * c->th_N[l] * 4, c->stream));
+    CK(cudaMemsetAsync(c->theta_v[l], 0, (size_t)rows_here(c, l) * c->th_N[l] * 4, c->stream));
   }
   c->adam_t = 0;
   for (int l = 0; l < c->L; ++l) {
@@ -482,7 +503,7 @@ extern "C" gist_status gist_init_params(gist_ctx* c, uint64_t seed) {
     const int fan_in = c->arch == GIST_ARCH_GAT ? c->dims[l] : rows;  // R21: GAT fan_in = d_l
     const float sc = std::sqrt(6.0f / (float)(fan_in + cols));  // fp32, correctly rounded (R11)
     LK(glorot_init(c->theta[l], rows, cols, two_blocks(c), c->dims[l], (int)pad8(c->dims[l]),
-                   c->th_N[l], (uint32_t)l, seed, sc, c->stream));
+                   c->th_N[l], (uint32_t)l, seed, sc, c->stream, c->sh_lo[l], c->sh_hi[l]));
   }
   TRY(check_launch(c, "init_params"));
   c->layer_set.assign(c->L, 1);
@@ -501,8 +522,18 @@ extern "C" gist_status gist_get_params(gist_ctx* c, int32_t layer, float* out) {
   if (layer < 0 || layer >= c->L || !out) return GIST_E_ARG;
   const int64_t K = c->th_K[layer], N = c->th_N[layer];
   std::vector<float> buf(K * N);
-  CK(cudaMemcpyAsync(buf.data(), c->theta[layer], K * N * 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  if (sharded(c)) {  // collective: the layer's rows from every rank
+    float* full = nullptr;
+    TRY(dalloc_t(c, &full, (size_t)K * N));
+    const gist_status st = shard_gather_layer(c, c->theta[layer], layer, full, c->stream);
+    if (st == GIST_OK) CK(cudaMemcpyAsync(buf.data(), full, K * N * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, full);
+    TRY(st);
+  } else {
+    CK(cudaMemcpyAsync(buf.data(), c->theta[layer], K * N * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
   const int64_t rows = wrows(c, c->dims[layer]);
   const int64_t cols = c->dims[layer + 1];
   for (int64_t r = 0; r < rows; ++r)
@@ -514,12 +545,15 @@ extern "C" gist_status gist_set_params(gist_ctx* c, int32_t layer, const float* 
   PRE(c);
   if (c->state == S_CREATED || c->state == S_PARTITIONED) return fail(c, GIST_E_STATE, "set_params: bad state");
   if (layer < 0 || layer >= c->L || !in) return GIST_E_ARG;
-  const int64_t K = c->th_K[layer], N = c->th_N[layer];
+  const int64_t N = c->th_N[layer];
+  const int64_t lo = c->sh_lo[layer], K = rows_here(c, layer);  // this rank's physical rows
   std::vector<float> buf(K * N, 0.f);
   const int64_t rows = wrows(c, c->dims[layer]);
   const int64_t cols = c->dims[layer + 1];
-  for (int64_t r = 0; r < rows; ++r)
-    std::memcpy(buf.data() + logical_to_phys_row(c, layer, r) * N, in + r * cols, cols * 4);
+  for (int64_t r = 0; r < rows; ++r) {
+    const int64_t pr = logical_to_phys_row(c, layer, r);
+    if (pr >= lo && pr < lo + K) std::memcpy(buf.data() + (pr - lo) * N, in + r * cols, cols * 4);
+  }
   CK(cudaMemcpyAsync(c->theta[layer], buf.data(), K * N * 4, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->h2d += K * N * 4;

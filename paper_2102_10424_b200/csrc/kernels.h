@@ -335,6 +335,9 @@ struct LayerMap {
   int ncols = 0;
   int Kp = 0, Np = 0;             // physical sub weight shape
   int64_t ldg = 0;                // global weight physical row stride
+  // owner-sharded Theta (GIST_THETA_SHARDED): the global buffer holds physical rows
+  // [row_lo, row_hi) only (it points at row row_lo); sub rows of other global rows are skipped
+  int64_t row_lo = 0, row_hi = INT64_MAX;
 };
 void extract_sub(const float* theta, const LayerMap& m, float* w_sub, cudaStream_t s);
 void scatter_sub(float* theta, const LayerMap& m, const float* w_sub, cudaStream_t s);
@@ -354,8 +357,10 @@ namespace gist {
 // the layer inside the registered window
 void scatter_sub_symm(const ncclDevComm& dc, ncclWindow_t win, size_t base, const LayerMap& m, const float* w_sub,
                       bool multimem, cudaStream_t s);
+// (sharded Theta: only physical rows [row_lo, row_hi); theta points at row row_lo)
 void glorot_init(float* theta, int rows_logical, int cols, int sage, int d_l, int glob_half, int64_t ldg,
-                 uint32_t layer, uint64_t seed, float scale, cudaStream_t s);
+                 uint32_t layer, uint64_t seed, float scale, cudaStream_t s, int64_t row_lo = 0,
+                 int64_t row_hi = INT64_MAX);
 
 // eval: per-row CE / argmax correctness over rows with split == code; reduce (deterministic)
 void eval_rows(const float* logits, int64_t ld, int64_t n, int k, const int32_t* labels, const uint8_t* split,

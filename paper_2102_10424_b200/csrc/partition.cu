@@ -91,18 +91,19 @@ __device__ __forceinline__ int64_t glob_row(const LayerMap& m, int p) {
 __global__ void k_extract(const float* __restrict__ theta, const LayerMap m, float* __restrict__ w, int p0) {
   const int p = p0 + blockIdx.y;
   const int64_t gr = glob_row(m, p);
+  if (gr >= 0 && (gr < m.row_lo || gr >= m.row_hi)) return;  // another rank's row (sharded Theta)
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m.Np; q += gridDim.x * blockDim.x) {
     float v = 0.f;
-    if (gr >= 0 && q < m.ncols) v = theta[gr * m.ldg + (m.cols ? m.cols[q] : q)];
+    if (gr >= 0 && q < m.ncols) v = theta[(gr - m.row_lo) * m.ldg + (m.cols ? m.cols[q] : q)];
     w[(int64_t)p * m.Np + q] = v;
   }
 }
 __global__ void k_scatter(float* __restrict__ theta, const LayerMap m, const float* __restrict__ w, int p0) {
   const int p = p0 + blockIdx.y;
   const int64_t gr = glob_row(m, p);
-  if (gr < 0) return;
+  if (gr < m.row_lo || gr >= m.row_hi) return;  // padding (gr < 0) or another rank's row
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < m.ncols; q += gridDim.x * blockDim.x)
-    theta[gr * m.ldg + (m.cols ? m.cols[q] : q)] = w[(int64_t)p * m.Np + q];
+    theta[(gr - m.row_lo) * m.ldg + (m.cols ? m.cols[q] : q)] = w[(int64_t)p * m.Np + q];
 }
 static dim3 grid_for(const LayerMap& m, int rows) {
   unsigned gx = (unsigned)cdiv(m.Np, 256);
@@ -177,8 +178,13 @@ void scatter_sub_symm(const ncclDevComm& dc, ncclWindow_t win, size_t base, cons
 // Glorot uniform (R11): u = (w0 >> 8) 2^-24, t = 2u - 1 (exact), W = fl32(t * scale).
 // Logical (r, c) of Theta_l (SAGE: r < d self rows, r >= d neighbour rows).
 __global__ void k_glorot(float* __restrict__ theta, int rows, int cols, int sage, int d_l, int glob_half,
-                         int64_t ldg, uint32_t layer, uint64_t seed, float scale, int r0) {
+                         int64_t ldg, uint32_t layer, uint64_t seed, float scale, int r0, int64_t row_lo,
+                         int64_t row_hi) {
   const int r = r0 + blockIdx.y;
+  {  // sharded Theta: only this rank's physical rows
+    const int64_t pr = (sage && r >= d_l) ? (int64_t)glob_half + (r - d_l) : (int64_t)r;
+    if (pr < row_lo || pr >= row_hi) return;
+  }
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
     const uint64_t flat = (uint64_t)r * (uint64_t)cols + (uint64_t)c;
     const U4 o = philox4x32_10(U4{(uint32_t)flat, layer, (uint32_t)(flat >> 32), PURPOSE_INIT}, (uint32_t)seed,
@@ -186,16 +192,17 @@ __global__ void k_glorot(float* __restrict__ theta, int rows, int cols, int sage
     const float u = __fmul_rn((float)(o.x >> 8), 5.9604644775390625e-08f);  // 2^-24, exact
     const float t = __fsub_rn(__fmul_rn(2.0f, u), 1.0f);
     const int64_t pr = (sage && r >= d_l) ? (int64_t)glob_half + (r - d_l) : (int64_t)r;
-    theta[pr * ldg + c] = __fmul_rn(t, scale);
+    theta[(pr - row_lo) * ldg + c] = __fmul_rn(t, scale);
   }
 }
 void glorot_init(float* theta, int rows_logical, int cols, int sage, int d_l, int glob_half, int64_t ldg,
-                 uint32_t layer, uint64_t seed, float scale, cudaStream_t s) {
+                 uint32_t layer, uint64_t seed, float scale, cudaStream_t s, int64_t row_lo, int64_t row_hi) {
   const unsigned gx = (unsigned)cdiv(cols, 256);
   for (int r0 = 0; r0 < rows_logical; r0 += 65535) {
     const int rows = rows_logical - r0 < 65535 ? rows_logical - r0 : 65535;
     dim3 grid(gx > 16 ? 16 : gx, (unsigned)rows);
-    k_glorot<<<grid, 256, 0, s>>>(theta, rows_logical, cols, sage, d_l, glob_half, ldg, layer, seed, scale, r0);
+    k_glorot<<<grid, 256, 0, s>>>(theta, rows_logical, cols, sage, d_l, glob_half, ldg, layer, seed, scale, r0,
+                                  row_lo, row_hi);
   }
 }
 

@@ -41,7 +41,10 @@ gist_status alloc_slots(gist_ctx* c, int m) {
     TRY(dalloc_t(c, &c->Wball, tot));
     CK(cudaMemsetAsync(c->Wball, 0, tot * 2, c->stream));
   }
-  if (W > 1 && c->cfg.agg_mode == GIST_AGG_ALLGATHER) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
+  if (W > 1 && c->cfg.agg_mode == GIST_AGG_ALLGATHER && !sharded(c)) TRY(dalloc_t(c, &c->Wrecv, (size_t)W * tot));
+  if (c->xscr) dfree(c, c->xscr);
+  c->xscr = nullptr;
+  if (sharded(c)) TRY(dalloc_t(c, &c->xscr, (size_t)m * smax));  // every slot's packed rows (owned rows only)
   if (c->bctr) dfree(c, c->bctr);
   TRY(dalloc_t(c, &c->bctr, 2 * (size_t)std::max(c->slots_per_rank, 1)));
   if (!c->dstate) {
@@ -213,7 +216,9 @@ extern "C" gist_status gist_partition(gist_ctx* c, uint64_t seed, int32_t m) {
     }
   }
   // extract Theta^(i) for local slots (R6), reset optimizer state (R8)
+  if (sharded(c)) TRY(shard_extract(c));  // owner-sharded Theta: the rows come from their owners
   for (Slot& sl : c->slots) {
+    if (sharded(c)) break;
     const auto& shp = c->shapes[sl.index];
     for (int l = 0; l < c->L; ++l) {
       const LayerShape& sh = shp[l];
@@ -273,6 +278,14 @@ extern "C" gist_status gist_aggregate(gist_ctx* c) {
   std::vector<float*> wvec(c->theta.begin(), c->theta.end());
   std::vector<Part> parts = {{c->Wall, &wvec}};
   if (persistent_adam(c)) parts.push_back({c->Mall, &c->theta_m}), parts.push_back({c->Vall, &c->theta_v});
+  if (sharded(c)) {  // owner-sharded Theta: the updated rows go back to their owners
+    TRY(shard_aggregate(c));
+    c->prof_now = false;
+    TRY(check_launch(c, "aggregate"));
+    c->round += 1;
+    c->state = S_PARAMS;
+    return GIST_OK;
+  }
   if (c->p2p_base) {  // agg_mode P2P (f2): owners store their blocks into every replica
     // barrier 1: every rank has finished this round's reads of its replica (gist_partition's
     // extraction) before any peer overwrites it

@@ -20,7 +20,7 @@ GIST_PREC_FP32, GIST_PREC_BF16, GIST_PREC_TF32 = 0, 1, 2
 GIST_GRAPH_DEVICE = 0
 TRACE_NODES, TRACE_ACT, TRACE_LOGITS, TRACE_GRAD, TRACE_LOSS = range(5)
 (STAT_ROUND, STAT_STEP, STAT_SELF_LOOPS_DROPPED, STAT_LAST_NNZ_B, STAT_LAST_NB, STAT_KERNELS,
- STAT_H2D_BYTES, STAT_D2H_BYTES, STAT_MAX_NB, STAT_BLOCK_AGG, STAT_BLOCK_DENSITY_PPM) = range(11)
+ STAT_H2D_BYTES, STAT_D2H_BYTES, STAT_MAX_NB, STAT_BLOCK_AGG, STAT_BLOCK_DENSITY_PPM, STAT_THETA_BYTES) = range(12)
 
 # every symbol include/gist.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -47,6 +47,7 @@ class GistConfig(C.Structure):
         ("graph_residency", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
         ("device", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
         ("opt_state", C.c_int32), ("agg_mode", C.c_int32), ("loopback", C.c_void_p), ("eval_scale", C.c_int32),
+        ("theta_mode", C.c_int32),
     ]
 
 
@@ -121,7 +122,8 @@ class Gist:
                  clusters_per_batch: int = 1, batch_seed: int = 0, rank: int = 0, world_size: int = 1,
                  device: int = 0, nccl_unique_id: bytes | None = None, stream: int | None = None,
                  beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, opt_state: str = "reset",
-                 agg_mode: str = "allgather", loopback: "Loopback | None" = None, eval_scale: str = "none"):
+                 agg_mode: str = "allgather", loopback: "Loopback | None" = None, eval_scale: str = "none",
+                 theta: str = "replicated"):
         L = lib()
         self.arch = arch
         self.dims = [int(d) for d in dims]
@@ -145,6 +147,7 @@ class Gist:
         cfg.opt_state = {"reset": GIST_OPT_STATE_RESET, "persistent": GIST_OPT_STATE_PERSISTENT}[opt_state]
         cfg.agg_mode = {"allgather": GIST_AGG_ALLGATHER, "p2p": GIST_AGG_P2P, "symm": GIST_AGG_SYMM}[agg_mode]
         cfg.eval_scale = {"none": 0, "mean": 1}[eval_scale]
+        cfg.theta_mode = {"replicated": 0, "sharded": 1}[theta]
         self._lb = loopback  # keeps the group alive while this context exists
         cfg.loopback = loopback.h if loopback is not None else None
         self._cfg = cfg

@@ -29,11 +29,12 @@ ZETA, ROUNDS = 3, 3
 
 
 def _world(W, arch, dims, m, q, g, precision="fp32", agg_mode="allgather", opt_state="reset",
-           optimizer="adam", lr=0.003, parts=None, timeout=600):
+           optimizer="adam", lr=0.003, parts=None, timeout=600, theta="replicated", extra=None):
     from paper_2102_10424_b200.gist import Gist, Loopback
     lb = Loopback(W) if W > 1 else None
     ctxs = [Gist(arch, dims, optimizer=optimizer, precision=precision, clusters_per_batch=q, batch_seed=5,
-                 opt_state=opt_state, agg_mode=agg_mode, rank=r, world_size=W, loopback=lb) for r in range(W)]
+                 opt_state=opt_state, agg_mode=agg_mode, rank=r, world_size=W, loopback=lb, theta=theta)
+            for r in range(W)]
     out = [None] * W
     errs = []
 
@@ -49,6 +50,8 @@ def _world(W, arch, dims, m, q, g, precision="fp32", agg_mode="allgather", opt_s
                 c.aggregate()
                 hist.append([c.get_params(l).copy() for l in range(len(dims) - 1)])
             res = {"hist": hist, "losses": losses, "eval": c.eval(2), "logits": c.eval_logits(0)}
+            if extra is not None:
+                res["extra"] = extra(c, r)
             if parts is not None:
                 res["parts"] = c.eval_parts(2, parts, int(parts.max()) + 1, max_rows=97)
                 res["plogits"] = c.eval_logits(1, parts, int(parts.max()) + 1, max_rows=97)
