@@ -88,6 +88,7 @@ struct StepPlan {
     std::vector<GemmPlanTC> fwd_tc, dw_tc, dx_tc;     // BF16 mode
     std::vector<SgemmGroup> fwd_f, dw_f, dx_f;        // FP32 mode
     std::vector<double> fwd_fl, dw_fl, dx_fl;         // algorithmic FLOPs (profiling)
+    std::vector<OptRanges> opt_l;                      // per-layer optimizer ranges (layer_opt)
     std::vector<double> fwd_by, bwd_by;               // SpMM compulsory bytes excl. nnz part (profiling)
     std::vector<BdPlan> fwd_bd, bwd_bd;               // block-diagonal tensor-core aggregation (c->bd)
     std::vector<double> bd_fl;                        // its FLOPs per launch (profiling)
@@ -121,6 +122,9 @@ struct gist_ctx {
   // run serialised so that the per-kernel event times of the live roofline are not inflated by
   // overlap (ncu's launch list is serialised too)
   cudaStream_t side_now = nullptr;
+  // the optimizer runs per layer on the dW stream right after that layer's dW GEMM (overlapping
+  // the rest of the backward chain) instead of one pass after the backward; GCN / GraphSAGE
+  bool layer_opt = false;
   cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr;
   // this step's batches were built on the dW stream, overlapping the previous step's optimizer
   bool batch_prefetched = false;

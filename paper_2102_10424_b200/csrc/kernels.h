@@ -301,6 +301,21 @@ template <typename T> void softmax_ce(const CeGroup<T>& G, cudaStream_t s);
 void adam_step(float* W, const float* G, float* M, float* V, int64_t n, float b1, float b2, float eps,
                StepState* st, bf16* Wb, cudaStream_t s);
 void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s);
+// One layer's optimizer over the slots of a lockstep group (grid.y = slot): the same element
+// update as adam_step / sgd_step, without the step-state advance (step_advance does it once the
+// step's last layer is done).  Launched on the dW stream right after that layer's dW GEMM.
+struct OptRanges {
+  float* W[kMaxGroup];
+  const float* G[kMaxGroup];
+  float* M[kMaxGroup];
+  float* V[kMaxGroup];
+  bf16* Wb[kMaxGroup];
+  int64_t n[kMaxGroup];  // elements (multiple of 4)
+  int count = 0;
+};
+void adam_ranges(const OptRanges& R, float b1, float b2, float eps, const StepState* st, cudaStream_t s);
+void sgd_ranges(const OptRanges& R, const StepState* st, cudaStream_t s);
+void step_advance(StepState* st, cudaStream_t s);
 // Re-associated last layer: Wcat[r][c2] = [W_top | W_bot] (half x 2Np, row-major) from the
 // bf16 shadow W = [W_top; W_bot] (2 half x Np), so dH = [dZ | Q] Wcat^T is one K = 2 Np GEMM.
 struct RelayoutGroup {

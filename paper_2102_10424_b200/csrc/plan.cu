@@ -30,6 +30,14 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
   const bool sage = c->arch == GIST_ARCH_SAGE;
   const bool tc = c->prec == GIST_PREC_BF16;  // BF16 tensor-core mode (bf16 operands and its fused features)
   const bool tf = c->prec == GIST_PREC_TF32;  // TF32 mode: FP32 storage, step GEMMs on tcgen05 kind::tf32
+  // per-layer optimizer on the dW stream for lockstep groups of >= 4 slots (measured: C3 8 slots
+  // 9,124 -> 9,178 steps/s; one slot per GPU 258 -> 270 us per step, so one pass there);
+  // GIST_LAYER_OPT=0 / 1 forces it off / on (the test switch pinning the two bit-identical); GAT
+  // keeps the one pass
+  {
+    const char* e = std::getenv("GIST_LAYER_OPT");
+    c->layer_opt = c->arch != GIST_ARCH_GAT && (e ? e[0] == '1' : c->slots.size() >= 4);
+  }
   // slots per lockstep group (GIST_GROUP overrides, <= kMaxGroup): measurements of the
   // L2-footprint / launch-count trade-off
   int gsz = kMaxGroup;
@@ -369,6 +377,21 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
         }
         g.fwd_f[l].n = g.dw_f[l].n = g.count;
         g.dx_f[l].n = l > 0 ? g.count : 0;
+      }
+    }
+    g.opt_l.assign(L, OptRanges());
+    for (int l = 0; l < L; ++l) {
+      OptRanges& R = g.opt_l[l];
+      R.count = g.count;
+      for (int j = 0; j < g.count; ++j) {
+        const Slot& sl = c->slots[g0 + j];
+        const LayerShape& sh = c->shapes[sl.index][l];
+        R.W[j] = sl.W + sh.off;
+        R.G[j] = sl.G + sh.off;
+        R.M[j] = sl.M ? sl.M + sh.off : nullptr;
+        R.V[j] = sl.V ? sl.V + sh.off : nullptr;
+        R.Wb[j] = sl.Wb ? sl.Wb + sh.off : nullptr;
+        R.n[j] = (int64_t)sh.Kp * sh.Np;
       }
     }
     P.groups.push_back(g);

@@ -107,6 +107,19 @@ static gist_status gat_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
   return GIST_OK;
 }
 
+// a7 for one layer of a group's slots on stream ds (layer_opt)
+static gist_status layer_optimizer(gist_ctx* c, const OptRanges& R, cudaStream_t ds) {
+  int64_t n = 0;
+  for (int j = 0; j < R.count; ++j) n += R.n[j];
+  if (c->cfg.optimizer == GIST_OPT_ADAM)
+    PL(GIST_PROF_OPTIM, (double)n * (28.0 + (R.Wb[0] ? 2.0 : 0.0)), ds,
+       adam_ranges(R, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate, ds));
+  else
+    PL(GIST_PROF_OPTIM, (double)n * (12.0 + (R.Wb[0] ? 2.0 : 0.0)), ds, sgd_ranges(R, c->dstate, ds));
+  ++c->nk;
+  return GIST_OK;
+}
+
 // One subTrain step of every slot of group g, in lockstep: every
 // kernel below is one launch over all slots of the group.
 template <typename T>
@@ -197,26 +210,29 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       // dZ_{l-1} = (dZ W_top^T + Q W_bot^T) * ReLU'
       if (bd && c->arch == GIST_ARCH_SAGE) bd_l(g.ra_bbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_bsp, g.ra_bby);
-      if (c->side_now) {
-        TRY(fork());
-        const int id = prof_begin(c, c->side_now, GIST_PROF_GEMM, g.ra_gemm_fl / 3);
-        gemm_bf16_launch(g.ra_dw, c->side_now);
-        prof_end(c, c->side_now, id);
+      // per-layer optimizer: it rewrites W_l, so the fork follows the step's last reader of W_l
+      // (GCN's dH = Q W^T reads W; GraphSAGE's reads the relayout copy)
+      if (c->layer_opt) tc_l(g.ra_dh, g.ra_gemm_fl / 3);
+      cudaStream_t ds = c->side_now ? c->side_now : s;
+      if (c->side_now) TRY(fork());
+      {
+        const int id = prof_begin(c, ds, GIST_PROF_GEMM, g.ra_gemm_fl / 3);
+        gemm_bf16_launch(g.ra_dw, ds);
+        prof_end(c, ds, id);
         ++c->nk;
-      } else {
-        tc_l(g.ra_dw, g.ra_gemm_fl / 3);
       }
-      tc_l(g.ra_dh, g.ra_gemm_fl / 3);
+      if (c->layer_opt) TRY(layer_optimizer(c, g.opt_l[l], ds));
+      if (!c->layer_opt) tc_l(g.ra_dh, g.ra_gemm_fl / 3);
       continue;
     }
-    if (c->side_now) {
-      TRY(fork());
-      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], c->side_now);
-    } else {
-      launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], s);
-    }
+    // per-layer optimizer: dW_l and the update of W_l follow dX_l (the step's last reader of W_l)
+    if (c->layer_opt && l > 0) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
+    cudaStream_t ds = c->side_now ? c->side_now : s;
+    if (c->side_now) TRY(fork());
+    launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], ds);
+    if (c->layer_opt) TRY(layer_optimizer(c, g.opt_l[l], ds));
     if (l == 0) break;
-    launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
+    if (!c->layer_opt) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
     if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
     spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
   }
@@ -246,6 +262,11 @@ static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, i
 static gist_status run_optimizer(gist_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t n = (int64_t)c->slots.size() * c->S_max;
+  if (c->layer_opt && c->arch != GIST_ARCH_GAT) {  // every layer was updated on the dW stream
+    PL(GIST_PROF_OPTIM, 16.0, s, step_advance(c->dstate, s));
+    ++c->nk;
+    return GIST_OK;
+  }
   if (c->cfg.optimizer == GIST_OPT_ADAM)
     PL(GIST_PROF_OPTIM, (double)n * (28.0 + (c->Wball ? 2.0 : 0.0)), s,
        adam_step(c->Wall, c->Gall, c->Mall, c->Vall, n, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate, c->Wball,

@@ -158,6 +158,87 @@ __global__ void k_sgd(float* __restrict__ W, const float* __restrict__ G, int64_
   }
   advance_if_last(st);
 }
+// per-layer optimizer over a group's slots (OptRanges): identical element arithmetic to k_adam /
+// k_sgd, so the update does not depend on whether it runs per layer or in one pass
+__global__ void k_adam_ranges(const __grid_constant__ OptRanges R, float b1, float b2, float eps,
+                              const StepState* st) {
+  pdl_wait();
+  pdl_trigger();
+  const int z = blockIdx.y;
+  __shared__ float s_step, s_bc2;
+  if (threadIdx.x == 0) {
+    const double t = (double)(st->t + 1);
+    s_step = st->lr / (float)(1.0 - pow((double)b1, t));
+    s_bc2 = sqrtf((float)(1.0 - pow((double)b2, t)));
+  }
+  __syncthreads();
+  const float step = s_step, bc2_sqrt = s_bc2;
+  float* __restrict__ W = R.W[z];
+  const float* __restrict__ G = R.G[z];
+  float* __restrict__ M = R.M[z];
+  float* __restrict__ V = R.V[z];
+  bf16* __restrict__ Wb = R.Wb[z];
+  const int64_t n4 = R.n[z] >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 w = reinterpret_cast<float4*>(W)[i];
+    const float4 g = reinterpret_cast<const float4*>(G)[i];
+    float4 m = reinterpret_cast<float4*>(M)[i];
+    float4 v = reinterpret_cast<float4*>(V)[i];
+    float* wp = &w.x; const float* gp = &g.x; float* mp = &m.x; float* vp = &v.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mp[j] = b1 * mp[j] + (1.f - b1) * gp[j];
+      vp[j] = b2 * vp[j] + (1.f - b2) * gp[j] * gp[j];
+      const float denom = sqrtf(vp[j]) / bc2_sqrt + eps;
+      wp[j] = wp[j] - step * (mp[j] / denom);
+    }
+    reinterpret_cast<float4*>(W)[i] = w;
+    reinterpret_cast<float4*>(M)[i] = m;
+    reinterpret_cast<float4*>(V)[i] = v;
+    if (Wb) {
+      reinterpret_cast<__nv_bfloat162*>(Wb)[2 * i] = __floats2bfloat162_rn(w.x, w.y);
+      reinterpret_cast<__nv_bfloat162*>(Wb)[2 * i + 1] = __floats2bfloat162_rn(w.z, w.w);
+    }
+  }
+}
+__global__ void k_sgd_ranges(const __grid_constant__ OptRanges R, const StepState* st) {
+  pdl_wait();
+  pdl_trigger();
+  const int z = blockIdx.y;
+  const float lr = st->lr;
+  float* __restrict__ W = R.W[z];
+  const float* __restrict__ G = R.G[z];
+  bf16* __restrict__ Wb = R.Wb[z];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < R.n[z]; i += (int64_t)gridDim.x * blockDim.x) {
+    const float w = W[i] - lr * G[i];
+    W[i] = w;
+    if (Wb) Wb[i] = __float2bfloat16_rn(w);
+  }
+}
+static unsigned ranges_blocks(const OptRanges& R, int per) {
+  int64_t mx = 0;
+  for (int j = 0; j < R.count; ++j) mx = R.n[j] > mx ? R.n[j] : mx;
+  const int64_t b = cdiv(mx / per, 256);
+  const int64_t cap = (int64_t)148 * 8 / (R.count > 0 ? R.count : 1);
+  return (unsigned)(b < 1 ? 1 : (b < cap ? b : (cap < 1 ? 1 : cap)));
+}
+void adam_ranges(const OptRanges& R, float b1, float b2, float eps, const StepState* st, cudaStream_t s) {
+  if (R.count <= 0) return;
+  launch_pdl(k_adam_ranges, dim3(ranges_blocks(R, 4), (unsigned)R.count), 256, 0, s, R, b1, b2, eps, st);
+}
+void sgd_ranges(const OptRanges& R, const StepState* st, cudaStream_t s) {
+  if (R.count <= 0) return;
+  launch_pdl(k_sgd_ranges, dim3(ranges_blocks(R, 1), (unsigned)R.count), 256, 0, s, R, st);
+}
+// the step state's advance once every layer's optimizer has run (per-layer mode)
+__global__ void k_step_advance(StepState* st) {
+  pdl_wait();
+  pdl_trigger();
+  st->z += 1;
+  st->t += 1;
+}
+void step_advance(StepState* st, cudaStream_t s) { launch_pdl(k_step_advance, 1, 1, 0, s, st); }
+
 void sgd_step(float* W, const float* G, int64_t n, StepState* st, bf16* Wb, cudaStream_t s) {
   if (n <= 0) return;
   const int64_t blocks = cdiv(n, 256) < 148 * 8 ? cdiv(n, 256) : 148 * 8;
