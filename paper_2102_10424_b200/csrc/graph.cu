@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(512, 2) k_batch_build(const __grid_constant__ 
     else if (end - rp[g] > 128) walk(std::integral_constant<int, 256>());
     else walk(std::integral_constant<int, 128>());
     cnt = (int)(out - out0) + intra;  // degree in the batch-induced subgraph
-    if (G.X) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
+    if (G.X && !G.skip_x) {  // layer-0 self block [X_b | .] of the GraphSAGE concat (R2)
       const uint4* xs = reinterpret_cast<const uint4*>(G.X + g * G.ldx);
       uint4* xd = reinterpret_cast<uint4*>(G.xdst[blockIdx.y] + (int64_t)v * G.ldxd);
       for (int i = lane; i < G.ldx / 8; i += 32) xd[i] = xs[i];
@@ -358,6 +358,28 @@ void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, con
     launch_pdl(k_batch_build<false, false>, grid, kBuildRows * 32, 0, s, G, rp, col, ccol, cid, arch, labels, split,
                skip_intra, cstart, num_clusters, 0);
   }
+}
+
+// The layer-0 self block [X_b | .] of a batch built with skip_x (the same copy as the build's):
+// one warp per row; rows of the batch built last, dummy rows (b_beg < 0) untouched
+__global__ void __launch_bounds__(256) k_batch_xcopy(const __grid_constant__ BatchGroup G) {
+  pdl_wait();
+  pdl_trigger();
+  const BatchSlot& S = G.s[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int nvec = (int)(G.ldx / 8);
+  const int wpg = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int v = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); v < G.nb_max; v += wpg) {
+    if (S.b_beg[v] < 0) continue;
+    const uint4* xs = reinterpret_cast<const uint4*>(G.X + (int64_t)S.b_nodes[v] * G.ldx);
+    uint4* xd = reinterpret_cast<uint4*>(G.xdst[blockIdx.y] + (int64_t)v * G.ldxd);
+    for (int i = lane; i < nvec; i += 32) xd[i] = xs[i];
+  }
+}
+void batch_xcopy(const BatchGroup& G, cudaStream_t s) {
+  if (G.nb_max <= 0 || !G.X) return;
+  const int per_slot = std::max(1, std::min((int)cdiv(G.nb_max, 8), 4 * device_sms() / std::max(G.n, 1)));
+  launch_pdl(k_batch_xcopy, dim3((unsigned)per_slot, (unsigned)G.n), 256, 0, s, G);
 }
 
 // ob > 0: packed per-edge codes (cid[u] << ob) | (u - cstart[cid[u]]) (one array instead of col +

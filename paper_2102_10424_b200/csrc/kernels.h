@@ -165,6 +165,7 @@ struct alignas(64) BdSlot {
 };
 struct BdGroup {
   CUtensorMap ma;  // all cluster blocks [num_clusters * BS, BS]
+  CUtensorMap mat;  // the same, boxes of 64 columns x BS rows (one block's k-block: k_bd_t)
   BdSlot s[kMaxGroup];
   int n = 0, q = 0, bs = 0, tn = 0;
   int64_t rows = 0;  // static batch rows (nb_max): dummy rows [n_b, rows) are zero-filled
@@ -174,6 +175,7 @@ struct BdGroup {
 struct BdPlan {
   BdGroup G;
   int bn = 128;
+  bool transposed = false;  // k_bd_t (see gemm_tc.cu)
   int64_t maxN = 0;
 };
 bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* ops, int n, int q, int64_t rows,
@@ -249,6 +251,9 @@ struct BatchGroup {
   const bf16* X = nullptr;
   int64_t ldx = 0, ldxd = 0;
   bf16* xdst[kMaxGroup] = {};
+  // the build leaves the X copy to batch_xcopy (early prefetch: the build overlaps the previous
+  // step's dW_0, which still reads the destination)
+  int skip_x = 0;
 };
 void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, cudaStream_t s);
 // skip_intra: intra-cluster edges only count towards the degree (they are aggregated by the
@@ -257,6 +262,8 @@ void batch_setup(const BatchGroup& G, const int64_t* cstart, const int64_t* rp, 
 void batch_build(const BatchGroup& G, const int64_t* rp, const int32_t* col, const int32_t* ccol,
                  const int32_t* cid, const int64_t* cstart, int num_clusters, int arch, const int32_t* labels,
                  const uint8_t* split, int skip_intra, int ob, cudaStream_t s);
+// the X copy of a batch built with skip_x: rows with b_beg >= 0 (dummy rows untouched, as in the build)
+void batch_xcopy(const BatchGroup& G, cudaStream_t s);
 // packed edge codes for the batch build: offset bits ob (0 = packing does not apply: use ccol)
 int pack_bits(int num_clusters, int64_t max_csize);
 void edge_codes(const int32_t* col, const int32_t* cid, const int64_t* cstart, int64_t nnz, int ob, int32_t* code,
@@ -276,7 +283,7 @@ void cluster_blocks(const int64_t* rp, const int32_t* col, const int32_t* cid, c
 // --------------------------------------------------------------------------
 template <typename T>
 struct CeSlot {
-  const float* logits;
+  float* logits;
   T* dlog;
   float* row_loss;
   const int32_t* lab;
@@ -286,6 +293,9 @@ struct CeSlot {
   uint32_t* done;  // CTAs of this slot finished (the last one reduces the loss and resets it)
   T* dlog_s = nullptr;              // optional second output: dlogits * scale[v] (row scale)
   const float* scale_s = nullptr;
+  // optional: logits = logits + add (fp32 addition), written back before the softmax (the
+  // re-associated last GraphSAGE layer's N (H W_bot), row stride ld)
+  const T* add = nullptr;
 };
 template <typename T>
 struct CeGroup {

@@ -189,9 +189,10 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           bf16 *P = (bf16*)sl.rP, *AGG = (bf16*)sl.rAGG, *DQ = (bf16*)sl.rDQ, *DZs = (bf16*)sl.rDZs;
           op_p.push_back(GemmOp{false, false, nb, Np, half, H, Kp, Wl + half * Np, Np, P, Np, false, false, nullptr, 0,
                                 nullptr, 0, nullptr, 0, /*keep_out*/ 1, 0});
-          GemmOp z{false, false, nb, Np, half, H, Kp, Wl, Np, sl.logits, Np, true, false, nullptr, 0, nullptr, 0};
-          z.add = AGG; z.ldadd = Np;
-          op_z.push_back(z);
+          // H W_top alone (independent of the aggregation: it runs on the side stream beside P's
+          // aggregation); the loss kernel adds N (H W_bot) in fp32, the same addition as an epilogue's
+          op_z.push_back(GemmOp{false, false, nb, Np, half, H, Kp, Wl, Np, sl.logits, Np, true, false, nullptr, 0,
+                                nullptr, 0});
           // forward aggregation of P
           SpmmArgs<T, T>& a = g.ra_fsp.a[j];
           a = SpmmArgs<T, T>();
@@ -250,6 +251,7 @@ gist_status build_plan(gist_ctx* c, StepPlan<T>& P) {
           g.ce.s[j].dlog = (T*)sl.rDQ;
           g.ce.s[j].dlog_s = bd ? (T*)sl.rDZs : nullptr;
           g.ce.s[j].scale_s = sl.scale;
+          g.ce.s[j].add = (const T*)sl.rAGG;  // logits = (H W_top) + N (H W_bot)
         }
         continue;
       }

@@ -120,10 +120,18 @@ static gist_status layer_optimizer(gist_ctx* c, const OptRanges& R, cudaStream_t
   return GIST_OK;
 }
 
-// One subTrain step (PAPER.md:113-117) of every slot of group g, in lockstep: every
-// kernel below is one launch over all slots of the group.
 template <typename T>
-static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t s) {
+static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs,
+                                  bool skip_x = false);
+
+// One subTrain step (PAPER.md:113-117) of every slot of group g, in lockstep: every
+// kernel below is one launch over all slots of the group.  early_pf: the next step's batch
+// build runs on the main stream right after the last backward aggregation (the last reader of
+// this step's batch structures), overlapping dW_0 (and its optimizer) on the dW stream; its copy
+// of the X rows into C_0 (which dW_0 reads) follows the join.
+template <typename T>
+static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t s,
+                                  bool early_pf) {
   const int L = c->L;
   for (int j = 0; j < g.count; ++j) c->slots[g.first + j].last_nb = c->slots[g.first + j].nb_of_step[z];
   int nnz_slot = -1;
@@ -177,12 +185,25 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
       continue;
     }
     if (g.reassoc && l == L - 1) {  // Z = H W_top + N (H W_bot)
+      // H W_top does not depend on the aggregation of P = H W_bot: on the side stream beside it
+      // (the loss kernel adds the two)
+      if (c->side_now) {
+        CK(cudaEventRecord(c->ev_dw_fork, s));
+        CK(cudaStreamWaitEvent(c->side_now, c->ev_dw_fork, 0));
+        gemm_bf16_launch(g.ra_z, c->side_now);
+        ++c->nk;
+      }
       LK(relayout_last(g.ra_wc, s));  // [W_top | W_bot] of this step's weights, for dH below
       ++c->nk;
       tc_l(g.ra_p, g.ra_gemm_fl / 6);
       if (bd) bd_l(g.ra_fbd, g.ra_bd_fl / 2);
       spmm_l(g.ra_fsp, g.ra_fby);
-      tc_l(g.ra_z, g.ra_gemm_fl / 6);
+      if (c->side_now) {
+        CK(cudaEventRecord(c->ev_dw_join, c->side_now));
+        CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
+      } else {
+        tc_l(g.ra_z, g.ra_gemm_fl / 6);
+      }
       continue;
     }
     if (bd) bd_l(g.fwd_bd[l], g.bd_fl[l]);
@@ -231,7 +252,10 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     if (c->side_now) TRY(fork());
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], ds);
     if (c->layer_opt) TRY(layer_optimizer(c, g.opt_l[l], ds));
-    if (l == 0) break;
+    if (l == 0) {
+      if (early_pf) TRY(prefetch_batch<T>(c, g, z + 1, s, /*skip_x*/ true));
+      break;
+    }
     if (!c->layer_opt) launch_gemm<T>(c, g.dx_tc[l], g.dx_f[l], g.dx_fl[l], s);
     if (bd) bd_l(g.bwd_bd[l], g.bd_fl[l]);
     spmm_l(g.bwd_spmm[l], g.bwd_by[l]);
@@ -240,18 +264,25 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     CK(cudaEventRecord(c->ev_dw_join, c->side_now));
     CK(cudaStreamWaitEvent(s, c->ev_dw_join, 0));
   }
+  if (early_pf && g.batch.X) {  // dW_0 has read C_0: the next batch's X rows may replace its left half
+    LK(batch_xcopy(g.batch, s));
+    ++c->nk;
+  }
   return GIST_OK;
 }
 
 // a1 of the next step for group g on stream bs: the build reads the batch index st->zb (the
 // device step state's z still points at the current step while its optimizer runs)
 template <typename T>
-static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs) {
+static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs,
+                                  bool skip_x) {
   double vol = 0.0;
   for (int j = 0; j < g.count; ++j) vol += (double)c->slots[g.first + j].vol_of_step[z];
   const int id = prof_begin(c, bs, GIST_PROF_BATCH, vol * (c->pack_ob ? 12.0 : 16.0) + g.count * c->nb_max_rows * 45.0);
   batch_setup(g.batch, c->cstart, c->rp, bs);
-  batch_build(g.batch, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
+  BatchGroup bg = g.batch;
+  bg.skip_x = skip_x ? 1 : 0;
+  batch_build(bg, c->rp, c->col, c->ccol, c->cid, c->cstart, (int)c->c, c->arch, c->labels, c->split,
               c->bd && c->prec == GIST_PREC_BF16 && c->arch == GIST_ARCH_SAGE, c->pack_ob, bs);
   prof_end(c, bs, id);
   c->nk += 2;
@@ -347,10 +378,15 @@ static gist_status enqueue_step(gist_ctx* c, bool build, bool prefetch) {
   const size_t ng = c->prec == GIST_PREC_BF16 ? c->plan_b.groups.size() : c->plan_f.groups.size();
   c->side_now = c->prof_now ? nullptr : c->dws;
   c->batch_prefetched = !build;
+  // GIST_BATCH_PREFETCH=1: the next step's builds during the optimizer (A/B against the early
+  // prefetch inside the backward, the default; GAT keeps the late one)
+  const char* e_pf = std::getenv("GIST_BATCH_PREFETCH");
+  const bool early = prefetch && c->side_now && c->arch != GIST_ARCH_GAT && !(e_pf && e_pf[0] == '1');
   for (size_t gi = 0; gi < ng; ++gi) {
-    if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], c->cur_z, s));
-    else TRY(run_group_step<float>(c, c->plan_f.groups[gi], c->cur_z, s));
+    if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], c->cur_z, s, early));
+    else TRY(run_group_step<float>(c, c->plan_f.groups[gi], c->cur_z, s, early));
   }
+  if (early) prefetch = false;  // done inside the step
   if (prefetch) {
     CK(cudaEventRecord(c->ev_dw_fork, s));
     CK(cudaStreamWaitEvent(c->dws, c->ev_dw_fork, 0));

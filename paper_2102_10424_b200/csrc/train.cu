@@ -27,7 +27,13 @@ __global__ void __launch_bounds__(256) k_softmax_ce(const __grid_constant__ CeGr
   if (v < G.rows) {
     const int64_t ld = G.ld;
     const int k = G.k;
-    const float* z = S.logits + (int64_t)v * ld;
+    float* zw = S.logits + (int64_t)v * ld;
+    if (S.add) {  // logits = partial logits + add (fp32), stored: every later reader sees the sum
+      const T* ap = S.add + (int64_t)v * ld;
+      for (int c = gl; c < ld; c += LPR) zw[c] = zw[c] + Elem<T>::to_f(ap[c]);
+      __syncwarp(gmask);
+    }
+    const float* z = zw;
     const bool tr = S.train[v] && nt > 0;
     float mx = -INFINITY;
     for (int c = gl; c < k; c += LPR) mx = fmaxf(mx, z[c]);

@@ -149,13 +149,15 @@ def test_loopback_rejects_mismatch():
     lb.close()
 
 
+@pytest.mark.parametrize("case", [0, 1])
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_step_schedules_bit_identical(monkeypatch, precision):
+def test_step_schedules_bit_identical(monkeypatch, precision, case):
     """The step is captured once per (own batch build, next-batch prefetch) variant as a CUDA graph
     and replayed; profiled steps run eagerly; the slots may run as several lockstep groups.  Every
     schedule enqueues the same kernels on the same data: Theta and the losses are bit-identical
-    to the eager, unprefetched, single-group run."""
-    _, kw, arch, dims, q = CASES[1]
+    to the eager, unprefetched, single-group run -- including the early next-batch build inside
+    the backward (default) and the late one during the optimizer (GIST_BATCH_PREFETCH=1)."""
+    _, kw, arch, dims, q = CASES[case]
     g = generate(tiny_spec(**kw), seed=4)
 
     def run(env, prof=0):
@@ -178,7 +180,8 @@ def test_step_schedules_bit_identical(monkeypatch, precision):
         return out
 
     ref = run({"GIST_GRAPH": "0", "GIST_BATCH_PREFETCH": "0"})
-    for env, prof in (({}, 0), ({}, 3), ({"GIST_GROUP": "3"}, 0), ({"GIST_GROUP": "1", "GIST_GRAPH": "0"}, 2)):
+    for env, prof in (({}, 0), ({}, 3), ({"GIST_GROUP": "3"}, 0), ({"GIST_GROUP": "1", "GIST_GRAPH": "0"}, 2),
+                      ({"GIST_BATCH_PREFETCH": "1"}, 0), ({"GIST_GROUP": "1"}, 0)):
         got = run(env, prof)
         for a, b in zip(got, ref):
             np.testing.assert_array_equal(a, b, err_msg=f"{env} profile {prof}")
