@@ -237,6 +237,29 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// split tcgen05.ld: issue now, wait later; the wait names the destination registers as in-out
+// operands, so no read of them can be scheduled above it
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 template <int BN, int ST = (BN == 256 ? 4 : (BN == 64 ? 8 : 6))>
 struct Cfg {
   static constexpr int STAGES = ST;
@@ -1023,6 +1046,344 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_pair(const __grid_cons
   }
 }
 
+// ---- Block-diagonal aggregation, transposed (intra-cluster part of Eq. (2)) ----
+// out[r0 + r][f] = scale[r0 + r] * sum_k Blk_c[r][k] H[h0 + k][f] (+ add[r0 + r][f]).  The cluster
+// block is symmetric (A symmetric), so the MMA computes the transpose D[f][r] = sum_k
+// H[h0 + k][f] Blk_c[k][r]: M = 128 features (A = H^T, read in place: MN-major), N = BSN = pad16(bs)
+// rows of the cluster (B = Blk_c, K-major), K = bs.  One unit = (slot, batch cluster, 128-feature
+// tile) covers every row of the cluster -- no partly filled 128-row tiles, no re-read of H per row
+// tile -- and the block stays in shared memory for the unit's neighbours (double-buffered across
+// clusters; a CTA owns a contiguous unit range, feature tiles fastest, so it loads each of its ~2
+// blocks once): 2-3x fewer operand bytes through L2 than the row-tile kernel.  The epilogue
+// transposes each 32-row chunk of the accumulator through shared memory so that every store and
+// residual load covers 8 rows x 64 contiguous bytes; TMEM loads are double-buffered.  Dummy rows
+// [n_b, rows) of every slot are zero-filled.  Phase trace: tools/bdt_trace.py (-DGIST_GEMM_TRACE;
+// the epilogue, ~1 us per 32-row chunk, paces the kernel).
+#ifdef GIST_GEMM_TRACE
+// k_bd_t phase trace (debug builds): [cta][unit slot 0..8 | 9 = CTA][phase] %globaltimer
+__device__ unsigned long long g_bdt_trace[160][10][8];
+__device__ __forceinline__ void btrace(int slot, int ph) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 160 && slot < 10) g_bdt_trace[blockIdx.x][slot][ph] = t;
+}
+#else
+__device__ __forceinline__ void btrace(int, int) {}
+#endif
+constexpr int kBdtStages = 4;
+constexpr int kBdtAStage = BM * BK * 2;  // 128 features x 64 rows (two 64 x 64 MN-major boxes)
+constexpr int kBdtSmemMax = 220 * 1024;  // dynamic shared memory cap (the descriptors are static)
+constexpr int kBdtStg = kEpiWarps * 32 * 32 * 4;  // epilogue transpose buffers
+__device__ __forceinline__ void st_bf16(bf16* p, float v, int keep, uint64_t pol) {
+  const unsigned short h = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  if (keep) asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(p), "h"(h), "l"(pol) : "memory");
+  else asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(h) : "memory");
+}
+
+template <bool ADD>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant__ BdGroup G) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int bs = G.bs, BSN = (bs + 15) & ~15, KB = (bs + BK - 1) / BK;
+  const uint32_t BREG = (uint32_t)KB * BSN * 128;  // one cluster block: KB k-blocks of BSN rows x 128 B
+  uint8_t* sblk = smem + kBdtStages * kBdtAStage;
+  float* stg_all = (float*)(sblk + 2 * BREG);  // epilogue transposes: 32 x 32 fp32 per warp
+  uint64_t* full = (uint64_t*)((uint8_t*)stg_all + kBdtStg);
+  uint64_t* empty = full + kBdtStages;
+  uint64_t* accf = empty + kBdtStages;  // [2]
+  uint64_t* acce = accf + 2;            // [2]
+  uint64_t* bfull = acce + 2;           // [2]
+  uint64_t* bempty = bfull + 2;         // [2]
+  uint32_t* tmem_slot = (uint32_t*)(bempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t TCOLS = 512;  // two accumulators of <= 256 columns
+  constexpr int per_max = ProbBd<128>::kMaxDesc;
+  __shared__ int32_t sd[kMaxGroup * per_max];
+  __shared__ __align__(16) BdTail stl[kMaxGroup];  // the slots' scalar fields (no dynamic param reads)
+  if (threadIdx.x == 0) btrace(9, 0);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBdtStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], kEpiWarps);
+      mbar_init(&bfull[b], 1);
+      mbar_init(&bempty[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&G.mat);
+    for (int z = 0; z < G.n; ++z) prefetch_map(&G.s[z].mb);
+  }
+  copy_tails(G.s, G.n, stl, offsetof(BdSlot, C));
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const int q = G.q, per = 3 * q + 4;
+  {  // this step's batch descriptors of every slot (the step index is read after the PDL wait)
+    const int zst = G.st->z;
+    for (int i = threadIdx.x; i < G.n * per; i += blockDim.x)
+      sd[i] = G.s[i / per].desc[(size_t)zst * per + (i % per)];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) btrace(9, 1);
+  int FT = 0;
+  for (int z = 0; z < G.n; ++z) FT = max(FT, (stl[z].N + BM - 1) / BM);
+  const int U = G.n * q * FT;
+  const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x), u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  struct Unit {
+    bool ok;
+    int z, c, r0, size, f0, h0;
+  };
+  auto decode = [&](int u) {
+    Unit t;
+    t.z = u / (q * FT);
+    const int rem = u - t.z * q * FT, k = rem / FT;
+    t.f0 = (rem - k * FT) * BM;
+    const int32_t* d = sd + t.z * per;
+    t.ok = k < d[3 * q + 2] && t.f0 < stl[t.z].N;
+    t.c = d[k];
+    t.r0 = d[q + k];
+    t.size = d[q + k + 1] - t.r0;
+    t.h0 = stl[t.z].global_rows ? (int)G.cstart[t.c] : t.r0;
+    return t;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------------------------------------- TMA producer
+      uint32_t it = 0, nbl = 0;
+      int cur = -1;
+      for (int u = u0; u < u1; ++u) {
+        const Unit t = decode(u);
+        if (!t.ok) continue;
+        btrace(u - u0, 0);
+        if (t.c != cur) {  // the next cluster block into the other buffer
+          const uint32_t bb = nbl & 1u, bph = (nbl >> 1) & 1u;
+          mbar_wait(&bempty[bb], bph ^ 1u);
+          btrace(u - u0, 7);
+          mbar_arrive_expect_tx(&bfull[bb], (uint32_t)KB * bs * 128);
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d(sblk + bb * BREG + (uint32_t)kb * BSN * 128, &G.mat, &bfull[bb], kb * BK, t.c * bs);
+          cur = t.c;
+          ++nbl;
+        }
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kBdtStages;
+          mbar_wait(&empty[s], ((it / kBdtStages) & 1u) ^ 1u);
+          uint8_t* sa = smem + s * kBdtAStage;
+          mbar_arrive_expect_tx(&full[s], kBdtAStage);
+#pragma unroll
+          for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 8192, &G.s[t.z].mb, &full[s], t.f0 + 64 * j, t.h0 + kb * BK);
+        }
+        btrace(u - u0, 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------------------------------------- MMA issuer
+      // F32 accumulate, bf16 A/B, A MN-major (features contiguous in H), B K-major, N = BSN, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(BSN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+      uint32_t it = 0, tc = 0, nbl = 0;
+      int cur = -1;
+      for (int u = u0; u < u1; ++u) {
+        const Unit t = decode(u);
+        if (!t.ok) continue;
+        if (t.c != cur) {
+          if (cur >= 0) umma_commit(&bempty[(nbl - 1) & 1u]);  // the previous block is free once read
+          mbar_wait(&bfull[nbl & 1u], (nbl >> 1) & 1u);
+          cur = t.c;
+          ++nbl;
+        }
+        const uint32_t sbk = smem_u32(sblk + ((nbl - 1) & 1u) * BREG);
+        const uint32_t b = tc & 1u;
+        mbar_wait(&acce[b], ((tc >> 1) & 1u) ^ 1u);
+        btrace(u - u0, 2);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem + b * 256;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % kBdtStages;
+          mbar_wait(&full[s], (it / kBdtStages) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * kBdtAStage);
+          const uint32_t sb = sbk + (uint32_t)kb * BSN * 128;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(dacc, make_desc(sa + k * 2048, 8192, 1024), make_desc(sb + k * 32, 16, 1024), idesc, (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&accf[b]);
+        btrace(u - u0, 3);
+        ++tc;
+      }
+    }
+  } else {  // ---------------------------------------------- epilogue warps 2 .. 9
+    // warp (lane quarter lq, half) drains 32-column chunks ch = half, half + 2, ... of the
+    // accumulator: lane f holds feature f0 + 32 lq + f of the chunk's 32 rows; the chunk goes
+    // through shared memory (16-byte groups XOR-swizzled by row: conflict-free both ways) so that
+    // lane r then owns row 32 ch + r with its 32 features -- one row scale, 16-byte residual loads
+    // and stores (the row-tile kernel's epilogue arithmetic: (acc * scale) + add, then bf16)
+    const int ew = warp - 2, lq = warp & 3, half = ew >> 2;
+    const int nch = (BSN + 31) / 32;  // <= 6: at most 3 chunks per warp
+    float* stg = stg_all + ew * 1024;
+    // After the transpose, pass p of a chunk has lane l on row 8 p + l / 4, features 8 (l % 4) ..
+    // +7 of the warp's 32: every store / residual load instruction covers 8 rows x 64 contiguous
+    // bytes.  The operands of those rows (residual groups under ADD, else row scales) are loaded
+    // for the next unit while this one drains (ADD: for this unit, before the accumulator wait).
+    const int pr = lane >> 2, pj = lane & 3;
+    struct Ops {
+      float sc[ADD ? 1 : 3][4];
+    };
+    auto load_ops = [&](const Unit& t, Ops& o) {  // row scales of the unit's chunks (!ADD)
+      const BdTail& S = stl[t.z];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int ch = half + 2 * k;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int r = ch * 32 + 8 * p + pr;
+          if constexpr (!ADD) o.sc[k][p] = (S.rscale && ch < nch && r < t.size) ? __ldg(S.rscale + t.r0 + r) : 1.f;
+        }
+      }
+    };
+    // ADD: the residual groups of chunk k (lane: row 8 p + l / 4, features 8 (l % 4) .. +7)
+    auto load_add = [&](const Unit& t, int k, uint4 (&a)[4]) {
+      const BdTail& S = stl[t.z];
+      const int fc = t.f0 + lq * 32, ch = half + 2 * k;
+      const bool jl = fc + 8 * pj + 8 <= S.N;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int r = ch * 32 + 8 * p + pr;
+        a[p] = (ch < nch && r < t.size && jl)
+                   ? __ldg(reinterpret_cast<const uint4*>(S.add + (int64_t)(t.r0 + r) * S.ldadd + fc + 8 * pj))
+                   : make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    auto next_unit = [&](int u) {
+      for (; u < u1; ++u)
+        if (decode(u).ok) break;
+      return u;
+    };
+    Ops cur, nxt;
+    int u = next_unit(u0);
+    if (!ADD && u < u1) load_ops(decode(u), cur);
+    uint32_t tc = 0;
+    for (; u < u1;) {
+      const Unit t = decode(u);
+      const int un = next_unit(u + 1);
+      uint4 acur[ADD ? 4 : 1], anxt[ADD ? 4 : 1];
+      if constexpr (ADD) load_add(t, 0, acur);
+      else if (un < u1) load_ops(decode(un), nxt);
+      const BdTail& S = stl[t.z];
+      const int fc = t.f0 + lq * 32;  // this warp's first feature
+      const bool jl = fc + 8 * pj + 8 <= S.N;
+      const int keep = S.keep_out;
+      const uint64_t pol = keep ? policy_evict_last() : 0ull;
+      int nk = 0;  // this warp's chunks: ch = half + 2 k inside the cluster
+#pragma unroll
+      for (int k = 0; k < 3; ++k) nk += (half + 2 * k < nch && (half + 2 * k) * 32 < t.size) ? 1 : 0;
+      const uint32_t b = tc & 1u;
+      mbar_wait(&accf[b], (tc >> 1) & 1u);
+      if (lane == 0 && ew == 0) btrace(u - u0, 4);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t trow = tmem + b * 256 + ((uint32_t)(lq * 32) << 16);
+      uint32_t va[32], vb[32];
+      if (nk > 0) {
+        tmem_ld32_issue(trow + half * 32, va);
+        tmem_wait_ld(va);
+      }
+      auto chunk = [&](int k, uint32_t (&v)[32]) {
+        const int ch = half + 2 * k;
+        // v[i] = D[feature lane][row i] -> [row i][feature lane], 16-byte group g of row i at
+        // physical group g ^ (i & 7) (conflict-free stores and loads)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stg[i * 32 + ((((lane >> 2) ^ (i & 7)) << 2) | (lane & 3))] = __uint_as_float(v[i]);
+        __syncwarp();
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int rr = 8 * p + pr, r = ch * 32 + rr;
+          float o[8];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 qv = *reinterpret_cast<const float4*>(stg + rr * 32 + (((2 * pj + h) ^ (rr & 7)) << 2));
+            o[4 * h] = qv.x; o[4 * h + 1] = qv.y; o[4 * h + 2] = qv.z; o[4 * h + 3] = qv.w;
+          }
+          if (r < t.size && jl) {
+            if constexpr (!ADD) {
+              if (S.rscale)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] *= cur.sc[k][p];
+            } else {
+              float tt[8];
+              unpack8(acur[p], tt);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] += tt[i];
+            }
+            bf16* cp = (bf16*)S.C + (int64_t)(t.r0 + r) * S.ldc + fc + 8 * pj;
+            if (keep) st16_hint(cp, o, pol);
+            else st16(cp, o);
+          }
+        }
+        __syncwarp();
+      };
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        if (k >= nk) break;
+        if (k == 0 && lane == 0 && ew == 0 && u == u0) btrace(8, 0);
+        if (k + 1 < nk) {
+          tmem_ld32_issue(trow + (half + 2 * (k + 1)) * 32, (k & 1) ? va : vb);
+          if constexpr (ADD) load_add(t, k + 1, anxt);
+        }
+        if (k & 1) chunk(k, vb);
+        else chunk(k, va);
+        if constexpr (ADD)
+          if (k + 1 < nk)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) acur[p] = anxt[p];
+        if (k + 1 < nk) tmem_wait_ld((k & 1) ? va : vb);
+        if (lane == 0 && ew == 0 && u == u0) btrace(8, 1 + k);
+      }
+      if (lane == 0 && ew == 0) btrace(u - u0, 5);
+      if (lane == 0 && ew == 4) btrace(u - u0, 6);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[b]);
+      ++tc;
+      if (!ADD) cur = nxt;
+      u = un;
+    }
+    if (lane == 0 && ew == 0) btrace(9, 2);
+    // inert dummy rows [n_b, rows) of every slot: exact zeros (warp per row, 16-byte stores)
+    const int gw = blockIdx.x * kEpiWarps + ew, nw = gridDim.x * kEpiWarps;
+    for (int z = 0; z < G.n; ++z) {
+      const BdTail& S = stl[z];
+      const int nbz = sd[z * per + 2 * q];
+      const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+      for (int64_t row = nbz + gw; row < G.rows; row += nw) {
+        bf16* cp = (bf16*)S.C + row * S.ldc;
+        for (int c8 = lane; c8 < S.N / 8; c8 += 32) *reinterpret_cast<uint4*>(cp + 8 * c8) = zero;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) btrace(9, 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+  }
+}
+
 int num_sms() { return device_sms(); }
 
 // ------------------------------------------------------------------ host side
@@ -1278,6 +1639,17 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;
+  // transposed kernel (k_bd_t) when two cluster blocks, the A ring and the epilogue transposes fit
+  // in shared memory (clusters of <= 160 rows) and the descriptors fit the staging (measured: C3
+  // block aggregation 3.11 -> 2.90 ms per profiled sample, 9,311 -> 9,385 steps/s, single-slot
+  // step 252 -> 247 us); GIST_BD_T=0 keeps the row-tile kernel (the test switch)
+  {
+    const char* e = std::getenv("GIST_BD_T");
+    const int BSN = (bs + 15) & ~15, KB = (bs + BK - 1) / BK;
+    P->transposed = !(e && e[0] == '0') && bs <= 192 && 3 * q + 4 <= ProbBd<128>::kMaxDesc &&
+                    kBdtStages * kBdtAStage + 2 * KB * BSN * 128 + kBdtStg + 1024 + 256 <= kBdtSmemMax && (bs % 8) == 0;
+    if (P->transposed && !make_map(&P->G.mat, blocks, bs, (int64_t)num_clusters * bs, bs, 64, bs)) return false;
+  }
   // single-slot launches: 128-wide tiles when 256-wide ones leave SMs idle (one slot per group:
   // block aggregation 35.6 -> 32.5 ms per profiled sample, 2,861 -> 2,867-2,873 steps/s,
   // profiles/r01s_*); multi-slot launches unchanged
@@ -1291,6 +1663,20 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
 
 void gemm_bd_launch(const BdPlan& P, cudaStream_t s) {
   if (P.G.n <= 0 || P.maxN <= 0) return;
+  if (P.transposed) {  // k_bd_t: one unit per (slot, batch cluster, 128-feature tile)
+    const int BSN = (P.G.bs + 15) & ~15, KB = (P.G.bs + BK - 1) / BK;
+    const int smem = kBdtStages * kBdtAStage + 2 * KB * BSN * 128 + kBdtStg + 1024 + 256;
+    const int units = P.G.n * P.G.q * (int)cdiv(P.maxN, BM);
+    const int grid = units < num_sms() ? units : num_sms();
+    if (P.G.s[0].add) {  // every slot of a launch adds a residual, or none does
+      ensure_smem((const void*)k_bd_t<true>, kBdtSmemMax);
+      launch_pdl(k_bd_t<true>, grid, kGemmThreads, smem, s, P.G);
+    } else {
+      ensure_smem((const void*)k_bd_t<false>, kBdtSmemMax);
+      launch_pdl(k_bd_t<false>, grid, kGemmThreads, smem, s, P.G);
+    }
+    return;
+  }
   if (P.bn == 256) launch_bd<256>(P, s);
   else launch_bd<128>(P, s);
 }
@@ -1320,6 +1706,9 @@ bool gemm_tf32(bool transA, bool transB, int64_t M, int64_t N, int64_t K, const 
 }  // namespace gist
 
 #ifdef GIST_GEMM_TRACE
+extern "C" int gist_debug_bdt_trace(unsigned long long* out) {  // [160][10][8]
+  return cudaMemcpyFromSymbol(out, gist::g_bdt_trace, sizeof(gist::g_bdt_trace)) == cudaSuccess ? 0 : -1;
+}
 extern "C" int gist_debug_gemm_trace(unsigned long long* out, int n) {
   if (n > 1024) n = 1024;
   return cudaMemcpyFromSymbol(out, gist::g_gemm_trace, (size_t)n * 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;

@@ -159,3 +159,16 @@ def test_bf16_block_diagonal_aggregation_rounds():
         ora.aggregate()
         for l in range(3):
             assert rel_err(gpu.get_params(l), ora.theta[l]) <= BF16_TOL, (t, l)
+
+
+@pytest.mark.parametrize("bdt", ["1", "0"])
+def test_bf16_block_diagonal_kernels(bdt, monkeypatch):
+    """Both block-diagonal aggregation kernels against the FP64 oracle: the transposed one (k_bd_t:
+    D^T = H^T Blk with Blk symmetric, one unit per cluster and 128-feature tile; the default when
+    two blocks fit in shared memory, clusters of <= 160 rows) and the row-tile one (GIST_BD_T=0;
+    the path of larger clusters)."""
+    monkeypatch.setenv("GIST_BD_T", bdt)
+    test_bf16_block_diagonal_aggregation_rounds()
+    monkeypatch.setenv("GIST_BD", "1")
+    name, kw, arch, dims, q = CASES[1]
+    test_bf16_one_step(name, kw, arch, dims, q)
