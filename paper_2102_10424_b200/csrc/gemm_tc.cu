@@ -1281,8 +1281,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
     for (; u < u1;) {
       const Unit t = decode(u);
       const int un = next_unit(u + 1);
-      uint4 acur[ADD ? 4 : 1], anxt[ADD ? 4 : 1];
-      if constexpr (ADD) load_add(t, 0, acur);
+      // ADD: the residual groups of chunk k in A[k], issued one chunk ahead (distinct registers
+      // per chunk: no copy that would wait for an in-flight load)
+      uint4 A[ADD ? 3 : 1][4];
+      if constexpr (ADD) load_add(t, 0, A[0]);
       else if (un < u1) load_ops(decode(un), nxt);
       const BdTail& S = stl[t.z];
       const int fc = t.f0 + lq * 32;  // this warp's first feature
@@ -1302,7 +1304,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
         tmem_ld32_issue(trow + half * 32, va);
         tmem_wait_ld(va);
       }
-      auto chunk = [&](int k, uint32_t (&v)[32]) {
+      auto chunk = [&](int k, uint32_t (&v)[32], const uint4 (&a)[4]) {
         const int ch = half + 2 * k;
         // v[i] = D[feature lane][row i] -> [row i][feature lane], 16-byte group g of row i at
         // physical group g ^ (i & 7) (conflict-free stores and loads)
@@ -1325,7 +1327,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
                 for (int i = 0; i < 8; ++i) o[i] *= cur.sc[k][p];
             } else {
               float tt[8];
-              unpack8(acur[p], tt);
+              unpack8(a[p], tt);
 #pragma unroll
               for (int i = 0; i < 8; ++i) o[i] += tt[i];
             }
@@ -1340,17 +1342,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
       for (int k = 0; k < 3; ++k) {
         if (k >= nk) break;
         if (k == 0 && lane == 0 && ew == 0 && u == u0) btrace(8, 0);
-        if (k + 1 < nk) {
-          tmem_ld32_issue(trow + (half + 2 * (k + 1)) * 32, (k & 1) ? va : vb);
-          if constexpr (ADD) load_add(t, k + 1, anxt);
+        if constexpr (ADD) {  // registers go to the residual prefetch; TMEM loads are short (~170 cycles)
+          if (k > 0) {
+            tmem_ld32_issue(trow + (half + 2 * k) * 32, va);
+            tmem_wait_ld(va);
+          }
+          if (k + 1 < nk) load_add(t, k + 1 < 3 ? k + 1 : 2, A[k + 1 < 3 ? k + 1 : 2]);
+          chunk(k, va, A[k < 3 ? k : 2]);
+        } else {
+          if (k + 1 < nk) tmem_ld32_issue(trow + (half + 2 * (k + 1)) * 32, (k & 1) ? va : vb);
+          if (k & 1) chunk(k, vb, A[0]);
+          else chunk(k, va, A[0]);
+          if (k + 1 < nk) tmem_wait_ld((k & 1) ? va : vb);
         }
-        if (k & 1) chunk(k, vb);
-        else chunk(k, va);
-        if constexpr (ADD)
-          if (k + 1 < nk)
-#pragma unroll
-            for (int p = 0; p < 4; ++p) acur[p] = anxt[p];
-        if (k + 1 < nk) tmem_wait_ld((k & 1) ? va : vb);
         if (lane == 0 && ew == 0 && u == u0) btrace(8, 1 + k);
       }
       if (lane == 0 && ew == 0) btrace(u - u0, 5);

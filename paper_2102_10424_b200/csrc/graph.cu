@@ -373,12 +373,22 @@ __global__ void __launch_bounds__(256) k_batch_xcopy(const __grid_constant__ Bat
     if (S.b_beg[v] < 0) continue;
     const uint4* xs = reinterpret_cast<const uint4*>(G.X + (int64_t)S.b_nodes[v] * G.ldx);
     uint4* xd = reinterpret_cast<uint4*>(G.xdst[blockIdx.y] + (int64_t)v * G.ldxd);
-    for (int i = lane; i < nvec; i += 32) xd[i] = xs[i];
+    // the row's random HBM read: up to four 16-byte loads per lane in flight before any store
+    for (int i0 = 0; i0 < nvec; i0 += 128) {
+      uint4 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + 32 * j + lane < nvec) t[j] = __ldg(xs + i0 + 32 * j + lane);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + 32 * j + lane < nvec) xd[i0 + 32 * j + lane] = t[j];
+    }
   }
 }
 void batch_xcopy(const BatchGroup& G, cudaStream_t s) {
   if (G.nb_max <= 0 || !G.X) return;
-  const int per_slot = std::max(1, std::min((int)cdiv(G.nb_max, 8), 4 * device_sms() / std::max(G.n, 1)));
+  // one row per warp: every row's gather latency overlaps every other's
+  const int per_slot = std::max(1, (int)cdiv(G.nb_max, 8));
   launch_pdl(k_batch_xcopy, dim3((unsigned)per_slot, (unsigned)G.n), 256, 0, s, G);
 }
 
