@@ -1086,8 +1086,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int bs = G.bs, BSN = (bs + 15) & ~15, KB = (bs + BK - 1) / BK;
   const uint32_t BREG = (uint32_t)KB * BSN * 128;  // one cluster block: KB k-blocks of BSN rows x 128 B
+  const uint32_t NBUF = (uint32_t)G.blk_bufs;      // 1 or 2 block buffers
   uint8_t* sblk = smem + kBdtStages * kBdtAStage;
-  float* stg_all = (float*)(sblk + 2 * BREG);  // epilogue transposes: 32 x 32 fp32 per warp
+  float* stg_all = (float*)(sblk + NBUF * BREG);  // epilogue transposes: 32 x 32 fp32 per warp
   uint64_t* full = (uint64_t*)((uint8_t*)stg_all + kBdtStg);
   uint64_t* empty = full + kBdtStages;
   uint64_t* accf = empty + kBdtStages;  // [2]
@@ -1169,7 +1170,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
         if (!t.ok) continue;
         btrace(u - u0, 0);
         if (t.c != cur) {  // the next cluster block into the other buffer
-          const uint32_t bb = nbl & 1u, bph = (nbl >> 1) & 1u;
+          const uint32_t bb = nbl % NBUF, bph = (nbl / NBUF) & 1u;
           mbar_wait(&bempty[bb], bph ^ 1u);
           btrace(u - u0, 7);
           mbar_arrive_expect_tx(&bfull[bb], (uint32_t)KB * bs * 128);
@@ -1200,12 +1201,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
         const Unit t = decode(u);
         if (!t.ok) continue;
         if (t.c != cur) {
-          if (cur >= 0) umma_commit(&bempty[(nbl - 1) & 1u]);  // the previous block is free once read
-          mbar_wait(&bfull[nbl & 1u], (nbl >> 1) & 1u);
+          if (cur >= 0) umma_commit(&bempty[(nbl - 1) % NBUF]);  // the previous block is free once read
+          mbar_wait(&bfull[nbl % NBUF], (nbl / NBUF) & 1u);
           cur = t.c;
           ++nbl;
         }
-        const uint32_t sbk = smem_u32(sblk + ((nbl - 1) & 1u) * BREG);
+        const uint32_t sbk = smem_u32(sblk + ((nbl - 1) % NBUF) * BREG);
         const uint32_t b = tc & 1u;
         mbar_wait(&acce[b], ((tc >> 1) & 1u) ^ 1u);
         btrace(u - u0, 2);
@@ -1643,15 +1644,22 @@ bool gemm_bd_prepare(const bf16* blocks, int num_clusters, int bs, const BdOp* o
     P->maxN = o.N > P->maxN ? o.N : P->maxN;
   }
   P->bn = P->maxN > 128 ? 256 : 128;
-  // transposed kernel (k_bd_t) when two cluster blocks, the A ring and the epilogue transposes fit
-  // in shared memory (clusters of <= 160 rows) and the descriptors fit the staging (measured: C3
+  // transposed kernel (k_bd_t) when the cluster block(s), the A ring and the epilogue transposes fit
+  // in shared memory (clusters of <= 256 rows) and the descriptors fit the staging (measured: C3
   // block aggregation 3.11 -> 2.90 ms per profiled sample, 9,311 -> 9,385 steps/s, single-slot
   // step 252 -> 247 us); GIST_BD_T=0 keeps the row-tile kernel (the test switch)
   {
     const char* e = std::getenv("GIST_BD_T");
+    const char* eb = std::getenv("GIST_BDT_BUFS");
     const int BSN = (bs + 15) & ~15, KB = (bs + BK - 1) / BK;
-    P->transposed = !(e && e[0] == '0') && bs <= 192 && 3 * q + 4 <= ProbBd<128>::kMaxDesc &&
-                    kBdtStages * kBdtAStage + 2 * KB * BSN * 128 + kBdtStg + 1024 + 256 <= kBdtSmemMax && (bs % 8) == 0;
+    auto bytes = [&](int nb) { return kBdtStages * kBdtAStage + nb * KB * BSN * 128 + kBdtStg + 1024 + 256; };
+    // two block buffers when they fit (clusters of <= 160 rows), else one (<= 256 rows: a block
+    // load waits for the previous cluster's MMAs); one buffer measured equal at C3 (9,440 vs
+    // 9,445 steps/s: the freed shared memory lets the inter-cluster pass co-reside, no gain);
+    // GIST_BDT_BUFS=1 forces one (the test switch)
+    P->G.blk_bufs = (eb && eb[0] == '1') ? 1 : (bytes(2) <= kBdtSmemMax ? 2 : 1);
+    P->transposed = !(e && e[0] == '0') && bs <= 256 && 3 * q + 4 <= ProbBd<128>::kMaxDesc &&
+                    bytes(P->G.blk_bufs) <= kBdtSmemMax && (bs % 8) == 0;
     if (P->transposed && !make_map(&P->G.mat, blocks, bs, (int64_t)num_clusters * bs, bs, 64, bs)) return false;
   }
   // single-slot launches: 128-wide tiles when 256-wide ones leave SMs idle (one slot per group:
@@ -1669,7 +1677,7 @@ void gemm_bd_launch(const BdPlan& P, cudaStream_t s) {
   if (P.G.n <= 0 || P.maxN <= 0) return;
   if (P.transposed) {  // k_bd_t: one unit per (slot, batch cluster, 128-feature tile)
     const int BSN = (P.G.bs + 15) & ~15, KB = (P.G.bs + BK - 1) / BK;
-    const int smem = kBdtStages * kBdtAStage + 2 * KB * BSN * 128 + kBdtStg + 1024 + 256;
+    const int smem = kBdtStages * kBdtAStage + P.G.blk_bufs * KB * BSN * 128 + kBdtStg + 1024 + 256;
     const int units = P.G.n * P.G.q * (int)cdiv(P.maxN, BM);
     const int grid = units < num_sms() ? units : num_sms();
     if (P.G.s[0].add) {  // every slot of a launch adds a residual, or none does

@@ -171,6 +171,7 @@ struct BdGroup {
   int64_t rows = 0;  // static batch rows (nb_max): dummy rows [n_b, rows) are zero-filled
   const StepState* st = nullptr;
   const int64_t* cstart = nullptr;
+  int blk_bufs = 2;  // k_bd_t: cluster-block buffers in shared memory
 };
 struct BdPlan {
   BdGroup G;

@@ -161,13 +161,14 @@ def test_bf16_block_diagonal_aggregation_rounds():
             assert rel_err(gpu.get_params(l), ora.theta[l]) <= BF16_TOL, (t, l)
 
 
-@pytest.mark.parametrize("bdt", ["1", "0"])
-def test_bf16_block_diagonal_kernels(bdt, monkeypatch):
+@pytest.mark.parametrize("bdt,bufs", [("1", "2"), ("1", "1"), ("0", "2")])
+def test_bf16_block_diagonal_kernels(bdt, bufs, monkeypatch):
     """Both block-diagonal aggregation kernels against the FP64 oracle: the transposed one (k_bd_t:
-    D^T = H^T Blk with Blk symmetric, one unit per cluster and 128-feature tile; the default when
-    two blocks fit in shared memory, clusters of <= 160 rows) and the row-tile one (GIST_BD_T=0;
-    the path of larger clusters)."""
+    D^T = H^T Blk with Blk symmetric, one unit per cluster and 128-feature tile) with two cluster
+    blocks in shared memory (clusters of <= 160 rows) or one (GIST_BDT_BUFS=1: the mode of clusters
+    of 161-256 rows), and the row-tile one (GIST_BD_T=0)."""
     monkeypatch.setenv("GIST_BD_T", bdt)
+    monkeypatch.setenv("GIST_BDT_BUFS", bufs)
     test_bf16_block_diagonal_aggregation_rounds()
     monkeypatch.setenv("GIST_BD", "1")
     name, kw, arch, dims, q = CASES[1]
