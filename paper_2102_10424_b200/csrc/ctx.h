@@ -125,6 +125,8 @@ struct gist_ctx {
   // the optimizer runs per layer on the dW stream right after that layer's dW GEMM (overlapping
   // the rest of the backward chain) instead of one pass after the backward; GCN / GraphSAGE
   bool layer_opt = false;
+  bool opt_side = false;  // this step's one-pass optimizer already enqueued on the dW stream (early prefetch)
+  bool opt_side_ok = false;
   cudaEvent_t ev_dw_fork = nullptr, ev_dw_join = nullptr;
   // this step's batches were built on the dW stream, overlapping the previous step's optimizer
   bool batch_prefetched = false;

@@ -123,6 +123,7 @@ static gist_status layer_optimizer(gist_ctx* c, const OptRanges& R, cudaStream_t
 template <typename T>
 static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, int z, cudaStream_t bs,
                                   bool skip_x = false);
+static gist_status run_optimizer_on(gist_ctx* c, cudaStream_t s);
 
 // One subTrain step of every slot of group g, in lockstep: every
 // kernel below is one launch over all slots of the group.  early_pf: the next step's batch
@@ -253,6 +254,13 @@ static gist_status run_group_step(gist_ctx* c, typename StepPlan<T>::Group& g, i
     launch_gemm<T>(c, g.dw_tc[l], g.dw_f[l], g.dw_fl[l], ds);
     if (c->layer_opt) TRY(layer_optimizer(c, g.opt_l[l], ds));
     if (l == 0) {
+      // one group, one-pass optimizer: it follows dW_0 on the dW stream, so the next batch's build
+      // on the main stream overlaps both (single sub-GCN per GPU: the step's tail is then
+      // max(build, dW_0 + optimizer) instead of build + optimizer)
+      if (early_pf && !c->layer_opt && c->opt_side_ok) {
+        TRY(run_optimizer_on(c, ds));
+        c->opt_side = true;
+      }
       if (early_pf) TRY(prefetch_batch<T>(c, g, z + 1, s, /*skip_x*/ true));
       break;
     }
@@ -290,14 +298,8 @@ static gist_status prefetch_batch(gist_ctx* c, typename StepPlan<T>::Group& g, i
 }
 
 // a7 over every local slot at once (the packed buffers are contiguous), then advance the step state
-static gist_status run_optimizer(gist_ctx* c) {
-  cudaStream_t s = c->stream;
+static gist_status run_optimizer_on(gist_ctx* c, cudaStream_t s) {
   const int64_t n = (int64_t)c->slots.size() * c->S_max;
-  if (c->layer_opt && c->arch != GIST_ARCH_GAT) {  // every layer was updated on the dW stream
-    PL(GIST_PROF_OPTIM, 16.0, s, step_advance(c->dstate, s));
-    ++c->nk;
-    return GIST_OK;
-  }
   if (c->cfg.optimizer == GIST_OPT_ADAM)
     PL(GIST_PROF_OPTIM, (double)n * (28.0 + (c->Wball ? 2.0 : 0.0)), s,
        adam_step(c->Wall, c->Gall, c->Mall, c->Vall, n, c->cfg.beta1, c->cfg.beta2, c->cfg.eps, c->dstate, c->Wball,
@@ -307,6 +309,16 @@ static gist_status run_optimizer(gist_ctx* c) {
        sgd_step(c->Wall, c->Gall, n, c->dstate, c->Wball, s));
   ++c->nk;  // (no step_advance launch: the optimizer's last CTA advances the step state)
   return GIST_OK;
+}
+static gist_status run_optimizer(gist_ctx* c) {
+  cudaStream_t s = c->stream;
+  if (c->layer_opt && c->arch != GIST_ARCH_GAT) {  // every layer was updated on the dW stream
+    PL(GIST_PROF_OPTIM, 16.0, s, step_advance(c->dstate, s));
+    ++c->nk;
+    return GIST_OK;
+  }
+  if (c->opt_side) return GIST_OK;  // enqueued after dW_0 on the dW stream (run_group_step)
+  return run_optimizer_on(c, s);
 }
 
 // host side of R7 for a whole subtrain call: cluster lists, offsets, n_b, tags per step
@@ -382,6 +394,8 @@ static gist_status enqueue_step(gist_ctx* c, bool build, bool prefetch) {
   // prefetch inside the backward, the default; GAT keeps the late one)
   const char* e_pf = std::getenv("GIST_BATCH_PREFETCH");
   const bool early = prefetch && c->side_now && c->arch != GIST_ARCH_GAT && !(e_pf && e_pf[0] == '1');
+  c->opt_side = false;
+  c->opt_side_ok = ng == 1;  // the one-pass optimizer covers every group's slots
   for (size_t gi = 0; gi < ng; ++gi) {
     if (c->prec == GIST_PREC_BF16) TRY(run_group_step<bf16>(c, c->plan_b.groups[gi], c->cur_z, s, early));
     else TRY(run_group_step<float>(c, c->plan_f.groups[gi], c->cur_z, s, early));
