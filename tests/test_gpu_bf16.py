@@ -19,7 +19,8 @@ def bf16_round(a):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (517, 131, 263), (3106, 512, 1216), (300, 48, 1024),
-                                   (1216, 512, 3106), (3106, 4096, 1024), (70, 8, 40)])
+                                   (1216, 512, 3106), (3106, 4096, 1024), (70, 8, 40),
+                                   (3106, 512, 96), (777, 300, 128)])  # K <= 128: 2-stage ring, double staging
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
 @pytest.mark.parametrize("out_f32,relu", [(True, False), (False, True)])
 def test_tc_gemm_layouts(M, N, K, ta, tb, out_f32, relu):
