@@ -314,6 +314,9 @@ void* gist_stream(gist_ctx* ctx);
 
 const char* gist_last_error(const gist_ctx* ctx);
 const char* gist_status_str(gist_status s);
+/* Releases every resource of the context (NULL: no-op).  After a failed CUDA / NCCL call (a
+ * sticky GIST_E_CUDA / GIST_E_NCCL status) the NCCL communicator is aborted (ncclCommAbort)
+ * rather than destroyed, so a rank whose peers are stuck in a collective does not wait for them. */
 void gist_destroy(gist_ctx* ctx);
 
 /* ---------------- kernel-level entry points (benchmark / parity) ----------------

@@ -149,16 +149,26 @@ extern "C" void gist_destroy(gist_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (size_t r = 0; r < c->peer_base.size(); ++r)
     if (c->peer_base[r] && c->peer_base[r] != c->p2p_base && !c->comm.lb) cudaIpcCloseMemHandle(c->peer_base[r]);
+  // after a failed CUDA / NCCL call (sticky status) a peer may be blocked in a collective: abort the
+  // communicator instead of the collective teardown (window deregistration, device communicator,
+  // ncclCommDestroy), which would wait for it
+  const bool abort = c->sticky != GIST_OK && c->comm.nccl;
   if (c->devcomm) {
-    ncclDevCommDestroy(c->comm.nccl, c->devcomm);
+    if (!abort) ncclDevCommDestroy(c->comm.nccl, c->devcomm);
     delete c->devcomm;
   }
-  if (c->win) ncclCommWindowDeregister(c->comm.nccl, c->win);
+  if (c->win && !abort) ncclCommWindowDeregister(c->comm.nccl, c->win);
   if (c->p2p_base) {
-    if (c->cfg.agg_mode == GIST_AGG_SYMM) ncclMemFree(c->p2p_base);
-    else cudaFree(c->p2p_base);
+    if (c->cfg.agg_mode == GIST_AGG_SYMM) {
+      if (!abort) ncclMemFree(c->p2p_base);
+    } else {
+      cudaFree(c->p2p_base);
+    }
   }
-  if (c->comm.nccl) ncclCommDestroy(c->comm.nccl);
+  if (c->comm.nccl) {
+    if (abort) ncclCommAbort(c->comm.nccl);
+    else ncclCommDestroy(c->comm.nccl);
+  }
   if (c->comm.lb) loopback_leave(c->comm.lb, c->comm.rank);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   drop_graphs(c);
