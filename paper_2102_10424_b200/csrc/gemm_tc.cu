@@ -1235,7 +1235,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
     // lane r then owns row 32 ch + r with its 32 features -- one row scale, 16-byte residual loads
     // and stores (the row-tile kernel's epilogue arithmetic: (acc * scale) + add, then bf16)
     const int ew = warp - 2, lq = warp & 3, half = ew >> 2;
-    const int nch = (BSN + 31) / 32;  // <= 6: at most 3 chunks per warp
+    const int nch = (BSN + 31) / 32;  // <= 8 (BSN <= 256): at most kCh = 4 chunks per warp
+    constexpr int kCh = 4;
     float* stg = stg_all + ew * 1024;
     // After the transpose, pass p of a chunk has lane l on row 8 p + l / 4, features 8 (l % 4) ..
     // +7 of the warp's 32: every store / residual load instruction covers 8 rows x 64 contiguous
@@ -1243,12 +1244,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
     // for the next unit while this one drains (ADD: for this unit, before the accumulator wait).
     const int pr = lane >> 2, pj = lane & 3;
     struct Ops {
-      float sc[ADD ? 1 : 3][4];
+      float sc[ADD ? 1 : kCh][4];
     };
     auto load_ops = [&](const Unit& t, Ops& o) {  // row scales of the unit's chunks (!ADD)
       const BdTail& S = stl[t.z];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < kCh; ++k) {
         const int ch = half + 2 * k;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -1284,7 +1285,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
       const int un = next_unit(u + 1);
       // ADD: the residual groups of chunk k in A[k], issued one chunk ahead (distinct registers
       // per chunk: no copy that would wait for an in-flight load)
-      uint4 A[ADD ? 3 : 1][4];
+      uint4 A[ADD ? kCh : 1][4];
       if constexpr (ADD) load_add(t, 0, A[0]);
       else if (un < u1) load_ops(decode(un), nxt);
       const BdTail& S = stl[t.z];
@@ -1294,7 +1295,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
       const uint64_t pol = keep ? policy_evict_last() : 0ull;
       int nk = 0;  // this warp's chunks: ch = half + 2 k inside the cluster
 #pragma unroll
-      for (int k = 0; k < 3; ++k) nk += (half + 2 * k < nch && (half + 2 * k) * 32 < t.size) ? 1 : 0;
+      for (int k = 0; k < kCh; ++k) nk += (half + 2 * k < nch && (half + 2 * k) * 32 < t.size) ? 1 : 0;
       const uint32_t b = tc & 1u;
       mbar_wait(&accf[b], (tc >> 1) & 1u);
       if (lane == 0 && ew == 0) btrace(u - u0, 4);
@@ -1340,7 +1341,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
         __syncwarp();
       };
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < kCh; ++k) {
         if (k >= nk) break;
         if (k == 0 && lane == 0 && ew == 0 && u == u0) btrace(8, 0);
         if constexpr (ADD) {  // registers go to the residual prefetch; TMEM loads are short (~170 cycles)
@@ -1348,8 +1349,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_bd_t(const __grid_constant_
             tmem_ld32_issue(trow + (half + 2 * k) * 32, va);
             tmem_wait_ld(va);
           }
-          if (k + 1 < nk) load_add(t, k + 1 < 3 ? k + 1 : 2, A[k + 1 < 3 ? k + 1 : 2]);
-          chunk(k, va, A[k < 3 ? k : 2]);
+          if (k + 1 < nk) load_add(t, k + 1 < kCh ? k + 1 : kCh - 1, A[k + 1 < kCh ? k + 1 : kCh - 1]);
+          chunk(k, va, A[k]);
         } else {
           if (k + 1 < nk) tmem_ld32_issue(trow + (half + 2 * (k + 1)) * 32, (k & 1) ? va : vb);
           if (k & 1) chunk(k, vb, A[0]);

@@ -174,3 +174,23 @@ def test_bf16_block_diagonal_kernels(bdt, bufs, monkeypatch):
     monkeypatch.setenv("GIST_BD", "1")
     name, kw, arch, dims, q = CASES[1]
     test_bf16_one_step(name, kw, arch, dims, q)
+
+
+def test_bf16_block_diagonal_large_clusters():
+    """Clusters of ~200 rows (> 160): the transposed block aggregation keeps one cluster block in
+    shared memory (a block load waits for the previous cluster's MMAs) -- the path taken without
+    any switch.  Rounds against the FP64 oracle at the BF16 tolerance."""
+    from paper_2102_10424_b200.gist import STAT_BLOCK_AGG
+    g = generate(tiny_spec(n=1000, nnz=24000, d0=36, classes=5, clusters=5, f_in=0.8), seed=6)
+    gpu, ora = make_pair(g, "sage", (36, 80, 5), optimizer="sgd", q=2, precision="bf16")
+    assert gpu.stat(STAT_BLOCK_AGG) == 1
+    for t in range(2):
+        gpu.partition(seed=9 + t, m=2)
+        ora.partition(seed=9 + t, m=2)
+        lg = gpu.subtrain(4, lr=0.1)
+        lo = ora.subtrain(4, lr=0.1)
+        assert np.max(np.abs(lg - lo)) <= BF16_TOL * max(1.0, np.max(np.abs(lo))), (t, lg, lo)
+        gpu.aggregate()
+        ora.aggregate()
+        for l in range(2):
+            assert rel_err(gpu.get_params(l), ora.theta[l]) <= BF16_TOL, (t, l)
