@@ -545,6 +545,22 @@ def main():
         roof.update({"kernel": dom, "achieved": achieved, "frac": achieved / roof["peak"], "traffic": traffic,
                      "avg_launch_ms": avg_ms, "work_per_launch": work_per,
                      "share_of_profiled_ms": pd["ms"] / max(sum(v["ms"] for v in step_classes.values()), 1e-9)})
+        # every step class against its own bound (same profiled round): tensor classes by algorithmic
+        # FLOP (agg_tc: 2 BS^2 w per batch cluster -- a dense contraction of a 34%-dense block, so its
+        # tensor fraction is low by construction), the others by compulsory bytes against HBM
+        class_roof = {}
+        for k, v in step_classes.items():
+            if v["launches"] <= 0 or v["ms"] <= 0:
+                continue
+            rate = v["work"] / (v["ms"] / 1e3)
+            if k in ("gemm", "agg_tc"):
+                pk_t = roof["peak"] if dom in ("gemm", "agg_tc") else (pk["bf16_sustained"] or pk["bf16"])
+                class_roof[k] = {"bound": roof["bound"] if dom in ("gemm", "agg_tc") else "tensor",
+                                 "achieved": rate / 1e12, "unit": "TFLOP/s", "frac": rate / 1e12 / pk_t}
+            else:
+                class_roof[k] = {"bound": "hbm", "achieved": rate / 1e9, "unit": "GB/s", "frac": rate / 1e9 / pk["hbm_gbs"]}
+            class_roof[k].update({"avg_launch_ms": v["ms"] / v["launches"], "launches": v["launches"]})
+        roof["classes"] = class_roof
         # subAgg (a9): the per-round collective and local scatter of the profiled round
         cm = prof.get("comm", {"ms": 0.0, "launches": 0, "work": 0.0})
         ag = prof["aggregate"]
