@@ -102,3 +102,19 @@ def test_heavy_rows_bit_identical_across_world_sizes(precision):
             for l in range(len(dims) - 1):
                 np.testing.assert_array_equal(got[r]["hist"][t][l], ref["hist"][t][l])
 
+
+
+@pytest.mark.parametrize("arch,dims", [("sage", (24, 600, 40, 5)), ("sage", (24, 256, 64, 5))])
+def test_heavy_rows_persistent_pass_bit_identical(arch, dims, monkeypatch):
+    """The persistent-warp inter-cluster pass (k_inter_persist: grouped launches of > 16,384 rows,
+    forced here with GIST_INTER_PERSIST=1) sums light rows and the CTA-split heavy rows in exactly
+    the order of k_spmm: the same bits as k_spmm (GIST_INTER_PERSIST=0) on the hub graph, BF16
+    block-diagonal path, m = 4 lockstep slots over 2 rounds."""
+    g = hub_graph(seed=3)
+    out = {}
+    for force in ("1", "0"):
+        monkeypatch.setenv("GIST_INTER_PERSIST", force)
+        out[force] = _world(1, arch, dims, 4, 2, g, precision="bf16")[0]
+    for t in range(len(out["0"]["hist"])):
+        for l in range(len(dims) - 1):
+            np.testing.assert_array_equal(out["1"]["hist"][t][l], out["0"]["hist"][t][l])
