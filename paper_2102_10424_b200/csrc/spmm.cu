@@ -481,8 +481,8 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     return;
   }
   if constexpr (std::is_same<TI, bf16>::value && std::is_same<TO, bf16>::value && LPR == 32 && (J == 2 || J == 3)) {
-    // grouped launches (> 16,384 rows: the 8-slot step; measured C3 9,388 -> 9,526 steps/s, inter-
-    // cluster passes 4.87 -> 4.60 ms per profiled sample); single-slot launches keep two gathers
+    // grouped launches (> 16,384 rows: the 8-slot step; measured C3 9,388 -> ~9,650 steps/s, inter-
+    // cluster passes 4.87 -> 4.42 ms per profiled sample); single-slot launches keep two gathers
     // in flight per row.  GIST_INTER_PERSIST=1 / 0 forces it on / off (the bit-identity test)
     const char* e_p = std::getenv("GIST_INTER_PERSIST");
     bool ok = !(e_p && e_p[0] == '0') && split_min > 0 && nchunks == 1 &&
@@ -491,7 +491,9 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
       ok = G.a[i].few_nnz && G.a[i].early && !G.a[i].colscale && !G.a[i].h_index && !G.a[i].self && !G.a[i].self_out &&
            (int64_t)(G.a[i].rows + G.a[i].row0) * (G.a[i].ldh / 8) < ((int64_t)1 << 31);
     if (ok) {  // persistent warps, ~4 CTAs per SM
-      const int64_t warps = 4LL * 8 * device_sms();
+      // rows dealt over 8 x (8 warps x SMs): ~3 rows per warp at 8 slots, two waves of CTAs
+      // (measured: 2 / 4 / 8 / 16 -> 5.68 / 4.63 / 4.42 / 4.44 ms per profiled sample)
+      const int64_t warps = 8LL * 8 * device_sms();
       const int rpw = (int)std::max<int64_t>(1, std::min<int64_t>(16, cdiv(rows * G.n, warps)));
       const dim3 pg((unsigned)cdiv(rows, 8LL * rpw), (unsigned)G.n);
       const size_t psm = (size_t)8 * 32 * J * 8 * sizeof(float);
