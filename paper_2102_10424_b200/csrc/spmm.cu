@@ -481,12 +481,12 @@ void launch(const SpmmGroup<TI, TO>& G, int64_t rows, int64_t w, cudaStream_t s)
     return;
   }
   if constexpr (std::is_same<TI, bf16>::value && std::is_same<TO, bf16>::value && LPR == 32 && (J == 2 || J == 3)) {
-    // grouped launches (> 16,384 rows: the 8-slot step; measured C3 9,388 -> ~9,650 steps/s, inter-
-    // cluster passes 4.87 -> 4.42 ms per profiled sample); single-slot launches keep two gathers
-    // in flight per row.  GIST_INTER_PERSIST=1 / 0 forces it on / off (the bit-identity test)
+    // grouped launches of > 8,192 rows (4 and 8 slots; measured C3 9,388 -> ~9,650 steps/s, inter-
+    // cluster passes 4.87 -> 4.42 ms per profiled sample; 4-slot W = 2 proxy step 514 -> 493 us);
+    // one- and two-slot launches keep two gathers in flight per row (measured equal / better).  GIST_INTER_PERSIST=1 / 0 forces it on / off (the bit-identity test)
     const char* e_p = std::getenv("GIST_INTER_PERSIST");
     bool ok = !(e_p && e_p[0] == '0') && split_min > 0 && nchunks == 1 &&
-              (rows * G.n > 16384 || (e_p && e_p[0] == '1'));
+              (rows * G.n > 8192 || (e_p && e_p[0] == '1'));
     for (int i = 0; i < G.n && ok; ++i)
       ok = G.a[i].few_nnz && G.a[i].early && !G.a[i].colscale && !G.a[i].h_index && !G.a[i].self && !G.a[i].self_out &&
            (int64_t)(G.a[i].rows + G.a[i].row0) * (G.a[i].ldh / 8) < ((int64_t)1 << 31);
